@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Benchmark: prompts ranked/sec (OPT-125M-shape score + sort) on B200; tau pairs/sec.
+
+Workload (BASELINE.json configs[1]): every rank scores 4096 synthetic prompts x 512
+token ids with the random-init OPT-125M-shape ranker (bf16 GEMM operands, fp32
+accumulate / residual), the scores are all-gathered to rank 0 (NCCL, the only
+collective), and rank 0 runs the ranking-policy step (sort + fill + starvation
+bump, max_batch 256) over the global batch. One step = that whole pass; value =
+prompts of all ranks / max-over-ranks device time. Scaling is weak (4096 prompts
+per GPU). Secondary lines in the same JSON: tau pairs/s and rank-step requests/s on
+the 1M-request cfg4 queue (BASELINE.json configs[3]).
+
+    python bench.py [--gpus N --steps K --warmup W]           # our B200 path
+    python bench.py --impl reference ...                      # CPU oracle port arm
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "prompts ranked/sec (OPT-125M score+sort) at 1/2/4/8 B200; tau pairs/sec"
+UNIT = "prompts/s"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    d = dict(FALLBACK_PEAKS)
+    d["source"] = "fallback (B200_PROFILING.md)"
+    return d
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self):
+        rows = [r.split(",") for r in self.out.strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if "Active" in r[5 + k]})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(rows), "reasons": reasons}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_cores():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle-port measurements (cpu_baseline and the --impl reference arm)
+# ---------------------------------------------------------------------------
+
+
+def cpu_port_step(cfg, params, ids_np):
+    """Oracle port of the path on the host: fp32 OPT-shape forward (torch CPU, all
+    threads) + the reference ranking step restated in Python."""
+    from oracle import opt_ranker, schedule_oracle
+
+    g = opt_ranker.forward(params, cfg, ids_np).numpy()
+
+    class R:
+        __slots__ = ("id", "arrival_time", "prompt_tokens", "generated_tokens", "score", "state", "priority",
+                     "starvation_count", "quantum")
+
+    reqs = []
+    for k, gv in enumerate(g):
+        r = R()
+        r.id, r.arrival_time, r.prompt_tokens, r.generated_tokens = k, float(k), ids_np.shape[1], 0
+        r.score, r.state, r.priority, r.starvation_count, r.quantum = -float(gv), "waiting", False, 0, 0
+        reqs.append(r)
+    schedule_oracle.schedule(reqs, 1 << 62, max_batch=256, threshold=100, quantum=50, calibrated=False)
+    return g
+
+
+def cpu_baseline(cfg, S, n_prompts=16, reps=1):
+    from paper_2408_15792_b200.ranker import init_params
+    torch.set_num_threads(cpu_cores())
+    params = {k: v.to(torch.bfloat16).float() for k, v in init_params(cfg, 0).items()}
+    ids = np.random.default_rng(1).integers(4, cfg.vocab, (n_prompts, S)).astype(np.int32)
+    cpu_port_step(cfg, params, ids[:2])  # warm-up
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        cpu_port_step(cfg, params, ids)
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": n_prompts / dt, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "port",
+            "sample": f"{n_prompts} prompts x {S} tokens per step: oracle fp32 OPT-125M-shape forward "
+                      f"(torch CPU) + oracle ranking step; {dt:.2f} s"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2408_15792_b200.ranker import RankerConfig, init_params
+    cfg = RankerConfig.opt_125m()
+    torch.set_num_threads(cpu_cores())
+    params = {k: v.to(torch.bfloat16).float() for k, v in init_params(cfg, 0).items()}
+    P = args.ref_prompts
+    ids = np.random.default_rng(1).integers(4, cfg.vocab, (P, args.seq)).astype(np.int32)
+    for _ in range(args.warmup):
+        cpu_port_step(cfg, params, ids)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        cpu_port_step(cfg, params, ids)
+    dt = (time.perf_counter() - t0) / args.steps
+    v = P / dt
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (random token ids, random-init weights, seed 0)",
+            "config": {"workload": f"OPT-125M-shape ranker scoring {args.batch} prompts x {args.seq} tokens + score "
+                                   f"sort; each CPU step is a bounded sample of {P} prompts",
+                       "global_batch": args.batch, "seq_len": args.seq, "parallelism": "cpu"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "port",
+                             "sample": f"{P} prompts x {args.seq} tokens per step (oracle port: fp32 OPT forward + "
+                                       "ranking step)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# B200 path
+# ---------------------------------------------------------------------------
+
+
+def timed(fn, reps, stream=None):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps):
+        fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def gemm_roofline(pk, M=1 << 20, reps=5):
+    """Per-launch CUDA-event timing of the four projection GEMMs at the forward's
+    chunk shape; achieved = algorithmic FLOPs per launch / average launch time."""
+    from paper_2408_15792_b200 import _lib
+    lib = _lib.load()
+    shapes = [(2304, 768, 0), (768, 768, 2), (3072, 768, 1), (768, 3072, 2)]
+    res = []
+    tot_f = tot_t = 0.0
+    for N, K, epi in shapes:
+        A = torch.randn(M, K, device="cuda").bfloat16()
+        W = (torch.randn(N, K, device="cuda") * 0.02).bfloat16()
+        b = torch.zeros(N, device="cuda").bfloat16()
+        C = torch.empty(M, N, device="cuda", dtype=torch.float32 if epi == 2 else torch.bfloat16)
+        R = C if epi == 2 else None
+
+        def f():
+            _lib.check(lib.rs_gemm_bf16(A.data_ptr(), W.data_ptr(), b.data_ptr(), None if R is None else R.data_ptr(),
+                                        C.data_ptr(), M, N, K, epi, _lib.stream_handle()))
+        f()
+        t = timed(f, reps)
+        fl = 2.0 * M * N * K
+        res.append({"N": N, "K": K, "ms": t, "tflops": fl / t / 1e9})
+        tot_f += fl
+        tot_t += t
+        del A, W, C
+    achieved = tot_f / tot_t / 1e9
+    return {"bound": "tensor", "kernel": "gemm_bf16_kernel (tcgen05, 4 OPT projections, M=2^20)",
+            "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops"],
+            "traffic": None, "per_shape": res}
+
+
+def tau_and_rankstep(pk, reps=5):
+    """cfg4 secondary metrics on rank 0: exact tau counts and one ranking step over
+    the 1M-request queue (device time, CUDA events)."""
+    sys.path.insert(0, str(ROOT / "tests" / "golden"))
+    import recipes
+    from paper_2408_15792_b200 import ranking
+    from paper_2408_15792_b200.schedulers import DeviceQueue, SchedulerConfig
+    x, y = recipes.tau_1m("f32")
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    out = torch.empty(6, dtype=torch.int64, device="cuda")
+    ranking.tau_counts_device(xd, yd, out)
+    t = timed(lambda: ranking.tau_counts_device(xd, yd, out), reps)
+    n = len(x)
+    pairs = n * (n - 1) / 2
+    tau_bytes = 8.0 * n
+    q = recipes.queue_1m()
+    dq = DeviceQueue.from_arrays(score=q["score"], scored=np.ones(n, bool), priority=q["priority"],
+                                 running=q["running"], prompt_tokens=q["prompt"], generated_tokens=q["generated"],
+                                 arrival_time=q["arrival"], ids=q["ids"], starvation=q["starvation"],
+                                 quantum=q["quantum"], score_dtype=torch.float32)
+    cfg = SchedulerConfig(max_batch=256, starvation_threshold=100, priority_quantum=50)
+    snap = [dq.flags.clone(), dq.starvation.clone(), dq.quantum.clone()]
+
+    def step():
+        dq.rank_step(cfg, None, length_calibrated=False)
+
+    step()
+    tr = timed(step, reps)
+    for dst, src in zip((dq.flags, dq.starvation, dq.quantum), snap):
+        dst.copy_(src)
+    rs_bytes = 34.0 * n
+    return {
+        "tau": {"metric": "Kendall tau-b pairs/sec (exact counts)", "value": pairs / (t / 1e3), "unit": "pairs/s",
+                "n": n, "ms": t, "roofline": {"bound": "hbm", "achieved": tau_bytes / t / 1e6, "peak": pk["hbm_gbs"],
+                                              "unit": "GB/s", "frac": tau_bytes / t / 1e6 / pk["hbm_gbs"],
+                                              "traffic": None, "algorithmic_bytes": tau_bytes}},
+        "rank_step": {"metric": "requests ranked/sec (sort + fill + starvation bump)", "value": n / (tr / 1e3),
+                      "unit": "requests/s", "n": n, "ms": tr,
+                      "roofline": {"bound": "hbm", "achieved": rs_bytes / tr / 1e6, "peak": pk["hbm_gbs"],
+                                   "unit": "GB/s", "frac": rs_bytes / tr / 1e6 / pk["hbm_gbs"], "traffic": None,
+                                   "algorithmic_bytes": rs_bytes}},
+    }
+
+
+def run_ours(args):
+    import torch.distributed as dist
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2408_15792_b200 import _lib
+    from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
+    from paper_2408_15792_b200.schedulers import DeviceQueue, SchedulerConfig
+    dev = _lib.device(local)
+    pk = peaks()
+    cfg = RankerConfig.opt_125m()
+    B, S = args.batch, args.seq
+    model = OptRanker(cfg, seed=0)
+    gen = torch.Generator().manual_seed(1000 + rank)
+    ids_host = torch.randint(4, cfg.vocab, (B, S), generator=gen, dtype=torch.int32).pin_memory()
+    ids_dev = ids_host.to(dev)
+    gathered = torch.empty(B * world, dtype=torch.float32, device=dev)
+    local_scores = gathered[rank * B:(rank + 1) * B] if world == 1 else torch.empty(B, dtype=torch.float32,
+                                                                                      device=dev)
+    g_out = torch.empty(B, dtype=torch.float32, device=dev)
+    sched = SchedulerConfig(max_batch=256, starvation_threshold=100, priority_quantum=50)
+    queue = None
+    if rank == 0:
+        n = B * world
+        queue = DeviceQueue(n, dev, score_dtype=torch.float32)
+        queue.score = gathered  # the gathered scores are the queue's score column
+        queue.flags.fill_(_lib.RS_FLAG_SCORED)
+        queue.arrival_rank.copy_(torch.arange(n, dtype=torch.int32))
+    run_host = torch.empty(sched.max_batch, dtype=torch.int64).pin_memory()
+    cnt_host = torch.empty(4, dtype=torch.int32).pin_memory()
+
+    def step():
+        model.forward(ids_dev, out=g_out, score_out=local_scores)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, local_scores)
+        if rank == 0:
+            queue.rank_step(sched, None, length_calibrated=False)
+
+    def step_e2e():
+        ids_dev.copy_(ids_host, non_blocking=True)
+        step()
+        if rank == 0:
+            run_host.copy_(queue.run_out[:sched.max_batch], non_blocking=True)
+            cnt_host.copy_(queue.counts, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    lib = _lib.load()
+    l0 = lib.rs_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    launches = int(lib.rs_launch_count() - l0)
+    value = B * world / (ms / 1e3)
+
+    # end to end through the public API with host buffers (H2D ids, D2H run ids)
+    step_e2e()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step_e2e()
+    barrier()
+    e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / args.steps)
+
+    extras = {}
+    if rank == 0 and not args.no_extras:
+        extras["roofline"] = gemm_roofline(pk)
+        extras.update(tau_and_rankstep(pk))
+        if world == 1:
+            extras["cpu_baseline"] = cpu_baseline(cfg, S, n_prompts=args.cpu_prompts)
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    flops = cfg.flops_per_prompt(S)
+    model_tflops = value * flops / 1e12 / world
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random token ids, random-init OPT-125M-shape weights, seed 0)",
+        "config": {"workload": f"OPT-125M-shape ranker scoring {B} prompts x {S} tokens per GPU (bf16 operands, "
+                               "fp32 accumulate/residual) + score all-gather + rank-step sort (max_batch 256)",
+                   "global_batch": B * world, "seq_len": S, "parallelism": f"dp{world}",
+                   "l2": "inputs larger than L2 (activations ~10 GB per 1M-token chunk)"},
+        "roofline": extras.get("roofline"),
+        "cpu_baseline": extras.get("cpu_baseline"),
+        "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * S * 4,
+                "d2h_bytes_per_step": sched.max_batch * 8 + 16, "ms_per_step": e2e_ms},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "model_flops": {"per_prompt": flops, "tflops_per_gpu": model_tflops,
+                        "frac_of_sustained": model_tflops / pk["bf16_tflops_sustained"],
+                        "frac_of_burst": model_tflops / pk["bf16_tflops"]},
+        "peaks": {k: pk.get(k) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained", "source")},
+        "tau": extras.get("tau"),
+        "rank_step": extras.get("rank_step"),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=4096)
+    ap.add_argument("--seq", type=int, default=512)
+    ap.add_argument("--cpu-prompts", type=int, default=16)
+    ap.add_argument("--ref-prompts", type=int, default=4)
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,182 @@
+/*
+ * rsb200.h — C ABI of the B200-native learning-to-rank scheduler hot path.
+ *
+ * One shared library (librsb200.so, built for sm_100a) exports these entry points.
+ * Every pointer argument named *_dev is a device pointer owned by the caller; every
+ * call is stream-ordered on `stream` (a cudaStream_t passed as void*, NULL = legacy
+ * default stream) and returns RS_OK or a negative status. rs_last_error() returns a
+ * thread-local message for the last failing call. No torch / C++ types cross this
+ * boundary.
+ *
+ * The reference (`ranksched` 0.1.0, pure Python + numpy) has no FFI; the functions
+ * below replace the bodies of its Python entry points, which the host package
+ * `paper_2408_15792_b200` re-exposes with the reference signatures:
+ *
+ *   rs_tau_counts          <- ranking.kendall_tau_b          ranking.py:24-63
+ *   rs_listmle_order       <- ranking.list_mle_loss/gradient ranking.py:71-120
+ *   rs_listmle_lengths     <- train_ranking inner step       predictors.py:379-384
+ *                             (bucket_lengths ranking.py:123-132 + stable argsort +
+ *                              loss/n + grad/n)
+ *   rs_arrival_rank        <- the (arrival_time, id) tail of RankingPolicy.sort_key
+ *                             schedulers.py:211-218
+ *   rs_rank_step           <- RankingPolicy.schedule + Policy.schedule/_fill
+ *                             schedulers.py:86-109, 203-240
+ *   rs_ranker_forward      <- RankingModelScorer.raw_outputs predictors.py:245-247
+ *                             (the OPT-125M-shape backbone of PAPER.md:195-201 that
+ *                              replaces _Net.forward predictors.py:190-196)
+ *   rs_ranker_* (training) <- _Net.backward / _Adam.step     predictors.py:198-225
+ */
+#ifndef RSB200_H
+#define RSB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* ---- status codes ------------------------------------------------------------ */
+#define RS_OK 0
+#define RS_ERR_INVALID (-1)          /* bad argument (shape, dtype, size)  -> ValueError  */
+#define RS_ERR_CUDA (-2)             /* CUDA runtime / launch failure       -> RuntimeError */
+#define RS_ERR_NAN (-3)              /* NaN in an ordering key              -> ValueError  */
+#define RS_ERR_NOT_PERMUTATION (-4)  /* true_order is not a permutation     -> ValueError  */
+#define RS_ERR_WORKSPACE (-5)        /* workspace too small                 -> ValueError  */
+#define RS_ERR_UNSUPPORTED (-6)      /* feature not built / device mismatch -> RuntimeError */
+
+/* ---- dtypes ------------------------------------------------------------------ */
+#define RS_F32 0
+#define RS_F64 1
+#define RS_I32 2
+#define RS_I64 3
+#define RS_BF16 4
+
+const char* rs_last_error(void);
+int rs_version(void);
+/* Number of SMs / compute capability of `device`; also resolves the driver entry
+ * point used to encode TMA descriptors. Must be called once per device before the
+ * ranker entry points (the Python wrapper does this). */
+int rs_device_init(int device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+/* ---- K10: exact Kendall tau-b pair counts (ranking.py:24-63) -----------------
+ * x, y: n values each of dtype RS_F32/RS_F64/RS_I32/RS_I64 (compared as float64,
+ * exactly like `np.asarray(x, dtype=np.float64)`, -0.0 == +0.0). NaN -> RS_ERR_NAN.
+ * counts_dev: int64[6] on device = {concordant, discordant, n1 (x-tied pairs),
+ * n2 (y-tied pairs), n3 (pairs tied in both), nan (1 if any NaN was seen; the
+ * counts are then meaningless)}. No host synchronisation. tau is finished on the
+ * host with the reference expression (ranking.py:60-63). */
+size_t rs_tau_workspace_size(int64_t n, int x_dtype, int y_dtype);
+int rs_tau_counts(const void* x_dev, int x_dtype, const void* y_dev, int y_dtype, int64_t n,
+                  int64_t* counts_dev, void* ws_dev, size_t ws_bytes, void* stream);
+
+/* ---- K6: ListMLE ------------------------------------------------------------
+ * rs_listmle_order: n_lists independent lists of length list_len, scores (RS_F32 or
+ * RS_F64) and an int64 permutation `order` per list (best first, ranking.py:86-120).
+ * loss_dev[n_lists] and grad_dev[n_lists*list_len] are written in the scores dtype.
+ * bad_dev (int32, device) is set to 1 if any `order` row is not a permutation; the
+ * call itself still returns RS_OK (the wrapper checks the flag and raises). */
+int rs_listmle_order(const void* scores_dev, int dtype, const int64_t* order_dev,
+                     int32_t n_lists, int32_t list_len, void* loss_dev, void* grad_dev,
+                     int32_t* bad_dev, void* stream);
+/* rs_listmle_lengths: the training form (predictors.py:379-384). g = net outputs
+ * (higher = shorter) f32 [n_lists*list_len]; lengths int32 true output lengths;
+ * the target order is argsort(lengths // bucket_width, stable) per list. Writes
+ * loss_dev[n_lists] = list_mle_loss/list_len and dg_dev = list_mle_gradient/list_len. */
+int rs_listmle_lengths(const float* g_dev, const int32_t* lengths_dev, int32_t n_lists,
+                       int32_t list_len, int32_t bucket_width, float* loss_dev, float* dg_dev,
+                       void* stream);
+
+/* ---- K9: one ranking-policy scheduling step ----------------------------------
+ * The queue is an SoA of the Request runtime fields the policy reads and writes
+ * (workload.py:40-61). Row order = candidate order (the order the reference's
+ * `candidates` list has; promoted/demoted come out in this order). */
+#define RS_FLAG_SCORED 1u
+#define RS_FLAG_PRIORITY 2u
+#define RS_FLAG_RUNNING 4u
+typedef struct rs_queue_soa {
+    int64_t n;
+    int32_t score_dtype;          /* RS_F32 or RS_F64 */
+    const void* score;            /* valid where flags & RS_FLAG_SCORED */
+    const int32_t* prompt_tokens;
+    const int32_t* generated_tokens;
+    const uint32_t* arrival_rank; /* position in (arrival_time, id) order; see rs_arrival_rank */
+    const int64_t* id;
+    uint8_t* flags;               /* in/out (priority bit is written) */
+    int32_t* starvation;          /* in/out */
+    int32_t* quantum;             /* in/out */
+} rs_queue_soa;
+
+/* arrival_rank[i] = rank of (arrival_time[i], id[i]) in ascending tuple order. */
+size_t rs_arrival_rank_workspace_size(int64_t n);
+int rs_arrival_rank(const double* arrival_dev, const int64_t* id_dev, int64_t n,
+                    uint32_t* rank_dev, void* ws_dev, size_t ws_bytes, void* stream);
+
+/* Writes run ids in fill order, promoted / demoted ids in candidate order, and
+ * counts_dev int32[4] = {n_run, n_promoted, n_demoted, nan} (nan = 1 if an effective
+ * score was NaN; the wrapper raises ValueError and the state must be discarded). run_dev needs max_batch
+ * slots, promoted_dev / demoted_dev need n slots. kv_budget < 0 means unlimited.
+ * preemptive = policy.preemptive && config.preemption (schedulers.py:100). */
+size_t rs_rank_step_workspace_size(int64_t n);
+int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv_budget,
+                 int32_t starvation_threshold, int32_t priority_quantum, int32_t length_calibrated,
+                 int32_t preemptive, int64_t* run_dev, int64_t* promoted_dev, int64_t* demoted_dev,
+                 int32_t* counts_dev, void* ws_dev, size_t ws_bytes, void* stream);
+
+/* ---- A5/K1-K5: OPT-shape ranker ------------------------------------------------
+ * Parameters live in ONE contiguous bf16 buffer laid out by rs_ranker_layout():
+ *   tok_emb[V,d] pos_emb[P+2,d] { ln1_w[d] ln1_b[d] qkv_w[3d,d] qkv_b[3d] out_w[d,d]
+ *   out_b[d] ln2_w[d] ln2_b[d] fc1_w[F,d] fc1_b[F] fc2_w[d,F] fc2_b[d] } x L
+ *   lnf_w[d] lnf_b[d] head_w[d] head_b[1]
+ * every tensor starting on a 64-element (128-byte) boundary. Weights are [out, in]
+ * row-major (torch nn.Linear layout). */
+typedef struct rs_ranker_config {
+    int32_t vocab;      /* 50272 */
+    int32_t max_pos;    /* 2048 (the table has max_pos + 2 rows, OPT offset 2) */
+    int32_t d_model;    /* 768 */
+    int32_t n_layers;   /* 12 */
+    int32_t n_heads;    /* 12 (head dim must be 64) */
+    int32_t d_ffn;      /* 3072 */
+    int32_t activation; /* 0 = ReLU (OPT), 1 = GELU(tanh) */
+} rs_ranker_config;
+
+#define RS_RANKER_N_GLOBAL 6  /* tok_emb pos_emb lnf_w lnf_b head_w head_b */
+#define RS_RANKER_N_PER_LAYER 12
+/* offsets (in bf16 elements) of every tensor in the order listed above (global ones
+ * first: tok, pos, lnf_w, lnf_b, head_w, head_b; then per layer in the order above);
+ * returns the total element count (padded). offsets may be NULL. */
+int64_t rs_ranker_layout(const rs_ranker_config* cfg, int64_t* offsets);
+
+/* Scores B prompts of S token ids (int32 [B,S], row-major). last_pos_dev (int32[B],
+ * may be NULL = S-1) is the index of each prompt's last real token. g_dev f32[B] =
+ * head(LN_f(h[last_pos])) — the net output; score_dev (f32[B], may be NULL) receives
+ * -g, the scheduler score (predictors.py:249-250). The residual stream is fp32, the
+ * GEMM operands bf16. */
+size_t rs_ranker_workspace_size(const rs_ranker_config* cfg, int32_t B, int32_t S);
+int rs_ranker_forward(const rs_ranker_config* cfg, const void* params_dev, const int32_t* ids_dev,
+                      const int32_t* last_pos_dev, int32_t B, int32_t S, float* g_dev, float* score_dev,
+                      void* ws_dev, size_t ws_bytes, void* stream);
+
+/* ---- building blocks exported for parity tests ---------------------------------
+ * C[M,N] (row-major) = epi(A[M,K] . W[N,K]^T + bias[N]) with A/W bf16 K-major.
+ * epi: 0 = none, 1 = ReLU, 3 = GELU(tanh) -> C bf16; 2 = + residual R[M,N] -> C, R
+ * fp32 (C may alias R: the residual stream is updated in place).
+ * M % 128 == 0, N % 64 == 0, K % 64 == 0 (the ranker's shapes). tcgen05 + TMA. */
+int rs_gemm_bf16(const void* A_dev, const void* W_dev, const void* bias_dev, const void* R_dev,
+                 void* C_dev, int32_t M, int32_t N, int32_t K, int32_t epi, void* stream);
+/* Causal multi-head attention over packed qkv [B*S, 3*H*64] bf16 -> out [B*S, H*64]. */
+int rs_attention_fwd(const void* qkv_dev, void* out_dev, int32_t B, int32_t S, int32_t H,
+                     void* stream);
+/* Number of kernels this library has launched in the process (all entry points). */
+uint64_t rs_launch_count(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSB200_H */

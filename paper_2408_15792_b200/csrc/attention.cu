@@ -1,0 +1,299 @@
+// K4: causal multi-head self-attention forward on tcgen05 (head dim 64, S <= 512).
+//
+// OPT attention (PAPER.md:195-201 backbone; HF OPTAttention semantics): per prompt and
+// head, softmax(q k^T / sqrt(64) + causal mask) v over the packed qkv activation
+// [B*S, 3*H*64] written by the QKV GEMM. The reference package has no backbone
+// (SPEC.md:12), so the oracle is oracle/opt_ranker.py.
+//
+// Persistent CTA per SM, one (prompt, head, 128-query tile) work item at a time:
+//   warp 0      TMA: Q tile (128x64) once per item, K_j / V_j blocks (128x64) in a
+//               2-stage ring
+//   warp 1      MMA: S_j = Q K_j^T  (M=128, N=128, K=64) into a double-buffered TMEM
+//               score tile; O_j = P_j V_j (M=128, N=64, K=128, V as an MN-major
+//               operand) into its own TMEM slice O_j (j < 4)
+//   warps 4-7   softmax: one query row per thread; block-local max m_j and sum l_j,
+//               P_j = exp(s - m_j) as bf16 into swizzled smem (the A operand of the
+//               PV MMA); at the end O = sum_j e^(m_j - m) O_j / sum_j e^(m_j - m) l_j.
+// Using a per-block max means no TMEM accumulator ever needs rescaling; the combine
+// of the <= 4 partial outputs happens once in registers.
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "sm100.cuh"
+#include "tma.cuh"
+
+namespace rs {
+using namespace sm100;
+
+constexpr int AT_TILE = 128;  // queries per item, keys per block
+constexpr int AT_D = 64;
+constexpr int AT_MAXKB = 4;  // S <= 512
+constexpr int AT_Q_BYTES = AT_TILE * AT_D * 2;   // 16 KB
+constexpr int AT_KV_BYTES = AT_TILE * AT_D * 2;  // 16 KB each of K and V
+constexpr int AT_P_BYTES = AT_TILE * AT_TILE * 2;  // 32 KB
+constexpr int AT_THREADS = 256;
+constexpr int AT_SMEM = AT_Q_BYTES + 4 * AT_KV_BYTES + 2 * AT_P_BYTES + 1024 + 256;
+
+struct AtBars {
+    uint64_t q_full, q_empty, o_full, o_empty;
+    uint64_t kv_full[2], kv_empty[2];
+    uint64_t s_full[2], s_empty[2];
+    uint64_t p_full[2], p_empty[2];
+    uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(AT_THREADS, 1)
+    attention_fwd_kernel(const __grid_constant__ CUtensorMap tqkv, __nv_bfloat16* __restrict__ out, int B, int S,
+                         int H) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;
+    uint8_t* sK = sQ + AT_Q_BYTES;          // 2 stages
+    uint8_t* sV = sK + 2 * AT_KV_BYTES;     // 2 stages
+    uint8_t* sP = sV + 2 * AT_KV_BYTES;     // 2 buffers
+    AtBars* bar = reinterpret_cast<AtBars*>(sP + 2 * AT_P_BYTES);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n_qt = (S + AT_TILE - 1) / AT_TILE;
+    const int n_items = B * H * n_qt;
+    const int dm = H * AT_D;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tqkv);
+        mbar_init(&bar->q_full, 1);
+        mbar_init(&bar->q_empty, 1);
+        mbar_init(&bar->o_full, 1);
+        mbar_init(&bar->o_empty, 4);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&bar->kv_full[i], 1);
+            mbar_init(&bar->kv_empty[i], 1);
+            mbar_init(&bar->s_full[i], 1);
+            mbar_init(&bar->s_empty[i], 4);
+            mbar_init(&bar->p_full[i], 4);
+            mbar_init(&bar->p_empty[i], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(&bar->tmem);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = bar->tmem;
+
+    // item -> (qt, b, h); heaviest query tiles (most key blocks) first
+    auto decode = [&](int item, int& b, int& h, int& qt) {
+        const int per = B * H;
+        qt = n_qt - 1 - item / per;
+        const int bh = item % per;
+        b = bh / H;
+        h = bh % H;
+    };
+
+    if (warp == 0) {
+        if (elect_one()) {
+            int t = 0, kvc = 0;
+            for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+                int b, h, qt;
+                decode(item, b, h, qt);
+                const int row0 = b * S;
+                mbar_wait(&bar->q_empty, (t & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar->q_full, AT_Q_BYTES);
+                tma_load_2d(sQ, &tqkv, &bar->q_full, h * AT_D, row0 + qt * AT_TILE);
+                for (int j = 0; j <= qt; ++j, ++kvc) {
+                    const int st = kvc & 1;
+                    mbar_wait(&bar->kv_empty[st], ((kvc >> 1) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&bar->kv_full[st], 2 * AT_KV_BYTES);
+                    tma_load_2d(sK + st * AT_KV_BYTES, &tqkv, &bar->kv_full[st], dm + h * AT_D, row0 + j * AT_TILE);
+                    tma_load_2d(sV + st * AT_KV_BYTES, &tqkv, &bar->kv_full[st], 2 * dm + h * AT_D,
+                                row0 + j * AT_TILE);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (elect_one()) {
+            constexpr uint32_t id_s = idesc_bf16(AT_TILE, AT_TILE);
+            constexpr uint32_t id_o = idesc_bf16(AT_TILE, AT_D, 0, 1);
+            int t = 0, kvc = 0, sc = 0, pc = 0;
+            for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+                int b, h, qt;
+                decode(item, b, h, qt);
+                const int nkb = qt + 1;
+                const int kvbase = kvc;
+                mbar_wait(&bar->q_full, t & 1);
+                auto issue_pv = [&](int jj) {
+                    const int pb = pc & 1;
+                    mbar_wait(&bar->p_full[pb], (pc >> 1) & 1);
+                    if (jj == 0) mbar_wait(&bar->o_empty, (t & 1) ^ 1);
+                    tc_fence_after();
+                    const int st = (kvbase + jj) & 1;
+                    const uint32_t pa = smem_u32(sP + pb * AT_P_BYTES);
+                    const uint32_t vb = smem_u32(sV + st * AT_KV_BYTES);
+                    const uint32_t d = tmem + 256 + jj * AT_D;
+#pragma unroll
+                    for (int kk = 0; kk < AT_TILE / 16; ++kk) {
+                        mma_bf16_ss(d, desc_kmajor_sw128(pa + (kk >> 2) * (AT_TILE * 128) + (kk & 3) * 32),
+                                    desc_mnmajor_sw128(vb + kk * 2048, 8192), id_o, kk != 0);
+                    }
+                    mma_commit(&bar->p_empty[pb]);
+                    mma_commit(&bar->kv_empty[st]);
+                    ++pc;
+                };
+                for (int j = 0; j < nkb; ++j, ++kvc, ++sc) {
+                    const int st = kvc & 1;
+                    const int sb = sc & 1;
+                    mbar_wait(&bar->s_empty[sb], ((sc >> 1) & 1) ^ 1);
+                    mbar_wait(&bar->kv_full[st], (kvc >> 1) & 1);
+                    tc_fence_after();
+                    const uint32_t qa = smem_u32(sQ);
+                    const uint32_t ka = smem_u32(sK + st * AT_KV_BYTES);
+#pragma unroll
+                    for (int k = 0; k < AT_D / 16; ++k)
+                        mma_bf16_ss(tmem + sb * AT_TILE, desc_kmajor_sw128(qa + k * 32), desc_kmajor_sw128(ka + k * 32),
+                                    id_s, k != 0);
+                    mma_commit(&bar->s_full[sb]);
+                    if (j == nkb - 1) mma_commit(&bar->q_empty);
+                    if (j >= 1) issue_pv(j - 1);
+                }
+                issue_pv(nkb - 1);
+                mma_commit(&bar->o_full);
+            }
+        }
+    } else if (warp >= 4) {
+        const int q4 = warp & 3;
+        const int r = q4 * 32 + lane;  // query row within the tile == TMEM lane
+        const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
+        const float sl2 = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
+        int t = 0, sc = 0, pc = 0;
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
+            int b, h, qt;
+            decode(item, b, h, qt);
+            const int nkb = qt + 1;
+            float mj[AT_MAXKB], lj[AT_MAXKB];
+            for (int j = 0; j < nkb; ++j, ++sc, ++pc) {
+                const int sb = sc & 1;
+                mbar_wait(&bar->s_full[sb], (sc >> 1) & 1);
+                tc_fence_after();
+                const uint32_t sa = tmem + lane_addr + sb * AT_TILE;
+                const int lim = (j == qt) ? r : AT_TILE - 1;  // causal: key c valid iff c <= lim
+                float m = -INFINITY;
+                uint32_t v[32];
+#pragma unroll 1
+                for (int c = 0; c < AT_TILE; c += 32) {
+                    tmem_ld_32x32b_x32(sa + c, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e)
+                        if (c + e <= lim) m = fmaxf(m, __uint_as_float(v[e]));
+                }
+                const int pb = pc & 1;
+                mbar_wait(&bar->p_empty[pb], ((pc >> 1) & 1) ^ 1);
+                uint8_t* prow = sP + pb * AT_P_BYTES;
+                const float ms = m * sl2;
+                float l = 0.f;
+#pragma unroll 1
+                for (int c = 0; c < AT_TILE; c += 32) {
+                    tmem_ld_32x32b_x32(sa + c, v);
+                    tmem_ld_wait();
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int e = 0; e < 32; e += 2) {
+                        float p0 = (c + e <= lim) ? exp2f(fmaf(__uint_as_float(v[e]), sl2, -ms)) : 0.f;
+                        float p1 = (c + e + 1 <= lim) ? exp2f(fmaf(__uint_as_float(v[e + 1]), sl2, -ms)) : 0.f;
+                        pk[e / 2] = pack_bf16(p0, p1);
+                        // the normaliser uses the bf16-rounded P the MMA consumes
+                        float2 rb = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&pk[e / 2]));
+                        l += rb.x + rb.y;
+                    }
+                    // 4 x 16-byte chunks of this row, K-major SW128 (chunk ^= row % 8)
+                    uint8_t* blk = prow + (c >> 6) * (AT_TILE * 128) + r * 128;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int ch = ((c & 63) >> 3) + q;
+                        *reinterpret_cast<uint4*>(blk + ((ch ^ (r & 7)) << 4)) =
+                            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    }
+                }
+                tc_fence_before();
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&bar->s_empty[sb]);
+                    mbar_arrive(&bar->p_full[pb]);
+                }
+                mj[j] = m;
+                lj[j] = l;
+            }
+            // combine the partial outputs
+            float mx = mj[0];
+            for (int j = 1; j < nkb; ++j) mx = fmaxf(mx, mj[j]);
+            float w[AT_MAXKB];
+            float den = 0.f;
+            for (int j = 0; j < nkb; ++j) {
+                w[j] = exp2f((mj[j] - mx) * sl2);
+                den += w[j] * lj[j];
+            }
+            const float inv = 1.f / den;
+            mbar_wait(&bar->o_full, t & 1);
+            tc_fence_after();
+            const int qi = qt * AT_TILE + r;
+            __nv_bfloat16* orow = out + ((size_t)b * S + qi) * dm + h * AT_D;
+#pragma unroll 1
+            for (int c = 0; c < AT_D; c += 32) {
+                float acc[32];
+#pragma unroll
+                for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+                for (int j = 0; j < nkb; ++j) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(tmem + lane_addr + 256 + j * AT_D + c, v);
+                    tmem_ld_wait();
+                    const float wj = w[j] * inv;
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) acc[e] = fmaf(wj, __uint_as_float(v[e]), acc[e]);
+                }
+                if (qi < S) {
+                    uint4* o4 = reinterpret_cast<uint4*>(orow + c);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        o4[q] = make_uint4(pack_bf16(acc[8 * q], acc[8 * q + 1]), pack_bf16(acc[8 * q + 2], acc[8 * q + 3]),
+                                           pack_bf16(acc[8 * q + 4], acc[8 * q + 5]),
+                                           pack_bf16(acc[8 * q + 6], acc[8 * q + 7]));
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar->o_empty);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+static int g_at_sms = 0;
+
+int attention_fwd(const void* qkv, void* out, int B, int S, int H, cudaStream_t st) {
+    RS_CHECK_ARG(B > 0 && S > 0 && H > 0, "attention: empty shape");
+    RS_CHECK_ARG(S <= AT_TILE * AT_MAXKB, "attention: S=%d > %d not supported by the TMEM layout", S,
+                 AT_TILE * AT_MAXKB);
+    if (g_at_sms == 0) {
+        int dev;
+        RS_CUDA(cudaGetDevice(&dev));
+        RS_CUDA(cudaDeviceGetAttribute(&g_at_sms, cudaDevAttrMultiProcessorCount, dev));
+        RS_CUDA(cudaFuncSetAttribute(attention_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM));
+    }
+    const uint64_t rows = (uint64_t)B * S;
+    const uint64_t cols = (uint64_t)3 * H * AT_D;
+    CUtensorMap m;
+    RS_TRY(make_tmap_bf16(&m, qkv, rows, cols, cols * 2, AT_TILE, AT_D));
+    const int n_items = B * H * ((S + AT_TILE - 1) / AT_TILE);
+    const int grid = n_items < g_at_sms ? n_items : g_at_sms;
+    attention_fwd_kernel<<<grid, AT_THREADS, AT_SMEM, st>>>(m, static_cast<__nv_bfloat16*>(out), B, S, H);
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
+}  // namespace rs
+
+extern "C" int rs_attention_fwd(const void* qkv, void* out, int32_t B, int32_t S, int32_t H, void* stream) {
+    return rs::attention_fwd(qkv, out, B, S, H, rs::as_stream(stream));
+}

@@ -1,0 +1,251 @@
+// K3: dense bf16 GEMM with fused epilogues on the 5th-generation tensor cores.
+//
+//   C[M,N] = epi(A[M,K] . W[N,K]^T + bias[N])      A, W bf16 K-major, fp32 accumulate
+//
+// Persistent, warp-specialised sm_100a kernel (one CTA per SM, 256 threads):
+//   warp 0      TMA producer: 128x64 A tile + 256x64 W tile per stage, 4-stage ring
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128, N=256, K=16)
+//               into a double-buffered TMEM accumulator (2 x 256 fp32 columns)
+//   warp 2      TMEM allocator (512 columns)
+//   warps 4-7   epilogue: tcgen05.ld 32 columns at a time, + bias, ReLU / GELU /
+//               residual add, bf16 pack, global store; releases the TMEM buffer so
+//               the next tile's MMAs overlap this tile's epilogue.
+// It replaces the `X @ w + b` of the reference's _Net.forward (predictors.py:190-196)
+// with the OPT-125M projections: QKV 768->2304, out 768->768 (+residual),
+// FC1 768->3072 (+ReLU), FC2 3072->768 (+residual).
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "gemm.cuh"
+#include "sm100.cuh"
+#include "tma.cuh"
+
+namespace rs {
+
+using namespace sm100;
+
+constexpr int G_BM = 128, G_BN = 256, G_BK = 64, G_STAGES = 4;
+constexpr int G_A_BYTES = G_BM * G_BK * 2;
+constexpr int G_B_BYTES = G_BN * G_BK * 2;
+constexpr int G_STAGE_BYTES = G_A_BYTES + G_B_BYTES;
+constexpr int G_THREADS = 256;
+constexpr int G_SMEM = G_STAGES * G_STAGE_BYTES + 1024 + 256;
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    return 0.5f * x * (1.0f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(G_THREADS, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                     const __nv_bfloat16* __restrict__ bias, const float* __restrict__ R, void* __restrict__ Cv,
+                     int M, int N, int K, int ldc) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + G_STAGES * G_A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + G_STAGES * G_STAGE_BYTES);
+    uint64_t* empty = full + G_STAGES;
+    uint64_t* tfull = empty + G_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tA);
+        tma_prefetch_desc(&tB);
+        for (int s = 0; s < G_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int tiles_n = N / G_BN;
+    const int n_tiles = (M / G_BM) * tiles_n;
+    const int kblocks = K / G_BK;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                const int m0 = (tile / tiles_n) * G_BM, n0 = (tile % tiles_n) * G_BN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], G_STAGE_BYTES);
+                    tma_load_2d(sA + stage * G_A_BYTES, &tA, &full[stage], kb * G_BK, m0);
+                    tma_load_2d(sB + stage * G_B_BYTES, &tB, &full[stage], kb * G_BK, n0);
+                    if (++stage == G_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (elect_one()) {
+            constexpr uint32_t idesc = idesc_bf16(G_BM, G_BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + acc * G_BN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * G_A_BYTES);
+                    const uint32_t b0 = smem_u32(sB + stage * G_B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < G_BK / 16; ++k) {
+                        mma_bf16_ss(d, desc_kmajor_sw128(a0 + k * 32), desc_kmajor_sw128(b0 + k * 32), idesc,
+                                    (kb | k) != 0);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (++stage == G_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3;  // TMEM lane quarter this warp may access
+        const int row = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+            const int m0 = (tile / tiles_n) * G_BM, n0 = (tile % tiles_n) * G_BN;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const size_t grow = (size_t)(m0 + row);
+            // EPI 2 (residual) keeps the residual stream in fp32: C, R are float.
+            __nv_bfloat16* crow = (EPI == 2) ? nullptr : static_cast<__nv_bfloat16*>(Cv) + grow * ldc + n0;
+            float* frow = (EPI == 2) ? static_cast<float*>(Cv) + grow * ldc + n0 : nullptr;
+            const float* rrow = (EPI == 2) ? R + grow * ldc + n0 : nullptr;
+#pragma unroll 1
+            for (int c = 0; c < G_BN; c += 32) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * G_BN + c, r);
+                tmem_ld_wait();
+                float v[32];
+                const uint4* bv = reinterpret_cast<const uint4*>(bias + n0 + c);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint4 b4 = __ldg(bv + j);
+                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b4);
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        float2 bf = __bfloat1622float2(b2[h]);
+                        v[j * 8 + 2 * h] = __uint_as_float(r[j * 8 + 2 * h]) + bf.x;
+                        v[j * 8 + 2 * h + 1] = __uint_as_float(r[j * 8 + 2 * h + 1]) + bf.y;
+                    }
+                }
+                if (EPI == 2) {
+                    const float4* rv = reinterpret_cast<const float4*>(rrow + c);
+                    float4* out = reinterpret_cast<float4*>(frow + c);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        float4 r4 = rv[j];
+                        out[j] = make_float4(v[4 * j] + r4.x, v[4 * j + 1] + r4.y, v[4 * j + 2] + r4.z,
+                                             v[4 * j + 3] + r4.w);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        if (EPI == 1) v[j] = fmaxf(v[j], 0.0f);
+                        if (EPI == 3) v[j] = gelu_tanh(v[j]);
+                    }
+                    uint4* out = reinterpret_cast<uint4*>(crow + c);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint4 o;
+                        o.x = pack_bf16(v[j * 8 + 0], v[j * 8 + 1]);
+                        o.y = pack_bf16(v[j * 8 + 2], v[j * 8 + 3]);
+                        o.z = pack_bf16(v[j * 8 + 4], v[j * 8 + 5]);
+                        o.w = pack_bf16(v[j * 8 + 6], v[j * 8 + 7]);
+                        out[j] = o;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<512>(tmem_base);
+}
+
+static int g_num_sms = 0;
+
+int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, void* C, int M, int N, int K, int epi,
+              cudaStream_t st) {
+    RS_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty shape");
+    RS_CHECK_ARG(M % G_BM == 0 && N % G_BN == 0 && K % G_BK == 0,
+                 "gemm: need M %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (got %d %d %d)", M, N, K);
+    RS_CHECK_ARG(epi >= 0 && epi <= 3, "gemm: bad epilogue %d", epi);
+    RS_CHECK_ARG(bias != nullptr, "gemm: bias is required");
+    RS_CHECK_ARG(epi != 2 || R != nullptr, "gemm: residual epilogue needs R");
+    if (g_num_sms == 0) {
+        int dev;
+        RS_CUDA(cudaGetDevice(&dev));
+        RS_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    CUtensorMap tA, tB;
+    RS_TRY(make_tmap_bf16(&tA, A, (uint64_t)M, (uint64_t)K, (uint64_t)K * 2, G_BM, G_BK));
+    RS_TRY(make_tmap_bf16(&tB, W, (uint64_t)N, (uint64_t)K, (uint64_t)K * 2, G_BN, G_BK));
+    const int n_tiles = (M / G_BM) * (N / G_BN);
+    const int grid = n_tiles < g_num_sms ? n_tiles : g_num_sms;
+    const __nv_bfloat16* b = static_cast<const __nv_bfloat16*>(bias);
+    const float* r = static_cast<const float*>(R);
+    void* c = C;
+#define RS_GEMM_LAUNCH(E)                                                                                     \
+    do {                                                                                                      \
+        static bool attr = false;                                                                             \
+        if (!attr) {                                                                                          \
+            RS_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM)); \
+            attr = true;                                                                                      \
+        }                                                                                                     \
+        gemm_bf16_kernel<E><<<grid, G_THREADS, G_SMEM, st>>>(tA, tB, b, r, c, M, N, K, N);                    \
+    } while (0)
+    switch (epi) {
+        case 0: RS_GEMM_LAUNCH(0); break;
+        case 1: RS_GEMM_LAUNCH(1); break;
+        case 2: RS_GEMM_LAUNCH(2); break;
+        default: RS_GEMM_LAUNCH(3); break;
+    }
+#undef RS_GEMM_LAUNCH
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
+}  // namespace rs
+
+extern "C" int rs_gemm_bf16(const void* A, const void* W, const void* bias, const void* R, void* C, int32_t M,
+                            int32_t N, int32_t K, int32_t epi, void* stream) {
+    return rs::gemm_bf16(A, W, bias, R, C, M, N, K, epi, rs::as_stream(stream));
+}

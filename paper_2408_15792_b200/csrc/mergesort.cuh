@@ -1,0 +1,291 @@
+// Stable merge sort on the device, optionally counting strict inversions.
+//
+// Tiles of 2048 keys (256 threads x 8) are sorted in shared memory (odd-even
+// transposition in registers, then merge-path merges in smem); then log2(n/2048)
+// global merge passes, each CTA producing one 2048-key output tile from a merge-path
+// partition of its run pair staged through shared memory.
+//
+// Inversion counting (pairs i<j with key_i > key_j) rides along for free: a
+// transposition swap removes exactly one inversion, and in a stable merge every
+// element taken from the right run passes exactly the still-unconsumed elements of
+// the left run (all strictly greater). Used for Kendall tau's discordant pairs
+// (Knight's algorithm; ranking.py:45-50 counts the same pairs by an O(n^2) row loop).
+#pragma once
+#include "common.cuh"
+
+namespace rs {
+
+constexpr int MS_THREADS = 256;
+constexpr int MS_ITEMS = 8;
+constexpr int MS_TILE = MS_THREADS * MS_ITEMS;
+
+template <typename K>
+struct KeyTraits;
+template <>
+struct KeyTraits<uint32_t> {
+    static __device__ __forceinline__ uint32_t sentinel() { return 0xffffffffu; }
+    static __device__ __forceinline__ bool less(uint32_t a, uint32_t b) { return a < b; }
+};
+template <>
+struct KeyTraits<uint64_t> {
+    static __device__ __forceinline__ uint64_t sentinel() { return ~0ull; }
+    static __device__ __forceinline__ bool less(uint64_t a, uint64_t b) { return a < b; }
+};
+
+// RankingPolicy sort key (schedulers.py:211-218): class bits (running-pin, unscored,
+// non-priority) in the top 3 bits of `cr`, arrival rank in the low 29 bits, and the
+// order-preserving image of the float64 effective score in `eff`.
+// Compared as (cr >> 29, eff, cr & RANK_MASK).
+struct __align__(16) RankKey {
+    uint64_t eff;
+    uint32_t cr;
+    uint32_t pad;
+};
+template <>
+struct KeyTraits<RankKey> {
+    static __device__ __forceinline__ RankKey sentinel() { return RankKey{~0ull, 0xffffffffu, 0u}; }
+    static __device__ __forceinline__ bool less(const RankKey& a, const RankKey& b) {
+        uint32_t ca = a.cr >> 29, cb = b.cr >> 29;
+        if (ca != cb) return ca < cb;
+        if (a.eff != b.eff) return a.eff < b.eff;
+        return a.cr < b.cr;
+    }
+};
+
+// (arrival_time, id) tuple key of the reference tie-break (schedulers.py:416-417).
+struct __align__(16) Key128 {
+    uint64_t hi;
+    uint64_t lo;
+};
+template <>
+struct KeyTraits<Key128> {
+    static __device__ __forceinline__ Key128 sentinel() { return Key128{~0ull, ~0ull}; }
+    static __device__ __forceinline__ bool less(const Key128& a, const Key128& b) {
+        return a.hi != b.hi ? a.hi < b.hi : a.lo < b.lo;
+    }
+};
+
+template <typename K>
+__device__ __forceinline__ int merge_path(const K* a, int na, const K* b, int nb, int diag) {
+    int lo = max(0, diag - nb), hi = min(diag, na);
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (!KeyTraits<K>::less(b[diag - 1 - mid], a[mid]))
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// Serially merge MS_ITEMS outputs starting at (i, j); a_total is the full length of
+// the left run and a_off the left-run index of a[0] (for inversion counting).
+template <typename K, bool HasVal, bool Count>
+__device__ __forceinline__ void serial_merge(const K* a, const uint32_t* av, int na, const K* b,
+                                             const uint32_t* bv, int nb, int i, int j,
+                                             K (&ok)[MS_ITEMS], uint32_t (&ov)[MS_ITEMS],
+                                             uint64_t a_remaining_base, unsigned long long& inv) {
+#pragma unroll
+    for (int k = 0; k < MS_ITEMS; ++k) {
+        bool take_a;
+        if (i >= na)
+            take_a = false;
+        else if (j >= nb)
+            take_a = true;
+        else
+            take_a = !KeyTraits<K>::less(b[j], a[i]);
+        if (take_a) {
+            ok[k] = a[i];
+            if (HasVal) ov[k] = av[i];
+            ++i;
+        } else {
+            ok[k] = b[j];
+            if (HasVal) ov[k] = bv[j];
+            ++j;
+            if (Count) inv += a_remaining_base - (uint64_t)i;
+        }
+    }
+}
+
+template <typename K, bool HasVal>
+struct MsSmem {
+    K keys[MS_TILE];
+    uint32_t vals[HasVal ? MS_TILE : 1];
+};
+
+__device__ __forceinline__ void block_add_count(unsigned long long v, unsigned long long* out) {
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+}
+
+// Sort each 2048-key tile. keys_in has n valid entries; the tail of the last tile is
+// padded with sentinels (which sort last, stably, and add no strict inversions).
+// vals_in == nullptr => payload is the global index.
+template <typename K, bool HasVal, bool Count>
+__global__ void __launch_bounds__(MS_THREADS) ms_block_sort(const K* __restrict__ keys_in,
+                                                            const uint32_t* __restrict__ vals_in,
+                                                            K* __restrict__ keys_out,
+                                                            uint32_t* __restrict__ vals_out,
+                                                            uint32_t n, unsigned long long* inv_out) {
+    __shared__ MsSmem<K, HasVal> sm;
+    const uint32_t base = blockIdx.x * MS_TILE;
+    for (int k = threadIdx.x; k < MS_TILE; k += MS_THREADS) {
+        uint32_t g = base + k;
+        sm.keys[k] = g < n ? keys_in[g] : KeyTraits<K>::sentinel();
+        if (HasVal) sm.vals[k] = g < n ? (vals_in ? vals_in[g] : g) : 0xffffffffu;
+    }
+    __syncthreads();
+    K rk[MS_ITEMS];
+    uint32_t rv[MS_ITEMS];
+#pragma unroll
+    for (int k = 0; k < MS_ITEMS; ++k) {
+        rk[k] = sm.keys[threadIdx.x * MS_ITEMS + k];
+        if (HasVal) rv[k] = sm.vals[threadIdx.x * MS_ITEMS + k];
+    }
+    unsigned long long inv = 0;
+    // Odd-even transposition: strict swaps only => stable, swap count = inversions.
+#pragma unroll
+    for (int r = 0; r < MS_ITEMS; ++r) {
+#pragma unroll
+        for (int k = (r & 1); k + 1 < MS_ITEMS; k += 2) {
+            if (KeyTraits<K>::less(rk[k + 1], rk[k])) {
+                K t = rk[k];
+                rk[k] = rk[k + 1];
+                rk[k + 1] = t;
+                if (HasVal) {
+                    uint32_t tv = rv[k];
+                    rv[k] = rv[k + 1];
+                    rv[k + 1] = tv;
+                }
+                if (Count) ++inv;
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < MS_ITEMS; ++k) {
+        sm.keys[threadIdx.x * MS_ITEMS + k] = rk[k];
+        if (HasVal) sm.vals[threadIdx.x * MS_ITEMS + k] = rv[k];
+    }
+    __syncthreads();
+    for (int s = MS_ITEMS; s < MS_TILE; s <<= 1) {
+        const int p = threadIdx.x * MS_ITEMS;
+        const int pb = p / (2 * s) * (2 * s);
+        const K* a = sm.keys + pb;
+        const K* b = sm.keys + pb + s;
+        const uint32_t* av = HasVal ? sm.vals + pb : nullptr;
+        const uint32_t* bv = HasVal ? sm.vals + pb + s : nullptr;
+        const int diag = p - pb;
+        const int i = merge_path(a, s, b, s, diag);
+        serial_merge<K, HasVal, Count>(a, av, s, b, bv, s, i, diag - i, rk, rv, (uint64_t)s, inv);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < MS_ITEMS; ++k) {
+            sm.keys[p + k] = rk[k];
+            if (HasVal) sm.vals[p + k] = rv[k];
+        }
+        __syncthreads();
+    }
+    for (int k = threadIdx.x; k < MS_TILE; k += MS_THREADS) {
+        keys_out[base + k] = sm.keys[k];
+        if (HasVal) vals_out[base + k] = sm.vals[k];
+    }
+    if (Count) block_add_count(inv, inv_out);
+}
+
+// One global merge pass: runs of width w -> runs of width 2w over npad keys.
+template <typename K, bool HasVal, bool Count>
+__global__ void __launch_bounds__(MS_THREADS) ms_merge_pass(const K* __restrict__ kin,
+                                                            const uint32_t* __restrict__ vin,
+                                                            K* __restrict__ kout,
+                                                            uint32_t* __restrict__ vout,
+                                                            uint32_t npad, uint32_t w,
+                                                            unsigned long long* inv_out) {
+    __shared__ MsSmem<K, HasVal> sm;
+    __shared__ int split[2];
+    const uint32_t out0 = blockIdx.x * MS_TILE;
+    const uint32_t base = out0 / (2 * w) * (2 * w);
+    const int lenA = (int)min(w, npad - base);
+    const int lenB = (int)min(w, npad - base - (uint32_t)lenA);
+    const K* A = kin + base;
+    const K* B = kin + base + lenA;
+    const int d0 = (int)(out0 - base);
+    const int d1 = d0 + MS_TILE;
+    if (threadIdx.x < 2) split[threadIdx.x] = merge_path(A, lenA, B, lenB, threadIdx.x ? d1 : d0);
+    __syncthreads();
+    const int a0 = split[0], a1 = split[1];
+    const int b0 = d0 - a0, b1 = d1 - a1;
+    const int na = a1 - a0, nb = b1 - b0;
+    for (int k = threadIdx.x; k < MS_TILE; k += MS_THREADS) {
+        if (k < na) {
+            sm.keys[k] = A[a0 + k];
+            if (HasVal) sm.vals[k] = vin[base + a0 + k];
+        } else {
+            sm.keys[k] = B[b0 + k - na];
+            if (HasVal) sm.vals[k] = vin[base + lenA + b0 + k - na];
+        }
+    }
+    __syncthreads();
+    K rk[MS_ITEMS];
+    uint32_t rv[MS_ITEMS];
+    unsigned long long inv = 0;
+    const int diag = threadIdx.x * MS_ITEMS;
+    const int i = merge_path(sm.keys, na, sm.keys + na, nb, diag);
+    // left-run elements not yet consumed when a right element is taken:
+    // lenA - (a0 + i_local)  => base term lenA - a0, minus the local i.
+    serial_merge<K, HasVal, Count>(sm.keys, HasVal ? sm.vals : nullptr, na, sm.keys + na,
+                                   HasVal ? sm.vals + na : nullptr, nb, i, diag - i, rk, rv,
+                                   (uint64_t)(lenA - a0), inv);
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < MS_ITEMS; ++k) {
+        sm.keys[diag + k] = rk[k];
+        if (HasVal) sm.vals[diag + k] = rv[k];
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < MS_TILE; k += MS_THREADS) {
+        kout[out0 + k] = sm.keys[k];
+        if (HasVal) vout[out0 + k] = sm.vals[k];
+    }
+    if (Count) block_add_count(inv, inv_out);
+}
+
+static inline uint32_t ms_padded(uint64_t n) {
+    return (uint32_t)((n + MS_TILE - 1) / MS_TILE * MS_TILE);
+}
+
+// Sort n keys (+ optional u32 payload). k0/k1 and v0/v1 are ping-pong buffers of
+// ms_padded(n) entries. On return *kres / *vres point at the sorted (padded) arrays.
+template <typename K, bool HasVal, bool Count>
+int merge_sort(const K* keys_in, const uint32_t* vals_in, uint32_t n, K* k0, K* k1, uint32_t* v0,
+               uint32_t* v1, unsigned long long* inv, cudaStream_t st, K** kres,
+               uint32_t** vres) {
+    const uint32_t npad = ms_padded(n);
+    const uint32_t tiles = npad / MS_TILE;
+    if (tiles == 0) {
+        *kres = k0;
+        if (vres) *vres = v0;
+        return RS_OK;
+    }
+    ms_block_sort<K, HasVal, Count><<<tiles, MS_THREADS, 0, st>>>(keys_in, vals_in, k0, v0, n, inv);
+    RS_LAUNCH_CHECK();
+    K* ki = k0;
+    K* ko = k1;
+    uint32_t* vi = v0;
+    uint32_t* vo = v1;
+    for (uint32_t w = MS_TILE; w < npad; w <<= 1) {
+        ms_merge_pass<K, HasVal, Count><<<tiles, MS_THREADS, 0, st>>>(ki, vi, ko, vo, npad, w, inv);
+        RS_LAUNCH_CHECK();
+        K* t = ki;
+        ki = ko;
+        ko = t;
+        uint32_t* tv = vi;
+        vi = vo;
+        vo = tv;
+    }
+    *kres = ki;
+    if (vres) *vres = vi;
+    return RS_OK;
+}
+
+}  // namespace rs

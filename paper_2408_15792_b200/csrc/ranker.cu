@@ -1,0 +1,339 @@
+// A5 / K1, K2, K5 + orchestration: the OPT-125M-shape ranker forward.
+//
+// Replaces RankingModelScorer.raw_outputs (predictors.py:245-247: standardise
+// features, _Net.forward) with the paper's predictor: an OPT
+// decoder over the prompt tokens whose last-token hidden state goes through a
+// Linear(d, 1) score head. Per layer (pre-LN, OPT-125M: do_layer_norm_before):
+//   x = LN1(h); qkv = x Wqkv^T + b; a = causal_attn(qkv); h = h + a Wo^T + bo
+//   x = LN2(h); f = relu(x W1^T + b1);                   h = h + f W2^T + b2
+// then g = w . LNf(h[last]) + b. Embedding h0 = E[ids] + P[pos + 2] (OPT's learned
+// positions carry an offset of 2).
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace rs {
+int attention_fwd(const void* qkv, void* out, int B, int S, int H, cudaStream_t st);
+
+constexpr float LN_EPS = 1e-5f;
+
+// One warp per token row: h = tok[id] + pos[p + 2]. The residual stream h is fp32.
+__global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ tok,
+                             const __nv_bfloat16* __restrict__ pos, float* __restrict__ h, int n_tok, int S,
+                             int d, int vocab, int n_rows_padded) {
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= n_rows_padded) return;
+    float4* dst = reinterpret_cast<float4*>(h + (size_t)row * d);
+    const int nv = d / 8;
+    if (row >= n_tok) {
+        for (int k = lane; k < 2 * nv; k += 32) dst[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    int id = ids[row];
+    id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
+    const int p = row % S + 2;
+    const uint4* a = reinterpret_cast<const uint4*>(tok + (size_t)id * d);
+    const uint4* b = reinterpret_cast<const uint4*>(pos + (size_t)p * d);
+    for (int k = lane; k < nv; k += 32) {
+        uint4 x = a[k], y = b[k];
+        const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&x);
+        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&y);
+        float o[8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float2 xf = __bfloat1622float2(x2[q]), yf = __bfloat1622float2(y2[q]);
+            o[2 * q] = xf.x + yf.x;
+            o[2 * q + 1] = xf.y + yf.y;
+        }
+        dst[2 * k] = make_float4(o[0], o[1], o[2], o[3]);
+        dst[2 * k + 1] = make_float4(o[4], o[5], o[6], o[7]);
+    }
+}
+
+template <int VPL>
+__device__ __forceinline__ void load_row_f32(const float* __restrict__ x, int lane, float (&v)[VPL * 8]) {
+    const float4* xr = reinterpret_cast<const float4*>(x);
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+        float4 a = xr[2 * (lane + 32 * k)], b = xr[2 * (lane + 32 * k) + 1];
+        v[k * 8 + 0] = a.x; v[k * 8 + 1] = a.y; v[k * 8 + 2] = a.z; v[k * 8 + 3] = a.w;
+        v[k * 8 + 4] = b.x; v[k * 8 + 5] = b.y; v[k * 8 + 6] = b.z; v[k * 8 + 7] = b.w;
+    }
+}
+// Two-pass mean / biased variance over a warp-distributed row (eps 1e-5, OPT).
+template <int VPL>
+__device__ __forceinline__ void row_stats(const float (&v)[VPL * 8], float& mean, float& rstd) {
+    constexpr int d = VPL * 256;
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < VPL * 8; ++e) s += v[e];
+    mean = warp_sum(s) * (1.0f / d);
+    float s2 = 0.f;
+#pragma unroll
+    for (int e = 0; e < VPL * 8; ++e) {
+        const float t = v[e] - mean;
+        s2 += t * t;
+    }
+    rstd = rsqrtf(warp_sum(s2) * (1.0f / d) + LN_EPS);
+}
+
+// LayerNorm over fp32 rows of d (d % 256 == 0, d <= 2048) -> bf16: one warp per row.
+template <int VPL>  // uint4 (8 bf16) vectors per lane = d / 256
+__global__ void layernorm_kernel(const float* __restrict__ x, const __nv_bfloat16* __restrict__ w,
+                                 const __nv_bfloat16* __restrict__ b, __nv_bfloat16* __restrict__ y, int rows) {
+    constexpr int d = VPL * 256;
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    float v[VPL * 8];
+    load_row_f32<VPL>(x + (size_t)row * d, lane, v);
+    float mean, rstd;
+    row_stats<VPL>(v, mean, rstd);
+    const uint4* wr = reinterpret_cast<const uint4*>(w);
+    const uint4* br = reinterpret_cast<const uint4*>(b);
+    uint4* yr = reinterpret_cast<uint4*>(y + (size_t)row * d);
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+        uint4 wu = wr[lane + 32 * k], bu = br[lane + 32 * k], o;
+        const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wu);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bu);
+        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float2 wf = __bfloat1622float2(w2[q]), bf = __bfloat1622float2(b2[q]);
+            o2[q] = __floats2bfloat162_rn((v[k * 8 + 2 * q] - mean) * rstd * wf.x + bf.x,
+                                          (v[k * 8 + 2 * q + 1] - mean) * rstd * wf.y + bf.y);
+        }
+        yr[lane + 32 * k] = o;
+    }
+}
+
+// K5: g[b] = head_w . LNf(h[b*S + last[b]]) + head_b, one warp per prompt, fp32 out.
+template <int VPL>
+__global__ void head_kernel(const float* __restrict__ h, const int32_t* __restrict__ last, int B, int S,
+                            const __nv_bfloat16* __restrict__ lw, const __nv_bfloat16* __restrict__ lb,
+                            const __nv_bfloat16* __restrict__ hw, const __nv_bfloat16* __restrict__ hb,
+                            float* __restrict__ g, float* __restrict__ score) {
+    constexpr int d = VPL * 256;
+    const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (p >= B) return;
+    int lp = last ? last[p] : S - 1;
+    lp = lp < 0 ? 0 : (lp >= S ? S - 1 : lp);
+    float v[VPL * 8];
+    load_row_f32<VPL>(h + ((size_t)p * S + lp) * d, lane, v);
+    float mean, rstd;
+    row_stats<VPL>(v, mean, rstd);
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+        const int base = (lane + 32 * k) * 8;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const float xn = (v[k * 8 + e] - mean) * rstd * __bfloat162float(lw[base + e]) + __bfloat162float(lb[base + e]);
+            acc = fmaf(xn, __bfloat162float(hw[base + e]), acc);
+        }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) {
+        const float gv = acc + __bfloat162float(hb[0]);
+        g[p] = gv;
+        if (score) score[p] = -gv;  // RankingModelScorer.score_batch negation (predictors.py:249-250)
+    }
+}
+
+struct RankerOffsets {
+    int64_t tok, pos, lnf_w, lnf_b, head_w, head_b;
+    int64_t per_layer0, layer_stride;
+    int64_t ln1_w, ln1_b, qkv_w, qkv_b, out_w, out_b, ln2_w, ln2_b, fc1_w, fc1_b, fc2_w, fc2_b;  // within layer
+    int64_t total;
+};
+
+static int64_t pad64(int64_t x) { return (x + 63) / 64 * 64; }
+
+static RankerOffsets ranker_offsets(const rs_ranker_config& c) {
+    RankerOffsets o{};
+    const int64_t d = c.d_model, F = c.d_ffn;
+    int64_t at = 0;
+    auto take = [&](int64_t n) {
+        int64_t r = at;
+        at += pad64(n);
+        return r;
+    };
+    o.tok = take((int64_t)c.vocab * d);
+    o.pos = take((int64_t)(c.max_pos + 2) * d);
+    o.per_layer0 = at;
+    int64_t l0 = at;
+    o.ln1_w = take(d) - l0;
+    o.ln1_b = take(d) - l0;
+    o.qkv_w = take(3 * d * d) - l0;
+    o.qkv_b = take(3 * d) - l0;
+    o.out_w = take(d * d) - l0;
+    o.out_b = take(d) - l0;
+    o.ln2_w = take(d) - l0;
+    o.ln2_b = take(d) - l0;
+    o.fc1_w = take(F * d) - l0;
+    o.fc1_b = take(F) - l0;
+    o.fc2_w = take(d * F) - l0;
+    o.fc2_b = take(d) - l0;
+    o.layer_stride = at - l0;
+    at = l0 + o.layer_stride * c.n_layers;
+    o.lnf_w = take(d);
+    o.lnf_b = take(d);
+    o.head_w = take(d);
+    o.head_b = take(1);
+    o.total = at;
+    return o;
+}
+
+static int check_cfg(const rs_ranker_config* c) {
+    RS_CHECK_ARG(c != nullptr, "ranker: config is NULL");
+    RS_CHECK_ARG(c->vocab > 0 && c->max_pos > 0 && c->n_layers > 0 && c->n_heads > 0, "ranker: bad config");
+    RS_CHECK_ARG(c->d_model == c->n_heads * 64, "ranker: head dim must be 64 (d_model = 64 * n_heads)");
+    RS_CHECK_ARG(c->d_model % 256 == 0 && c->d_model <= 2048, "ranker: d_model must be a multiple of 256, <= 2048");
+    RS_CHECK_ARG(c->d_ffn % 256 == 0, "ranker: d_ffn must be a multiple of 256");
+    RS_CHECK_ARG(c->activation == 0 || c->activation == 1, "ranker: activation must be 0 (ReLU) or 1 (GELU)");
+    return RS_OK;
+}
+
+constexpr int64_t RK_MAX_TOKENS = 1 << 20;  // activation chunk (tokens) per forward slice
+
+static int64_t chunk_prompts(int32_t B, int32_t S) {
+    int64_t bc = RK_MAX_TOKENS / S;
+    if (bc < 1) bc = 1;
+    if (bc > B) bc = B;
+    return bc;
+}
+
+struct RankerWs {
+    float* h;
+    __nv_bfloat16 *x, *qkv, *att, *ffn;
+};
+template <typename A>
+static void ranker_ws_layout(A& a, const rs_ranker_config& c, int64_t mp, RankerWs* w) {
+    auto h = a.template take<float>(mp * c.d_model);
+    auto x = a.template take<__nv_bfloat16>(mp * c.d_model);
+    auto q = a.template take<__nv_bfloat16>(mp * 3 * c.d_model);
+    auto t = a.template take<__nv_bfloat16>(mp * c.d_model);
+    auto f = a.template take<__nv_bfloat16>(mp * c.d_ffn);
+    if (w) *w = RankerWs{h, x, q, t, f};
+}
+struct RkSizer {
+    ArenaSizer s;
+    template <typename T>
+    T* take(size_t n) { s.take<T>(n); return nullptr; }
+};
+
+static int launch_ln(const float* x, const __nv_bfloat16* w, const __nv_bfloat16* b, __nv_bfloat16* y,
+                     int rows, int d, cudaStream_t st) {
+    const int wpb = 8;
+    const int grid = (rows + wpb - 1) / wpb;
+    switch (d / 256) {
+        case 1: layernorm_kernel<1><<<grid, 32 * wpb, 0, st>>>(x, w, b, y, rows); break;
+        case 2: layernorm_kernel<2><<<grid, 32 * wpb, 0, st>>>(x, w, b, y, rows); break;
+        case 3: layernorm_kernel<3><<<grid, 32 * wpb, 0, st>>>(x, w, b, y, rows); break;
+        case 4: layernorm_kernel<4><<<grid, 32 * wpb, 0, st>>>(x, w, b, y, rows); break;
+        case 8: layernorm_kernel<8><<<grid, 32 * wpb, 0, st>>>(x, w, b, y, rows); break;
+        default: set_error("layernorm: unsupported d=%d", d); return RS_ERR_INVALID;
+    }
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
+static int launch_head(const float* h, const int32_t* last, int B, int S, const __nv_bfloat16* P,
+                       const RankerOffsets& o, int d, float* g, float* score, cudaStream_t st) {
+    const int wpb = 8;
+    const int grid = (B + wpb - 1) / wpb;
+    const __nv_bfloat16 *lw = P + o.lnf_w, *lb = P + o.lnf_b, *hw = P + o.head_w, *hb = P + o.head_b;
+    switch (d / 256) {
+        case 1: head_kernel<1><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score); break;
+        case 2: head_kernel<2><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score); break;
+        case 3: head_kernel<3><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score); break;
+        case 4: head_kernel<4><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score); break;
+        case 8: head_kernel<8><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score); break;
+        default: set_error("head: unsupported d=%d", d); return RS_ERR_INVALID;
+    }
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" int64_t rs_ranker_layout(const rs_ranker_config* cfg, int64_t* off) {
+    if (check_cfg(cfg) != RS_OK) return -1;
+    RankerOffsets o = ranker_offsets(*cfg);
+    if (off) {
+        off[0] = o.tok;
+        off[1] = o.pos;
+        off[2] = o.lnf_w;
+        off[3] = o.lnf_b;
+        off[4] = o.head_w;
+        off[5] = o.head_b;
+        const int64_t per[RS_RANKER_N_PER_LAYER] = {o.ln1_w, o.ln1_b, o.qkv_w, o.qkv_b, o.out_w, o.out_b,
+                                                    o.ln2_w, o.ln2_b, o.fc1_w, o.fc1_b, o.fc2_w, o.fc2_b};
+        for (int l = 0; l < cfg->n_layers; ++l)
+            for (int k = 0; k < RS_RANKER_N_PER_LAYER; ++k)
+                off[RS_RANKER_N_GLOBAL + l * RS_RANKER_N_PER_LAYER + k] = o.per_layer0 + l * o.layer_stride + per[k];
+    }
+    return o.total;
+}
+
+extern "C" size_t rs_ranker_workspace_size(const rs_ranker_config* cfg, int32_t B, int32_t S) {
+    if (check_cfg(cfg) != RS_OK || B <= 0 || S <= 0) return 0;
+    const int64_t bc = chunk_prompts(B, S);
+    const int64_t mp = (bc * S + 127) / 128 * 128;
+    RkSizer s;
+    ranker_ws_layout(s, *cfg, mp, nullptr);
+    return s.s.used + 256;
+}
+
+extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params, const int32_t* ids,
+                                 const int32_t* last_pos, int32_t B, int32_t S, float* g, float* score,
+                                 void* ws, size_t ws_bytes, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    RS_TRY(check_cfg(cfg));
+    RS_CHECK_ARG(B > 0 && S > 0 && S <= cfg->max_pos, "ranker: need B > 0 and 0 < S <= max_pos");
+    RS_CHECK_ARG(S <= 512, "ranker: S <= 512 (attention TMEM layout)");
+    RS_CHECK_ARG(params && ids && g, "ranker: NULL pointer");
+    if (ws_bytes < rs_ranker_workspace_size(cfg, B, S)) {
+        set_error("ranker: workspace %zu < %zu", ws_bytes, rs_ranker_workspace_size(cfg, B, S));
+        return RS_ERR_WORKSPACE;
+    }
+    const RankerOffsets o = ranker_offsets(*cfg);
+    const __nv_bfloat16* P = static_cast<const __nv_bfloat16*>(params);
+    const int d = cfg->d_model, F = cfg->d_ffn, H = cfg->n_heads;
+    const int64_t bc_max = chunk_prompts(B, S);
+    for (int64_t b0 = 0; b0 < B; b0 += bc_max) {
+        const int bc = (int)((B - b0) < bc_max ? (B - b0) : bc_max);
+        const int n_tok = bc * S;
+        const int mp = (n_tok + 127) / 128 * 128;
+        Arena ar(ws, ws_bytes);
+        RankerWs w;
+        ranker_ws_layout(ar, *cfg, mp, &w);
+        {
+            const int wpb = 8;
+            embed_kernel<<<(mp + wpb - 1) / wpb, 32 * wpb, 0, st>>>(ids + b0 * S, P + o.tok, P + o.pos, w.h, n_tok, S,
+                                                                    d, cfg->vocab, mp);
+            RS_LAUNCH_CHECK();
+        }
+        // Rows past the last token are never written by attention but feed the
+        // out-projection (and, as masked keys, the PV MMA: 0 * NaN = NaN), so zero them.
+        if (mp > n_tok) RS_CUDA(cudaMemsetAsync(w.att + (size_t)n_tok * d, 0, (size_t)(mp - n_tok) * d * 2, st));
+        for (int l = 0; l < cfg->n_layers; ++l) {
+            const __nv_bfloat16* L = P + o.per_layer0 + (int64_t)l * o.layer_stride;
+            RS_TRY(launch_ln(w.h, L + o.ln1_w, L + o.ln1_b, w.x, mp, d, st));
+            RS_TRY(gemm_bf16(w.x, L + o.qkv_w, L + o.qkv_b, nullptr, w.qkv, mp, 3 * d, d, 0, st));
+            RS_TRY(attention_fwd(w.qkv, w.att, bc, S, H, st));
+            RS_TRY(gemm_bf16(w.att, L + o.out_w, L + o.out_b, w.h, w.h, mp, d, d, 2, st));
+            RS_TRY(launch_ln(w.h, L + o.ln2_w, L + o.ln2_b, w.x, mp, d, st));
+            RS_TRY(gemm_bf16(w.x, L + o.fc1_w, L + o.fc1_b, nullptr, w.ffn, mp, F, d, cfg->activation == 0 ? 1 : 3, st));
+            RS_TRY(gemm_bf16(w.ffn, L + o.fc2_w, L + o.fc2_b, w.h, w.h, mp, d, F, 2, st));
+        }
+        RS_TRY(launch_head(w.h, last_pos ? last_pos + b0 : nullptr, bc, S, P, o, d, g + b0,
+                           score ? score + b0 : nullptr, st));
+    }
+    return RS_OK;
+}

@@ -1,0 +1,372 @@
+// K9: one scheduling step of the ranking policy over an SoA queue.
+//
+// Reference (schedulers.py):
+//   Policy.schedule (:98-109)   sorted(candidates, key=sort_key); non-preemptive pins
+//                               RUNNING requests first
+//   RankingPolicy.sort_key (:211-218)  (unscored first, priority first, effective score,
+//                               arrival_time, id); effective_score (:203-208)
+//   Policy._fill (:86-96)       greedy in order; stop at max_batch; SKIP (not stop) a
+//                               request whose need = prompt + generated + 1 does not fit
+//   RankingPolicy.schedule (:219-240)  starvation count / quantum update in candidate
+//                               order, then promotion (count >= threshold) or demotion
+//                               (priority and quantum <= 0)
+// Device pipeline: key build -> stable merge sort of (RankKey, index) -> greedy fill
+// (one warp; prefix-sum resolution of each 32-wide chunk) -> elementwise state update
+// with order-preserving compaction of promoted / demoted ids.
+#include "common.cuh"
+#include "mergesort.cuh"
+
+namespace rs {
+
+constexpr uint32_t RANK_BITS = 29;
+constexpr uint32_t RANK_MASK = (1u << RANK_BITS) - 1u;
+
+__global__ void build_rank_keys(rs_queue_soa q, int calibrated, int preemptive, RankKey* __restrict__ keys,
+                                int* __restrict__ err) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (uint32_t)q.n) return;
+    const uint8_t f = q.flags[i];
+    const bool scored = f & RS_FLAG_SCORED;
+    const bool prio = f & RS_FLAG_PRIORITY;
+    const bool running = f & RS_FLAG_RUNNING;
+    double eff = 0.0;
+    if (scored) {
+        double s = q.score_dtype == RS_F32 ? (double)static_cast<const float*>(q.score)[i]
+                                           : static_cast<const double*>(q.score)[i];
+        eff = calibrated ? s - (double)q.generated_tokens[i] : s;
+        if (eff != eff) atomicOr(err, 1);
+    }
+    const uint32_t pin = preemptive ? 0u : (running ? 0u : 1u);
+    const uint32_t cls = (pin << 2) | ((scored ? 1u : 0u) << 1) | (prio ? 0u : 1u);
+    RankKey k;
+    k.eff = orderable_f64(eff);
+    k.cr = (cls << RANK_BITS) | (q.arrival_rank[i] & RANK_MASK);
+    k.pad = 0;
+    keys[i] = k;
+}
+
+// Unlimited KV budget: run = first min(max_batch, n) of the sorted order.
+__global__ void fill_unlimited(const uint32_t* __restrict__ order, const int64_t* __restrict__ id, uint32_t n,
+                               int32_t max_batch, int64_t* __restrict__ run, uint8_t* __restrict__ sched,
+                               int32_t* __restrict__ counts) {
+    const uint32_t m = min((uint32_t)max_batch, n);
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < m; k += gridDim.x * blockDim.x) {
+        uint32_t idx = order[k];
+        run[k] = id[idx];
+        sched[idx] = 1;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = (int32_t)m;
+}
+
+// Budgeted greedy fill, one warp. Within each 32-wide chunk of the sorted order:
+// drop lanes whose own need already exceeds the remaining budget (kv_used only
+// grows, so they can never fit), take the longest prefix of the rest that fits
+// cumulatively, skip the first lane that does not, repeat.
+__global__ void fill_budget(const uint32_t* __restrict__ order, const int32_t* __restrict__ prompt,
+                            const int32_t* __restrict__ gen, const int64_t* __restrict__ id, uint32_t n,
+                            int32_t max_batch, int64_t budget, int64_t* __restrict__ run,
+                            uint8_t* __restrict__ sched, int32_t* __restrict__ counts) {
+    const int lane = threadIdx.x;
+    int64_t used = 0;
+    int32_t taken = 0;
+    for (uint32_t base = 0; base < n && taken < max_batch; base += 32) {
+        const uint32_t k = base + lane;
+        uint32_t idx = 0;
+        int64_t need = 0;
+        bool pending = k < n;
+        if (pending) {
+            idx = order[k];
+            need = (int64_t)prompt[idx] + (int64_t)gen[idx] + 1;
+        }
+        while (taken < max_batch) {
+            if (pending && need > budget - used) pending = false;  // can never fit
+            unsigned mask = __ballot_sync(0xffffffffu, pending);
+            if (!mask) break;
+            int64_t x = pending ? need : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            // lanes that fit if every pending lane up to them is taken
+            const bool fits = pending && (used + x <= budget);
+            const unsigned fmask = __ballot_sync(0xffffffffu, fits);
+            // the taken set is the run of fitting pending lanes before the first
+            // pending lane that does not fit
+            const unsigned nofit = mask & ~fmask;
+            const unsigned before = nofit ? ((nofit & (0u - nofit)) - 1u) : 0xffffffffu;
+            unsigned tmask = fmask & before;
+            // respect max_batch: keep only the lowest (max_batch - taken) lanes
+            const int room = max_batch - taken;
+            if (__popc(tmask) > room) {
+                unsigned m2 = tmask;
+                for (int r = 0; r < room; ++r) m2 &= m2 - 1;  // drop the lowest `room` bits
+                tmask &= ~m2;
+            }
+            const bool take = (tmask >> lane) & 1u;
+            if (take) {
+                const int slot = taken + __popc(tmask & ((1u << lane) - 1u));
+                run[slot] = id[idx];
+                sched[idx] = 1;
+            }
+            int64_t add = take ? need : 0;
+            add = warp_sum(add);
+            used += add;
+            taken += __popc(tmask);
+            if (take) pending = false;
+            // the first non-fitting pending lane is skipped
+            if (nofit && taken < max_batch) {
+                const int f = __ffs(nofit) - 1;
+                if (lane == f && !((tmask >> lane) & 1u)) pending = false;
+            }
+            if (__popc(tmask) == 0 && !nofit) break;
+        }
+    }
+    if (lane == 0) counts[0] = taken;
+}
+
+constexpr int UPD_THREADS = 1024;
+
+// State update (schedulers.py:224-240) + per-block counts of promoted / demoted.
+__global__ void starvation_update(rs_queue_soa q, const uint8_t* __restrict__ sched, int32_t threshold,
+                                  int32_t pquantum, uint8_t* __restrict__ pd, uint32_t* __restrict__ bcnt) {
+    const uint32_t i = blockIdx.x * UPD_THREADS + threadIdx.x;
+    uint8_t code = 0;
+    if (i < (uint32_t)q.n) {
+        uint8_t f = q.flags[i];
+        int32_t st = q.starvation[i];
+        int32_t qu = q.quantum[i];
+        bool prio = f & RS_FLAG_PRIORITY;
+        if (sched[i]) {
+            st = 0;
+            if (prio) qu -= 1;
+        } else {
+            st += 1;
+        }
+        if (threshold > 0 && st >= threshold) {
+            prio = true;
+            qu = pquantum;
+            st = 0;
+            code = 1;
+        } else if (prio && qu <= 0) {
+            prio = false;
+            code = 2;
+        }
+        q.flags[i] = prio ? (f | RS_FLAG_PRIORITY) : (f & ~RS_FLAG_PRIORITY);
+        q.starvation[i] = st;
+        q.quantum[i] = qu;
+        pd[i] = code;
+    }
+    const int np = __syncthreads_count(code == 1);
+    const int nd = __syncthreads_count(code == 2);
+    if (threadIdx.x == 0) {
+        bcnt[2 * blockIdx.x] = np;
+        bcnt[2 * blockIdx.x + 1] = nd;
+    }
+}
+
+// Exclusive scan of the interleaved (promoted, demoted) block counts by one block;
+// writes the totals to counts[1], counts[2].
+__global__ void scan_pairs(uint32_t* __restrict__ bcnt, uint32_t nblk, int32_t* __restrict__ counts) {
+    __shared__ uint32_t tp[1024], td[1024];
+    const uint32_t per = (nblk + 1023) / 1024;
+    const uint32_t b0 = threadIdx.x * per, b1 = min(nblk, b0 + per);
+    uint32_t sp = 0, sd = 0;
+    for (uint32_t b = b0; b < b1; ++b) {
+        sp += bcnt[2 * b];
+        sd += bcnt[2 * b + 1];
+    }
+    tp[threadIdx.x] = sp;
+    td[threadIdx.x] = sd;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t ap = 0, ad = 0;
+        for (int t = 0; t < 1024; ++t) {
+            uint32_t vp = tp[t], vd = td[t];
+            tp[t] = ap;
+            td[t] = ad;
+            ap += vp;
+            ad += vd;
+        }
+        counts[1] = (int32_t)ap;
+        counts[2] = (int32_t)ad;
+    }
+    __syncthreads();
+    uint32_t ap = tp[threadIdx.x], ad = td[threadIdx.x];
+    for (uint32_t b = b0; b < b1; ++b) {
+        uint32_t vp = bcnt[2 * b], vd = bcnt[2 * b + 1];
+        bcnt[2 * b] = ap;
+        bcnt[2 * b + 1] = ad;
+        ap += vp;
+        ad += vd;
+    }
+}
+
+__global__ void scatter_pd(const uint8_t* __restrict__ pd, const int64_t* __restrict__ id, uint32_t n,
+                           const uint32_t* __restrict__ boff, int64_t* __restrict__ prom, int64_t* __restrict__ dem) {
+    __shared__ uint32_t wp[UPD_THREADS / 32], wd[UPD_THREADS / 32];
+    const uint32_t i = blockIdx.x * UPD_THREADS + threadIdx.x;
+    const uint8_t c = i < n ? pd[i] : 0;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned bp = __ballot_sync(0xffffffffu, c == 1);
+    const unsigned bd = __ballot_sync(0xffffffffu, c == 2);
+    if (lane == 0) {
+        wp[w] = __popc(bp);
+        wd[w] = __popc(bd);
+    }
+    __syncthreads();
+    if (w == 0) {
+        uint32_t xp = wp[lane], xd = wd[lane];
+        uint32_t ip = xp, id2 = xd;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t yp = __shfl_up_sync(0xffffffffu, ip, o);
+            uint32_t yd = __shfl_up_sync(0xffffffffu, id2, o);
+            if (lane >= (uint32_t)o) {
+                ip += yp;
+                id2 += yd;
+            }
+        }
+        wp[lane] = ip - xp;
+        wd[lane] = id2 - xd;
+    }
+    __syncthreads();
+    const unsigned below = (1u << lane) - 1u;
+    if (c == 1) prom[boff[2 * blockIdx.x] + wp[w] + __popc(bp & below)] = id[i];
+    if (c == 2) dem[boff[2 * blockIdx.x + 1] + wd[w] + __popc(bd & below)] = id[i];
+}
+
+__global__ void build_arrival_keys(const double* __restrict__ arr, const int64_t* __restrict__ id, uint32_t n,
+                                   Key128* __restrict__ keys) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) keys[i] = Key128{orderable_f64(arr[i]), orderable_i64(id[i])};
+}
+__global__ void invert_perm(const uint32_t* __restrict__ order, uint32_t n, uint32_t* __restrict__ rank) {
+    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) rank[order[k]] = k;
+}
+
+struct RankWs {
+    RankKey* ka;
+    RankKey* kb;
+    uint32_t* va;
+    uint32_t* vb;
+    uint8_t* sched;
+    uint8_t* pd;
+    uint32_t* bcnt;
+    int* err;
+};
+template <typename A>
+static void rank_layout(A& a, uint64_t n, RankWs* w) {
+    const uint32_t np = ms_padded(n);
+    const uint32_t nblk = (uint32_t)((n + UPD_THREADS - 1) / UPD_THREADS) + 1;
+    auto ka = a.template take<RankKey>(np);
+    auto kb = a.template take<RankKey>(np);
+    auto va = a.template take<uint32_t>(np);
+    auto vb = a.template take<uint32_t>(np);
+    auto sc = a.template take<uint8_t>(n + 1);
+    auto pd = a.template take<uint8_t>(n + 1);
+    auto bc = a.template take<uint32_t>(2 * nblk);
+    auto er = a.template take<int>(4);
+    if (w) *w = RankWs{ka, kb, va, vb, sc, pd, bc, er};
+}
+struct RankSizer {
+    ArenaSizer s;
+    template <typename T>
+    T* take(size_t c) { s.take<T>(c); return nullptr; }
+};
+
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" size_t rs_arrival_rank_workspace_size(int64_t n) {
+    const uint32_t np = ms_padded((uint64_t)(n > 0 ? n : 1));
+    ArenaSizer s;
+    s.take<Key128>(np);
+    s.take<Key128>(np);
+    s.take<uint32_t>(np);
+    s.take<uint32_t>(np);
+    return s.used + 256;
+}
+
+extern "C" int rs_arrival_rank(const double* arr, const int64_t* id, int64_t n, uint32_t* rank, void* ws,
+                               size_t ws_bytes, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    RS_CHECK_ARG(n >= 0 && n <= (int64_t)RANK_MASK, "rs_arrival_rank: n out of range");
+    if (n == 0) return RS_OK;
+    if (ws_bytes < rs_arrival_rank_workspace_size(n)) {
+        set_error("rs_arrival_rank: workspace too small");
+        return RS_ERR_WORKSPACE;
+    }
+    const uint32_t un = (uint32_t)n, np = ms_padded(un);
+    Arena ar(ws, ws_bytes);
+    Key128* ka = ar.take<Key128>(np);
+    Key128* kb = ar.take<Key128>(np);
+    uint32_t* va = ar.take<uint32_t>(np);
+    uint32_t* vb = ar.take<uint32_t>(np);
+    const int T = 256;
+    build_arrival_keys<<<(un + T - 1) / T, T, 0, st>>>(arr, id, un, kb);
+    RS_LAUNCH_CHECK();
+    Key128* sk;
+    uint32_t* sv;
+    RS_TRY((merge_sort<Key128, true, false>(kb, nullptr, un, ka, kb, va, vb, nullptr, st, &sk, &sv)));
+    invert_perm<<<(un + T - 1) / T, T, 0, st>>>(sv, un, rank);
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
+extern "C" size_t rs_rank_step_workspace_size(int64_t n) {
+    RankSizer s;
+    rank_layout(s, (uint64_t)(n > 0 ? n : 1), nullptr);
+    return s.s.used + 256;
+}
+
+extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv_budget, int32_t threshold,
+                            int32_t pquantum, int32_t calibrated, int32_t preemptive, int64_t* run,
+                            int64_t* prom, int64_t* dem, int32_t* counts, void* ws, size_t ws_bytes,
+                            void* stream) {
+    cudaStream_t st = as_stream(stream);
+    RS_CHECK_ARG(q != nullptr, "rs_rank_step: queue is NULL");
+    RS_CHECK_ARG(q->n >= 0 && q->n <= (int64_t)RANK_MASK, "rs_rank_step: n out of range");
+    RS_CHECK_ARG(max_batch >= 1, "max_batch must be >= 1");
+    RS_CHECK_ARG(threshold >= 0, "starvation_threshold must be >= 0");
+    RS_CHECK_ARG(pquantum >= 1, "priority_quantum must be >= 1");
+    RS_CHECK_ARG(q->score_dtype == RS_F32 || q->score_dtype == RS_F64, "score dtype must be f32/f64");
+    const uint32_t n = (uint32_t)q->n;
+    if (n == 0) {
+        RS_CUDA(cudaMemsetAsync(counts, 0, 4 * sizeof(int32_t), st));
+        return RS_OK;
+    }
+    if (ws_bytes < rs_rank_step_workspace_size(n)) {
+        set_error("rs_rank_step: workspace too small");
+        return RS_ERR_WORKSPACE;
+    }
+    Arena ar(ws, ws_bytes);
+    RankWs w;
+    rank_layout(ar, n, &w);
+    RS_CUDA(cudaMemsetAsync(w.sched, 0, n, st));
+    RS_CUDA(cudaMemsetAsync(counts, 0, 4 * sizeof(int32_t), st));
+    const int T = 256;
+    build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
+    RS_LAUNCH_CHECK();
+    RankKey* sk;
+    uint32_t* order;
+    RS_TRY((merge_sort<RankKey, true, false>(w.kb, nullptr, n, w.ka, w.kb, w.va, w.vb, nullptr, st, &sk, &order)));
+    if (kv_budget < 0) {
+        fill_unlimited<<<(min(n, (uint32_t)max_batch) + T - 1) / T, T, 0, st>>>(order, q->id, n, max_batch, run,
+                                                                             w.sched, counts);
+    } else {
+        fill_budget<<<1, 32, 0, st>>>(order, q->prompt_tokens, q->generated_tokens, q->id, n, max_batch,
+                                      kv_budget, run, w.sched, counts);
+    }
+    RS_LAUNCH_CHECK();
+    const uint32_t nblk = (n + UPD_THREADS - 1) / UPD_THREADS;
+    starvation_update<<<nblk, UPD_THREADS, 0, st>>>(*q, w.sched, threshold, pquantum, w.pd, w.bcnt);
+    RS_LAUNCH_CHECK();
+    scan_pairs<<<1, 1024, 0, st>>>(w.bcnt, nblk, counts);
+    RS_LAUNCH_CHECK();
+    scatter_pd<<<nblk, UPD_THREADS, 0, st>>>(w.pd, q->id, n, w.bcnt, prom, dem);
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}

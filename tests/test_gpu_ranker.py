@@ -1,0 +1,79 @@
+"""K1-K5 OPT-shape ranker on the B200 vs the fp32 oracle (oracle/opt_ranker.py, pinned
+to transformers' OPTModel). Tolerance: |g - g_ref| <= 1e-2 * max(1, |g_ref|),
+tau(g, g_ref) >= 0.99."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import opt_ranker
+from oracle import ranking_oracle as ro
+
+pytestmark = pytest.mark.gpu
+
+
+def _attn_ref(qkv, B, S, H):
+    q, k, v = qkv.float().view(B, S, 3, H, 64).permute(2, 0, 3, 1, 4)
+    o = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+    return o.permute(0, 2, 1, 3).reshape(B * S, H * 64)
+
+
+@pytest.mark.parametrize("B,S,H", [(1, 128, 1), (2, 64, 12), (3, 200, 12), (4, 512, 12), (37, 128, 12),
+                                   (2, 384, 2)])
+def test_attention_matches_fp32(B, S, H):
+    from paper_2408_15792_b200 import _lib
+    _lib.device()
+    g = torch.Generator(device="cuda").manual_seed(B * S + H)
+    qkv = (torch.randn(B * S, 3 * H * 64, device="cuda", generator=g) * 1.5).bfloat16()
+    out = torch.full((B * S, H * 64), float("nan"), dtype=torch.bfloat16, device="cuda")
+    _lib.check(_lib.load().rs_attention_fwd(qkv.data_ptr(), out.data_ptr(), B, S, H, _lib.stream_handle()))
+    ref = _attn_ref(qkv, B, S, H)
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2, err
+
+
+@pytest.mark.parametrize("n_layers,B,S", [(1, 2, 128), (2, 8, 64), (2, 3, 100)])
+def test_ranker_small_matches_oracle(n_layers, B, S):
+    from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
+    cfg = RankerConfig.opt_125m(n_layers=n_layers)
+    m = OptRanker(cfg, seed=n_layers)
+    ids = torch.randint(4, cfg.vocab, (B, S), generator=torch.Generator().manual_seed(S), dtype=torch.int32)
+    last = torch.randint(0, S, (B,), generator=torch.Generator().manual_seed(1), dtype=torch.int32)
+    g = m.forward(ids.cuda(), last.cuda()).cpu().double()
+    ref = opt_ranker.forward(m.params_cpu_fp32(), cfg, ids.numpy(), last.numpy()).double()
+    assert ((g - ref).abs() <= 1e-2 * ref.abs().clamp(min=1)).all(), (g, ref)
+
+
+def test_opt125m_full_depth_matches_oracle():
+    from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
+    cfg = RankerConfig.opt_125m()
+    m = OptRanker(cfg, seed=0)
+    B, S = 256, 128
+    ids = torch.randint(4, cfg.vocab, (B, S), generator=torch.Generator().manual_seed(0), dtype=torch.int32)
+    g = m.forward(ids.cuda()).cpu().double()
+    ref = opt_ranker.forward(m.params_cpu_fp32(), cfg, ids.numpy()).double()
+    assert ((g - ref).abs() <= 1e-2 * ref.abs().clamp(min=1)).all(), (g - ref).abs().max()
+    tau = ro.kendall_tau_b(g.numpy(), ref.numpy())[0]
+    assert tau >= 0.99, tau
+
+
+def test_opt125m_s512_matches_oracle():
+    from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
+    cfg = RankerConfig.opt_125m()
+    m = OptRanker(cfg, seed=0)
+    B, S = 8, 512
+    ids = torch.randint(4, cfg.vocab, (B, S), generator=torch.Generator().manual_seed(5), dtype=torch.int32)
+    g = m.forward(ids.cuda()).cpu().double()
+    ref = opt_ranker.forward(m.params_cpu_fp32(), cfg, ids.numpy()).double()
+    assert ((g - ref).abs() <= 1e-2 * ref.abs().clamp(min=1)).all(), (g - ref).abs().max()
+
+
+def test_ranker_batch_independence_and_chunking():
+    """A prompt's score does not depend on its batch neighbours (chunked activations)."""
+    from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
+    cfg = RankerConfig.opt_125m(n_layers=2)
+    m = OptRanker(cfg, seed=3)
+    ids = torch.randint(4, cfg.vocab, (2100, 512), generator=torch.Generator().manual_seed(9), dtype=torch.int32)
+    g_all = m.forward(ids.cuda())
+    g_part = m.forward(ids[2090:].cuda())
+    torch.testing.assert_close(g_all[2090:], g_part, rtol=0, atol=0)

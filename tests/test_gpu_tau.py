@@ -1,0 +1,87 @@
+"""K10 tau counts on the B200 vs the reference (golden vectors) — bit-exact C, D, tau."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def test_tau_golden_bit_exact(golden):
+    from paper_2408_15792_b200.ranking import kendall_tau_b
+    for c in golden["tau_golden"]["cases"]:
+        r = kendall_tau_b(c["x"], c["y"])
+        assert (r.concordant, r.discordant, r.n_pairs) == (c["concordant"], c["discordant"], c["n_pairs"]), c["tag"]
+        assert r.tau == c["tau"], c["tag"]
+
+
+@pytest.mark.parametrize("xdt", [np.float32, np.float64, np.int32, np.int64])
+@pytest.mark.parametrize("ydt", [np.float32, np.float64, np.int32, np.int64])
+def test_tau_dtypes_agree_with_oracle(xdt, ydt):
+    from oracle import tau_c
+    from paper_2408_15792_b200.ranking import kendall_tau_b
+    rng = np.random.default_rng(17)
+    n = 5000
+    x = rng.integers(-50, 50, n).astype(xdt)
+    y = rng.integers(0, 30, n).astype(ydt)
+    r = kendall_tau_b(x, y)
+    C, D, n1, n2, _ = tau_c.tau_counts(x, y)
+    assert (r.concordant, r.discordant) == (C, D)
+    n0 = n * (n - 1) // 2
+    assert r.tau == (C - D) / math.sqrt((n0 - n1) * (n0 - n2))
+
+
+def test_tau_float64_precision_semantics():
+    # int64 values that collide once cast to float64 must tie (np.asarray(..., float64))
+    from paper_2408_15792_b200.ranking import kendall_tau_b
+    from oracle import ranking_oracle as ro
+    big = 2 ** 53
+    x = np.array([big, big + 1, big + 2, 5, -3], dtype=np.int64)
+    y = np.array([1, 2, 3, 4, 5], dtype=np.int64)
+    r = kendall_tau_b(x, y)
+    assert (r.tau, r.concordant, r.discordant, r.n_pairs) == ro.kendall_tau_b(x, y)
+
+
+def test_tau_rejects_bad_input():
+    from paper_2408_15792_b200.ranking import kendall_tau_b
+    with pytest.raises(ValueError):
+        kendall_tau_b([1, 2], [1, 2, 3])
+    with pytest.raises(ValueError):
+        kendall_tau_b([1.0, float("nan"), 2.0], [1, 2, 3])
+    assert kendall_tau_b([], []).tau == 0.0
+
+
+def test_tau_1m_matches_reference(golden):
+    import recipes
+    from paper_2408_15792_b200.ranking import kendall_tau_b
+    if "large_golden" not in golden:
+        pytest.skip("large golden not generated")
+    for variant, g in golden["large_golden"]["tau"].items():
+        x, y = recipes.tau_1m(variant)
+        r = kendall_tau_b(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda())
+        assert (r.concordant, r.discordant) == (g["concordant"], g["discordant"]), variant
+        n0 = g["n"] * (g["n"] - 1) // 2
+        assert r.tau == (g["concordant"] - g["discordant"]) / math.sqrt((n0 - g["n1"]) * (n0 - g["n2"]))
+
+
+def test_tau_large_n_properties():
+    """Size-independent identities at 16M: tau(x, x) = 1 with ties excluded, antisymmetry,
+    permutation invariance, and C + D + n1 + n2 - n3 = n0."""
+    from paper_2408_15792_b200.ranking import tau_counts_device
+    g = torch.Generator(device="cuda").manual_seed(3)
+    n = 1 << 24
+    x = torch.randn(n, device="cuda", generator=g)
+    y = torch.randint(1, 2049, (n,), device="cuda", generator=g, dtype=torch.int32)
+    c = tau_counts_device(x, y).cpu().tolist()
+    n0 = n * (n - 1) // 2
+    C, D, n1, n2, n3, nan = c
+    assert nan == 0 and C + D + n1 + n2 - n3 == n0
+    cm = tau_counts_device(-x, y).cpu().tolist()
+    assert (cm[0], cm[1]) == (D, C)
+    perm = torch.randperm(n, device="cuda", generator=g)
+    cp = tau_counts_device(x[perm].contiguous(), y[perm].contiguous()).cpu().tolist()
+    assert cp[:5] == c[:5]
+    cs = tau_counts_device(y, y).cpu().tolist()
+    assert cs[1] == 0 and cs[0] == n0 - cs[2]
