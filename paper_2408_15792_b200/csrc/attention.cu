@@ -30,15 +30,42 @@ constexpr int AT_MAXKB = 4;  // S <= 512
 constexpr int AT_Q_BYTES = AT_TILE * AT_D * 2;   // 16 KB
 constexpr int AT_KV_BYTES = AT_TILE * AT_D * 2;  // 16 KB each of K and V
 constexpr int AT_P_BYTES = AT_TILE * AT_TILE * 2;  // 32 KB
-constexpr int AT_THREADS = 256;
-constexpr int AT_SMEM = AT_Q_BYTES + 4 * AT_KV_BYTES + 2 * AT_P_BYTES + 1024 + 256;
+constexpr int AT_QST = 2;   // Q buffers: the next item's Q loads while this one computes
+constexpr int AT_KVST = 3;  // K/V ring depth (runs ahead across items)
+constexpr int AT_THREADS = 384;  // 4 control warps + 8 softmax warps
+
+__device__ __forceinline__ float fast_exp2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+// 2^x for x <= 0 on the FMA pipe (offloads the MUFU): round-to-nearest split
+// x = j + f, f in [-0.5, 0.5], degree-4 polynomial for 2^f (rel. err ~1e-5, far below
+// the bf16 rounding P gets), exponent add for 2^j.
+__device__ __forceinline__ float poly_exp2(float x) {
+    x = fmaxf(x, -126.0f);
+    const float t = x + 12582912.0f;  // 1.5 * 2^23: low mantissa bits = round(x)
+    const float j = t - 12582912.0f;
+    const float f = x - j;
+    float p = fmaf(f, 0.0096181291f, 0.0555041087f);
+    p = fmaf(p, f, 0.2402265070f);
+    p = fmaf(p, f, 0.6931471806f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + ((__float_as_int(t) - 0x4B400000) << 23));
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+constexpr int AT_SMEM = AT_QST * AT_Q_BYTES + AT_KVST * 2 * AT_KV_BYTES + 2 * AT_P_BYTES + 1024 + 8192;
 
 struct AtBars {
-    uint64_t q_full, q_empty, o_full, o_empty;
-    uint64_t kv_full[2], kv_empty[2];
+    uint64_t q_full[AT_QST], q_empty[AT_QST], o_full, o_empty;
+    uint64_t kv_full[AT_KVST], kv_empty[AT_KVST];
     uint64_t s_full[2], s_empty[2];
     uint64_t p_full[2], p_empty[2];
     uint32_t tmem;
+    float redm[2 * 2 * 128];         // row-max exchange between the two column halves
+    float redl[2 * AT_MAXKB * 128];  // row-sum exchange at the end of an item
 };
 
 __global__ void __launch_bounds__(AT_THREADS, 1)
@@ -46,10 +73,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                          int H) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;
-    uint8_t* sK = sQ + AT_Q_BYTES;          // 2 stages
-    uint8_t* sV = sK + 2 * AT_KV_BYTES;     // 2 stages
-    uint8_t* sP = sV + 2 * AT_KV_BYTES;     // 2 buffers
+    uint8_t* sQ = smem;                          // AT_QST buffers
+    uint8_t* sK = sQ + AT_QST * AT_Q_BYTES;      // AT_KVST stages
+    uint8_t* sV = sK + AT_KVST * AT_KV_BYTES;    // AT_KVST stages
+    uint8_t* sP = sV + AT_KVST * AT_KV_BYTES;    // 2 buffers
     AtBars* bar = reinterpret_cast<AtBars*>(sP + 2 * AT_P_BYTES);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -59,16 +86,20 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tqkv);
-        mbar_init(&bar->q_full, 1);
-        mbar_init(&bar->q_empty, 1);
-        mbar_init(&bar->o_full, 1);
-        mbar_init(&bar->o_empty, 4);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < AT_QST; ++i) {
+            mbar_init(&bar->q_full[i], 1);
+            mbar_init(&bar->q_empty[i], 1);
+        }
+        for (int i = 0; i < AT_KVST; ++i) {
             mbar_init(&bar->kv_full[i], 1);
             mbar_init(&bar->kv_empty[i], 1);
+        }
+        mbar_init(&bar->o_full, 1);
+        mbar_init(&bar->o_empty, 8);
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&bar->s_full[i], 1);
-            mbar_init(&bar->s_empty[i], 4);
-            mbar_init(&bar->p_full[i], 4);
+            mbar_init(&bar->s_empty[i], 8);
+            mbar_init(&bar->p_full[i], 8);
             mbar_init(&bar->p_empty[i], 1);
         }
         fence_barrier_init();
@@ -95,12 +126,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                 int b, h, qt;
                 decode(item, b, h, qt);
                 const int row0 = b * S;
-                mbar_wait(&bar->q_empty, (t & 1) ^ 1);
-                mbar_arrive_expect_tx(&bar->q_full, AT_Q_BYTES);
-                tma_load_2d(sQ, &tqkv, &bar->q_full, h * AT_D, row0 + qt * AT_TILE);
+                const int qb = t % AT_QST;
+                mbar_wait(&bar->q_empty[qb], ((t / AT_QST) & 1) ^ 1);
+                mbar_arrive_expect_tx(&bar->q_full[qb], AT_Q_BYTES);
+                tma_load_2d(sQ + qb * AT_Q_BYTES, &tqkv, &bar->q_full[qb], h * AT_D, row0 + qt * AT_TILE);
                 for (int j = 0; j <= qt; ++j, ++kvc) {
-                    const int st = kvc & 1;
-                    mbar_wait(&bar->kv_empty[st], ((kvc >> 1) & 1) ^ 1);
+                    const int st = kvc % AT_KVST;
+                    mbar_wait(&bar->kv_empty[st], ((kvc / AT_KVST) & 1) ^ 1);
                     mbar_arrive_expect_tx(&bar->kv_full[st], 2 * AT_KV_BYTES);
                     tma_load_2d(sK + st * AT_KV_BYTES, &tqkv, &bar->kv_full[st], dm + h * AT_D, row0 + j * AT_TILE);
                     tma_load_2d(sV + st * AT_KV_BYTES, &tqkv, &bar->kv_full[st], 2 * dm + h * AT_D,
@@ -118,13 +150,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                 decode(item, b, h, qt);
                 const int nkb = qt + 1;
                 const int kvbase = kvc;
-                mbar_wait(&bar->q_full, t & 1);
+                const int qb = t % AT_QST;
+                mbar_wait(&bar->q_full[qb], (t / AT_QST) & 1);
                 auto issue_pv = [&](int jj) {
                     const int pb = pc & 1;
                     mbar_wait(&bar->p_full[pb], (pc >> 1) & 1);
                     if (jj == 0) mbar_wait(&bar->o_empty, (t & 1) ^ 1);
                     tc_fence_after();
-                    const int st = (kvbase + jj) & 1;
+                    const int st = (kvbase + jj) % AT_KVST;
                     const uint32_t pa = smem_u32(sP + pb * AT_P_BYTES);
                     const uint32_t vb = smem_u32(sV + st * AT_KV_BYTES);
                     const uint32_t d = tmem + 256 + jj * AT_D;
@@ -138,19 +171,19 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                     ++pc;
                 };
                 for (int j = 0; j < nkb; ++j, ++kvc, ++sc) {
-                    const int st = kvc & 1;
+                    const int st = kvc % AT_KVST;
                     const int sb = sc & 1;
                     mbar_wait(&bar->s_empty[sb], ((sc >> 1) & 1) ^ 1);
-                    mbar_wait(&bar->kv_full[st], (kvc >> 1) & 1);
+                    mbar_wait(&bar->kv_full[st], (kvc / AT_KVST) & 1);
                     tc_fence_after();
-                    const uint32_t qa = smem_u32(sQ);
+                    const uint32_t qa = smem_u32(sQ + qb * AT_Q_BYTES);
                     const uint32_t ka = smem_u32(sK + st * AT_KV_BYTES);
 #pragma unroll
                     for (int k = 0; k < AT_D / 16; ++k)
                         mma_bf16_ss(tmem + sb * AT_TILE, desc_kmajor_sw128(qa + k * 32), desc_kmajor_sw128(ka + k * 32),
                                     id_s, k != 0);
                     mma_commit(&bar->s_full[sb]);
-                    if (j == nkb - 1) mma_commit(&bar->q_empty);
+                    if (j == nkb - 1) mma_commit(&bar->q_empty[qb]);
                     if (j >= 1) issue_pv(j - 1);
                 }
                 issue_pv(nkb - 1);
@@ -158,61 +191,77 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             }
         }
     } else if (warp >= 4) {
+        // 8 softmax warps: warp w and w+4 share TMEM lane quarter q4 (rows q4*32..+31)
+        // and split the 128 key columns of each block (half 0: keys 0-63, half 1: 64-127).
         const int q4 = warp & 3;
+        const int half = (warp - 4) >> 2;
         const int r = q4 * 32 + lane;  // query row within the tile == TMEM lane
         const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
         const float sl2 = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
+        float* redm = bar->redm;  // [2 parity][2 half][128]
+        float* redl = bar->redl;  // [2 half][AT_MAXKB][128]
         int t = 0, sc = 0, pc = 0;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++t) {
             int b, h, qt;
             decode(item, b, h, qt);
             const int nkb = qt + 1;
             float mj[AT_MAXKB], lj[AT_MAXKB];
-            for (int j = 0; j < nkb; ++j, ++sc, ++pc) {
+#pragma unroll
+            for (int j = 0; j < AT_MAXKB; ++j) {
+                mj[j] = 0.f;
+                lj[j] = 0.f;
+            }
+#pragma unroll
+            for (int j = 0; j < AT_MAXKB; ++j) {
+                if (j >= nkb) break;
                 const int sb = sc & 1;
                 mbar_wait(&bar->s_full[sb], (sc >> 1) & 1);
                 tc_fence_after();
-                const uint32_t sa = tmem + lane_addr + sb * AT_TILE;
-                const int lim = (j == qt) ? r : AT_TILE - 1;  // causal: key c valid iff c <= lim
+                const uint32_t sa = tmem + lane_addr + sb * AT_TILE + half * 64;
+                // causal: key c (within this half) valid iff half*64 + c <= lim
+                const int lim = ((j == qt) ? r : AT_TILE - 1) - half * 64;
+                uint32_t v[64];
+                tmem_ld_32x32b_x32(sa, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+                tmem_ld_32x32b_x32(sa + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+                tmem_ld_wait();
                 float m = -INFINITY;
-                uint32_t v[32];
-#pragma unroll 1
-                for (int c = 0; c < AT_TILE; c += 32) {
-                    tmem_ld_32x32b_x32(sa + c, v);
-                    tmem_ld_wait();
+                if (lim >= 63) {
 #pragma unroll
-                    for (int e = 0; e < 32; ++e)
-                        if (c + e <= lim) m = fmaxf(m, __uint_as_float(v[e]));
+                    for (int e = 0; e < 64; ++e) m = fmaxf(m, __uint_as_float(v[e]));
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 64; ++e)
+                        if (e <= lim) m = fmaxf(m, __uint_as_float(v[e]));
                 }
+                // row max across the two halves (smem, double-buffered by block parity)
+                redm[(sb * 2 + half) * AT_TILE + r] = m;
+                named_bar_sync(1 + q4, 64);
+                m = fmaxf(redm[(sb * 2 + 0) * AT_TILE + r], redm[(sb * 2 + 1) * AT_TILE + r]);
                 const int pb = pc & 1;
                 mbar_wait(&bar->p_empty[pb], ((pc >> 1) & 1) ^ 1);
-                uint8_t* prow = sP + pb * AT_P_BYTES;
                 const float ms = m * sl2;
                 float l = 0.f;
-#pragma unroll 1
-                for (int c = 0; c < AT_TILE; c += 32) {
-                    tmem_ld_32x32b_x32(sa + c, v);
-                    tmem_ld_wait();
-                    uint32_t pk[16];
+                uint32_t pk[32];
 #pragma unroll
-                    for (int e = 0; e < 32; e += 2) {
-                        float p0 = (c + e <= lim) ? exp2f(fmaf(__uint_as_float(v[e]), sl2, -ms)) : 0.f;
-                        float p1 = (c + e + 1 <= lim) ? exp2f(fmaf(__uint_as_float(v[e + 1]), sl2, -ms)) : 0.f;
-                        pk[e / 2] = pack_bf16(p0, p1);
-                        // the normaliser uses the bf16-rounded P the MMA consumes
-                        float2 rb = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&pk[e / 2]));
-                        l += rb.x + rb.y;
-                    }
-                    // 4 x 16-byte chunks of this row, K-major SW128 (chunk ^= row % 8)
-                    uint8_t* blk = prow + (c >> 6) * (AT_TILE * 128) + r * 128;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int ch = ((c & 63) >> 3) + q;
-                        *reinterpret_cast<uint4*>(blk + ((ch ^ (r & 7)) << 4)) =
-                            make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                    }
+                for (int e = 0; e < 64; e += 2) {
+                    // even columns on the MUFU, odd ones by polynomial on the FMA pipe
+                    float p0 = fast_exp2(fmaf(__uint_as_float(v[e]), sl2, -ms));
+                    float p1 = poly_exp2(fmaf(__uint_as_float(v[e + 1]), sl2, -ms));
+                    if (e > lim) p0 = 0.f;
+                    if (e + 1 > lim) p1 = 0.f;
+                    pk[e / 2] = pack_bf16(p0, p1);
+                    // the normaliser uses the bf16-rounded P the MMA consumes
+                    float2 rb = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&pk[e / 2]));
+                    l += rb.x + rb.y;
                 }
                 tc_fence_before();
+                // this row's 8 x 16-byte chunks of key block `half`, K-major SW128
+                // (chunk index ^= row % 8)
+                uint8_t* blk = sP + pb * AT_P_BYTES + half * (AT_TILE * 128) + r * 128;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    *reinterpret_cast<uint4*>(blk + ((q ^ (r & 7)) << 4)) =
+                        make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
@@ -221,27 +270,41 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                 }
                 mj[j] = m;
                 lj[j] = l;
+                ++sc;
+                ++pc;
             }
-            // combine the partial outputs
+            // combine the partial outputs: exchange the per-half row sums, then each
+            // warp of the pair produces 32 of the 64 output columns
+#pragma unroll
+            for (int j = 0; j < AT_MAXKB; ++j)
+                if (j < nkb) redl[(half * AT_MAXKB + j) * AT_TILE + r] = lj[j];
+            named_bar_sync(1 + q4, 64);
             float mx = mj[0];
-            for (int j = 1; j < nkb; ++j) mx = fmaxf(mx, mj[j]);
+#pragma unroll
+            for (int j = 1; j < AT_MAXKB; ++j)
+                if (j < nkb) mx = fmaxf(mx, mj[j]);
             float w[AT_MAXKB];
             float den = 0.f;
-            for (int j = 0; j < nkb; ++j) {
-                w[j] = exp2f((mj[j] - mx) * sl2);
-                den += w[j] * lj[j];
+#pragma unroll
+            for (int j = 0; j < AT_MAXKB; ++j) {
+                w[j] = 0.f;
+                if (j < nkb) {
+                    w[j] = exp2f((mj[j] - mx) * sl2);
+                    den += w[j] * (redl[(0 * AT_MAXKB + j) * AT_TILE + r] + redl[(1 * AT_MAXKB + j) * AT_TILE + r]);
+                }
             }
+            named_bar_sync(1 + q4, 64);  // redl may be rewritten by the next item
             const float inv = 1.f / den;
             mbar_wait(&bar->o_full, t & 1);
             tc_fence_after();
             const int qi = qt * AT_TILE + r;
-            __nv_bfloat16* orow = out + ((size_t)b * S + qi) * dm + h * AT_D;
-#pragma unroll 1
-            for (int c = 0; c < AT_D; c += 32) {
-                float acc[32];
+            const int c = half * 32;
+            float acc[32];
 #pragma unroll
-                for (int e = 0; e < 32; ++e) acc[e] = 0.f;
-                for (int j = 0; j < nkb; ++j) {
+            for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+#pragma unroll
+            for (int j = 0; j < AT_MAXKB; ++j) {
+                if (j < nkb) {
                     uint32_t v[32];
                     tmem_ld_32x32b_x32(tmem + lane_addr + 256 + j * AT_D + c, v);
                     tmem_ld_wait();
@@ -249,18 +312,19 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 #pragma unroll
                     for (int e = 0; e < 32; ++e) acc[e] = fmaf(wj, __uint_as_float(v[e]), acc[e]);
                 }
-                if (qi < S) {
-                    uint4* o4 = reinterpret_cast<uint4*>(orow + c);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        o4[q] = make_uint4(pack_bf16(acc[8 * q], acc[8 * q + 1]), pack_bf16(acc[8 * q + 2], acc[8 * q + 3]),
-                                           pack_bf16(acc[8 * q + 4], acc[8 * q + 5]),
-                                           pack_bf16(acc[8 * q + 6], acc[8 * q + 7]));
-                }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->o_empty);
+            if (qi < S) {
+                __nv_bfloat16* orow = out + ((size_t)b * S + qi) * dm + h * AT_D + c;
+                uint4* o4 = reinterpret_cast<uint4*>(orow);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    o4[q] = make_uint4(pack_bf16(acc[8 * q], acc[8 * q + 1]), pack_bf16(acc[8 * q + 2], acc[8 * q + 3]),
+                                       pack_bf16(acc[8 * q + 4], acc[8 * q + 5]),
+                                       pack_bf16(acc[8 * q + 6], acc[8 * q + 7]));
+            }
         }
     }
     tc_fence_before();

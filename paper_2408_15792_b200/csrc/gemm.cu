@@ -200,6 +200,207 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     if (warp == 2) tmem_dealloc<512>(tmem_base);
 }
 
+// ---------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a 256 x 256 output tile per cluster of 2 CTAs. Each CTA
+// TMA-loads its 128-row half of A and its 128-row half of W into the same smem offsets;
+// the leader issues tcgen05.mma.cta_group::2 (M=256, N=256, K=16) over both halves, so
+// every SM streams only half of the W tile (half the smem operand bandwidth of the
+// 1-CTA kernel at the same tile size). Accumulators live in each CTA's TMEM (its 128
+// rows x 256 columns, double-buffered); the epilogue stages 32x32 sub-tiles in swizzled
+// smem and writes them with TMA stores.
+// ---------------------------------------------------------------------------------------
+constexpr int G2_BM = 256, G2_BN = 256, G2_BK = 64, G2_STAGES = 6;
+constexpr int G2_HALF = 128;
+constexpr int G2_A_BYTES = G2_HALF * G2_BK * 2;  // 16 KB per CTA
+constexpr int G2_B_BYTES = G2_HALF * G2_BK * 2;  // 16 KB per CTA
+constexpr int G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;
+constexpr int G2_EPI_BUF = 32 * 32 * 4;          // one 32x32 fp32 (or bf16) staging sub-tile
+constexpr int G2_SMEM = G2_STAGES * G2_STAGE_BYTES + 4 * 2 * G2_EPI_BUF + 1024 + 256;
+
+template <int EPI>
+__global__ void __launch_bounds__(G_THREADS, 1)
+    gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
+                         const __grid_constant__ CUtensorMap tC, const __nv_bfloat16* __restrict__ bias,
+                         const float* __restrict__ R, int M, int N, int K, int ldc) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + G2_STAGES * G2_A_BYTES;
+    uint8_t* sE = smem + G2_STAGES * G2_STAGE_BYTES;  // epilogue staging: 4 warps x 2 buffers
+    uint64_t* full = reinterpret_cast<uint64_t*>(sE + 4 * 2 * G2_EPI_BUF);
+    uint64_t* empty = full + G2_STAGES;
+    uint64_t* tfull = empty + G2_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tA);
+        tma_prefetch_desc(&tB);
+        tma_prefetch_desc(&tC);
+        for (int s = 0; s < G2_STAGES; ++s) {
+            mbar_init(&full[s], 2);  // leader: both CTAs' producers arrive (+ 64 KB of tx)
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);  // leader: 4 epilogue warps x 2 CTAs
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc_2sm<512>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int tiles_n = N / G2_BN;
+    const int n_tiles = (M / G2_BM) * tiles_n;
+    const int kblocks = K / G2_BK;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = cid; tile < n_tiles; tile += ncl) {
+                const int m0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
+                const int n0 = (tile % tiles_n) * G2_BN + rank * G2_HALF;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader)
+                        mbar_arrive_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);
+                    else
+                        mbar_arrive_cluster(&full[stage], 0);
+                    tma_load_2d_2sm(sA + stage * G2_A_BYTES, &tA, &full[stage], kb * G2_BK, m0, pol_a);
+                    tma_load_2d_2sm(sB + stage * G2_B_BYTES, &tB, &full[stage], kb * G2_BK, n0, pol_b);
+                    if (++stage == G2_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && elect_one()) {
+            constexpr uint32_t idesc = idesc_bf16(G2_BM, G2_BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = cid; tile < n_tiles; tile += ncl) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem_base + acc * G2_BN;
+                for (int kb = 0; kb < kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + stage * G2_A_BYTES);
+                    const uint32_t b0 = smem_u32(sB + stage * G2_B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < G2_BK / 16; ++k)
+                        mma_bf16_ss_2sm(d, desc_kmajor_sw128(a0 + k * 32), desc_kmajor_sw128(b0 + k * 32), idesc,
+                                        (kb | k) != 0);
+                    mma_commit_2sm(&empty[stage], 0x3);
+                    if (++stage == G2_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                mma_commit_2sm(&tfull[acc], 0x3);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        const int q = warp & 3;
+        const int row = q * 32 + lane;
+        uint8_t* ebuf = sE + q * 2 * G2_EPI_BUF;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        int nst = 0;  // staging sub-tiles issued by this warp (buffer = nst & 1)
+        for (int tile = cid; tile < n_tiles; tile += ncl) {
+            const int m0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
+            const int n0 = (tile % tiles_n) * G2_BN;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const float* rrow = (EPI == 2) ? R + (size_t)(m0 + row) * ldc + n0 : nullptr;
+#pragma unroll 1
+            for (int c = 0; c < G2_BN; c += 32, ++nst) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * G2_BN + c, r);
+                float v[32];
+                const uint4* bv = reinterpret_cast<const uint4*>(bias + n0 + c);
+                float4 rr[8];
+                if (EPI == 2) {
+                    const float4* rv = reinterpret_cast<const float4*>(rrow + c);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) rr[j] = rv[j];
+                }
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint4 b4 = __ldg(bv + j);
+                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b4);
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        float2 bf = __bfloat1622float2(b2[h]);
+                        v[j * 8 + 2 * h] = __uint_as_float(r[j * 8 + 2 * h]) + bf.x;
+                        v[j * 8 + 2 * h + 1] = __uint_as_float(r[j * 8 + 2 * h + 1]) + bf.y;
+                    }
+                }
+                uint8_t* buf = ebuf + (nst & 1) * G2_EPI_BUF;
+                // the TMA store that last read this buffer (two sub-tiles ago) must be done
+                if (lane == 0 && nst >= 2) tma_store_wait_read<1>();
+                __syncwarp();
+                if (EPI == 2) {
+                    // fp32 32x32 sub-tile, 128-B rows, SWIZZLE_128B: chunk j ^ (row % 8)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                            make_float4(v[4 * j] + rr[j].x, v[4 * j + 1] + rr[j].y, v[4 * j + 2] + rr[j].z,
+                                        v[4 * j + 3] + rr[j].w);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        if (EPI == 1) v[j] = fmaxf(v[j], 0.0f);
+                        if (EPI == 3) v[j] = gelu_tanh(v[j]);
+                    }
+                    // bf16 32x32 sub-tile, 64-B rows, SWIZZLE_64B: chunk j ^ ((row / 2) % 4)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                            make_uint4(pack_bf16(v[j * 8 + 0], v[j * 8 + 1]), pack_bf16(v[j * 8 + 2], v[j * 8 + 3]),
+                                       pack_bf16(v[j * 8 + 4], v[j * 8 + 5]), pack_bf16(v[j * 8 + 6], v[j * 8 + 7]));
+                }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tC, buf, n0 + c, m0 + q * 32);
+                    tma_store_commit();
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+        if (lane == 0) tma_store_wait<0>();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc_2sm<512>(tmem_base);
+}
+
 static int g_num_sms = 0;
 
 int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, void* C, int M, int N, int K, int epi,
@@ -214,6 +415,53 @@ int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, voi
         int dev;
         RS_CUDA(cudaGetDevice(&dev));
         RS_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    if (M % G2_BM == 0 && N % G2_BN == 0) {
+        // CTA-pair kernel (the path the ranker takes: it pads M to 256)
+        CUtensorMap tA, tB, tC;
+        RS_TRY(make_tmap_bf16(&tA, A, (uint64_t)M, (uint64_t)K, (uint64_t)K * 2, G2_HALF, G2_BK));
+        RS_TRY(make_tmap_bf16(&tB, W, (uint64_t)N, (uint64_t)K, (uint64_t)K * 2, G2_HALF, G2_BK));
+        if (epi == 2)
+            RS_TRY(make_tmap_2d(&tC, C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)M, (uint64_t)N, (uint64_t)N * 4,
+                                32, 32, CU_TENSOR_MAP_SWIZZLE_128B));
+        else
+            RS_TRY(make_tmap_2d(&tC, C, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)M, (uint64_t)N, (uint64_t)N * 2,
+                                32, 32, CU_TENSOR_MAP_SWIZZLE_64B));
+        const int n_tiles = (M / G2_BM) * (N / G2_BN);
+        int clusters = g_num_sms / 2;
+        if (n_tiles < clusters) clusters = n_tiles;
+        const __nv_bfloat16* b = static_cast<const __nv_bfloat16*>(bias);
+        const float* r = static_cast<const float*>(R);
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(2 * clusters);
+        lc.blockDim = dim3(G_THREADS);
+        lc.dynamicSmemBytes = G2_SMEM;
+        lc.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+#define RS_GEMM2_LAUNCH(E)                                                                                        \
+    do {                                                                                                          \
+        static bool attr = false;                                                                                 \
+        if (!attr) {                                                                                              \
+            RS_CUDA(cudaFuncSetAttribute(gemm_bf16_2sm_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM)); \
+            attr = true;                                                                                          \
+        }                                                                                                         \
+        RS_CUDA(cudaLaunchKernelEx(&lc, gemm_bf16_2sm_kernel<E>, tA, tB, tC, b, r, M, N, K, N));                \
+    } while (0)
+        switch (epi) {
+            case 0: RS_GEMM2_LAUNCH(0); break;
+            case 1: RS_GEMM2_LAUNCH(1); break;
+            case 2: RS_GEMM2_LAUNCH(2); break;
+            default: RS_GEMM2_LAUNCH(3); break;
+        }
+#undef RS_GEMM2_LAUNCH
+        RS_LAUNCH_CHECK();
+        return RS_OK;
     }
     CUtensorMap tA, tB;
     RS_TRY(make_tmap_bf16(&tA, A, (uint64_t)M, (uint64_t)K, (uint64_t)K * 2, G_BM, G_BK));

@@ -284,7 +284,7 @@ extern "C" int64_t rs_ranker_layout(const rs_ranker_config* cfg, int64_t* off) {
 extern "C" size_t rs_ranker_workspace_size(const rs_ranker_config* cfg, int32_t B, int32_t S) {
     if (check_cfg(cfg) != RS_OK || B <= 0 || S <= 0) return 0;
     const int64_t bc = chunk_prompts(B, S);
-    const int64_t mp = (bc * S + 127) / 128 * 128;
+    const int64_t mp = (bc * S + 255) / 256 * 256;  // CTA-pair GEMM tiles are 256 rows
     RkSizer s;
     ranker_ws_layout(s, *cfg, mp, nullptr);
     return s.s.used + 256;
@@ -309,7 +309,7 @@ extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params
     for (int64_t b0 = 0; b0 < B; b0 += bc_max) {
         const int bc = (int)((B - b0) < bc_max ? (B - b0) : bc_max);
         const int n_tok = bc * S;
-        const int mp = (n_tok + 127) / 128 * 128;
+        const int mp = (n_tok + 255) / 256 * 256;
         Arena ar(ws, ws_bytes);
         RankerWs w;
         ranker_ws_layout(ar, *cfg, mp, &w);

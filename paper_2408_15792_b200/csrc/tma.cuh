@@ -32,4 +32,26 @@ static inline int make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t rows
     }
     return RS_OK;
 }
+// Generic 2-D map (any element type) for TMA stores of epilogue sub-tiles.
+static inline int make_tmap_2d(CUtensorMap* m, const void* base, CUtensorMapDataType dt, uint32_t esize, uint64_t rows,
+                               uint64_t cols, uint64_t row_pitch_bytes, uint32_t box_rows, uint32_t box_cols,
+                               CUtensorMapSwizzle sw) {
+    if (!g_encode_tiled) {
+        int s = resolve_tma_encoder();
+        if (s != RS_OK) return s;
+    }
+    (void)esize;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {row_pitch_bytes};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode_tiled(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (store) failed (%d)", (int)r);
+        return RS_ERR_INVALID;
+    }
+    return RS_OK;
+}
 }  // namespace rs

@@ -1,0 +1,153 @@
+"""Scorer plugin for the OPT-shape ranker (drop-in for the ranksched Scorer protocol).
+
+The reference Scorer contract (predictors.py:35-51): class attributes `kind`,
+`length_calibrated`, `warmup_tokens`, `charges_predictor`; `score_batch(requests,
+seed) -> list[float | None]`; `to_dict()` with a `kind` key. RankingModelScorer
+(predictors.py:228-259) negates the net output so that the ascending sort puts
+predicted-short requests first; OptRankerScorer keeps that orientation with the
+paper's OPT backbone in place of the 24-feature _Net.
+
+Serialization (predictors.py:486-527 uses JSON for the tiny linear model): 125M bf16
+parameters do not fit the JSON payload, so save_scorer writes the JSON header (same
+`format`/`version` keys, kind "opt-ranker") plus a raw little-endian bf16 sidecar
+`<path>.bin` whose sha256 the header records.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import hashlib
+import json
+import pathlib
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .ranker import OptRanker, RankerConfig
+from .workload import prompt_token_ids
+
+_SCORER_FORMAT = "ranksched-scorer"
+_SCORER_VERSION = 1
+
+
+class OptRankerScorer:
+    """OPT-125M-shape ranker; score = -(net output), not length calibrated."""
+
+    kind = "opt-ranker"
+    length_calibrated = False
+    warmup_tokens = 0
+    charges_predictor = True
+
+    def __init__(self, model: OptRanker | None = None, seq_len: int = 128, cfg: RankerConfig | None = None,
+                 seed: int = 0):
+        self.model = model if model is not None else OptRanker(cfg or RankerConfig(), seed=seed)
+        self.seq_len = int(seq_len)
+        self.weights_path: str | None = None
+
+    def encode(self, requests) -> tuple[torch.Tensor, torch.Tensor]:
+        """Prompts -> (ids int32 [n, S], last_pos int32 [n]) in pinned host memory."""
+        n = len(requests)
+        ids = torch.empty((n, self.seq_len), dtype=torch.int32).pin_memory()
+        last = torch.empty(n, dtype=torch.int32).pin_memory()
+        ids_np, last_np = ids.numpy(), last.numpy()
+        for k, r in enumerate(requests):
+            ids_np[k], last_np[k] = prompt_token_ids(getattr(r, "prompt", "") or "", self.seq_len,
+                                                     self.model.cfg.vocab)
+        return ids, last
+
+    def raw_outputs(self, requests) -> np.ndarray:
+        if not requests:
+            return np.zeros(0)
+        ids, last = self.encode(requests)
+        dev = self.model.dev
+        g = self.model.forward(ids.to(dev, non_blocking=True), last.to(dev, non_blocking=True))
+        return g.double().cpu().numpy()
+
+    def score_batch(self, requests, seed) -> list[float | None]:
+        return [-float(v) for v in self.raw_outputs(list(requests))]
+
+    def to_dict(self) -> dict:
+        if self.weights_path is None:
+            raise ValueError("opt-ranker weights are saved by save_scorer(); call it before to_dict()")
+        return {"kind": self.kind, "config": dataclasses.asdict(self.model.cfg), "seq_len": self.seq_len,
+                "weights": self.weights_path, "weights_sha256": _sha256_file(self.weights_path)}
+
+
+def _sha256_file(path) -> str:
+    h = hashlib.sha256()
+    with open(path, "rb") as fh:
+        for chunk in iter(lambda: fh.read(1 << 24), b""):
+            h.update(chunk)
+    return h.hexdigest()
+
+
+def save_scorer(scorer: OptRankerScorer, path: str) -> None:
+    """JSON header at `path` + raw bf16 parameters at `path + '.bin'`."""
+    p = pathlib.Path(path)
+    weights = str(p) + ".bin"
+    scorer.model.flat.view(torch.int16).cpu().numpy().tofile(weights)
+    scorer.weights_path = weights
+    payload = {"format": _SCORER_FORMAT, "version": _SCORER_VERSION}
+    payload.update(scorer.to_dict())
+    p.write_text(json.dumps(payload) + "\n", encoding="utf-8")
+
+
+def scorer_from_dict(obj: dict):
+    """`kind == "opt-ranker"` -> OptRankerScorer; other kinds belong to the reference
+    (ranksched.predictors.scorer_from_dict; install() chains the two)."""
+    kind = obj.get("kind")
+    if kind != OptRankerScorer.kind:
+        raise ValueError(f"unknown scorer kind {kind!r}")
+    cfg = RankerConfig(**obj["config"])
+    model = OptRanker(cfg, seed=None)
+    weights = obj["weights"]
+    if obj.get("weights_sha256") and _sha256_file(weights) != obj["weights_sha256"]:
+        raise ValueError(f"{weights}: checksum mismatch")
+    raw = np.fromfile(weights, dtype=np.int16)
+    if raw.size != model.flat.numel():
+        raise ValueError(f"{weights}: {raw.size} parameters, expected {model.flat.numel()}")
+    model.flat.view(torch.int16).copy_(torch.from_numpy(raw))
+    s = OptRankerScorer(model, seq_len=obj.get("seq_len", 128))
+    s.weights_path = weights
+    return s
+
+
+def load_scorer(path: str):
+    with open(path, "r", encoding="utf-8") as fh:
+        obj = json.load(fh)
+    if obj.get("format") != _SCORER_FORMAT:
+        raise ValueError(f"{path}: not a scorer file")
+    if obj.get("version") != _SCORER_VERSION:
+        raise ValueError(f"{path}: unsupported scorer version {obj.get('version')}")
+    return scorer_from_dict(obj)
+
+
+@dataclass(frozen=True)
+class TrainConfig:
+    """The reference's TrainConfig fields (predictors.py:308-318) plus the ranker shape.
+
+    Defaults follow the paper's recipe for the OPT predictor: Adam lr
+    2e-5, betas (0.9, 0.999), list (batch) size 32, bucket width 10, 5 epochs.
+    `lists_per_step` batches that many independent lists per optimizer step (the
+    reference does one list per step; with lists_per_step=1 the update sequence is
+    the reference's)."""
+
+    epochs: int = 5
+    batch_size: int = 32
+    learning_rate: float = 2e-5
+    betas: tuple[float, float] = (0.9, 0.999)
+    bucket_width: int = 10
+    hidden: int = 0
+    checkpoint_every: int = 20
+    eval_fraction: float = 0.2
+    seed: int = 0
+    seq_len: int = 128
+    lists_per_step: int = 1
+
+
+@dataclass
+class TrainResult:
+    scorer: object
+    report: dict = field(default_factory=dict)
