@@ -160,6 +160,23 @@ int rs_ranker_forward(const rs_ranker_config* cfg, const void* params_dev, const
                       const int32_t* last_pos_dev, int32_t B, int32_t S, float* g_dev, float* score_dev,
                       void* ws_dev, size_t ws_bytes, void* stream);
 
+/* ---- A10/K7/K8: training (ListMLE over whole lists, predictors.py:347-406) ----------
+ * Accumulates into grad_dev (fp32, rs_ranker_layout order and length) the gradient of
+ * sum over lists of list_mle_loss(g_list, order_list) / list_len, where g = the ranker's
+ * net output for the list's prompts and order_list = stable argsort of
+ * lengths // bucket_width (predictors.py:379-384). ids: int32 [n_lists * list_len, S]
+ * (S <= 128); lengths: int32 [n_lists * list_len]; loss_dev[n_lists] = per-list loss / n.
+ * Processes lists_per_micro lists at a time. Deterministic (no float atomics). */
+size_t rs_ranker_grad_workspace_size(const rs_ranker_config* cfg, int32_t lists_per_micro, int32_t list_len, int32_t S);
+int rs_ranker_grad(const rs_ranker_config* cfg, const void* params_dev, float* grad_dev, const int32_t* ids_dev,
+                   const int32_t* lengths_dev, int32_t n_lists, int32_t list_len, int32_t S, int32_t bucket_width,
+                   int32_t lists_per_micro, float* loss_dev, void* ws_dev, size_t ws_bytes, void* stream);
+/* Adam (predictors.py:218-225) over the flat buffer: g = grad * grad_scale; m, v, fp32
+ * master updated with bias correction at step t (>= 1); the bf16 working copy is
+ * rewritten and grad is zeroed for the next accumulation. */
+int rs_adam_step(float* master_dev, float* m_dev, float* v_dev, float* grad_dev, void* params_bf16_dev, int64_t n,
+                 float lr, float beta1, float beta2, float eps, int64_t t, float grad_scale, void* stream);
+
 /* ---- building blocks exported for parity tests ---------------------------------
  * C[M,N] (row-major) = epi(A[M,K] . W[N,K]^T + bias[N]) with A/W bf16 K-major.
  * epi: 0 = none, 1 = ReLU, 3 = GELU(tanh) -> C bf16; 2 = + residual R[M,N] -> C, R
@@ -170,6 +187,21 @@ int rs_gemm_bf16(const void* A_dev, const void* W_dev, const void* bias_dev, con
 /* Causal multi-head attention over packed qkv [B*S, 3*H*64] bf16 -> out [B*S, H*64]. */
 int rs_attention_fwd(const void* qkv_dev, void* out_dev, int32_t B, int32_t S, int32_t H,
                      void* stream);
+/* Diagnostics: as rs_attention_fwd, and CTA 0's softmax warp writes per-block phase
+ * timestamps (clock64) to trace_dev[64 * 8] (zero-initialise it). */
+int rs_attention_fwd_trace(const void* qkv_dev, void* out_dev, int32_t B, int32_t S, int32_t H,
+                           unsigned long long* trace_dev, void* stream);
+/* General CTA-pair GEMM used by the backward pass: a_mn / b_mn = operand stored
+ * MN-contiguous ([K, M] / [K, N]); epi 4 = fp32 out, 5 = bf16 out * (aux > 0) (ReLU
+ * backward, aux bf16 [M, N]), 6 = fp32 split-K partials (C holds k_splits x [M, N]).
+ * M, N multiples of 256, K of 64. bias may be NULL for epi >= 4. */
+int rs_gemm_bf16_ex(const void* A_dev, const void* W_dev, const void* bias_dev, const void* aux_dev, void* C_dev,
+                    int32_t M, int32_t N, int32_t K, int32_t epi, int32_t a_mn, int32_t b_mn, int32_t k_splits,
+                    void* stream);
+/* Causal attention backward for S <= 128: dqkv [B*S, 3*H*64] bf16 from the forward's
+ * qkv, its output att [B*S, H*64] and dout = d loss / d att. */
+int rs_attention_bwd(const void* qkv_dev, const void* att_dev, const void* dout_dev, void* dqkv_dev, int32_t B,
+                     int32_t S, int32_t H, void* stream);
 /* Number of kernels this library has launched in the process (all entry points). */
 uint64_t rs_launch_count(void);
 

@@ -65,6 +65,15 @@ SIGNATURES = {
     "rs_gemm_bf16": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "rs_attention_fwd": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "rs_launch_count": (ctypes.c_uint64, []),
+    "rs_ranker_grad_workspace_size": (c_sz, [ctypes.POINTER(RankerConfig), c_i32, c_i32, c_i32]),
+    "rs_ranker_grad": (ctypes.c_int, [ctypes.POINTER(RankerConfig), c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32,
+                                      c_i32, c_vp, c_vp, c_sz, c_vp]),
+    "rs_adam_step": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.c_float, ctypes.c_float,
+                                    ctypes.c_float, ctypes.c_float, c_i64, ctypes.c_float, c_vp]),
+    "rs_attention_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
+    "rs_attention_fwd_trace": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp]),
+    "rs_gemm_bf16_ex": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                       c_vp]),
 }
 
 _lock = threading.Lock()

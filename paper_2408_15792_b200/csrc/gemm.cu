@@ -217,11 +217,15 @@ constexpr int G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;
 constexpr int G2_EPI_BUF = 32 * 32 * 4;          // one 32x32 fp32 (or bf16) staging sub-tile
 constexpr int G2_SMEM = G2_STAGES * G2_STAGE_BYTES + 4 * 2 * G2_EPI_BUF + 1024 + 256;
 
-template <int EPI>
+// EPI: 0 bf16, 1 ReLU->bf16, 2 +fp32 residual->fp32, 3 GELU->bf16, 4 fp32 (bias optional),
+// 5 bf16 * (mask > 0) with the bf16 mask in `aux` (ReLU backward), 6 fp32 split-K partial
+// (slice `split` of C). A_MN / B_MN: operand stored MN-contiguous ([K, M] / [K, N]).
+template <int EPI, bool A_MN = false, bool B_MN = false>
 __global__ void __launch_bounds__(G_THREADS, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                          const __grid_constant__ CUtensorMap tC, const __nv_bfloat16* __restrict__ bias,
-                         const float* __restrict__ R, int M, int N, int K, int ldc) {
+                         const void* __restrict__ aux, int M, int N, int K, int ldc, int k_splits) {
+    const float* R = static_cast<const float*>(aux);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
@@ -257,26 +261,48 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     const int tiles_n = N / G2_BN;
-    const int n_tiles = (M / G2_BM) * tiles_n;
-    const int kblocks = K / G2_BK;
+    const int n_work = (M / G2_BM) * tiles_n * k_splits;
+    const int kblocks_all = K / G2_BK;
+    const int kb_per = (kblocks_all + k_splits - 1) / k_splits;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    // work item w -> output tile (w / k_splits) and K split (w % k_splits)
+    auto kb_range = [&](int w, int& kb0, int& kb1) {
+        const int sp = w % k_splits;
+        kb0 = sp * kb_per;
+        kb1 = min(kblocks_all, kb0 + kb_per);
+    };
 
     if (warp == 0) {
         if (elect_one()) {
             const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = cid; tile < n_tiles; tile += ncl) {
+            for (int w = cid; w < n_work; w += ncl) {
+                const int tile = w / k_splits;
+                int kb0, kb1;
+                kb_range(w, kb0, kb1);
                 const int m0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
                 const int n0 = (tile % tiles_n) * G2_BN + rank * G2_HALF;
-                for (int kb = 0; kb < kblocks; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader)
                         mbar_arrive_expect_tx(&full[stage], 2 * G2_STAGE_BYTES);
                     else
                         mbar_arrive_cluster(&full[stage], 0);
-                    tma_load_2d_2sm(sA + stage * G2_A_BYTES, &tA, &full[stage], kb * G2_BK, m0, pol_a);
-                    tma_load_2d_2sm(sB + stage * G2_B_BYTES, &tB, &full[stage], kb * G2_BK, n0, pol_b);
+                    if (A_MN) {  // two 64(M) x 64(K) boxes, 8 KB apart (the MN-major LBO)
+                        tma_load_2d_2sm(sA + stage * G2_A_BYTES, &tA, &full[stage], m0, kb * G2_BK, pol_a);
+                        tma_load_2d_2sm(sA + stage * G2_A_BYTES + 8192, &tA, &full[stage], m0 + 64, kb * G2_BK,
+                                        pol_a);
+                    } else {
+                        tma_load_2d_2sm(sA + stage * G2_A_BYTES, &tA, &full[stage], kb * G2_BK, m0, pol_a);
+                    }
+                    if (B_MN) {
+                        tma_load_2d_2sm(sB + stage * G2_B_BYTES, &tB, &full[stage], n0, kb * G2_BK, pol_b);
+                        tma_load_2d_2sm(sB + stage * G2_B_BYTES + 8192, &tB, &full[stage], n0 + 64, kb * G2_BK,
+                                        pol_b);
+                    } else {
+                        tma_load_2d_2sm(sB + stage * G2_B_BYTES, &tB, &full[stage], kb * G2_BK, n0, pol_b);
+                    }
                     if (++stage == G2_STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -286,24 +312,30 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         }
     } else if (warp == 1) {
         if (leader && elect_one()) {
-            constexpr uint32_t idesc = idesc_bf16(G2_BM, G2_BN);
+            constexpr uint32_t idesc = idesc_bf16(G2_BM, G2_BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = cid; tile < n_tiles; tile += ncl) {
+            for (int w = cid; w < n_work; w += ncl) {
+                int kb0, kb1;
+                kb_range(w, kb0, kb1);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * G2_BN;
-                for (int kb = 0; kb < kblocks; ++kb) {
+                for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a0 = smem_u32(sA + stage * G2_A_BYTES);
                     const uint32_t b0 = smem_u32(sB + stage * G2_B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < G2_BK / 16; ++k)
-                        mma_bf16_ss_2sm(d, desc_kmajor_sw128(a0 + k * 32), desc_kmajor_sw128(b0 + k * 32), idesc,
-                                        (kb | k) != 0);
+                    for (int k = 0; k < G2_BK / 16; ++k) {
+                        // K-major: +32 B per 16-element K step inside the 128-B swizzle row;
+                        // MN-major: +16 K rows of 128 B
+                        const uint64_t ad = A_MN ? desc_mnmajor_sw128(a0 + k * 2048, 8192) : desc_kmajor_sw128(a0 + k * 32);
+                        const uint64_t bd = B_MN ? desc_mnmajor_sw128(b0 + k * 2048, 8192) : desc_kmajor_sw128(b0 + k * 32);
+                        mma_bf16_ss_2sm(d, ad, bd, idesc, (kb != kb0) || (k != 0));
+                    }
                     mma_commit_2sm(&empty[stage], 0x3);
                     if (++stage == G2_STAGES) {
                         stage = 0;
@@ -324,12 +356,17 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         int nst = 0;  // staging sub-tiles issued by this warp (buffer = nst & 1)
-        for (int tile = cid; tile < n_tiles; tile += ncl) {
+        for (int w = cid; w < n_work; w += ncl) {
+            const int tile = w / k_splits;
             const int m0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
             const int n0 = (tile % tiles_n) * G2_BN;
+            // split-K partials land in slice (w % k_splits) of a [k_splits * M, N] buffer
+            const int mo = (EPI == 6) ? m0 + (w % k_splits) * M : m0;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const float* rrow = (EPI == 2) ? R + (size_t)(m0 + row) * ldc + n0 : nullptr;
+            const __nv_bfloat16* mrow =
+                (EPI == 5) ? static_cast<const __nv_bfloat16*>(aux) + (size_t)(m0 + row) * ldc + n0 : nullptr;
 #pragma unroll 1
             for (int c = 0; c < G2_BN; c += 32, ++nst) {
                 uint32_t r[32];
@@ -337,34 +374,63 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 float v[32];
                 const uint4* bv = reinterpret_cast<const uint4*>(bias + n0 + c);
                 float4 rr[8];
+                uint4 mk[4];
                 if (EPI == 2) {
                     const float4* rv = reinterpret_cast<const float4*>(rrow + c);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) rr[j] = rv[j];
                 }
+                if (EPI == 5) {
+                    const uint4* mv = reinterpret_cast<const uint4*>(mrow + c);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) mk[j] = mv[j];
+                }
                 tmem_ld_wait();
+                if (bias != nullptr) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    uint4 b4 = __ldg(bv + j);
-                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b4);
+                    for (int j = 0; j < 4; ++j) {
+                        uint4 b4 = __ldg(bv + j);
+                        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b4);
 #pragma unroll
-                    for (int h = 0; h < 4; ++h) {
-                        float2 bf = __bfloat1622float2(b2[h]);
-                        v[j * 8 + 2 * h] = __uint_as_float(r[j * 8 + 2 * h]) + bf.x;
-                        v[j * 8 + 2 * h + 1] = __uint_as_float(r[j * 8 + 2 * h + 1]) + bf.y;
+                        for (int h = 0; h < 4; ++h) {
+                            float2 bf = __bfloat1622float2(b2[h]);
+                            v[j * 8 + 2 * h] = __uint_as_float(r[j * 8 + 2 * h]) + bf.x;
+                            v[j * 8 + 2 * h + 1] = __uint_as_float(r[j * 8 + 2 * h + 1]) + bf.y;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                }
+                if (EPI == 5) {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const __nv_bfloat162* m2 = reinterpret_cast<const __nv_bfloat162*>(&mk[j]);
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            float2 mf = __bfloat1622float2(m2[h]);
+                            if (!(mf.x > 0.f)) v[j * 8 + 2 * h] = 0.f;
+                            if (!(mf.y > 0.f)) v[j * 8 + 2 * h + 1] = 0.f;
+                        }
                     }
                 }
                 uint8_t* buf = ebuf + (nst & 1) * G2_EPI_BUF;
                 // the TMA store that last read this buffer (two sub-tiles ago) must be done
                 if (lane == 0 && nst >= 2) tma_store_wait_read<1>();
                 __syncwarp();
-                if (EPI == 2) {
+                if (EPI == 2 || EPI == 4 || EPI == 6) {
                     // fp32 32x32 sub-tile, 128-B rows, SWIZZLE_128B: chunk j ^ (row % 8)
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
-                            make_float4(v[4 * j] + rr[j].x, v[4 * j + 1] + rr[j].y, v[4 * j + 2] + rr[j].z,
-                                        v[4 * j + 3] + rr[j].w);
+                    for (int j = 0; j < 8; ++j) {
+                        float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                        if (EPI == 2) {
+                            o.x += rr[j].x;
+                            o.y += rr[j].y;
+                            o.z += rr[j].z;
+                            o.w += rr[j].w;
+                        }
+                        *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = o;
+                    }
                 } else {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
@@ -381,7 +447,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_2d(&tC, buf, n0 + c, m0 + q * 32);
+                    tma_store_2d(&tC, buf, n0 + c, mo + q * 32);
                     tma_store_commit();
                 }
             }
@@ -403,6 +469,90 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 
 static int g_num_sms = 0;
 
+template <int E, bool AM, bool BM>
+static int launch_2sm(cudaLaunchConfig_t& lc, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
+                      const __nv_bfloat16* b, const void* aux, int M, int N, int K, int k_splits) {
+    static bool attr = false;
+    if (!attr) {
+        RS_CUDA(cudaFuncSetAttribute(gemm_bf16_2sm_kernel<E, AM, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     G2_SMEM));
+        attr = true;
+    }
+    RS_CUDA(cudaLaunchKernelEx(&lc, gemm_bf16_2sm_kernel<E, AM, BM>, tA, tB, tC, b, aux, M, N, K, N, k_splits));
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
+// General CTA-pair GEMM: C = epi(op(A) . op(B)^T [+ bias]) with
+//   a_mn = 0: A stored [M, K] (K contiguous)   a_mn = 1: A stored [K, M] (M contiguous)
+//   b_mn = 0: W stored [N, K]                   b_mn = 1: W stored [K, N]
+// M, N multiples of 256, K a multiple of 64. epi 6 writes k_splits fp32 partial slices.
+int gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux, void* C, int M, int N, int K,
+                 int epi, int a_mn, int b_mn, int k_splits, cudaStream_t st) {
+    RS_CHECK_ARG(M > 0 && N > 0 && K > 0 && M % G2_BM == 0 && N % G2_BN == 0 && K % G2_BK == 0,
+                 "gemm_ex: need M, N %% 256 == 0 and K %% 64 == 0 (got %d %d %d)", M, N, K);
+    RS_CHECK_ARG(epi >= 0 && epi <= 6, "gemm_ex: bad epilogue %d", epi);
+
+    RS_CHECK_ARG((epi != 2 && epi != 5) || aux != nullptr, "gemm_ex: epilogue %d needs aux", epi);
+    RS_CHECK_ARG(k_splits >= 1 && (epi == 6 || k_splits == 1), "gemm_ex: split-K needs epilogue 6");
+    if (g_num_sms == 0) {
+        int dev;
+        RS_CUDA(cudaGetDevice(&dev));
+        RS_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    CUtensorMap tA, tB, tC;
+    if (a_mn)
+        RS_TRY(make_tmap_bf16(&tA, A, (uint64_t)K, (uint64_t)M, (uint64_t)M * 2, G2_BK, 64));
+    else
+        RS_TRY(make_tmap_bf16(&tA, A, (uint64_t)M, (uint64_t)K, (uint64_t)K * 2, G2_HALF, G2_BK));
+    if (b_mn)
+        RS_TRY(make_tmap_bf16(&tB, W, (uint64_t)K, (uint64_t)N, (uint64_t)N * 2, G2_BK, 64));
+    else
+        RS_TRY(make_tmap_bf16(&tB, W, (uint64_t)N, (uint64_t)K, (uint64_t)K * 2, G2_HALF, G2_BK));
+    const bool f32out = epi == 2 || epi == 4 || epi == 6;
+    const uint64_t crows = (uint64_t)M * (epi == 6 ? k_splits : 1);
+    if (f32out)
+        RS_TRY(make_tmap_2d(&tC, C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, crows, (uint64_t)N, (uint64_t)N * 4, 32, 32,
+                            CU_TENSOR_MAP_SWIZZLE_128B));
+    else
+        RS_TRY(make_tmap_2d(&tC, C, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, crows, (uint64_t)N, (uint64_t)N * 2, 32, 32,
+                            CU_TENSOR_MAP_SWIZZLE_64B));
+    const int n_work = (M / G2_BM) * (N / G2_BN) * k_splits;
+    int clusters = g_num_sms / 2;
+    if (n_work < clusters) clusters = n_work;
+    const __nv_bfloat16* b = static_cast<const __nv_bfloat16*>(bias);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(2 * clusters);
+    lc.blockDim = dim3(G_THREADS);
+    lc.dynamicSmemBytes = G2_SMEM;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    const int sel = epi * 4 + a_mn * 2 + b_mn;
+    switch (sel) {
+        case 0 * 4 + 0: return launch_2sm<0, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        case 1 * 4 + 0: return launch_2sm<1, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        case 2 * 4 + 0: return launch_2sm<2, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        case 3 * 4 + 0: return launch_2sm<3, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        // backward: dgrad (B MN-major) with bf16 / fp32 / ReLU-mask outputs, wgrad (both MN-major)
+        case 0 * 4 + 1: return launch_2sm<0, false, true>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        case 4 * 4 + 1: return launch_2sm<4, false, true>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        case 5 * 4 + 1: return launch_2sm<5, false, true>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        case 4 * 4 + 3: return launch_2sm<4, true, true>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        case 6 * 4 + 3: return launch_2sm<6, true, true>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        case 4 * 4 + 0: return launch_2sm<4, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        case 6 * 4 + 0: return launch_2sm<6, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        default:
+            set_error("gemm_ex: unsupported combination epi=%d a_mn=%d b_mn=%d", epi, a_mn, b_mn);
+            return RS_ERR_UNSUPPORTED;
+    }
+}
+
 int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, void* C, int M, int N, int K, int epi,
               cudaStream_t st) {
     RS_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty shape");
@@ -416,53 +566,8 @@ int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, voi
         RS_CUDA(cudaGetDevice(&dev));
         RS_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    if (M % G2_BM == 0 && N % G2_BN == 0) {
-        // CTA-pair kernel (the path the ranker takes: it pads M to 256)
-        CUtensorMap tA, tB, tC;
-        RS_TRY(make_tmap_bf16(&tA, A, (uint64_t)M, (uint64_t)K, (uint64_t)K * 2, G2_HALF, G2_BK));
-        RS_TRY(make_tmap_bf16(&tB, W, (uint64_t)N, (uint64_t)K, (uint64_t)K * 2, G2_HALF, G2_BK));
-        if (epi == 2)
-            RS_TRY(make_tmap_2d(&tC, C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)M, (uint64_t)N, (uint64_t)N * 4,
-                                32, 32, CU_TENSOR_MAP_SWIZZLE_128B));
-        else
-            RS_TRY(make_tmap_2d(&tC, C, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)M, (uint64_t)N, (uint64_t)N * 2,
-                                32, 32, CU_TENSOR_MAP_SWIZZLE_64B));
-        const int n_tiles = (M / G2_BM) * (N / G2_BN);
-        int clusters = g_num_sms / 2;
-        if (n_tiles < clusters) clusters = n_tiles;
-        const __nv_bfloat16* b = static_cast<const __nv_bfloat16*>(bias);
-        const float* r = static_cast<const float*>(R);
-        cudaLaunchConfig_t lc = {};
-        lc.gridDim = dim3(2 * clusters);
-        lc.blockDim = dim3(G_THREADS);
-        lc.dynamicSmemBytes = G2_SMEM;
-        lc.stream = st;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        lc.attrs = at;
-        lc.numAttrs = 1;
-#define RS_GEMM2_LAUNCH(E)                                                                                        \
-    do {                                                                                                          \
-        static bool attr = false;                                                                                 \
-        if (!attr) {                                                                                              \
-            RS_CUDA(cudaFuncSetAttribute(gemm_bf16_2sm_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, G2_SMEM)); \
-            attr = true;                                                                                          \
-        }                                                                                                         \
-        RS_CUDA(cudaLaunchKernelEx(&lc, gemm_bf16_2sm_kernel<E>, tA, tB, tC, b, r, M, N, K, N));                \
-    } while (0)
-        switch (epi) {
-            case 0: RS_GEMM2_LAUNCH(0); break;
-            case 1: RS_GEMM2_LAUNCH(1); break;
-            case 2: RS_GEMM2_LAUNCH(2); break;
-            default: RS_GEMM2_LAUNCH(3); break;
-        }
-#undef RS_GEMM2_LAUNCH
-        RS_LAUNCH_CHECK();
-        return RS_OK;
-    }
+    if (M % G2_BM == 0 && N % G2_BN == 0)  // CTA-pair kernel (the ranker pads M to 256)
+        return gemm_bf16_ex(A, W, bias, R, C, M, N, K, epi, 0, 0, 1, st);
     CUtensorMap tA, tB;
     RS_TRY(make_tmap_bf16(&tA, A, (uint64_t)M, (uint64_t)K, (uint64_t)K * 2, G_BM, G_BK));
     RS_TRY(make_tmap_bf16(&tB, W, (uint64_t)N, (uint64_t)K, (uint64_t)K * 2, G_BN, G_BK));
@@ -492,6 +597,12 @@ int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, voi
 }
 
 }  // namespace rs
+
+extern "C" int rs_gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux, void* C, int32_t M,
+                               int32_t N, int32_t K, int32_t epi, int32_t a_mn, int32_t b_mn, int32_t k_splits,
+                               void* stream) {
+    return rs::gemm_bf16_ex(A, W, bias, aux, C, M, N, K, epi, a_mn, b_mn, k_splits, rs::as_stream(stream));
+}
 
 extern "C" int rs_gemm_bf16(const void* A, const void* W, const void* bias, const void* R, void* C, int32_t M,
                             int32_t N, int32_t K, int32_t epi, void* stream) {

@@ -214,3 +214,10 @@ extern "C" int rs_listmle_lengths(const float* g, const int32_t* lengths, int32_
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
+
+namespace rs {
+int listmle_lengths_launch(const float* g, const int32_t* lengths, int n_lists, int L, int width, float* loss,
+                           float* dg, cudaStream_t st) {
+    return rs_listmle_lengths(g, lengths, n_lists, L, width, loss, dg, st);
+}
+}  // namespace rs

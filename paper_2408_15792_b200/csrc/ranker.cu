@@ -296,7 +296,7 @@ extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params
     cudaStream_t st = as_stream(stream);
     RS_TRY(check_cfg(cfg));
     RS_CHECK_ARG(B > 0 && S > 0 && S <= cfg->max_pos, "ranker: need B > 0 and 0 < S <= max_pos");
-    RS_CHECK_ARG(S <= 512, "ranker: S <= 512 (attention TMEM layout)");
+    RS_CHECK_ARG(S <= 2048, "ranker: S <= 2048");
     RS_CHECK_ARG(params && ids && g, "ranker: NULL pointer");
     if (ws_bytes < rs_ranker_workspace_size(cfg, B, S)) {
         set_error("ranker: workspace %zu < %zu", ws_bytes, rs_ranker_workspace_size(cfg, B, S));
@@ -337,3 +337,40 @@ extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params
     }
     return RS_OK;
 }
+
+// ---- building blocks shared with the training pass (ranker_train.cu) -----------------
+namespace rs {
+int ranker_embed(const int32_t* ids, const void* P, int64_t off_tok, int64_t off_pos, float* h, int n_tok, int S,
+                 int d, int vocab, int mp, cudaStream_t st) {
+    const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(P);
+    const int wpb = 8;
+    embed_kernel<<<(mp + wpb - 1) / wpb, 32 * wpb, 0, st>>>(ids, p + off_tok, p + off_pos, h, n_tok, S, d, vocab, mp);
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+int ranker_ln(const float* x, const void* w, const void* b, void* y, int rows, int d, cudaStream_t st) {
+    return launch_ln(x, static_cast<const __nv_bfloat16*>(w), static_cast<const __nv_bfloat16*>(b),
+                     static_cast<__nv_bfloat16*>(y), rows, d, st);
+}
+int ranker_head(const float* h, const int32_t* last, int B, int S, const void* P, const rs_ranker_config* cfg, float* g,
+                float* score, cudaStream_t st) {
+    const RankerOffsets o = ranker_offsets(*cfg);
+    return launch_head(h, last, B, S, static_cast<const __nv_bfloat16*>(P), o, cfg->d_model, g, score, st);
+}
+// which: 0 tok, 1 pos, 2 lnf_w, 3 lnf_b, 4 head_w, 5 head_b, then 6 + per-layer index
+int64_t ranker_offset(const rs_ranker_config* cfg, int which, int layer) {
+    const RankerOffsets o = ranker_offsets(*cfg);
+    switch (which) {
+        case 0: return o.tok;
+        case 1: return o.pos;
+        case 2: return o.lnf_w;
+        case 3: return o.lnf_b;
+        case 4: return o.head_w;
+        case 5: return o.head_b;
+        default: break;
+    }
+    const int64_t per[RS_RANKER_N_PER_LAYER] = {o.ln1_w, o.ln1_b, o.qkv_w, o.qkv_b, o.out_w, o.out_b,
+                                                o.ln2_w, o.ln2_b, o.fc1_w, o.fc1_b, o.fc2_w, o.fc2_b};
+    return o.per_layer0 + (int64_t)layer * o.layer_stride + per[which - 6];
+}
+}  // namespace rs

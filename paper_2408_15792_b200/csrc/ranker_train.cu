@@ -1,0 +1,219 @@
+// A10 / K7: one ListMLE gradient pass of the OPT-shape ranker over whole lists.
+//
+// Reference: train_ranking's minibatch body (predictors.py:379-385): order lists by
+// bucketed true length, forward, list_mle_loss/n, list_mle_gradient/n, backward, Adam.
+// Here a call accumulates the gradient of sum_lists (ListMLE(list)/list_len) into an fp32
+// buffer laid out like the bf16 parameters (rs_ranker_layout), micro-batching whole
+// lists (ListMLE couples a list's prompts); the caller all-reduces it across
+// data-parallel ranks (NCCL) and applies rs_adam_step with grad_scale = 1/total_lists.
+//
+// Per micro-batch: forward keeping the activations backward needs (fp32 residual stream
+// before each LayerNorm, bf16 LN outputs, qkv, attention output, FFN activations),
+// the score head, the fused ListMLE kernel (K6), then the backward:
+//   head + final LN -> per layer, in reverse:
+//   FC2  (wgrad dW2 = dh^T f, bias sum, dgrad df = (dh W2) * relu'(f))
+//   FC1  (wgrad dW1 = df^T x2, bias sum, dgrad dx = df W1) -> LN2 backward into dh
+//   out  (wgrad dWo = dh^T a, bias sum, dgrad da = dh Wo) -> attention backward -> dqkv
+//   QKV  (wgrad dWqkv = dqkv^T x1, bias sum, dgrad dx = dqkv Wqkv) -> LN1 backward into dh
+//   -> token / position embedding scatter-add.
+// dgrad GEMMs read the weights MN-major, wgrad GEMMs read both activations MN-major
+// (split-K partial slices reduced in a fixed order), so the pass is deterministic.
+#include <cuda_bf16.h>
+#include "common.cuh"
+#include "gemm.cuh"
+#include "train.cuh"
+
+namespace rs {
+int attention_fwd(const void* qkv, void* out, int B, int S, int H, cudaStream_t st);
+int ranker_embed(const int32_t* ids, const void* P, int64_t off_tok, int64_t off_pos, float* h, int n_tok, int S,
+                 int d, int vocab, int mp, cudaStream_t st);
+int ranker_ln(const float* x, const void* w, const void* b, void* y, int rows, int d, cudaStream_t st);
+int ranker_head(const float* h, const int32_t* last, int B, int S, const void* P, const rs_ranker_config* cfg, float* g,
+                float* score, cudaStream_t st);
+int64_t ranker_offset(const rs_ranker_config* cfg, int which, int layer);
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = __float2bfloat16_rn(x[i]);
+}
+
+enum { OFF_TOK = 0, OFF_POS, OFF_LNF_W, OFF_LNF_B, OFF_HEAD_W, OFF_HEAD_B,
+       OFF_LN1_W = 6, OFF_LN1_B, OFF_QKV_W, OFF_QKV_B, OFF_OUT_W, OFF_OUT_B, OFF_LN2_W, OFF_LN2_B, OFF_FC1_W,
+       OFF_FC1_B, OFF_FC2_W, OFF_FC2_B };
+
+struct TrainWs {
+    // saved activations, per layer (host-side pointer tables into the workspace)
+    float* h_in[64];  // L + 1 entries (h_in[L] = final residual stream)
+    float* h_mid[64];
+    __nv_bfloat16 *x1[64], *qkv[64], *att[64], *x2[64], *f[64];
+    // backward scratch
+    float *dh, *dx, *wpart, *rpart, *g, *dg;
+    __nv_bfloat16 *dh16, *da, *dqkv, *df;
+    void* ews;
+    size_t ews_bytes;
+};
+
+static int wgrad_splits(int M, int N, int K) {
+    const int tiles = (M / 256) * (N / 256);
+    int s = (148 + tiles - 1) / tiles;
+    const int kb = K / 64;
+    if (s > kb / 8) s = kb / 8;
+    if (s > 64) s = 64;
+    return s < 1 ? 1 : s;
+}
+
+template <typename A>
+static void train_layout(A& a, const rs_ranker_config& c, int64_t Tp, int P, TrainWs* w) {
+    const int L = c.n_layers;
+    const int64_t d = c.d_model, F = c.d_ffn;
+    TrainWs t{};
+    for (int l = 0; l <= L; ++l) t.h_in[l] = a.template take<float>(Tp * d);
+    for (int l = 0; l < L; ++l) {
+        t.h_mid[l] = a.template take<float>(Tp * d);
+        t.x1[l] = a.template take<__nv_bfloat16>(Tp * d);
+        t.qkv[l] = a.template take<__nv_bfloat16>(Tp * 3 * d);
+        t.att[l] = a.template take<__nv_bfloat16>(Tp * d);
+        t.x2[l] = a.template take<__nv_bfloat16>(Tp * d);
+        t.f[l] = a.template take<__nv_bfloat16>(Tp * F);
+    }
+    const int64_t wmax = (F * d > 3 * d * d ? F * d : 3 * d * d);
+    t.dh = a.template take<float>(Tp * d);
+    t.dx = a.template take<float>(Tp * d);
+    t.wpart = a.template take<float>((int64_t)64 * wmax);
+    const int64_t nrb = (Tp + 63) / 64 + 1;
+    t.rpart = a.template take<float>(nrb * 2 * (F > 3 * d ? F : 3 * d) + (int64_t)(P + 1) * (3 * d + 1));
+    t.g = a.template take<float>(P);
+    t.dg = a.template take<float>(P);
+    t.dh16 = a.template take<__nv_bfloat16>(Tp * d);
+    t.da = a.template take<__nv_bfloat16>(Tp * d);
+    t.dqkv = a.template take<__nv_bfloat16>(Tp * 3 * d);
+    t.df = a.template take<__nv_bfloat16>(Tp * F);
+    t.ews_bytes = embed_backward_ws((int)Tp);
+    t.ews = a.template take<uint8_t>(t.ews_bytes);
+    if (w) *w = t;
+}
+struct TrSizer {
+    ArenaSizer s;
+    template <typename T>
+    T* take(size_t n) { s.take<T>(n); return nullptr; }
+};
+
+int listmle_lengths_launch(const float* g, const int32_t* lengths, int n_lists, int L, int width, float* loss,
+                           float* dg, cudaStream_t st);
+
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" size_t rs_ranker_grad_workspace_size(const rs_ranker_config* cfg, int32_t lists_per_micro, int32_t list_len,
+                                                int32_t S) {
+    if (!cfg || lists_per_micro <= 0 || list_len <= 0 || S <= 0 || cfg->n_layers > 63) return 0;
+    const int P = lists_per_micro * list_len;
+    const int64_t Tp = ((int64_t)P * S + 255) / 256 * 256;
+    TrSizer s;
+    train_layout(s, *cfg, Tp, P, nullptr);
+    return s.s.used + 4096;
+}
+
+extern "C" int rs_ranker_grad(const rs_ranker_config* cfg, const void* params, float* grad, const int32_t* ids,
+                              const int32_t* lengths, int32_t n_lists, int32_t list_len, int32_t S,
+                              int32_t bucket_width, int32_t lists_per_micro, float* loss_out, void* ws,
+                              size_t ws_bytes, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    RS_CHECK_ARG(cfg && params && grad && ids && lengths && loss_out, "rs_ranker_grad: NULL argument");
+    RS_CHECK_ARG(n_lists > 0 && list_len >= 1 && S >= 1 && S <= 128, "rs_ranker_grad: need S <= 128 (got %d)", S);
+    RS_CHECK_ARG(bucket_width >= 1, "bucket_width must be >= 1");
+    RS_CHECK_ARG(lists_per_micro >= 1, "lists_per_micro must be >= 1");
+    RS_CHECK_ARG(cfg->n_layers <= 63 && cfg->d_model == cfg->n_heads * 64, "rs_ranker_grad: bad config");
+    if (ws_bytes < rs_ranker_grad_workspace_size(cfg, lists_per_micro, list_len, S)) {
+        set_error("rs_ranker_grad: workspace too small");
+        return RS_ERR_WORKSPACE;
+    }
+    const int L = cfg->n_layers, d = cfg->d_model, F = cfg->d_ffn, H = cfg->n_heads;
+    const __nv_bfloat16* P16 = static_cast<const __nv_bfloat16*>(params);
+    auto off = [&](int which, int layer) { return ranker_offset(cfg, which, layer); };
+    for (int l0 = 0; l0 < n_lists; l0 += lists_per_micro) {
+        const int ml = (n_lists - l0) < lists_per_micro ? (n_lists - l0) : lists_per_micro;
+        const int P = ml * list_len;
+        const int n_tok = P * S;
+        const int64_t Tp = ((int64_t)n_tok + 255) / 256 * 256;
+        Arena ar(ws, ws_bytes);
+        TrainWs w;
+        {
+            const int Pm = lists_per_micro * list_len;
+            const int64_t Tm = ((int64_t)Pm * S + 255) / 256 * 256;
+            train_layout(ar, *cfg, Tm, Pm, &w);
+        }
+        const int32_t* mids = ids + (int64_t)l0 * list_len * S;
+        const int32_t* mlen = lengths + (int64_t)l0 * list_len;
+        // ---- forward, keeping activations ----
+        RS_TRY(ranker_embed(mids, P16, off(OFF_TOK, 0), off(OFF_POS, 0), w.h_in[0], n_tok, S, d, cfg->vocab, (int)Tp,
+                            st));
+        if (Tp > n_tok) {
+            for (int l = 0; l < L; ++l)
+                RS_CUDA(cudaMemsetAsync(w.att[l] + (size_t)n_tok * d, 0, (size_t)(Tp - n_tok) * d * 2, st));
+        }
+        for (int l = 0; l < L; ++l) {
+            RS_TRY(ranker_ln(w.h_in[l], P16 + off(OFF_LN1_W, l), P16 + off(OFF_LN1_B, l), w.x1[l], (int)Tp, d, st));
+            RS_TRY(gemm_bf16(w.x1[l], P16 + off(OFF_QKV_W, l), P16 + off(OFF_QKV_B, l), nullptr, w.qkv[l], (int)Tp,
+                             3 * d, d, 0, st));
+            RS_TRY(attention_fwd(w.qkv[l], w.att[l], P, S, H, st));
+            RS_TRY(gemm_bf16(w.att[l], P16 + off(OFF_OUT_W, l), P16 + off(OFF_OUT_B, l), w.h_in[l], w.h_mid[l],
+                             (int)Tp, d, d, 2, st));
+            RS_TRY(ranker_ln(w.h_mid[l], P16 + off(OFF_LN2_W, l), P16 + off(OFF_LN2_B, l), w.x2[l], (int)Tp, d, st));
+            RS_TRY(gemm_bf16(w.x2[l], P16 + off(OFF_FC1_W, l), P16 + off(OFF_FC1_B, l), nullptr, w.f[l], (int)Tp, F, d,
+                             cfg->activation == 0 ? 1 : 3, st));
+            RS_TRY(gemm_bf16(w.f[l], P16 + off(OFF_FC2_W, l), P16 + off(OFF_FC2_B, l), w.h_mid[l], w.h_in[l + 1],
+                             (int)Tp, d, F, 2, st));
+        }
+        RS_TRY(ranker_head(w.h_in[L], nullptr, P, S, P16, cfg, w.g, nullptr, st));
+        // ---- ListMLE (K6): per-list loss / n and dg = grad / n ----
+        RS_TRY(listmle_lengths_launch(w.g, mlen, ml, list_len, bucket_width, loss_out + l0, w.dg, st));
+        // ---- backward ----
+        RS_CUDA(cudaMemsetAsync(w.dh, 0, (size_t)Tp * d * sizeof(float), st));
+        // padding rows take part in the wgrad reductions: keep their gradients zero
+        if (Tp > n_tok)
+            RS_CUDA(cudaMemsetAsync(w.dqkv + (size_t)n_tok * 3 * d, 0, (size_t)(Tp - n_tok) * 3 * d * 2, st));
+        RS_TRY(head_backward(w.h_in[L], nullptr, P, S, P16 + off(OFF_LNF_W, 0), P16 + off(OFF_LNF_B, 0),
+                             P16 + off(OFF_HEAD_W, 0), w.dg, w.dh, w.rpart, d, grad + off(OFF_HEAD_W, 0),
+                             grad + off(OFF_LNF_W, 0), grad + off(OFF_HEAD_B, 0), st));
+        f32_to_bf16_kernel<<<1184, 256, 0, st>>>(w.dh, w.dh16, (int64_t)Tp * d);
+        RS_LAUNCH_CHECK();
+        const int T = (int)Tp;
+        for (int l = L - 1; l >= 0; --l) {
+            int sp;
+            // FC2: h_out = h_mid + f W2^T + b2
+            sp = wgrad_splits(d, F, T);
+            RS_TRY(gemm_bf16_ex(w.dh16, w.f[l], nullptr, nullptr, w.wpart, d, F, T, 6, 1, 1, sp, st));
+            RS_TRY(slices_add(w.wpart, sp, (int64_t)d * F, grad + off(OFF_FC2_W, l), st));
+            RS_TRY(colsum_add(w.dh, false, n_tok, d, w.rpart, grad + off(OFF_FC2_B, l), st));
+            RS_TRY(gemm_bf16_ex(w.dh16, P16 + off(OFF_FC2_W, l), nullptr, w.f[l], w.df, T, F, d, 5, 0, 1, 1, st));
+            // FC1: f = relu(x2 W1^T + b1)
+            sp = wgrad_splits(F, d, T);
+            RS_TRY(gemm_bf16_ex(w.df, w.x2[l], nullptr, nullptr, w.wpart, F, d, T, 6, 1, 1, sp, st));
+            RS_TRY(slices_add(w.wpart, sp, (int64_t)F * d, grad + off(OFF_FC1_W, l), st));
+            RS_TRY(colsum_add(w.df, true, n_tok, F, w.rpart, grad + off(OFF_FC1_B, l), st));
+            RS_TRY(gemm_bf16_ex(w.df, P16 + off(OFF_FC1_W, l), nullptr, nullptr, w.dx, T, d, F, 4, 0, 1, 1, st));
+            RS_TRY(ln_backward(w.dx, w.h_mid[l], P16 + off(OFF_LN2_W, l), w.dh, w.dh16, w.rpart, n_tok, d,
+                               grad + off(OFF_LN2_W, l), nullptr, st));
+            // out-proj: h_mid = h_in + a Wo^T + bo
+            sp = wgrad_splits(d, d, T);
+            RS_TRY(gemm_bf16_ex(w.dh16, w.att[l], nullptr, nullptr, w.wpart, d, d, T, 6, 1, 1, sp, st));
+            RS_TRY(slices_add(w.wpart, sp, (int64_t)d * d, grad + off(OFF_OUT_W, l), st));
+            RS_TRY(colsum_add(w.dh, false, n_tok, d, w.rpart, grad + off(OFF_OUT_B, l), st));
+            RS_TRY(gemm_bf16_ex(w.dh16, P16 + off(OFF_OUT_W, l), nullptr, nullptr, w.da, T, d, d, 0, 0, 1, 1, st));
+            RS_TRY(attention_bwd(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, st));
+            // QKV: qkv = x1 Wqkv^T + b
+            sp = wgrad_splits(3 * d, d, T);
+            RS_TRY(gemm_bf16_ex(w.dqkv, w.x1[l], nullptr, nullptr, w.wpart, 3 * d, d, T, 6, 1, 1, sp, st));
+            RS_TRY(slices_add(w.wpart, sp, (int64_t)3 * d * d, grad + off(OFF_QKV_W, l), st));
+            RS_TRY(colsum_add(w.dqkv, true, n_tok, 3 * d, w.rpart, grad + off(OFF_QKV_B, l), st));
+            RS_TRY(gemm_bf16_ex(w.dqkv, P16 + off(OFF_QKV_W, l), nullptr, nullptr, w.dx, T, d, 3 * d, 4, 0, 1, 1, st));
+            RS_TRY(ln_backward(w.dx, w.h_in[l], P16 + off(OFF_LN1_W, l), w.dh, w.dh16, w.rpart, n_tok, d,
+                               grad + off(OFF_LN1_W, l), nullptr, st));
+        }
+        RS_TRY(embed_backward(mids, P, S, cfg->vocab, w.dh, d, grad + off(OFF_TOK, 0), grad + off(OFF_POS, 0), w.ews,
+                              w.ews_bytes, st));
+    }
+    return RS_OK;
+}

@@ -1,0 +1,80 @@
+"""ListMLE training of the OPT-shape ranker on B200s (A10/A11 of SURVEY §8a).
+
+Reference: train_ranking (predictors.py:347-406): per minibatch list, order by bucketed
+true length (stable), forward, list_mle_loss / n, list_mle_gradient / n, backward, Adam
+(predictors.py:209-225). Here one optimizer step consumes many whole lists: each rank
+accumulates the gradient of its lists with rs_ranker_grad (forward + fused ListMLE +
+tcgen05 backward), the gradients are summed across data-parallel ranks with one NCCL
+all-reduce of the flat fp32 buffer, and every rank applies the same fused Adam
+(rs_adam_step, grad_scale = 1 / global lists) to its fp32 master copy. With one list
+per step and one rank this is the reference's update sequence.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .ranker import OptRanker
+
+
+class RankerTrainer:
+    def __init__(self, model: OptRanker, lr: float = 2e-5, betas=(0.9, 0.999), eps: float = 1e-8,
+                 bucket_width: int = 10, lists_per_micro: int = 16, group=None):
+        if bucket_width < 1:
+            raise ValueError("bucket_width must be >= 1")
+        self.model = model
+        self.lr, self.betas, self.eps = float(lr), (float(betas[0]), float(betas[1])), float(eps)
+        self.bucket_width = int(bucket_width)
+        self.lists_per_micro = int(lists_per_micro)
+        self.group = group
+        dev = model.dev
+        self.master = model.flat.float()
+        self.m = torch.zeros_like(self.master)
+        self.v = torch.zeros_like(self.master)
+        self.grad = torch.zeros_like(self.master)
+        self.t = 0
+
+    def _world(self) -> int:
+        return dist.get_world_size(self.group) if dist.is_available() and dist.is_initialized() else 1
+
+    def accumulate(self, ids: torch.Tensor, lengths: torch.Tensor, list_len: int) -> torch.Tensor:
+        """Add the gradient of sum_lists ListMLE/list_len for this rank's lists to .grad;
+        returns the per-list losses (device tensor)."""
+        n_prompts, S = ids.shape
+        if n_prompts % list_len:
+            raise ValueError("ids rows must be whole lists")
+        n_lists = n_prompts // list_len
+        dev = self.model.dev
+        ids = ids.to(dev, torch.int32).contiguous()
+        lengths = lengths.to(dev, torch.int32).contiguous().view(-1)
+        loss = torch.empty(n_lists, dtype=torch.float32, device=dev)
+        lib = _lib.load()
+        c = self.model.cfg.c()
+        mb = min(self.lists_per_micro, n_lists)
+        need = lib.rs_ranker_grad_workspace_size(ctypes.byref(c), mb, list_len, S)
+        ws, wn = _lib.workspace.get(need, dev)
+        _lib.check(lib.rs_ranker_grad(ctypes.byref(c), self.model.flat.data_ptr(), self.grad.data_ptr(),
+                                      ids.data_ptr(), lengths.data_ptr(), n_lists, list_len, S, self.bucket_width,
+                                      mb, loss.data_ptr(), ws, wn, _lib.stream_handle(dev)), "rs_ranker_grad")
+        return loss
+
+    def apply(self, total_lists: int) -> None:
+        """All-reduce the accumulated gradient across ranks (NCCL) and take one Adam step."""
+        if self._world() > 1:
+            dist.all_reduce(self.grad, op=dist.ReduceOp.SUM, group=self.group)
+        self.t += 1
+        _lib.check(_lib.load().rs_adam_step(self.master.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
+                                            self.grad.data_ptr(), self.model.flat.data_ptr(), self.master.numel(),
+                                            self.lr, self.betas[0], self.betas[1], self.eps, self.t,
+                                            1.0 / float(total_lists), _lib.stream_handle(self.model.dev)),
+                   "rs_adam_step")
+
+    def step(self, ids: torch.Tensor, lengths: torch.Tensor, list_len: int, total_lists: int | None = None):
+        loss = self.accumulate(ids, lengths, list_len)
+        n_lists = ids.shape[0] // list_len
+        self.apply(total_lists if total_lists is not None else n_lists * self._world())
+        return loss

@@ -1,0 +1,29 @@
+"""Attention backward (S <= 128) vs torch autograd in fp32."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("B,S,H", [(1, 128, 1), (3, 64, 12), (2, 100, 4), (5, 128, 12)])
+def test_attention_bwd_matches_autograd(B, S, H):
+    from paper_2408_15792_b200 import _lib
+    _lib.device()
+    g = torch.Generator(device="cuda").manual_seed(B * S + H)
+    qkv = (torch.randn(B * S, 3 * H * 64, device="cuda", generator=g)).bfloat16()
+    dout = torch.randn(B * S, H * 64, device="cuda", generator=g).bfloat16()
+    att = torch.empty(B * S, H * 64, dtype=torch.bfloat16, device="cuda")
+    lib = _lib.load()
+    _lib.check(lib.rs_attention_fwd(qkv.data_ptr(), att.data_ptr(), B, S, H, _lib.stream_handle()))
+    dqkv = torch.full((B * S, 3 * H * 64), float("nan"), dtype=torch.bfloat16, device="cuda")
+    _lib.check(lib.rs_attention_bwd(qkv.data_ptr(), att.data_ptr(), dout.data_ptr(), dqkv.data_ptr(), B, S, H,
+                                    _lib.stream_handle()))
+    x = qkv.float().requires_grad_(True)
+    q, k, v = x.view(B, S, 3, H, 64).permute(2, 0, 3, 1, 4)
+    o = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+    o.permute(0, 2, 1, 3).reshape(B * S, H * 64).backward(dout.float())
+    ref = x.grad
+    err = (dqkv.float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    assert err <= 3e-2 * max(1.0, scale), (err, scale)

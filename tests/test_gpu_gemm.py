@@ -63,3 +63,43 @@ def test_gemm_residual_in_place():
     _lib.check(_lib.load().rs_gemm_bf16(A.data_ptr(), W.data_ptr(), b.data_ptr(), h.data_ptr(), h.data_ptr(),
                                         256, 768, 768, 2, _lib.stream_handle()))
     assert (h - want).abs().max().item() < 1e-3
+
+
+def _gemm_ex(A, W, aux, M, N, K, epi, a_mn, b_mn, splits=1, bias=None, out_dtype=torch.float32):
+    from paper_2408_15792_b200 import _lib
+    _lib.device()
+    rows = M * (splits if epi == 6 else 1)
+    C = torch.empty(rows, N, dtype=out_dtype, device="cuda")
+    _lib.check(_lib.load().rs_gemm_bf16_ex(A.data_ptr(), W.data_ptr(), None if bias is None else bias.data_ptr(),
+                                           None if aux is None else aux.data_ptr(), C.data_ptr(), M, N, K, epi,
+                                           a_mn, b_mn, splits, _lib.stream_handle()))
+    return C
+
+
+@pytest.mark.parametrize("T,Nf,Kin", [(512, 768, 3072), (1024, 3072, 768), (256, 2304, 768), (768, 768, 768)])
+def test_dgrad_matches_fp32(T, Nf, Kin):
+    """dX[T, Kin] = dY[T, Nf] . W[Nf, Kin] with W read MN-major (the backward data GEMM)."""
+    g = torch.Generator(device="cuda").manual_seed(T + Nf)
+    dY = torch.randn(T, Nf, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(Nf, Kin, device="cuda", generator=g) * 0.05).bfloat16()
+    ref = dY.float() @ W.float()
+    C = _gemm_ex(dY, W, None, T, Kin, Nf, 4, 0, 1)
+    assert (C - ref).abs().max().item() <= 2e-2 * max(1.0, ref.abs().max().item())
+    mask = torch.randn(T, Kin, device="cuda", generator=g).bfloat16()
+    Cm = _gemm_ex(dY, W, mask, T, Kin, Nf, 5, 0, 1, out_dtype=torch.bfloat16).float()
+    refm = ref * (mask.float() > 0)
+    assert (Cm - refm).abs().max().item() <= 2e-2 * max(1.0, ref.abs().max().item())
+
+
+@pytest.mark.parametrize("T,Nf,Kin,splits", [(4096, 768, 3072, 1), (8192, 3072, 768, 4), (2048, 768, 768, 8),
+                                             (1024, 2304, 768, 3)])
+def test_wgrad_matches_fp32(T, Nf, Kin, splits):
+    """dW[Nf, Kin] = dY^T X over T tokens: both operands MN-major; split-K partial slices."""
+    g = torch.Generator(device="cuda").manual_seed(T + Kin)
+    dY = torch.randn(T, Nf, device="cuda", generator=g).bfloat16()
+    X = torch.randn(T, Kin, device="cuda", generator=g).bfloat16()
+    ref = dY.float().t() @ X.float()
+    epi = 6 if splits > 1 else 4
+    C = _gemm_ex(dY, X, None, Nf, Kin, T, epi, 1, 1, splits)
+    got = C.view(splits, Nf, Kin).sum(0) if splits > 1 else C
+    assert (got - ref).abs().max().item() <= 1e-2 * max(1.0, ref.abs().max().item())
