@@ -35,9 +35,23 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    while (!mbar_try_wait(bar, parity)) {
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// Watchdog: a pipeline that deadlocks (a protocol bug) traps after ~10 s instead of
+// hanging the GPU; the host then sees cudaErrorLaunchFailure. The timer is read only
+// every 4096 failed polls, so the steady-state cost is one counter increment.
+static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
+    const uint64_t t0 = globaltimer_ns();
+    for (uint32_t k = 1;; ++k) {
+        if (mbar_try_wait(bar, parity)) return;
+        if ((k & 4095u) == 0 && globaltimer_ns() - t0 > 10000000000ull) __trap();
     }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    if (!mbar_try_wait(bar, parity)) mbar_wait_slow(bar, parity);
 }
 
 // ---- TMA ------------------------------------------------------------------------
