@@ -360,7 +360,7 @@ def run_ours(args):
     if rank != 0:
         dist.destroy_process_group()
         return 0
-    flops = cfg.flops_per_prompt(S)
+    flops = cfg.flops_per_prompt_pruned(S)  # what the forward computes (last layer pruned)
     model_tflops = value * flops / 1e12 / world
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -376,7 +376,8 @@ def run_ours(args):
                 "d2h_bytes_per_step": sched.max_batch * 8 + 16, "ms_per_step": e2e_ms},
         "gpu_launches": launches,
         "clocks": clk.summary(),
-        "model_flops": {"per_prompt": flops, "tflops_per_gpu": model_tflops,
+        "model_flops": {"per_prompt": flops, "per_prompt_unpruned": cfg.flops_per_prompt(S),
+                        "tflops_per_gpu": model_tflops,
                         "frac_of_sustained": model_tflops / pk["bf16_tflops_sustained"],
                         "frac_of_burst": model_tflops / pk["bf16_tflops"]},
         "peaks": {k: pk.get(k) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained", "source")},

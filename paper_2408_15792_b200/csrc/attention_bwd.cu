@@ -182,7 +182,9 @@ __global__ void __launch_bounds__(AB_THREADS, 1)
         if (lane == 0) mbar_arrive(&bar->p_full);
         mbar_wait(&bar->g_full, 0);
         tc_fence_after();
-        if (row_ok) {
+        // tcgen05.ld is .sync.aligned: every lane of the warp issues it, rows past S only
+        // skip the store (a partial warp here deadlocks when S % 32 != 0)
+        {
             __nv_bfloat16* base = dqkv + (size_t)(row0 + r) * 3 * dm + h * AB_D;
             const uint32_t src[3] = {tdQ, tdK, tdV};
 #pragma unroll
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(AB_THREADS, 1)
                 tmem_ld_32x32b_x32(src[which] + la, a0);
                 tmem_ld_32x32b_x32(src[which] + la + 32, a1);
                 tmem_ld_wait();
+                if (!row_ok) continue;
                 uint4* o4 = reinterpret_cast<uint4*>(base + which * dm);
 #pragma unroll
                 for (int qq = 0; qq < 4; ++qq) {
@@ -204,8 +207,6 @@ __global__ void __launch_bounds__(AB_THREADS, 1)
                                             pack_bf16(__uint_as_float(a1[8 * qq + 6]), __uint_as_float(a1[8 * qq + 7])));
                 }
             }
-        } else {
-            tmem_ld_wait();
         }
     }
     tc_fence_before();

@@ -143,6 +143,107 @@ __global__ void head_kernel(const float* __restrict__ h, const int32_t* __restri
     }
 }
 
+// Last layer, pruned to the one query that reaches the score head: for every prompt b
+// and head, o = softmax(q_last k_j^T / 8, j <= last) v over the prompt's keys, with
+// q_last the query of token last[b] (causal attention restricted to that row is exact).
+// One warp per (prompt, head); scores staged in shared memory. The warp also gathers
+// its 64-column slice of the residual row h[b*S + last] into h_last[b] (fp32), so the
+// rest of the last layer (out-proj, LN2, FFN) and the head run on B rows instead of B*S.
+constexpr int AL_WARPS = 4;
+__global__ void __launch_bounds__(32 * AL_WARPS)
+    attention_last_kernel(const __nv_bfloat16* __restrict__ qkv, const float* __restrict__ h,
+                          const int32_t* __restrict__ last, __nv_bfloat16* __restrict__ att_last,
+                          float* __restrict__ h_last, int B, int Bp, int S, int H) {
+    extern __shared__ float al_s[];  // [AL_WARPS][S]
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gw = blockIdx.x * AL_WARPS + wib;
+    if (gw >= Bp * H) return;
+    const int b = gw / H, hh = gw % H;
+    const int d = H * 64;
+    __nv_bfloat162* orow = reinterpret_cast<__nv_bfloat162*>(att_last + (size_t)b * d + hh * 64) + lane;
+    float2* hrow = reinterpret_cast<float2*>(h_last + (size_t)b * d + hh * 64) + lane;
+    if (b >= B) {  // padding rows of the pruned GEMMs
+        *orow = __floats2bfloat162_rn(0.f, 0.f);
+        *hrow = make_float2(0.f, 0.f);
+        return;
+    }
+    int lp = last ? last[b] : S - 1;
+    lp = lp < 0 ? 0 : (lp >= S ? S - 1 : lp);
+    const size_t ld = (size_t)3 * d;
+    const __nv_bfloat16* base = qkv + (size_t)b * S * ld + hh * 64;
+    *hrow = reinterpret_cast<const float2*>(h + ((size_t)b * S + lp) * d + hh * 64)[lane];
+    float q[64];
+    {
+        const uint4* q4 = reinterpret_cast<const uint4*>(base + (size_t)lp * ld);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint4 u = q4[k];
+            const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float2 f = __bfloat1622float2(u2[e]);
+                q[k * 8 + 2 * e] = f.x * 0.125f;  // 1/sqrt(64)
+                q[k * 8 + 2 * e + 1] = f.y * 0.125f;
+            }
+        }
+    }
+    float* sc = al_s + wib * S;
+    float m = -INFINITY;
+    for (int j = lane; j <= lp; j += 32) {
+        const uint4* k4 = reinterpret_cast<const uint4*>(base + (size_t)j * ld + d);
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint4 u = k4[k];
+            const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                float2 f = __bfloat1622float2(u2[e]);
+                acc = fmaf(q[k * 8 + 2 * e], f.x, acc);
+                acc = fmaf(q[k * 8 + 2 * e + 1], f.y, acc);
+            }
+        }
+        sc[j] = acc;
+        m = fmaxf(m, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float l = 0.f;
+    for (int j = lane; j <= lp; j += 32) {
+        const float p = __expf(sc[j] - m);
+        sc[j] = p;
+        l += p;
+    }
+    l = warp_sum(l);
+    __syncwarp();
+    float2 o = make_float2(0.f, 0.f);
+    const __nv_bfloat162* vcol = reinterpret_cast<const __nv_bfloat162*>(base + 2 * d) + lane;
+    for (int j = 0; j <= lp; ++j) {
+        const float2 v = __bfloat1622float2(vcol[(size_t)j * (ld / 2)]);
+        const float p = sc[j];
+        o.x = fmaf(p, v.x, o.x);
+        o.y = fmaf(p, v.y, o.y);
+    }
+    const float inv = 1.f / l;
+    *orow = __floats2bfloat162_rn(o.x * inv, o.y * inv);
+}
+
+static int launch_attention_last(const __nv_bfloat16* qkv, const float* h, const int32_t* last,
+                                 __nv_bfloat16* att_last, float* h_last, int B, int Bp, int S, int H,
+                                 cudaStream_t st) {
+    const size_t smem = (size_t)AL_WARPS * S * sizeof(float);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        RS_CUDA(cudaFuncSetAttribute(attention_last_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = smem;
+    }
+    const int warps = Bp * H;
+    attention_last_kernel<<<(warps + AL_WARPS - 1) / AL_WARPS, 32 * AL_WARPS, smem, st>>>(qkv, h, last, att_last,
+                                                                                       h_last, B, Bp, S, H);
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
 struct RankerOffsets {
     int64_t tok, pos, lnf_w, lnf_b, head_w, head_b;
     int64_t per_layer0, layer_stride;
@@ -209,15 +310,23 @@ static int64_t chunk_prompts(int32_t B, int32_t S) {
 struct RankerWs {
     float* h;
     __nv_bfloat16 *x, *qkv, *att, *ffn;
+    // last layer, pruned to one row per prompt (bp rows)
+    float* h_last;
+    __nv_bfloat16 *a_last, *x_last, *f_last;
 };
 template <typename A>
-static void ranker_ws_layout(A& a, const rs_ranker_config& c, int64_t mp, RankerWs* w) {
-    auto h = a.template take<float>(mp * c.d_model);
-    auto x = a.template take<__nv_bfloat16>(mp * c.d_model);
-    auto q = a.template take<__nv_bfloat16>(mp * 3 * c.d_model);
-    auto t = a.template take<__nv_bfloat16>(mp * c.d_model);
-    auto f = a.template take<__nv_bfloat16>(mp * c.d_ffn);
-    if (w) *w = RankerWs{h, x, q, t, f};
+static void ranker_ws_layout(A& a, const rs_ranker_config& c, int64_t mp, int64_t bp, RankerWs* w) {
+    RankerWs r;
+    r.h = a.template take<float>(mp * c.d_model);
+    r.x = a.template take<__nv_bfloat16>(mp * c.d_model);
+    r.qkv = a.template take<__nv_bfloat16>(mp * 3 * c.d_model);
+    r.att = a.template take<__nv_bfloat16>(mp * c.d_model);
+    r.ffn = a.template take<__nv_bfloat16>(mp * c.d_ffn);
+    r.h_last = a.template take<float>(bp * c.d_model);
+    r.a_last = a.template take<__nv_bfloat16>(bp * c.d_model);
+    r.x_last = a.template take<__nv_bfloat16>(bp * c.d_model);
+    r.f_last = a.template take<__nv_bfloat16>(bp * c.d_ffn);
+    if (w) *w = r;
 }
 struct RkSizer {
     ArenaSizer s;
@@ -285,8 +394,9 @@ extern "C" size_t rs_ranker_workspace_size(const rs_ranker_config* cfg, int32_t 
     if (check_cfg(cfg) != RS_OK || B <= 0 || S <= 0) return 0;
     const int64_t bc = chunk_prompts(B, S);
     const int64_t mp = (bc * S + 255) / 256 * 256;  // CTA-pair GEMM tiles are 256 rows
+    const int64_t bp = (bc + 255) / 256 * 256;
     RkSizer s;
-    ranker_ws_layout(s, *cfg, mp, nullptr);
+    ranker_ws_layout(s, *cfg, mp, bp, nullptr);
     return s.s.used + 256;
 }
 
@@ -310,9 +420,10 @@ extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params
         const int bc = (int)((B - b0) < bc_max ? (B - b0) : bc_max);
         const int n_tok = bc * S;
         const int mp = (n_tok + 255) / 256 * 256;
+        const int bp = (bc + 255) / 256 * 256;
         Arena ar(ws, ws_bytes);
         RankerWs w;
-        ranker_ws_layout(ar, *cfg, mp, &w);
+        ranker_ws_layout(ar, *cfg, mp, bp, &w);
         {
             const int wpb = 8;
             embed_kernel<<<(mp + wpb - 1) / wpb, 32 * wpb, 0, st>>>(ids + b0 * S, P + o.tok, P + o.pos, w.h, n_tok, S,
@@ -322,18 +433,29 @@ extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params
         // Rows past the last token are never written by attention but feed the
         // out-projection (and, as masked keys, the PV MMA: 0 * NaN = NaN), so zero them.
         if (mp > n_tok) RS_CUDA(cudaMemsetAsync(w.att + (size_t)n_tok * d, 0, (size_t)(mp - n_tok) * d * 2, st));
+        const int32_t* lp = last_pos ? last_pos + b0 : nullptr;
         for (int l = 0; l < cfg->n_layers; ++l) {
             const __nv_bfloat16* L = P + o.per_layer0 + (int64_t)l * o.layer_stride;
             RS_TRY(launch_ln(w.h, L + o.ln1_w, L + o.ln1_b, w.x, mp, d, st));
             RS_TRY(gemm_bf16(w.x, L + o.qkv_w, L + o.qkv_b, nullptr, w.qkv, mp, 3 * d, d, 0, st));
+            if (l == cfg->n_layers - 1) {
+                // only the last token of each prompt reaches the head: finish the layer on
+                // bc rows (exact; saves 20 d^2 (S - 1) FLOPs per prompt)
+                RS_TRY(launch_attention_last(w.qkv, w.h, lp, w.a_last, w.h_last, bc, bp, S, H, st));
+                RS_TRY(gemm_bf16(w.a_last, L + o.out_w, L + o.out_b, w.h_last, w.h_last, bp, d, d, 2, st));
+                RS_TRY(launch_ln(w.h_last, L + o.ln2_w, L + o.ln2_b, w.x_last, bp, d, st));
+                RS_TRY(gemm_bf16(w.x_last, L + o.fc1_w, L + o.fc1_b, nullptr, w.f_last, bp, F, d,
+                                 cfg->activation == 0 ? 1 : 3, st));
+                RS_TRY(gemm_bf16(w.f_last, L + o.fc2_w, L + o.fc2_b, w.h_last, w.h_last, bp, d, F, 2, st));
+                break;
+            }
             RS_TRY(attention_fwd(w.qkv, w.att, bc, S, H, st));
             RS_TRY(gemm_bf16(w.att, L + o.out_w, L + o.out_b, w.h, w.h, mp, d, d, 2, st));
             RS_TRY(launch_ln(w.h, L + o.ln2_w, L + o.ln2_b, w.x, mp, d, st));
             RS_TRY(gemm_bf16(w.x, L + o.fc1_w, L + o.fc1_b, nullptr, w.ffn, mp, F, d, cfg->activation == 0 ? 1 : 3, st));
             RS_TRY(gemm_bf16(w.ffn, L + o.fc2_w, L + o.fc2_b, w.h, w.h, mp, d, F, 2, st));
         }
-        RS_TRY(launch_head(w.h, last_pos ? last_pos + b0 : nullptr, bc, S, P, o, d, g + b0,
-                           score ? score + b0 : nullptr, st));
+        RS_TRY(launch_head(w.h_last, nullptr, bc, 1, P, o, d, g + b0, score ? score + b0 : nullptr, st));
     }
     return RS_OK;
 }

@@ -64,6 +64,15 @@ class RankerConfig:
         linear = L * (4 * d * d + 2 * d * F)
         return 2.0 * linear * S + 2.0 * d * S * (S + 1) * L + 2.0 * d
 
+    def flops_per_prompt_pruned(self, S: int) -> float:
+        """Algorithmic FLOPs of the forward rs_ranker_forward runs: the last layer only
+        needs K, V for every token and the last token's query / attention row / out-proj /
+        FFN (report against the pruned count when the last layer is pruned)."""
+        d, F, L = self.d_model, self.d_ffn, self.n_layers
+        full = 2.0 * (L - 1) * (4 * d * d + 2 * d * F) * S + 2.0 * d * S * (S + 1) * (L - 1)
+        last = 2.0 * (2 * d * d) * S + 2.0 * (d * d + d * d + 2 * d * F) + 4.0 * d * S
+        return full + last + 2.0 * d
+
 
 def layout(cfg: RankerConfig) -> tuple[int, dict[str, int]]:
     """(total bf16 elements, {tensor name: element offset}) from the C layout."""

@@ -28,8 +28,87 @@ def _small_cfg(**kw):
     return RankerConfig.opt_125m(**base)
 
 
+class _Round(torch.autograd.Function):
+    """Storage-precision emulation: forward value and/or backward gradient rounded to bf16
+    exactly where rs_ranker_grad stores a bf16 tensor (ranker_train.cu)."""
+
+    @staticmethod
+    def forward(ctx, x, fwd, bwd):
+        ctx.bwd = bwd
+        return x.bfloat16().float() if fwd else x.clone()
+
+    @staticmethod
+    def backward(ctx, g):
+        return (g.bfloat16().float() if ctx.bwd else g), None, None
+
+
+def _r(x, fwd=True, bwd=False):
+    return _Round.apply(x, fwd, bwd)
+
+
+def _forward_with_grad(params, cfg, ids, emulate=False):
+    """fp32 OPT-shape forward with autograd (the oracle, oracle/opt_ranker.py semantics).
+    emulate=True rounds activations / activation gradients to bf16 where the CUDA
+    training pass stores them in bf16 (x1, qkv, att, x2, f forward; dqkv, da, df and the
+    GEMM copy of dh backward); the residual stream stays fp32 in both."""
+    import torch.nn.functional as F
+    r = _r if emulate else (lambda x, fwd=True, bwd=False: x)
+    dev = params["tok_emb"].device
+    ids = torch.as_tensor(ids, dtype=torch.long, device=dev)
+    B, S = ids.shape
+    d, H = cfg.d_model, cfg.n_heads
+    hd = d // H
+    h = params["tok_emb"][ids] + params["pos_emb"][torch.arange(S, device=dev) + 2][None]
+    mask = torch.full((S, S), float("-inf"), device=dev).triu(1)
+    for layer in range(cfg.n_layers):
+        p = {k.split(".")[-1]: v for k, v in params.items() if k.startswith(f"layers.{layer}.")}
+        x = r(F.layer_norm(h, (d,), p["ln1_w"], p["ln1_b"], eps=1e-5))
+        qkv = r(x @ p["qkv_w"].t() + p["qkv_b"], True, True)
+        q, k, v = qkv.split(d, dim=-1)
+        q = q.view(B, S, H, hd).transpose(1, 2) * (hd ** -0.5)
+        k = k.view(B, S, H, hd).transpose(1, 2)
+        v = v.view(B, S, H, hd).transpose(1, 2)
+        att = (torch.softmax(q @ k.transpose(-1, -2) + mask, dim=-1) @ v).transpose(1, 2).reshape(B, S, d)
+        att = r(att, True, True)
+        h = h + r(att @ p["out_w"].t() + p["out_b"], False, True)
+        x = r(F.layer_norm(h, (d,), p["ln2_w"], p["ln2_b"], eps=1e-5))
+        f = r(torch.relu(x @ p["fc1_w"].t() + p["fc1_b"]), True, True)
+        h = h + r(f @ p["fc2_w"].t() + p["fc2_b"], False, True)
+    x = F.layer_norm(h[:, -1], (d,), params["lnf_w"], params["lnf_b"], eps=1e-5)
+    return x @ params["head_w"] + params["head_b"][0]
+
+
+def _ref_grads(model, cfg, ids, lengths, n_lists, list_len, emulate):
+    ref_params = {k: v.cuda().clone().requires_grad_(True) for k, v in model.params_cpu_fp32().items()}
+    with torch.enable_grad():
+        out = _forward_with_grad(ref_params, cfg, ids.numpy(), emulate)
+        L = _listmle_torch(out.view(n_lists, list_len), lengths.view(n_lists, list_len).numpy(), 10)
+        L.backward()
+    losses = np.array([_listmle_torch(out.view(n_lists, list_len)[i:i + 1].detach(),
+                                      lengths.view(n_lists, list_len)[i:i + 1].numpy(), 10).item()
+                       for i in range(n_lists)])
+    return {k: v.grad.detach() for k, v in ref_params.items()}, losses
+
+
+# ListMLE is invariant to a common shift of a list's scores (ranking.py:86-99), so the
+# exact gradients of head_b and lnf_b vanish; they are checked in absolute terms.
+_SHIFT_INVARIANT = ("head_b", "lnf_b")
+
+
 @pytest.mark.parametrize("S,list_len,n_lists,mb", [(64, 16, 4, 2), (128, 8, 3, 3), (100, 16, 2, 1)])
 def test_gradient_matches_autograd(S, list_len, n_lists, mb):
+    """rs_ranker_grad vs torch fp32 autograd on the same bf16-rounded parameters.
+
+    Bar: per-tensor relative Frobenius error <= 2e-2, or, where storing
+    activations / activation gradients in bf16 by itself moves the gradient further than
+    that, no further from fp32 than that storage-precision floor allows: the floor is
+    the deviation of the same autograd graph with bf16 rounding at every point the CUDA
+    pass stores bf16 (`emulate=True`), and the bar is 1.5 x floor + 2e-3. ListMLE only
+    sees score differences within a list, so parameters shared by every prompt (biases,
+    LayerNorm vectors, position embeddings) get gradients that nearly cancel over a
+    list; bf16 rounding noise is large relative to them (floors of 4-20% here), while
+    the weight matrices sit near 2-4%. The CUDA pass is also compared with the
+    emulation itself (two independent bf16 noises: <= 2 x floor + 2e-3)."""
     from paper_2408_15792_b200.ranker import OptRanker, init_params
     from paper_2408_15792_b200.trainer import RankerTrainer
     cfg = _small_cfg()
@@ -44,57 +123,33 @@ def test_gradient_matches_autograd(S, list_len, n_lists, mb):
     lengths = torch.randint(1, 2049, (n,), generator=g, dtype=torch.int32)
     tr = RankerTrainer(model, lists_per_micro=mb)
     loss = tr.accumulate(ids.cuda(), lengths.cuda(), list_len).cpu()
-    # oracle: fp32 autograd on the same bf16-rounded parameters
-    ref_params = {k: v.clone().requires_grad_(True) for k, v in model.params_cpu_fp32().items()}
-    # (opt_ranker's functions run under no_grad; the same forward with autograd here)
-    with torch.enable_grad():
-        out = _forward_with_grad(ref_params, cfg, ids.numpy())
-        L = _listmle_torch(out.view(n_lists, list_len), lengths.view(n_lists, list_len).numpy(), 10)
-        L.backward()
-    ref_loss = np.array([_listmle_torch(out.view(n_lists, list_len)[i:i + 1].detach(),
-                                        lengths.view(n_lists, list_len)[i:i + 1].numpy(), 10).item()
-                         for i in range(n_lists)])
+    ref32, ref_loss = _ref_grads(model, cfg, ids, lengths, n_lists, list_len, emulate=False)
+    emu, _ = _ref_grads(model, cfg, ids, lengths, n_lists, list_len, emulate=True)
     np.testing.assert_allclose(loss.numpy(), ref_loss, rtol=2e-2, atol=2e-3)
-    grads = {n_: tr.grad[model.offsets[n_]:model.offsets[n_] + p.numel()].view(p.shape).cpu()
-             for n_, p in ref_params.items()}
-    worst = []
-    for name, p in ref_params.items():
-        ref = p.grad
-        if ref is None or ref.norm() == 0:
+    hw_scale = ref32["head_w"].norm().item()
+    report, bad = [], []
+    for name, ref in ref32.items():
+        got = tr.grad[model.offsets[name]:model.offsets[name] + ref.numel()].view(ref.shape)
+        e = emu[name]
+        if name in _SHIFT_INVARIANT:
+            err = (got - ref).abs().max().item()
+            report.append((err / hw_scale, name, "abs/|d head_w|"))
+            if err > 1e-2 * hw_scale:
+                bad.append(report[-1])
             continue
         if name in ("tok_emb", "pos_emb"):
             used = ref.abs().sum(1) > 0
-            got, ref = grads[name][used], ref[used]
-        else:
-            got = grads[name]
-        rel = ((got - ref).norm() / ref.norm()).item()
-        worst.append((rel, name))
-        assert rel <= 2e-2, (name, rel)
-    assert len(worst) > 20
-
-
-def _forward_with_grad(params, cfg, ids):
-    import torch.nn.functional as F
-    ids = torch.as_tensor(ids, dtype=torch.long)
-    B, S = ids.shape
-    d, H = cfg.d_model, cfg.n_heads
-    hd = d // H
-    h = params["tok_emb"][ids] + params["pos_emb"][torch.arange(S) + 2][None]
-    mask = torch.full((S, S), float("-inf")).triu(1)
-    for layer in range(cfg.n_layers):
-        p = {k.split(".")[-1]: v for k, v in params.items() if k.startswith(f"layers.{layer}.")}
-        x = F.layer_norm(h, (d,), p["ln1_w"], p["ln1_b"], eps=1e-5)
-        qkv = x @ p["qkv_w"].t() + p["qkv_b"]
-        q, k, v = qkv.split(d, dim=-1)
-        q = q.view(B, S, H, hd).transpose(1, 2) * (hd ** -0.5)
-        k = k.view(B, S, H, hd).transpose(1, 2)
-        v = v.view(B, S, H, hd).transpose(1, 2)
-        att = (torch.softmax(q @ k.transpose(-1, -2) + mask, dim=-1) @ v).transpose(1, 2).reshape(B, S, d)
-        h = h + att @ p["out_w"].t() + p["out_b"]
-        x = F.layer_norm(h, (d,), p["ln2_w"], p["ln2_b"], eps=1e-5)
-        h = h + torch.relu(x @ p["fc1_w"].t() + p["fc1_b"]) @ p["fc2_w"].t() + p["fc2_b"]
-    x = F.layer_norm(h[:, -1], (d,), params["lnf_w"], params["lnf_b"], eps=1e-5)
-    return x @ params["head_w"] + params["head_b"][0]
+            got, ref, e = got[used], ref[used], e[used]
+        if ref.norm() == 0:
+            continue
+        r_emu = ((got - e).norm() / e.norm()).item()
+        r_32 = ((got - ref).norm() / ref.norm()).item()
+        floor = ((e - ref).norm() / ref.norm()).item()
+        report.append((r_emu, name, r_32, floor))
+        if not r_32 <= max(2e-2, 1.5 * floor + 2e-3) or not r_emu <= max(2e-2, 2 * floor + 2e-3):
+            bad.append(report[-1])
+    assert not bad, (bad, sorted(report, key=lambda t: -t[0])[:8])
+    assert len(report) > 20
 
 
 def test_adam_first_step_is_minus_lr_sign():
@@ -106,14 +161,31 @@ def test_adam_first_step_is_minus_lr_sign():
     master = torch.randn(n, device="cuda", generator=g)
     p0 = master.clone()
     grad = torch.randn(n, device="cuda", generator=g)
-    sign = torch.sign(grad)
+    g0 = grad.clone()
     m, v = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
     pb = torch.empty(n, dtype=torch.bfloat16, device="cuda")
     _lib.check(_lib.load().rs_adam_step(master.data_ptr(), m.data_ptr(), v.data_ptr(), grad.data_ptr(), pb.data_ptr(),
                                         n, 1e-2, 0.9, 0.999, 1e-8, 1, 1.0, _lib.stream_handle()))
-    torch.testing.assert_close(master, p0 - 1e-2 * sign, rtol=0, atol=1e-6)
+    want = p0.double() - 1e-2 * g0.double() / (g0.double().abs() + 1e-8)  # m_hat/(sqrt(v_hat)+eps)
+    torch.testing.assert_close(master.double(), want, rtol=0, atol=1e-6)
+    assert (master - p0).abs().sub(1e-2).abs().max().item() < 1e-4  # |step| = lr (sign of g)
     assert grad.abs().max().item() == 0.0
     torch.testing.assert_close(pb.float(), master, rtol=1e-2, atol=1e-2)
+
+
+def test_adam_converges_on_quadratic():
+    """test_predictors.py:126-131: 200 Adam steps on p^2 from p = 5 at lr 0.3 reach |p| < 1e-2."""
+    from paper_2408_15792_b200 import _lib
+    _lib.device()
+    lib = _lib.load()
+    master = torch.tensor([5.0], device="cuda")
+    m, v, grad = torch.zeros(1, device="cuda"), torch.zeros(1, device="cuda"), torch.zeros(1, device="cuda")
+    pb = torch.empty(1, dtype=torch.bfloat16, device="cuda")
+    for t in range(1, 201):
+        grad.copy_(2 * master)
+        _lib.check(lib.rs_adam_step(master.data_ptr(), m.data_ptr(), v.data_ptr(), grad.data_ptr(), pb.data_ptr(), 1,
+                                    0.3, 0.9, 0.999, 1e-8, t, 1.0, _lib.stream_handle()))
+    assert abs(master.item()) < 1e-2
 
 
 def test_training_reduces_loss_and_is_deterministic():
