@@ -264,6 +264,51 @@ def tau_and_rankstep(pk, reps=5):
     }
 
 
+def train_step_metric(args, world, rank, pk):
+    """cfg3 (BASELINE.json configs[2]): one ListMLE optimizer step over a global batch of
+    1024 lists x 64 prompts x 128 tokens, lists sharded across ranks, gradient all-reduce
+    (NCCL) + fused Adam. Device time by CUDA events, max over ranks."""
+    from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
+    from paper_2408_15792_b200.trainer import RankerTrainer
+    cfg = RankerConfig.opt_125m()
+    n_lists, list_len, S = args.train_lists, 64, args.train_seq
+    mine = len(range(rank, n_lists, world))
+    model = OptRanker(cfg, seed=0)
+    tr = RankerTrainer(model, lr=2e-5, lists_per_micro=args.train_micro)
+    gen = torch.Generator().manual_seed(2000 + rank)
+    ids = torch.randint(4, cfg.vocab, (mine * list_len, S), generator=gen, dtype=torch.int32).cuda()
+    lengths = torch.randint(1, 2049, (mine * list_len,), generator=gen, dtype=torch.int32).cuda()
+
+    def step():
+        tr.accumulate(ids, lengths, list_len)
+        tr.apply(n_lists)
+
+    step()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.train_steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.train_steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    prompts = n_lists * list_len
+    flops = 3.0 * cfg.flops_per_prompt(S) * prompts  # fwd + dgrad + wgrad
+    tflops = flops / (ms / 1e3) / 1e12 / world
+    del tr, model, ids, lengths
+    torch.cuda.empty_cache()
+    return {"metric": "ListMLE training prompts/sec (1024 lists x 64 prompts x 128 tokens per step, DP)",
+            "value": prompts / (ms / 1e3), "unit": "prompts/s", "ms_per_step": ms, "steps": args.train_steps,
+            "global_lists": n_lists, "list_len": list_len, "seq_len": S, "flops_per_step": flops,
+            "tflops_per_gpu": tflops, "frac_of_sustained": tflops / pk["bf16_tflops_sustained"]}
+
+
 def run_ours(args):
     import torch.distributed as dist
     world, rank, local = dist_env()
@@ -353,6 +398,9 @@ def run_ours(args):
     if rank == 0 and not args.no_extras:
         extras["roofline"] = gemm_roofline(pk)
         extras.update(tau_and_rankstep(pk))
+    if not args.no_extras and not args.no_train:
+        extras["train_step"] = train_step_metric(args, world, rank, pk)
+    if rank == 0 and not args.no_extras:
         if world == 1:
             extras["cpu_baseline"] = cpu_baseline(cfg, S, n_prompts=args.cpu_prompts)
     if world > 1:
@@ -383,6 +431,7 @@ def run_ours(args):
         "peaks": {k: pk.get(k) for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained", "source")},
         "tau": extras.get("tau"),
         "rank_step": extras.get("rank_step"),
+        "train_step": extras.get("train_step"),
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -401,6 +450,11 @@ def main():
     ap.add_argument("--cpu-prompts", type=int, default=16)
     ap.add_argument("--ref-prompts", type=int, default=4)
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--train-lists", type=int, default=1024)
+    ap.add_argument("--train-seq", type=int, default=128)
+    ap.add_argument("--train-micro", type=int, default=16)
+    ap.add_argument("--train-steps", type=int, default=1)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

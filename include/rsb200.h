@@ -163,14 +163,16 @@ int rs_ranker_forward(const rs_ranker_config* cfg, const void* params_dev, const
 /* ---- A10/K7/K8: training (ListMLE over whole lists, predictors.py:347-406) ----------
  * Accumulates into grad_dev (fp32, rs_ranker_layout order and length) the gradient of
  * sum over lists of list_mle_loss(g_list, order_list) / list_len, where g = the ranker's
- * net output for the list's prompts and order_list = stable argsort of
- * lengths // bucket_width (predictors.py:379-384). ids: int32 [n_lists * list_len, S]
- * (S <= 128); lengths: int32 [n_lists * list_len]; loss_dev[n_lists] = per-list loss / n.
- * Processes lists_per_micro lists at a time. Deterministic (no float atomics). */
+ * net output for the list's prompts (read at last_pos, like rs_ranker_forward; NULL =
+ * S-1) and order_list = stable argsort of lengths // bucket_width (predictors.py:379-384).
+ * ids: int32 [n_lists * list_len, S] (S <= 128); lengths: int32 [n_lists * list_len];
+ * loss_dev[n_lists] = per-list loss / n. Processes lists_per_micro lists at a time.
+ * Deterministic (no float atomics). */
 size_t rs_ranker_grad_workspace_size(const rs_ranker_config* cfg, int32_t lists_per_micro, int32_t list_len, int32_t S);
 int rs_ranker_grad(const rs_ranker_config* cfg, const void* params_dev, float* grad_dev, const int32_t* ids_dev,
-                   const int32_t* lengths_dev, int32_t n_lists, int32_t list_len, int32_t S, int32_t bucket_width,
-                   int32_t lists_per_micro, float* loss_dev, void* ws_dev, size_t ws_bytes, void* stream);
+                   const int32_t* last_pos_dev, const int32_t* lengths_dev, int32_t n_lists, int32_t list_len,
+                   int32_t S, int32_t bucket_width, int32_t lists_per_micro, float* loss_dev, void* ws_dev,
+                   size_t ws_bytes, void* stream);
 /* Adam (predictors.py:218-225) over the flat buffer: g = grad * grad_scale; m, v, fp32
  * master updated with bias correction at step t (>= 1); the bf16 working copy is
  * rewritten and grad is zeroed for the next accumulation. */

@@ -66,8 +66,8 @@ SIGNATURES = {
     "rs_attention_fwd": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "rs_launch_count": (ctypes.c_uint64, []),
     "rs_ranker_grad_workspace_size": (c_sz, [ctypes.POINTER(RankerConfig), c_i32, c_i32, c_i32]),
-    "rs_ranker_grad": (ctypes.c_int, [ctypes.POINTER(RankerConfig), c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32,
-                                      c_i32, c_vp, c_vp, c_sz, c_vp]),
+    "rs_ranker_grad": (ctypes.c_int, [ctypes.POINTER(RankerConfig), c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32,
+                                      c_i32, c_i32, c_vp, c_vp, c_sz, c_vp]),
     "rs_adam_step": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.c_float, ctypes.c_float,
                                     ctypes.c_float, ctypes.c_float, c_i64, ctypes.c_float, c_vp]),
     "rs_attention_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),

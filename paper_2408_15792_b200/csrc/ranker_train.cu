@@ -116,7 +116,7 @@ extern "C" size_t rs_ranker_grad_workspace_size(const rs_ranker_config* cfg, int
 }
 
 extern "C" int rs_ranker_grad(const rs_ranker_config* cfg, const void* params, float* grad, const int32_t* ids,
-                              const int32_t* lengths, int32_t n_lists, int32_t list_len, int32_t S,
+                              const int32_t* last_pos, const int32_t* lengths, int32_t n_lists, int32_t list_len, int32_t S,
                               int32_t bucket_width, int32_t lists_per_micro, float* loss_out, void* ws,
                               size_t ws_bytes, void* stream) {
     cudaStream_t st = as_stream(stream);
@@ -146,6 +146,7 @@ extern "C" int rs_ranker_grad(const rs_ranker_config* cfg, const void* params, f
         }
         const int32_t* mids = ids + (int64_t)l0 * list_len * S;
         const int32_t* mlen = lengths + (int64_t)l0 * list_len;
+        const int32_t* mlast = last_pos ? last_pos + (int64_t)l0 * list_len : nullptr;
         // ---- forward, keeping activations ----
         RS_TRY(ranker_embed(mids, P16, off(OFF_TOK, 0), off(OFF_POS, 0), w.h_in[0], n_tok, S, d, cfg->vocab, (int)Tp,
                             st));
@@ -166,7 +167,7 @@ extern "C" int rs_ranker_grad(const rs_ranker_config* cfg, const void* params, f
             RS_TRY(gemm_bf16(w.f[l], P16 + off(OFF_FC2_W, l), P16 + off(OFF_FC2_B, l), w.h_mid[l], w.h_in[l + 1],
                              (int)Tp, d, F, 2, st));
         }
-        RS_TRY(ranker_head(w.h_in[L], nullptr, P, S, P16, cfg, w.g, nullptr, st));
+        RS_TRY(ranker_head(w.h_in[L], mlast, P, S, P16, cfg, w.g, nullptr, st));
         // ---- ListMLE (K6): per-list loss / n and dg = grad / n ----
         RS_TRY(listmle_lengths_launch(w.g, mlen, ml, list_len, bucket_width, loss_out + l0, w.dg, st));
         // ---- backward ----
@@ -174,7 +175,7 @@ extern "C" int rs_ranker_grad(const rs_ranker_config* cfg, const void* params, f
         // padding rows take part in the wgrad reductions: keep their gradients zero
         if (Tp > n_tok)
             RS_CUDA(cudaMemsetAsync(w.dqkv + (size_t)n_tok * 3 * d, 0, (size_t)(Tp - n_tok) * 3 * d * 2, st));
-        RS_TRY(head_backward(w.h_in[L], nullptr, P, S, P16 + off(OFF_LNF_W, 0), P16 + off(OFF_LNF_B, 0),
+        RS_TRY(head_backward(w.h_in[L], mlast, P, S, P16 + off(OFF_LNF_W, 0), P16 + off(OFF_LNF_B, 0),
                              P16 + off(OFF_HEAD_W, 0), w.dg, w.dh, w.rpart, d, grad + off(OFF_HEAD_W, 0),
                              grad + off(OFF_LNF_W, 0), grad + off(OFF_HEAD_B, 0), st));
         f32_to_bf16_kernel<<<1184, 256, 0, st>>>(w.dh, w.dh16, (int64_t)Tp * d);

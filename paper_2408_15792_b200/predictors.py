@@ -145,9 +145,107 @@ class TrainConfig:
     seed: int = 0
     seq_len: int = 128
     lists_per_step: int = 1
+    lists_per_micro: int = 16
+    ranker: RankerConfig = RankerConfig()
 
 
 @dataclass
 class TrainResult:
     scorer: object
     report: dict = field(default_factory=dict)
+
+
+def _encode(requests, seq_len: int, vocab: int):
+    ids = np.empty((len(requests), seq_len), dtype=np.int32)
+    last = np.empty(len(requests), dtype=np.int32)
+    for k, r in enumerate(requests):
+        ids[k], last[k] = prompt_token_ids(getattr(r, "prompt", "") or "", seq_len, vocab)
+    return ids, last
+
+
+def train_ranking(trace, cfg: TrainConfig = TrainConfig(), eval_trace=None, model: OptRanker | None = None,
+                  group=None) -> TrainResult:
+    """ListMLE training of the OPT-shape ranker (reference: train_ranking,
+    predictors.py:347-406, same split, shuffling, list construction, checkpoints and
+    report keys).
+
+    Every minibatch of `batch_size` requests is one ranked list whose target order is
+    the stable argsort of bucketed true lengths (predictors.py:379-381); the list's
+    ListMLE loss / n and its gradient come from the fused device pass (rs_ranker_grad,
+    forward + K6 + tcgen05 backward). `lists_per_step` consecutive lists share one Adam
+    step (gradient = mean over lists); 1 reproduces the reference's one-list-per-step
+    sequence. Under torch.distributed the lists of a step are split across ranks and
+    the gradient is all-reduced (NCCL) before the replicated Adam step.
+    """
+    from . import dp
+    from .ranking import kendall_tau_b
+    from .trainer import RankerTrainer
+
+    reqs = list(trace)
+    if len(reqs) < 4:
+        raise ValueError("need at least 4 requests to train")
+    if cfg.bucket_width < 1:
+        raise ValueError("bucket_width must be >= 1")
+    if cfg.lists_per_step < 1:
+        raise ValueError("lists_per_step must be >= 1")
+    y_all = np.array([r.true_output_tokens for r in reqs], dtype=np.int64)
+    if eval_trace is not None:
+        tr_reqs, ev_reqs = reqs, list(eval_trace)
+    else:  # _split_features (predictors.py:327-340)
+        rng0 = np.random.default_rng(cfg.seed)
+        idx = rng0.permutation(len(y_all))
+        n_eval = max(1, int(round(cfg.eval_fraction * len(y_all))))
+        if n_eval >= len(y_all):
+            raise ValueError("trace too small to split for evaluation")
+        tr_reqs = [reqs[i] for i in idx[n_eval:]]
+        ev_reqs = [reqs[i] for i in idx[:n_eval]]
+    rc = cfg.ranker
+    if model is None:
+        model = OptRanker(rc, seed=cfg.seed)
+    dev = model.dev
+    ids_np, last_np = _encode(tr_reqs, cfg.seq_len, rc.vocab)
+    eids_np, elast_np = _encode(ev_reqs, cfg.seq_len, rc.vocab)
+    y = np.array([r.true_output_tokens for r in tr_reqs], dtype=np.int64)
+    ye = np.array([r.true_output_tokens for r in ev_reqs], dtype=np.int64)
+    ids = torch.from_numpy(ids_np).to(dev)
+    last = torch.from_numpy(last_np).to(dev)
+    yd = torch.from_numpy(y.astype(np.int32)).to(dev)
+    eids = torch.from_numpy(eids_np).to(dev)
+    elast = torch.from_numpy(elast_np).to(dev)
+
+    world, rank = dp.world_rank(group)
+    trainer = RankerTrainer(model, lr=cfg.learning_rate, betas=cfg.betas, bucket_width=cfg.bucket_width,
+                            lists_per_micro=cfg.lists_per_micro, group=group)
+
+    def eval_tau() -> float:
+        g = model.forward(eids, elast)
+        return kendall_tau_b(-g, ye).tau
+
+    rng = np.random.default_rng(cfg.seed + 1)
+    step = 0
+    window: list[torch.Tensor] = []
+    checkpoints: list[dict] = []
+    for _epoch in range(cfg.epochs):
+        order = rng.permutation(len(y))
+        lists = [order[s:s + cfg.batch_size] for s in range(0, len(order), cfg.batch_size)]
+        lists = [b for b in lists if len(b) >= 2]
+        for g0 in range(0, len(lists), cfg.lists_per_step):
+            grp = lists[g0:g0 + cfg.lists_per_step]
+            losses = []
+            for b in dp.shard_lists(grp, world, rank):
+                bi = torch.from_numpy(b).to(dev)
+                losses.append(trainer.accumulate(ids[bi], yd[bi], len(b), last[bi]))
+            trainer.apply(len(grp))
+            step_loss = torch.cat(losses).sum() if losses else torch.zeros((), device=dev)
+            dp.allreduce_sum_(step_loss, group)
+            window.append(step_loss / len(grp))
+            step += 1
+            if step % cfg.checkpoint_every == 0:
+                checkpoints.append({"step": step, "train_loss": float(torch.stack(window).mean().item()),
+                                    "eval_tau": eval_tau()})
+                window = []
+    final_tau = eval_tau()
+    scorer = OptRankerScorer(model, seq_len=cfg.seq_len)
+    report = {"kind": "ranking", "steps": step, "checkpoints": checkpoints, "eval_tau": final_tau,
+              "n_train": len(y), "n_eval": len(ye)}
+    return TrainResult(scorer, report)

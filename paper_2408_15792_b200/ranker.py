@@ -16,7 +16,7 @@ from dataclasses import dataclass, replace
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, dp
 
 GLOBAL_NAMES = ("tok_emb", "pos_emb", "lnf_w", "lnf_b", "head_w", "head_b")
 LAYER_NAMES = ("ln1_w", "ln1_b", "qkv_w", "qkv_b", "out_w", "out_b", "ln2_w", "ln2_b", "fc1_w", "fc1_b",
@@ -151,3 +151,15 @@ class OptRanker:
                                          None if score_out is None else score_out.data_ptr(), ws, wn,
                                          _lib.stream_handle(self.dev)), "rs_ranker_forward")
         return g
+
+    def forward_sharded(self, ids: torch.Tensor, last_pos: torch.Tensor | None = None, group=None) -> torch.Tensor:
+        """Data-parallel scoring: this rank scores its contiguous shard of the
+        global batch `ids` [B, S] and the fp32 outputs of all B prompts are all-gathered
+        (NCCL) in prompt order. One rank: plain forward."""
+        world, rank = dp.world_rank(group)
+        lo, hi = dp.shard_range(ids.shape[0], world, rank)
+        if hi > lo:
+            g = self.forward(ids[lo:hi], None if last_pos is None else last_pos[lo:hi])
+        else:
+            g = torch.empty(0, dtype=torch.float32, device=ids.device)
+        return dp.gather_scores(g, ids.shape[0], group)

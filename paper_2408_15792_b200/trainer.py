@@ -15,9 +15,7 @@ from __future__ import annotations
 import ctypes
 
 import torch
-import torch.distributed as dist
-
-from . import _lib
+from . import _lib, dp
 from .ranker import OptRanker
 
 
@@ -39,11 +37,13 @@ class RankerTrainer:
         self.t = 0
 
     def _world(self) -> int:
-        return dist.get_world_size(self.group) if dist.is_available() and dist.is_initialized() else 1
+        return dp.world_rank(self.group)[0]
 
-    def accumulate(self, ids: torch.Tensor, lengths: torch.Tensor, list_len: int) -> torch.Tensor:
+    def accumulate(self, ids: torch.Tensor, lengths: torch.Tensor, list_len: int,
+                   last_pos: torch.Tensor | None = None) -> torch.Tensor:
         """Add the gradient of sum_lists ListMLE/list_len for this rank's lists to .grad;
-        returns the per-list losses (device tensor)."""
+        returns the per-list losses (device tensor). last_pos (int32 [n], optional) is
+        each prompt's last real token (the score is read there, as in forward)."""
         n_prompts, S = ids.shape
         if n_prompts % list_len:
             raise ValueError("ids rows must be whole lists")
@@ -51,6 +51,7 @@ class RankerTrainer:
         dev = self.model.dev
         ids = ids.to(dev, torch.int32).contiguous()
         lengths = lengths.to(dev, torch.int32).contiguous().view(-1)
+        lp = None if last_pos is None else last_pos.to(dev, torch.int32).contiguous().view(-1)
         loss = torch.empty(n_lists, dtype=torch.float32, device=dev)
         lib = _lib.load()
         c = self.model.cfg.c()
@@ -58,14 +59,13 @@ class RankerTrainer:
         need = lib.rs_ranker_grad_workspace_size(ctypes.byref(c), mb, list_len, S)
         ws, wn = _lib.workspace.get(need, dev)
         _lib.check(lib.rs_ranker_grad(ctypes.byref(c), self.model.flat.data_ptr(), self.grad.data_ptr(),
-                                      ids.data_ptr(), lengths.data_ptr(), n_lists, list_len, S, self.bucket_width,
+                                      ids.data_ptr(), _lib.ptr(lp), lengths.data_ptr(), n_lists, list_len, S, self.bucket_width,
                                       mb, loss.data_ptr(), ws, wn, _lib.stream_handle(dev)), "rs_ranker_grad")
         return loss
 
     def apply(self, total_lists: int) -> None:
         """All-reduce the accumulated gradient across ranks (NCCL) and take one Adam step."""
-        if self._world() > 1:
-            dist.all_reduce(self.grad, op=dist.ReduceOp.SUM, group=self.group)
+        dp.allreduce_sum_(self.grad, self.group)
         self.t += 1
         _lib.check(_lib.load().rs_adam_step(self.master.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
                                             self.grad.data_ptr(), self.model.flat.data_ptr(), self.master.numel(),
@@ -73,8 +73,9 @@ class RankerTrainer:
                                             1.0 / float(total_lists), _lib.stream_handle(self.model.dev)),
                    "rs_adam_step")
 
-    def step(self, ids: torch.Tensor, lengths: torch.Tensor, list_len: int, total_lists: int | None = None):
-        loss = self.accumulate(ids, lengths, list_len)
+    def step(self, ids: torch.Tensor, lengths: torch.Tensor, list_len: int, total_lists: int | None = None,
+             last_pos: torch.Tensor | None = None):
+        loss = self.accumulate(ids, lengths, list_len, last_pos)
         n_lists = ids.shape[0] // list_len
         self.apply(total_lists if total_lists is not None else n_lists * self._world())
         return loss
