@@ -189,10 +189,6 @@ int rs_gemm_bf16(const void* A_dev, const void* W_dev, const void* bias_dev, con
 /* Causal multi-head attention over packed qkv [B*S, 3*H*64] bf16 -> out [B*S, H*64]. */
 int rs_attention_fwd(const void* qkv_dev, void* out_dev, int32_t B, int32_t S, int32_t H,
                      void* stream);
-/* Diagnostics: as rs_attention_fwd, and CTA 0's softmax warp writes per-block phase
- * timestamps (clock64) to trace_dev[64 * 8] (zero-initialise it). */
-int rs_attention_fwd_trace(const void* qkv_dev, void* out_dev, int32_t B, int32_t S, int32_t H,
-                           unsigned long long* trace_dev, void* stream);
 /* General CTA-pair GEMM used by the backward pass: a_mn / b_mn = operand stored
  * MN-contiguous ([K, M] / [K, N]); epi 4 = fp32 out, 5 = bf16 out * (aux > 0) (ReLU
  * backward, aux bf16 [M, N]), 6 = fp32 split-K partials (C holds k_splits x [M, N]).

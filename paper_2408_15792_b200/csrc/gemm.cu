@@ -215,7 +215,15 @@ constexpr int G2_A_BYTES = G2_HALF * G2_BK * 2;  // 16 KB per CTA
 constexpr int G2_B_BYTES = G2_HALF * G2_BK * 2;  // 16 KB per CTA
 constexpr int G2_STAGE_BYTES = G2_A_BYTES + G2_B_BYTES;
 constexpr int G2_EPI_BUF = 32 * 32 * 4;          // one 32x32 fp32 (or bf16) staging sub-tile
-constexpr int G2_SMEM = G2_STAGES * G2_STAGE_BYTES + 4 * 2 * G2_EPI_BUF + 1024 + 256;
+// The residual epilogue (EPI 2) streams R through the staging buffers with TMA (5 per
+// warp, 2 sub-tiles prefetched ahead) and gives up one mainloop stage for them: with
+// K = 768 the mainloop is short and the fp32 R read + C write (8 B per output) bound it.
+template <int EPI>
+struct G2Cfg {
+    static constexpr int stages = EPI == 2 ? 5 : G2_STAGES;
+    static constexpr int nbuf = EPI == 2 ? 4 : 2;
+    static constexpr int smem = stages * G2_STAGE_BYTES + 4 * nbuf * G2_EPI_BUF + 1024 + 512;
+};
 
 // EPI: 0 bf16, 1 ReLU->bf16, 2 +fp32 residual->fp32, 3 GELU->bf16, 4 fp32 (bias optional),
 // 5 bf16 * (mask > 0) with the bf16 mask in `aux` (ReLU backward), 6 fp32 split-K partial
@@ -223,19 +231,22 @@ constexpr int G2_SMEM = G2_STAGES * G2_STAGE_BYTES + 4 * 2 * G2_EPI_BUF + 1024 +
 template <int EPI, bool A_MN = false, bool B_MN = false>
 __global__ void __launch_bounds__(G_THREADS, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
-                         const __grid_constant__ CUtensorMap tC, const __nv_bfloat16* __restrict__ bias,
-                         const void* __restrict__ aux, int M, int N, int K, int ldc, int k_splits) {
-    const float* R = static_cast<const float*>(aux);
+                         const __grid_constant__ CUtensorMap tC, const __grid_constant__ CUtensorMap tR,
+                         const __nv_bfloat16* __restrict__ bias, const void* __restrict__ aux, int M, int N, int K,
+                         int ldc, int k_splits) {
+    constexpr int G2_STAGES = G2Cfg<EPI>::stages;
+    constexpr int NBUF = G2Cfg<EPI>::nbuf;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + G2_STAGES * G2_A_BYTES;
-    uint8_t* sE = smem + G2_STAGES * G2_STAGE_BYTES;  // epilogue staging: 4 warps x 2 buffers
-    uint64_t* full = reinterpret_cast<uint64_t*>(sE + 4 * 2 * G2_EPI_BUF);
+    uint8_t* sE = smem + G2_STAGES * G2_STAGE_BYTES;  // epilogue staging: 4 warps x NBUF buffers
+    uint64_t* full = reinterpret_cast<uint64_t*>(sE + 4 * NBUF * G2_EPI_BUF);
     uint64_t* empty = full + G2_STAGES;
     uint64_t* tfull = empty + G2_STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* rfull = tempty + 2;  // [4 warps][NBUF]: residual sub-tile landed (EPI 2)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rfull + 4 * NBUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -244,6 +255,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         tma_prefetch_desc(&tA);
         tma_prefetch_desc(&tB);
         tma_prefetch_desc(&tC);
+        if (EPI == 2) tma_prefetch_desc(&tR);
         for (int s = 0; s < G2_STAGES; ++s) {
             mbar_init(&full[s], 2);  // leader: both CTAs' producers arrive (+ 64 KB of tx)
             mbar_init(&empty[s], 1);
@@ -252,6 +264,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 8);  // leader: 4 epilogue warps x 2 CTAs
         }
+        for (int a = 0; a < 4 * NBUF; ++a) mbar_init(&rfull[a], 1);
         fence_barrier_init();
     }
     if (warp == 2) tmem_alloc_2sm<512>(tmem_slot);
@@ -274,7 +287,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 
     if (warp == 0) {
         if (elect_one()) {
-            const uint64_t pol_a = policy_evict_first(), pol_b = policy_evict_last();
+            const uint64_t pol_a = policy_evict_normal(), pol_b = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
             for (int w = cid; w < n_work; w += ncl) {
@@ -352,10 +365,26 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     } else if (warp >= 4) {
         const int q = warp & 3;
         const int row = q * 32 + lane;
-        uint8_t* ebuf = sE + q * 2 * G2_EPI_BUF;
+        uint8_t* ebuf = sE + q * NBUF * G2_EPI_BUF;
+        uint64_t* rf = rfull + q * NBUF;
         int acc = 0;
         uint32_t acc_phase = 0;
-        int nst = 0;  // staging sub-tiles issued by this warp (buffer = nst & 1)
+        int nst = 0;  // staging sub-tiles issued by this warp (buffer = nst % NBUF)
+        // EPI 2: sub-tile n of this warp's sequence is column chunk n % 8 of work item
+        // cid + (n / 8) * ncl; its residual is TMA-loaded PD sub-tiles ahead
+        constexpr int PD = NBUF - 2;
+        auto prefetch_r = [&](int n) {
+            const int w = cid + (n >> 3) * ncl;
+            if (w >= n_work) return;
+            const int tile = w / k_splits;
+            const int rm0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
+            const int rn0 = (tile % tiles_n) * G2_BN;
+            const int b = n % NBUF;
+            mbar_arrive_expect_tx(&rf[b], G2_EPI_BUF);
+            tma_load_2d(ebuf + b * G2_EPI_BUF, &tR, &rf[b], rn0 + (n & 7) * 32, rm0 + q * 32);
+        };
+        if (EPI == 2 && lane == 0)
+            for (int n = 0; n < PD; ++n) prefetch_r(n);
         for (int w = cid; w < n_work; w += ncl) {
             const int tile = w / k_splits;
             const int m0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
@@ -364,7 +393,6 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             const int mo = (EPI == 6) ? m0 + (w % k_splits) * M : m0;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const float* rrow = (EPI == 2) ? R + (size_t)(m0 + row) * ldc + n0 : nullptr;
             const __nv_bfloat16* mrow =
                 (EPI == 5) ? static_cast<const __nv_bfloat16*>(aux) + (size_t)(m0 + row) * ldc + n0 : nullptr;
 #pragma unroll 1
@@ -373,17 +401,23 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * G2_BN + c, r);
                 float v[32];
                 const uint4* bv = reinterpret_cast<const uint4*>(bias + n0 + c);
-                float4 rr[8];
                 uint4 mk[4];
-                if (EPI == 2) {
-                    const float4* rv = reinterpret_cast<const float4*>(rrow + c);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) rr[j] = rv[j];
-                }
                 if (EPI == 5) {
                     const uint4* mv = reinterpret_cast<const uint4*>(mrow + c);
 #pragma unroll
                     for (int j = 0; j < 4; ++j) mk[j] = mv[j];
+                }
+                uint8_t* buf = ebuf + (nst % NBUF) * G2_EPI_BUF;
+                if (EPI == 2) {
+                    // reuse of buffer (nst + PD) % NBUF: its last store (sub-tile nst - 2) has
+                    // been read; then queue that residual sub-tile
+                    if (lane == 0) {
+                        tma_store_wait_read<1>();
+                        prefetch_r(nst + PD);
+                    }
+                } else {
+                    // the TMA store that last read this buffer (two sub-tiles ago) must be done
+                    if (lane == 0 && nst >= 2) tma_store_wait_read<1>();
                 }
                 tmem_ld_wait();
                 if (bias != nullptr) {
@@ -414,22 +448,22 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                         }
                     }
                 }
-                uint8_t* buf = ebuf + (nst & 1) * G2_EPI_BUF;
-                // the TMA store that last read this buffer (two sub-tiles ago) must be done
-                if (lane == 0 && nst >= 2) tma_store_wait_read<1>();
+                if (EPI == 2) mbar_wait(&rf[nst % NBUF], (nst / NBUF) & 1);
                 __syncwarp();
                 if (EPI == 2 || EPI == 4 || EPI == 6) {
                     // fp32 32x32 sub-tile, 128-B rows, SWIZZLE_128B: chunk j ^ (row % 8)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
+                        float4* p = reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
                         float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
                         if (EPI == 2) {
-                            o.x += rr[j].x;
-                            o.y += rr[j].y;
-                            o.z += rr[j].z;
-                            o.w += rr[j].w;
+                            const float4 rr = *p;
+                            o.x += rr.x;
+                            o.y += rr.y;
+                            o.z += rr.z;
+                            o.w += rr.w;
                         }
-                        *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = o;
+                        *p = o;
                     }
                 } else {
 #pragma unroll
@@ -471,14 +505,16 @@ static int g_num_sms = 0;
 
 template <int E, bool AM, bool BM>
 static int launch_2sm(cudaLaunchConfig_t& lc, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
-                      const __nv_bfloat16* b, const void* aux, int M, int N, int K, int k_splits) {
+                      const CUtensorMap& tR, const __nv_bfloat16* b, const void* aux, int M, int N, int K,
+                      int k_splits) {
     static bool attr = false;
     if (!attr) {
         RS_CUDA(cudaFuncSetAttribute(gemm_bf16_2sm_kernel<E, AM, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     G2_SMEM));
+                                     G2Cfg<E>::smem));
         attr = true;
     }
-    RS_CUDA(cudaLaunchKernelEx(&lc, gemm_bf16_2sm_kernel<E, AM, BM>, tA, tB, tC, b, aux, M, N, K, N, k_splits));
+    lc.dynamicSmemBytes = G2Cfg<E>::smem;
+    RS_CUDA(cudaLaunchKernelEx(&lc, gemm_bf16_2sm_kernel<E, AM, BM>, tA, tB, tC, tR, b, aux, M, N, K, N, k_splits));
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
@@ -500,7 +536,7 @@ int gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux
         RS_CUDA(cudaGetDevice(&dev));
         RS_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
-    CUtensorMap tA, tB, tC;
+    CUtensorMap tA, tB, tC, tR;
     if (a_mn)
         RS_TRY(make_tmap_bf16(&tA, A, (uint64_t)K, (uint64_t)M, (uint64_t)M * 2, G2_BK, 64));
     else
@@ -517,6 +553,11 @@ int gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux
     else
         RS_TRY(make_tmap_2d(&tC, C, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, crows, (uint64_t)N, (uint64_t)N * 2, 32, 32,
                             CU_TENSOR_MAP_SWIZZLE_64B));
+    if (epi == 2)  // the residual R [M, N] fp32, read in the store's sub-tile geometry
+        RS_TRY(make_tmap_2d(&tR, aux, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)M, (uint64_t)N, (uint64_t)N * 4, 32,
+                            32, CU_TENSOR_MAP_SWIZZLE_128B));
+    else
+        tR = tC;
     const int n_work = (M / G2_BM) * (N / G2_BN) * k_splits;
     int clusters = g_num_sms / 2;
     if (n_work < clusters) clusters = n_work;
@@ -524,7 +565,6 @@ int gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(2 * clusters);
     lc.blockDim = dim3(G_THREADS);
-    lc.dynamicSmemBytes = G2_SMEM;
     lc.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -535,18 +575,18 @@ int gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux
     lc.numAttrs = 1;
     const int sel = epi * 4 + a_mn * 2 + b_mn;
     switch (sel) {
-        case 0 * 4 + 0: return launch_2sm<0, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
-        case 1 * 4 + 0: return launch_2sm<1, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
-        case 2 * 4 + 0: return launch_2sm<2, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
-        case 3 * 4 + 0: return launch_2sm<3, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        case 0 * 4 + 0: return launch_2sm<0, false, false>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
+        case 1 * 4 + 0: return launch_2sm<1, false, false>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
+        case 2 * 4 + 0: return launch_2sm<2, false, false>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
+        case 3 * 4 + 0: return launch_2sm<3, false, false>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
         // backward: dgrad (B MN-major) with bf16 / fp32 / ReLU-mask outputs, wgrad (both MN-major)
-        case 0 * 4 + 1: return launch_2sm<0, false, true>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
-        case 4 * 4 + 1: return launch_2sm<4, false, true>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
-        case 5 * 4 + 1: return launch_2sm<5, false, true>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
-        case 4 * 4 + 3: return launch_2sm<4, true, true>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
-        case 6 * 4 + 3: return launch_2sm<6, true, true>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
-        case 4 * 4 + 0: return launch_2sm<4, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
-        case 6 * 4 + 0: return launch_2sm<6, false, false>(lc, tA, tB, tC, b, aux, M, N, K, k_splits);
+        case 0 * 4 + 1: return launch_2sm<0, false, true>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
+        case 4 * 4 + 1: return launch_2sm<4, false, true>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
+        case 5 * 4 + 1: return launch_2sm<5, false, true>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
+        case 4 * 4 + 3: return launch_2sm<4, true, true>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
+        case 6 * 4 + 3: return launch_2sm<6, true, true>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
+        case 4 * 4 + 0: return launch_2sm<4, false, false>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
+        case 6 * 4 + 0: return launch_2sm<6, false, false>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
         default:
             set_error("gemm_ex: unsupported combination epi=%d a_mn=%d b_mn=%d", epi, a_mn, b_mn);
             return RS_ERR_UNSUPPORTED;
