@@ -182,13 +182,18 @@ int rs_adam_step(float* master_dev, float* m_dev, float* v_dev, float* grad_dev,
 /* ---- building blocks exported for parity tests ---------------------------------
  * C[M,N] (row-major) = epi(A[M,K] . W[N,K]^T + bias[N]) with A/W bf16 K-major.
  * epi: 0 = none, 1 = ReLU, 3 = GELU(tanh) -> C bf16; 2 = + residual R[M,N] -> C, R
- * fp32 (C may alias R: the residual stream is updated in place).
+ * fp32 (C may alias R: the residual stream is updated in place); 7 = as 0 with the last
+ * third of the columns (v of a fused q|k|v projection) written as fp16 (M % 256 == 0).
  * M % 128 == 0, N % 64 == 0, K % 64 == 0 (the ranker's shapes). tcgen05 + TMA. */
 int rs_gemm_bf16(const void* A_dev, const void* W_dev, const void* bias_dev, const void* R_dev,
                  void* C_dev, int32_t M, int32_t N, int32_t K, int32_t epi, void* stream);
-/* Causal multi-head attention over packed qkv [B*S, 3*H*64] bf16 -> out [B*S, H*64]. */
+/* Causal multi-head attention over packed qkv [B*S, 3*H*64] bf16 -> out [B*S, H*64] bf16.
+ * rs_attention_fwd_f16v: the same with the v block of qkv in fp16 (the layout the
+ * ranker forward's QKV GEMM writes); P is then fp16 as well. */
 int rs_attention_fwd(const void* qkv_dev, void* out_dev, int32_t B, int32_t S, int32_t H,
                      void* stream);
+int rs_attention_fwd_f16v(const void* qkv_dev, void* out_dev, int32_t B, int32_t S, int32_t H,
+                          void* stream);
 /* General CTA-pair GEMM used by the backward pass: a_mn / b_mn = operand stored
  * MN-contiguous ([K, M] / [K, N]); epi 4 = fp32 out, 5 = bf16 out * (aux > 0) (ReLU
  * backward, aux bf16 [M, N]), 6 = fp32 split-K partials (C holds k_splits x [M, N]).

@@ -9,13 +9,13 @@
 // 0..t (causal). A group of 4 / n_qt units keeps all its K/V blocks resident in smem
 // (4 x 32 KB); the group's q-tiles are split between two softmax "slots" balanced by
 // block count, and the two slots ping-pong on the tensor core:
-//   warp 0      TMA: Q tiles (double-buffered per slot), K/V blocks of the group (each
-//               buffer refilled for the next group as soon as its last PV retires)
-//   warp 1      MMA: per slot S = Q K_j^T (M=128, N=128) into the slot's TMEM S region,
+//   warp 8      TMA: K/V blocks through a 5-deep ring (the next group's blocks land
+//               while this group works); warps 10, 11: Q tiles of slot 0 / slot 1
+//   warp 9      MMA: per slot S = Q K_j^T (M=128, N=128) into the slot's TMEM S region,
 //               then O += P V_j (M=128, N=64) with P read from TMEM (tcgen05 A operand
 //               in tensor memory) and V as an MN-major smem operand
-//   warp 2      TMEM allocator (512 columns: slot s uses S at 256 s, O at 256 s + 128)
-//   warps 4-7   slot 0 softmax, warps 8-11 slot 1: one query row per thread, the whole
+//   warp 10     also the TMEM allocator (512 columns: slot s uses S at 256 s, O at 256 s + 128)
+//   warps 0-3   slot 0 softmax, warps 4-7 slot 1: one query row per thread, the whole
 //               128-key block in registers; online softmax with a lazily updated row
 //               maximum (O is rescaled in TMEM only when the block max exceeds the running
 //               max by more than 2^8); exponentials split between MUFU ex2 and a
@@ -35,13 +35,22 @@ constexpr int AT_D = 64;
 constexpr int AT_MAXKB = 4;  // S <= 512
 constexpr int AT_BUF = AT_TILE * AT_D * 2;  // 16 KB: one Q tile or one K / V block
 constexpr int AT_THREADS = 384;
-constexpr int AT_SMEM = (2 * 2 + 2 * AT_MAXKB) * AT_BUF + 1024 + 1024;
+// Warp roles. The SM's warp schedulers favour higher warp ids, so the latency-critical
+// control warps sit above the 8 softmax warps (else the MMA issuer starves behind them).
+constexpr int AT_W_KV = 8, AT_W_MMA = 9, AT_W_Q0 = 10;  // + AT_W_Q0 + 1; softmax: warps 0-7
+constexpr int AT_KVB = 5;  // K/V ring depth (one group of <= 4 blocks + a spare)
+// Q [2 slots][2] + K, V [AT_KVB] + barriers (224 KB + 2 KB)
+constexpr int AT_SMEM = (4 + 2 * AT_KVB) * AT_BUF + 1024 + 1024;
 constexpr float AT_RESCALE = 8.0f;  // lazy-rescale threshold (log2 units)
+#ifndef AT_PINGPONG
+#define AT_PINGPONG 0  // strict slot alternation of the exponential pass (measured slower)
+#endif
 
 struct AtBars {
     uint64_t q_full[2][2], q_empty[2][2];
-    uint64_t kv_full[AT_MAXKB], kv_empty[AT_MAXKB];
+    uint64_t kv_full[AT_KVB], kv_empty[AT_KVB];
     uint64_t s_full[2], p_full[2], o_full[2];
+    uint64_t order[2];  // softmax ping-pong: slot s may start its exponentials after order[s]
     uint32_t tmem;
 };
 
@@ -139,15 +148,16 @@ __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_
         : "memory");
 }
 
+template <bool F16V>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tqkv, __nv_bfloat16* __restrict__ out, int B, int S,
-                         int H) {
+                         int H, unsigned long long* __restrict__ trace) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;                  // [slot][buf]
-    uint8_t* sK = sQ + 4 * AT_BUF;       // [AT_MAXKB]
-    uint8_t* sV = sK + AT_MAXKB * AT_BUF;  // [AT_MAXKB]
-    AtBars* bar = reinterpret_cast<AtBars*>(sV + AT_MAXKB * AT_BUF);
+    uint8_t* sQ = smem;                  // [slot][2]
+    uint8_t* sK = sQ + 4 * AT_BUF;       // [AT_KVB]
+    uint8_t* sV = sK + AT_KVB * AT_BUF;  // [AT_KVB]
+    AtBars* bar = reinterpret_cast<AtBars*>(sV + AT_KVB * AT_BUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_qt = (S + AT_TILE - 1) / AT_TILE;
@@ -156,7 +166,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     const int gU = AT_MAXKB / n_qt;  // units per group
     const int n_groups = (n_units + gU - 1) / gU;
 
-    if (warp == 0 && lane == 0) {
+    if (warp == AT_W_KV && lane == 0) {
         tma_prefetch_desc(&tqkv);
         for (int s = 0; s < 2; ++s) {
             for (int q = 0; q < 2; ++q) {
@@ -166,129 +176,168 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             mbar_init(&bar->s_full[s], 1);
             mbar_init(&bar->p_full[s], 4);
             mbar_init(&bar->o_full[s], 1);
+            mbar_init(&bar->order[s], 4);
         }
-        for (int i = 0; i < AT_MAXKB; ++i) {
+        for (int i = 0; i < AT_KVB; ++i) {
             mbar_init(&bar->kv_full[i], 1);
-            // buffer i holds key block j = i % n_qt of its unit: used by n_qt - j q-tiles
-            mbar_init(&bar->kv_empty[i], i < gU * n_qt ? n_qt - i % n_qt : 1);
+            mbar_init(&bar->kv_empty[i], 1);  // committed by the buffer's last PV
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<512>(&bar->tmem);
+    if (warp == AT_W_Q0) tmem_alloc<512>(&bar->tmem);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bar->tmem;
 
-    if (warp == 0) {
+    // K/V blocks stream through a ring of AT_KVB buffers in load order: load n of this CTA
+    // (group gi, block j from n_qt - 1 down to 0, unit k) goes to buffer n % AT_KVB, so the
+    // next group's first blocks land while this group still works (the ring holds one
+    // group plus a spare). Q is single-buffered per slot; its next tile loads as soon as
+    // the current tile's last S retires (a softmax + PV ahead of its use).
+    auto kv_seq = [&](int gi, int U, int k, int j) { return gi * gU * n_qt + (n_qt - 1 - j) * U + k; };
+    if (warp == AT_W_KV) {
         if (elect_one()) {
-            int tseq[2] = {0, 0};
-            auto load_q = [&](int s, int unit, int t) {
-                const int qb = tseq[s] & 1;
-                mbar_wait(&bar->q_empty[s][qb], ((tseq[s] >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(&bar->q_full[s][qb], AT_BUF);
-                const int b = unit / H, h = unit % H;
-                tma_load_2d(sQ + (s * 2 + qb) * AT_BUF, &tqkv, &bar->q_full[s][qb], h * AT_D, b * S + t * AT_TILE);
-                ++tseq[s];
-            };
             int gi = 0;
             for (int g = blockIdx.x; g < n_groups; g += gridDim.x, ++gi) {
                 const int U = min(gU, n_units - g * gU);
-                int k, t;
-#pragma unroll
-                for (int s = 0; s < 2; ++s)
-                    if (at_slot_tile(n_qt, U, s, 0, k, t)) load_q(s, g * gU + k, t);
                 for (int j = n_qt - 1; j >= 0; --j)
                     for (int kk = 0; kk < U; ++kk) {
-                        const int buf = kk * n_qt + j;
+                        const int n = kv_seq(gi, U, kk, j);
+                        const int buf = n % AT_KVB;
                         const int unit = g * gU + kk;
                         const int b = unit / H, h = unit % H;
-                        mbar_wait(&bar->kv_empty[buf], (gi & 1) ^ 1);
+                        mbar_wait(&bar->kv_empty[buf], ((n / AT_KVB) & 1) ^ 1);
                         mbar_arrive_expect_tx(&bar->kv_full[buf], 2 * AT_BUF);
                         tma_load_2d(sK + buf * AT_BUF, &tqkv, &bar->kv_full[buf], dm + h * AT_D, b * S + j * AT_TILE);
                         tma_load_2d(sV + buf * AT_BUF, &tqkv, &bar->kv_full[buf], 2 * dm + h * AT_D,
                                     b * S + j * AT_TILE);
                     }
-                for (int i = 1; i < AT_MAXKB; ++i)
-#pragma unroll
-                    for (int s = 0; s < 2; ++s)
-                        if (at_slot_tile(n_qt, U, s, i, k, t)) load_q(s, g * gU + k, t);
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == AT_W_Q0 || warp == AT_W_Q0 + 1) {
+        // Q producer for slot warp - AT_W_Q0
+        const int s = warp - AT_W_Q0;
+        if (elect_one()) {
+            int tq = 0;
+            for (int g = blockIdx.x; g < n_groups; g += gridDim.x) {
+                const int U = min(gU, n_units - g * gU);
+                int k, t;
+                for (int i = 0; at_slot_tile(n_qt, U, s, i, k, t); ++i, ++tq) {
+                    const int unit = g * gU + k;
+                    const int b = unit / H, h = unit % H;
+                    const int qb = tq & 1;
+                    mbar_wait(&bar->q_empty[s][qb], ((tq >> 1) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&bar->q_full[s][qb], AT_BUF);
+                    tma_load_2d(sQ + (s * 2 + qb) * AT_BUF, &tqkv, &bar->q_full[s][qb], h * AT_D, b * S + t * AT_TILE);
+                }
+            }
+        }
+    } else if (warp == AT_W_MMA) {
         if (elect_one()) {
             constexpr uint32_t id_s = idesc_bf16(AT_TILE, AT_TILE);
-            constexpr uint32_t id_o = idesc_bf16(AT_TILE, AT_D, 0, 1);
-            int tseq[2] = {0, 0}, bseq[2] = {0, 0};
+            // PV: bf16 P x bf16 V, or fp16 P x fp16 V (N = 64)
+            constexpr uint32_t id_o = F16V ? (idesc_bf16(AT_TILE, AT_D, 0, 1) & ~((7u << 7) | (7u << 10)))
+                                           : idesc_bf16(AT_TILE, AT_D, 0, 1);
+            // All MMA-issuer state stays in registers: with ~225 KB of shared memory the L1
+            // left for local memory is tiny, and a spilled / dynamically indexed array costs
+            // an L2 round trip per access on this latency-critical path.
+            struct Slot {
+                int tseq, bseq;  // tiles / blocks issued so far
+                int i, k, t, j;  // tile index in the group's list, its unit, q-tile, block
+                bool live;
+            };
+            Slot s0{0, 0, 0, 0, 0, 0, false}, s1{0, 0, 0, 0, 0, 0, false};
+            uint32_t uses = 0;  // PVs still to read each K/V buffer, 4 bits per ring slot
             int gi = 0;
             for (int g = blockIdx.x; g < n_groups; g += gridDim.x, ++gi) {
                 const int U = min(gU, n_units - g * gU);
-                // per-slot cursor: tile index i, its unit k / q-tile t, current block j
-                int ci[2] = {0, 0}, ck[2], ct[2], cj[2];
-                bool live[2];
-#pragma unroll
-                for (int s = 0; s < 2; ++s) {
-                    live[s] = at_slot_tile(n_qt, U, s, 0, ck[s], ct[s]);
-                    cj[s] = ct[s];
-                }
-                auto issue_s = [&](int s) {
-                    const int qb = tseq[s] & 1;
-                    const int buf = ck[s] * n_qt + cj[s];
-                    if (cj[s] == ct[s]) mbar_wait(&bar->q_full[s][qb], (tseq[s] >> 1) & 1);
-                    mbar_wait(&bar->kv_full[buf], gi & 1);
+                for (int j = 0; j < n_qt; ++j)
+                    for (int kk = 0; kk < U; ++kk) {
+                        const int b4 = 4 * (kv_seq(gi, U, kk, j) % AT_KVB);
+                        uses = (uses & ~(15u << b4)) | ((uint32_t)(n_qt - j) << b4);
+                    }
+                auto start = [&](Slot& c, int slot) {
+                    c.i = 0;
+                    c.live = at_slot_tile(n_qt, U, slot, 0, c.k, c.t);
+                    c.j = c.t;
+                };
+                auto issue_s = [&](Slot& c, int slot) {
+                    const int n = kv_seq(gi, U, c.k, c.j);
+                    const int buf = n % AT_KVB;
+                    const int qb = c.tseq & 1;
+                    if (c.j == c.t) mbar_wait(&bar->q_full[slot][qb], (c.tseq >> 1) & 1);
+                    mbar_wait(&bar->kv_full[buf], (n / AT_KVB) & 1);
                     tc_fence_after();
-                    const uint32_t qa = smem_u32(sQ + (s * 2 + qb) * AT_BUF);
+                    const uint32_t qa = smem_u32(sQ + (slot * 2 + qb) * AT_BUF);
                     const uint32_t ka = smem_u32(sK + buf * AT_BUF);
 #pragma unroll
                     for (int kk = 0; kk < AT_D / 16; ++kk)
-                        mma_bf16_ss(tmem + s * 256, desc_kmajor_sw128(qa + kk * 32), desc_kmajor_sw128(ka + kk * 32),
-                                    id_s, kk != 0);
-                    mma_commit(&bar->s_full[s]);
-                    if (cj[s] == 0) mma_commit(&bar->q_empty[s][qb]);  // last S of the tile
+                        mma_bf16_ss(tmem + slot * 256, desc_kmajor_sw128(qa + kk * 32),
+                                    desc_kmajor_sw128(ka + kk * 32), id_s, kk != 0);
+                    mma_commit(&bar->s_full[slot]);
+                    if (c.j == 0) mma_commit(&bar->q_empty[slot][qb]);  // last S of the tile
                 };
+                auto issue_pv = [&](Slot& c, int slot) {
+                    const int buf = kv_seq(gi, U, c.k, c.j) % AT_KVB;
+                    ++c.bseq;
+                    tc_fence_after();
+                    const uint32_t vb = smem_u32(sV + buf * AT_BUF);
 #pragma unroll
-                for (int s = 0; s < 2; ++s)
-                    if (live[s]) issue_s(s);
-                while (live[0] || live[1]) {
-                    // issue for whichever slot's P is ready first (no head-of-line blocking:
-                    // the two slots settle into ping-pong on their own)
-                    int s = -1;
-                    while (s < 0) {
-                        if (live[0] && mbar_try_wait(&bar->p_full[0], bseq[0] & 1)) s = 0;
-                        else if (live[1] && mbar_try_wait(&bar->p_full[1], bseq[1] & 1)) s = 1;
+                    for (int kk = 0; kk < AT_TILE / 16; ++kk)
+                        mma_bf16_ts(tmem + slot * 256 + 128, tmem + slot * 256 + kk * 8,
+                                    desc_mnmajor_sw128(vb + kk * 2048, 8192), id_o, (c.j != c.t) || kk != 0);
+                    uses -= 1u << (4 * buf);
+                    if (((uses >> (4 * buf)) & 15u) == 0) mma_commit(&bar->kv_empty[buf]);
+                    if (c.j == 0) {  // tile done: O is final once this PV retires
+                        mma_commit(&bar->o_full[slot]);
+                        ++c.tseq;
+                        ++c.i;
+                        c.live = at_slot_tile(n_qt, U, slot, c.i, c.k, c.t);
+                        c.j = c.t;
+                    } else {
+                        --c.j;
                     }
-                    {
-                        const int buf = ck[s] * n_qt + cj[s];
-                        ++bseq[s];
-                        tc_fence_after();
-                        const uint32_t vb = smem_u32(sV + buf * AT_BUF);
-#pragma unroll
-                        for (int kk = 0; kk < AT_TILE / 16; ++kk)
-                            mma_bf16_ts(tmem + s * 256 + 128, tmem + s * 256 + kk * 8,
-                                        desc_mnmajor_sw128(vb + kk * 2048, 8192), id_o, (cj[s] != ct[s]) || kk != 0);
-                        mma_commit(&bar->kv_empty[buf]);
-                        if (cj[s] == 0) {  // tile done: O is final once this PV retires
-                            mma_commit(&bar->o_full[s]);
-                            ++tseq[s];
-                            ++ci[s];
-                            live[s] = at_slot_tile(n_qt, U, s, ci[s], ck[s], ct[s]);
-                            cj[s] = ct[s];
-                        } else {
-                            --cj[s];
-                        }
-                        if (live[s]) issue_s(s);
-                    }
+                    if (c.live) issue_s(c, slot);
+                };
+                start(s0, 0);
+                start(s1, 1);
+                if (s0.live) issue_s(s0, 0);
+                if (s1.live) issue_s(s1, 1);
+                while (s0.live || s1.live) {
+                    // issue for whichever slot's P is ready first (no head-of-line blocking)
+                    // (test_wait: try_wait may park the thread on one barrier while the other
+                    // slot is ready)
+                    if (s0.live && mbar_test_wait(&bar->p_full[0], s0.bseq & 1))
+                        issue_pv(s0, 0);
+                    else if (s1.live && mbar_test_wait(&bar->p_full[1], s1.bseq & 1))
+                        issue_pv(s1, 1);
                 }
             }
         }
-    } else if (warp >= 4) {
-        const int s = (warp - 4) >> 2;  // slot
+    } else if (warp < 8) {
+        const int s = warp >> 2;         // slot
         const int q4 = warp & 3;         // TMEM lane quarter
         const int r = q4 * 32 + lane;    // query row within the tile == TMEM lane
         const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
         const uint32_t tS = tmem + s * 256 + lane_addr, tO = tS + 128;
         const float c = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
         const uint64_t c2 = f2pack(c, c);
+        // The two slots take turns on the exponential pass (MUFU-bound): slot 0's n-th pass,
+        // then slot 1's n-th, then slot 0's (n+1)-th ... so one slot's exponentials overlap
+        // the other slot's MMAs instead of both slots contending and then idling together.
+        // Alternation stops at the shorter slot's block count (the last group may be uneven).
+        int n_alt = 0;
+        {
+            int tot[2] = {0, 0};
+            for (int g = blockIdx.x; g < n_groups; g += gridDim.x) {
+                const int U = min(gU, n_units - g * gU);
+                int k, t;
+                for (int ss = 0; ss < 2; ++ss)
+                    for (int i = 0; at_slot_tile(n_qt, U, ss, i, k, t); ++i) tot[ss] += t + 1;
+            }
+            n_alt = AT_PINGPONG ? min(tot[0], tot[1]) : 0;
+        }
         int tseq = 0, bseq = 0;
         for (int g = blockIdx.x; g < n_groups; g += gridDim.x) {
             const int U = min(gU, n_units - g * gU);
@@ -298,7 +347,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                 const int b = unit / H, h = unit % H;
                 float m_run = 0.f, l = 0.f;
                 for (int j = t; j >= 0; --j, ++bseq) {
+                    const bool trs = trace != nullptr && blockIdx.x == 0 && (warp & 3) == 0 && lane == 0 && bseq < 64;
+                    if (trs) trace[(s * 64 + bseq) * 4 + 0] = clock64();
                     mbar_wait(&bar->s_full[s], bseq & 1);
+                    if (trs) trace[(s * 64 + bseq) * 4 + 1] = clock64();
                     tc_fence_after();
                     // pass 1: row max over the block, 32 columns at a time (a whole row in
                     // registers would leave ptxas no room for ILP; TMEM loads are cheap)
@@ -306,13 +358,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                     float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc) {
+                        // diagonal block: chunks past this warp's 32 rows are fully masked, the
+                        // chunk on its rows is masked per lane (key e valid iff e <= lane)
+                        if (diag && cc > q4) break;
                         uint32_t v[32];
                         tmem_ld_32x32b_x32(tS + cc * 32, v);
                         tmem_ld_wait();
-                        if (diag) {
+                        if (diag && cc == q4) {
 #pragma unroll
                             for (int e = 0; e < 32; ++e)
-                                if (cc * 32 + e > r) v[e] = __float_as_uint(-INFINITY);
+                                if (e > lane) v[e] = __float_as_uint(-INFINITY);
                         }
 #pragma unroll
                         for (int e = 0; e < 32; e += 8)
@@ -329,41 +384,54 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                         alpha = exp2_mufu(m_run - mb);
                         m_run = mb;
                     }
+                    if (trs) trace[(s * 64 + bseq) * 4 + 2] = clock64();
                     // pass 2: P = 2^(s c - m_run), bf16 pairs over the first 64 S columns (the
                     // PV MMA's A operand; chunk cc's 16 P columns lie in S columns already read)
+                    if (bseq < n_alt && (s == 1 || bseq > 0))
+                        mbar_wait(&bar->order[s], (s == 0 ? bseq - 1 : bseq) & 1);
                     const uint64_t nm2 = f2pack(-m_run, -m_run);
                     uint64_t lsum[4] = {f2pack(0.f, 0.f), f2pack(0.f, 0.f), f2pack(0.f, 0.f), f2pack(0.f, 0.f)};
 #pragma unroll
                     for (int cc = 0; cc < 4; ++cc) {
+                        uint32_t pk[16];
+                        if (diag && cc > q4) {  // fully masked: P = 0
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) pk[e] = 0u;
+                            tmem_st_32x32b_x16(tS + cc * 16, pk);
+                            continue;
+                        }
                         uint32_t v[32];
                         tmem_ld_32x32b_x32(tS + cc * 32, v);
                         tmem_ld_wait();
-                        if (diag) {
+                        if (diag && cc == q4) {
 #pragma unroll
                             for (int e = 0; e < 32; ++e)
-                                if (cc * 32 + e > r) v[e] = __float_as_uint(-INFINITY);
+                                if (e > lane) v[e] = __float_as_uint(-INFINITY);
                         }
-                        uint32_t pk[16];
 #pragma unroll
                         for (int e = 0; e < 32; e += 2) {
-                            float x0, x1, p0, p1;
+                            float x0, x1;
                             f2unpack(ffma2(f2pack(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), c2, nm2), x0, x1);
-                            if ((e & 2) == 0) {
+                            float p0, p1;
+                            if ((e & 2) == 0) {  // half on MUFU, half on the FMA pipe
                                 p0 = exp2_mufu(x0);
                                 p1 = exp2_mufu(x1);
                             } else {
                                 exp2_poly2(x0, x1, p0, p1);
                             }
                             lsum[(e >> 1) & 3] = fadd2(lsum[(e >> 1) & 3], f2pack(p0, p1));
-                            pk[e / 2] = pack_bf16(p0, p1);
+                            pk[e / 2] = F16V ? pack_f16(p0, p1) : pack_bf16(p0, p1);
                         }
                         tmem_st_32x32b_x16(tS + cc * 16, pk);
                     }
-                    float l0, l1;
-                    f2unpack(fadd2(fadd2(lsum[0], lsum[1]), fadd2(lsum[2], lsum[3])), l0, l1);
-                    l = l * alpha + l0 + l1;
+                    {
+                        float l0, l1;
+                        f2unpack(fadd2(fadd2(lsum[0], lsum[1]), fadd2(lsum[2], lsum[3])), l0, l1);
+                        l = l * alpha + l0 + l1;
+                    }
                     if (__any_sync(0xffffffffu, alpha != 1.f)) {
-                        // O holds PV of the earlier blocks (retired: the S commit covers them)
+                        // O holds PV of the earlier blocks,
+                        // retired: the S commit covers them
 #pragma unroll
                         for (int hh = 0; hh < 2; ++hh) {
                             uint32_t o[32];
@@ -377,7 +445,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                     tmem_st_wait();
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&bar->p_full[s]);
+                    if (lane == 0) {
+                        mbar_arrive(&bar->p_full[s]);
+                        if (bseq < n_alt) mbar_arrive(&bar->order[s ^ 1]);
+                    }
+                    if (trs) trace[(s * 64 + bseq) * 4 + 3] = clock64();
                 }
                 // epilogue: O / l -> bf16 rows of `out`
                 mbar_wait(&bar->o_full[s], tseq & 1);
@@ -404,35 +476,60 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 2) tmem_dealloc<512>(tmem);
+    if (warp == AT_W_Q0) tmem_dealloc<512>(tmem);
 }
 
-static int g_at_sms = 0;
-
-int attention_fwd(const void* qkv, void* out, int B, int S, int H, cudaStream_t st) {
-    RS_CHECK_ARG(B > 0 && S > 0 && H > 0, "attention: empty shape");
-    RS_CHECK_ARG(S <= AT_TILE * AT_MAXKB, "attention: S=%d > %d not supported", S, AT_TILE * AT_MAXKB);
-    if (g_at_sms == 0) {
+template <bool F16V>
+static int launch_attention(const void* qkv, void* out, int B, int S, int H, unsigned long long* trace,
+                            cudaStream_t st) {
+    static int sms = 0;
+    if (sms == 0) {
         int dev;
         RS_CUDA(cudaGetDevice(&dev));
-        RS_CUDA(cudaDeviceGetAttribute(&g_at_sms, cudaDevAttrMultiProcessorCount, dev));
-        RS_CUDA(cudaFuncSetAttribute(attention_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM));
+        RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        RS_CUDA(cudaFuncSetAttribute(attention_fwd_kernel<F16V>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM));
     }
     const uint64_t rows = (uint64_t)B * S;
     const uint64_t cols = (uint64_t)3 * H * AT_D;
     CUtensorMap m;
-    RS_TRY(make_tmap_bf16(&m, qkv, rows, cols, cols * 2, AT_TILE, AT_D));
+    RS_TRY(make_tmap_bf16(&m, qkv, rows, cols, cols * 2, AT_TILE, AT_D));  // 16-bit elements; V may be fp16
     const int n_qt = (S + AT_TILE - 1) / AT_TILE;
     const int gU = AT_MAXKB / n_qt;
     const int n_groups = (B * H + gU - 1) / gU;
-    const int grid = n_groups < g_at_sms ? n_groups : g_at_sms;
-    attention_fwd_kernel<<<grid, AT_THREADS, AT_SMEM, st>>>(m, static_cast<__nv_bfloat16*>(out), B, S, H);
+    const int grid = n_groups < sms ? n_groups : sms;
+    attention_fwd_kernel<F16V><<<grid, AT_THREADS, AT_SMEM, st>>>(m, static_cast<__nv_bfloat16*>(out), B, S, H, trace);
     RS_LAUNCH_CHECK();
     return RS_OK;
+}
+
+int attention_fwd_impl(const void* qkv, void* out, int B, int S, int H, int v_f16, unsigned long long* trace,
+                       cudaStream_t st) {
+    RS_CHECK_ARG(B > 0 && S > 0 && H > 0, "attention: empty shape");
+    RS_CHECK_ARG(S <= AT_TILE * AT_MAXKB, "attention: S=%d > %d not supported", S, AT_TILE * AT_MAXKB);
+    return v_f16 ? launch_attention<true>(qkv, out, B, S, H, trace, st)
+                 : launch_attention<false>(qkv, out, B, S, H, trace, st);
+}
+
+int attention_fwd(const void* qkv, void* out, int B, int S, int H, cudaStream_t st) {
+    return attention_fwd_impl(qkv, out, B, S, H, 0, nullptr, st);
+}
+int attention_fwd_f16v(const void* qkv, void* out, int B, int S, int H, cudaStream_t st) {
+    return attention_fwd_impl(qkv, out, B, S, H, 1, nullptr, st);
 }
 
 }  // namespace rs
 
 extern "C" int rs_attention_fwd(const void* qkv, void* out, int32_t B, int32_t S, int32_t H, void* stream) {
     return rs::attention_fwd(qkv, out, B, S, H, rs::as_stream(stream));
+}
+
+extern "C" int rs_attention_fwd_f16v(const void* qkv, void* out, int32_t B, int32_t S, int32_t H, void* stream) {
+    return rs::attention_fwd_f16v(qkv, out, B, S, H, rs::as_stream(stream));
+}
+
+// Diagnostics only (tools/attn_trace.py): CTA 0 timeline, trace[0..511] softmax phases,
+// trace[1024..1279] MMA issue times.
+extern "C" __attribute__((visibility("default"))) int rs_attention_fwd_trace(const void* qkv, void* out, int32_t B, int32_t S, int32_t H,
+                                      unsigned long long* trace, void* stream) {
+    return rs::attention_fwd_impl(qkv, out, B, S, H, 1, trace, rs::as_stream(stream));
 }

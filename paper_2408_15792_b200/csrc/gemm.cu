@@ -227,13 +227,14 @@ struct G2Cfg {
 
 // EPI: 0 bf16, 1 ReLU->bf16, 2 +fp32 residual->fp32, 3 GELU->bf16, 4 fp32 (bias optional),
 // 5 bf16 * (mask > 0) with the bf16 mask in `aux` (ReLU backward), 6 fp32 split-K partial
-// (slice `split` of C). A_MN / B_MN: operand stored MN-contiguous ([K, M] / [K, N]).
+// (slice `split` of C), 7 = 0 with the last third of the columns (the V block of a fused
+// q|k|v projection) in fp16. A_MN / B_MN: operand stored MN-contiguous ([K, M] / [K, N]).
 template <int EPI, bool A_MN = false, bool B_MN = false>
 __global__ void __launch_bounds__(G_THREADS, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                          const __grid_constant__ CUtensorMap tC, const __grid_constant__ CUtensorMap tR,
                          const __nv_bfloat16* __restrict__ bias, const void* __restrict__ aux, int M, int N, int K,
-                         int ldc, int k_splits) {
+                         int ldc, int k_splits, int f16_col0) {
     constexpr int G2_STAGES = G2Cfg<EPI>::stages;
     constexpr int NBUF = G2Cfg<EPI>::nbuf;
     extern __shared__ uint8_t smem_raw[];
@@ -472,11 +473,19 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                         if (EPI == 3) v[j] = gelu_tanh(v[j]);
                     }
                     // bf16 32x32 sub-tile, 64-B rows, SWIZZLE_64B: chunk j ^ ((row / 2) % 4)
+                    if (EPI == 7 && n0 >= f16_col0) {  // fp16 columns (the attention V operand)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                        *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
-                            make_uint4(pack_bf16(v[j * 8 + 0], v[j * 8 + 1]), pack_bf16(v[j * 8 + 2], v[j * 8 + 3]),
-                                       pack_bf16(v[j * 8 + 4], v[j * 8 + 5]), pack_bf16(v[j * 8 + 6], v[j * 8 + 7]));
+                        for (int j = 0; j < 4; ++j)
+                            *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                                make_uint4(pack_f16(v[j * 8 + 0], v[j * 8 + 1]), pack_f16(v[j * 8 + 2], v[j * 8 + 3]),
+                                           pack_f16(v[j * 8 + 4], v[j * 8 + 5]), pack_f16(v[j * 8 + 6], v[j * 8 + 7]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            *reinterpret_cast<uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+                                make_uint4(pack_bf16(v[j * 8 + 0], v[j * 8 + 1]), pack_bf16(v[j * 8 + 2], v[j * 8 + 3]),
+                                           pack_bf16(v[j * 8 + 4], v[j * 8 + 5]), pack_bf16(v[j * 8 + 6], v[j * 8 + 7]));
+                    }
                 }
                 fence_proxy_async_smem();
                 __syncwarp();
@@ -514,7 +523,8 @@ static int launch_2sm(cudaLaunchConfig_t& lc, const CUtensorMap& tA, const CUten
         attr = true;
     }
     lc.dynamicSmemBytes = G2Cfg<E>::smem;
-    RS_CUDA(cudaLaunchKernelEx(&lc, gemm_bf16_2sm_kernel<E, AM, BM>, tA, tB, tC, tR, b, aux, M, N, K, N, k_splits));
+    RS_CUDA(cudaLaunchKernelEx(&lc, gemm_bf16_2sm_kernel<E, AM, BM>, tA, tB, tC, tR, b, aux, M, N, K, N, k_splits,
+                               (2 * N) / 3));
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
@@ -527,7 +537,8 @@ int gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux
                  int epi, int a_mn, int b_mn, int k_splits, cudaStream_t st) {
     RS_CHECK_ARG(M > 0 && N > 0 && K > 0 && M % G2_BM == 0 && N % G2_BN == 0 && K % G2_BK == 0,
                  "gemm_ex: need M, N %% 256 == 0 and K %% 64 == 0 (got %d %d %d)", M, N, K);
-    RS_CHECK_ARG(epi >= 0 && epi <= 6, "gemm_ex: bad epilogue %d", epi);
+    RS_CHECK_ARG(epi >= 0 && epi <= 7, "gemm_ex: bad epilogue %d", epi);
+    RS_CHECK_ARG(epi != 7 || ((2 * N) / 3) % G2_BN == 0, "gemm_ex: epilogue 7 needs 2N/3 %% 256 == 0");
 
     RS_CHECK_ARG((epi != 2 && epi != 5) || aux != nullptr, "gemm_ex: epilogue %d needs aux", epi);
     RS_CHECK_ARG(k_splits >= 1 && (epi == 6 || k_splits == 1), "gemm_ex: split-K needs epilogue 6");
@@ -579,6 +590,7 @@ int gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux
         case 1 * 4 + 0: return launch_2sm<1, false, false>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
         case 2 * 4 + 0: return launch_2sm<2, false, false>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
         case 3 * 4 + 0: return launch_2sm<3, false, false>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
+        case 7 * 4 + 0: return launch_2sm<7, false, false>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
         // backward: dgrad (B MN-major) with bf16 / fp32 / ReLU-mask outputs, wgrad (both MN-major)
         case 0 * 4 + 1: return launch_2sm<0, false, true>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
         case 4 * 4 + 1: return launch_2sm<4, false, true>(lc, tA, tB, tC, tR, b, aux, M, N, K, k_splits);
@@ -598,7 +610,7 @@ int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, voi
     RS_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty shape");
     RS_CHECK_ARG(M % G_BM == 0 && N % G_BN == 0 && K % G_BK == 0,
                  "gemm: need M %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (got %d %d %d)", M, N, K);
-    RS_CHECK_ARG(epi >= 0 && epi <= 3, "gemm: bad epilogue %d", epi);
+    RS_CHECK_ARG(epi >= 0 && epi <= 3 || epi == 7, "gemm: bad epilogue %d", epi);
     RS_CHECK_ARG(bias != nullptr, "gemm: bias is required");
     RS_CHECK_ARG(epi != 2 || R != nullptr, "gemm: residual epilogue needs R");
     if (g_num_sms == 0) {
@@ -608,6 +620,7 @@ int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, voi
     }
     if (M % G2_BM == 0 && N % G2_BN == 0)  // CTA-pair kernel (the ranker pads M to 256)
         return gemm_bf16_ex(A, W, bias, R, C, M, N, K, epi, 0, 0, 1, st);
+    RS_CHECK_ARG(epi != 7, "gemm: epilogue 7 needs M %% 256 == 0");
     CUtensorMap tA, tB;
     RS_TRY(make_tmap_bf16(&tA, A, (uint64_t)M, (uint64_t)K, (uint64_t)K * 2, G_BM, G_BK));
     RS_TRY(make_tmap_bf16(&tB, W, (uint64_t)N, (uint64_t)K, (uint64_t)K * 2, G_BN, G_BK));

@@ -9,11 +9,13 @@
 // then g = w . LNf(h[last]) + b. Embedding h0 = E[ids] + P[pos + 2] (OPT's learned
 // positions carry an offset of 2).
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include "common.cuh"
 #include "gemm.cuh"
 
 namespace rs {
 int attention_fwd(const void* qkv, void* out, int B, int S, int H, cudaStream_t st);
+int attention_fwd_f16v(const void* qkv, void* out, int B, int S, int H, cudaStream_t st);
 
 constexpr float LN_EPS = 1e-5f;
 
@@ -217,9 +219,10 @@ __global__ void __launch_bounds__(32 * AL_WARPS)
     l = warp_sum(l);
     __syncwarp();
     float2 o = make_float2(0.f, 0.f);
-    const __nv_bfloat162* vcol = reinterpret_cast<const __nv_bfloat162*>(base + 2 * d) + lane;
+    // V is fp16 in the forward's q|k|v activation (QKV GEMM epilogue 7)
+    const __half2* vcol = reinterpret_cast<const __half2*>(base + 2 * d) + lane;
     for (int j = 0; j <= lp; ++j) {
-        const float2 v = __bfloat1622float2(vcol[(size_t)j * (ld / 2)]);
+        const float2 v = __half22float2(vcol[(size_t)j * (ld / 2)]);
         const float p = sc[j];
         o.x = fmaf(p, v.x, o.x);
         o.y = fmaf(p, v.y, o.y);
@@ -437,7 +440,8 @@ extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params
         for (int l = 0; l < cfg->n_layers; ++l) {
             const __nv_bfloat16* L = P + o.per_layer0 + (int64_t)l * o.layer_stride;
             RS_TRY(launch_ln(w.h, L + o.ln1_w, L + o.ln1_b, w.x, mp, d, st));
-            RS_TRY(gemm_bf16(w.x, L + o.qkv_w, L + o.qkv_b, nullptr, w.qkv, mp, 3 * d, d, 0, st));
+            // q, k bf16 and v fp16 (the attention's PV runs in fp16, see attention.cu)
+            RS_TRY(gemm_bf16(w.x, L + o.qkv_w, L + o.qkv_b, nullptr, w.qkv, mp, 3 * d, d, 7, st));
             if (l == cfg->n_layers - 1) {
                 // only the last token of each prompt reaches the head: finish the layer on
                 // bc rows (exact; saves 20 d^2 (S - 1) FLOPs per prompt)
@@ -449,7 +453,7 @@ extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params
                 RS_TRY(gemm_bf16(w.f_last, L + o.fc2_w, L + o.fc2_b, w.h_last, w.h_last, bp, d, F, 2, st));
                 break;
             }
-            RS_TRY(attention_fwd(w.qkv, w.att, bc, S, H, st));
+            RS_TRY(attention_fwd_f16v(w.qkv, w.att, bc, S, H, st));
             RS_TRY(gemm_bf16(w.att, L + o.out_w, L + o.out_b, w.h, w.h, mp, d, d, 2, st));
             RS_TRY(launch_ln(w.h, L + o.ln2_w, L + o.ln2_b, w.x, mp, d, st));
             RS_TRY(gemm_bf16(w.x, L + o.fc1_w, L + o.fc1_b, nullptr, w.ffn, mp, F, d, cfg->activation == 0 ? 1 : 3, st));

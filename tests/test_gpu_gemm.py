@@ -103,3 +103,22 @@ def test_wgrad_matches_fp32(T, Nf, Kin, splits):
     C = _gemm_ex(dY, X, None, Nf, Kin, T, epi, 1, 1, splits)
     got = C.view(splits, Nf, Kin).sum(0) if splits > 1 else C
     assert (got - ref).abs().max().item() <= 1e-2 * max(1.0, ref.abs().max().item())
+
+
+def test_gemm_qkv_f16_v_epilogue():
+    """Epilogue 7: bf16 q|k columns, fp16 v columns (the last third)."""
+    from paper_2408_15792_b200 import _lib
+    _lib.device()
+    M, N, K = 512, 2304, 768
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randn(M, K, device="cuda", generator=g).bfloat16()
+    W = (torch.randn(N, K, device="cuda", generator=g) * 0.05).bfloat16()
+    b = (torch.randn(N, device="cuda", generator=g) * 0.1).bfloat16()
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    _lib.check(_lib.load().rs_gemm_bf16(A.data_ptr(), W.data_ptr(), b.data_ptr(), None, C.data_ptr(), M, N, K, 7,
+                                        _lib.stream_handle()))
+    ref = A.float() @ W.float().t() + b.float()
+    qk = C[:, :2 * N // 3].float()
+    v = C[:, 2 * N // 3:].view(torch.float16).float()
+    torch.testing.assert_close(qk, ref[:, :2 * N // 3], rtol=2e-2, atol=2e-2)
+    torch.testing.assert_close(v, ref[:, 2 * N // 3:], rtol=2e-3, atol=2e-3)

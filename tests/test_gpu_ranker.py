@@ -32,6 +32,26 @@ def test_attention_matches_fp32(B, S, H):
     assert err < 2e-2, err
 
 
+@pytest.mark.parametrize("B,S,H", [(1, 128, 1), (2, 64, 12), (3, 200, 12), (4, 512, 12), (37, 128, 12),
+                                   (2, 384, 2), (5, 100, 12)])
+def test_attention_f16v_matches_fp32(B, S, H):
+    """The ranker forward's layout: q, k bf16 and v fp16 in one [B*S, 3*H*64] buffer
+    (QKV GEMM epilogue 7); P is fp16 and the row sums come from the PV MMA."""
+    from paper_2408_15792_b200 import _lib
+    _lib.device()
+    g = torch.Generator(device="cuda").manual_seed(B * S + H + 7)
+    x = torch.randn(B * S, 3 * H * 64, device="cuda", generator=g) * 1.5
+    qkv = x.bfloat16()
+    d = H * 64
+    qkv[:, 2 * d:] = x[:, 2 * d:].half().view(torch.bfloat16)
+    out = torch.full((B * S, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+    _lib.check(_lib.load().rs_attention_fwd_f16v(qkv.data_ptr(), out.data_ptr(), B, S, H, _lib.stream_handle()))
+    ref_in = torch.cat([qkv[:, :2 * d].float(), qkv[:, 2 * d:].view(torch.float16).float()], 1)
+    ref = _attn_ref(ref_in, B, S, H)
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2, err
+
+
 @pytest.mark.parametrize("n_layers,B,S", [(1, 2, 128), (2, 8, 64), (2, 3, 100)])
 def test_ranker_small_matches_oracle(n_layers, B, S):
     from paper_2408_15792_b200.ranker import OptRanker, RankerConfig

@@ -11,6 +11,6 @@ _lib.device()
 qkv = torch.randn(B * S, 2304, device="cuda").bfloat16()
 out = torch.empty(B * S, 768, device="cuda").bfloat16()
 for _ in range(reps):
-    _lib.check(_lib.load().rs_attention_fwd(qkv.data_ptr(), out.data_ptr(), B, S, 12, _lib.stream_handle()))
+    _lib.check(_lib.load().rs_attention_fwd_f16v(qkv.data_ptr(), out.data_ptr(), B, S, 12, _lib.stream_handle()))
 torch.cuda.synchronize()
 print("ok")

@@ -8,7 +8,7 @@ def clk():
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for B in (2048, 512):
     qkv = (torch.randn(B * 512, 2304, device="cuda") * 0.5).bfloat16(); out = torch.empty(B * 512, 768, device="cuda").bfloat16()
-    f = lambda: _lib.load().rs_attention_fwd(qkv.data_ptr(), out.data_ptr(), B, 512, 12, _lib.stream_handle())
+    f = lambda: _lib.load().rs_attention_fwd_f16v(qkv.data_ptr(), out.data_ptr(), B, 512, 12, _lib.stream_handle())
     f(); torch.cuda.synchronize()
     for reps in (1, 3, 10):
         e0.record()
