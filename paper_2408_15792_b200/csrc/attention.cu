@@ -42,15 +42,11 @@ constexpr int AT_KVB = 5;  // K/V ring depth (one group of <= 4 blocks + a spare
 // Q [2 slots][2] + K, V [AT_KVB] + barriers (224 KB + 2 KB)
 constexpr int AT_SMEM = (4 + 2 * AT_KVB) * AT_BUF + 1024 + 1024;
 constexpr float AT_RESCALE = 8.0f;  // lazy-rescale threshold (log2 units)
-#ifndef AT_PINGPONG
-#define AT_PINGPONG 0  // strict slot alternation of the exponential pass (measured slower)
-#endif
 
 struct AtBars {
     uint64_t q_full[2][2], q_empty[2][2];
     uint64_t kv_full[AT_KVB], kv_empty[AT_KVB];
     uint64_t s_full[2], p_full[2], o_full[2];
-    uint64_t order[2];  // softmax ping-pong: slot s may start its exponentials after order[s]
     uint32_t tmem;
 };
 
@@ -151,7 +147,7 @@ __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_
 template <bool F16V>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tqkv, __nv_bfloat16* __restrict__ out, int B, int S,
-                         int H, unsigned long long* __restrict__ trace) {
+                         int H) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;                  // [slot][2]
@@ -176,7 +172,6 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
             mbar_init(&bar->s_full[s], 1);
             mbar_init(&bar->p_full[s], 4);
             mbar_init(&bar->o_full[s], 1);
-            mbar_init(&bar->order[s], 4);
         }
         for (int i = 0; i < AT_KVB; ++i) {
             mbar_init(&bar->kv_full[i], 1);
@@ -323,21 +318,6 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         const uint32_t tS = tmem + s * 256 + lane_addr, tO = tS + 128;
         const float c = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
         const uint64_t c2 = f2pack(c, c);
-        // The two slots take turns on the exponential pass (MUFU-bound): slot 0's n-th pass,
-        // then slot 1's n-th, then slot 0's (n+1)-th ... so one slot's exponentials overlap
-        // the other slot's MMAs instead of both slots contending and then idling together.
-        // Alternation stops at the shorter slot's block count (the last group may be uneven).
-        int n_alt = 0;
-        {
-            int tot[2] = {0, 0};
-            for (int g = blockIdx.x; g < n_groups; g += gridDim.x) {
-                const int U = min(gU, n_units - g * gU);
-                int k, t;
-                for (int ss = 0; ss < 2; ++ss)
-                    for (int i = 0; at_slot_tile(n_qt, U, ss, i, k, t); ++i) tot[ss] += t + 1;
-            }
-            n_alt = AT_PINGPONG ? min(tot[0], tot[1]) : 0;
-        }
         int tseq = 0, bseq = 0;
         for (int g = blockIdx.x; g < n_groups; g += gridDim.x) {
             const int U = min(gU, n_units - g * gU);
@@ -347,10 +327,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                 const int b = unit / H, h = unit % H;
                 float m_run = 0.f, l = 0.f;
                 for (int j = t; j >= 0; --j, ++bseq) {
-                    const bool trs = trace != nullptr && blockIdx.x == 0 && (warp & 3) == 0 && lane == 0 && bseq < 64;
-                    if (trs) trace[(s * 64 + bseq) * 4 + 0] = clock64();
                     mbar_wait(&bar->s_full[s], bseq & 1);
-                    if (trs) trace[(s * 64 + bseq) * 4 + 1] = clock64();
                     tc_fence_after();
                     // pass 1: row max over the block, 32 columns at a time (a whole row in
                     // registers would leave ptxas no room for ILP; TMEM loads are cheap)
@@ -384,11 +361,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                         alpha = exp2_mufu(m_run - mb);
                         m_run = mb;
                     }
-                    if (trs) trace[(s * 64 + bseq) * 4 + 2] = clock64();
                     // pass 2: P = 2^(s c - m_run), bf16 pairs over the first 64 S columns (the
                     // PV MMA's A operand; chunk cc's 16 P columns lie in S columns already read)
-                    if (bseq < n_alt && (s == 1 || bseq > 0))
-                        mbar_wait(&bar->order[s], (s == 0 ? bseq - 1 : bseq) & 1);
                     const uint64_t nm2 = f2pack(-m_run, -m_run);
                     uint64_t lsum[4] = {f2pack(0.f, 0.f), f2pack(0.f, 0.f), f2pack(0.f, 0.f), f2pack(0.f, 0.f)};
 #pragma unroll
@@ -445,11 +419,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                     tmem_st_wait();
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive(&bar->p_full[s]);
-                        if (bseq < n_alt) mbar_arrive(&bar->order[s ^ 1]);
-                    }
-                    if (trs) trace[(s * 64 + bseq) * 4 + 3] = clock64();
+                    if (lane == 0) mbar_arrive(&bar->p_full[s]);
                 }
                 // epilogue: O / l -> bf16 rows of `out`
                 mbar_wait(&bar->o_full[s], tseq & 1);
@@ -480,8 +450,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 }
 
 template <bool F16V>
-static int launch_attention(const void* qkv, void* out, int B, int S, int H, unsigned long long* trace,
-                            cudaStream_t st) {
+static int launch_attention(const void* qkv, void* out, int B, int S, int H, cudaStream_t st) {
     static int sms = 0;
     if (sms == 0) {
         int dev;
@@ -497,24 +466,22 @@ static int launch_attention(const void* qkv, void* out, int B, int S, int H, uns
     const int gU = AT_MAXKB / n_qt;
     const int n_groups = (B * H + gU - 1) / gU;
     const int grid = n_groups < sms ? n_groups : sms;
-    attention_fwd_kernel<F16V><<<grid, AT_THREADS, AT_SMEM, st>>>(m, static_cast<__nv_bfloat16*>(out), B, S, H, trace);
+    attention_fwd_kernel<F16V><<<grid, AT_THREADS, AT_SMEM, st>>>(m, static_cast<__nv_bfloat16*>(out), B, S, H);
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
 
-int attention_fwd_impl(const void* qkv, void* out, int B, int S, int H, int v_f16, unsigned long long* trace,
-                       cudaStream_t st) {
+int attention_fwd_impl(const void* qkv, void* out, int B, int S, int H, int v_f16, cudaStream_t st) {
     RS_CHECK_ARG(B > 0 && S > 0 && H > 0, "attention: empty shape");
     RS_CHECK_ARG(S <= AT_TILE * AT_MAXKB, "attention: S=%d > %d not supported", S, AT_TILE * AT_MAXKB);
-    return v_f16 ? launch_attention<true>(qkv, out, B, S, H, trace, st)
-                 : launch_attention<false>(qkv, out, B, S, H, trace, st);
+    return v_f16 ? launch_attention<true>(qkv, out, B, S, H, st) : launch_attention<false>(qkv, out, B, S, H, st);
 }
 
 int attention_fwd(const void* qkv, void* out, int B, int S, int H, cudaStream_t st) {
-    return attention_fwd_impl(qkv, out, B, S, H, 0, nullptr, st);
+    return attention_fwd_impl(qkv, out, B, S, H, 0, st);
 }
 int attention_fwd_f16v(const void* qkv, void* out, int B, int S, int H, cudaStream_t st) {
-    return attention_fwd_impl(qkv, out, B, S, H, 1, nullptr, st);
+    return attention_fwd_impl(qkv, out, B, S, H, 1, st);
 }
 
 }  // namespace rs
@@ -525,11 +492,4 @@ extern "C" int rs_attention_fwd(const void* qkv, void* out, int32_t B, int32_t S
 
 extern "C" int rs_attention_fwd_f16v(const void* qkv, void* out, int32_t B, int32_t S, int32_t H, void* stream) {
     return rs::attention_fwd_f16v(qkv, out, B, S, H, rs::as_stream(stream));
-}
-
-// Diagnostics only (tools/attn_trace.py): CTA 0 timeline, trace[0..511] softmax phases,
-// trace[1024..1279] MMA issue times.
-extern "C" __attribute__((visibility("default"))) int rs_attention_fwd_trace(const void* qkv, void* out, int32_t B, int32_t S, int32_t H,
-                                      unsigned long long* trace, void* stream) {
-    return rs::attention_fwd_impl(qkv, out, B, S, H, 1, trace, rs::as_stream(stream));
 }
