@@ -49,8 +49,9 @@ def _r(x, fwd=True, bwd=False):
 def _forward_with_grad(params, cfg, ids, emulate=False):
     """fp32 OPT-shape forward with autograd (the oracle, oracle/opt_ranker.py semantics).
     emulate=True rounds activations / activation gradients to bf16 where the CUDA
-    training pass stores them in bf16 (x1, qkv, att, x2, f forward; dqkv, da, df and the
-    GEMM copy of dh backward); the residual stream stays fp32 in both."""
+    training pass stores them in bf16 (x1, qkv, att, x2, f and the attention P forward;
+    dqkv, da, df, the attention dS and the GEMM copy of dh backward); the residual stream
+    stays fp32 in both."""
     import torch.nn.functional as F
     r = _r if emulate else (lambda x, fwd=True, bwd=False: x)
     dev = params["tok_emb"].device
@@ -68,8 +69,16 @@ def _forward_with_grad(params, cfg, ids, emulate=False):
         q = q.view(B, S, H, hd).transpose(1, 2) * (hd ** -0.5)
         k = k.view(B, S, H, hd).transpose(1, 2)
         v = v.view(B, S, H, hd).transpose(1, 2)
-        att = (torch.softmax(q @ k.transpose(-1, -2) + mask, dim=-1) @ v).transpose(1, 2).reshape(B, S, d)
-        att = r(att, True, True)
+        sc = q @ k.transpose(-1, -2) + mask
+        if emulate:
+            # attention kernels: P = exp(s - max) rounded to bf16 for the PV product,
+            # normalised by the fp32 row sum; dS rounded to bf16 for the dQ / dK products
+            sc = r(sc, False, True)
+            e = torch.exp(sc - sc.amax(-1, keepdim=True).detach())
+            att = (r(e) @ v) / e.sum(-1, keepdim=True)
+        else:
+            att = torch.softmax(sc, dim=-1) @ v
+        att = r(att.transpose(1, 2).reshape(B, S, d), True, True)
         h = h + r(att @ p["out_w"].t() + p["out_b"], False, True)
         x = r(F.layer_norm(h, (d,), p["ln2_w"], p["ln2_b"], eps=1e-5))
         f = r(torch.relu(x @ p["fc1_w"].t() + p["fc1_b"]), True, True)
