@@ -264,6 +264,39 @@ def tau_and_rankstep(pk, reps=5):
     }
 
 
+def size_sweep(pk, reps=3):
+    """at the cfg4 size (1M) tau and the rank-step are latency-bound (8 / 34 MB
+    of compulsory traffic is microseconds of HBM time), so their HBM fraction is also
+    reported at sizes well above L2 (synthetic fp32 scores N(0,1), lengths U[1, 2048])."""
+    from paper_2408_15792_b200 import ranking
+    from paper_2408_15792_b200.schedulers import DeviceQueue, SchedulerConfig
+    out = {"tau": [], "rank_step": []}
+    g = torch.Generator(device="cuda").manual_seed(11)
+    for n in (1 << 20, 1 << 24, 1 << 26):
+        x = torch.randn(n, device="cuda", generator=g)
+        y = torch.randint(1, 2049, (n,), device="cuda", generator=g, dtype=torch.int32)
+        res = torch.empty(6, dtype=torch.int64, device="cuda")
+        ranking.tau_counts_device(x, y, res)
+        t = timed(lambda: ranking.tau_counts_device(x, y, res), reps)
+        out["tau"].append({"n": n, "ms": t, "pairs_per_s": n * (n - 1) / 2 / (t / 1e3),
+                           "achieved_gbs": 8.0 * n / t / 1e6, "frac": 8.0 * n / t / 1e6 / pk["hbm_gbs"]})
+        del x, y
+    cfg = SchedulerConfig(max_batch=256, starvation_threshold=100, priority_quantum=50)
+    for n in (1 << 20, 1 << 24):
+        dq = DeviceQueue(n, torch.device("cuda"), score_dtype=torch.float32)
+        dq.score.copy_(torch.randn(n, device="cuda", generator=g))
+        from paper_2408_15792_b200 import _lib
+        dq.flags.fill_(_lib.RS_FLAG_SCORED)
+        dq.arrival_rank.copy_(torch.arange(n, dtype=torch.int32))
+        dq.rank_step(cfg, None, length_calibrated=False)
+        t = timed(lambda: dq.rank_step(cfg, None, length_calibrated=False), reps)
+        out["rank_step"].append({"n": n, "ms": t, "requests_per_s": n / (t / 1e3), "achieved_gbs": 34.0 * n / t / 1e6,
+                                 "frac": 34.0 * n / t / 1e6 / pk["hbm_gbs"]})
+        del dq
+    torch.cuda.empty_cache()
+    return out
+
+
 def train_step_metric(args, world, rank, pk):
     """cfg3 (BASELINE.json configs[2]): one ListMLE optimizer step over a global batch of
     1024 lists x 64 prompts x 128 tokens, lists sharded across ranks, gradient all-reduce
@@ -398,6 +431,7 @@ def run_ours(args):
     if rank == 0 and not args.no_extras:
         extras["roofline"] = gemm_roofline(pk)
         extras.update(tau_and_rankstep(pk))
+        extras["size_sweep"] = size_sweep(pk)
     if not args.no_extras and not args.no_train:
         extras["train_step"] = train_step_metric(args, world, rank, pk)
     if rank == 0 and not args.no_extras:
@@ -432,6 +466,7 @@ def run_ours(args):
         "tau": extras.get("tau"),
         "rank_step": extras.get("rank_step"),
         "train_step": extras.get("train_step"),
+        "size_sweep": extras.get("size_sweep"),
     }
     print(json.dumps(line), flush=True)
     if world > 1:

@@ -187,12 +187,6 @@ int rs_adam_step(float* master_dev, float* m_dev, float* v_dev, float* grad_dev,
  * M % 128 == 0, N % 64 == 0, K % 64 == 0 (the ranker's shapes). tcgen05 + TMA. */
 int rs_gemm_bf16(const void* A_dev, const void* W_dev, const void* bias_dev, const void* R_dev,
                  void* C_dev, int32_t M, int32_t N, int32_t K, int32_t epi, void* stream);
-/* Residual projection fused with the next LayerNorm (the ranker's out-proj -> LN2 and
- * FC2 -> next layer's LN1): h[M,N] fp32 (in place) += A[M,K] . W[N,K]^T + bias[N], then
- * xout[M,N] bf16 = (h - mean) * rstd * lnw + lnb per row (eps 1e-5). M, N % 256 == 0. */
-int rs_gemm_bf16_res_ln(const void* A_dev, const void* W_dev, const void* bias_dev, float* h_dev,
-                        const void* lnw_dev, const void* lnb_dev, void* xout_dev, int32_t M, int32_t N,
-                        int32_t K, void* stream);
 /* Causal multi-head attention over packed qkv [B*S, 3*H*64] bf16 -> out [B*S, H*64] bf16.
  * rs_attention_fwd_f16v: the same with the v block of qkv in fp16 (the layout the
  * ranker forward's QKV GEMM writes); P is then fp16 as well. */

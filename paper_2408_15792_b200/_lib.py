@@ -64,7 +64,6 @@ SIGNATURES = {
                                          c_vp, c_vp, c_sz, c_vp]),
     "rs_gemm_bf16": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "rs_attention_fwd": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
-    "rs_gemm_bf16_res_ln": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "rs_attention_fwd_f16v": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "rs_launch_count": (ctypes.c_uint64, []),
     "rs_ranker_grad_workspace_size": (c_sz, [ctypes.POINTER(RankerConfig), c_i32, c_i32, c_i32]),

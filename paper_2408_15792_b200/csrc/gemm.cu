@@ -220,9 +220,8 @@ constexpr int G2_EPI_BUF = 32 * 32 * 4;          // one 32x32 fp32 (or bf16) sta
 // K = 768 the mainloop is short and the fp32 R read + C write (8 B per output) bound it.
 template <int EPI>
 struct G2Cfg {
-    static constexpr bool res = EPI == 2 || EPI == 8;
-    static constexpr int stages = res ? 5 : G2_STAGES;
-    static constexpr int nbuf = res ? 4 : 2;
+    static constexpr int stages = EPI == 2 ? 5 : G2_STAGES;
+    static constexpr int nbuf = EPI == 2 ? 4 : 2;
     static constexpr int smem = stages * G2_STAGE_BYTES + 4 * nbuf * G2_EPI_BUF + 1024 + 512;
 };
 
@@ -235,9 +234,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     gemm_bf16_2sm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                          const __grid_constant__ CUtensorMap tC, const __grid_constant__ CUtensorMap tR,
                          const __nv_bfloat16* __restrict__ bias, const void* __restrict__ aux, int M, int N, int K,
-                         int ldc, int k_splits, int f16_col0, const __nv_bfloat16* __restrict__ lnw,
-                         const __nv_bfloat16* __restrict__ lnb, __nv_bfloat16* __restrict__ xout) {
-    constexpr bool RES = G2Cfg<EPI>::res;  // fp32 residual epilogue (2, 8)
+                         int ldc, int k_splits, int f16_col0) {
     constexpr int G2_STAGES = G2Cfg<EPI>::stages;
     constexpr int NBUF = G2Cfg<EPI>::nbuf;
     extern __shared__ uint8_t smem_raw[];
@@ -259,7 +256,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         tma_prefetch_desc(&tA);
         tma_prefetch_desc(&tB);
         tma_prefetch_desc(&tC);
-        if (RES) tma_prefetch_desc(&tR);
+        if (EPI == 2) tma_prefetch_desc(&tR);
         for (int s = 0; s < G2_STAGES; ++s) {
             mbar_init(&full[s], 2);  // leader: both CTAs' producers arrive (+ 64 KB of tx)
             mbar_init(&empty[s], 1);
@@ -282,19 +279,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     const int kblocks_all = K / G2_BK;
     const int kb_per = (kblocks_all + k_splits - 1) / k_splits;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-    // Each cluster walks a sequence of sub-tiles u = 0, 1, ...: work item i = u / nsub is
-    // w = cid + i * ncl. Normally a work item is one (tile, K split) and nsub = 1; with
-    // EPI 8 (residual + LayerNorm) a work item is a whole 256-row block and its tiles_n
-    // column tiles run back to back, so the epilogue sees complete rows.
-    const int nsub = EPI == 8 ? tiles_n : 1;
-    const int n_items = EPI == 8 ? M / G2_BM : n_work;
-    auto sub_tile = [&](int u, int& tile, int& sp, int& nt) -> bool {
-        const int w = cid + (u / nsub) * ncl;
-        if (w >= n_items) return false;
-        nt = u % nsub;
-        tile = EPI == 8 ? w * tiles_n + nt : w / k_splits;
-        sp = EPI == 8 ? 0 : w % k_splits;
-        return true;
+    // work item w -> output tile (w / k_splits) and K split (w % k_splits)
+    auto kb_range = [&](int w, int& kb0, int& kb1) {
+        const int sp = w % k_splits;
+        kb0 = sp * kb_per;
+        kb1 = min(kblocks_all, kb0 + kb_per);
     };
 
     if (warp == 0) {
@@ -302,9 +291,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             const uint64_t pol_a = policy_evict_normal(), pol_b = policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
-            int tile, sp, nt;
-            for (int u = 0; sub_tile(u, tile, sp, nt); ++u) {
-                const int kb0 = sp * kb_per, kb1 = min(kblocks_all, kb0 + kb_per);
+            for (int w = cid; w < n_work; w += ncl) {
+                const int tile = w / k_splits;
+                int kb0, kb1;
+                kb_range(w, kb0, kb1);
                 const int m0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
                 const int n0 = (tile % tiles_n) * G2_BN + rank * G2_HALF;
                 for (int kb = kb0; kb < kb1; ++kb) {
@@ -341,9 +331,9 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            int tile, sp, nt;
-            for (int u = 0; sub_tile(u, tile, sp, nt); ++u) {
-                const int kb0 = sp * kb_per, kb1 = min(kblocks_all, kb0 + kb_per);
+            for (int w = cid; w < n_work; w += ncl) {
+                int kb0, kb1;
+                kb_range(w, kb0, kb1);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem_base + acc * G2_BN;
@@ -385,23 +375,23 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         // cid + (n / 8) * ncl; its residual is TMA-loaded PD sub-tiles ahead
         constexpr int PD = NBUF - 2;
         auto prefetch_r = [&](int n) {
-            int ptile, psp, pnt;
-            if (!sub_tile(n >> 3, ptile, psp, pnt)) return;
-            const int rm0 = (ptile / tiles_n) * G2_BM + rank * G2_HALF;
-            const int rn0 = (ptile % tiles_n) * G2_BN;
+            const int w = cid + (n >> 3) * ncl;
+            if (w >= n_work) return;
+            const int tile = w / k_splits;
+            const int rm0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
+            const int rn0 = (tile % tiles_n) * G2_BN;
             const int b = n % NBUF;
             mbar_arrive_expect_tx(&rf[b], G2_EPI_BUF);
             tma_load_2d(ebuf + b * G2_EPI_BUF, &tR, &rf[b], rn0 + (n & 7) * 32, rm0 + q * 32);
         };
-        if (RES && lane == 0)
+        if (EPI == 2 && lane == 0)
             for (int n = 0; n < PD; ++n) prefetch_r(n);
-        float st_k = 0.f, st_s1 = 0.f, st_s2 = 0.f;  // EPI 8: shifted row sums for the LayerNorm
-        int tile, sp, nt;
-        for (int u = 0; sub_tile(u, tile, sp, nt); ++u) {
+        for (int w = cid; w < n_work; w += ncl) {
+            const int tile = w / k_splits;
             const int m0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
             const int n0 = (tile % tiles_n) * G2_BN;
-            // split-K partials land in slice sp of a [k_splits * M, N] buffer
-            const int mo = (EPI == 6) ? m0 + sp * M : m0;
+            // split-K partials land in slice (w % k_splits) of a [k_splits * M, N] buffer
+            const int mo = (EPI == 6) ? m0 + (w % k_splits) * M : m0;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const __nv_bfloat16* mrow =
@@ -419,7 +409,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                     for (int j = 0; j < 4; ++j) mk[j] = mv[j];
                 }
                 uint8_t* buf = ebuf + (nst % NBUF) * G2_EPI_BUF;
-                if (RES) {
+                if (EPI == 2) {
                     // reuse of buffer (nst + PD) % NBUF: its last store (sub-tile nst - 2) has
                     // been read; then queue that residual sub-tile
                     if (lane == 0) {
@@ -459,26 +449,20 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                         }
                     }
                 }
-                if (RES) mbar_wait(&rf[nst % NBUF], (nst / NBUF) & 1);
+                if (EPI == 2) mbar_wait(&rf[nst % NBUF], (nst / NBUF) & 1);
                 __syncwarp();
-                if (RES || EPI == 4 || EPI == 6) {
+                if (EPI == 2 || EPI == 4 || EPI == 6) {
                     // fp32 32x32 sub-tile, 128-B rows, SWIZZLE_128B: chunk j ^ (row % 8)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         float4* p = reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4));
                         float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                        if (RES) {
+                        if (EPI == 2) {
                             const float4 rr = *p;
                             o.x += rr.x;
                             o.y += rr.y;
                             o.z += rr.z;
                             o.w += rr.w;
-                        }
-                        if (EPI == 8) {  // row statistics, shifted by the row's first value
-                            if (nt == 0 && c == 0 && j == 0) st_k = o.x;
-                            const float a = o.x - st_k, b = o.y - st_k, cc = o.z - st_k, d = o.w - st_k;
-                            st_s1 += (a + b) + (cc + d);
-                            st_s2 = fmaf(a, a, fmaf(b, b, fmaf(cc, cc, fmaf(d, d, st_s2))));
                         }
                         *p = o;
                     }
@@ -517,36 +501,6 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                 acc = 0;
                 acc_phase ^= 1;
             }
-            if (EPI == 8 && nt == nsub - 1) {
-                // The warp's 32 rows are complete in C: x = LN(row) * lnw + lnb (bf16), the
-                // next GEMM's A operand. Rows are re-read from L2 (just written), 512 B per
-                // warp instruction; each row's mean / rstd come from its owning lane.
-                if (lane == 0) tma_store_wait<0>();
-                __syncwarp();
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                const float inv_n = 1.f / (float)N;
-                const float mu_s = st_s1 * inv_n;
-                const float mean = st_k + mu_s;
-                const float rstd = rsqrtf(fmaxf(st_s2 * inv_n - mu_s * mu_s, 0.f) + 1e-5f);
-                st_s1 = st_s2 = 0.f;
-                for (int i = 0; i < 32; ++i) {
-                    const float mi = __shfl_sync(0xffffffffu, mean, i), ri = __shfl_sync(0xffffffffu, rstd, i);
-                    const size_t row = (size_t)(m0 + q * 32 + i);
-                    const float4* hr = reinterpret_cast<const float4*>(static_cast<const float*>(aux) + row * N);
-                    uint2* xr = reinterpret_cast<uint2*>(xout + row * N);
-                    for (int cb = lane; cb < N / 4; cb += 32) {
-                        const float4 hv = __ldcg(hr + cb);
-                        const uint2 wu = __ldg(reinterpret_cast<const uint2*>(lnw) + cb);
-                        const uint2 bu = __ldg(reinterpret_cast<const uint2*>(lnb) + cb);
-                        const float2 w01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wu.x));
-                        const float2 w23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wu.y));
-                        const float2 b01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bu.x));
-                        const float2 b23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bu.y));
-                        xr[cb] = make_uint2(pack_bf16((hv.x - mi) * ri * w01.x + b01.x, (hv.y - mi) * ri * w01.y + b01.y),
-                                            pack_bf16((hv.z - mi) * ri * w23.x + b23.x, (hv.w - mi) * ri * w23.y + b23.y));
-                    }
-                }
-            }
         }
         if (lane == 0) tma_store_wait<0>();
     }
@@ -561,8 +515,7 @@ static int g_num_sms = 0;
 template <int E, bool AM, bool BM>
 static int launch_2sm(cudaLaunchConfig_t& lc, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
                       const CUtensorMap& tR, const __nv_bfloat16* b, const void* aux, int M, int N, int K,
-                      int k_splits, const __nv_bfloat16* lnw = nullptr, const __nv_bfloat16* lnb = nullptr,
-                      __nv_bfloat16* xout = nullptr) {
+                      int k_splits) {
     static bool attr = false;
     if (!attr) {
         RS_CUDA(cudaFuncSetAttribute(gemm_bf16_2sm_kernel<E, AM, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -571,7 +524,7 @@ static int launch_2sm(cudaLaunchConfig_t& lc, const CUtensorMap& tA, const CUten
     }
     lc.dynamicSmemBytes = G2Cfg<E>::smem;
     RS_CUDA(cudaLaunchKernelEx(&lc, gemm_bf16_2sm_kernel<E, AM, BM>, tA, tB, tC, tR, b, aux, M, N, K, N, k_splits,
-                               (2 * N) / 3, lnw, lnb, xout));
+                               (2 * N) / 3));
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
@@ -652,43 +605,6 @@ int gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux
     }
 }
 
-// Residual GEMM + LayerNorm of the result (EPI 8): h[M,N] (fp32, in place) += A . W^T +
-// bias, then x = LN(h) * lnw + lnb (bf16 [M,N]) for the next projection. One CTA pair owns
-// whole 256-row blocks so its epilogue sees complete rows (N % 256 == 0).
-int gemm_bf16_res_ln(const void* A, const void* W, const void* bias, float* h, const void* lnw, const void* lnb,
-                     void* xout, int M, int N, int K, cudaStream_t st) {
-    RS_CHECK_ARG(M > 0 && N > 0 && K > 0 && M % G2_BM == 0 && N % G2_BN == 0 && K % G2_BK == 0,
-                 "gemm_res_ln: need M, N %% 256 == 0 and K %% 64 == 0 (got %d %d %d)", M, N, K);
-    RS_CHECK_ARG(A && W && bias && h && lnw && lnb && xout, "gemm_res_ln: NULL argument");
-    if (g_num_sms == 0) {
-        int dev;
-        RS_CUDA(cudaGetDevice(&dev));
-        RS_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    CUtensorMap tA, tB, tC;
-    RS_TRY(make_tmap_bf16(&tA, A, (uint64_t)M, (uint64_t)K, (uint64_t)K * 2, G2_HALF, G2_BK));
-    RS_TRY(make_tmap_bf16(&tB, W, (uint64_t)N, (uint64_t)K, (uint64_t)K * 2, G2_HALF, G2_BK));
-    RS_TRY(make_tmap_2d(&tC, h, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)M, (uint64_t)N, (uint64_t)N * 4, 32, 32,
-                        CU_TENSOR_MAP_SWIZZLE_128B));
-    const int n_items = M / G2_BM;
-    int clusters = g_num_sms / 2;
-    if (n_items < clusters) clusters = n_items;
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(2 * clusters);
-    lc.blockDim = dim3(G_THREADS);
-    lc.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    return launch_2sm<8, false, false>(lc, tA, tB, tC, tC, static_cast<const __nv_bfloat16*>(bias), h, M, N, K, 1,
-                                       static_cast<const __nv_bfloat16*>(lnw), static_cast<const __nv_bfloat16*>(lnb),
-                                       static_cast<__nv_bfloat16*>(xout));
-}
-
 int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, void* C, int M, int N, int K, int epi,
               cudaStream_t st) {
     RS_CHECK_ARG(M > 0 && N > 0 && K > 0, "gemm: empty shape");
@@ -744,9 +660,4 @@ extern "C" int rs_gemm_bf16_ex(const void* A, const void* W, const void* bias, c
 extern "C" int rs_gemm_bf16(const void* A, const void* W, const void* bias, const void* R, void* C, int32_t M,
                             int32_t N, int32_t K, int32_t epi, void* stream) {
     return rs::gemm_bf16(A, W, bias, R, C, M, N, K, epi, rs::as_stream(stream));
-}
-
-extern "C" int rs_gemm_bf16_res_ln(const void* A, const void* W, const void* bias, float* h, const void* lnw,
-                                   const void* lnb, void* xout, int32_t M, int32_t N, int32_t K, void* stream) {
-    return rs::gemm_bf16_res_ln(A, W, bias, h, lnw, lnb, xout, M, N, K, rs::as_stream(stream));
 }

@@ -12,8 +12,3 @@ namespace rs {
 int gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux, void* C, int M, int N, int K,
                  int epi, int a_mn, int b_mn, int k_splits, cudaStream_t st);
 }  // namespace rs
-namespace rs {
-// h (fp32 [M,N], in place) += A . W^T + bias, then xout = LayerNorm(h) * lnw + lnb (bf16)
-int gemm_bf16_res_ln(const void* A, const void* W, const void* bias, float* h, const void* lnw, const void* lnb,
-                     void* xout, int M, int N, int K, cudaStream_t st);
-}  // namespace rs

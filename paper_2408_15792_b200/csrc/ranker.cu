@@ -54,6 +54,71 @@ __global__ void embed_kernel(const int32_t* __restrict__ ids, const __nv_bfloat1
 }
 
 template <int VPL>
+__device__ __forceinline__ void row_stats(const float (&v)[VPL * 8], float& mean, float& rstd);
+
+// Embedding fused with layer 0's first LayerNorm: one warp per token row writes the fp32
+// residual row h = tok[id] + pos[p + 2] and x = LN1(h) (bf16, the QKV GEMM's A operand).
+template <int VPL>
+__global__ void embed_ln_kernel(const int32_t* __restrict__ ids, const __nv_bfloat16* __restrict__ tok,
+                                const __nv_bfloat16* __restrict__ pos, const __nv_bfloat16* __restrict__ lw,
+                                const __nv_bfloat16* __restrict__ lb, float* __restrict__ h,
+                                __nv_bfloat16* __restrict__ x, int n_tok, int S, int vocab, int n_rows_padded) {
+    constexpr int d = VPL * 256;
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= n_rows_padded) return;
+    float4* dst = reinterpret_cast<float4*>(h + (size_t)row * d);
+    uint4* xr = reinterpret_cast<uint4*>(x + (size_t)row * d);
+    if (row >= n_tok) {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+            dst[2 * (lane + 32 * k)] = make_float4(0.f, 0.f, 0.f, 0.f);
+            dst[2 * (lane + 32 * k) + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+            xr[lane + 32 * k] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        return;
+    }
+    int id = ids[row];
+    id = id < 0 ? 0 : (id >= vocab ? vocab - 1 : id);
+    const int p = row % S + 2;
+    const uint4* a = reinterpret_cast<const uint4*>(tok + (size_t)id * d);
+    const uint4* b = reinterpret_cast<const uint4*>(pos + (size_t)p * d);
+    float v[VPL * 8];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+        uint4 xa = a[lane + 32 * k], yb = b[lane + 32 * k];
+        const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xa);
+        const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&yb);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float2 xf = __bfloat1622float2(x2[q]), yf = __bfloat1622float2(y2[q]);
+            v[k * 8 + 2 * q] = xf.x + yf.x;
+            v[k * 8 + 2 * q + 1] = xf.y + yf.y;
+        }
+        dst[2 * (lane + 32 * k)] = make_float4(v[k * 8 + 0], v[k * 8 + 1], v[k * 8 + 2], v[k * 8 + 3]);
+        dst[2 * (lane + 32 * k) + 1] = make_float4(v[k * 8 + 4], v[k * 8 + 5], v[k * 8 + 6], v[k * 8 + 7]);
+    }
+    float mean, rstd;
+    row_stats<VPL>(v, mean, rstd);
+    const uint4* wr = reinterpret_cast<const uint4*>(lw);
+    const uint4* br = reinterpret_cast<const uint4*>(lb);
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+        uint4 wu = wr[lane + 32 * k], bu = br[lane + 32 * k], o;
+        const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wu);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bu);
+        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            float2 wf = __bfloat1622float2(w2[q]), bf = __bfloat1622float2(b2[q]);
+            o2[q] = __floats2bfloat162_rn((v[k * 8 + 2 * q] - mean) * rstd * wf.x + bf.x,
+                                          (v[k * 8 + 2 * q + 1] - mean) * rstd * wf.y + bf.y);
+        }
+        xr[lane + 32 * k] = o;
+    }
+}
+
+template <int VPL>
 __device__ __forceinline__ void load_row_f32(const float* __restrict__ x, int lane, float (&v)[VPL * 8]) {
     const float4* xr = reinterpret_cast<const float4*>(x);
 #pragma unroll
@@ -427,10 +492,23 @@ extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params
         Arena ar(ws, ws_bytes);
         RankerWs w;
         ranker_ws_layout(ar, *cfg, mp, bp, &w);
+        const __nv_bfloat16* L0 = P + o.per_layer0;
         {
             const int wpb = 8;
-            embed_kernel<<<(mp + wpb - 1) / wpb, 32 * wpb, 0, st>>>(ids + b0 * S, P + o.tok, P + o.pos, w.h, n_tok, S,
-                                                                    d, cfg->vocab, mp);
+            const int grid = (mp + wpb - 1) / wpb;
+            switch (d / 256) {  // h0 = embeddings; x = LN1 of layer 0
+                case 1: embed_ln_kernel<1><<<grid, 32 * wpb, 0, st>>>(ids + b0 * S, P + o.tok, P + o.pos, L0 + o.ln1_w,
+                                                                      L0 + o.ln1_b, w.h, w.x, n_tok, S, cfg->vocab, mp); break;
+                case 2: embed_ln_kernel<2><<<grid, 32 * wpb, 0, st>>>(ids + b0 * S, P + o.tok, P + o.pos, L0 + o.ln1_w,
+                                                                      L0 + o.ln1_b, w.h, w.x, n_tok, S, cfg->vocab, mp); break;
+                case 3: embed_ln_kernel<3><<<grid, 32 * wpb, 0, st>>>(ids + b0 * S, P + o.tok, P + o.pos, L0 + o.ln1_w,
+                                                                      L0 + o.ln1_b, w.h, w.x, n_tok, S, cfg->vocab, mp); break;
+                case 4: embed_ln_kernel<4><<<grid, 32 * wpb, 0, st>>>(ids + b0 * S, P + o.tok, P + o.pos, L0 + o.ln1_w,
+                                                                      L0 + o.ln1_b, w.h, w.x, n_tok, S, cfg->vocab, mp); break;
+                case 8: embed_ln_kernel<8><<<grid, 32 * wpb, 0, st>>>(ids + b0 * S, P + o.tok, P + o.pos, L0 + o.ln1_w,
+                                                                      L0 + o.ln1_b, w.h, w.x, n_tok, S, cfg->vocab, mp); break;
+                default: set_error("ranker: unsupported d=%d", d); return RS_ERR_INVALID;
+            }
             RS_LAUNCH_CHECK();
         }
         // Rows past the last token are never written by attention but feed the
@@ -439,7 +517,7 @@ extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params
         const int32_t* lp = last_pos ? last_pos + b0 : nullptr;
         for (int l = 0; l < cfg->n_layers; ++l) {
             const __nv_bfloat16* L = P + o.per_layer0 + (int64_t)l * o.layer_stride;
-            RS_TRY(launch_ln(w.h, L + o.ln1_w, L + o.ln1_b, w.x, mp, d, st));
+            if (l > 0) RS_TRY(launch_ln(w.h, L + o.ln1_w, L + o.ln1_b, w.x, mp, d, st));  // layer 0: embed_ln
             // q, k bf16 and v fp16 (the attention's PV runs in fp16, see attention.cu)
             RS_TRY(gemm_bf16(w.x, L + o.qkv_w, L + o.qkv_b, nullptr, w.qkv, mp, 3 * d, d, 7, st));
             if (l == cfg->n_layers - 1) {
