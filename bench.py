@@ -297,6 +297,70 @@ def size_sweep(pk, reps=3):
     return out
 
 
+def synthetic_poisson(n, rate=40.0, seed=7, mu=5.3, sigma=0.9, max_len=2048):
+    """generate_poisson(rate, n, sharegpt, seed) in shape (workload.py:288-313, DIST_PRESETS
+    'sharegpt' = lognormal(5.3, 0.9) clipped to [1, 2048]); prompts become synthetic token
+    ids of length U[8, 128] (the A1 map's role)."""
+    from paper_2408_15792_b200.workload import Request
+    rng = np.random.default_rng(seed)
+    lengths = np.clip(np.rint(rng.lognormal(mu, sigma, n)), 1, max_len).astype(np.int64)
+    arrivals = np.cumsum(rng.exponential(1.0 / rate, n))
+    plen = rng.integers(8, 129, n)
+    reqs = [Request(id=i, arrival_time=float(arrivals[i]), prompt_tokens=int(plen[i]),
+                    true_output_tokens=int(lengths[i])) for i in range(n)]
+    return reqs, plen
+
+
+def engine_metric(args, world, rank, pk):
+    """cfg5 (BASELINE.json configs[4]): end-to-end scheduler loop. Every request's prompt
+    is scored once by the OPT-125M-shape ranker (S = 128, prompts sharded across ranks,
+    scores all-gathered: the score cache), then rank 0 runs the reference engine loop
+    (admission, ranking-policy step with starvation bump, execute, retirement) on the
+    device (paper_2408_15792_b200.engine) with max_batch 256, threshold 100, quantum 50,
+    the default cost preset. Wall clock of scoring + loop (the loop syncs once per step)."""
+    from paper_2408_15792_b200 import engine
+    from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
+    from paper_2408_15792_b200.schedulers import SchedulerConfig
+    n = args.e2e_requests
+    reqs, plen = synthetic_poisson(n)
+    cfg = RankerConfig.opt_125m()
+    model = OptRanker(cfg, seed=0)
+    gen = torch.Generator().manual_seed(3)
+    ids = torch.randint(4, cfg.vocab, (n, 128), generator=gen, dtype=torch.int32)
+    last = torch.from_numpy((plen - 1).astype(np.int32))
+    ids_d, last_d = ids.cuda(), last.cuda()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    t0 = time.perf_counter()
+    g = model.forward_sharded(ids_d, last_d)
+    scores = (-g).double().cpu().numpy()
+    t1 = time.perf_counter()
+    res = None
+    if rank == 0:
+        sched = SchedulerConfig(max_batch=256, starvation_threshold=100, priority_quantum=50)
+        eng = engine.DeviceEngine(reqs, scores, sched, engine.COST_PRESETS["default"])
+        t2 = time.perf_counter()
+        res = eng.run()
+        t3 = time.perf_counter()
+    if world > 1:
+        torch.distributed.barrier()
+    del model, ids_d
+    torch.cuda.empty_cache()
+    if rank != 0:
+        return None
+    score_s, loop_s = t1 - t0, t3 - t2
+    m = res.metrics
+    return {"metric": "end-to-end scheduler loop requests/sec (score cache + device engine)",
+            "value": n / (score_s + loop_s), "unit": "requests/s", "requests": n, "steps": res.steps,
+            "score_s": score_s, "loop_s": loop_s, "steps_per_s": res.steps / loop_s,
+            "prompts_scored_per_s": n / score_s, "sim": {k: m[k] for k in ("n_finished", "makespan_s",
+                                                                          "mean_latency_s", "p90_max_waiting_s",
+                                                                          "execution_order_tau")},
+            "workload": f"{n} Poisson(40/s) requests, sharegpt lengths, prompts 8-128 tokens, max_batch 256, "
+                        "starvation 100/50, default cost preset"}
+
+
 def train_step_metric(args, world, rank, pk):
     """cfg3 (BASELINE.json configs[2]): one ListMLE optimizer step over a global batch of
     1024 lists x 64 prompts x 128 tokens, lists sharded across ranks, gradient all-reduce
@@ -434,6 +498,8 @@ def run_ours(args):
         extras["size_sweep"] = size_sweep(pk)
     if not args.no_extras and not args.no_train:
         extras["train_step"] = train_step_metric(args, world, rank, pk)
+    if not args.no_extras and args.e2e_requests > 0:
+        extras["e2e_loop"] = engine_metric(args, world, rank, pk)
     if rank == 0 and not args.no_extras:
         if world == 1:
             extras["cpu_baseline"] = cpu_baseline(cfg, S, n_prompts=args.cpu_prompts)
@@ -467,6 +533,7 @@ def run_ours(args):
         "rank_step": extras.get("rank_step"),
         "train_step": extras.get("train_step"),
         "size_sweep": extras.get("size_sweep"),
+        "e2e_loop": extras.get("e2e_loop"),
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -490,6 +557,8 @@ def main():
     ap.add_argument("--train-seq", type=int, default=128)
     ap.add_argument("--train-micro", type=int, default=16)
     ap.add_argument("--train-steps", type=int, default=1)
+    ap.add_argument("--e2e-requests", type=int, default=20000,
+                    help="cfg5 loop size (BASELINE configs[4] is 100000; 0 disables)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -126,6 +126,54 @@ int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv_budget,
                  int32_t preemptive, int64_t* run_dev, int64_t* promoted_dev, int64_t* demoted_dev,
                  int32_t* counts_dev, void* ws_dev, size_t ws_bytes, void* stream);
 
+/* ---- §8f #1: device-resident engine step (the caller of the hot path) ------------
+ * The reference loop (engine.run, engine.py:382-460) with its queue resident in HBM:
+ * rs_engine_admit appends newly arrived requests to the queue (engine.py:218-243),
+ * rs_rank_step schedules, rs_engine_execute runs _Sim.execute (engine.py:247-284):
+ * preemption, prefill / decode / predictor time, one token per scheduled request with
+ * the _ReqTrack bookkeeping (engine.py:108-125), retirement and a stable compaction of
+ * the queue. Requests are referred to by their index r in the trace (queue id = r). */
+typedef struct rs_engine_queue {   /* all columns writable; n = alive rows */
+    int64_t n;
+    int32_t score_dtype;           /* RS_F32 or RS_F64 */
+    void* score;
+    int32_t* prompt_tokens;
+    int32_t* generated_tokens;
+    uint32_t* arrival_rank;
+    int64_t* id;
+    uint8_t* flags;
+    int32_t* starvation;
+    int32_t* quantum;
+} rs_engine_queue;
+typedef struct rs_engine_trace {   /* per request r of the trace */
+    const void* score;             /* the score cache (same dtype as the queue's) */
+    const int32_t* prompt_tokens;
+    const int32_t* true_output;
+    const uint32_t* arrival_rank;  /* position in (arrival_time, id) order */
+    const int64_t* arrival_ns;
+    int32_t* row_of;               /* queue row while alive */
+    int32_t* run_stamp;            /* init -1 */
+    int64_t* first_token_ns;       /* init -1 */
+    int64_t* last_event_ns;
+    int64_t* max_gap_ns;           /* init 0 */
+    int64_t* finish_ns;            /* init -1 */
+    int32_t* n_preempted;          /* init 0 */
+} rs_engine_trace;
+typedef struct rs_engine_cost {    /* CostModel (engine.py:42-78) */
+    int64_t decode_ns;
+    int64_t prefill_ns_per_token;
+    const int64_t* decode_table;   /* device, may be NULL */
+    int32_t decode_table_len;
+} rs_engine_cost;
+int rs_engine_admit(const rs_engine_queue* q, const rs_engine_trace* tr, const int32_t* req_dev, int32_t k,
+                    int64_t n_alive, void* stream);
+/* out_dev int64[6] = {now_ns (in/out), iter_ns, prefill_ns, n_alive after, n_preempted, n_finished};
+ * preempted_dev (alive order, >= n slots), finished_dev (fill order, >= max_batch slots).
+ * run_dev / counts_dev are rs_rank_step's run ids and counts; step must differ per call. */
+int rs_engine_execute(const rs_engine_queue* q, const rs_engine_trace* tr, const rs_engine_cost* cost,
+                      const int64_t* run_dev, const int32_t* counts_dev, int32_t step, int64_t predictor_ns,
+                      int64_t* out_dev, int64_t* preempted_dev, int64_t* finished_dev, void* stream);
+
 /* ---- A5/K1-K5: OPT-shape ranker ------------------------------------------------
  * Parameters live in ONE contiguous bf16 buffer laid out by rs_ranker_layout():
  *   tok_emb[V,d] pos_emb[P+2,d] { ln1_w[d] ln1_b[d] qkv_w[3d,d] qkv_b[3d] out_w[d,d]

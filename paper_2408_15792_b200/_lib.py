@@ -43,6 +43,23 @@ class QueueSoA(ctypes.Structure):
                 ("starvation", c_vp), ("quantum", c_vp)]
 
 
+class EngineQueue(ctypes.Structure):
+    _fields_ = [("n", c_i64), ("score_dtype", c_i32), ("score", c_vp), ("prompt_tokens", c_vp),
+                ("generated_tokens", c_vp), ("arrival_rank", c_vp), ("id", c_vp), ("flags", c_vp),
+                ("starvation", c_vp), ("quantum", c_vp)]
+
+
+class EngineTrace(ctypes.Structure):
+    _fields_ = [("score", c_vp), ("prompt_tokens", c_vp), ("true_output", c_vp), ("arrival_rank", c_vp),
+                ("arrival_ns", c_vp), ("row_of", c_vp), ("run_stamp", c_vp), ("first_token_ns", c_vp),
+                ("last_event_ns", c_vp), ("max_gap_ns", c_vp), ("finish_ns", c_vp), ("n_preempted", c_vp)]
+
+
+class EngineCost(ctypes.Structure):
+    _fields_ = [("decode_ns", c_i64), ("prefill_ns_per_token", c_i64), ("decode_table", c_vp),
+                ("decode_table_len", c_i32)]
+
+
 # name -> (restype, argtypes); the list mirrors include/rsb200.h exactly and
 # tests/test_lib_exports.py checks every declared symbol is exported.
 SIGNATURES = {
@@ -55,6 +72,11 @@ SIGNATURES = {
     "rs_listmle_lengths": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "rs_arrival_rank_workspace_size": (c_sz, [c_i64]),
     "rs_arrival_rank": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_sz, c_vp]),
+    "rs_engine_admit": (ctypes.c_int, [ctypes.POINTER(EngineQueue), ctypes.POINTER(EngineTrace), c_vp, c_i32, c_i64,
+                                       c_vp]),
+    "rs_engine_execute": (ctypes.c_int, [ctypes.POINTER(EngineQueue), ctypes.POINTER(EngineTrace),
+                                         ctypes.POINTER(EngineCost), c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp,
+                                         c_vp]),
     "rs_rank_step_workspace_size": (c_sz, [c_i64]),
     "rs_rank_step": (ctypes.c_int, [ctypes.POINTER(QueueSoA), c_i32, c_i64, c_i32, c_i32, c_i32, c_i32,
                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),

@@ -1,0 +1,230 @@
+// Device-resident engine step (the caller of the hot path):
+// admission into the resident queue and the reference's `_Sim.execute`
+// (engine.py:247-284) — preempt running requests left out of the batch, charge prefill
+// for the ones (re)starting, advance the clock by prefill + decode + predictor time,
+// emit one token per scheduled request (`_ReqTrack.on_token`, engine.py:108-125), retire
+// finished requests and compact the queue in place (stable, so row order stays the
+// `alive` dict's insertion order the ranking policy's promoted / demoted lists follow).
+// One CTA: a step touches each alive row a few times (µs of work) and every phase needs
+// the previous one complete, so grid-wide synchronisation would cost more than it saves.
+#include "common.cuh"
+
+namespace rs {
+
+constexpr int EX_THREADS = 1024;
+constexpr uint8_t EX_DONE = 8;  // row finished this step (dropped by the compaction)
+
+__device__ __forceinline__ int block_excl_scan(int v, int* warp_tot, int& total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        int t = lane < (int)(blockDim.x >> 5) ? warp_tot[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
+        }
+        warp_tot[lane] = t;  // inclusive
+    }
+    __syncthreads();
+    total = warp_tot[(blockDim.x >> 5) - 1];
+    const int before = wid ? warp_tot[wid - 1] : 0;
+    __syncthreads();
+    return before + x - v;
+}
+
+__global__ void __launch_bounds__(EX_THREADS) engine_admit_kernel(rs_engine_queue q, rs_engine_trace tr,
+                                                                  const int32_t* __restrict__ req, int32_t k,
+                                                                  int64_t n_alive) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= k) return;
+    const int r = req[i];
+    const int64_t row = n_alive + i;
+    if (q.score_dtype == RS_F64)
+        static_cast<double*>(q.score)[row] = static_cast<const double*>(tr.score)[r];
+    else
+        static_cast<float*>(q.score)[row] = static_cast<const float*>(tr.score)[r];
+    q.flags[row] = RS_FLAG_SCORED;
+    q.prompt_tokens[row] = tr.prompt_tokens[r];
+    q.generated_tokens[row] = 0;
+    q.arrival_rank[row] = tr.arrival_rank[r];
+    q.id[row] = r;
+    q.starvation[row] = 0;
+    q.quantum[row] = 0;
+    tr.row_of[r] = (int32_t)row;
+    tr.last_event_ns[r] = tr.arrival_ns[r];
+}
+
+__global__ void __launch_bounds__(EX_THREADS) engine_execute_kernel(rs_engine_queue q, rs_engine_trace tr,
+                                                                    rs_engine_cost cost, const int64_t* __restrict__ run,
+                                                                    const int32_t* __restrict__ counts, int32_t step,
+                                                                    int64_t predictor_ns, int64_t* __restrict__ out,
+                                                                    int64_t* __restrict__ preempted,
+                                                                    int64_t* __restrict__ finished) {
+    __shared__ int warp_tot[32];
+    __shared__ unsigned long long prefill_tokens;
+    __shared__ int n_pre;
+    const int tid = threadIdx.x;
+    const int n_run = counts[0];
+    const int64_t n = q.n;
+    if (tid == 0) {
+        prefill_tokens = 0ull;
+        n_pre = 0;
+    }
+    for (int k = tid; k < n_run; k += EX_THREADS) tr.run_stamp[run[k]] = step;
+    __syncthreads();
+    // 1. preemption / prefill (engine.py:248-262), preempted ids in alive order
+    for (int64_t base = 0; base < n; base += EX_THREADS) {
+        const int64_t row = base + tid;
+        int pre = 0;
+        unsigned long long pf = 0ull;
+        if (row < n) {
+            const int64_t id = q.id[row];
+            const bool running = q.flags[row] & RS_FLAG_RUNNING;
+            const bool in_run = tr.run_stamp[id] == step;
+            if (running && !in_run) {
+                q.flags[row] &= (uint8_t)~RS_FLAG_RUNNING;
+                tr.n_preempted[id] += 1;
+                pre = 1;
+            } else if (in_run && !running) {
+                pf = (unsigned long long)(q.prompt_tokens[row] + q.generated_tokens[row]);
+                q.flags[row] |= RS_FLAG_RUNNING;
+            }
+        }
+        if (pf) atomicAdd(&prefill_tokens, pf);
+        int total;
+        const int pos = block_excl_scan(pre, warp_tot, total);
+        if (pre) preempted[n_pre + pos] = q.id[row];
+        __syncthreads();
+        if (tid == 0) n_pre += total;
+        __syncthreads();
+    }
+    // 2. clock
+    __shared__ long long now_s;
+    if (tid == 0) {
+        long long dec;
+        if (cost.decode_table_len > 0) {
+            const int b = n_run < cost.decode_table_len ? n_run : cost.decode_table_len;
+            dec = cost.decode_table[b - 1];
+        } else {
+            dec = cost.decode_ns;
+        }
+        const long long iter = (long long)prefill_tokens * cost.prefill_ns_per_token + dec + predictor_ns;
+        now_s = out[0] + iter;
+        out[0] = now_s;
+        out[1] = iter;
+        out[2] = (long long)prefill_tokens * cost.prefill_ns_per_token;
+        out[4] = n_pre;
+    }
+    __syncthreads();
+    const long long now = now_s;
+    // 3. one token per scheduled request, in fill order (engine.py:270-280)
+    int done_before = 0;
+    for (int base = 0; base < n_run; base += EX_THREADS) {
+        const int k = base + tid;
+        int fin = 0;
+        int64_t id = 0;
+        if (k < n_run) {
+            id = run[k];
+            const int row = tr.row_of[id];
+            const int g = q.generated_tokens[row] + 1;
+            q.generated_tokens[row] = g;
+            const long long gap = now - tr.last_event_ns[id];
+            if (gap > tr.max_gap_ns[id]) tr.max_gap_ns[id] = gap;
+            if (tr.first_token_ns[id] < 0) tr.first_token_ns[id] = now;
+            tr.last_event_ns[id] = now;
+            if (g >= tr.true_output[id]) {
+                tr.finish_ns[id] = now;
+                q.flags[row] |= EX_DONE;
+                fin = 1;
+            }
+        }
+        int total;
+        const int pos = block_excl_scan(fin, warp_tot, total);
+        if (fin) finished[done_before + pos] = id;
+        done_before += total;
+    }
+    __syncthreads();
+    // 4. stable in-place compaction of the rows still alive
+    int64_t kept = 0;
+    for (int64_t base = 0; base < n; base += EX_THREADS) {
+        const int64_t row = base + tid;
+        const bool valid = row < n;
+        double sc = 0.0;
+        uint8_t fl = 0;
+        int32_t pr = 0, ge = 0, st = 0, qu = 0;
+        uint32_t ar = 0;
+        int64_t id = 0;
+        if (valid) {
+            sc = q.score_dtype == RS_F64 ? static_cast<const double*>(q.score)[row]
+                                         : (double)static_cast<const float*>(q.score)[row];
+            fl = q.flags[row];
+            pr = q.prompt_tokens[row];
+            ge = q.generated_tokens[row];
+            ar = q.arrival_rank[row];
+            id = q.id[row];
+            st = q.starvation[row];
+            qu = q.quantum[row];
+        }
+        const int keep = valid && !(fl & EX_DONE);
+        int total;
+        const int pos = block_excl_scan(keep, warp_tot, total);  // (its barriers order reads before writes)
+        if (keep) {
+            const int64_t dst = kept + pos;
+            if (q.score_dtype == RS_F64)
+                static_cast<double*>(q.score)[dst] = sc;
+            else
+                static_cast<float*>(q.score)[dst] = (float)sc;
+            q.flags[dst] = fl;
+            q.prompt_tokens[dst] = pr;
+            q.generated_tokens[dst] = ge;
+            q.arrival_rank[dst] = ar;
+            q.id[dst] = id;
+            q.starvation[dst] = st;
+            q.quantum[dst] = qu;
+            tr.row_of[id] = (int32_t)dst;
+        }
+        kept += total;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        out[3] = kept;
+        out[5] = done_before;
+    }
+}
+
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" int rs_engine_admit(const rs_engine_queue* q, const rs_engine_trace* tr, const int32_t* req_dev,
+                               int32_t k, int64_t n_alive, void* stream) {
+    RS_CHECK_ARG(q && tr && (k == 0 || req_dev), "rs_engine_admit: NULL argument");
+    RS_CHECK_ARG(k >= 0 && n_alive >= 0, "rs_engine_admit: negative count");
+    if (k == 0) return RS_OK;
+    engine_admit_kernel<<<(k + EX_THREADS - 1) / EX_THREADS, EX_THREADS, 0, as_stream(stream)>>>(*q, *tr, req_dev, k,
+                                                                                              n_alive);
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
+extern "C" int rs_engine_execute(const rs_engine_queue* q, const rs_engine_trace* tr, const rs_engine_cost* cost,
+                                 const int64_t* run_dev, const int32_t* counts_dev, int32_t step,
+                                 int64_t predictor_ns, int64_t* out_dev, int64_t* preempted_dev,
+                                 int64_t* finished_dev, void* stream) {
+    RS_CHECK_ARG(q && tr && cost && run_dev && counts_dev && out_dev && preempted_dev && finished_dev,
+                 "rs_engine_execute: NULL argument");
+    RS_CHECK_ARG(cost->decode_table_len == 0 || cost->decode_table != nullptr, "rs_engine_execute: decode table");
+    engine_execute_kernel<<<1, EX_THREADS, 0, as_stream(stream)>>>(*q, *tr, *cost, run_dev, counts_dev, step,
+                                                                    predictor_ns, out_dev, preempted_dev,
+                                                                    finished_dev);
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}

@@ -1,0 +1,325 @@
+"""Device-resident scheduler loop: the reference's `engine.run` (engine.py:382-460) for
+the ranking policy, with the queue, the policy state and the latency bookkeeping in HBM.
+
+SURVEY §8f #1 / BASELINE.json configs[4]. Per step, exactly as the reference:
+`jump_if_idle` / `admit_due` (engine.py:218-243; admission and the KV drop rule are
+host decisions on the sorted arrival times), scoring of the newly admitted requests
+(charged `predictor_ns_per_request` once each when the scorer `charges_predictor`),
+`RankingPolicy.schedule` (rs_rank_step), `_Sim.execute` (rs_engine_execute) and the
+step record. Scores come from a per-request score cache: the OPT ranker is a pure
+function of the prompt, so scoring every request once up front — batched
+on the GPU(s) — gives the same scores `rescore=True` would recompute every step, and
+the reference charges predictor time only at the first scoring either way.
+
+Records, per-request rows and metrics use the reference's keys and arithmetic (integer
+nanoseconds, math.fsum means, nearest-rank p90), so a run can be compared bit for bit
+with `ranksched.engine.run(trace, "ranking", scorer)` on the same scores
+(tests/test_gpu_engine.py, against fixtures recorded from the reference).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .schedulers import SchedulerConfig, UNLIMITED_KV
+
+NS_PER_S = 1_000_000_000
+
+
+@dataclass(frozen=True)
+class CostModel:
+    """Iteration timing in nanoseconds (the reference's CostModel, engine.py:42-78)."""
+
+    decode_ns: int = 25_000_000
+    prefill_ns_per_token: int = 40_000
+    predictor_ns_per_request: int = 500_000
+    decode_table: tuple[int, ...] | None = None
+
+    def __post_init__(self):
+        if self.decode_ns <= 0:
+            raise ValueError("decode_ns must be > 0")
+        if self.prefill_ns_per_token < 0 or self.predictor_ns_per_request < 0:
+            raise ValueError("cost components must be >= 0")
+        if self.decode_table is not None:
+            object.__setattr__(self, "decode_table", tuple(self.decode_table))
+            if not self.decode_table or any(v <= 0 for v in self.decode_table):
+                raise ValueError("decode_table entries must be > 0")
+
+
+COST_PRESETS = {
+    "default": CostModel(),
+    "fast": CostModel(decode_ns=1_000_000, prefill_ns_per_token=2_000, predictor_ns_per_request=20_000),
+    "unit": CostModel(decode_ns=NS_PER_S, prefill_ns_per_token=0, predictor_ns_per_request=0),
+}
+
+
+@dataclass
+class EngineResult:
+    metrics: dict
+    requests: list[dict]
+    records: list[dict] = field(default_factory=list, repr=False)
+    steps: int = 0
+
+
+def _p90(values):
+    s = sorted(values)
+    return s[math.ceil(0.9 * len(s)) - 1]
+
+
+def _latency_stats(lat, ptl, mw, makespan):
+    """ranking.latency_stats (ranking.py:167-201): fsum means, nearest-rank p90."""
+    n = len(lat)
+    if n == 0:
+        return dict(mean_latency=0.0, p90_latency=0.0, mean_per_token_latency=0.0, p90_per_token_latency=0.0,
+                    throughput=0.0, mean_max_waiting_time=0.0, p90_max_waiting_time=0.0, makespan=float(makespan))
+    return dict(mean_latency=math.fsum(lat) / n, p90_latency=_p90(lat), mean_per_token_latency=math.fsum(ptl) / n,
+                p90_per_token_latency=_p90(ptl), throughput=n / makespan if makespan > 0 else 0.0,
+                mean_max_waiting_time=math.fsum(mw) / n, p90_max_waiting_time=_p90(mw), makespan=float(makespan))
+
+
+class DeviceEngine:
+    """One simulation of a trace under the ranking policy, state resident on `dev`."""
+
+    def __init__(self, requests, scores, sched: SchedulerConfig = SchedulerConfig(),
+                 cost: CostModel = COST_PRESETS["default"], kv_budget: int | None = None,
+                 length_calibrated: bool = False, charges_predictor: bool = True, dev=None):
+        self.reqs = list(requests)
+        n = len(self.reqs)
+        if len(scores) != n:
+            raise ValueError("one score per request")
+        self.sched, self.cost = sched, cost
+        self.kv_budget = UNLIMITED_KV if kv_budget is None else int(kv_budget)
+        if self.kv_budget < 1:
+            raise ValueError("kv_budget must be >= 1")
+        if sched.max_batch > 1024:
+            raise ValueError("max_batch > 1024 is not supported by rs_engine_execute")
+        self.length_calibrated = bool(length_calibrated)
+        self.charges_predictor = bool(charges_predictor)
+        self.dev = dev or _lib.device()
+        d = self.dev
+        self.ids = np.array([r.id for r in self.reqs], dtype=np.int64)
+        arr_s = [r.arrival_time for r in self.reqs]
+        if any(b < a for a, b in zip(arr_s, arr_s[1:])):
+            raise ValueError("trace requests not sorted by arrival_time")
+        self.arrival_ns = np.array([int(round(t * NS_PER_S)) for t in arr_s], dtype=np.int64)
+        self.prompt = np.array([r.prompt_tokens for r in self.reqs], dtype=np.int32)
+        self.true_out = np.array([r.true_output_tokens for r in self.reqs], dtype=np.int32)
+        # arrival rank: position in (arrival_time, id) order (the sort key's tail)
+        order = np.lexsort((self.ids, np.array(arr_s, dtype=np.float64)))
+        rank = np.empty(n, dtype=np.uint32)
+        rank[order] = np.arange(n, dtype=np.uint32)
+        sc = np.asarray(scores, dtype=np.float64)
+        if np.isnan(sc).any():
+            raise ValueError("ranking policy: NaN score")
+        i32, i64 = torch.int32, torch.int64
+        self.t_score = torch.from_numpy(sc).to(d)
+        self.t_prompt = torch.from_numpy(self.prompt).to(d)
+        self.t_true = torch.from_numpy(self.true_out).to(d)
+        self.t_rank = torch.from_numpy(rank.view(np.int32)).to(d)
+        self.t_arr = torch.from_numpy(self.arrival_ns).to(d)
+        self.row_of = torch.full((n,), -1, dtype=i32, device=d)
+        self.stamp = torch.full((n,), -1, dtype=i32, device=d)
+        self.first_tok = torch.full((n,), -1, dtype=i64, device=d)
+        self.last_ev = torch.zeros(n, dtype=i64, device=d)
+        self.max_gap = torch.zeros(n, dtype=i64, device=d)
+        self.finish = torch.full((n,), -1, dtype=i64, device=d)
+        self.n_pre = torch.zeros(n, dtype=i32, device=d)
+        cap = max(n, 1)
+        self.q_score = torch.zeros(cap, dtype=torch.float64, device=d)
+        self.q_flags = torch.zeros(cap, dtype=torch.uint8, device=d)
+        self.q_prompt = torch.zeros(cap, dtype=i32, device=d)
+        self.q_gen = torch.zeros(cap, dtype=i32, device=d)
+        self.q_rank = torch.zeros(cap, dtype=i32, device=d)
+        self.q_id = torch.zeros(cap, dtype=i64, device=d)
+        self.q_starv = torch.zeros(cap, dtype=i32, device=d)
+        self.q_quant = torch.zeros(cap, dtype=i32, device=d)
+        self.run_out = torch.empty(max(sched.max_batch, 1), dtype=i64, device=d)
+        self.prom_out = torch.empty(cap, dtype=i64, device=d)
+        self.dem_out = torch.empty(cap, dtype=i64, device=d)
+        self.pre_out = torch.empty(cap, dtype=i64, device=d)
+        self.fin_out = torch.empty(max(sched.max_batch, 1), dtype=i64, device=d)
+        self.counts = torch.zeros(4, dtype=i32, device=d)
+        self.out = torch.zeros(6, dtype=i64, device=d)
+        self.out_host = torch.zeros(6, dtype=i64).pin_memory()
+        self.cnt_host = torch.zeros(4, dtype=i32).pin_memory()
+        self.adm_host = torch.zeros(cap, dtype=i32).pin_memory()
+        self.adm_dev = torch.zeros(cap, dtype=i32, device=d)
+        dt = cost.decode_table
+        self.t_table = torch.tensor(dt, dtype=i64, device=d) if dt else None
+        self._trace = _lib.EngineTrace(self.t_score.data_ptr(), self.t_prompt.data_ptr(), self.t_true.data_ptr(),
+                                       self.t_rank.data_ptr(), self.t_arr.data_ptr(), self.row_of.data_ptr(),
+                                       self.stamp.data_ptr(), self.first_tok.data_ptr(), self.last_ev.data_ptr(),
+                                       self.max_gap.data_ptr(), self.finish.data_ptr(), self.n_pre.data_ptr())
+        self._cost = _lib.EngineCost(cost.decode_ns, cost.prefill_ns_per_token,
+                                     None if self.t_table is None else self.t_table.data_ptr(),
+                                     0 if dt is None else len(dt))
+
+    def _queue(self, n_alive: int) -> _lib.EngineQueue:
+        return _lib.EngineQueue(n_alive, _lib.RS_F64, self.q_score.data_ptr(), self.q_prompt.data_ptr(),
+                                self.q_gen.data_ptr(), self.q_rank.data_ptr(), self.q_id.data_ptr(),
+                                self.q_flags.data_ptr(), self.q_starv.data_ptr(), self.q_quant.data_ptr())
+
+    def _soa(self, n_alive: int) -> _lib.QueueSoA:
+        return _lib.QueueSoA(n_alive, _lib.RS_F64, self.q_score.data_ptr(), self.q_prompt.data_ptr(),
+                             self.q_gen.data_ptr(), self.q_rank.data_ptr(), self.q_id.data_ptr(),
+                             self.q_flags.data_ptr(), self.q_starv.data_ptr(), self.q_quant.data_ptr())
+
+    def run(self, record: bool = False, stop_after_finished: int | None = None,
+            time_limit_s: float | None = None) -> EngineResult:
+        lib = _lib.load()
+        st = _lib.stream_handle(self.dev)
+        n = len(self.reqs)
+        limit_ns = None if time_limit_s is None else int(round(time_limit_s * NS_PER_S))
+        sched = self.sched
+        budget = -1 if self.kv_budget >= UNLIMITED_KV else self.kv_budget
+        ws_n = 0
+        ws = wn = None
+        now, nxt, n_alive, step, n_finished = 0, 0, 0, 0, 0
+        tot_prefill = tot_decode = tot_pred = 0
+        dropped_all: set[int] = set()
+        records = []
+        while True:
+            if n_alive == 0 and nxt < n and self.arrival_ns[nxt] > now:  # jump_if_idle
+                now = int(self.arrival_ns[nxt])
+            admitted, dropped = [], []
+            while nxt < n and self.arrival_ns[nxt] <= now:  # admit_due
+                r = nxt
+                nxt += 1
+                if self.prompt[r] + self.true_out[r] > self.kv_budget:
+                    dropped.append(r)
+                    continue
+                admitted.append(r)
+            if admitted:
+                k = len(admitted)
+                self.adm_host[:k] = torch.from_numpy(np.asarray(admitted, dtype=np.int32))
+                self.adm_dev[:k].copy_(self.adm_host[:k], non_blocking=True)
+                q = self._queue(n_alive)
+                _lib.check(lib.rs_engine_admit(ctypes.byref(q), ctypes.byref(self._trace), self.adm_dev.data_ptr(),
+                                               k, n_alive, st), "rs_engine_admit")
+                n_alive += k
+            dropped_all.update(dropped)
+            if n_alive == 0:
+                break
+            if limit_ns is not None and now >= limit_ns:
+                break
+            predictor_ns = len(admitted) * self.cost.predictor_ns_per_request if self.charges_predictor else 0
+            if n_alive > ws_n:
+                ws_n = max(n_alive, 2 * ws_n)
+                ws, wn = _lib.workspace.get(lib.rs_rank_step_workspace_size(ws_n), self.dev)
+            soa = self._soa(n_alive)
+            _lib.check(lib.rs_rank_step(ctypes.byref(soa), sched.max_batch, budget, sched.starvation_threshold,
+                                        sched.priority_quantum, int(self.length_calibrated), int(sched.preemption),
+                                        self.run_out.data_ptr(), self.prom_out.data_ptr(), self.dem_out.data_ptr(),
+                                        self.counts.data_ptr(), ws, wn, st), "rs_rank_step")
+            self.out_host[0] = now
+            self.out.copy_(self.out_host, non_blocking=True)
+            q = self._queue(n_alive)
+            _lib.check(lib.rs_engine_execute(ctypes.byref(q), ctypes.byref(self._trace), ctypes.byref(self._cost),
+                                             self.run_out.data_ptr(), self.counts.data_ptr(), step, predictor_ns,
+                                             self.out.data_ptr(), self.pre_out.data_ptr(), self.fin_out.data_ptr(),
+                                             st), "rs_engine_execute")
+            self.out_host.copy_(self.out, non_blocking=True)
+            self.cnt_host.copy_(self.counts, non_blocking=True)
+            torch.cuda.current_stream(self.dev).synchronize()
+            o = self.out_host.tolist()
+            c = self.cnt_host.tolist()
+            if c[3]:
+                raise ValueError("ranking policy: NaN effective score")
+            now, n_alive = int(o[0]), int(o[3])
+            n_finished += int(o[5])
+            tot_prefill += int(o[2])
+            tot_pred += predictor_ns
+            tot_decode += int(o[1]) - int(o[2]) - predictor_ns
+            if record:
+                ids = self.ids
+                records.append({
+                    "step": step, "now_ns": now, "iter_ns": int(o[1]),
+                    "run": ids[self.run_out[:c[0]].cpu().numpy()].tolist(),
+                    "preempted": ids[self.pre_out[:o[4]].cpu().numpy()].tolist(),
+                    "promoted": ids[self.prom_out[:c[1]].cpu().numpy()].tolist(),
+                    "demoted": ids[self.dem_out[:c[2]].cpu().numpy()].tolist(),
+                    "admitted": ids[admitted].tolist(), "dropped": ids[dropped].tolist(),
+                    "finished": ids[self.fin_out[:o[5]].cpu().numpy()].tolist(),
+                    "scored": ids[admitted].tolist(), "predictor_ns": predictor_ns,
+                })
+            step += 1
+            if stop_after_finished is not None and n_finished >= stop_after_finished:
+                break
+            if limit_ns is not None and now >= limit_ns:
+                break
+        rows = self._rows(dropped_all, nxt)
+        metrics = self._metrics(rows, now, step)
+        metrics.update(total_prefill_ns=tot_prefill, total_decode_ns=tot_decode, total_predictor_ns=tot_pred)
+        return EngineResult(metrics, rows, records, step)
+
+    def _rows(self, dropped: set[int], n_arrived: int) -> list[dict]:
+        first = self.first_tok.cpu().numpy()
+        fin = self.finish.cpu().numpy()
+        gap = self.max_gap.cpu().numpy()
+        npre = self.n_pre.cpu().numpy()
+        rows = []
+        for i, r in enumerate(self.reqs):
+            arrived = i < n_arrived
+            if i in dropped:
+                status = "dropped"
+            elif not arrived:
+                status = "unarrived"
+            elif fin[i] >= 0:
+                status = "finished"
+            else:
+                status = "unfinished"
+            row = {"id": r.id, "arrival_s": r.arrival_time, "prompt_tokens": r.prompt_tokens,
+                   "output_tokens": r.true_output_tokens, "status": status, "first_token_s": None, "finish_s": None,
+                   "latency_s": None, "per_token_latency_s": None, "max_wait_s": None,
+                   "n_preempted": int(npre[i]) if arrived and i not in dropped else 0}
+            if arrived and first[i] >= 0:
+                row["first_token_s"] = int(first[i]) / NS_PER_S
+                row["max_wait_s"] = int(gap[i]) / NS_PER_S
+            if arrived and fin[i] >= 0:
+                row["finish_s"] = int(fin[i]) / NS_PER_S
+                lat_ns = int(fin[i]) - int(self.arrival_ns[i])
+                row["latency_s"] = lat_ns / NS_PER_S
+                row["per_token_latency_s"] = lat_ns / r.true_output_tokens / NS_PER_S
+            rows.append(row)
+        return rows
+
+    def _metrics(self, rows: list[dict], now_ns: int, steps: int) -> dict:
+        from .ranking import kendall_tau_b
+        done = [r for r in rows if r["status"] == "finished"]
+        stats = _latency_stats([r["latency_s"] for r in done], [r["per_token_latency_s"] for r in done],
+                               [r["max_wait_s"] for r in done], now_ns / NS_PER_S)
+        tau = kendall_tau_b([r["first_token_s"] for r in done], [r["output_tokens"] for r in done]).tau \
+            if len(done) >= 2 else 0.0
+        return {"n_finished": len(done), "n_dropped": sum(1 for r in rows if r["status"] == "dropped"),
+                "n_unfinished": sum(1 for r in rows if r["status"] in ("unfinished", "unarrived")),
+                "n_preemptions": sum(r["n_preempted"] for r in rows), "steps": steps,
+                "makespan_s": stats["makespan"], "throughput_rps": stats["throughput"],
+                "mean_latency_s": stats["mean_latency"], "p90_latency_s": stats["p90_latency"],
+                "mean_per_token_latency_s": stats["mean_per_token_latency"],
+                "p90_per_token_latency_s": stats["p90_per_token_latency"],
+                "mean_max_waiting_s": stats["mean_max_waiting_time"],
+                "p90_max_waiting_s": stats["p90_max_waiting_time"], "execution_order_tau": tau}
+
+
+def run(trace, scorer=None, scores=None, sched: SchedulerConfig = SchedulerConfig(),
+        cost: CostModel = COST_PRESETS["default"], kv_budget: int | None = None, seed: int = 0,
+        record: bool = False, stop_after_finished: int | None = None, time_limit_s: float | None = None):
+    """engine.run(trace, "ranking", scorer, ...) on the device. Give either a scorer (its
+    score_batch is called once over the whole trace: the score cache) or `scores`."""
+    reqs = list(trace)
+    if scores is None:
+        if scorer is None:
+            raise ValueError("policy 'ranking' needs a scorer")
+        scores = scorer.score_batch(reqs, seed) if reqs else []
+        if any(s is None for s in scores):
+            raise ValueError("the device engine needs a score for every request (warm-up scorers unsupported)")
+    length_calibrated = getattr(scorer, "length_calibrated", False) if scorer is not None else False
+    charges = getattr(scorer, "charges_predictor", True) if scorer is not None else True
+    eng = DeviceEngine(reqs, scores, sched, cost, kv_budget, length_calibrated, charges)
+    return eng.run(record=record, stop_after_finished=stop_after_finished, time_limit_s=time_limit_s)

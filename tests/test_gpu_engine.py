@@ -1,0 +1,46 @@
+"""Device-resident engine loop (paper_2408_15792_b200.engine) vs the reference's own
+engine.run(trace, "ranking", scorer) on the same traces and scores: step records
+(run / preempted / promoted / demoted / admitted / dropped / finished / scored /
+predictor_ns / iter_ns / now_ns) bit-identical (sha256 of the canonical records),
+per-request rows and metrics equal. Fixtures: tests/golden/make_engine_golden.py."""
+
+import hashlib
+import json
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _canonical(obj):
+    return json.dumps(obj, sort_keys=True, separators=(",", ":"))
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2, 3])
+def test_engine_matches_reference_run(golden, idx):
+    from paper_2408_15792_b200 import engine
+    from paper_2408_15792_b200.schedulers import SchedulerConfig
+    from paper_2408_15792_b200.workload import Request
+    c = golden["engine_golden"]["cases"][idx]
+    reqs = [Request(id=i, arrival_time=a, prompt_tokens=p, true_output_tokens=o) for i, a, p, o in c["requests"]]
+    sched = SchedulerConfig(**c["sched"])
+    res = engine.run(reqs, scores=c["scores"], sched=sched, cost=engine.COST_PRESETS[c["cost"]],
+                     kv_budget=c["kv_budget"], record=True)
+    assert res.records[:len(c["first_records"])] == c["first_records"]
+    assert len(res.records) == c["n_steps"]
+    assert hashlib.sha256(_canonical(res.records).encode()).hexdigest() == c["records_sha256"]
+    assert res.requests == c["rows"]
+    for k, v in c["metrics"].items():
+        assert res.metrics[k] == v, (k, res.metrics[k], v)
+
+
+def test_engine_rejects_bad_config():
+    from paper_2408_15792_b200 import engine
+    from paper_2408_15792_b200.workload import Request
+    reqs = [Request(id=0, arrival_time=0.0, prompt_tokens=1, true_output_tokens=1)]
+    with pytest.raises(ValueError):
+        engine.run(reqs, scores=[0.0], kv_budget=0)
+    with pytest.raises(ValueError):
+        engine.run(reqs)  # no scorer, no scores
+    with pytest.raises(ValueError):
+        engine.run(reqs, scores=[float("nan")])
