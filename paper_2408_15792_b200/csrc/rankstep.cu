@@ -125,6 +125,165 @@ __global__ void fill_budget(const uint32_t* __restrict__ order, const int32_t* _
     if (lane == 0) counts[0] = taken;
 }
 
+// ---- unlimited KV budget: top-k selection instead of a full sort ------------------
+// With no budget the batch is the first k = min(max_batch, n) keys of the sorted order
+// (Policy._fill never skips), and the state update only needs membership. The keys are
+// distinct 96-bit integers [class:3 | eff:64 | arrival rank:29], so an MSB-first radix
+// select (11-bit digits, histograms of the keys still matching the chosen prefix) finds
+// the bucket holding the k-th key; once that bucket holds <= SEL_CAP keys, every key at
+// or below it (< k + SEL_CAP) is gathered and sorted by one block. Passes after the
+// decision are no-ops (the level count is data-dependent and decided on the device).
+constexpr int SEL_BITS = 11, SEL_BINS = 1 << SEL_BITS, SEL_LEVELS = 9;  // 99 >= 96 bits
+constexpr int SEL_CAP = 2048;
+constexpr int SEL_SORT = 4096;  // >= max_batch + SEL_CAP, power of two
+constexpr int SEL_THREADS = 1024;
+
+struct SelState {
+    unsigned long long prefix;  // digits chosen so far (level digits, MSB first)
+    uint32_t level;             // next level to histogram
+    uint32_t less;              // keys strictly below the current prefix bucket
+    uint32_t done;              // 1: final level reached (prefix covers the k-th key)
+    uint32_t final_level;
+    uint32_t n_cand;
+};
+
+__device__ __forceinline__ unsigned __int128 sel_value(const RankKey& k) {
+    // [class:3 | eff:64 | rank:29] << 3 -> 99 bits, digit L = bits [88 - 11 L, 99 - 11 L)
+    const unsigned __int128 v = ((unsigned __int128)(k.cr >> 29) << 93) | ((unsigned __int128)k.eff << 29) |
+                                (unsigned __int128)(k.cr & RANK_MASK);
+    return v << 3;
+}
+__device__ __forceinline__ uint32_t sel_digit(unsigned __int128 v, uint32_t level) {
+    return (uint32_t)(v >> (88 - SEL_BITS * level)) & (SEL_BINS - 1);
+}
+__device__ __forceinline__ unsigned long long sel_prefix(unsigned __int128 v, uint32_t levels) {
+    // first `levels` digits (levels <= 5 fit in 64 bits; the select stops earlier in
+    // practice, deeper levels compare the 128-bit value directly)
+    return levels == 0 ? 0ull : (unsigned long long)(v >> (99 - SEL_BITS * levels));
+}
+
+__global__ void __launch_bounds__(SEL_THREADS) sel_hist(const RankKey* __restrict__ keys, uint32_t n,
+                                                        const SelState* __restrict__ st,
+                                                        unsigned __int128* __restrict__ pfx128,
+                                                        uint32_t* __restrict__ hist) {
+    if (st->done) return;
+    __shared__ uint32_t h[SEL_BINS];
+    for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) h[b] = 0;
+    __syncthreads();
+    const uint32_t level = st->level;
+    const unsigned __int128 want = *pfx128;  // prefix digits in place (lower bits zero)
+    const int shift = 99 - SEL_BITS * (int)level;
+    for (uint32_t i = blockIdx.x * SEL_THREADS + threadIdx.x; i < n; i += gridDim.x * SEL_THREADS) {
+        const unsigned __int128 v = sel_value(keys[i]);
+        if (level == 0 || (v >> shift) == (want >> shift)) atomicAdd(&h[sel_digit(v, level)], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS)
+        if (h[b]) atomicAdd(&hist[b], h[b]);
+}
+
+__global__ void __launch_bounds__(SEL_THREADS) sel_pick(SelState* __restrict__ st,
+                                                        unsigned __int128* __restrict__ pfx128,
+                                                        uint32_t* __restrict__ hist, uint32_t k) {
+    if (st->done) return;
+    __shared__ uint32_t c[SEL_BINS];
+    __shared__ uint32_t pick, below;
+    for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) c[b] = hist[b];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t need = k - st->less;  // >= 1
+        uint32_t acc = 0, b = 0;
+        for (; b < SEL_BINS; ++b) {
+            if (acc + c[b] >= need) break;
+            acc += c[b];
+        }
+        pick = b;
+        below = acc;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) hist[b] = 0;
+    if (threadIdx.x == 0) {
+        const uint32_t level = st->level;
+        *pfx128 |= (unsigned __int128)pick << (88 - SEL_BITS * level);
+        st->less += below;
+        st->level = level + 1;
+        if (c[pick] <= SEL_CAP || level + 1 == SEL_LEVELS) {
+            st->done = 1;
+            st->final_level = level + 1;
+        }
+    }
+}
+
+// every key at or below the chosen bucket (exactly st->less + bucket size of them)
+__global__ void __launch_bounds__(SEL_THREADS) sel_gather(const RankKey* __restrict__ keys, uint32_t n,
+                                                          SelState* __restrict__ st,
+                                                          const unsigned __int128* __restrict__ pfx128,
+                                                          RankKey* __restrict__ ck, uint32_t* __restrict__ ci) {
+    const int shift = 99 - SEL_BITS * (int)st->final_level;
+    const unsigned __int128 lim = *pfx128 >> shift;
+    for (uint32_t i = blockIdx.x * SEL_THREADS + threadIdx.x; i < n; i += gridDim.x * SEL_THREADS) {
+        const RankKey kk = keys[i];
+        if ((sel_value(kk) >> shift) <= lim) {
+            const uint32_t slot = atomicAdd(&st->n_cand, 1u);
+            if (slot < SEL_SORT) {
+                ck[slot] = kk;
+                ci[slot] = i;
+            }
+        }
+    }
+}
+
+// one block: sort the <= SEL_SORT candidates (bitonic, smem), emit the first k in order
+__global__ void __launch_bounds__(SEL_THREADS) sel_sort_emit(const RankKey* __restrict__ ck,
+                                                             const uint32_t* __restrict__ ci,
+                                                             const SelState* __restrict__ st,
+                                                             const int64_t* __restrict__ id, uint32_t k,
+                                                             int64_t* __restrict__ run, uint8_t* __restrict__ sched,
+                                                             int32_t* __restrict__ counts) {
+    extern __shared__ uint8_t sm[];
+    RankKey* sk = reinterpret_cast<RankKey*>(sm);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(sk + SEL_SORT);
+    const uint32_t m = min(st->n_cand, (uint32_t)SEL_SORT);
+    uint32_t P = 1;
+    while (P < m) P <<= 1;
+    for (uint32_t i = threadIdx.x; i < P; i += SEL_THREADS) {
+        if (i < m) {
+            sk[i] = ck[i];
+            sv[i] = ci[i];
+        } else {
+            sk[i] = KeyTraits<RankKey>::sentinel();
+            sv[i] = 0xffffffffu;
+        }
+    }
+    __syncthreads();
+    for (uint32_t size = 2; size <= P; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+            for (uint32_t i = threadIdx.x; i < P; i += SEL_THREADS) {
+                const uint32_t j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    const RankKey a = sk[i], b = sk[j];
+                    const bool swap = up ? KeyTraits<RankKey>::less(b, a) : KeyTraits<RankKey>::less(a, b);
+                    if (swap) {
+                        sk[i] = b;
+                        sk[j] = a;
+                        const uint32_t t = sv[i];
+                        sv[i] = sv[j];
+                        sv[j] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t r = threadIdx.x; r < k; r += SEL_THREADS) {
+        const uint32_t idx = sv[r];
+        run[r] = id[idx];
+        sched[idx] = 1;
+    }
+    if (threadIdx.x == 0) counts[0] = (int32_t)k;
+}
+
 constexpr int UPD_THREADS = 1024;
 
 // State update (schedulers.py:224-240) + per-block counts of promoted / demoted.
@@ -165,10 +324,11 @@ __global__ void starvation_update(rs_queue_soa q, const uint8_t* __restrict__ sc
     }
 }
 
-// Exclusive scan of the interleaved (promoted, demoted) block counts by one block;
-// writes the totals to counts[1], counts[2].
-__global__ void scan_pairs(uint32_t* __restrict__ bcnt, uint32_t nblk, int32_t* __restrict__ counts) {
-    __shared__ uint32_t tp[1024], td[1024];
+// Exclusive scan of the interleaved (promoted, demoted) block counts by one block
+// (per-thread chunk sums, then warp-shuffle scans); writes the totals to counts[1, 2].
+__global__ void __launch_bounds__(1024) scan_pairs(uint32_t* __restrict__ bcnt, uint32_t nblk,
+                                                   int32_t* __restrict__ counts) {
+    __shared__ uint32_t wp[32], wd[32];
     const uint32_t per = (nblk + 1023) / 1024;
     const uint32_t b0 = threadIdx.x * per, b1 = min(nblk, b0 + per);
     uint32_t sp = 0, sd = 0;
@@ -176,25 +336,42 @@ __global__ void scan_pairs(uint32_t* __restrict__ bcnt, uint32_t nblk, int32_t* 
         sp += bcnt[2 * b];
         sd += bcnt[2 * b + 1];
     }
-    tp[threadIdx.x] = sp;
-    td[threadIdx.x] = sd;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint32_t ap = 0, ad = 0;
-        for (int t = 0; t < 1024; ++t) {
-            uint32_t vp = tp[t], vd = td[t];
-            tp[t] = ap;
-            td[t] = ad;
-            ap += vp;
-            ad += vd;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t ip = sp, id2 = sd;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t yp = __shfl_up_sync(0xffffffffu, ip, o), yd = __shfl_up_sync(0xffffffffu, id2, o);
+        if (lane >= (uint32_t)o) {
+            ip += yp;
+            id2 += yd;
         }
-        counts[1] = (int32_t)ap;
-        counts[2] = (int32_t)ad;
+    }
+    if (lane == 31) {
+        wp[w] = ip;
+        wd[w] = id2;
     }
     __syncthreads();
-    uint32_t ap = tp[threadIdx.x], ad = td[threadIdx.x];
+    if (w == 0) {
+        uint32_t xp = wp[lane], xd = wd[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t yp = __shfl_up_sync(0xffffffffu, xp, o), yd = __shfl_up_sync(0xffffffffu, xd, o);
+            if (lane >= (uint32_t)o) {
+                xp += yp;
+                xd += yd;
+            }
+        }
+        wp[lane] = xp;  // inclusive over warps
+        wd[lane] = xd;
+        if (lane == 31) {
+            counts[1] = (int32_t)xp;
+            counts[2] = (int32_t)xd;
+        }
+    }
+    __syncthreads();
+    uint32_t ap = (w ? wp[w - 1] : 0u) + ip - sp, ad = (w ? wd[w - 1] : 0u) + id2 - sd;
     for (uint32_t b = b0; b < b1; ++b) {
-        uint32_t vp = bcnt[2 * b], vd = bcnt[2 * b + 1];
+        const uint32_t vp = bcnt[2 * b], vd = bcnt[2 * b + 1];
         bcnt[2 * b] = ap;
         bcnt[2 * b + 1] = ad;
         ap += vp;
@@ -255,6 +432,11 @@ struct RankWs {
     uint8_t* pd;
     uint32_t* bcnt;
     int* err;
+    SelState* sel;
+    unsigned __int128* pfx;
+    uint32_t* hist;
+    RankKey* ck;
+    uint32_t* ci;
 };
 template <typename A>
 static void rank_layout(A& a, uint64_t n, RankWs* w) {
@@ -268,7 +450,12 @@ static void rank_layout(A& a, uint64_t n, RankWs* w) {
     auto pd = a.template take<uint8_t>(n + 1);
     auto bc = a.template take<uint32_t>(2 * nblk);
     auto er = a.template take<int>(4);
-    if (w) *w = RankWs{ka, kb, va, vb, sc, pd, bc, er};
+    auto sl = a.template take<SelState>(1);
+    auto px = a.template take<unsigned __int128>(1);
+    auto hi = a.template take<uint32_t>(SEL_BINS);
+    auto ck = a.template take<RankKey>(SEL_SORT);
+    auto ci = a.template take<uint32_t>(SEL_SORT);
+    if (w) *w = RankWs{ka, kb, va, vb, sc, pd, bc, er, sl, px, hi, ck, ci};
 }
 struct RankSizer {
     ArenaSizer s;
@@ -350,15 +537,39 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
     const int T = 256;
     build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
     RS_LAUNCH_CHECK();
-    RankKey* sk;
-    uint32_t* order;
-    RS_TRY((merge_sort<RankKey, true, false>(w.kb, nullptr, n, w.ka, w.kb, w.va, w.vb, nullptr, st, &sk, &order)));
-    if (kv_budget < 0) {
-        fill_unlimited<<<(min(n, (uint32_t)max_batch) + T - 1) / T, T, 0, st>>>(order, q->id, n, max_batch, run,
-                                                                             w.sched, counts);
+    const uint32_t k = min(n, (uint32_t)max_batch);
+    if (kv_budget < 0 && n > (uint32_t)SEL_CAP && k + SEL_CAP <= (uint32_t)SEL_SORT) {
+        // top-k select (see sel_hist): <= SEL_LEVELS histogram passes, most no-ops
+        static bool attr = false;
+        const size_t smem = SEL_SORT * (sizeof(RankKey) + sizeof(uint32_t));
+        if (!attr) {
+            RS_CUDA(cudaFuncSetAttribute(sel_sort_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        RS_CUDA(cudaMemsetAsync(w.sel, 0, sizeof(SelState), st));
+        RS_CUDA(cudaMemsetAsync(w.pfx, 0, sizeof(unsigned __int128), st));
+        RS_CUDA(cudaMemsetAsync(w.hist, 0, SEL_BINS * sizeof(uint32_t), st));
+        const uint32_t gb = min((n + SEL_THREADS - 1) / SEL_THREADS, 296u);
+        for (int level = 0; level < SEL_LEVELS; ++level) {
+            sel_hist<<<gb, SEL_THREADS, 0, st>>>(w.kb, n, w.sel, w.pfx, w.hist);
+            RS_LAUNCH_CHECK();
+            sel_pick<<<1, SEL_THREADS, 0, st>>>(w.sel, w.pfx, w.hist, k);
+            RS_LAUNCH_CHECK();
+        }
+        sel_gather<<<gb, SEL_THREADS, 0, st>>>(w.kb, n, w.sel, w.pfx, w.ck, w.ci);
+        RS_LAUNCH_CHECK();
+        sel_sort_emit<<<1, SEL_THREADS, smem, st>>>(w.ck, w.ci, w.sel, q->id, k, run, w.sched, counts);
     } else {
-        fill_budget<<<1, 32, 0, st>>>(order, q->prompt_tokens, q->generated_tokens, q->id, n, max_batch,
-                                      kv_budget, run, w.sched, counts);
+        RankKey* sk;
+        uint32_t* order;
+        RS_TRY((merge_sort<RankKey, true, false>(w.kb, nullptr, n, w.ka, w.kb, w.va, w.vb, nullptr, st, &sk,
+                                                 &order)));
+        if (kv_budget < 0) {
+            fill_unlimited<<<(k + T - 1) / T, T, 0, st>>>(order, q->id, n, max_batch, run, w.sched, counts);
+        } else {
+            fill_budget<<<1, 32, 0, st>>>(order, q->prompt_tokens, q->generated_tokens, q->id, n, max_batch,
+                                          kv_budget, run, w.sched, counts);
+        }
     }
     RS_LAUNCH_CHECK();
     const uint32_t nblk = (n + UPD_THREADS - 1) / UPD_THREADS;

@@ -173,87 +173,97 @@ class DeviceEngine:
     def run(self, record: bool = False, stop_after_finished: int | None = None,
             time_limit_s: float | None = None) -> EngineResult:
         lib = _lib.load()
+        rank_step, execute, admit, check = lib.rs_rank_step, lib.rs_engine_execute, lib.rs_engine_admit, _lib.check
         st = _lib.stream_handle(self.dev)
+        stream = torch.cuda.current_stream(self.dev)
         n = len(self.reqs)
         limit_ns = None if time_limit_s is None else int(round(time_limit_s * NS_PER_S))
         sched = self.sched
         budget = -1 if self.kv_budget >= UNLIMITED_KV else self.kv_budget
+        fits = (self.prompt.astype(np.int64) + self.true_out) <= self.kv_budget
+        q, soa = self._queue(0), self._soa(0)
+        q_ref, soa_ref, tr_ref, cost_ref = (ctypes.byref(q), ctypes.byref(soa), ctypes.byref(self._trace),
+                                            ctypes.byref(self._cost))
+        run_p, prom_p, dem_p, cnt_p = (self.run_out.data_ptr(), self.prom_out.data_ptr(), self.dem_out.data_ptr(),
+                                       self.counts.data_ptr())
+        out_p, pre_p, fin_p, adm_p = (self.out.data_ptr(), self.pre_out.data_ptr(), self.fin_out.data_ptr(),
+                                      self.adm_dev.data_ptr())
+        adm_np = self.adm_host.numpy()
+        out_np, cnt_np = self.out_host.numpy(), self.cnt_host.numpy()
         ws_n = 0
         ws = wn = None
         now, nxt, n_alive, step, n_finished = 0, 0, 0, 0, 0
         tot_prefill = tot_decode = tot_pred = 0
-        dropped_all: set[int] = set()
+        dropped_all: list[int] = []
         records = []
         while True:
             if n_alive == 0 and nxt < n and self.arrival_ns[nxt] > now:  # jump_if_idle
                 now = int(self.arrival_ns[nxt])
-            admitted, dropped = [], []
-            while nxt < n and self.arrival_ns[nxt] <= now:  # admit_due
-                r = nxt
-                nxt += 1
-                if self.prompt[r] + self.true_out[r] > self.kv_budget:
-                    dropped.append(r)
-                    continue
-                admitted.append(r)
-            if admitted:
+            # admit_due: the arrivals up to `now`; requests that could never hold their
+            # full context in the KV budget are dropped (engine.py:224-243)
+            end = int(np.searchsorted(self.arrival_ns, now, side="right"))
+            admitted = dropped = None
+            k = 0
+            if end > nxt:
+                idx = np.arange(nxt, end)
+                ok = fits[nxt:end]
+                admitted, dropped = idx[ok], idx[~ok]
+                nxt = end
                 k = len(admitted)
-                self.adm_host[:k] = torch.from_numpy(np.asarray(admitted, dtype=np.int32))
-                self.adm_dev[:k].copy_(self.adm_host[:k], non_blocking=True)
-                q = self._queue(n_alive)
-                _lib.check(lib.rs_engine_admit(ctypes.byref(q), ctypes.byref(self._trace), self.adm_dev.data_ptr(),
-                                               k, n_alive, st), "rs_engine_admit")
-                n_alive += k
-            dropped_all.update(dropped)
+                if len(dropped):
+                    dropped_all.extend(dropped.tolist())
+                if k:
+                    adm_np[:k] = admitted
+                    self.adm_dev[:k].copy_(self.adm_host[:k], non_blocking=True)
+                    q.n = n_alive
+                    check(admit(q_ref, tr_ref, adm_p, k, n_alive, st), "rs_engine_admit")
+                    n_alive += k
             if n_alive == 0:
                 break
             if limit_ns is not None and now >= limit_ns:
                 break
-            predictor_ns = len(admitted) * self.cost.predictor_ns_per_request if self.charges_predictor else 0
+            predictor_ns = k * self.cost.predictor_ns_per_request if self.charges_predictor else 0
             if n_alive > ws_n:
                 ws_n = max(n_alive, 2 * ws_n)
                 ws, wn = _lib.workspace.get(lib.rs_rank_step_workspace_size(ws_n), self.dev)
-            soa = self._soa(n_alive)
-            _lib.check(lib.rs_rank_step(ctypes.byref(soa), sched.max_batch, budget, sched.starvation_threshold,
-                                        sched.priority_quantum, int(self.length_calibrated), int(sched.preemption),
-                                        self.run_out.data_ptr(), self.prom_out.data_ptr(), self.dem_out.data_ptr(),
-                                        self.counts.data_ptr(), ws, wn, st), "rs_rank_step")
-            self.out_host[0] = now
+            soa.n = n_alive
+            check(rank_step(soa_ref, sched.max_batch, budget, sched.starvation_threshold, sched.priority_quantum,
+                            int(self.length_calibrated), int(sched.preemption), run_p, prom_p, dem_p, cnt_p, ws, wn,
+                            st), "rs_rank_step")
+            out_np[0] = now
             self.out.copy_(self.out_host, non_blocking=True)
-            q = self._queue(n_alive)
-            _lib.check(lib.rs_engine_execute(ctypes.byref(q), ctypes.byref(self._trace), ctypes.byref(self._cost),
-                                             self.run_out.data_ptr(), self.counts.data_ptr(), step, predictor_ns,
-                                             self.out.data_ptr(), self.pre_out.data_ptr(), self.fin_out.data_ptr(),
-                                             st), "rs_engine_execute")
+            q.n = n_alive
+            check(execute(q_ref, tr_ref, cost_ref, run_p, cnt_p, step, predictor_ns, out_p, pre_p, fin_p, st),
+                  "rs_engine_execute")
             self.out_host.copy_(self.out, non_blocking=True)
             self.cnt_host.copy_(self.counts, non_blocking=True)
-            torch.cuda.current_stream(self.dev).synchronize()
-            o = self.out_host.tolist()
-            c = self.cnt_host.tolist()
-            if c[3]:
+            stream.synchronize()
+            if cnt_np[3]:
                 raise ValueError("ranking policy: NaN effective score")
-            now, n_alive = int(o[0]), int(o[3])
-            n_finished += int(o[5])
-            tot_prefill += int(o[2])
+            now, iter_ns, prefill_ns, n_alive = int(out_np[0]), int(out_np[1]), int(out_np[2]), int(out_np[3])
+            n_finished += int(out_np[5])
+            tot_prefill += prefill_ns
             tot_pred += predictor_ns
-            tot_decode += int(o[1]) - int(o[2]) - predictor_ns
+            tot_decode += iter_ns - prefill_ns - predictor_ns
             if record:
-                ids = self.ids
+                ids, c = self.ids, cnt_np.tolist()
+                adm = [] if admitted is None else ids[admitted].tolist()
                 records.append({
-                    "step": step, "now_ns": now, "iter_ns": int(o[1]),
+                    "step": step, "now_ns": now, "iter_ns": iter_ns,
                     "run": ids[self.run_out[:c[0]].cpu().numpy()].tolist(),
-                    "preempted": ids[self.pre_out[:o[4]].cpu().numpy()].tolist(),
+                    "preempted": ids[self.pre_out[:int(out_np[4])].cpu().numpy()].tolist(),
                     "promoted": ids[self.prom_out[:c[1]].cpu().numpy()].tolist(),
                     "demoted": ids[self.dem_out[:c[2]].cpu().numpy()].tolist(),
-                    "admitted": ids[admitted].tolist(), "dropped": ids[dropped].tolist(),
-                    "finished": ids[self.fin_out[:o[5]].cpu().numpy()].tolist(),
-                    "scored": ids[admitted].tolist(), "predictor_ns": predictor_ns,
+                    "admitted": adm, "dropped": [] if dropped is None else ids[dropped].tolist(),
+                    "finished": ids[self.fin_out[:int(out_np[5])].cpu().numpy()].tolist(),
+                    "scored": adm, "predictor_ns": predictor_ns,
                 })
             step += 1
             if stop_after_finished is not None and n_finished >= stop_after_finished:
                 break
             if limit_ns is not None and now >= limit_ns:
                 break
-        rows = self._rows(dropped_all, nxt)
+        rows = self._rows(set(dropped_all), nxt)
         metrics = self._metrics(rows, now, step)
         metrics.update(total_prefill_ns=tot_prefill, total_decode_ns=tot_decode, total_predictor_ns=tot_pred)
         return EngineResult(metrics, rows, records, step)

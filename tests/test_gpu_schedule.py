@@ -118,3 +118,37 @@ def test_schedule_random_vs_oracle_large():
         assert (d.run, d.promoted, d.demoted) == (run, prom, dem)
         assert [(r.priority, r.starvation_count, r.quantum) for r in dev_reqs] == \
             [(r.priority, r.starvation_count, r.quantum) for r in ora_reqs]
+
+
+@pytest.mark.parametrize("n,max_batch,dist", [(3000, 256, "normal"), (100_000, 256, "ties"), (1 << 20, 1024, "normal"),
+                                              (50_000, 2048, "bf16"), (10_000, 1, "ties")])
+def test_topk_select_matches_full_sort(n, max_batch, dist):
+    """Unlimited KV uses the radix top-k select; a budget that never binds takes the
+    full-sort path. Both must give the same batch, promotions and state."""
+    import torch
+    from paper_2408_15792_b200 import _lib
+    from paper_2408_15792_b200.schedulers import DeviceQueue, SchedulerConfig
+    rng = np.random.default_rng(n + max_batch)
+    if dist == "normal":
+        score = rng.normal(size=n).astype(np.float32).astype(np.float64)
+    elif dist == "ties":
+        score = rng.integers(0, 7, n).astype(np.float64)
+    else:
+        score = rng.normal(size=n).astype(np.float32)
+        score = (score.view(np.uint32) & 0xFFFF0000).view(np.float32).astype(np.float64)
+    kw = dict(score=score, scored=rng.random(n) > 0.01, priority=rng.random(n) < 0.02, running=rng.random(n) < 0.3,
+              prompt_tokens=rng.integers(1, 100, n).astype(np.int32),
+              generated_tokens=rng.integers(0, 100, n).astype(np.int32), arrival_time=rng.random(n) * 100,
+              ids=rng.permutation(n).astype(np.int64), starvation=rng.integers(0, 100, n).astype(np.int32),
+              quantum=rng.integers(0, 3, n).astype(np.int32))
+    cfg = SchedulerConfig(max_batch=max_batch, starvation_threshold=50, priority_quantum=5)
+    out = []
+    for kv in (None, 1 << 60):
+        q = DeviceQueue.from_arrays(**kw)
+        q.rank_step(cfg, kv, length_calibrated=False)
+        d = q.decision()
+        out.append((d, q.flags.cpu().numpy().copy(), q.starvation.cpu().numpy().copy(), q.quantum.cpu().numpy().copy()))
+    (d0, f0, s0, q0), (d1, f1, s1, q1) = out
+    assert d0.run == d1.run and len(d0.run) == min(n, max_batch)
+    assert d0.promoted == d1.promoted and d0.demoted == d1.demoted
+    assert (f0 == f1).all() and (s0 == s1).all() and (q0 == q1).all()
