@@ -194,15 +194,34 @@ __global__ void __launch_bounds__(MS_THREADS) ms_block_sort(const K* __restrict_
 }
 
 // One global merge pass: runs of width w -> runs of width 2w over npad keys.
+// Merge-path split of every output tile boundary of a pass, one thread each (the
+// binary searches are dependent global loads: done here in parallel for all tiles
+// instead of serially at the start of every merging CTA).
+template <typename K>
+__global__ void ms_partition(const K* __restrict__ kin, uint32_t npad, uint32_t w, uint32_t tiles,
+                             int* __restrict__ split) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t > tiles) return;
+    const uint32_t out = t * MS_TILE;
+    if (t == tiles || out % (2 * w) == 0) {  // run-pair boundary: nothing taken yet
+        split[t] = 0;
+        return;
+    }
+    const uint32_t base = out / (2 * w) * (2 * w);
+    const int lenA = (int)min(w, npad - base);
+    const int lenB = (int)min(w, npad - base - (uint32_t)lenA);
+    split[t] = merge_path(kin + base, lenA, kin + base + lenA, lenB, (int)(out - base));
+}
+
 template <typename K, bool HasVal, bool Count>
 __global__ void __launch_bounds__(MS_THREADS) ms_merge_pass(const K* __restrict__ kin,
                                                             const uint32_t* __restrict__ vin,
                                                             K* __restrict__ kout,
                                                             uint32_t* __restrict__ vout,
                                                             uint32_t npad, uint32_t w,
-                                                            unsigned long long* inv_out) {
+                                                            unsigned long long* inv_out,
+                                                            const int* __restrict__ splits) {
     __shared__ MsSmem<K, HasVal> sm;
-    __shared__ int split[2];
     const uint32_t out0 = blockIdx.x * MS_TILE;
     const uint32_t base = out0 / (2 * w) * (2 * w);
     const int lenA = (int)min(w, npad - base);
@@ -211,9 +230,9 @@ __global__ void __launch_bounds__(MS_THREADS) ms_merge_pass(const K* __restrict_
     const K* B = kin + base + lenA;
     const int d0 = (int)(out0 - base);
     const int d1 = d0 + MS_TILE;
-    if (threadIdx.x < 2) split[threadIdx.x] = merge_path(A, lenA, B, lenB, threadIdx.x ? d1 : d0);
-    __syncthreads();
-    const int a0 = split[0], a1 = split[1];
+    // the tile's end split: the next tile's start, or the whole left run at a run end
+    const int a0 = splits[blockIdx.x];
+    const int a1 = (d1 == lenA + lenB) ? lenA : splits[blockIdx.x + 1];
     const int b0 = d0 - a0, b1 = d1 - a1;
     const int na = a1 - a0, nb = b1 - b0;
     for (int k = threadIdx.x; k < MS_TILE; k += MS_THREADS) {
@@ -254,12 +273,16 @@ static inline uint32_t ms_padded(uint64_t n) {
     return (uint32_t)((n + MS_TILE - 1) / MS_TILE * MS_TILE);
 }
 
+// ints of scratch merge_sort needs for the per-pass tile splits
+static inline uint32_t ms_splits(uint64_t n) { return (uint32_t)((n + MS_TILE - 1) / MS_TILE) + 2; }
+
 // Sort n keys (+ optional u32 payload). k0/k1 and v0/v1 are ping-pong buffers of
-// ms_padded(n) entries. On return *kres / *vres point at the sorted (padded) arrays.
+// ms_padded(n) entries, splits ms_splits(n) ints. On return *kres / *vres point at the
+// sorted (padded) arrays.
 template <typename K, bool HasVal, bool Count>
 int merge_sort(const K* keys_in, const uint32_t* vals_in, uint32_t n, K* k0, K* k1, uint32_t* v0,
                uint32_t* v1, unsigned long long* inv, cudaStream_t st, K** kres,
-               uint32_t** vres) {
+               uint32_t** vres, int* splits) {
     const uint32_t npad = ms_padded(n);
     const uint32_t tiles = npad / MS_TILE;
     if (tiles == 0) {
@@ -274,7 +297,9 @@ int merge_sort(const K* keys_in, const uint32_t* vals_in, uint32_t n, K* k0, K* 
     uint32_t* vi = v0;
     uint32_t* vo = v1;
     for (uint32_t w = MS_TILE; w < npad; w <<= 1) {
-        ms_merge_pass<K, HasVal, Count><<<tiles, MS_THREADS, 0, st>>>(ki, vi, ko, vo, npad, w, inv);
+        ms_partition<K><<<(tiles + 1 + 255) / 256, 256, 0, st>>>(ki, npad, w, tiles, splits);
+        RS_LAUNCH_CHECK();
+        ms_merge_pass<K, HasVal, Count><<<tiles, MS_THREADS, 0, st>>>(ki, vi, ko, vo, npad, w, inv, splits);
         RS_LAUNCH_CHECK();
         K* t = ki;
         ki = ko;

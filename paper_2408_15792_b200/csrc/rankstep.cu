@@ -437,6 +437,7 @@ struct RankWs {
     uint32_t* hist;
     RankKey* ck;
     uint32_t* ci;
+    int* splits;
 };
 template <typename A>
 static void rank_layout(A& a, uint64_t n, RankWs* w) {
@@ -455,7 +456,8 @@ static void rank_layout(A& a, uint64_t n, RankWs* w) {
     auto hi = a.template take<uint32_t>(SEL_BINS);
     auto ck = a.template take<RankKey>(SEL_SORT);
     auto ci = a.template take<uint32_t>(SEL_SORT);
-    if (w) *w = RankWs{ka, kb, va, vb, sc, pd, bc, er, sl, px, hi, ck, ci};
+    auto sp = a.template take<int>(ms_splits(np));
+    if (w) *w = RankWs{ka, kb, va, vb, sc, pd, bc, er, sl, px, hi, ck, ci, sp};
 }
 struct RankSizer {
     ArenaSizer s;
@@ -474,6 +476,7 @@ extern "C" size_t rs_arrival_rank_workspace_size(int64_t n) {
     s.take<Key128>(np);
     s.take<uint32_t>(np);
     s.take<uint32_t>(np);
+    s.take<int>(ms_splits(np));
     return s.used + 256;
 }
 
@@ -492,12 +495,13 @@ extern "C" int rs_arrival_rank(const double* arr, const int64_t* id, int64_t n, 
     Key128* kb = ar.take<Key128>(np);
     uint32_t* va = ar.take<uint32_t>(np);
     uint32_t* vb = ar.take<uint32_t>(np);
+    int* splits = ar.take<int>(ms_splits(np));
     const int T = 256;
     build_arrival_keys<<<(un + T - 1) / T, T, 0, st>>>(arr, id, un, kb);
     RS_LAUNCH_CHECK();
     Key128* sk;
     uint32_t* sv;
-    RS_TRY((merge_sort<Key128, true, false>(kb, nullptr, un, ka, kb, va, vb, nullptr, st, &sk, &sv)));
+    RS_TRY((merge_sort<Key128, true, false>(kb, nullptr, un, ka, kb, va, vb, nullptr, st, &sk, &sv, splits)));
     invert_perm<<<(un + T - 1) / T, T, 0, st>>>(sv, un, rank);
     RS_LAUNCH_CHECK();
     return RS_OK;
@@ -563,7 +567,7 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         RankKey* sk;
         uint32_t* order;
         RS_TRY((merge_sort<RankKey, true, false>(w.kb, nullptr, n, w.ka, w.kb, w.va, w.vb, nullptr, st, &sk,
-                                                 &order)));
+                                                 &order, w.splits)));
         if (kv_budget < 0) {
             fill_unlimited<<<(k + T - 1) / T, T, 0, st>>>(order, q->id, n, max_batch, run, w.sched, counts);
         } else {

@@ -172,6 +172,7 @@ struct TauWs {
     uint32_t* blk;
     unsigned long long* acc;
     int* flag;
+    int* splits;
 };
 
 template <typename A>
@@ -189,7 +190,8 @@ static void tau_layout(A& a, uint64_t n, bool need64, TauWs* w) {
     auto t_blk = a.template take<uint32_t>(nblk);
     auto t_acc = a.template take<unsigned long long>(8);
     auto t_flag = a.template take<int>(4);
-    if (w) *w = TauWs{t_ux, t_uy, t_ka, t_kb, t_32a, t_32b, t_va, t_vb, t_blk, t_acc, t_flag};
+    auto t_sp = a.template take<int>(ms_splits(np));
+    if (w) *w = TauWs{t_ux, t_uy, t_ka, t_kb, t_32a, t_32b, t_va, t_vb, t_blk, t_acc, t_flag, t_sp};
 }
 struct SizerAdapter {
     ArenaSizer s;
@@ -213,7 +215,7 @@ static int image_of(const void* v, int dt, uint32_t n, uint32_t* out, TauWs& w, 
     uint64_t* sk;
     uint32_t* sv;
     RS_TRY((merge_sort<uint64_t, true, false>(w.k64a, nullptr, n, w.k64b, w.k64a, w.va, w.vb, nullptr, st,
-                                              &sk, &sv)));
+                                              &sk, &sv, w.splits)));
     const uint32_t nb = (n + RK_THREADS - 1) / RK_THREADS;
     rank_heads_count<<<nb, RK_THREADS, 0, st>>>(sk, n, w.blk);
     RS_LAUNCH_CHECK();
@@ -264,7 +266,7 @@ extern "C" int rs_tau_counts(const void* x, int xd, const void* y, int yd, int64
     RS_LAUNCH_CHECK();
     uint64_t* sk;
     RS_TRY((merge_sort<uint64_t, false, false>(w.k64b, nullptr, un, w.k64a, w.k64b, nullptr, nullptr, nullptr,
-                                               st, &sk, nullptr)));
+                                               st, &sk, nullptr, w.splits)));
     tied_pairs<ProjHi><<<g, T, 0, st>>>(sk, un, ProjHi{}, w.acc + 1);
     RS_LAUNCH_CHECK();
     tied_pairs<ProjFull><<<g, T, 0, st>>>(sk, un, ProjFull{}, w.acc + 3);
@@ -273,7 +275,7 @@ extern "C" int rs_tau_counts(const void* x, int xd, const void* y, int yd, int64
     RS_LAUNCH_CHECK();
     uint32_t* sy;
     RS_TRY((merge_sort<uint32_t, false, true>(w.uy, nullptr, un, w.k32a, w.k32b, nullptr, nullptr, w.acc + 0, st,
-                                              &sy, nullptr)));
+                                              &sy, nullptr, w.splits)));
     tied_pairs32<<<g, T, 0, st>>>(sy, un, w.acc + 2);
     RS_LAUNCH_CHECK();
     // NaN keys are flagged in counts[5] (the reference's NaN behaviour is inconsistent

@@ -326,6 +326,7 @@ size_t embed_backward_ws(int n) {
     s.take<uint32_t>(np);
     s.take<uint32_t>(np);
     s.take<uint32_t>(np);
+    s.take<int>(ms_splits(np));
     return s.used + 256;
 }
 
@@ -343,10 +344,11 @@ int embed_backward(const int32_t* ids, int B, int S, int vocab, const float* dh,
     uint32_t* k1 = ar.take<uint32_t>(np);
     uint32_t* v0 = ar.take<uint32_t>(np);
     uint32_t* v1 = ar.take<uint32_t>(np);
+    int* splits = ar.take<int>(ms_splits(np));
     ids_to_keys_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n, vocab, keys);
     RS_LAUNCH_CHECK();
     uint32_t *sk, *sv;
-    RS_TRY((merge_sort<uint32_t, true, false>(keys, nullptr, n, k0, k1, v0, v1, nullptr, st, &sk, &sv)));
+    RS_TRY((merge_sort<uint32_t, true, false>(keys, nullptr, n, k0, k1, v0, v1, nullptr, st, &sk, &sv, splits)));
     embed_bwd_tok_kernel<<<(n + 7) / 8, 256, 0, st>>>(sk, sv, n, dh, d, dE);
     RS_LAUNCH_CHECK();
     embed_bwd_pos_kernel<<<S, 256, 0, st>>>(dh, B, S, d, dP);
