@@ -145,6 +145,7 @@ struct SelState {
     uint32_t done;              // 1: final level reached (prefix covers the k-th key)
     uint32_t final_level;
     uint32_t n_cand;
+    uint32_t arrived;  // blocks done with the current level's histogram
 };
 
 __device__ __forceinline__ unsigned __int128 sel_value(const RankKey& k) {
@@ -162,10 +163,12 @@ __device__ __forceinline__ unsigned long long sel_prefix(unsigned __int128 v, ui
     return levels == 0 ? 0ull : (unsigned long long)(v >> (99 - SEL_BITS * levels));
 }
 
+__device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c);
+
 __global__ void __launch_bounds__(SEL_THREADS) sel_hist(const RankKey* __restrict__ keys, uint32_t n,
-                                                        const SelState* __restrict__ st,
+                                                        SelState* __restrict__ st,
                                                         unsigned __int128* __restrict__ pfx128,
-                                                        uint32_t* __restrict__ hist) {
+                                                        uint32_t* __restrict__ hist, uint32_t k) {
     if (st->done) return;
     __shared__ uint32_t h[SEL_BINS];
     for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) h[b] = 0;
@@ -180,15 +183,23 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(const RankKey* __restric
     __syncthreads();
     for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS)
         if (h[b]) atomicAdd(&hist[b], h[b]);
+    // the last block to finish picks the bucket (no separate launch per level)
+    __threadfence();
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&st->arrived, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        sel_pick_block(st, pfx128, hist, k, h);
+    }
 }
 
-__global__ void __launch_bounds__(SEL_THREADS) sel_pick(SelState* __restrict__ st,
-                                                        unsigned __int128* __restrict__ pfx128,
-                                                        uint32_t* __restrict__ hist, uint32_t k) {
-    if (st->done) return;
-    __shared__ uint32_t c[SEL_BINS];
+// One block: choose the bucket holding the k-th key from the level's global histogram
+// (c = shared scratch of SEL_BINS words), clear the histogram for the next level.
+__device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c) {
     __shared__ uint32_t pick, below;
-    for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) c[b] = hist[b];
+    for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) c[b] = __ldcg(&hist[b]);
     __syncthreads();
     if (threadIdx.x == 0) {
         const uint32_t need = k - st->less;  // >= 1
@@ -207,6 +218,7 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_pick(SelState* __restrict__ s
         *pfx128 |= (unsigned __int128)pick << (88 - SEL_BITS * level);
         st->less += below;
         st->level = level + 1;
+        st->arrived = 0;
         if (c[pick] <= SEL_CAP || level + 1 == SEL_LEVELS) {
             st->done = 1;
             st->final_level = level + 1;
@@ -555,9 +567,7 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         RS_CUDA(cudaMemsetAsync(w.hist, 0, SEL_BINS * sizeof(uint32_t), st));
         const uint32_t gb = min((n + SEL_THREADS - 1) / SEL_THREADS, 296u);
         for (int level = 0; level < SEL_LEVELS; ++level) {
-            sel_hist<<<gb, SEL_THREADS, 0, st>>>(w.kb, n, w.sel, w.pfx, w.hist);
-            RS_LAUNCH_CHECK();
-            sel_pick<<<1, SEL_THREADS, 0, st>>>(w.sel, w.pfx, w.hist, k);
+            sel_hist<<<gb, SEL_THREADS, 0, st>>>(w.kb, n, w.sel, w.pfx, w.hist, k);
             RS_LAUNCH_CHECK();
         }
         sel_gather<<<gb, SEL_THREADS, 0, st>>>(w.kb, n, w.sel, w.pfx, w.ck, w.ci);
