@@ -154,6 +154,34 @@ __global__ void reduce_rows_add_kernel(const float* __restrict__ part, int n_par
     out[c] += acc;
 }
 
+// First level of a two-level column reduction: scratch[g][c] = sum of partial rows
+// [64 g, 64 g + 64) (fixed order), so no thread walks thousands of dependent rows.
+__global__ void reduce_rows_group_kernel(const float* __restrict__ part, int n_part, int cols,
+                                         float* __restrict__ scratch) {
+    const int c = blockIdx.y * blockDim.x + threadIdx.x;
+    if (c >= cols) return;
+    const int p0 = blockIdx.x * 64, p1 = min(n_part, p0 + 64);
+    float acc = 0.f;
+    for (int p = p0; p < p1; ++p) acc += part[(size_t)p * cols + c];
+    scratch[(size_t)blockIdx.x * cols + c] = acc;
+}
+
+// out[c] += sum of the n_part partial rows of `part` (deterministic; scratch holds
+// ceil(n_part / 64) rows and must not overlap part).
+static int reduce_rows_add(const float* part, int n_part, int cols, float* out, float* scratch, cudaStream_t st) {
+    if (n_part <= 64) {
+        reduce_rows_add_kernel<<<(cols + 255) / 256, 256, 0, st>>>(part, n_part, cols, out);
+        RS_LAUNCH_CHECK();
+        return RS_OK;
+    }
+    const int g = (n_part + 63) / 64;
+    reduce_rows_group_kernel<<<dim3(g, (cols + 255) / 256), 256, 0, st>>>(part, n_part, cols, scratch);
+    RS_LAUNCH_CHECK();
+    reduce_rows_add_kernel<<<(cols + 255) / 256, 256, 0, st>>>(scratch, g, cols, out);
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
 // out[i] += sum over k of part[k * n + i] (split-K partial slices, fixed order).
 __global__ void reduce_slices_add_kernel(const float* __restrict__ part, int k, int64_t n, float* __restrict__ out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -293,9 +321,7 @@ int ln_backward(const float* dy, const float* x, const void* w, float* dh, void*
     // part rows are [dw | db] of 2d columns: reduce both halves in one pass into
     // a contiguous [dw_out, db_out] pair (the callers' LN weight and bias are adjacent).
     (void)db_out;
-    reduce_rows_add_kernel<<<(2 * d + 255) / 256, 256, 0, st>>>(part, nblk, 2 * d, dw_out);
-    RS_LAUNCH_CHECK();
-    return RS_OK;
+    return reduce_rows_add(part, nblk, 2 * d, dw_out, part + (size_t)nblk * 2 * d, st);
 }
 
 int colsum_add(const void* x, bool is_bf16, int rows, int cols, float* part, float* out, cudaStream_t st) {
@@ -307,9 +333,7 @@ int colsum_add(const void* x, bool is_bf16, int rows, int cols, float* part, flo
     else
         colsum_partial_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(x), rows, cols, part);
     RS_LAUNCH_CHECK();
-    reduce_rows_add_kernel<<<(cols + 255) / 256, 256, 0, st>>>(part, nblk, cols, out);
-    RS_LAUNCH_CHECK();
-    return RS_OK;
+    return reduce_rows_add(part, nblk, cols, out, part + (size_t)nblk * cols, st);
 }
 
 int slices_add(const float* part, int k, int64_t n, float* out, cudaStream_t st) {
@@ -374,8 +398,7 @@ int head_backward(const float* h, const int32_t* last, int B, int S, const void*
     const int cols = 3 * d + 1;
     float* tot = part + (size_t)B * cols;
     RS_CUDA(cudaMemsetAsync(tot, 0, cols * sizeof(float), st));
-    reduce_rows_add_kernel<<<(cols + 255) / 256, 256, 0, st>>>(part, B, cols, tot);
-    RS_LAUNCH_CHECK();
+    RS_TRY(reduce_rows_add(part, B, cols, tot, tot + cols, st));
     // scatter: d hw -> g_hw, (d lnf_w, d lnf_b) -> g_lnf (adjacent), d hb -> g_hb
     reduce_rows_add_kernel<<<(d + 255) / 256, 256, 0, st>>>(tot, 1, d, g_hw);
     RS_LAUNCH_CHECK();
