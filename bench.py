@@ -194,7 +194,7 @@ def gemm_roofline(pk, M=1 << 20, reps=5):
     chunk shape; achieved = algorithmic FLOPs per launch / average launch time."""
     from paper_2408_15792_b200 import _lib
     lib = _lib.load()
-    shapes = [(2304, 768, 0), (768, 768, 2), (3072, 768, 1), (768, 3072, 2)]
+    shapes = [(2304, 768, 7), (768, 768, 2), (3072, 768, 1), (768, 3072, 2)]
     res = []
     tot_f = tot_t = 0.0
     for N, K, epi in shapes:
@@ -215,9 +215,19 @@ def gemm_roofline(pk, M=1 << 20, reps=5):
         tot_t += t
         del A, W, C
     achieved = tot_f / tot_t / 1e9
-    return {"bound": "tensor", "kernel": "gemm_bf16_kernel (tcgen05, 4 OPT projections, M=2^20)",
+    # DRAM bytes of the same four launches from the committed ncu --set full capture
+    traffic = None
+    tp = ROOT / "profiles" / "r01_gemm_traffic.json"
+    if tp.exists():
+        tr = json.loads(tp.read_text())["per_shape"]
+        keys = [f"{N}x{K}" for N, K, _ in shapes]
+        if all(k in tr for k in keys):
+            traffic = sum((tr[k]["dram_read_gb"] + tr[k]["dram_write_gb"]) * 1e9 for k in keys)
+    return {"bound": "tensor", "kernel": "gemm_bf16_2sm_kernel (tcgen05 CTA pair; the 4 OPT projections at M=2^20, "
+                                         "one launch each)",
             "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_tflops"],
-            "traffic": None, "per_shape": res}
+            "traffic": traffic, "traffic_unit": "bytes per launch set (ncu dram read + write)",
+            "algorithmic_flops": tot_f, "per_shape": res}
 
 
 def tau_and_rankstep(pk, reps=5):
