@@ -38,9 +38,9 @@ constexpr int AT_THREADS = 384;
 // Warp roles. The SM's warp schedulers favour higher warp ids, so the latency-critical
 // control warps sit above the 8 softmax warps (else the MMA issuer starves behind them).
 constexpr int AT_W_KV = 8, AT_W_MMA = 9, AT_W_Q0 = 10;  // + AT_W_Q0 + 1; softmax: warps 0-7
-constexpr int AT_KVB = 5;  // K/V ring depth (one group of <= 4 blocks + a spare)
-// Q [2 slots][2] + K, V [AT_KVB] + barriers (224 KB + 2 KB)
-constexpr int AT_SMEM = (4 + 2 * AT_KVB) * AT_BUF + 1024 + 1024;
+constexpr int AT_KVB = 4;  // K/V ring depth (one group of <= 4 blocks)
+// Q [2 slots][2] + K, V [AT_KVB] + the fp16 "ones" tile (F16V) + barriers
+constexpr int AT_SMEM = (4 + 2 * AT_KVB + 1) * AT_BUF + 1024 + 1024;
 constexpr float AT_RESCALE = 8.0f;  // lazy-rescale threshold (log2 units)
 
 struct AtBars {
@@ -153,7 +153,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     uint8_t* sQ = smem;                  // [slot][2]
     uint8_t* sK = sQ + 4 * AT_BUF;       // [AT_KVB]
     uint8_t* sV = sK + AT_KVB * AT_BUF;  // [AT_KVB]
-    AtBars* bar = reinterpret_cast<AtBars*>(sV + AT_KVB * AT_BUF);
+    uint8_t* sOnes = sV + AT_KVB * AT_BUF;  // F16V: 128 keys x 64 fp16, column 0 = 1
+    AtBars* bar = reinterpret_cast<AtBars*>(sOnes + AT_BUF);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n_qt = (S + AT_TILE - 1) / AT_TILE;
@@ -180,6 +181,18 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
         fence_barrier_init();
     }
     if (warp == AT_W_Q0) tmem_alloc<512>(&bar->tmem);
+    if (F16V) {
+        // The PV MMA runs with N = 80: V (64 columns) plus this tile as the next 64-wide
+        // MN chunk, whose first column is all ones, so O column 64 accumulates the row sum
+        // of the fp16 P the MMA actually used (no ALU sums). MN-major SW128 layout: key
+        // row k at k * 128 B, 16-B chunk c stored at position c ^ (k % 8).
+        for (int i = threadIdx.x; i < AT_BUF / 16; i += AT_THREADS) {
+            const int k = i >> 3, cpos = i & 7;
+            const uint32_t one = (cpos == (k & 7)) ? 0x3C00u : 0u;  // chunk 0 holds column 0
+            reinterpret_cast<uint4*>(sOnes)[i] = make_uint4(one, 0u, 0u, 0u);
+        }
+        fence_proxy_async_smem();
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -231,8 +244,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
     } else if (warp == AT_W_MMA) {
         if (elect_one()) {
             constexpr uint32_t id_s = idesc_bf16(AT_TILE, AT_TILE);
-            // PV: bf16 P x bf16 V, or fp16 P x fp16 V (N = 64)
-            constexpr uint32_t id_o = F16V ? (idesc_bf16(AT_TILE, AT_D, 0, 1) & ~((7u << 7) | (7u << 10)))
+            // PV: bf16 P x bf16 V (N = 64), or fp16 P x [fp16 V | ones] (N = 80)
+            constexpr uint32_t id_o = F16V ? (idesc_bf16(AT_TILE, AT_D + 16, 0, 1) & ~((7u << 7) | (7u << 10)))
                                            : idesc_bf16(AT_TILE, AT_D, 0, 1);
             // All MMA-issuer state stays in registers: with ~225 KB of shared memory the L1
             // left for local memory is tiny, and a spilled / dynamically indexed array costs
@@ -278,10 +291,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                     ++c.bseq;
                     tc_fence_after();
                     const uint32_t vb = smem_u32(sV + buf * AT_BUF);
+                    const uint32_t lbo = F16V ? (uint32_t)(sOnes - (sV + buf * AT_BUF)) : 8192u;  // V -> ones
 #pragma unroll
                     for (int kk = 0; kk < AT_TILE / 16; ++kk)
                         mma_bf16_ts(tmem + slot * 256 + 128, tmem + slot * 256 + kk * 8,
-                                    desc_mnmajor_sw128(vb + kk * 2048, 8192), id_o, (c.j != c.t) || kk != 0);
+                                    desc_mnmajor_sw128(vb + kk * 2048, lbo), id_o, (c.j != c.t) || kk != 0);
                     uses -= 1u << (4 * buf);
                     if (((uses >> (4 * buf)) & 15u) == 0) mma_commit(&bar->kv_empty[buf]);
                     if (c.j == 0) {  // tile done: O is final once this PV retires
@@ -393,12 +407,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                             } else {
                                 exp2_poly2(x0, x1, p0, p1);
                             }
-                            lsum[(e >> 1) & 3] = fadd2(lsum[(e >> 1) & 3], f2pack(p0, p1));
-                            pk[e / 2] = F16V ? pack_f16(p0, p1) : pack_bf16(p0, p1);
+                            if (F16V) {
+                                pk[e / 2] = pack_f16(p0, p1);  // row sum: O column 64 (ones column)
+                            } else {
+                                lsum[(e >> 1) & 3] = fadd2(lsum[(e >> 1) & 3], f2pack(p0, p1));
+                                pk[e / 2] = pack_bf16(p0, p1);
+                            }
                         }
                         tmem_st_32x32b_x16(tS + cc * 16, pk);
                     }
-                    {
+                    if (!F16V) {
                         float l0, l1;
                         f2unpack(fadd2(fadd2(lsum[0], lsum[1]), fadd2(lsum[2], lsum[3])), l0, l1);
                         l = l * alpha + l0 + l1;
@@ -407,7 +425,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                         // O holds PV of the earlier blocks,
                         // retired: the S commit covers them
 #pragma unroll
-                        for (int hh = 0; hh < 2; ++hh) {
+                        for (int hh = 0; hh < (F16V ? 3 : 2); ++hh) {  // F16V: + the row-sum column
                             uint32_t o[32];
                             tmem_ld_32x32b_x32(tO + hh * 32, o);
                             tmem_ld_wait();
@@ -427,7 +445,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                 uint32_t o[64];
                 tmem_ld_32x32b_x32(tO, *reinterpret_cast<uint32_t(*)[32]>(&o[0]));
                 tmem_ld_32x32b_x32(tO + 32, *reinterpret_cast<uint32_t(*)[32]>(&o[32]));
-                tmem_ld_wait();
+                if (F16V) {
+                    uint32_t ls;
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(ls) : "r"(tO + 64));
+                    tmem_ld_wait();
+                    l = __uint_as_float(ls);
+                } else {
+                    tmem_ld_wait();
+                }
                 tc_fence_before();
                 const float inv = 1.f / l;
                 const int qi = t * AT_TILE + r;
