@@ -42,6 +42,10 @@ constexpr int AT_KVB = 4;  // K/V ring depth (one group of <= 4 blocks)
 // Q [2 slots][2] + K, V [AT_KVB] + the fp16 "ones" tile (F16V) + barriers
 constexpr int AT_SMEM = (4 + 2 * AT_KVB + 1) * AT_BUF + 1024 + 1024;
 constexpr float AT_RESCALE = 8.0f;  // lazy-rescale threshold (log2 units)
+// which of every 8 exponential pairs go to MUFU (bit set) vs the FMA-pipe polynomial
+#ifndef AT_MUFU_MASK
+#define AT_MUFU_MASK 0x57u  // 5 of 8 on MUFU (measured best of 0x11, 0x15, 0x55, 0x57, 0x77)
+#endif
 
 struct AtBars {
     uint64_t q_full[2][2], q_empty[2][2];
@@ -401,7 +405,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                             float x0, x1;
                             f2unpack(ffma2(f2pack(__uint_as_float(v[e]), __uint_as_float(v[e + 1])), c2, nm2), x0, x1);
                             float p0, p1;
-                            if ((e & 2) == 0) {  // half on MUFU, half on the FMA pipe
+                            if (((AT_MUFU_MASK >> ((e >> 1) & 7)) & 1) != 0) {  // MUFU, else the FMA pipe
                                 p0 = exp2_mufu(x0);
                                 p1 = exp2_mufu(x1);
                             } else {
