@@ -241,7 +241,11 @@ def tau_and_rankstep(pk, reps=5):
     xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
     out = torch.empty(6, dtype=torch.int64, device="cuda")
     ranking.tau_counts_device(xd, yd, out)
-    t = timed(lambda: ranking.tau_counts_device(xd, yd, out), reps)
+    t_eager = timed(lambda: ranking.tau_counts_device(xd, yd, out), reps)
+    plan = ranking.TauPlan(xd, yd)  # same kernels, replayed as one CUDA graph
+    plan()
+    t = timed(plan, reps)
+    assert torch.equal(plan.out, out), "graph and eager tau counts differ"
     n = len(x)
     pairs = n * (n - 1) / 2
     tau_bytes = 8.0 * n
@@ -257,17 +261,21 @@ def tau_and_rankstep(pk, reps=5):
         dq.rank_step(cfg, None, length_calibrated=False)
 
     step()
+    tr_eager = timed(step, reps)
+    step = dq.rank_step_graph(cfg, None, length_calibrated=False)
+    step()
     tr = timed(step, reps)
     for dst, src in zip((dq.flags, dq.starvation, dq.quantum), snap):
         dst.copy_(src)
     rs_bytes = 34.0 * n
     return {
         "tau": {"metric": "Kendall tau-b pairs/sec (exact counts)", "value": pairs / (t / 1e3), "unit": "pairs/s",
-                "n": n, "ms": t, "roofline": {"bound": "hbm", "achieved": tau_bytes / t / 1e6, "peak": pk["hbm_gbs"],
+                "n": n, "ms": t, "ms_eager": t_eager, "note": "ms: the kernels replayed as one CUDA graph",
+                "roofline": {"bound": "hbm", "achieved": tau_bytes / t / 1e6, "peak": pk["hbm_gbs"],
                                               "unit": "GB/s", "frac": tau_bytes / t / 1e6 / pk["hbm_gbs"],
                                               "traffic": None, "algorithmic_bytes": tau_bytes}},
         "rank_step": {"metric": "requests ranked/sec (sort + fill + starvation bump)", "value": n / (tr / 1e3),
-                      "unit": "requests/s", "n": n, "ms": tr,
+                      "unit": "requests/s", "n": n, "ms": tr, "ms_eager": tr_eager,
                       "roofline": {"bound": "hbm", "achieved": rs_bytes / tr / 1e6, "peak": pk["hbm_gbs"],
                                    "unit": "GB/s", "frac": rs_bytes / tr / 1e6 / pk["hbm_gbs"], "traffic": None,
                                    "algorithmic_bytes": rs_bytes}},

@@ -75,6 +75,42 @@ def tau_counts_device(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None
     return out
 
 
+class TauPlan:
+    """rs_tau_counts for fixed device inputs, captured once as a CUDA graph.
+
+    At ~1M rows the exact count is launch-bound (two merge sorts: ~50 small kernels); a
+    graph replays the same kernels with one launch. x, y and out must keep their
+    storage for the plan's lifetime (the graph holds their addresses); the plan owns
+    its workspace.
+    """
+
+    def __init__(self, x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None):
+        if x.numel() != y.numel() or not x.is_cuda or not y.is_cuda:
+            raise ValueError("TauPlan expects two equal-length CUDA tensors")
+        self.x, self.y = x, y
+        self.dev = x.device
+        self.out = out if out is not None else torch.empty(6, dtype=torch.int64, device=self.dev)
+        lib = _lib.load()
+        self._xd, self._yd = _TORCH_DT[x.dtype], _TORCH_DT[y.dtype]
+        self._ws = torch.empty(max(lib.rs_tau_workspace_size(x.numel(), self._xd, self._yd), 1), dtype=torch.uint8,
+                               device=self.dev)
+        self._call()  # eager once (one-time kernel attributes), then capture
+        torch.cuda.synchronize(self.dev)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._call()
+
+    def _call(self):
+        lib = _lib.load()
+        _lib.check(lib.rs_tau_counts(self.x.data_ptr(), self._xd, self.y.data_ptr(), self._yd, self.x.numel(),
+                                     self.out.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
+                                     _lib.stream_handle(self.dev)), "rs_tau_counts")
+
+    def __call__(self) -> torch.Tensor:
+        self.graph.replay()
+        return self.out
+
+
 def tau_from_counts(counts, n: int) -> TauResult:
     """Finish tau exactly as the reference does (ranking.py:58-63), on Python ints."""
     c, d, n1, n2, _n3, nan = (int(v) for v in counts)

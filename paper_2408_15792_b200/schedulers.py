@@ -141,6 +141,32 @@ class DeviceQueue:
                                     self.prom_out.data_ptr(), self.dem_out.data_ptr(), self.counts.data_ptr(),
                                     ws, wn, _lib.stream_handle(self.dev)), "rs_rank_step")
 
+    def rank_step_graph(self, config: SchedulerConfig, kv_budget: int | None, length_calibrated: bool,
+                        preemptive: bool = True):
+        """rank_step captured once as a CUDA graph for this queue (fixed n and buffers):
+        returns a callable that replays it (one launch instead of ~20 at 1M rows)."""
+        lib = _lib.load()
+        ws = torch.empty(max(lib.rs_rank_step_workspace_size(self.n), 1), dtype=torch.uint8, device=self.dev)
+        if self.run_out.numel() < config.max_batch:
+            self.run_out = torch.empty(config.max_batch, dtype=torch.int64, device=self.dev)
+        budget = -1 if kv_budget is None or kv_budget >= UNLIMITED_KV else int(kv_budget)
+        soa = self.soa()
+
+        def call():
+            _lib.check(lib.rs_rank_step(ctypes.byref(soa), config.max_batch, budget, config.starvation_threshold,
+                                        config.priority_quantum, int(length_calibrated),
+                                        int(preemptive and config.preemption), self.run_out.data_ptr(),
+                                        self.prom_out.data_ptr(), self.dem_out.data_ptr(), self.counts.data_ptr(),
+                                        ws.data_ptr(), ws.numel(), _lib.stream_handle(self.dev)), "rs_rank_step")
+
+        call()  # eager once (one-time kernel attributes), then capture
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            call()
+        self._graph_keep = (g, ws, soa)
+        return g.replay
+
     def decision(self) -> BatchDecision:
         c = self.counts.cpu().tolist()
         if c[3]:

@@ -85,3 +85,19 @@ def test_tau_large_n_properties():
     assert cp[:5] == c[:5]
     cs = tau_counts_device(y, y).cpu().tolist()
     assert cs[1] == 0 and cs[0] == n0 - cs[2]
+
+
+def test_tau_plan_graph_matches_eager():
+    """TauPlan (the kernels captured as one CUDA graph) gives the eager counts, and
+    replays track input updates made in place."""
+    import torch
+    from paper_2408_15792_b200 import ranking
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(300_000, device="cuda", generator=g)
+    y = torch.randint(1, 2049, (300_000,), device="cuda", generator=g, dtype=torch.int32)
+    plan = ranking.TauPlan(x, y)
+    want = ranking.tau_counts_device(x, y).clone()
+    assert torch.equal(plan(), want)
+    x.copy_(torch.randn(300_000, device="cuda", generator=g))
+    want2 = ranking.tau_counts_device(x, y).clone()
+    assert torch.equal(plan(), want2) and not torch.equal(want, want2)
