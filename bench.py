@@ -311,6 +311,19 @@ def size_sweep(pk, reps=3):
         out["rank_step"].append({"n": n, "ms": t, "requests_per_s": n / (t / 1e3), "achieved_gbs": 34.0 * n / t / 1e6,
                                  "frac": 34.0 * n / t / 1e6 / pk["hbm_gbs"]})
         del dq
+    # ListMLE loss + grad in the training form (12.06 B/item = g fp32 +
+    # length int32 read, dg fp32 written, + 4 B loss per list), 1M lists x 64 = 809.5 MB.
+    out["listmle"] = []
+    for n_lists in (1 << 20,):
+        L = 64
+        gl = torch.randn(n_lists, L, device="cuda", generator=g)
+        ln = torch.randint(1, 2049, (n_lists, L), device="cuda", generator=g, dtype=torch.int32)
+        ranking.listmle_from_lengths(gl, ln)
+        t = timed(lambda: ranking.listmle_from_lengths(gl, ln), reps)
+        nbytes = 12.0 * n_lists * L + 4.0 * n_lists
+        out["listmle"].append({"lists": n_lists, "list_len": L, "ms": t, "items_per_s": n_lists * L / (t / 1e3),
+                               "achieved_gbs": nbytes / t / 1e6, "frac": nbytes / t / 1e6 / pk["hbm_gbs"]})
+        del gl, ln
     torch.cuda.empty_cache()
     return out
 

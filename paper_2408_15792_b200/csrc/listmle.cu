@@ -167,6 +167,254 @@ __global__ void listmle_lengths_kernel(const float* __restrict__ gnet, const int
     for (int k = lane; k < L; k += 32) dg[k] = gt[rank[k]] * inv;
 }
 
+// ---- register-resident form for lists of <= 64 items (the cfg3 shape) -------------------
+// One warp per list, two items per lane, nothing staged in shared memory. Target order
+// = a warp bitonic sort of the unique keys (label, index); the two log-sum-exp scans run
+// on (max, scaled-sum) pairs in base 2 — one ex2 per combine instead of the exp + log1p of
+// logaddexp — so the kernel is ALU/MUFU-light enough to stream at a good HBM fraction.
+// Element p of the sorted sequence lives in lane p >> 1, slot p & 1.
+struct Lse2 {
+    float m, s;  // value = m + log2(s); identity (LSE2_NONE, 0)
+};
+
+__device__ __forceinline__ float fast_ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float fast_lg2(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Identity element: a finite sentinel instead of -inf keeps (identity, identity) free
+// of inf - inf (ex2(0) * 0 = 0), so the combine needs no branch.
+constexpr float LSE2_NONE = -1e30f;
+
+__device__ __forceinline__ Lse2 lse2_comb(Lse2 a, Lse2 b) {
+    const bool ab = a.m >= b.m;
+    const float M = fmaxf(a.m, b.m), mn = fminf(a.m, b.m);
+    const float sb = ab ? a.s : b.s, ss = ab ? b.s : a.s;
+    return Lse2{M, fmaf(ss, fast_ex2(mn - M), sb)};
+}
+
+__device__ __forceinline__ Lse2 shfl_down_lse2(Lse2 v, int o) {
+    return Lse2{__shfl_down_sync(0xffffffffu, v.m, o), __shfl_down_sync(0xffffffffu, v.s, o)};
+}
+__device__ __forceinline__ Lse2 shfl_up_lse2(Lse2 v, int o) {
+    return Lse2{__shfl_up_sync(0xffffffffu, v.m, o), __shfl_up_sync(0xffffffffu, v.s, o)};
+}
+
+template <typename K>
+__device__ __forceinline__ K kmin(K a, K b) { return a < b ? a : b; }
+template <>
+__device__ __forceinline__ uint32_t kmin<uint32_t>(uint32_t a, uint32_t b) { return min(a, b); }
+template <typename K>
+__device__ __forceinline__ K kmax(K a, K b) { return a < b ? b : a; }
+template <>
+__device__ __forceinline__ uint32_t kmax<uint32_t>(uint32_t a, uint32_t b) { return max(a, b); }
+
+template <typename K>
+__device__ __forceinline__ void warp_bitonic64(K& e0, K& e1) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+        const bool asc = ((2 * lane) & k) == 0;  // for k >= 4, (p & k) is the same for both slots
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 1) {
+                const K lo = kmin(e0, e1), hi = kmax(e0, e1);
+                e0 = asc ? lo : hi;
+                e1 = asc ? hi : lo;
+            } else {
+                const int lm = j >> 1;
+                const bool take_min = ((lane & lm) == 0) == asc;
+                const K o0 = __shfl_xor_sync(0xffffffffu, e0, lm);
+                const K o1 = __shfl_xor_sync(0xffffffffu, e1, lm);
+                e0 = take_min ? kmin(o0, e0) : kmax(o0, e0);
+                e1 = take_min ? kmin(o1, e1) : kmax(o1, e1);
+            }
+        }
+    }
+}
+
+// Keys below 2^16 (labels < 1023: lengths < 10230 at the default width) sort two per
+// register: the pair of a lane shares its compare direction and partner lane at every
+// shuffle stage, so one u16x2 min/max does both slots.
+__device__ __forceinline__ uint32_t vmin16x2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("min.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+__device__ __forceinline__ uint32_t vmax16x2(uint32_t a, uint32_t b) {
+    uint32_t d;
+    asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+    return d;
+}
+
+__device__ __forceinline__ uint32_t warp_bitonic64_packed(uint32_t P) {  // slot 0 low, slot 1 high
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 2; k <= 64; k <<= 1) {
+        const bool asc = ((2 * lane) & k) == 0;
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 1) {
+                const uint32_t Q = __byte_perm(P, 0, 0x1032);  // halves swapped
+                const uint32_t mn = vmin16x2(P, Q), mx = vmax16x2(P, Q);
+                P = __byte_perm(asc ? mn : mx, asc ? mx : mn, 0x7610);
+            } else {
+                const int lm = j >> 1;
+                const bool take_min = ((lane & lm) == 0) == asc;
+                const uint32_t O = __shfl_xor_sync(0xffffffffu, P, lm);
+                P = take_min ? vmin16x2(O, P) : vmax16x2(O, P);
+            }
+        }
+    }
+    return P;
+}
+
+// Sorted slot -> item index, for the three key widths.
+__device__ __forceinline__ void listmle64_order(int lab0, int lab1, int L, int& s0, int& s1) {
+    const int lane = threadIdx.x & 31;
+    const int i0 = lane, i1 = lane + 32;
+    const bool ok0 = i0 >= L || (lab0 >= 0 && lab0 < 1023), ok1 = i1 >= L || (lab1 >= 0 && lab1 < 1023);
+    if (__all_sync(0xffffffffu, ok0 && ok1)) {
+        const uint32_t k0 = i0 < L ? ((uint32_t)lab0 << 6) | (uint32_t)i0 : 0xFFFFu;
+        const uint32_t k1 = i1 < L ? ((uint32_t)lab1 << 6) | (uint32_t)i1 : 0xFFFFu;
+        const uint32_t P = warp_bitonic64_packed(k0 | (k1 << 16));
+        s0 = (int)(P & 63);
+        s1 = (int)((P >> 16) & 63);
+        return;
+    }
+    const bool w0 = i0 >= L || (lab0 >= 0 && lab0 < (1 << 25)), w1 = i1 >= L || (lab1 >= 0 && lab1 < (1 << 25));
+    if (__all_sync(0xffffffffu, w0 && w1)) {
+        uint32_t k0 = i0 < L ? ((uint32_t)lab0 << 6) | (uint32_t)i0 : ~0u;
+        uint32_t k1 = i1 < L ? ((uint32_t)lab1 << 6) | (uint32_t)i1 : ~0u;
+        warp_bitonic64<uint32_t>(k0, k1);
+        s0 = (int)(k0 & 63);
+        s1 = (int)(k1 & 63);
+        return;
+    }
+    uint64_t k0 = i0 < L ? ((uint64_t)((uint32_t)lab0 ^ 0x80000000u) << 32) | (uint64_t)i0 : ~0ull;
+    uint64_t k1 = i1 < L ? ((uint64_t)((uint32_t)lab1 ^ 0x80000000u) << 32) | (uint64_t)i1 : ~0ull;
+    warp_bitonic64<uint64_t>(k0, k1);
+    s0 = (int)(k0 & 63);
+    s1 = (int)(k1 & 63);
+}
+
+__device__ __forceinline__ float warp_max_f(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Scores in target order (t0 at p = 2 lane, t1 at p + 1; base-2 units) -> loss and grads.
+__device__ __forceinline__ void listmle64_scan(float t0, float t1, bool v0, bool v1, int L, float inv, int s0,
+                                               int s1, float* __restrict__ loss_out, float* __restrict__ dg) {
+    const int lane = threadIdx.x & 31;
+    constexpr float LN2 = 0.6931471805599453f;
+    float lse0, lse1, L0, L1;
+    const float M = warp_max_f(fmaxf(v0 ? t0 : LSE2_NONE, v1 ? t1 : LSE2_NONE));
+    const float m = -warp_max_f(fmaxf(v0 ? -t0 : LSE2_NONE, v1 ? -t1 : LSE2_NONE));
+    if (M - m <= 100.f) {
+        // Range fits fp32 after one shift by the list max (every 2^(t - M) >= 2^-100 is a
+        // normal float), so both log-sum-exps are plain prefix sums of shifted exponentials.
+        const float w0 = v0 ? fast_ex2(t0 - M) : 0.f, w1 = v1 ? fast_ex2(t1 - M) : 0.f;
+        const float r0 = w0 + w1;
+        float x = r0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float y = __shfl_down_sync(0xffffffffu, x, o);
+            if (lane + o < 32) x += y;
+        }
+        float tail = __shfl_down_sync(0xffffffffu, x, 1);
+        if (lane == 31) tail = 0.f;
+        lse0 = M + fast_lg2(r0 + tail);
+        lse1 = M + fast_lg2(w1 + tail);
+        // -lse is largest at the last item (lse_{L-1} = t_{L-1}), the shift of the second sum
+        const float lastv = ((L - 1) & 1) ? lse1 : lse0;
+        const float Mu = -__shfl_sync(0xffffffffu, lastv, (L - 1) >> 1);
+        const float q0 = v0 ? fast_ex2(-lse0 - Mu) : 0.f, q1 = v1 ? fast_ex2(-lse1 - Mu) : 0.f;
+        const float c1 = q0 + q1;
+        x = c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        float head = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane == 0) head = 0.f;
+        L0 = Mu + fast_lg2(head + q0);
+        L1 = Mu + fast_lg2(head + c1);
+    } else {
+        // wide range: (max, scaled-sum) pairs
+        const Lse2 e1{v1 ? t1 : LSE2_NONE, v1 ? 1.f : 0.f};
+        const Lse2 e0 = lse2_comb(Lse2{v0 ? t0 : LSE2_NONE, v0 ? 1.f : 0.f}, e1);
+        Lse2 x = e0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const Lse2 y = shfl_down_lse2(x, o);
+            if (lane + o < 32) x = lse2_comb(x, y);
+        }
+        Lse2 tail = shfl_down_lse2(x, 1);
+        if (lane == 31) tail = Lse2{LSE2_NONE, 0.f};
+        const Lse2 l0 = lse2_comb(e0, tail), l1 = lse2_comb(e1, tail);
+        lse0 = l0.m + fast_lg2(l0.s);
+        lse1 = l1.m + fast_lg2(l1.s);
+        const Lse2 f0{v0 ? -lse0 : LSE2_NONE, v0 ? 1.f : 0.f};
+        const Lse2 f1 = lse2_comb(f0, Lse2{v1 ? -lse1 : LSE2_NONE, v1 ? 1.f : 0.f});
+        x = f1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const Lse2 y = shfl_up_lse2(x, o);
+            if (lane >= o) x = lse2_comb(x, y);
+        }
+        Lse2 head = shfl_up_lse2(x, 1);
+        if (lane == 0) head = Lse2{LSE2_NONE, 0.f};
+        const Lse2 c0 = lse2_comb(head, f0), c1 = lse2_comb(head, f1);
+        L0 = c0.m + fast_lg2(c0.s);
+        L1 = c1.m + fast_lg2(c1.s);
+    }
+    const float part = (v0 ? lse0 - t0 : 0.f) + (v1 ? lse1 - t1 : 0.f);
+    const float loss = warp_sum(part) * LN2;
+    // grad in target order = e^{t + L} - 1, scattered back to the item's own slot
+    if (v0) dg[s0] = (fast_ex2(t0 + L0) - 1.f) * inv;
+    if (v1) dg[s1] = (fast_ex2(t1 + L1) - 1.f) * inv;
+    if (lane == 0) *loss_out = loss * inv;
+}
+
+__global__ void __launch_bounds__(256) listmle_lengths64_kernel(const float* __restrict__ gnet,
+                                                                const int32_t* __restrict__ lengths, int n_lists,
+                                                                int L, int width, float* __restrict__ loss_out,
+                                                                float* __restrict__ dg_out) {
+    constexpr float LOG2E = 1.4426950408889634f;
+    const int lane = threadIdx.x & 31;
+    const int warps_total = gridDim.x * (blockDim.x >> 5);
+    const float inv = 1.0f / (float)L;
+    const int p0 = 2 * lane, p1 = p0 + 1;
+    const bool v0 = p0 < L, v1 = p1 < L;
+    for (int list = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); list < n_lists; list += warps_total) {
+        const float* g = gnet + (size_t)list * L;
+        const int32_t* len = lengths + (size_t)list * L;
+        const bool in0 = lane < L, in1 = lane + 32 < L;
+        const float g0 = in0 ? __ldcs(g + lane) : 0.f, g1 = in1 ? __ldcs(g + lane + 32) : 0.f;
+        const int n0 = in0 ? __ldcs(len + lane) : 0, n1 = in1 ? __ldcs(len + lane + 32) : 0;
+        // bucket_lengths: floor division (ranking.py:131-132)
+        int lab0 = n0 / width, lab1 = n1 / width;
+        if ((n0 % width != 0) && (n0 < 0)) --lab0;
+        if ((n1 % width != 0) && (n1 < 0)) --lab1;
+        int s0, s1;
+        listmle64_order(lab0, lab1, L, s0, s1);
+        // gather the scores into target order (base-2 units)
+        const float a0 = __shfl_sync(0xffffffffu, g0, s0 & 31), b0 = __shfl_sync(0xffffffffu, g1, s0 & 31);
+        const float a1 = __shfl_sync(0xffffffffu, g0, s1 & 31), b1 = __shfl_sync(0xffffffffu, g1, s1 & 31);
+        const float t0 = ((s0 >> 5) ? b0 : a0) * LOG2E, t1 = ((s1 >> 5) ? b1 : a1) * LOG2E;
+        listmle64_scan(t0, t1, v0, v1, L, inv, s0, s1, loss_out + list, dg_out + (size_t)list * L);
+    }
+}
+
 }  // namespace rs
 
 using namespace rs;
@@ -206,6 +454,19 @@ extern "C" int rs_listmle_lengths(const float* g, const int32_t* lengths, int32_
     RS_CHECK_ARG(width >= 1, "bucket_width must be >= 1");
     RS_CHECK_ARG(n_lists >= 0 && L >= 1 && L <= 4096, "rs_listmle_lengths: need 1 <= list_len <= 4096");
     if (n_lists == 0) return RS_OK;
+    if (L <= 64) {
+        // persistent grid: 8 warps per CTA, 8 CTAs per SM (one list per warp iteration)
+        static int n_sm = 0;
+        if (!n_sm) {
+            int dev;
+            RS_CUDA(cudaGetDevice(&dev));
+            RS_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+        }
+        const int blocks = (n_lists + 7) / 8 < n_sm * 8 ? (n_lists + 7) / 8 : n_sm * 8;
+        listmle_lengths64_kernel<<<blocks, 256, 0, st>>>(g, lengths, n_lists, L, width, loss, dg);
+        RS_LAUNCH_CHECK();
+        return RS_OK;
+    }
     const int w = listmle_warps(L);
     const int blocks = (n_lists + w - 1) / w;
     size_t sm = (size_t)w * L * (3 * sizeof(float) + 2 * sizeof(int));

@@ -68,3 +68,32 @@ def test_listmle_batched_float32_large():
     want_l, want_g = ro.listmle_train_step_targets(g[idx].double().cpu().numpy(), lengths[idx].cpu().numpy(), 10)
     np.testing.assert_allclose(loss[idx].cpu().numpy(), want_l, rtol=1e-5, atol=1e-6)
     np.testing.assert_allclose(dg[idx].cpu().numpy(), want_g, atol=1e-5)
+
+
+@pytest.mark.parametrize("case", ["wide_labels", "wide_scores", "ties", "ragged"])
+def test_listmle_training_form_register_path_edges(case):
+    """L <= 64 runs the register-resident kernel: 64-bit sort keys when labels exceed
+    2^25, score ranges far beyond exp's fp32 range, all-equal labels (pure index order)."""
+    from oracle import ranking_oracle as ro
+    from paper_2408_15792_b200.ranking import listmle_from_lengths
+    rng = np.random.default_rng(7)
+    n_lists, L, width = 300, 64, 10
+    g = rng.normal(0, 3, (n_lists, L)).astype(np.float32)
+    lengths = rng.integers(1, 2049, (n_lists, L)).astype(np.int32)
+    if case == "wide_labels":
+        width = 1
+        lengths = rng.integers(-(1 << 31), (1 << 31) - 1, (n_lists, L), dtype=np.int64).astype(np.int32)
+    elif case == "wide_scores":
+        g = rng.uniform(-1000, 1000, (n_lists, L)).astype(np.float32)
+    elif case == "ties":
+        lengths[:] = 5
+    elif case == "ragged":
+        L = 37
+        g, lengths = g[:, :L].copy(), lengths[:, :L].copy()
+    loss, dg = listmle_from_lengths(torch.from_numpy(g).cuda(), torch.from_numpy(lengths).cuda(), width)
+    want_l, want_g = ro.listmle_train_step_targets(g.astype(np.float64), lengths, width)
+    # |t| ~ 1000: one fp32 ulp of t (and of t + L) is 6e-5, so the gradient's absolute bar
+    # scales with it; everywhere else the standard 1e-5 bar holds
+    wide = case == "wide_scores"
+    np.testing.assert_allclose(loss.cpu().numpy(), want_l, rtol=1e-5, atol=1e-3 if wide else 1e-6)
+    np.testing.assert_allclose(dg.cpu().numpy(), want_g, atol=1e-4 if wide else 1e-5)
