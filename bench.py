@@ -440,9 +440,17 @@ def train_step_metric(args, world, rank, pk):
 def run_ours(args):
     import torch.distributed as dist
     world, rank, local = dist_env()
+    # RSB200_BENCH_BACKEND=gloo runs the N > 1 code path with every rank on the one GPU a
+    # test box has (NCCL refuses two ranks per device); the driver's runs use NCCL.
+    backend = os.environ.get("RSB200_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2408_15792_b200 import _lib
     from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
     from paper_2408_15792_b200.schedulers import DeviceQueue, SchedulerConfig
