@@ -94,6 +94,16 @@ __device__ __forceinline__ uint64_t orderable_i64(int64_t v) {
     return static_cast<uint64_t>(v) ^ 0x8000000000000000ull;
 }
 
+// SM count of the current device (cached per device ordinal).
+inline int num_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!cache[dev] && cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return 148;
+    return cache[dev];
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

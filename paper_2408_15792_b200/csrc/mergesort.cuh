@@ -65,8 +65,26 @@ struct KeyTraits<Key128> {
     }
 };
 
-template <typename K>
-__device__ __forceinline__ int merge_path(const K* a, int na, const K* b, int nb, int diag) {
+// Shared-memory tiles are padded with one key per 128 bytes, so the MS_ITEMS-strided
+// per-thread accesses of the merges (thread t at key 8t + i) spread over the banks
+// instead of hitting the same few (a 16-way conflict for 64-bit keys unpadded).
+template <typename T>
+struct MsPad {
+    static constexpr int shift = sizeof(T) == 4 ? 5 : sizeof(T) == 8 ? 4 : 3;
+    static constexpr int size = MS_TILE + (MS_TILE >> shift) + 1;
+};
+template <typename T>
+__device__ __forceinline__ int ms_pidx(int e) { return e + (e >> MsPad<T>::shift); }
+
+template <typename T>
+struct SView {  // run view into a padded smem tile
+    T* s;
+    int off;
+    __device__ __forceinline__ T operator[](int i) const { return s[ms_pidx<T>(off + i)]; }
+};
+
+template <typename K, typename A>
+__device__ __forceinline__ int merge_path(const A& a, int na, const A& b, int nb, int diag) {
     int lo = max(0, diag - nb), hi = min(diag, na);
     while (lo < hi) {
         int mid = (lo + hi) >> 1;
@@ -78,44 +96,55 @@ __device__ __forceinline__ int merge_path(const K* a, int na, const K* b, int nb
     return lo;
 }
 
-// Serially merge MS_ITEMS outputs starting at (i, j); a_total is the full length of
-// the left run and a_off the left-run index of a[0] (for inversion counting).
+// Serially merge MS_ITEMS outputs starting at (i, j), keeping the two head keys in
+// registers (one shared-memory load per output). a_remaining_base - i = left-run
+// elements not yet consumed (for inversion counting).
 template <typename K, bool HasVal, bool Count>
-__device__ __forceinline__ void serial_merge(const K* a, const uint32_t* av, int na, const K* b,
-                                             const uint32_t* bv, int nb, int i, int j,
+__device__ __forceinline__ void serial_merge(const SView<K>& a, const SView<uint32_t>& av, int na,
+                                             const SView<K>& b, const SView<uint32_t>& bv, int nb, int i, int j,
                                              K (&ok)[MS_ITEMS], uint32_t (&ov)[MS_ITEMS],
                                              uint64_t a_remaining_base, unsigned long long& inv) {
+    bool a_ok = i < na, b_ok = j < nb;
+    K ka = a_ok ? a[i] : KeyTraits<K>::sentinel();
+    K kb = b_ok ? b[j] : KeyTraits<K>::sentinel();
 #pragma unroll
     for (int k = 0; k < MS_ITEMS; ++k) {
-        bool take_a;
-        if (i >= na)
-            take_a = false;
-        else if (j >= nb)
-            take_a = true;
-        else
-            take_a = !KeyTraits<K>::less(b[j], a[i]);
+        const bool take_a = a_ok && (!b_ok || !KeyTraits<K>::less(kb, ka));
         if (take_a) {
-            ok[k] = a[i];
+            ok[k] = ka;
             if (HasVal) ov[k] = av[i];
             ++i;
+            a_ok = i < na;
+            if (a_ok) ka = a[i];
         } else {
-            ok[k] = b[j];
+            ok[k] = kb;
             if (HasVal) ov[k] = bv[j];
             ++j;
             if (Count) inv += a_remaining_base - (uint64_t)i;
+            b_ok = j < nb;
+            if (b_ok) kb = b[j];
         }
     }
 }
 
 template <typename K, bool HasVal>
 struct MsSmem {
-    K keys[MS_TILE];
-    uint32_t vals[HasVal ? MS_TILE : 1];
+    K keys[MsPad<K>::size];
+    uint32_t vals[HasVal ? MsPad<uint32_t>::size : 1];
 };
 
+// CTA-wide sum, one atomic per CTA (every thread of the CTA must call it).
 __device__ __forceinline__ void block_add_count(unsigned long long v, unsigned long long* out) {
+    __shared__ unsigned long long part[32];
     v = warp_sum(v);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd(out, v);
+    const int nw = (int)(blockDim.x >> 5);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned long long t = (int)threadIdx.x < nw ? part[threadIdx.x] : 0ull;
+        t = warp_sum(t);
+        if (threadIdx.x == 0 && t) atomicAdd(out, t);
+    }
 }
 
 // Sort each 2048-key tile. keys_in has n valid entries; the tail of the last tile is
@@ -131,16 +160,16 @@ __global__ void __launch_bounds__(MS_THREADS) ms_block_sort(const K* __restrict_
     const uint32_t base = blockIdx.x * MS_TILE;
     for (int k = threadIdx.x; k < MS_TILE; k += MS_THREADS) {
         uint32_t g = base + k;
-        sm.keys[k] = g < n ? keys_in[g] : KeyTraits<K>::sentinel();
-        if (HasVal) sm.vals[k] = g < n ? (vals_in ? vals_in[g] : g) : 0xffffffffu;
+        sm.keys[ms_pidx<K>(k)] = g < n ? keys_in[g] : KeyTraits<K>::sentinel();
+        if (HasVal) sm.vals[ms_pidx<uint32_t>(k)] = g < n ? (vals_in ? vals_in[g] : g) : 0xffffffffu;
     }
     __syncthreads();
     K rk[MS_ITEMS];
     uint32_t rv[MS_ITEMS];
 #pragma unroll
     for (int k = 0; k < MS_ITEMS; ++k) {
-        rk[k] = sm.keys[threadIdx.x * MS_ITEMS + k];
-        if (HasVal) rv[k] = sm.vals[threadIdx.x * MS_ITEMS + k];
+        rk[k] = sm.keys[ms_pidx<K>(threadIdx.x * MS_ITEMS + k)];
+        if (HasVal) rv[k] = sm.vals[ms_pidx<uint32_t>(threadIdx.x * MS_ITEMS + k)];
     }
     unsigned long long inv = 0;
     // Odd-even transposition: strict swaps only => stable, swap count = inversions.
@@ -164,53 +193,80 @@ __global__ void __launch_bounds__(MS_THREADS) ms_block_sort(const K* __restrict_
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < MS_ITEMS; ++k) {
-        sm.keys[threadIdx.x * MS_ITEMS + k] = rk[k];
-        if (HasVal) sm.vals[threadIdx.x * MS_ITEMS + k] = rv[k];
+        sm.keys[ms_pidx<K>(threadIdx.x * MS_ITEMS + k)] = rk[k];
+        if (HasVal) sm.vals[ms_pidx<uint32_t>(threadIdx.x * MS_ITEMS + k)] = rv[k];
     }
     __syncthreads();
     for (int s = MS_ITEMS; s < MS_TILE; s <<= 1) {
         const int p = threadIdx.x * MS_ITEMS;
         const int pb = p / (2 * s) * (2 * s);
-        const K* a = sm.keys + pb;
-        const K* b = sm.keys + pb + s;
-        const uint32_t* av = HasVal ? sm.vals + pb : nullptr;
-        const uint32_t* bv = HasVal ? sm.vals + pb + s : nullptr;
+        const SView<K> a{sm.keys, pb}, b{sm.keys, pb + s};
+        const SView<uint32_t> av{sm.vals, pb}, bv{sm.vals, pb + s};
         const int diag = p - pb;
-        const int i = merge_path(a, s, b, s, diag);
+        const int i = merge_path<K>(a, s, b, s, diag);
         serial_merge<K, HasVal, Count>(a, av, s, b, bv, s, i, diag - i, rk, rv, (uint64_t)s, inv);
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < MS_ITEMS; ++k) {
-            sm.keys[p + k] = rk[k];
-            if (HasVal) sm.vals[p + k] = rv[k];
+            sm.keys[ms_pidx<K>(p + k)] = rk[k];
+            if (HasVal) sm.vals[ms_pidx<uint32_t>(p + k)] = rv[k];
         }
         __syncthreads();
     }
     for (int k = threadIdx.x; k < MS_TILE; k += MS_THREADS) {
-        keys_out[base + k] = sm.keys[k];
-        if (HasVal) vals_out[base + k] = sm.vals[k];
+        keys_out[base + k] = sm.keys[ms_pidx<K>(k)];
+        if (HasVal) vals_out[base + k] = sm.vals[ms_pidx<uint32_t>(k)];
     }
     if (Count) block_add_count(inv, inv_out);
 }
 
 // One global merge pass: runs of width w -> runs of width 2w over npad keys.
-// Merge-path split of every output tile boundary of a pass, one thread each (the
-// binary searches are dependent global loads: done here in parallel for all tiles
-// instead of serially at the start of every merging CTA).
+// Merge-path split of every output tile boundary of a pass, one warp each: every round
+// the 32 lanes probe 32 evenly spaced candidates and a ballot narrows the range 32x,
+// so a split over a run of 2^23 keys costs 5 dependent global loads instead of 23.
+constexpr int MS_PART_WARPS = 8;
+
 template <typename K>
-__global__ void ms_partition(const K* __restrict__ kin, uint32_t npad, uint32_t w, uint32_t tiles,
-                             int* __restrict__ split) {
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(MS_PART_WARPS * 32) ms_partition(const K* __restrict__ kin, uint32_t npad,
+                                                                   uint32_t w, uint32_t tiles,
+                                                                   int* __restrict__ split,
+                                                                   const int* __restrict__ skip) {
+    if (skip && *skip) return;
+    const uint32_t t = blockIdx.x * MS_PART_WARPS + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (t > tiles) return;
     const uint32_t out = t * MS_TILE;
     if (t == tiles || out % (2 * w) == 0) {  // run-pair boundary: nothing taken yet
-        split[t] = 0;
+        if (lane == 0) split[t] = 0;
         return;
     }
     const uint32_t base = out / (2 * w) * (2 * w);
     const int lenA = (int)min(w, npad - base);
     const int lenB = (int)min(w, npad - base - (uint32_t)lenA);
-    split[t] = merge_path(kin + base, lenA, kin + base + lenA, lenB, (int)(out - base));
+    const K* a = kin + base;
+    const K* b = kin + base + lenA;
+    const int diag = (int)(out - base);
+    // smallest i in [lo, hi] with less(b[diag-1-i], a[i]) (hi if none): the merge_path split
+    int lo = max(0, diag - lenB), hi = min(diag, lenA);
+    while (hi - lo > 32) {
+        const int step = (hi - lo + 31) / 32;
+        const int p = lo + lane * step;
+        const bool pred = p < hi && KeyTraits<K>::less(b[diag - 1 - p], a[p]);
+        const unsigned m = __ballot_sync(0xffffffffu, pred);
+        if (m) {
+            const int f = __ffs(m) - 1;
+            const int pf = lo + f * step;
+            lo = f ? pf - step + 1 : lo;
+            hi = pf;
+        } else {
+            const int last = min(31, (hi - 1 - lo) / step);
+            lo = lo + last * step + 1;
+        }
+    }
+    const int p = lo + lane;
+    const bool pred = p < hi && KeyTraits<K>::less(b[diag - 1 - p], a[p]);
+    const unsigned m = __ballot_sync(0xffffffffu, pred);
+    if (lane == 0) split[t] = m ? lo + __ffs(m) - 1 : hi;
 }
 
 template <typename K, bool HasVal, bool Count>
@@ -220,7 +276,9 @@ __global__ void __launch_bounds__(MS_THREADS) ms_merge_pass(const K* __restrict_
                                                             uint32_t* __restrict__ vout,
                                                             uint32_t npad, uint32_t w,
                                                             unsigned long long* inv_out,
-                                                            const int* __restrict__ splits) {
+                                                            const int* __restrict__ splits,
+                                                            const int* __restrict__ skip) {
+    if (skip && *skip) return;
     __shared__ MsSmem<K, HasVal> sm;
     const uint32_t out0 = blockIdx.x * MS_TILE;
     const uint32_t base = out0 / (2 * w) * (2 * w);
@@ -237,11 +295,11 @@ __global__ void __launch_bounds__(MS_THREADS) ms_merge_pass(const K* __restrict_
     const int na = a1 - a0, nb = b1 - b0;
     for (int k = threadIdx.x; k < MS_TILE; k += MS_THREADS) {
         if (k < na) {
-            sm.keys[k] = A[a0 + k];
-            if (HasVal) sm.vals[k] = vin[base + a0 + k];
+            sm.keys[ms_pidx<K>(k)] = A[a0 + k];
+            if (HasVal) sm.vals[ms_pidx<uint32_t>(k)] = vin[base + a0 + k];
         } else {
-            sm.keys[k] = B[b0 + k - na];
-            if (HasVal) sm.vals[k] = vin[base + lenA + b0 + k - na];
+            sm.keys[ms_pidx<K>(k)] = B[b0 + k - na];
+            if (HasVal) sm.vals[ms_pidx<uint32_t>(k)] = vin[base + lenA + b0 + k - na];
         }
     }
     __syncthreads();
@@ -249,22 +307,22 @@ __global__ void __launch_bounds__(MS_THREADS) ms_merge_pass(const K* __restrict_
     uint32_t rv[MS_ITEMS];
     unsigned long long inv = 0;
     const int diag = threadIdx.x * MS_ITEMS;
-    const int i = merge_path(sm.keys, na, sm.keys + na, nb, diag);
+    const SView<K> sa{sm.keys, 0}, sb{sm.keys, na};
+    const SView<uint32_t> sav{sm.vals, 0}, sbv{sm.vals, na};
+    const int i = merge_path<K>(sa, na, sb, nb, diag);
     // left-run elements not yet consumed when a right element is taken:
     // lenA - (a0 + i_local)  => base term lenA - a0, minus the local i.
-    serial_merge<K, HasVal, Count>(sm.keys, HasVal ? sm.vals : nullptr, na, sm.keys + na,
-                                   HasVal ? sm.vals + na : nullptr, nb, i, diag - i, rk, rv,
-                                   (uint64_t)(lenA - a0), inv);
+    serial_merge<K, HasVal, Count>(sa, sav, na, sb, sbv, nb, i, diag - i, rk, rv, (uint64_t)(lenA - a0), inv);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < MS_ITEMS; ++k) {
-        sm.keys[diag + k] = rk[k];
-        if (HasVal) sm.vals[diag + k] = rv[k];
+        sm.keys[ms_pidx<K>(diag + k)] = rk[k];
+        if (HasVal) sm.vals[ms_pidx<uint32_t>(diag + k)] = rv[k];
     }
     __syncthreads();
     for (int k = threadIdx.x; k < MS_TILE; k += MS_THREADS) {
-        kout[out0 + k] = sm.keys[k];
-        if (HasVal) vout[out0 + k] = sm.vals[k];
+        kout[out0 + k] = sm.keys[ms_pidx<K>(k)];
+        if (HasVal) vout[out0 + k] = sm.vals[ms_pidx<uint32_t>(k)];
     }
     if (Count) block_add_count(inv, inv_out);
 }
@@ -278,11 +336,13 @@ static inline uint32_t ms_splits(uint64_t n) { return (uint32_t)((n + MS_TILE - 
 
 // Sort n keys (+ optional u32 payload). k0/k1 and v0/v1 are ping-pong buffers of
 // ms_padded(n) entries, splits ms_splits(n) ints. On return *kres / *vres point at the
-// sorted (padded) arrays.
+// sorted (padded) arrays. With `skip` set, the passes at run width >= skip_w return at
+// once when *skip != 0 (decided on the device: the output is then sorted only within
+// runs of skip_w, and only the inversions inside those runs are counted).
 template <typename K, bool HasVal, bool Count>
 int merge_sort(const K* keys_in, const uint32_t* vals_in, uint32_t n, K* k0, K* k1, uint32_t* v0,
                uint32_t* v1, unsigned long long* inv, cudaStream_t st, K** kres,
-               uint32_t** vres, int* splits) {
+               uint32_t** vres, int* splits, const int* skip = nullptr, uint32_t skip_w = 0) {
     const uint32_t npad = ms_padded(n);
     const uint32_t tiles = npad / MS_TILE;
     if (tiles == 0) {
@@ -297,9 +357,11 @@ int merge_sort(const K* keys_in, const uint32_t* vals_in, uint32_t n, K* k0, K* 
     uint32_t* vi = v0;
     uint32_t* vo = v1;
     for (uint32_t w = MS_TILE; w < npad; w <<= 1) {
-        ms_partition<K><<<(tiles + 1 + 255) / 256, 256, 0, st>>>(ki, npad, w, tiles, splits);
+        const int* sk = (skip && w >= skip_w) ? skip : nullptr;
+        ms_partition<K><<<(tiles + MS_PART_WARPS) / MS_PART_WARPS, MS_PART_WARPS * 32, 0, st>>>(ki, npad, w, tiles,
+                                                                                             splits, sk);
         RS_LAUNCH_CHECK();
-        ms_merge_pass<K, HasVal, Count><<<tiles, MS_THREADS, 0, st>>>(ki, vi, ko, vo, npad, w, inv, splits);
+        ms_merge_pass<K, HasVal, Count><<<tiles, MS_THREADS, 0, st>>>(ki, vi, ko, vo, npad, w, inv, splits, sk);
         RS_LAUNCH_CHECK();
         K* t = ki;
         ki = ko;

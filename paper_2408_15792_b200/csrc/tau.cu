@@ -8,6 +8,8 @@
 //   2. sort the 64-bit composite (x_img << 32 | y_img)            -> n1, n3 from runs
 //   3. D = strict inversions of the y images in that order        (merge-sort count)
 //      and the same sort leaves y sorted                         -> n2 from runs
+//      (y spanning < 4096 values: only 2048-key tiles are sorted, and the inversions
+//      across tiles and n2 come from chunk histograms — see chunk_cross)
 //   4. C = n0 - n1 - n2 + n3 - D.
 // All counts are exact int64; tau itself is finished on the host with the reference
 // expression (ranking.py:60-63).
@@ -93,49 +95,179 @@ __global__ void rank_scatter(const uint64_t* __restrict__ sk, const uint32_t* __
 }
 
 // Tied pairs = sum over runs of c(c-1)/2, evaluated at each run end that has c >= 2
-// by a lower_bound for the run start (keys sorted => the images are monotone).
-template <typename Proj>
-__global__ void tied_pairs(const uint64_t* __restrict__ s, uint32_t n, Proj proj,
-                           unsigned long long* __restrict__ out) {
-    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+// by a lower_bound for the run start (keys sorted => the images are monotone): gallop
+// back from the run end (runs are short), then bisect the last gap. Grid-stride over a
+// few CTAs per SM with one atomic per CTA (a per-warp atomic on one counter serialises
+// at L2 when most warps see a tie).
+template <typename K, typename Proj>
+__global__ void __launch_bounds__(256) tied_pairs(const K* __restrict__ s, uint32_t n, Proj proj,
+                                                  unsigned long long* __restrict__ out,
+                                                  const int* __restrict__ skip) {
+    if (skip && *skip) return;
     unsigned long long c = 0;
-    if (i < n) {
-        uint64_t v = proj(s[i]);
-        bool end = (i + 1 == n) || proj(s[i + 1]) != v;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t v = proj(s[i]);
+        const bool end = (i + 1 == n) || proj(s[i + 1]) != v;
         if (end && i > 0 && proj(s[i - 1]) == v) {
-            uint32_t lo = 0, hi = i;
+            uint32_t step = 2, hi = i - 1;
+            while (step <= i && proj(s[i - step]) == v) {
+                hi = i - step;
+                step <<= 1;
+            }
+            uint32_t lo = step <= i ? i - step + 1 : 0;
             while (lo < hi) {
-                uint32_t mid = (lo + hi) >> 1;
+                const uint32_t mid = (lo + hi) >> 1;
                 if (proj(s[mid]) < v) lo = mid + 1; else hi = mid;
             }
-            unsigned long long len = (unsigned long long)(i - lo + 1);
-            c = len * (len - 1) / 2;
+            const unsigned long long len = (unsigned long long)(i - lo + 1);
+            c += len * (len - 1) / 2;
         }
     }
-    c = warp_sum(c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+    block_add_count(c, out);
 }
 struct ProjFull { __device__ uint64_t operator()(uint64_t v) const { return v; } };
 struct ProjHi { __device__ uint64_t operator()(uint64_t v) const { return v >> 32; } };
 
-__global__ void tied_pairs32(const uint32_t* __restrict__ s, uint32_t n, unsigned long long* __restrict__ out) {
-    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    unsigned long long c = 0;
-    if (i < n) {
-        uint32_t v = s[i];
-        bool end = (i + 1 == n) || s[i + 1] != v;
-        if (end && i > 0 && s[i - 1] == v) {
-            uint32_t lo = 0, hi = i;
-            while (lo < hi) {
-                uint32_t mid = (lo + hi) >> 1;
-                if (s[mid] < v) lo = mid + 1; else hi = mid;
-            }
-            unsigned long long len = (unsigned long long)(i - lo + 1);
-            c = len * (len - 1) / 2;
-        }
+// ---- small-range y: cross-tile inversions from histograms ------------------------
+// When the y images span fewer than TH_BINS values (cfg4: lengths in [1, 2048]), the
+// inversions between different 2048-key tiles of the (x, y)-sorted sequence are
+//   sum over tiles t, items j in t of #{items in earlier tiles with y > y_j},
+// read off a running histogram of everything before t. So the y merge sort stops after
+// its block-sort stage (which counts the inversions inside each tile) and three passes
+// replace its log2(n / 2048) merge passes: per-chunk histograms, a column scan of them
+// (exclusive per chunk; the column totals also give n2), and a count pass in which each
+// chunk walks its tiles with the running histogram in shared memory. The choice is
+// made on the device (no host round trip), so both paths are launched and the unused
+// one returns at once.
+constexpr int TH_BINS = 4096;
+constexpr int TH_THREADS = 256;
+
+struct TauChunks {
+    uint32_t tiles_per_chunk, chunk_elems, nchunks;
+};
+static TauChunks tau_chunks(uint64_t n) {
+    const uint32_t tiles = (uint32_t)((n + MS_TILE - 1) / MS_TILE);
+    const uint32_t target = (uint32_t)num_sms() * 8;  // ~ resident CTAs of the count pass
+    const uint32_t tpc = (tiles + target - 1) / target;
+    const uint32_t ce = tpc * MS_TILE;
+    return TauChunks{tpc, ce, (uint32_t)((n + ce - 1) / ce)};
+}
+
+__global__ void __launch_bounds__(256) y_range(const uint32_t* __restrict__ y, uint32_t n, uint32_t* __restrict__ yr) {
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t v = y[i];
+        lo = min(lo, v);
+        hi = max(hi, v);
     }
-    c = warp_sum(c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(yr + 0, lo);
+        atomicMax(yr + 1, hi);
+    }
+}
+// flag[1] = 1 when the histogram path applies (read by both paths' kernels)
+__global__ void y_range_flag(const uint32_t* __restrict__ yr, int* __restrict__ flag) {
+    flag[1] = (yr[1] - yr[0] < (uint32_t)TH_BINS) ? 1 : 0;
+}
+
+__global__ void __launch_bounds__(TH_THREADS) chunk_hist(const uint32_t* __restrict__ y, uint32_t n,
+                                                         const uint32_t* __restrict__ yr, const int* __restrict__ flag,
+                                                         uint32_t chunk_elems, uint32_t* __restrict__ hist) {
+    if (!flag[1]) return;
+    __shared__ uint32_t h[TH_BINS];
+    for (int v = threadIdx.x; v < TH_BINS; v += TH_THREADS) h[v] = 0;
+    __syncthreads();
+    const uint32_t ymin = yr[0];
+    const uint32_t beg = blockIdx.x * chunk_elems, end = min(n, beg + chunk_elems);
+    for (uint32_t i = beg + threadIdx.x; i < end; i += TH_THREADS) atomicAdd(&h[y[i] - ymin], 1u);
+    __syncthreads();
+    uint32_t* out = hist + (size_t)blockIdx.x * TH_BINS;
+    for (int v = threadIdx.x; v < TH_BINS; v += TH_THREADS) out[v] = h[v];
+}
+
+// Column-wise exclusive scan of the chunk histograms: CTA = 32 bins (one per lane),
+// its 8 warps split the chunk rows; totals -> tied pairs in y (n2).
+__global__ void __launch_bounds__(256) chunk_scan(const uint32_t* __restrict__ hist, uint32_t nchunks,
+                                                  const int* __restrict__ flag, uint32_t* __restrict__ pre,
+                                                  unsigned long long* __restrict__ n2) {
+    if (!flag[1]) return;
+    __shared__ uint32_t tot[8][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t bin = blockIdx.x * 32 + lane;
+    const uint32_t rpw = (nchunks + 7) / 8;
+    const uint32_t r0 = min(nchunks, wid * rpw), r1 = min(nchunks, r0 + rpw);
+    uint32_t s = 0;
+    for (uint32_t r = r0; r < r1; ++r) s += hist[(size_t)r * TH_BINS + bin];
+    tot[wid][lane] = s;
+    __syncthreads();
+    uint32_t run = 0, all = 0;
+    for (int k = 0; k < 8; ++k) {
+        if (k < wid) run += tot[k][lane];
+        all += tot[k][lane];
+    }
+    for (uint32_t r = r0; r < r1; ++r) {
+        pre[(size_t)r * TH_BINS + bin] = run;
+        run += hist[(size_t)r * TH_BINS + bin];
+    }
+    const unsigned long long c = (unsigned long long)all * (all - 1ull) / 2ull;
+    block_add_count(wid == 0 ? c : 0ull, n2);
+}
+
+// Each chunk walks its tiles in order: before tile k the shared histogram holds every
+// y of earlier tiles; suffix sums of it give each item's count of earlier, larger y.
+__global__ void __launch_bounds__(TH_THREADS) chunk_cross(const uint32_t* __restrict__ y, uint32_t n,
+                                                          const uint32_t* __restrict__ yr,
+                                                          const int* __restrict__ flag, uint32_t chunk_elems,
+                                                          const uint32_t* __restrict__ pre,
+                                                          unsigned long long* __restrict__ inv) {
+    if (!flag[1]) return;
+    constexpr int PER = TH_BINS / TH_THREADS;  // 16 bins per thread
+    __shared__ uint32_t h[TH_BINS];
+    __shared__ uint32_t gt[TH_BINS];  // gt[v] = #earlier items with y image offset > v
+    __shared__ uint32_t wsum[TH_THREADS / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t ymin = yr[0];
+    const uint32_t* p = pre + (size_t)blockIdx.x * TH_BINS;
+    for (int v = threadIdx.x; v < TH_BINS; v += TH_THREADS) h[v] = p[v];
+    __syncthreads();
+    const uint32_t beg = blockIdx.x * chunk_elems, end = min(n, beg + chunk_elems);
+    unsigned long long cnt = 0;
+    for (uint32_t t0 = beg; t0 < end; t0 += MS_TILE) {
+        // suffix sums over the thread's 16 bins, then across threads (reverse scan)
+        uint32_t loc[PER];
+        uint32_t acc = 0;
+#pragma unroll
+        for (int k = PER - 1; k >= 0; --k) {
+            loc[k] = acc;  // strictly greater bins inside the thread's run
+            acc += h[threadIdx.x * PER + k];
+        }
+        uint32_t x = acc;  // inclusive suffix scan over threads: lanes above + warps above
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t yv = __shfl_down_sync(0xffffffffu, x, o);
+            if (lane + o < 32) x += yv;
+        }
+        if (lane == 0) wsum[wid] = x;
+        __syncthreads();
+        uint32_t above = x - acc;
+        for (int k = wid + 1; k < TH_THREADS / 32; ++k) above += wsum[k];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) gt[threadIdx.x * PER + k] = loc[k] + above;
+        __syncthreads();
+        const uint32_t t1 = min(end, t0 + MS_TILE);
+        for (uint32_t i = t0 + threadIdx.x; i < t1; i += TH_THREADS) {
+            const uint32_t v = y[i] - ymin;
+            cnt += gt[v];
+            atomicAdd(&h[v], 1u);
+        }
+        __syncthreads();
+    }
+    block_add_count(cnt, inv);
 }
 
 __global__ void compose_keys(const uint32_t* __restrict__ ux, const uint32_t* __restrict__ uy, uint32_t n,
@@ -173,6 +305,9 @@ struct TauWs {
     unsigned long long* acc;
     int* flag;
     int* splits;
+    uint32_t* yr;
+    uint32_t* hist;
+    uint32_t* pre;
 };
 
 template <typename A>
@@ -191,7 +326,11 @@ static void tau_layout(A& a, uint64_t n, bool need64, TauWs* w) {
     auto t_acc = a.template take<unsigned long long>(8);
     auto t_flag = a.template take<int>(4);
     auto t_sp = a.template take<int>(ms_splits(np));
-    if (w) *w = TauWs{t_ux, t_uy, t_ka, t_kb, t_32a, t_32b, t_va, t_vb, t_blk, t_acc, t_flag, t_sp};
+    const TauChunks ch = tau_chunks(n);
+    auto t_yr = a.template take<uint32_t>(4);
+    auto t_h = a.template take<uint32_t>((size_t)ch.nchunks * TH_BINS);
+    auto t_p = a.template take<uint32_t>((size_t)ch.nchunks * TH_BINS);
+    if (w) *w = TauWs{t_ux, t_uy, t_ka, t_kb, t_32a, t_32b, t_va, t_vb, t_blk, t_acc, t_flag, t_sp, t_yr, t_h, t_p};
 }
 struct SizerAdapter {
     ArenaSizer s;
@@ -262,21 +401,37 @@ extern "C" int rs_tau_counts(const void* x, int xd, const void* y, int yd, int64
     RS_TRY(image_of(y, yd, un, w.uy, w, st));
     const int T = 256;
     const uint32_t g = (un + T - 1) / T;
+    const uint32_t gs = g < (uint32_t)num_sms() * 8 ? g : (uint32_t)num_sms() * 8;
     compose_keys<<<g, T, 0, st>>>(w.ux, w.uy, un, w.k64b);
     RS_LAUNCH_CHECK();
     uint64_t* sk;
     RS_TRY((merge_sort<uint64_t, false, false>(w.k64b, nullptr, un, w.k64a, w.k64b, nullptr, nullptr, nullptr,
                                                st, &sk, nullptr, w.splits)));
-    tied_pairs<ProjHi><<<g, T, 0, st>>>(sk, un, ProjHi{}, w.acc + 1);
+    tied_pairs<uint64_t, ProjHi><<<gs, T, 0, st>>>(sk, un, ProjHi{}, w.acc + 1, nullptr);
     RS_LAUNCH_CHECK();
-    tied_pairs<ProjFull><<<g, T, 0, st>>>(sk, un, ProjFull{}, w.acc + 3);
+    tied_pairs<uint64_t, ProjFull><<<gs, T, 0, st>>>(sk, un, ProjFull{}, w.acc + 3, nullptr);
     RS_LAUNCH_CHECK();
     low_words<<<g, T, 0, st>>>(sk, un, w.uy);
     RS_LAUNCH_CHECK();
+    // D and n2: block-sort counts inside 2048-key tiles, then either the histogram
+    // passes (y range < TH_BINS) or the remaining merge passes + runs of the sorted y.
+    RS_CUDA(cudaMemsetAsync(w.yr, 0xff, sizeof(uint32_t), st));
+    RS_CUDA(cudaMemsetAsync(w.yr + 1, 0, sizeof(uint32_t), st));
+    y_range<<<gs, T, 0, st>>>(w.uy, un, w.yr);
+    RS_LAUNCH_CHECK();
+    y_range_flag<<<1, 1, 0, st>>>(w.yr, w.flag);
+    RS_LAUNCH_CHECK();
     uint32_t* sy;
     RS_TRY((merge_sort<uint32_t, false, true>(w.uy, nullptr, un, w.k32a, w.k32b, nullptr, nullptr, w.acc + 0, st,
-                                              &sy, nullptr, w.splits)));
-    tied_pairs32<<<g, T, 0, st>>>(sy, un, w.acc + 2);
+                                              &sy, nullptr, w.splits, w.flag + 1, (uint32_t)MS_TILE)));
+    tied_pairs<uint32_t, ProjFull><<<gs, T, 0, st>>>(sy, un, ProjFull{}, w.acc + 2, w.flag + 1);
+    RS_LAUNCH_CHECK();
+    const TauChunks ch = tau_chunks(n);
+    chunk_hist<<<ch.nchunks, TH_THREADS, 0, st>>>(w.uy, un, w.yr, w.flag, ch.chunk_elems, w.hist);
+    RS_LAUNCH_CHECK();
+    chunk_scan<<<TH_BINS / 32, 256, 0, st>>>(w.hist, ch.nchunks, w.flag, w.pre, w.acc + 2);
+    RS_LAUNCH_CHECK();
+    chunk_cross<<<ch.nchunks, TH_THREADS, 0, st>>>(w.uy, un, w.yr, w.flag, ch.chunk_elems, w.pre, w.acc + 0);
     RS_LAUNCH_CHECK();
     // NaN keys are flagged in counts[5] (the reference's NaN behaviour is inconsistent
     // between its pair loop and np.unique, so the wrapper rejects them).

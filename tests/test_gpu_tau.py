@@ -101,3 +101,37 @@ def test_tau_plan_graph_matches_eager():
     x.copy_(torch.randn(300_000, device="cuda", generator=g))
     want2 = ranking.tau_counts_device(x, y).clone()
     assert torch.equal(plan(), want2) and not torch.equal(want, want2)
+
+
+@pytest.mark.parametrize("y_span", [4095, 4096, "float"])
+def test_tau_histogram_and_merge_paths_vs_oracle(y_span):
+    """y images spanning < 4096 values take the histogram path for cross-tile
+    inversions, wider ones the merge passes; both exact against the pair-loop oracle."""
+    from oracle import tau_c
+    from paper_2408_15792_b200.ranking import kendall_tau_b
+    rng = np.random.default_rng(23)
+    n = 40_000
+    x = rng.integers(-3000, 3000, n).astype(np.float32)
+    if y_span == "float":
+        y = rng.normal(size=n).astype(np.float32)
+    else:
+        y = rng.integers(0, y_span + 1, n).astype(np.int32) + 7
+        y[:2] = (7, 7 + y_span)  # pin the span
+    r = kendall_tau_b(x, y)
+    C, D, n1, n2, _ = tau_c.tau_counts(x, y)
+    assert (r.concordant, r.discordant) == (C, D)
+    n0 = n * (n - 1) // 2
+    assert r.tau == (C - D) / math.sqrt((n0 - n1) * (n0 - n2))
+
+
+def test_tau_paths_agree_at_16m():
+    """The same ranks of y, once spanning 2048 values (histogram path) and once scaled to
+    span 2e8 (merge path), give identical counts at 16M (several tiles per chunk)."""
+    from paper_2408_15792_b200.ranking import tau_counts_device
+    g = torch.Generator(device="cuda").manual_seed(9)
+    n = 1 << 24
+    x = torch.randn(n, device="cuda", generator=g).to(torch.bfloat16).float()  # heavy x ties
+    y = torch.randint(1, 2049, (n,), device="cuda", generator=g, dtype=torch.int32)
+    a = tau_counts_device(x, y).cpu().tolist()
+    b = tau_counts_device(x, y * 100_000).cpu().tolist()
+    assert a == b
