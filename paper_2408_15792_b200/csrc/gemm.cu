@@ -220,8 +220,11 @@ constexpr int G2_EPI_BUF = 32 * 32 * 4;          // one 32x32 fp32 (or bf16) sta
 // K = 768 the mainloop is short and the fp32 R read + C write (8 B per output) bound it.
 template <int EPI>
 struct G2Cfg {
-    static constexpr int stages = EPI == 2 ? 5 : G2_STAGES;
-    static constexpr int nbuf = EPI == 2 ? 4 : 2;
+    // EPI 2 (fp32 residual) and 5 (bf16 ReLU mask) stream an input sub-tile per output
+    // sub-tile through the staging buffers
+    static constexpr bool streams = EPI == 2 || EPI == 5;
+    static constexpr int stages = streams ? 5 : G2_STAGES;
+    static constexpr int nbuf = streams ? 4 : 2;
     static constexpr int smem = stages * G2_STAGE_BYTES + 4 * nbuf * G2_EPI_BUF + 1024 + 512;
 };
 
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         tma_prefetch_desc(&tA);
         tma_prefetch_desc(&tB);
         tma_prefetch_desc(&tC);
-        if (EPI == 2) tma_prefetch_desc(&tR);
+        if (G2Cfg<EPI>::streams) tma_prefetch_desc(&tR);
         for (int s = 0; s < G2_STAGES; ++s) {
             mbar_init(&full[s], 2);  // leader: both CTAs' producers arrive (+ 64 KB of tx)
             mbar_init(&empty[s], 1);
@@ -381,10 +384,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             const int rm0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
             const int rn0 = (tile % tiles_n) * G2_BN;
             const int b = n % NBUF;
-            mbar_arrive_expect_tx(&rf[b], G2_EPI_BUF);
+            mbar_arrive_expect_tx(&rf[b], EPI == 2 ? G2_EPI_BUF : G2_EPI_BUF / 2);
             tma_load_2d(ebuf + b * G2_EPI_BUF, &tR, &rf[b], rn0 + (n & 7) * 32, rm0 + q * 32);
         };
-        if (EPI == 2 && lane == 0)
+        if (G2Cfg<EPI>::streams && lane == 0)
             for (int n = 0; n < PD; ++n) prefetch_r(n);
         for (int w = cid; w < n_work; w += ncl) {
             const int tile = w / k_splits;
@@ -394,24 +397,16 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             const int mo = (EPI == 6) ? m0 + (w % k_splits) * M : m0;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const __nv_bfloat16* mrow =
-                (EPI == 5) ? static_cast<const __nv_bfloat16*>(aux) + (size_t)(m0 + row) * ldc + n0 : nullptr;
 #pragma unroll 1
             for (int c = 0; c < G2_BN; c += 32, ++nst) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * G2_BN + c, r);
                 float v[32];
                 const uint4* bv = reinterpret_cast<const uint4*>(bias + n0 + c);
-                uint4 mk[4];
-                if (EPI == 5) {
-                    const uint4* mv = reinterpret_cast<const uint4*>(mrow + c);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) mk[j] = mv[j];
-                }
                 uint8_t* buf = ebuf + (nst % NBUF) * G2_EPI_BUF;
-                if (EPI == 2) {
+                if (G2Cfg<EPI>::streams) {
                     // reuse of buffer (nst + PD) % NBUF: its last store (sub-tile nst - 2) has
-                    // been read; then queue that residual sub-tile
+                    // been read; then queue that residual / mask sub-tile
                     if (lane == 0) {
                         tma_store_wait_read<1>();
                         prefetch_r(nst + PD);
@@ -437,10 +432,14 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
                 }
+                if (G2Cfg<EPI>::streams) mbar_wait(&rf[nst % NBUF], (nst / NBUF) & 1);
                 if (EPI == 5) {
+                    // the mask sub-tile sits in this buffer in the output's SW64 layout
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const __nv_bfloat162* m2 = reinterpret_cast<const __nv_bfloat162*>(&mk[j]);
+                        const uint4 m4 =
+                            *reinterpret_cast<const uint4*>(buf + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4));
+                        const __nv_bfloat162* m2 = reinterpret_cast<const __nv_bfloat162*>(&m4);
 #pragma unroll
                         for (int h = 0; h < 4; ++h) {
                             float2 mf = __bfloat1622float2(m2[h]);
@@ -449,7 +448,6 @@ __global__ void __launch_bounds__(G_THREADS, 1)
                         }
                     }
                 }
-                if (EPI == 2) mbar_wait(&rf[nst % NBUF], (nst / NBUF) & 1);
                 __syncwarp();
                 if (EPI == 2 || EPI == 4 || EPI == 6) {
                     // fp32 32x32 sub-tile, 128-B rows, SWIZZLE_128B: chunk j ^ (row % 8)
@@ -567,6 +565,9 @@ int gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux
     if (epi == 2)  // the residual R [M, N] fp32, read in the store's sub-tile geometry
         RS_TRY(make_tmap_2d(&tR, aux, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)M, (uint64_t)N, (uint64_t)N * 4, 32,
                             32, CU_TENSOR_MAP_SWIZZLE_128B));
+    else if (epi == 5)  // the ReLU mask [M, N] bf16, likewise
+        RS_TRY(make_tmap_2d(&tR, aux, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (uint64_t)M, (uint64_t)N, (uint64_t)N * 2, 32,
+                            32, CU_TENSOR_MAP_SWIZZLE_64B));
     else
         tR = tC;
     const int n_work = (M / G2_BM) * (N / G2_BN) * k_splits;

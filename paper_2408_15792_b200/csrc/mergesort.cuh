@@ -327,6 +327,50 @@ __global__ void __launch_bounds__(MS_THREADS) ms_merge_pass(const K* __restrict_
     if (Count) block_add_count(inv, inv_out);
 }
 
+// Small inputs (one CTA's worth): a bitonic network over (key, index) pairs in shared
+// memory, 1024 threads. Ties are broken by the original index, so the result equals the
+// stable sort's; the merge sort's single-tile path is one 256-thread CTA walking eight
+// dependent merge levels, which leaves a lone SM latency-bound (~30 us for 2048
+// 16-byte keys against ~3 us here) — that is the per-step rank sort of the engine loop.
+constexpr int MS_SMALL_MAX = 4096;
+constexpr int MS_SMALL_THREADS = 1024;
+
+template <typename K>
+__global__ void __launch_bounds__(MS_SMALL_THREADS) ms_small_sort(const K* __restrict__ keys_in, uint32_t n,
+                                                                  uint32_t npow2, uint32_t npad,
+                                                                  K* __restrict__ keys_out,
+                                                                  uint32_t* __restrict__ vals_out) {
+    extern __shared__ __align__(16) unsigned char ms_small_raw[];
+    K* sk = reinterpret_cast<K*>(ms_small_raw);
+    uint32_t* sv = reinterpret_cast<uint32_t*>(sk + npow2);
+    for (uint32_t i = threadIdx.x; i < npow2; i += MS_SMALL_THREADS) {
+        sk[i] = i < n ? keys_in[i] : KeyTraits<K>::sentinel();
+        sv[i] = i;  // padding indices (>= n) keep the sentinels last
+    }
+    __syncthreads();
+    for (uint32_t k = 2; k <= npow2; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            for (uint32_t t = threadIdx.x; t < (npow2 >> 1); t += MS_SMALL_THREADS) {
+                const uint32_t i = 2 * j * (t / j) + (t % j), p = i + j;
+                const K a = sk[i], b = sk[p];
+                const uint32_t ia = sv[i], ib = sv[p];
+                const bool b_lt_a = KeyTraits<K>::less(b, a) || (!KeyTraits<K>::less(a, b) && ib < ia);
+                if (b_lt_a == ((i & k) == 0)) {
+                    sk[i] = b;
+                    sk[p] = a;
+                    sv[i] = ib;
+                    sv[p] = ia;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < npad; i += MS_SMALL_THREADS) {
+        keys_out[i] = i < n ? sk[i] : KeyTraits<K>::sentinel();
+        if (vals_out) vals_out[i] = i < n ? sv[i] : 0xffffffffu;
+    }
+}
+
 static inline uint32_t ms_padded(uint64_t n) {
     return (uint32_t)((n + MS_TILE - 1) / MS_TILE * MS_TILE);
 }
@@ -346,6 +390,22 @@ int merge_sort(const K* keys_in, const uint32_t* vals_in, uint32_t n, K* k0, K* 
     const uint32_t npad = ms_padded(n);
     const uint32_t tiles = npad / MS_TILE;
     if (tiles == 0) {
+        *kres = k0;
+        if (vres) *vres = v0;
+        return RS_OK;
+    }
+    if (!Count && vals_in == nullptr && n <= (uint32_t)MS_SMALL_MAX) {
+        uint32_t np2 = 1;
+        while (np2 < n) np2 <<= 1;
+        const size_t smem = (size_t)np2 * (sizeof(K) + sizeof(uint32_t));
+        static bool attr = false;  // per template instance
+        if (!attr) {
+            RS_CUDA(cudaFuncSetAttribute(ms_small_sort<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(MS_SMALL_MAX * (sizeof(K) + sizeof(uint32_t)))));
+            attr = true;
+        }
+        ms_small_sort<K><<<1, MS_SMALL_THREADS, smem, st>>>(keys_in, n, np2, npad, k0, HasVal ? v0 : nullptr);
+        RS_LAUNCH_CHECK();
         *kres = k0;
         if (vres) *vres = v0;
         return RS_OK;
