@@ -22,7 +22,12 @@ constexpr int AB_T = 128, AB_D = 64;
 constexpr int AB_TILE_BYTES = AB_T * AB_D * 2;  // 16 KB
 constexpr int AB_SQ_BYTES = AB_T * AB_T * 2;    // 32 KB (P or dS)
 constexpr int AB_THREADS = 192;
-constexpr int AB_SMEM = 5 * AB_TILE_BYTES + 2 * AB_SQ_BYTES + 1024 + 256;
+// Two CTAs per SM (each CTA is a serial load -> MMA -> softmax -> MMA -> store chain, so a
+// second resident CTA overlaps one's phases with the other's): 112 KB of tiles and 256
+// TMEM columns each. V is dead once S / dP are computed and O once D is, so dS reuses V's
+// slot (plus one more 16 KB chunk) and P is written over O.
+constexpr int AB_SMEM_TILES = 3 * AB_TILE_BYTES + 2 * AB_SQ_BYTES;  // Q K dO | V+dS | O+P
+constexpr int AB_SMEM = AB_SMEM_TILES + 128;
 
 struct AbBars {
     uint64_t load_full, s_full, p_full, g_full;
@@ -41,20 +46,24 @@ __device__ __forceinline__ float tile_elem(const uint8_t* tile, int row, int c) 
     return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(tile + off));
 }
 
-__global__ void __launch_bounds__(AB_THREADS, 1)
+__global__ void __launch_bounds__(AB_THREADS, 2)
     attention_bwd_kernel(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tatt,
                          const __grid_constant__ CUtensorMap tdo, __nv_bfloat16* __restrict__ dqkv, int B, int S,
                          int H) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // the SW128 tiles need 1024-B alignment; dynamic shared memory of a kernel without
+    // static shared memory starts at the window base (checked, not padded: padding would
+    // push two CTAs past the SM's 228 KB)
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw;
+    if ((smem_u32(smem) & 1023u) != 0u) __trap();
     uint8_t* sQ = smem;
     uint8_t* sK = sQ + AB_TILE_BYTES;
-    uint8_t* sV = sK + AB_TILE_BYTES;
-    uint8_t* sO = sV + AB_TILE_BYTES;
-    uint8_t* sdO = sO + AB_TILE_BYTES;
-    uint8_t* sP = sdO + AB_TILE_BYTES;
-    uint8_t* sdS = sP + AB_SQ_BYTES;
-    AbBars* bar = reinterpret_cast<AbBars*>(sdS + AB_SQ_BYTES);
+    uint8_t* sdO = sK + AB_TILE_BYTES;
+    uint8_t* sV = sdO + AB_TILE_BYTES;  // dS chunk 0 once S / dP are done
+    uint8_t* sdS = sV;                  // 32 KB: V's slot + the next 16 KB
+    uint8_t* sP = sdS + AB_SQ_BYTES;    // 32 KB: O in its first 16 KB until D is taken
+    uint8_t* sO = sP;
+    AbBars* bar = reinterpret_cast<AbBars*>(sP + AB_SQ_BYTES);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int b = blockIdx.x / H, h = blockIdx.x % H;
@@ -69,12 +78,13 @@ __global__ void __launch_bounds__(AB_THREADS, 1)
         mbar_init(&bar->g_full, 1);
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<512>(&bar->tmem);
+    if (warp == 1) tmem_alloc<256>(&bar->tmem);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = bar->tmem;
-    const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem + 256, tdK = tmem + 320, tdQ = tmem + 384;
+    // S, dP first; the gradient accumulators reuse their columns once P / dS are out
+    const uint32_t tS = tmem, tdP = tmem + 128, tdV = tmem, tdK = tmem + 64, tdQ = tmem + 128;
 
     if (warp == 0) {
         if (elect_one()) {
@@ -212,7 +222,7 @@ __global__ void __launch_bounds__(AB_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 1) tmem_dealloc<512>(tmem);
+    if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
 int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv, int B, int S, int H, cudaStream_t st) {
@@ -221,6 +231,7 @@ int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv
     static bool attr = false;
     if (!attr) {
         RS_CUDA(cudaFuncSetAttribute(attention_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AB_SMEM));
+        RS_CUDA(cudaFuncSetAttribute(attention_bwd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
         attr = true;
     }
     const uint64_t rows = (uint64_t)B * S;

@@ -10,6 +10,7 @@
 // positions carry an offset of 2).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <stdlib.h>
 #include "common.cuh"
 #include "gemm.cuh"
 
@@ -368,8 +369,18 @@ static int check_cfg(const rs_ranker_config* c) {
 
 constexpr int64_t RK_MAX_TOKENS = 1 << 20;  // activation chunk (tokens) per forward slice
 
+static int64_t chunk_tokens() {
+    static int64_t t = 0;
+    if (!t) {
+        const char* e = getenv("RSB200_CHUNK_TOKENS");
+        t = e ? atoll(e) : RK_MAX_TOKENS;
+        if (t < 256) t = RK_MAX_TOKENS;
+    }
+    return t;
+}
+
 static int64_t chunk_prompts(int32_t B, int32_t S) {
-    int64_t bc = RK_MAX_TOKENS / S;
+    int64_t bc = chunk_tokens() / S;
     if (bc < 1) bc = 1;
     if (bc > B) bc = B;
     return bc;
