@@ -230,6 +230,16 @@ def gemm_roofline(pk, M=1 << 20, reps=5):
             "algorithmic_flops": tot_f, "per_shape": res}
 
 
+def sort_traffic(key):
+    """DRAM bytes (read + write) of one call from the committed ncu capture, or None."""
+    p = ROOT / "profiles" / "r01_sort_traffic.json"
+    try:
+        d = json.loads(p.read_text())[key]
+        return d["dram_read_bytes"] + d["dram_write_bytes"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def tau_and_rankstep(pk, reps=5):
     """cfg4 secondary metrics on rank 0: exact tau counts and one ranking step over
     the 1M-request queue (device time, CUDA events)."""
@@ -273,11 +283,12 @@ def tau_and_rankstep(pk, reps=5):
                 "n": n, "ms": t, "ms_eager": t_eager, "note": "ms: the kernels replayed as one CUDA graph",
                 "roofline": {"bound": "hbm", "achieved": tau_bytes / t / 1e6, "peak": pk["hbm_gbs"],
                                               "unit": "GB/s", "frac": tau_bytes / t / 1e6 / pk["hbm_gbs"],
-                                              "traffic": None, "algorithmic_bytes": tau_bytes}},
+                                              "traffic": sort_traffic("tau_1m"), "algorithmic_bytes": tau_bytes}},
         "rank_step": {"metric": "requests ranked/sec (sort + fill + starvation bump)", "value": n / (tr / 1e3),
                       "unit": "requests/s", "n": n, "ms": tr, "ms_eager": tr_eager,
                       "roofline": {"bound": "hbm", "achieved": rs_bytes / tr / 1e6, "peak": pk["hbm_gbs"],
-                                   "unit": "GB/s", "frac": rs_bytes / tr / 1e6 / pk["hbm_gbs"], "traffic": None,
+                                   "unit": "GB/s", "frac": rs_bytes / tr / 1e6 / pk["hbm_gbs"],
+                                   "traffic": sort_traffic("rank_step_1m"),
                                    "algorithmic_bytes": rs_bytes}},
     }
 
