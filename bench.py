@@ -607,8 +607,8 @@ def main():
     ap.add_argument("--train-seq", type=int, default=128)
     ap.add_argument("--train-micro", type=int, default=16)
     ap.add_argument("--train-steps", type=int, default=1)
-    ap.add_argument("--e2e-requests", type=int, default=20000,
-                    help="cfg5 loop size (BASELINE configs[4] is 100000; 0 disables)")
+    ap.add_argument("--e2e-requests", type=int, default=100000,
+                    help="cfg5 loop size (BASELINE configs[4]: 100000; 0 disables)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -173,6 +173,14 @@ int rs_engine_admit(const rs_engine_queue* q, const rs_engine_trace* tr, const i
 int rs_engine_execute(const rs_engine_queue* q, const rs_engine_trace* tr, const rs_engine_cost* cost,
                       const int64_t* run_dev, const int32_t* counts_dev, int32_t step, int64_t predictor_ns,
                       int64_t* out_dev, int64_t* preempted_dev, int64_t* finished_dev, void* stream);
+/* Same step with the surviving rows compacted out of place into q_out's columns (same
+ * capacity and score dtype; q_out->n is ignored) by many CTAs instead of in place by one —
+ * the caller swaps the two column sets every step. scratch_dev: int32[ceil(n / 1024)].
+ * q_out == NULL is rs_engine_execute. */
+int rs_engine_execute_ex(const rs_engine_queue* q, const rs_engine_queue* q_out, const rs_engine_trace* tr,
+                         const rs_engine_cost* cost, const int64_t* run_dev, const int32_t* counts_dev, int32_t step,
+                         int64_t predictor_ns, int64_t* out_dev, int64_t* preempted_dev, int64_t* finished_dev,
+                         int32_t* scratch_dev, void* stream);
 
 /* ---- A5/K1-K5: OPT-shape ranker ------------------------------------------------
  * Parameters live in ONE contiguous bf16 buffer laid out by rs_ranker_layout():

@@ -62,6 +62,16 @@ __global__ void __launch_bounds__(EX_THREADS) engine_admit_kernel(rs_engine_queu
     tr.last_event_ns[r] = tr.arrival_ns[r];
 }
 
+constexpr uint8_t EX_PRE = 16;     // row preempted this step (cleared before the kernel ends)
+constexpr int EX_PRE_CAP = 4096;   // preempted rows ordered in shared memory up to this many
+
+// Phases 1-3 of _Sim.execute on one CTA (µs of work: every phase needs the previous one
+// complete). Preemption only concerns rows that were RUNNING (<= last step's batch) and
+// prefill only rows in this step's run, so neither phase walks the queue with ordered
+// scans: preempted rows are collected unordered and put back in alive (row) order by a
+// shared-memory bitonic sort. Compaction is either in place (InPlace, one CTA, ordered
+// block scans) or left to engine_compact_* (out of place, many CTAs).
+template <bool InPlace>
 __global__ void __launch_bounds__(EX_THREADS) engine_execute_kernel(rs_engine_queue q, rs_engine_trace tr,
                                                                     rs_engine_cost cost, const int64_t* __restrict__ run,
                                                                     const int32_t* __restrict__ counts, int32_t step,
@@ -71,6 +81,7 @@ __global__ void __launch_bounds__(EX_THREADS) engine_execute_kernel(rs_engine_qu
     __shared__ int warp_tot[32];
     __shared__ unsigned long long prefill_tokens;
     __shared__ int n_pre;
+    __shared__ int pre_rows[EX_PRE_CAP];
     const int tid = threadIdx.x;
     const int n_run = counts[0];
     const int64_t n = q.n;
@@ -80,32 +91,73 @@ __global__ void __launch_bounds__(EX_THREADS) engine_execute_kernel(rs_engine_qu
     }
     for (int k = tid; k < n_run; k += EX_THREADS) tr.run_stamp[run[k]] = step;
     __syncthreads();
-    // 1. preemption / prefill (engine.py:248-262), preempted ids in alive order
-    for (int64_t base = 0; base < n; base += EX_THREADS) {
-        const int64_t row = base + tid;
-        int pre = 0;
-        unsigned long long pf = 0ull;
-        if (row < n) {
+    // 1a. preemption (engine.py:248-256): RUNNING rows left out of the batch
+    for (int64_t row = tid; row < n; row += EX_THREADS) {
+        const uint8_t fl = q.flags[row];
+        if (fl & RS_FLAG_RUNNING) {
             const int64_t id = q.id[row];
-            const bool running = q.flags[row] & RS_FLAG_RUNNING;
-            const bool in_run = tr.run_stamp[id] == step;
-            if (running && !in_run) {
-                q.flags[row] &= (uint8_t)~RS_FLAG_RUNNING;
+            if (tr.run_stamp[id] != step) {
+                q.flags[row] = (uint8_t)((fl & ~RS_FLAG_RUNNING) | EX_PRE);
                 tr.n_preempted[id] += 1;
-                pre = 1;
-            } else if (in_run && !running) {
-                pf = (unsigned long long)(q.prompt_tokens[row] + q.generated_tokens[row]);
-                q.flags[row] |= RS_FLAG_RUNNING;
+                const int slot = atomicAdd(&n_pre, 1);
+                if (slot < EX_PRE_CAP) pre_rows[slot] = (int)row;
             }
         }
-        if (pf) atomicAdd(&prefill_tokens, pf);
-        int total;
-        const int pos = block_excl_scan(pre, warp_tot, total);
-        if (pre) preempted[n_pre + pos] = q.id[row];
-        __syncthreads();
-        if (tid == 0) n_pre += total;
-        __syncthreads();
     }
+    __syncthreads();
+    const int total_pre = n_pre;
+    if (total_pre <= EX_PRE_CAP) {
+        int np2 = 1;
+        while (np2 < total_pre) np2 <<= 1;
+        for (int i = total_pre + tid; i < np2; i += EX_THREADS) pre_rows[i] = 0x7fffffff;
+        __syncthreads();
+        for (int k = 2; k <= np2; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int t = tid; t < (np2 >> 1); t += EX_THREADS) {
+                    const int i = 2 * j * (t / j) + (t % j), p = i + j;
+                    const int a = pre_rows[i], b = pre_rows[p];
+                    if ((b < a) == ((i & k) == 0)) {
+                        pre_rows[i] = b;
+                        pre_rows[p] = a;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int i = tid; i < total_pre; i += EX_THREADS) {
+            const int row = pre_rows[i];
+            preempted[i] = q.id[row];
+            q.flags[row] &= (uint8_t)~EX_PRE;
+        }
+    } else {
+        // more than EX_PRE_CAP preemptions (max_batch > EX_PRE_CAP): ordered block scans
+        int base_out = 0;
+        for (int64_t base = 0; base < n; base += EX_THREADS) {
+            const int64_t row = base + tid;
+            int pre = 0;
+            if (row < n && (q.flags[row] & EX_PRE)) {
+                pre = 1;
+                q.flags[row] &= (uint8_t)~EX_PRE;
+            }
+            int total;
+            const int pos = block_excl_scan(pre, warp_tot, total);
+            if (pre) preempted[base_out + pos] = q.id[row];
+            base_out += total;
+        }
+    }
+    // 1b. prefill (engine.py:257-262): scheduled rows that were not running
+    unsigned long long pf = 0ull;
+    for (int k = tid; k < n_run; k += EX_THREADS) {
+        const int row = tr.row_of[run[k]];
+        const uint8_t fl = q.flags[row];
+        if (!(fl & RS_FLAG_RUNNING)) {
+            pf += (unsigned long long)(q.prompt_tokens[row] + q.generated_tokens[row]);
+            q.flags[row] = (uint8_t)(fl | RS_FLAG_RUNNING);
+        }
+    }
+    pf = warp_sum(pf);
+    if ((tid & 31) == 0 && pf) atomicAdd(&prefill_tokens, pf);
+    __syncthreads();
     // 2. clock
     __shared__ long long now_s;
     if (tid == 0) {
@@ -121,7 +173,7 @@ __global__ void __launch_bounds__(EX_THREADS) engine_execute_kernel(rs_engine_qu
         out[0] = now_s;
         out[1] = iter;
         out[2] = (long long)prefill_tokens * cost.prefill_ns_per_token;
-        out[4] = n_pre;
+        out[4] = total_pre;
     }
     __syncthreads();
     const long long now = now_s;
@@ -152,6 +204,8 @@ __global__ void __launch_bounds__(EX_THREADS) engine_execute_kernel(rs_engine_qu
         done_before += total;
     }
     __syncthreads();
+    if (tid == 0) out[5] = done_before;
+    if (!InPlace) return;
     // 4. stable in-place compaction of the rows still alive
     int64_t kept = 0;
     for (int64_t base = 0; base < n; base += EX_THREADS) {
@@ -194,10 +248,57 @@ __global__ void __launch_bounds__(EX_THREADS) engine_execute_kernel(rs_engine_qu
         kept += total;
         __syncthreads();
     }
-    if (tid == 0) {
-        out[3] = kept;
-        out[5] = done_before;
+    if (tid == 0) out[3] = kept;
+}
+
+// Out-of-place stable compaction (queue q -> q_out) over many CTAs: per-CTA survivor
+// counts, then each CTA sums the counts before it (<= n / 1024 of them) and scatters.
+__global__ void __launch_bounds__(EX_THREADS) engine_compact_count(const uint8_t* __restrict__ flags, int64_t n,
+                                                                   int32_t* __restrict__ block_keep) {
+    __shared__ int warp_tot[32];
+    const int64_t row = (int64_t)blockIdx.x * EX_THREADS + threadIdx.x;
+    const int keep = row < n && !(flags[row] & EX_DONE);
+    int total;
+    block_excl_scan(keep, warp_tot, total);
+    if (threadIdx.x == 0) block_keep[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(EX_THREADS) engine_compact_scatter(rs_engine_queue q, rs_engine_queue qo,
+                                                                     rs_engine_trace tr,
+                                                                     const int32_t* __restrict__ block_keep,
+                                                                     int64_t* __restrict__ out) {
+    __shared__ int warp_tot[32];
+    __shared__ long long base_s;
+    const int tid = threadIdx.x;
+    if (tid < 32) {
+        long long b = 0;
+        for (int k = tid; k < (int)blockIdx.x; k += 32) b += block_keep[k];
+        b = warp_sum(b);
+        if (tid == 0) base_s = b;
     }
+    const int64_t row = (int64_t)blockIdx.x * EX_THREADS + tid;
+    const bool valid = row < q.n;
+    const uint8_t fl = valid ? q.flags[row] : (uint8_t)EX_DONE;
+    const int keep = !(fl & EX_DONE);
+    int total;
+    const int pos = block_excl_scan(keep, warp_tot, total);  // its barriers publish base_s
+    if (keep) {
+        const int64_t dst = base_s + pos;
+        if (q.score_dtype == RS_F64)
+            static_cast<double*>(qo.score)[dst] = static_cast<const double*>(q.score)[row];
+        else
+            static_cast<float*>(qo.score)[dst] = static_cast<const float*>(q.score)[row];
+        const int64_t id = q.id[row];
+        qo.flags[dst] = fl;
+        qo.prompt_tokens[dst] = q.prompt_tokens[row];
+        qo.generated_tokens[dst] = q.generated_tokens[row];
+        qo.arrival_rank[dst] = q.arrival_rank[row];
+        qo.id[dst] = id;
+        qo.starvation[dst] = q.starvation[row];
+        qo.quantum[dst] = q.quantum[row];
+        tr.row_of[id] = (int32_t)dst;
+    }
+    if (blockIdx.x == gridDim.x - 1 && tid == 0) out[3] = base_s + total;
 }
 
 }  // namespace rs
@@ -215,16 +316,39 @@ extern "C" int rs_engine_admit(const rs_engine_queue* q, const rs_engine_trace* 
     return RS_OK;
 }
 
+extern "C" int rs_engine_execute_ex(const rs_engine_queue* q, const rs_engine_queue* q_out,
+                                    const rs_engine_trace* tr, const rs_engine_cost* cost, const int64_t* run_dev,
+                                    const int32_t* counts_dev, int32_t step, int64_t predictor_ns, int64_t* out_dev,
+                                    int64_t* preempted_dev, int64_t* finished_dev, int32_t* scratch_dev,
+                                    void* stream) {
+    RS_CHECK_ARG(q && tr && cost && run_dev && counts_dev && out_dev && preempted_dev && finished_dev,
+                 "rs_engine_execute: NULL argument");
+    RS_CHECK_ARG(cost->decode_table_len == 0 || cost->decode_table != nullptr, "rs_engine_execute: decode table");
+    RS_CHECK_ARG(q_out == nullptr || (scratch_dev != nullptr && q_out->score_dtype == q->score_dtype),
+                 "rs_engine_execute_ex: out-of-place compaction needs scratch and a matching q_out");
+    cudaStream_t st = as_stream(stream);
+    if (q_out == nullptr) {
+        engine_execute_kernel<true><<<1, EX_THREADS, 0, st>>>(*q, *tr, *cost, run_dev, counts_dev, step, predictor_ns,
+                                                               out_dev, preempted_dev, finished_dev);
+        RS_LAUNCH_CHECK();
+        return RS_OK;
+    }
+    engine_execute_kernel<false><<<1, EX_THREADS, 0, st>>>(*q, *tr, *cost, run_dev, counts_dev, step, predictor_ns,
+                                                            out_dev, preempted_dev, finished_dev);
+    RS_LAUNCH_CHECK();
+    const int64_t nb64 = (q->n + EX_THREADS - 1) / EX_THREADS;
+    const unsigned nb = nb64 > 0 ? (unsigned)nb64 : 1u;
+    engine_compact_count<<<nb, EX_THREADS, 0, st>>>(q->flags, q->n, scratch_dev);
+    RS_LAUNCH_CHECK();
+    engine_compact_scatter<<<nb, EX_THREADS, 0, st>>>(*q, *q_out, *tr, scratch_dev, out_dev);
+    RS_LAUNCH_CHECK();
+    return RS_OK;
+}
+
 extern "C" int rs_engine_execute(const rs_engine_queue* q, const rs_engine_trace* tr, const rs_engine_cost* cost,
                                  const int64_t* run_dev, const int32_t* counts_dev, int32_t step,
                                  int64_t predictor_ns, int64_t* out_dev, int64_t* preempted_dev,
                                  int64_t* finished_dev, void* stream) {
-    RS_CHECK_ARG(q && tr && cost && run_dev && counts_dev && out_dev && preempted_dev && finished_dev,
-                 "rs_engine_execute: NULL argument");
-    RS_CHECK_ARG(cost->decode_table_len == 0 || cost->decode_table != nullptr, "rs_engine_execute: decode table");
-    engine_execute_kernel<<<1, EX_THREADS, 0, as_stream(stream)>>>(*q, *tr, *cost, run_dev, counts_dev, step,
-                                                                    predictor_ns, out_dev, preempted_dev,
-                                                                    finished_dev);
-    RS_LAUNCH_CHECK();
-    return RS_OK;
+    return rs_engine_execute_ex(q, nullptr, tr, cost, run_dev, counts_dev, step, predictor_ns, out_dev, preempted_dev,
+                                finished_dev, nullptr, stream);
 }

@@ -88,7 +88,8 @@ class DeviceEngine:
 
     def __init__(self, requests, scores, sched: SchedulerConfig = SchedulerConfig(),
                  cost: CostModel = COST_PRESETS["default"], kv_budget: int | None = None,
-                 length_calibrated: bool = False, charges_predictor: bool = True, dev=None):
+                 length_calibrated: bool = False, charges_predictor: bool = True, dev=None,
+                 in_place_compaction: bool = False):
         self.reqs = list(requests)
         n = len(self.reqs)
         if len(scores) != n:
@@ -97,8 +98,6 @@ class DeviceEngine:
         self.kv_budget = UNLIMITED_KV if kv_budget is None else int(kv_budget)
         if self.kv_budget < 1:
             raise ValueError("kv_budget must be >= 1")
-        if sched.max_batch > 1024:
-            raise ValueError("max_batch > 1024 is not supported by rs_engine_execute")
         self.length_calibrated = bool(length_calibrated)
         self.charges_predictor = bool(charges_predictor)
         self.dev = dev or _lib.device()
@@ -131,14 +130,20 @@ class DeviceEngine:
         self.finish = torch.full((n,), -1, dtype=i64, device=d)
         self.n_pre = torch.zeros(n, dtype=i32, device=d)
         cap = max(n, 1)
-        self.q_score = torch.zeros(cap, dtype=torch.float64, device=d)
-        self.q_flags = torch.zeros(cap, dtype=torch.uint8, device=d)
-        self.q_prompt = torch.zeros(cap, dtype=i32, device=d)
-        self.q_gen = torch.zeros(cap, dtype=i32, device=d)
-        self.q_rank = torch.zeros(cap, dtype=i32, device=d)
-        self.q_id = torch.zeros(cap, dtype=i64, device=d)
-        self.q_starv = torch.zeros(cap, dtype=i32, device=d)
-        self.q_quant = torch.zeros(cap, dtype=i32, device=d)
+        # Queue columns. Out-of-place compaction (the default) keeps two column sets and
+        # swaps them every step: execute compacts the survivors of set `cur` into the other
+        # set with many CTAs (rs_engine_execute_ex); in place, one CTA does it (the
+        # rs_engine_execute path, kept selectable for tests).
+        self.in_place = bool(in_place_compaction)
+        self._sets = []
+        for _ in range(1 if self.in_place else 2):
+            self._sets.append({
+                "score": torch.zeros(cap, dtype=torch.float64, device=d),
+                "flags": torch.zeros(cap, dtype=torch.uint8, device=d),
+                "prompt": torch.zeros(cap, dtype=i32, device=d), "gen": torch.zeros(cap, dtype=i32, device=d),
+                "rank": torch.zeros(cap, dtype=i32, device=d), "id": torch.zeros(cap, dtype=i64, device=d),
+                "starv": torch.zeros(cap, dtype=i32, device=d), "quant": torch.zeros(cap, dtype=i32, device=d)})
+        self.compact_scratch = torch.zeros((cap + 1023) // 1024 + 1, dtype=i32, device=d)
         self.run_out = torch.empty(max(sched.max_batch, 1), dtype=i64, device=d)
         self.prom_out = torch.empty(cap, dtype=i64, device=d)
         self.dem_out = torch.empty(cap, dtype=i64, device=d)
@@ -160,15 +165,16 @@ class DeviceEngine:
                                      None if self.t_table is None else self.t_table.data_ptr(),
                                      0 if dt is None else len(dt))
 
-    def _queue(self, n_alive: int) -> _lib.EngineQueue:
-        return _lib.EngineQueue(n_alive, _lib.RS_F64, self.q_score.data_ptr(), self.q_prompt.data_ptr(),
-                                self.q_gen.data_ptr(), self.q_rank.data_ptr(), self.q_id.data_ptr(),
-                                self.q_flags.data_ptr(), self.q_starv.data_ptr(), self.q_quant.data_ptr())
+    @staticmethod
+    def _cols(c):
+        return (c["score"].data_ptr(), c["prompt"].data_ptr(), c["gen"].data_ptr(), c["rank"].data_ptr(),
+                c["id"].data_ptr(), c["flags"].data_ptr(), c["starv"].data_ptr(), c["quant"].data_ptr())
 
-    def _soa(self, n_alive: int) -> _lib.QueueSoA:
-        return _lib.QueueSoA(n_alive, _lib.RS_F64, self.q_score.data_ptr(), self.q_prompt.data_ptr(),
-                             self.q_gen.data_ptr(), self.q_rank.data_ptr(), self.q_id.data_ptr(),
-                             self.q_flags.data_ptr(), self.q_starv.data_ptr(), self.q_quant.data_ptr())
+    def _queue(self, n_alive: int, which: int = 0) -> _lib.EngineQueue:
+        return _lib.EngineQueue(n_alive, _lib.RS_F64, *self._cols(self._sets[which]))
+
+    def _soa(self, n_alive: int, which: int = 0) -> _lib.QueueSoA:
+        return _lib.QueueSoA(n_alive, _lib.RS_F64, *self._cols(self._sets[which]))
 
     def run(self, record: bool = False, stop_after_finished: int | None = None,
             time_limit_s: float | None = None) -> EngineResult:
@@ -181,9 +187,15 @@ class DeviceEngine:
         sched = self.sched
         budget = -1 if self.kv_budget >= UNLIMITED_KV else self.kv_budget
         fits = (self.prompt.astype(np.int64) + self.true_out) <= self.kv_budget
-        q, soa = self._queue(0), self._soa(0)
-        q_ref, soa_ref, tr_ref, cost_ref = (ctypes.byref(q), ctypes.byref(soa), ctypes.byref(self._trace),
-                                            ctypes.byref(self._cost))
+        nsets = len(self._sets)
+        qs = [self._queue(0, i) for i in range(nsets)]
+        soas = [self._soa(0, i) for i in range(nsets)]
+        q_refs = [ctypes.byref(x) for x in qs]
+        soa_refs = [ctypes.byref(x) for x in soas]
+        tr_ref, cost_ref = ctypes.byref(self._trace), ctypes.byref(self._cost)
+        execute_ex = lib.rs_engine_execute_ex
+        scratch_p = self.compact_scratch.data_ptr()
+        cur = 0
         run_p, prom_p, dem_p, cnt_p = (self.run_out.data_ptr(), self.prom_out.data_ptr(), self.dem_out.data_ptr(),
                                        self.counts.data_ptr())
         out_p, pre_p, fin_p, adm_p = (self.out.data_ptr(), self.pre_out.data_ptr(), self.fin_out.data_ptr(),
@@ -215,8 +227,8 @@ class DeviceEngine:
                 if k:
                     adm_np[:k] = admitted
                     self.adm_dev[:k].copy_(self.adm_host[:k], non_blocking=True)
-                    q.n = n_alive
-                    check(admit(q_ref, tr_ref, adm_p, k, n_alive, st), "rs_engine_admit")
+                    qs[cur].n = n_alive
+                    check(admit(q_refs[cur], tr_ref, adm_p, k, n_alive, st), "rs_engine_admit")
                     n_alive += k
             if n_alive == 0:
                 break
@@ -226,15 +238,20 @@ class DeviceEngine:
             if n_alive > ws_n:
                 ws_n = max(n_alive, 2 * ws_n)
                 ws, wn = _lib.workspace.get(lib.rs_rank_step_workspace_size(ws_n), self.dev)
-            soa.n = n_alive
-            check(rank_step(soa_ref, sched.max_batch, budget, sched.starvation_threshold, sched.priority_quantum,
+            soas[cur].n = n_alive
+            check(rank_step(soa_refs[cur], sched.max_batch, budget, sched.starvation_threshold, sched.priority_quantum,
                             int(self.length_calibrated), int(sched.preemption), run_p, prom_p, dem_p, cnt_p, ws, wn,
                             st), "rs_rank_step")
             out_np[0] = now
             self.out.copy_(self.out_host, non_blocking=True)
-            q.n = n_alive
-            check(execute(q_ref, tr_ref, cost_ref, run_p, cnt_p, step, predictor_ns, out_p, pre_p, fin_p, st),
-                  "rs_engine_execute")
+            qs[cur].n = n_alive
+            if nsets == 1:
+                check(execute(q_refs[0], tr_ref, cost_ref, run_p, cnt_p, step, predictor_ns, out_p, pre_p, fin_p, st),
+                      "rs_engine_execute")
+            else:
+                check(execute_ex(q_refs[cur], q_refs[1 - cur], tr_ref, cost_ref, run_p, cnt_p, step, predictor_ns,
+                                 out_p, pre_p, fin_p, scratch_p, st), "rs_engine_execute_ex")
+                cur = 1 - cur
             self.out_host.copy_(self.out, non_blocking=True)
             self.cnt_host.copy_(self.counts, non_blocking=True)
             stream.synchronize()
@@ -319,7 +336,8 @@ class DeviceEngine:
 
 def run(trace, scorer=None, scores=None, sched: SchedulerConfig = SchedulerConfig(),
         cost: CostModel = COST_PRESETS["default"], kv_budget: int | None = None, seed: int = 0,
-        record: bool = False, stop_after_finished: int | None = None, time_limit_s: float | None = None):
+        record: bool = False, stop_after_finished: int | None = None, time_limit_s: float | None = None,
+        in_place_compaction: bool = False):
     """engine.run(trace, "ranking", scorer, ...) on the device. Give either a scorer (its
     score_batch is called once over the whole trace: the score cache) or `scores`."""
     reqs = list(trace)
@@ -331,5 +349,6 @@ def run(trace, scorer=None, scores=None, sched: SchedulerConfig = SchedulerConfi
             raise ValueError("the device engine needs a score for every request (warm-up scorers unsupported)")
     length_calibrated = getattr(scorer, "length_calibrated", False) if scorer is not None else False
     charges = getattr(scorer, "charges_predictor", True) if scorer is not None else True
-    eng = DeviceEngine(reqs, scores, sched, cost, kv_budget, length_calibrated, charges)
+    eng = DeviceEngine(reqs, scores, sched, cost, kv_budget, length_calibrated, charges,
+                       in_place_compaction=in_place_compaction)
     return eng.run(record=record, stop_after_finished=stop_after_finished, time_limit_s=time_limit_s)

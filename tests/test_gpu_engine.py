@@ -16,8 +16,9 @@ def _canonical(obj):
     return json.dumps(obj, sort_keys=True, separators=(",", ":"))
 
 
+@pytest.mark.parametrize("in_place", [False, True])
 @pytest.mark.parametrize("idx", [0, 1, 2, 3])
-def test_engine_matches_reference_run(golden, idx):
+def test_engine_matches_reference_run(golden, idx, in_place):
     from paper_2408_15792_b200 import engine
     from paper_2408_15792_b200.schedulers import SchedulerConfig
     from paper_2408_15792_b200.workload import Request
@@ -25,7 +26,7 @@ def test_engine_matches_reference_run(golden, idx):
     reqs = [Request(id=i, arrival_time=a, prompt_tokens=p, true_output_tokens=o) for i, a, p, o in c["requests"]]
     sched = SchedulerConfig(**c["sched"])
     res = engine.run(reqs, scores=c["scores"], sched=sched, cost=engine.COST_PRESETS[c["cost"]],
-                     kv_budget=c["kv_budget"], record=True)
+                     kv_budget=c["kv_budget"], record=True, in_place_compaction=in_place)
     assert res.records[:len(c["first_records"])] == c["first_records"]
     assert len(res.records) == c["n_steps"]
     assert hashlib.sha256(_canonical(res.records).encode()).hexdigest() == c["records_sha256"]
@@ -44,3 +45,24 @@ def test_engine_rejects_bad_config():
         engine.run(reqs)  # no scorer, no scores
     with pytest.raises(ValueError):
         engine.run(reqs, scores=[float("nan")])
+
+
+def test_engine_out_of_place_matches_in_place_at_scale():
+    """Thousands of alive rows (multi-CTA compaction, many preemptions): the out-of-place
+    step gives the same records as the single-CTA in-place one."""
+    import numpy as np
+    from paper_2408_15792_b200 import engine
+    from paper_2408_15792_b200.schedulers import SchedulerConfig
+    from paper_2408_15792_b200.workload import Request
+    rng = np.random.default_rng(3)
+    n = 6000
+    arr = np.cumsum(rng.exponential(1.0 / 200.0, n))
+    out = np.clip(np.rint(rng.lognormal(5.0, 0.9, n)), 1, 2048).astype(int)
+    reqs = [Request(id=i, arrival_time=float(arr[i]), prompt_tokens=int(rng.integers(8, 129)),
+                    true_output_tokens=int(out[i])) for i in range(n)]
+    scores = rng.normal(size=n).round(2).tolist()  # ties exercise the arrival tie-break
+    sched = SchedulerConfig(max_batch=64, starvation_threshold=20, priority_quantum=5)
+    a = engine.run(reqs, scores=scores, sched=sched, record=True, stop_after_finished=1500)
+    b = engine.run(reqs, scores=scores, sched=sched, record=True, stop_after_finished=1500, in_place_compaction=True)
+    assert max(len(r["preempted"]) for r in a.records) > 0
+    assert a.steps == b.steps and a.records == b.records and a.requests == b.requests
