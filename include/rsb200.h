@@ -182,6 +182,18 @@ int rs_engine_execute_ex(const rs_engine_queue* q, const rs_engine_queue* q_out,
                          int64_t predictor_ns, int64_t* out_dev, int64_t* preempted_dev, int64_t* finished_dev,
                          int32_t* scratch_dev, void* stream);
 
+/* ---- §8f #2: prompt strings -> token ids on the device ---------------------------
+ * The scorer's id map (workload.prompt_token_ids; the reference's salted crc32 token
+ * hash, workload.py:125-126): whitespace tokens, the first min(seq_len, 2048), lower-cased,
+ * id = 4 + crc32(salt + token) % (vocab - 4), padded with pad_id; empty prompt -> {2}.
+ * text_dev: the prompts' UTF-8 bytes back to back; offsets_dev int64[n + 1]; salt_crc =
+ * crc32(salt). ids_dev int32[n, seq_len], last_dev int32[n] (last token index), bad_dev
+ * int32[n] = 1 for a prompt whose result depends on non-ASCII bytes (str.split / lower
+ * are Unicode-aware): the caller must reject it. */
+int rs_tokenize(const uint8_t* text_dev, const int64_t* offsets_dev, int32_t n, int32_t seq_len, int32_t vocab,
+                int32_t pad_id, uint32_t salt_crc, int32_t* ids_dev, int32_t* last_dev, int32_t* bad_dev,
+                void* stream);
+
 /* ---- A5/K1-K5: OPT-shape ranker ------------------------------------------------
  * Parameters live in ONE contiguous bf16 buffer laid out by rs_ranker_layout():
  *   tok_emb[V,d] pos_emb[P+2,d] { ln1_w[d] ln1_b[d] qkv_w[3d,d] qkv_b[3d] out_w[d,d]

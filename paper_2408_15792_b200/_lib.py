@@ -80,6 +80,7 @@ SIGNATURES = {
     "rs_engine_execute_ex": (ctypes.c_int, [ctypes.POINTER(EngineQueue), ctypes.POINTER(EngineQueue),
                                             ctypes.POINTER(EngineTrace), ctypes.POINTER(EngineCost), c_vp, c_vp, c_i32,
                                             c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "rs_tokenize": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, ctypes.c_uint32, c_vp, c_vp, c_vp, c_vp]),
     "rs_rank_step_workspace_size": (c_sz, [c_i64]),
     "rs_rank_step": (ctypes.c_int, [ctypes.POINTER(QueueSoA), c_i32, c_i64, c_i32, c_i32, c_i32, c_i32,
                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),

@@ -26,7 +26,7 @@ import torch
 
 from . import _lib
 from .ranker import OptRanker, RankerConfig
-from .workload import prompt_token_ids
+from .workload import prompt_token_ids, prompt_token_ids_device
 
 _SCORER_FORMAT = "ranksched-scorer"
 _SCORER_VERSION = 1
@@ -41,10 +41,13 @@ class OptRankerScorer:
     charges_predictor = True
 
     def __init__(self, model: OptRanker | None = None, seq_len: int = 128, cfg: RankerConfig | None = None,
-                 seed: int = 0):
+                 seed: int = 0, device_tokenizer: bool = False):
         self.model = model if model is not None else OptRanker(cfg or RankerConfig(), seed=seed)
         self.seq_len = int(seq_len)
         self.weights_path: str | None = None
+        # True: prompts -> ids on the device (rs_tokenize, identical ids; ASCII prompts
+        # only — others raise); False: the host map, any Unicode prompt
+        self.device_tokenizer = bool(device_tokenizer)
 
     def encode(self, requests) -> tuple[torch.Tensor, torch.Tensor]:
         """Prompts -> (ids int32 [n, S], last_pos int32 [n]) in pinned host memory."""
@@ -60,9 +63,14 @@ class OptRankerScorer:
     def raw_outputs(self, requests) -> np.ndarray:
         if not requests:
             return np.zeros(0)
-        ids, last = self.encode(requests)
         dev = self.model.dev
-        g = self.model.forward(ids.to(dev, non_blocking=True), last.to(dev, non_blocking=True))
+        if self.device_tokenizer:
+            ids, last = prompt_token_ids_device([getattr(r, "prompt", "") or "" for r in requests], self.seq_len,
+                                                self.model.cfg.vocab, device=dev)
+            g = self.model.forward(ids, last)
+        else:
+            ids, last = self.encode(requests)
+            g = self.model.forward(ids.to(dev, non_blocking=True), last.to(dev, non_blocking=True))
         return g.double().cpu().numpy()
 
     def score_batch(self, requests, seed) -> list[float | None]:
