@@ -66,3 +66,21 @@ def test_engine_out_of_place_matches_in_place_at_scale():
     b = engine.run(reqs, scores=scores, sched=sched, record=True, stop_after_finished=1500, in_place_compaction=True)
     assert max(len(r["preempted"]) for r in a.records) > 0
     assert a.steps == b.steps and a.records == b.records and a.requests == b.requests
+
+
+def test_engine_mass_preemption_keeps_alive_order():
+    """More preemptions in one step than the shared-memory ordering holds (4096): the
+    ordered-scan path must still emit them in alive (= admission = id) order."""
+    from paper_2408_15792_b200 import engine
+    from paper_2408_15792_b200.schedulers import SchedulerConfig
+    from paper_2408_15792_b200.workload import Request
+    n1 = 6000
+    reqs = [Request(id=i, arrival_time=0.0, prompt_tokens=4, true_output_tokens=50) for i in range(n1)]
+    reqs += [Request(id=n1 + i, arrival_time=1e-3, prompt_tokens=4, true_output_tokens=50) for i in range(n1)]
+    scores = [1.0] * n1 + [0.0] * n1  # the second burst outranks the first
+    sched = SchedulerConfig(max_batch=n1, starvation_threshold=0, priority_quantum=50)
+    for in_place in (False, True):
+        res = engine.run(reqs, scores=scores, sched=sched, record=True, stop_after_finished=1,
+                         in_place_compaction=in_place)
+        pre = [r["preempted"] for r in res.records if r["preempted"]]
+        assert pre and len(pre[0]) == n1 and pre[0] == sorted(pre[0]) == list(range(n1))
