@@ -270,19 +270,18 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_sort_emit(const RankKey* __re
     __syncthreads();
     for (uint32_t size = 2; size <= P; size <<= 1) {
         for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            for (uint32_t i = threadIdx.x; i < P; i += SEL_THREADS) {
-                const uint32_t j = i ^ stride;
-                if (j > i) {
-                    const bool up = (i & size) == 0;
-                    const RankKey a = sk[i], b = sk[j];
-                    const bool swap = up ? KeyTraits<RankKey>::less(b, a) : KeyTraits<RankKey>::less(a, b);
-                    if (swap) {
-                        sk[i] = b;
-                        sk[j] = a;
-                        const uint32_t t = sv[i];
-                        sv[i] = sv[j];
-                        sv[j] = t;
-                    }
+            // one compare-exchange per thread slot (pairs enumerated directly, no idle half)
+            for (uint32_t t = threadIdx.x; t < (P >> 1); t += SEL_THREADS) {
+                const uint32_t i = 2 * stride * (t / stride) + (t % stride), j = i + stride;
+                const bool up = (i & size) == 0;
+                const RankKey a = sk[i], b = sk[j];
+                const bool swap = up ? KeyTraits<RankKey>::less(b, a) : KeyTraits<RankKey>::less(a, b);
+                if (swap) {
+                    sk[i] = b;
+                    sk[j] = a;
+                    const uint32_t tv = sv[i];
+                    sv[i] = sv[j];
+                    sv[j] = tv;
                 }
             }
             __syncthreads();
@@ -554,8 +553,9 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
     build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
     RS_LAUNCH_CHECK();
     const uint32_t k = min(n, (uint32_t)max_batch);
-    if (kv_budget < 0 && n > (uint32_t)SEL_CAP && k + SEL_CAP <= (uint32_t)SEL_SORT) {
-        // top-k select (see sel_hist): <= SEL_LEVELS histogram passes, most no-ops
+    if (kv_budget < 0 && n > (uint32_t)MS_SMALL_MAX && k + SEL_CAP <= (uint32_t)SEL_SORT) {
+        // top-k select (see sel_hist): <= SEL_LEVELS histogram passes, most no-ops. Queues
+        // of <= MS_SMALL_MAX rows take the one-kernel full sort below instead.
         static bool attr = false;
         const size_t smem = SEL_SORT * (sizeof(RankKey) + sizeof(uint32_t));
         if (!attr) {
