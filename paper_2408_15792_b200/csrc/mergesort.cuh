@@ -220,26 +220,17 @@ __global__ void __launch_bounds__(MS_THREADS) ms_block_sort(const K* __restrict_
     if (Count) block_add_count(inv, inv_out);
 }
 
-// One global merge pass: runs of width w -> runs of width 2w over npad keys.
-// Merge-path split of every output tile boundary of a pass, one warp each: every round
-// the 32 lanes probe 32 evenly spaced candidates and a ballot narrows the range 32x,
-// so a split over a run of 2^23 keys costs 5 dependent global loads instead of 23.
-constexpr int MS_PART_WARPS = 8;
-
+// One global merge pass: runs of width w -> runs of width 2w over npad keys. Each CTA
+// finds its tile's merge-path splits itself, one warp per split: every round the 32 lanes
+// probe 32 evenly spaced candidates and a ballot narrows the range 32x, so a split over a
+// run of 2^23 keys costs 5 dependent global loads instead of 23 (no separate partition
+// kernel, so a pass is one launch).
 template <typename K>
-__global__ void __launch_bounds__(MS_PART_WARPS * 32) ms_partition(const K* __restrict__ kin, uint32_t npad,
-                                                                   uint32_t w, uint32_t tiles,
-                                                                   int* __restrict__ split,
-                                                                   const int* __restrict__ skip) {
-    if (skip && *skip) return;
-    const uint32_t t = blockIdx.x * MS_PART_WARPS + (threadIdx.x >> 5);
+__device__ __forceinline__ int ms_split_warp(const K* __restrict__ kin, uint32_t npad, uint32_t w, uint32_t t,
+                                             uint32_t tiles) {
     const int lane = threadIdx.x & 31;
-    if (t > tiles) return;
     const uint32_t out = t * MS_TILE;
-    if (t == tiles || out % (2 * w) == 0) {  // run-pair boundary: nothing taken yet
-        if (lane == 0) split[t] = 0;
-        return;
-    }
+    if (t >= tiles || out % (2 * w) == 0) return 0;  // run-pair boundary: nothing taken yet
     const uint32_t base = out / (2 * w) * (2 * w);
     const int lenA = (int)min(w, npad - base);
     const int lenB = (int)min(w, npad - base - (uint32_t)lenA);
@@ -266,7 +257,7 @@ __global__ void __launch_bounds__(MS_PART_WARPS * 32) ms_partition(const K* __re
     const int p = lo + lane;
     const bool pred = p < hi && KeyTraits<K>::less(b[diag - 1 - p], a[p]);
     const unsigned m = __ballot_sync(0xffffffffu, pred);
-    if (lane == 0) split[t] = m ? lo + __ffs(m) - 1 : hi;
+    return m ? lo + __ffs(m) - 1 : hi;
 }
 
 template <typename K, bool HasVal, bool Count>
@@ -276,10 +267,15 @@ __global__ void __launch_bounds__(MS_THREADS) ms_merge_pass(const K* __restrict_
                                                             uint32_t* __restrict__ vout,
                                                             uint32_t npad, uint32_t w,
                                                             unsigned long long* inv_out,
-                                                            const int* __restrict__ splits,
                                                             const int* __restrict__ skip) {
     if (skip && *skip) return;
     __shared__ MsSmem<K, HasVal> sm;
+    __shared__ int s_split[2];
+    if (threadIdx.x < 64) {  // warp 0: this tile's start split, warp 1: the next tile's
+        const int v = ms_split_warp<K>(kin, npad, w, blockIdx.x + (threadIdx.x >> 5), gridDim.x);
+        if ((threadIdx.x & 31) == 0) s_split[threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
     const uint32_t out0 = blockIdx.x * MS_TILE;
     const uint32_t base = out0 / (2 * w) * (2 * w);
     const int lenA = (int)min(w, npad - base);
@@ -289,8 +285,8 @@ __global__ void __launch_bounds__(MS_THREADS) ms_merge_pass(const K* __restrict_
     const int d0 = (int)(out0 - base);
     const int d1 = d0 + MS_TILE;
     // the tile's end split: the next tile's start, or the whole left run at a run end
-    const int a0 = splits[blockIdx.x];
-    const int a1 = (d1 == lenA + lenB) ? lenA : splits[blockIdx.x + 1];
+    const int a0 = s_split[0];
+    const int a1 = (d1 == lenA + lenB) ? lenA : s_split[1];
     const int b0 = d0 - a0, b1 = d1 - a1;
     const int na = a1 - a0, nb = b1 - b0;
     for (int k = threadIdx.x; k < MS_TILE; k += MS_THREADS) {
@@ -375,7 +371,8 @@ static inline uint32_t ms_padded(uint64_t n) {
     return (uint32_t)((n + MS_TILE - 1) / MS_TILE * MS_TILE);
 }
 
-// ints of scratch merge_sort needs for the per-pass tile splits
+// ints of scratch reserved for per-pass tile splits (the passes now find their own splits;
+// kept so callers' workspace layouts stay valid)
 static inline uint32_t ms_splits(uint64_t n) { return (uint32_t)((n + MS_TILE - 1) / MS_TILE) + 2; }
 
 // Sort n keys (+ optional u32 payload). k0/k1 and v0/v1 are ping-pong buffers of
@@ -418,10 +415,7 @@ int merge_sort(const K* keys_in, const uint32_t* vals_in, uint32_t n, K* k0, K* 
     uint32_t* vo = v1;
     for (uint32_t w = MS_TILE; w < npad; w <<= 1) {
         const int* sk = (skip && w >= skip_w) ? skip : nullptr;
-        ms_partition<K><<<(tiles + MS_PART_WARPS) / MS_PART_WARPS, MS_PART_WARPS * 32, 0, st>>>(ki, npad, w, tiles,
-                                                                                             splits, sk);
-        RS_LAUNCH_CHECK();
-        ms_merge_pass<K, HasVal, Count><<<tiles, MS_THREADS, 0, st>>>(ki, vi, ko, vo, npad, w, inv, splits, sk);
+        ms_merge_pass<K, HasVal, Count><<<tiles, MS_THREADS, 0, st>>>(ki, vi, ko, vo, npad, w, inv, sk);
         RS_LAUNCH_CHECK();
         K* t = ki;
         ki = ko;
