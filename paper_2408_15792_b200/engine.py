@@ -149,10 +149,14 @@ class DeviceEngine:
         self.dem_out = torch.empty(cap, dtype=i64, device=d)
         self.pre_out = torch.empty(cap, dtype=i64, device=d)
         self.fin_out = torch.empty(max(sched.max_batch, 1), dtype=i64, device=d)
-        self.counts = torch.zeros(4, dtype=i32, device=d)
-        self.out = torch.zeros(6, dtype=i64, device=d)
-        self.out_host = torch.zeros(6, dtype=i64).pin_memory()
-        self.cnt_host = torch.zeros(4, dtype=i32).pin_memory()
+        # one 64-byte status block per step: out int64[6] (execute) | counts int32[4] (rank step),
+        # read back with a single D2H copy
+        self.stat = torch.zeros(8, dtype=i64, device=d)
+        self.out = self.stat[:6]
+        self.counts = self.stat[6:].view(i32)
+        self.stat_host = torch.zeros(8, dtype=i64).pin_memory()
+        self.out_host = self.stat_host[:6]
+        self.cnt_host = self.stat_host[6:].view(i32)
         self.adm_host = torch.zeros(cap, dtype=i32).pin_memory()
         self.adm_dev = torch.zeros(cap, dtype=i32, device=d)
         dt = cost.decode_table
@@ -205,6 +209,7 @@ class DeviceEngine:
         ws_n = 0
         ws = wn = None
         now, nxt, n_alive, step, n_finished = 0, 0, 0, 0, 0
+        dev_now = None  # the device copy of the clock (out[0]) when known to equal `now`
         tot_prefill = tot_decode = tot_pred = 0
         dropped_all: list[int] = []
         records = []
@@ -242,8 +247,10 @@ class DeviceEngine:
             check(rank_step(soa_refs[cur], sched.max_batch, budget, sched.starvation_threshold, sched.priority_quantum,
                             int(self.length_calibrated), int(sched.preemption), run_p, prom_p, dem_p, cnt_p, ws, wn,
                             st), "rs_rank_step")
-            out_np[0] = now
-            self.out.copy_(self.out_host, non_blocking=True)
+            if now != dev_now:  # the clock moved on the host (idle jump / first step)
+                out_np[0] = now
+                self.out[:1].copy_(self.out_host[:1], non_blocking=True)
+                dev_now = now
             qs[cur].n = n_alive
             if nsets == 1:
                 check(execute(q_refs[0], tr_ref, cost_ref, run_p, cnt_p, step, predictor_ns, out_p, pre_p, fin_p, st),
@@ -252,12 +259,12 @@ class DeviceEngine:
                 check(execute_ex(q_refs[cur], q_refs[1 - cur], tr_ref, cost_ref, run_p, cnt_p, step, predictor_ns,
                                  out_p, pre_p, fin_p, scratch_p, st), "rs_engine_execute_ex")
                 cur = 1 - cur
-            self.out_host.copy_(self.out, non_blocking=True)
-            self.cnt_host.copy_(self.counts, non_blocking=True)
+            self.stat_host.copy_(self.stat, non_blocking=True)
             stream.synchronize()
             if cnt_np[3]:
                 raise ValueError("ranking policy: NaN effective score")
             now, iter_ns, prefill_ns, n_alive = int(out_np[0]), int(out_np[1]), int(out_np[2]), int(out_np[3])
+            dev_now = now
             n_finished += int(out_np[5])
             tot_prefill += prefill_ns
             tot_pred += predictor_ns
