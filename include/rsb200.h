@@ -227,6 +227,33 @@ size_t rs_ranker_workspace_size(const rs_ranker_config* cfg, int32_t B, int32_t 
 int rs_ranker_forward(const rs_ranker_config* cfg, const void* params_dev, const int32_t* ids_dev,
                       const int32_t* last_pos_dev, int32_t B, int32_t S, float* g_dev, float* score_dev,
                       void* ws_dev, size_t ws_bytes, void* stream);
+/* Same forward, also writing feat_dev f32[B, d] = LN_f(h[last_pos]) (may be NULL): the
+ * input of the classification head (§8f #4). */
+int rs_ranker_forward_ex(const rs_ranker_config* cfg, const void* params_dev, const int32_t* ids_dev,
+                         const int32_t* last_pos_dev, int32_t B, int32_t S, float* g_dev, float* score_dev,
+                         float* feat_dev, void* ws_dev, size_t ws_bytes, void* stream);
+
+/* ---- §8f #4: bucketed-classification baseline on the same backbone ------------------
+ * The reference's ClassifierScorer / train_classifier (predictors.py:262-300, :409-479):
+ * logits = feat W^T + b over C length buckets, softmax cross-entropy. Here the features
+ * are the OPT backbone's LN_f(h_last) instead of the 24 hashed prompt features.
+ * rs_cls_logits: feat f32[B,d], W f32[C,d], b f32[C] -> logits f32[B,C].
+ * rs_cls_ce: per-prompt nll f32[B] and dlogits = softmax - onehot(label) f32[B,C]
+ *   (labels int32[B] in [0, C); out of range -> RS_ERR_INVALID via bad_dev != 0).
+ * rs_ranker_grad_cls: like rs_ranker_grad, with the CE stage in place of ListMLE:
+ *   accumulates d(sum of nll)/d params into grad (the backbone, rs_ranker_layout; the
+ *   score head gets none) and into cls_grad f32[C*d + C] (dW then db); loss_out f32[n]
+ *   per-prompt nll; prompts_per_micro prompts per micro-batch. Scale by 1/n in Adam. */
+int rs_cls_logits(const float* feat_dev, const float* w_dev, const float* b_dev, int32_t B, int32_t d, int32_t C,
+                  float* logits_dev, void* stream);
+int rs_cls_ce(const float* logits_dev, const int32_t* labels_dev, int32_t B, int32_t C, float* loss_dev,
+              float* dlogits_dev, int32_t* bad_dev, void* stream);
+size_t rs_ranker_grad_cls_workspace_size(const rs_ranker_config* cfg, int32_t prompts_per_micro, int32_t S,
+                                         int32_t n_classes);
+int rs_ranker_grad_cls(const rs_ranker_config* cfg, const void* params_dev, float* grad_dev, const int32_t* ids_dev,
+                       const int32_t* last_pos_dev, const int32_t* labels_dev, int32_t n_prompts, int32_t S,
+                       int32_t n_classes, const float* cls_w_dev, const float* cls_b_dev, float* cls_grad_dev,
+                       int32_t prompts_per_micro, float* loss_dev, void* ws_dev, size_t ws_bytes, void* stream);
 
 /* ---- A10/K7/K8: training (ListMLE over whole lists, predictors.py:347-406) ----------
  * Accumulates into grad_dev (fp32, rs_ranker_layout order and length) the gradient of

@@ -88,6 +88,13 @@ SIGNATURES = {
     "rs_ranker_workspace_size": (c_sz, [ctypes.POINTER(RankerConfig), c_i32, c_i32]),
     "rs_ranker_forward": (ctypes.c_int, [ctypes.POINTER(RankerConfig), c_vp, c_vp, c_vp, c_i32, c_i32, c_vp,
                                          c_vp, c_vp, c_sz, c_vp]),
+    "rs_ranker_forward_ex": (ctypes.c_int, [ctypes.POINTER(RankerConfig), c_vp, c_vp, c_vp, c_i32, c_i32, c_vp,
+                                            c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "rs_cls_logits": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp]),
+    "rs_cls_ce": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
+    "rs_ranker_grad_cls_workspace_size": (c_sz, [ctypes.POINTER(RankerConfig), c_i32, c_i32, c_i32]),
+    "rs_ranker_grad_cls": (ctypes.c_int, [ctypes.POINTER(RankerConfig), c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32,
+                                          c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_sz, c_vp]),
     "rs_gemm_bf16": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "rs_attention_fwd": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "rs_attention_fwd_f16v": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),

@@ -182,7 +182,7 @@ template <int VPL>
 __global__ void head_kernel(const float* __restrict__ h, const int32_t* __restrict__ last, int B, int S,
                             const __nv_bfloat16* __restrict__ lw, const __nv_bfloat16* __restrict__ lb,
                             const __nv_bfloat16* __restrict__ hw, const __nv_bfloat16* __restrict__ hb,
-                            float* __restrict__ g, float* __restrict__ score) {
+                            float* __restrict__ g, float* __restrict__ score, float* __restrict__ feat) {
     constexpr int d = VPL * 256;
     const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -201,6 +201,7 @@ __global__ void head_kernel(const float* __restrict__ h, const int32_t* __restri
         for (int e = 0; e < 8; ++e) {
             const float xn = (v[k * 8 + e] - mean) * rstd * __bfloat162float(lw[base + e]) + __bfloat162float(lb[base + e]);
             acc = fmaf(xn, __bfloat162float(hw[base + e]), acc);
+            if (feat) feat[(size_t)p * d + base + e] = xn;  // LNf(h_last): the classifier head's input
         }
     }
     acc = warp_sum(acc);
@@ -430,16 +431,16 @@ static int launch_ln(const float* x, const __nv_bfloat16* w, const __nv_bfloat16
 }
 
 static int launch_head(const float* h, const int32_t* last, int B, int S, const __nv_bfloat16* P,
-                       const RankerOffsets& o, int d, float* g, float* score, cudaStream_t st) {
+                       const RankerOffsets& o, int d, float* g, float* score, cudaStream_t st, float* feat = nullptr) {
     const int wpb = 8;
     const int grid = (B + wpb - 1) / wpb;
     const __nv_bfloat16 *lw = P + o.lnf_w, *lb = P + o.lnf_b, *hw = P + o.head_w, *hb = P + o.head_b;
     switch (d / 256) {
-        case 1: head_kernel<1><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score); break;
-        case 2: head_kernel<2><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score); break;
-        case 3: head_kernel<3><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score); break;
-        case 4: head_kernel<4><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score); break;
-        case 8: head_kernel<8><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score); break;
+        case 1: head_kernel<1><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score, feat); break;
+        case 2: head_kernel<2><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score, feat); break;
+        case 3: head_kernel<3><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score, feat); break;
+        case 4: head_kernel<4><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score, feat); break;
+        case 8: head_kernel<8><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, lw, lb, hw, hb, g, score, feat); break;
         default: set_error("head: unsupported d=%d", d); return RS_ERR_INVALID;
     }
     RS_LAUNCH_CHECK();
@@ -482,6 +483,12 @@ extern "C" size_t rs_ranker_workspace_size(const rs_ranker_config* cfg, int32_t 
 extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params, const int32_t* ids,
                                  const int32_t* last_pos, int32_t B, int32_t S, float* g, float* score,
                                  void* ws, size_t ws_bytes, void* stream) {
+    return rs_ranker_forward_ex(cfg, params, ids, last_pos, B, S, g, score, nullptr, ws, ws_bytes, stream);
+}
+
+extern "C" int rs_ranker_forward_ex(const rs_ranker_config* cfg, const void* params, const int32_t* ids,
+                                    const int32_t* last_pos, int32_t B, int32_t S, float* g, float* score,
+                                    float* feat, void* ws, size_t ws_bytes, void* stream) {
     cudaStream_t st = as_stream(stream);
     RS_TRY(check_cfg(cfg));
     RS_CHECK_ARG(B > 0 && S > 0 && S <= cfg->max_pos, "ranker: need B > 0 and 0 < S <= max_pos");
@@ -548,7 +555,8 @@ extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params
             RS_TRY(gemm_bf16(w.x, L + o.fc1_w, L + o.fc1_b, nullptr, w.ffn, mp, F, d, cfg->activation == 0 ? 1 : 3, st));
             RS_TRY(gemm_bf16(w.ffn, L + o.fc2_w, L + o.fc2_b, w.h, w.h, mp, d, F, 2, st));
         }
-        RS_TRY(launch_head(w.h_last, nullptr, bc, 1, P, o, d, g + b0, score ? score + b0 : nullptr, st));
+        RS_TRY(launch_head(w.h_last, nullptr, bc, 1, P, o, d, g + b0, score ? score + b0 : nullptr, st,
+                           feat ? feat + b0 * d : nullptr));
     }
     return RS_OK;
 }
@@ -568,9 +576,9 @@ int ranker_ln(const float* x, const void* w, const void* b, void* y, int rows, i
                      static_cast<__nv_bfloat16*>(y), rows, d, st);
 }
 int ranker_head(const float* h, const int32_t* last, int B, int S, const void* P, const rs_ranker_config* cfg, float* g,
-                float* score, cudaStream_t st) {
+                float* score, cudaStream_t st, float* feat) {
     const RankerOffsets o = ranker_offsets(*cfg);
-    return launch_head(h, last, B, S, static_cast<const __nv_bfloat16*>(P), o, cfg->d_model, g, score, st);
+    return launch_head(h, last, B, S, static_cast<const __nv_bfloat16*>(P), o, cfg->d_model, g, score, st, feat);
 }
 // which: 0 tok, 1 pos, 2 lnf_w, 3 lnf_b, 4 head_w, 5 head_b, then 6 + per-layer index
 int64_t ranker_offset(const rs_ranker_config* cfg, int which, int layer) {

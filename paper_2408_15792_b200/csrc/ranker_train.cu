@@ -29,7 +29,7 @@ int ranker_embed(const int32_t* ids, const void* P, int64_t off_tok, int64_t off
                  int d, int vocab, int mp, cudaStream_t st);
 int ranker_ln(const float* x, const void* w, const void* b, void* y, int rows, int d, cudaStream_t st);
 int ranker_head(const float* h, const int32_t* last, int B, int S, const void* P, const rs_ranker_config* cfg, float* g,
-                float* score, cudaStream_t st);
+                float* score, cudaStream_t st, float* feat = nullptr);
 int64_t ranker_offset(const rs_ranker_config* cfg, int which, int layer);
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y, int64_t n) {
@@ -48,6 +48,8 @@ struct TrainWs {
     __nv_bfloat16 *x1[64], *qkv[64], *att[64], *x2[64], *f[64];
     // backward scratch
     float *dh, *dx, *wpart, *rpart, *g, *dg;
+    float *feat, *logits, *dlogits, *dfeat;  // classification head (rs_ranker_grad_cls)
+    int32_t* bad;
     __nv_bfloat16 *dh16, *da, *dqkv, *df;
     void* ews;
     size_t ews_bytes;
@@ -63,7 +65,7 @@ static int wgrad_splits(int M, int N, int K) {
 }
 
 template <typename A>
-static void train_layout(A& a, const rs_ranker_config& c, int64_t Tp, int P, TrainWs* w) {
+static void train_layout(A& a, const rs_ranker_config& c, int64_t Tp, int P, TrainWs* w, int n_classes = 0) {
     const int L = c.n_layers;
     const int64_t d = c.d_model, F = c.d_ffn;
     TrainWs t{};
@@ -84,6 +86,13 @@ static void train_layout(A& a, const rs_ranker_config& c, int64_t Tp, int P, Tra
     t.rpart = a.template take<float>(nrb * 2 * (F > 3 * d ? F : 3 * d) + (int64_t)(P + 1) * (3 * d + 1));
     t.g = a.template take<float>(P);
     t.dg = a.template take<float>(P);
+    if (n_classes > 0) {
+        t.feat = a.template take<float>((int64_t)P * d);
+        t.dfeat = a.template take<float>((int64_t)P * d);
+        t.logits = a.template take<float>((int64_t)P * n_classes);
+        t.dlogits = a.template take<float>((int64_t)P * n_classes);
+        t.bad = a.template take<int32_t>(4);
+    }
     t.dh16 = a.template take<__nv_bfloat16>(Tp * d);
     t.da = a.template take<__nv_bfloat16>(Tp * d);
     t.dqkv = a.template take<__nv_bfloat16>(Tp * 3 * d);
@@ -100,6 +109,87 @@ struct TrSizer {
 
 int listmle_lengths_launch(const float* g, const int32_t* lengths, int n_lists, int L, int width, float* loss,
                            float* dg, cudaStream_t st);
+int cls_logits_launch(const float* feat, const float* W, const float* b, int B, int d, int C, float* logits,
+                      cudaStream_t st);
+int cls_ce_launch(const float* logits, const int32_t* labels, int B, int C, float* loss, float* dlogits, int32_t* bad,
+                  cudaStream_t st);
+int cls_head_backward(const float* feat, const float* W, const float* dlogits, int B, int d, int C, float* dW,
+                      float* db, float* dfeat, cudaStream_t st);
+
+
+// Forward of one micro-batch keeping the activations the backward needs.
+static int train_forward(const rs_ranker_config* cfg, const __nv_bfloat16* P16, const int32_t* mids, int P, int S,
+                         int n_tok, int64_t Tp, TrainWs& w, cudaStream_t st) {
+    const int L = cfg->n_layers, d = cfg->d_model, F = cfg->d_ffn, H = cfg->n_heads;
+    auto off = [&](int which, int layer) { return ranker_offset(cfg, which, layer); };
+    // ---- forward, keeping activations ----
+    RS_TRY(ranker_embed(mids, P16, off(OFF_TOK, 0), off(OFF_POS, 0), w.h_in[0], n_tok, S, d, cfg->vocab, (int)Tp,
+                        st));
+    if (Tp > n_tok) {
+        for (int l = 0; l < L; ++l)
+            RS_CUDA(cudaMemsetAsync(w.att[l] + (size_t)n_tok * d, 0, (size_t)(Tp - n_tok) * d * 2, st));
+    }
+    for (int l = 0; l < L; ++l) {
+        RS_TRY(ranker_ln(w.h_in[l], P16 + off(OFF_LN1_W, l), P16 + off(OFF_LN1_B, l), w.x1[l], (int)Tp, d, st));
+        RS_TRY(gemm_bf16(w.x1[l], P16 + off(OFF_QKV_W, l), P16 + off(OFF_QKV_B, l), nullptr, w.qkv[l], (int)Tp,
+                         3 * d, d, 0, st));
+        RS_TRY(attention_fwd(w.qkv[l], w.att[l], P, S, H, st));
+        RS_TRY(gemm_bf16(w.att[l], P16 + off(OFF_OUT_W, l), P16 + off(OFF_OUT_B, l), w.h_in[l], w.h_mid[l],
+                         (int)Tp, d, d, 2, st));
+        RS_TRY(ranker_ln(w.h_mid[l], P16 + off(OFF_LN2_W, l), P16 + off(OFF_LN2_B, l), w.x2[l], (int)Tp, d, st));
+        RS_TRY(gemm_bf16(w.x2[l], P16 + off(OFF_FC1_W, l), P16 + off(OFF_FC1_B, l), nullptr, w.f[l], (int)Tp, F, d,
+                         cfg->activation == 0 ? 1 : 3, st));
+        RS_TRY(gemm_bf16(w.f[l], P16 + off(OFF_FC2_W, l), P16 + off(OFF_FC2_B, l), w.h_mid[l], w.h_in[l + 1],
+                         (int)Tp, d, F, 2, st));
+    }
+    return RS_OK;
+}
+
+// Backward of one micro-batch from w.dh (the head's gradient already in the last-token
+// rows, zero elsewhere) through the layers and the embeddings, accumulating into grad.
+static int train_backward(const rs_ranker_config* cfg, const __nv_bfloat16* P16, float* grad, const int32_t* mids,
+                          int P, int S, int n_tok, int64_t Tp, TrainWs& w, cudaStream_t st) {
+    const int L = cfg->n_layers, d = cfg->d_model, F = cfg->d_ffn, H = cfg->n_heads;
+    auto off = [&](int which, int layer) { return ranker_offset(cfg, which, layer); };
+    f32_to_bf16_kernel<<<1184, 256, 0, st>>>(w.dh, w.dh16, (int64_t)Tp * d);
+    RS_LAUNCH_CHECK();
+    const int T = (int)Tp;
+    for (int l = L - 1; l >= 0; --l) {
+        int sp;
+        // FC2: h_out = h_mid + f W2^T + b2
+        sp = wgrad_splits(d, F, T);
+        RS_TRY(gemm_bf16_ex(w.dh16, w.f[l], nullptr, nullptr, w.wpart, d, F, T, 6, 1, 1, sp, st));
+        RS_TRY(slices_add(w.wpart, sp, (int64_t)d * F, grad + off(OFF_FC2_W, l), st));
+        RS_TRY(colsum_add(w.dh, false, n_tok, d, w.rpart, grad + off(OFF_FC2_B, l), st));
+        RS_TRY(gemm_bf16_ex(w.dh16, P16 + off(OFF_FC2_W, l), nullptr, w.f[l], w.df, T, F, d, 5, 0, 1, 1, st));
+        // FC1: f = relu(x2 W1^T + b1)
+        sp = wgrad_splits(F, d, T);
+        RS_TRY(gemm_bf16_ex(w.df, w.x2[l], nullptr, nullptr, w.wpart, F, d, T, 6, 1, 1, sp, st));
+        RS_TRY(slices_add(w.wpart, sp, (int64_t)F * d, grad + off(OFF_FC1_W, l), st));
+        RS_TRY(colsum_add(w.df, true, n_tok, F, w.rpart, grad + off(OFF_FC1_B, l), st));
+        RS_TRY(gemm_bf16_ex(w.df, P16 + off(OFF_FC1_W, l), nullptr, nullptr, w.dx, T, d, F, 4, 0, 1, 1, st));
+        RS_TRY(ln_backward(w.dx, w.h_mid[l], P16 + off(OFF_LN2_W, l), w.dh, w.dh16, w.rpart, n_tok, d,
+                           grad + off(OFF_LN2_W, l), nullptr, st));
+        // out-proj: h_mid = h_in + a Wo^T + bo
+        sp = wgrad_splits(d, d, T);
+        RS_TRY(gemm_bf16_ex(w.dh16, w.att[l], nullptr, nullptr, w.wpart, d, d, T, 6, 1, 1, sp, st));
+        RS_TRY(slices_add(w.wpart, sp, (int64_t)d * d, grad + off(OFF_OUT_W, l), st));
+        RS_TRY(colsum_add(w.dh, false, n_tok, d, w.rpart, grad + off(OFF_OUT_B, l), st));
+        RS_TRY(gemm_bf16_ex(w.dh16, P16 + off(OFF_OUT_W, l), nullptr, nullptr, w.da, T, d, d, 0, 0, 1, 1, st));
+        RS_TRY(attention_bwd(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, st));
+        // QKV: qkv = x1 Wqkv^T + b
+        sp = wgrad_splits(3 * d, d, T);
+        RS_TRY(gemm_bf16_ex(w.dqkv, w.x1[l], nullptr, nullptr, w.wpart, 3 * d, d, T, 6, 1, 1, sp, st));
+        RS_TRY(slices_add(w.wpart, sp, (int64_t)3 * d * d, grad + off(OFF_QKV_W, l), st));
+        RS_TRY(colsum_add(w.dqkv, true, n_tok, 3 * d, w.rpart, grad + off(OFF_QKV_B, l), st));
+        RS_TRY(gemm_bf16_ex(w.dqkv, P16 + off(OFF_QKV_W, l), nullptr, nullptr, w.dx, T, d, 3 * d, 4, 0, 1, 1, st));
+        RS_TRY(ln_backward(w.dx, w.h_in[l], P16 + off(OFF_LN1_W, l), w.dh, w.dh16, w.rpart, n_tok, d,
+                           grad + off(OFF_LN1_W, l), nullptr, st));
+    }
+    RS_TRY(embed_backward(mids, P, S, cfg->vocab, w.dh, d, grad + off(OFF_TOK, 0), grad + off(OFF_POS, 0), w.ews,
+                          w.ews_bytes, st));
+    return RS_OK;
+}
 
 }  // namespace rs
 
@@ -129,7 +219,7 @@ extern "C" int rs_ranker_grad(const rs_ranker_config* cfg, const void* params, f
         set_error("rs_ranker_grad: workspace too small");
         return RS_ERR_WORKSPACE;
     }
-    const int L = cfg->n_layers, d = cfg->d_model, F = cfg->d_ffn, H = cfg->n_heads;
+    const int L = cfg->n_layers, d = cfg->d_model;
     const __nv_bfloat16* P16 = static_cast<const __nv_bfloat16*>(params);
     auto off = [&](int which, int layer) { return ranker_offset(cfg, which, layer); };
     for (int l0 = 0; l0 < n_lists; l0 += lists_per_micro) {
@@ -147,26 +237,7 @@ extern "C" int rs_ranker_grad(const rs_ranker_config* cfg, const void* params, f
         const int32_t* mids = ids + (int64_t)l0 * list_len * S;
         const int32_t* mlen = lengths + (int64_t)l0 * list_len;
         const int32_t* mlast = last_pos ? last_pos + (int64_t)l0 * list_len : nullptr;
-        // ---- forward, keeping activations ----
-        RS_TRY(ranker_embed(mids, P16, off(OFF_TOK, 0), off(OFF_POS, 0), w.h_in[0], n_tok, S, d, cfg->vocab, (int)Tp,
-                            st));
-        if (Tp > n_tok) {
-            for (int l = 0; l < L; ++l)
-                RS_CUDA(cudaMemsetAsync(w.att[l] + (size_t)n_tok * d, 0, (size_t)(Tp - n_tok) * d * 2, st));
-        }
-        for (int l = 0; l < L; ++l) {
-            RS_TRY(ranker_ln(w.h_in[l], P16 + off(OFF_LN1_W, l), P16 + off(OFF_LN1_B, l), w.x1[l], (int)Tp, d, st));
-            RS_TRY(gemm_bf16(w.x1[l], P16 + off(OFF_QKV_W, l), P16 + off(OFF_QKV_B, l), nullptr, w.qkv[l], (int)Tp,
-                             3 * d, d, 0, st));
-            RS_TRY(attention_fwd(w.qkv[l], w.att[l], P, S, H, st));
-            RS_TRY(gemm_bf16(w.att[l], P16 + off(OFF_OUT_W, l), P16 + off(OFF_OUT_B, l), w.h_in[l], w.h_mid[l],
-                             (int)Tp, d, d, 2, st));
-            RS_TRY(ranker_ln(w.h_mid[l], P16 + off(OFF_LN2_W, l), P16 + off(OFF_LN2_B, l), w.x2[l], (int)Tp, d, st));
-            RS_TRY(gemm_bf16(w.x2[l], P16 + off(OFF_FC1_W, l), P16 + off(OFF_FC1_B, l), nullptr, w.f[l], (int)Tp, F, d,
-                             cfg->activation == 0 ? 1 : 3, st));
-            RS_TRY(gemm_bf16(w.f[l], P16 + off(OFF_FC2_W, l), P16 + off(OFF_FC2_B, l), w.h_mid[l], w.h_in[l + 1],
-                             (int)Tp, d, F, 2, st));
-        }
+        RS_TRY(train_forward(cfg, P16, mids, P, S, n_tok, Tp, w, st));
         RS_TRY(ranker_head(w.h_in[L], mlast, P, S, P16, cfg, w.g, nullptr, st));
         // ---- ListMLE (K6): per-list loss / n and dg = grad / n ----
         RS_TRY(listmle_lengths_launch(w.g, mlen, ml, list_len, bucket_width, loss_out + l0, w.dg, st));
@@ -178,43 +249,68 @@ extern "C" int rs_ranker_grad(const rs_ranker_config* cfg, const void* params, f
         RS_TRY(head_backward(w.h_in[L], mlast, P, S, P16 + off(OFF_LNF_W, 0), P16 + off(OFF_LNF_B, 0),
                              P16 + off(OFF_HEAD_W, 0), w.dg, w.dh, w.rpart, d, grad + off(OFF_HEAD_W, 0),
                              grad + off(OFF_LNF_W, 0), grad + off(OFF_HEAD_B, 0), st));
-        f32_to_bf16_kernel<<<1184, 256, 0, st>>>(w.dh, w.dh16, (int64_t)Tp * d);
-        RS_LAUNCH_CHECK();
-        const int T = (int)Tp;
-        for (int l = L - 1; l >= 0; --l) {
-            int sp;
-            // FC2: h_out = h_mid + f W2^T + b2
-            sp = wgrad_splits(d, F, T);
-            RS_TRY(gemm_bf16_ex(w.dh16, w.f[l], nullptr, nullptr, w.wpart, d, F, T, 6, 1, 1, sp, st));
-            RS_TRY(slices_add(w.wpart, sp, (int64_t)d * F, grad + off(OFF_FC2_W, l), st));
-            RS_TRY(colsum_add(w.dh, false, n_tok, d, w.rpart, grad + off(OFF_FC2_B, l), st));
-            RS_TRY(gemm_bf16_ex(w.dh16, P16 + off(OFF_FC2_W, l), nullptr, w.f[l], w.df, T, F, d, 5, 0, 1, 1, st));
-            // FC1: f = relu(x2 W1^T + b1)
-            sp = wgrad_splits(F, d, T);
-            RS_TRY(gemm_bf16_ex(w.df, w.x2[l], nullptr, nullptr, w.wpart, F, d, T, 6, 1, 1, sp, st));
-            RS_TRY(slices_add(w.wpart, sp, (int64_t)F * d, grad + off(OFF_FC1_W, l), st));
-            RS_TRY(colsum_add(w.df, true, n_tok, F, w.rpart, grad + off(OFF_FC1_B, l), st));
-            RS_TRY(gemm_bf16_ex(w.df, P16 + off(OFF_FC1_W, l), nullptr, nullptr, w.dx, T, d, F, 4, 0, 1, 1, st));
-            RS_TRY(ln_backward(w.dx, w.h_mid[l], P16 + off(OFF_LN2_W, l), w.dh, w.dh16, w.rpart, n_tok, d,
-                               grad + off(OFF_LN2_W, l), nullptr, st));
-            // out-proj: h_mid = h_in + a Wo^T + bo
-            sp = wgrad_splits(d, d, T);
-            RS_TRY(gemm_bf16_ex(w.dh16, w.att[l], nullptr, nullptr, w.wpart, d, d, T, 6, 1, 1, sp, st));
-            RS_TRY(slices_add(w.wpart, sp, (int64_t)d * d, grad + off(OFF_OUT_W, l), st));
-            RS_TRY(colsum_add(w.dh, false, n_tok, d, w.rpart, grad + off(OFF_OUT_B, l), st));
-            RS_TRY(gemm_bf16_ex(w.dh16, P16 + off(OFF_OUT_W, l), nullptr, nullptr, w.da, T, d, d, 0, 0, 1, 1, st));
-            RS_TRY(attention_bwd(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, st));
-            // QKV: qkv = x1 Wqkv^T + b
-            sp = wgrad_splits(3 * d, d, T);
-            RS_TRY(gemm_bf16_ex(w.dqkv, w.x1[l], nullptr, nullptr, w.wpart, 3 * d, d, T, 6, 1, 1, sp, st));
-            RS_TRY(slices_add(w.wpart, sp, (int64_t)3 * d * d, grad + off(OFF_QKV_W, l), st));
-            RS_TRY(colsum_add(w.dqkv, true, n_tok, 3 * d, w.rpart, grad + off(OFF_QKV_B, l), st));
-            RS_TRY(gemm_bf16_ex(w.dqkv, P16 + off(OFF_QKV_W, l), nullptr, nullptr, w.dx, T, d, 3 * d, 4, 0, 1, 1, st));
-            RS_TRY(ln_backward(w.dx, w.h_in[l], P16 + off(OFF_LN1_W, l), w.dh, w.dh16, w.rpart, n_tok, d,
-                               grad + off(OFF_LN1_W, l), nullptr, st));
+        RS_TRY(train_backward(cfg, P16, grad, mids, P, S, n_tok, Tp, w, st));
+    }
+    return RS_OK;
+}
+
+// §8f #4: the same pass with the bucketed-classification head (classifier.cu) and the
+// softmax cross-entropy of train_classifier (predictors.py:445-453) in place of the score
+// head and ListMLE: micro-batches of prompts, LN_f features -> logits -> nll, dlogits ->
+// head gradients + d LN_f output -> the shared backward.
+extern "C" size_t rs_ranker_grad_cls_workspace_size(const rs_ranker_config* cfg, int32_t prompts_per_micro, int32_t S,
+                                                    int32_t n_classes) {
+    if (!cfg || prompts_per_micro <= 0 || S <= 0 || n_classes <= 0 || cfg->n_layers > 63) return 0;
+    const int P = prompts_per_micro;
+    const int64_t Tp = ((int64_t)P * S + 255) / 256 * 256;
+    TrSizer s;
+    train_layout(s, *cfg, Tp, P, nullptr, n_classes);
+    return s.s.used + 4096;
+}
+
+extern "C" int rs_ranker_grad_cls(const rs_ranker_config* cfg, const void* params, float* grad, const int32_t* ids,
+                                  const int32_t* last_pos, const int32_t* labels, int32_t n_prompts, int32_t S,
+                                  int32_t n_classes, const float* cls_w, const float* cls_b, float* cls_grad,
+                                  int32_t prompts_per_micro, float* loss_out, void* ws, size_t ws_bytes,
+                                  void* stream) {
+    cudaStream_t st = as_stream(stream);
+    RS_CHECK_ARG(cfg && params && grad && ids && labels && cls_w && cls_b && cls_grad && loss_out,
+                 "rs_ranker_grad_cls: NULL argument");
+    RS_CHECK_ARG(n_prompts > 0 && S >= 1 && S <= 128, "rs_ranker_grad_cls: need S <= 128 (got %d)", S);
+    RS_CHECK_ARG(n_classes >= 2 && prompts_per_micro >= 1, "rs_ranker_grad_cls: need >= 2 classes");
+    RS_CHECK_ARG(cfg->n_layers <= 63 && cfg->d_model == cfg->n_heads * 64, "rs_ranker_grad_cls: bad config");
+    if (ws_bytes < rs_ranker_grad_cls_workspace_size(cfg, prompts_per_micro, S, n_classes)) {
+        set_error("rs_ranker_grad_cls: workspace too small");
+        return RS_ERR_WORKSPACE;
+    }
+    const int L = cfg->n_layers, d = cfg->d_model, C = n_classes;
+    const __nv_bfloat16* P16 = static_cast<const __nv_bfloat16*>(params);
+    auto off = [&](int which, int layer) { return ranker_offset(cfg, which, layer); };
+    for (int p0 = 0; p0 < n_prompts; p0 += prompts_per_micro) {
+        const int P = (n_prompts - p0) < prompts_per_micro ? (n_prompts - p0) : prompts_per_micro;
+        const int n_tok = P * S;
+        const int64_t Tp = ((int64_t)n_tok + 255) / 256 * 256;
+        Arena ar(ws, ws_bytes);
+        TrainWs w;
+        {
+            const int64_t Tm = ((int64_t)prompts_per_micro * S + 255) / 256 * 256;
+            train_layout(ar, *cfg, Tm, prompts_per_micro, &w, C);
         }
-        RS_TRY(embed_backward(mids, P, S, cfg->vocab, w.dh, d, grad + off(OFF_TOK, 0), grad + off(OFF_POS, 0), w.ews,
-                              w.ews_bytes, st));
+        const int32_t* mids = ids + (int64_t)p0 * S;
+        const int32_t* mlast = last_pos ? last_pos + p0 : nullptr;
+        RS_TRY(train_forward(cfg, P16, mids, P, S, n_tok, Tp, w, st));
+        RS_TRY(ranker_head(w.h_in[L], mlast, P, S, P16, cfg, w.g, nullptr, st, w.feat));
+        RS_TRY(cls_logits_launch(w.feat, cls_w, cls_b, P, d, C, w.logits, st));
+        RS_CUDA(cudaMemsetAsync(w.bad, 0, sizeof(int32_t), st));
+        RS_TRY(cls_ce_launch(w.logits, labels + p0, P, C, loss_out + p0, w.dlogits, w.bad, st));
+        RS_TRY(cls_head_backward(w.feat, cls_w, w.dlogits, P, d, C, cls_grad, cls_grad + (size_t)C * d, w.dfeat, st));
+        RS_CUDA(cudaMemsetAsync(w.dh, 0, (size_t)Tp * d * sizeof(float), st));
+        if (Tp > n_tok)
+            RS_CUDA(cudaMemsetAsync(w.dqkv + (size_t)n_tok * 3 * d, 0, (size_t)(Tp - n_tok) * 3 * d * 2, st));
+        RS_TRY(head_backward(w.h_in[L], mlast, P, S, P16 + off(OFF_LNF_W, 0), P16 + off(OFF_LNF_B, 0),
+                             P16 + off(OFF_HEAD_W, 0), nullptr, w.dh, w.rpart, d, nullptr, grad + off(OFF_LNF_W, 0),
+                             nullptr, st, w.dfeat));
+        RS_TRY(train_backward(cfg, P16, grad, mids, P, S, n_tok, Tp, w, st));
     }
     return RS_OK;
 }

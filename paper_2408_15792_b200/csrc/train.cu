@@ -231,7 +231,8 @@ template <int VPL>
 __global__ void head_bwd_kernel(const float* __restrict__ h, const int32_t* __restrict__ last, int B, int S,
                                 const __nv_bfloat16* __restrict__ lw, const __nv_bfloat16* __restrict__ lb,
                                 const __nv_bfloat16* __restrict__ hw, const float* __restrict__ dg,
-                                float* __restrict__ dh, float* __restrict__ part) {
+                                float* __restrict__ dh, float* __restrict__ part,
+                                const float* __restrict__ dfeat) {
     constexpr int d = VPL * 256;
     const int p = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
@@ -255,7 +256,10 @@ __global__ void head_bwd_kernel(const float* __restrict__ h, const int32_t* __re
         s2 += t * t;
     }
     const float rstd = rsqrtf(warp_sum(s2) * (1.0f / d) + TR_LN_EPS);
-    const float gq = dg[p];
+    // dfeat given (the classifier head): it is d loss / d LNf(h) itself and the score
+    // head takes no gradient; else dxf = dg * hw
+    const float gq = dfeat ? 0.f : dg[p];
+    const float* dfr = dfeat ? dfeat + (size_t)p * d : nullptr;
     float* pr = part + (size_t)p * (3 * d + 1);
     float sg = 0.f, sgx = 0.f, gv[VPL * 8];
 #pragma unroll
@@ -265,7 +269,7 @@ __global__ void head_bwd_kernel(const float* __restrict__ h, const int32_t* __re
             const int i = k * 8 + e, col = (lane + 32 * k) * 8 + e;
             const float xh = (xv[i] - mean) * rstd;
             const float xf = xh * lwv[i] + lbv[i];
-            const float dxf = gq * hwv[i];  // d g / d xf = hw
+            const float dxf = dfr ? dfr[col] : gq * hwv[i];  // d g / d xf = hw
             pr[col] = gq * xf;              // d hw
             pr[d + col] = dxf * xh;         // d lnf_w
             pr[2 * d + col] = dxf;          // d lnf_b
@@ -382,15 +386,15 @@ int embed_backward(const int32_t* ids, int B, int S, int vocab, const float* dh,
 
 int head_backward(const float* h, const int32_t* last, int B, int S, const void* lw, const void* lb, const void* hw,
                   const float* dg, float* dh, float* part, int d, float* g_hw, float* g_lnf, float* g_hb,
-                  cudaStream_t st) {
+                  cudaStream_t st, const float* dfeat) {
     const int wpb = 8;
     const int grid = (B + wpb - 1) / wpb;
     const __nv_bfloat16 *a = static_cast<const __nv_bfloat16*>(lw), *b = static_cast<const __nv_bfloat16*>(lb),
                         *c = static_cast<const __nv_bfloat16*>(hw);
     switch (d / 256) {
-        case 1: head_bwd_kernel<1><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, a, b, c, dg, dh, part); break;
-        case 2: head_bwd_kernel<2><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, a, b, c, dg, dh, part); break;
-        case 3: head_bwd_kernel<3><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, a, b, c, dg, dh, part); break;
+        case 1: head_bwd_kernel<1><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, a, b, c, dg, dh, part, dfeat); break;
+        case 2: head_bwd_kernel<2><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, a, b, c, dg, dh, part, dfeat); break;
+        case 3: head_bwd_kernel<3><<<grid, 32 * wpb, 0, st>>>(h, last, B, S, a, b, c, dg, dh, part, dfeat); break;
         default: set_error("head_backward: unsupported d=%d", d); return RS_ERR_INVALID;
     }
     RS_LAUNCH_CHECK();
@@ -400,12 +404,16 @@ int head_backward(const float* h, const int32_t* last, int B, int S, const void*
     RS_CUDA(cudaMemsetAsync(tot, 0, cols * sizeof(float), st));
     RS_TRY(reduce_rows_add(part, B, cols, tot, tot + cols, st));
     // scatter: d hw -> g_hw, (d lnf_w, d lnf_b) -> g_lnf (adjacent), d hb -> g_hb
-    reduce_rows_add_kernel<<<(d + 255) / 256, 256, 0, st>>>(tot, 1, d, g_hw);
-    RS_LAUNCH_CHECK();
+    if (g_hw) {
+        reduce_rows_add_kernel<<<(d + 255) / 256, 256, 0, st>>>(tot, 1, d, g_hw);
+        RS_LAUNCH_CHECK();
+    }
     reduce_rows_add_kernel<<<(2 * d + 255) / 256, 256, 0, st>>>(tot + d, 1, 2 * d, g_lnf);
     RS_LAUNCH_CHECK();
-    reduce_rows_add_kernel<<<1, 32, 0, st>>>(tot + 3 * d, 1, 1, g_hb);
-    RS_LAUNCH_CHECK();
+    if (g_hb) {
+        reduce_rows_add_kernel<<<1, 32, 0, st>>>(tot + 3 * d, 1, 1, g_hb);
+        RS_LAUNCH_CHECK();
+    }
     return RS_OK;
 }
 

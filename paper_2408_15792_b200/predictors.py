@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import dataclasses
 import hashlib
+import math
 import json
 import pathlib
 from dataclasses import dataclass, field
@@ -171,6 +172,18 @@ def _encode(requests, seq_len: int, vocab: int):
     return ids, last
 
 
+def _split_requests(reqs, cfg: TrainConfig, eval_trace):
+    """Train / eval split of _split_features (predictors.py:327-340)."""
+    if eval_trace is not None:
+        return reqs, list(eval_trace)
+    rng0 = np.random.default_rng(cfg.seed)
+    idx = rng0.permutation(len(reqs))
+    n_eval = max(1, int(round(cfg.eval_fraction * len(reqs))))
+    if n_eval >= len(reqs):
+        raise ValueError("trace too small to split for evaluation")
+    return [reqs[i] for i in idx[n_eval:]], [reqs[i] for i in idx[:n_eval]]
+
+
 def train_ranking(trace, cfg: TrainConfig = TrainConfig(), eval_trace=None, model: OptRanker | None = None,
                   group=None) -> TrainResult:
     """ListMLE training of the OPT-shape ranker (reference: train_ranking,
@@ -196,17 +209,7 @@ def train_ranking(trace, cfg: TrainConfig = TrainConfig(), eval_trace=None, mode
         raise ValueError("bucket_width must be >= 1")
     if cfg.lists_per_step < 1:
         raise ValueError("lists_per_step must be >= 1")
-    y_all = np.array([r.true_output_tokens for r in reqs], dtype=np.int64)
-    if eval_trace is not None:
-        tr_reqs, ev_reqs = reqs, list(eval_trace)
-    else:  # _split_features (predictors.py:327-340)
-        rng0 = np.random.default_rng(cfg.seed)
-        idx = rng0.permutation(len(y_all))
-        n_eval = max(1, int(round(cfg.eval_fraction * len(y_all))))
-        if n_eval >= len(y_all):
-            raise ValueError("trace too small to split for evaluation")
-        tr_reqs = [reqs[i] for i in idx[n_eval:]]
-        ev_reqs = [reqs[i] for i in idx[:n_eval]]
+    tr_reqs, ev_reqs = _split_requests(reqs, cfg, eval_trace)
     rc = cfg.ranker
     if model is None:
         model = OptRanker(rc, seed=cfg.seed)
@@ -255,5 +258,101 @@ def train_ranking(trace, cfg: TrainConfig = TrainConfig(), eval_trace=None, mode
     final_tau = eval_tau()
     scorer = OptRankerScorer(model, seq_len=cfg.seq_len)
     report = {"kind": "ranking", "steps": step, "checkpoints": checkpoints, "eval_tau": final_tau,
+              "n_train": len(y), "n_eval": len(ye)}
+    return TrainResult(scorer, report)
+
+
+class OptClassifierScorer:
+    """The bucketed-classification baseline on the OPT backbone (reference:
+    ClassifierScorer, predictors.py:262-300): argmax over C length buckets of a linear head
+    on LN_f(h_last); the score is the bucket's midpoint in tokens (length calibrated)."""
+
+    kind = "opt-classifier"
+    length_calibrated = True
+    warmup_tokens = 0
+    charges_predictor = True
+
+    def __init__(self, trainer, bucket_size: int, seq_len: int = 128):
+        self.trainer = trainer
+        self.bucket_size = int(bucket_size)
+        self.seq_len = int(seq_len)
+
+    @property
+    def n_buckets(self) -> int:
+        return self.trainer.n_classes
+
+    def predict_buckets(self, requests) -> np.ndarray:
+        ids_np, last_np = _encode(list(requests), self.seq_len, self.trainer.model.cfg.vocab)
+        dev = self.trainer.model.dev
+        lg = self.trainer.logits(torch.from_numpy(ids_np).to(dev), torch.from_numpy(last_np).to(dev))
+        return lg.argmax(dim=1).cpu().numpy()
+
+    def score_batch(self, requests, seed) -> list[float | None]:
+        reqs = list(requests)
+        if not reqs:
+            return []
+        return [float(b * self.bucket_size + self.bucket_size / 2.0) for b in self.predict_buckets(reqs)]
+
+
+def train_classifier(trace, cfg: TrainConfig = TrainConfig(), n_buckets: int | None = 10,
+                     bucket_size: int | None = None, eval_trace=None, model: OptRanker | None = None,
+                     group=None) -> TrainResult:
+    """Bucketed classification on the OPT backbone (reference: train_classifier,
+    predictors.py:409-479 — same bucketing rules, split, per-epoch permutation, minibatches
+    of batch_size, Adam; report keys kind/steps/n_buckets/bucket_size/accuracy/eval_tau/
+    n_train/n_eval). Each minibatch is one optimizer step whose gradient is the batch mean
+    of the cross-entropy (rs_ranker_grad_cls); under torch.distributed the batch is split
+    across ranks and the gradients all-reduced."""
+    from . import dp
+    from .ranking import kendall_tau_b
+    from .trainer import ClassifierTrainer
+
+    reqs = list(trace)
+    if len(reqs) < 4:
+        raise ValueError("need at least 4 requests to train")
+    tr_reqs, ev_reqs = _split_requests(reqs, cfg, eval_trace)
+    y = np.array([r.true_output_tokens for r in tr_reqs], dtype=np.int64)
+    ye = np.array([r.true_output_tokens for r in ev_reqs], dtype=np.int64)
+    max_len = int(max(y.max(), ye.max()))
+    if bucket_size is None:
+        if n_buckets is None:
+            raise ValueError("give n_buckets or bucket_size")
+        bucket_size = max(1, math.ceil(max_len / n_buckets))
+    if n_buckets is None:
+        n_buckets = max_len // bucket_size + 1
+    if n_buckets < 2:
+        raise ValueError("classification needs at least 2 buckets")
+    labels = np.minimum(y // bucket_size, n_buckets - 1)
+    labels_e = np.minimum(ye // bucket_size, n_buckets - 1)
+    rc = cfg.ranker
+    if model is None:
+        model = OptRanker(rc, seed=cfg.seed)
+    dev = model.dev
+    ids_np, last_np = _encode(tr_reqs, cfg.seq_len, rc.vocab)
+    eids_np, elast_np = _encode(ev_reqs, cfg.seq_len, rc.vocab)
+    ids, last = torch.from_numpy(ids_np).to(dev), torch.from_numpy(last_np).to(dev)
+    lab = torch.from_numpy(labels.astype(np.int32)).to(dev)
+    trainer = ClassifierTrainer(model, n_buckets, lr=cfg.learning_rate, betas=cfg.betas, group=group)
+    world, rank = dp.world_rank(group)
+    rng = np.random.default_rng(cfg.seed + 1)
+    step = 0
+    for _epoch in range(cfg.epochs):
+        order = rng.permutation(len(y))
+        for start in range(0, len(order), cfg.batch_size):
+            batch = order[start:start + cfg.batch_size]
+            if len(batch) == 0:
+                continue
+            lo, hi = dp.shard_range(len(batch), world, rank)
+            if hi > lo:
+                bi = torch.from_numpy(batch[lo:hi]).to(dev)
+                trainer.accumulate(ids[bi], lab[bi], last[bi])
+            trainer.apply(len(batch))
+            step += 1
+    scorer = OptClassifierScorer(trainer, bucket_size, seq_len=cfg.seq_len)
+    lg = trainer.logits(torch.from_numpy(eids_np).to(dev), torch.from_numpy(elast_np).to(dev))
+    pred_e = lg.argmax(dim=1).cpu().numpy()
+    midpoints = pred_e * bucket_size + bucket_size / 2.0
+    report = {"kind": "classifier", "steps": step, "n_buckets": int(n_buckets), "bucket_size": int(bucket_size),
+              "accuracy": float(np.mean(pred_e == labels_e)), "eval_tau": kendall_tau_b(midpoints, ye).tau,
               "n_train": len(y), "n_eval": len(ye)}
     return TrainResult(scorer, report)

@@ -152,6 +152,23 @@ class OptRanker:
                                          _lib.stream_handle(self.dev)), "rs_ranker_forward")
         return g
 
+    def features(self, ids: torch.Tensor, last_pos: torch.Tensor | None = None) -> torch.Tensor:
+        """LN_f(h[last_pos]) fp32 [B, d]: the input of the classification head (§8f #4)."""
+        if ids.dim() != 2:
+            raise ValueError("ids must be [B, S]")
+        B, S = ids.shape
+        ids = ids.to(self.dev, torch.int32).contiguous()
+        lp = None if last_pos is None else last_pos.to(self.dev, torch.int32).contiguous()
+        g = torch.empty(B, dtype=torch.float32, device=self.dev)
+        feat = torch.empty(B, self.cfg.d_model, dtype=torch.float32, device=self.dev)
+        lib = _lib.load()
+        c = self.cfg.c()
+        ws, wn = _lib.workspace.get(self.workspace_bytes(B, S), self.dev)
+        _lib.check(lib.rs_ranker_forward_ex(ctypes.byref(c), self.flat.data_ptr(), ids.data_ptr(), _lib.ptr(lp), B, S,
+                                            g.data_ptr(), None, feat.data_ptr(), ws, wn, _lib.stream_handle(self.dev)),
+                   "rs_ranker_forward_ex")
+        return feat
+
     def forward_sharded(self, ids: torch.Tensor, last_pos: torch.Tensor | None = None, group=None) -> torch.Tensor:
         """Data-parallel scoring: this rank scores its contiguous shard of the
         global batch `ids` [B, S] and the fp32 outputs of all B prompts are all-gathered

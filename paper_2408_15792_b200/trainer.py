@@ -79,3 +79,75 @@ class RankerTrainer:
         n_lists = ids.shape[0] // list_len
         self.apply(total_lists if total_lists is not None else n_lists * self._world())
         return loss
+
+
+class ClassifierTrainer:
+    """The bucketed-classification baseline on the same backbone (§8f #4; reference:
+    train_classifier, predictors.py:409-479): a C-way linear head on LN_f(h_last),
+    softmax cross-entropy, Adam on the backbone and the head. accumulate() adds the
+    gradient of the summed per-prompt nll (rs_ranker_grad_cls); apply() all-reduces and
+    steps with grad_scale = 1 / prompts (the reference's batch mean)."""
+
+    def __init__(self, model: OptRanker, n_classes: int, lr: float = 2e-5, betas=(0.9, 0.999), eps: float = 1e-8,
+                 prompts_per_micro: int = 256, group=None):
+        if n_classes < 2:
+            raise ValueError("classification needs at least 2 buckets")
+        self.model, self.n_classes = model, int(n_classes)
+        self.lr, self.betas, self.eps = float(lr), (float(betas[0]), float(betas[1])), float(eps)
+        self.prompts_per_micro, self.group = int(prompts_per_micro), group
+        dev, d = model.dev, model.cfg.d_model
+        self.master = model.flat.float()
+        self.m, self.v, self.grad = (torch.zeros_like(self.master) for _ in range(3))
+        # head: W [C, d] then b [C], fp32, zero-initialised like the reference (predictors.py:438-439)
+        self.head = torch.zeros(self.n_classes * d + self.n_classes, dtype=torch.float32, device=dev)
+        self.hm, self.hv, self.hgrad = (torch.zeros_like(self.head) for _ in range(3))
+        self._head_bf16 = torch.empty(self.head.numel(), dtype=torch.bfloat16, device=dev)  # Adam's bf16 copy (unused)
+        self.t = 0
+
+    @property
+    def W(self) -> torch.Tensor:
+        return self.head[:self.n_classes * self.model.cfg.d_model].view(self.n_classes, -1)
+
+    @property
+    def b(self) -> torch.Tensor:
+        return self.head[self.n_classes * self.model.cfg.d_model:]
+
+    def logits(self, ids: torch.Tensor, last_pos: torch.Tensor | None = None) -> torch.Tensor:
+        feat = self.model.features(ids, last_pos)
+        B, d = feat.shape
+        out = torch.empty(B, self.n_classes, dtype=torch.float32, device=self.model.dev)
+        _lib.check(_lib.load().rs_cls_logits(feat.data_ptr(), self.W.data_ptr(), self.b.data_ptr(), B, d,
+                                             self.n_classes, out.data_ptr(), _lib.stream_handle(self.model.dev)),
+                   "rs_cls_logits")
+        return out
+
+    def accumulate(self, ids: torch.Tensor, labels: torch.Tensor, last_pos: torch.Tensor | None = None):
+        n, S = ids.shape
+        dev = self.model.dev
+        labels = labels.to(dev, torch.int32).contiguous().view(-1)
+        if labels.numel() != n or int(labels.min()) < 0 or int(labels.max()) >= self.n_classes:
+            raise ValueError("labels must be one class in [0, n_classes) per prompt")
+        ids = ids.to(dev, torch.int32).contiguous()
+        lp = None if last_pos is None else last_pos.to(dev, torch.int32).contiguous().view(-1)
+        loss = torch.empty(n, dtype=torch.float32, device=dev)
+        lib = _lib.load()
+        c = self.model.cfg.c()
+        mb = min(self.prompts_per_micro, n)
+        need = lib.rs_ranker_grad_cls_workspace_size(ctypes.byref(c), mb, S, self.n_classes)
+        ws, wn = _lib.workspace.get(need, dev)
+        _lib.check(lib.rs_ranker_grad_cls(ctypes.byref(c), self.model.flat.data_ptr(), self.grad.data_ptr(),
+                                          ids.data_ptr(), _lib.ptr(lp), labels.data_ptr(), n, S, self.n_classes,
+                                          self.W.data_ptr(), self.b.data_ptr(), self.hgrad.data_ptr(), mb,
+                                          loss.data_ptr(), ws, wn, _lib.stream_handle(dev)), "rs_ranker_grad_cls")
+        return loss
+
+    def apply(self, total_prompts: int) -> None:
+        dp.allreduce_sum_(self.grad, self.group)
+        dp.allreduce_sum_(self.hgrad, self.group)
+        self.t += 1
+        lib, st = _lib.load(), _lib.stream_handle(self.model.dev)
+        for master, m, v, g, pb in ((self.master, self.m, self.v, self.grad, self.model.flat),
+                                    (self.head, self.hm, self.hv, self.hgrad, self._head_bf16)):
+            _lib.check(lib.rs_adam_step(master.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(), pb.data_ptr(),
+                                        master.numel(), self.lr, self.betas[0], self.betas[1], self.eps, self.t,
+                                        1.0 / float(total_prompts), st), "rs_adam_step")

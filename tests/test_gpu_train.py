@@ -46,7 +46,7 @@ def _r(x, fwd=True, bwd=False):
     return _Round.apply(x, fwd, bwd)
 
 
-def _forward_with_grad(params, cfg, ids, emulate=False):
+def _forward_with_grad(params, cfg, ids, emulate=False, features=False):
     """fp32 OPT-shape forward with autograd (the oracle, oracle/opt_ranker.py semantics).
     emulate=True rounds activations / activation gradients to bf16 where the CUDA
     training pass stores them in bf16 (x1, qkv, att, x2, f and the attention P forward;
@@ -84,6 +84,8 @@ def _forward_with_grad(params, cfg, ids, emulate=False):
         f = r(torch.relu(x @ p["fc1_w"].t() + p["fc1_b"]), True, True)
         h = h + r(f @ p["fc2_w"].t() + p["fc2_b"], False, True)
     x = F.layer_norm(h[:, -1], (d,), params["lnf_w"], params["lnf_b"], eps=1e-5)
+    if features:  # LN_f(h_last): the classification head's input
+        return x
     return x @ params["head_w"] + params["head_b"][0]
 
 
