@@ -46,8 +46,8 @@ def install(ranksched) -> None:
       reference imported them (ranking, predictors, engine, the package namespace);
     * engine.make_policy: "ranking" -> the device RankingPolicy, every other policy
       name -> the reference's own factory;
-    * predictors.scorer_from_dict / load_scorer: kind "opt-ranker" -> OptRankerScorer,
-      everything else -> the reference's if-chain.
+    * predictors.scorer_from_dict / load_scorer: kinds "opt-ranker" / "opt-classifier" ->
+      OptRankerScorer / OptClassifierScorer, everything else -> the reference's if-chain.
     """
     from . import predictors as b_pred
     from . import ranking as b_rank
@@ -67,7 +67,7 @@ def install(ranksched) -> None:
         return ref_make_policy(name, config, length_calibrated)
 
     def scorer_from_dict(obj):
-        if obj.get("kind") == b_pred.OptRankerScorer.kind:
+        if obj.get("kind") in (b_pred.OptRankerScorer.kind, b_pred.OptClassifierScorer.kind):
             return b_pred.scorer_from_dict(obj)
         return ref_from_dict(obj)
 

@@ -92,7 +92,7 @@ def _sha256_file(path) -> str:
     return h.hexdigest()
 
 
-def save_scorer(scorer: OptRankerScorer, path: str) -> None:
+def save_scorer(scorer, path: str) -> None:
     """JSON header at `path` + raw bf16 parameters at `path + '.bin'`."""
     p = pathlib.Path(path)
     weights = str(p) + ".bin"
@@ -104,10 +104,11 @@ def save_scorer(scorer: OptRankerScorer, path: str) -> None:
 
 
 def scorer_from_dict(obj: dict):
-    """`kind == "opt-ranker"` -> OptRankerScorer; other kinds belong to the reference
+    """`kind == "opt-ranker"` -> OptRankerScorer, "opt-classifier" -> OptClassifierScorer;
+    other kinds belong to the reference
     (ranksched.predictors.scorer_from_dict; install() chains the two)."""
     kind = obj.get("kind")
-    if kind != OptRankerScorer.kind:
+    if kind not in (OptRankerScorer.kind, "opt-classifier"):
         raise ValueError(f"unknown scorer kind {kind!r}")
     cfg = RankerConfig(**obj["config"])
     model = OptRanker(cfg, seed=None)
@@ -118,7 +119,12 @@ def scorer_from_dict(obj: dict):
     if raw.size != model.flat.numel():
         raise ValueError(f"{weights}: {raw.size} parameters, expected {model.flat.numel()}")
     model.flat.view(torch.int16).copy_(torch.from_numpy(raw))
-    s = OptRankerScorer(model, seq_len=obj.get("seq_len", 128))
+    if kind == "opt-classifier":
+        s = OptClassifierScorer(model, torch.tensor(obj["head_weights"], dtype=torch.float32),
+                                torch.tensor(obj["head_bias"], dtype=torch.float32), obj["bucket_size"],
+                                seq_len=obj.get("seq_len", 128))
+    else:
+        s = OptRankerScorer(model, seq_len=obj.get("seq_len", 128))
     s.weights_path = weights
     return s
 
@@ -265,26 +271,33 @@ def train_ranking(trace, cfg: TrainConfig = TrainConfig(), eval_trace=None, mode
 class OptClassifierScorer:
     """The bucketed-classification baseline on the OPT backbone (reference:
     ClassifierScorer, predictors.py:262-300): argmax over C length buckets of a linear head
-    on LN_f(h_last); the score is the bucket's midpoint in tokens (length calibrated)."""
+    (W [C, d], b [C], fp32) on LN_f(h_last); the score is the bucket's midpoint in tokens
+    (length calibrated)."""
 
     kind = "opt-classifier"
     length_calibrated = True
     warmup_tokens = 0
     charges_predictor = True
 
-    def __init__(self, trainer, bucket_size: int, seq_len: int = 128):
-        self.trainer = trainer
+    def __init__(self, model: OptRanker, weights: torch.Tensor, bias: torch.Tensor, bucket_size: int,
+                 seq_len: int = 128):
+        self.model = model
+        self.weights = weights.to(model.dev, torch.float32).contiguous()
+        self.bias = bias.to(model.dev, torch.float32).contiguous()
         self.bucket_size = int(bucket_size)
         self.seq_len = int(seq_len)
+        self.weights_path: str | None = None
 
     @property
     def n_buckets(self) -> int:
-        return self.trainer.n_classes
+        return int(self.bias.numel())
 
     def predict_buckets(self, requests) -> np.ndarray:
-        ids_np, last_np = _encode(list(requests), self.seq_len, self.trainer.model.cfg.vocab)
-        dev = self.trainer.model.dev
-        lg = self.trainer.logits(torch.from_numpy(ids_np).to(dev), torch.from_numpy(last_np).to(dev))
+        from .trainer import classifier_logits
+        ids_np, last_np = _encode(list(requests), self.seq_len, self.model.cfg.vocab)
+        dev = self.model.dev
+        lg = classifier_logits(self.model, self.weights, self.bias, torch.from_numpy(ids_np).to(dev),
+                               torch.from_numpy(last_np).to(dev))
         return lg.argmax(dim=1).cpu().numpy()
 
     def score_batch(self, requests, seed) -> list[float | None]:
@@ -292,6 +305,14 @@ class OptClassifierScorer:
         if not reqs:
             return []
         return [float(b * self.bucket_size + self.bucket_size / 2.0) for b in self.predict_buckets(reqs)]
+
+    def to_dict(self) -> dict:
+        if self.weights_path is None:
+            raise ValueError("opt-classifier backbone weights are saved by save_scorer(); call it before to_dict()")
+        return {"kind": self.kind, "config": dataclasses.asdict(self.model.cfg), "seq_len": self.seq_len,
+                "bucket_size": self.bucket_size, "head_weights": self.weights.cpu().tolist(),
+                "head_bias": self.bias.cpu().tolist(), "weights": self.weights_path,
+                "weights_sha256": _sha256_file(self.weights_path)}
 
 
 def train_classifier(trace, cfg: TrainConfig = TrainConfig(), n_buckets: int | None = 10,
@@ -348,7 +369,8 @@ def train_classifier(trace, cfg: TrainConfig = TrainConfig(), n_buckets: int | N
                 trainer.accumulate(ids[bi], lab[bi], last[bi])
             trainer.apply(len(batch))
             step += 1
-    scorer = OptClassifierScorer(trainer, bucket_size, seq_len=cfg.seq_len)
+    scorer = OptClassifierScorer(model, trainer.W.detach().clone(), trainer.b.detach().clone(), bucket_size,
+                                 seq_len=cfg.seq_len)
     lg = trainer.logits(torch.from_numpy(eids_np).to(dev), torch.from_numpy(elast_np).to(dev))
     pred_e = lg.argmax(dim=1).cpu().numpy()
     midpoints = pred_e * bucket_size + bucket_size / 2.0

@@ -81,6 +81,20 @@ class RankerTrainer:
         return loss
 
 
+def classifier_logits(model: OptRanker, W: torch.Tensor, b: torch.Tensor, ids: torch.Tensor,
+                      last_pos: torch.Tensor | None = None) -> torch.Tensor:
+    """logits [B, C] = LN_f(h_last) W^T + b (rs_ranker_forward_ex features + rs_cls_logits)."""
+    feat = model.features(ids, last_pos)
+    B, d = feat.shape
+    C = W.shape[0]
+    W = W.to(model.dev, torch.float32).contiguous()
+    b = b.to(model.dev, torch.float32).contiguous()
+    out = torch.empty(B, C, dtype=torch.float32, device=model.dev)
+    _lib.check(_lib.load().rs_cls_logits(feat.data_ptr(), W.data_ptr(), b.data_ptr(), B, d, C, out.data_ptr(),
+                                         _lib.stream_handle(model.dev)), "rs_cls_logits")
+    return out
+
+
 class ClassifierTrainer:
     """The bucketed-classification baseline on the same backbone (§8f #4; reference:
     train_classifier, predictors.py:409-479): a C-way linear head on LN_f(h_last),
@@ -113,13 +127,7 @@ class ClassifierTrainer:
         return self.head[self.n_classes * self.model.cfg.d_model:]
 
     def logits(self, ids: torch.Tensor, last_pos: torch.Tensor | None = None) -> torch.Tensor:
-        feat = self.model.features(ids, last_pos)
-        B, d = feat.shape
-        out = torch.empty(B, self.n_classes, dtype=torch.float32, device=self.model.dev)
-        _lib.check(_lib.load().rs_cls_logits(feat.data_ptr(), self.W.data_ptr(), self.b.data_ptr(), B, d,
-                                             self.n_classes, out.data_ptr(), _lib.stream_handle(self.model.dev)),
-                   "rs_cls_logits")
-        return out
+        return classifier_logits(self.model, self.W, self.b, ids, last_pos)
 
     def accumulate(self, ids: torch.Tensor, labels: torch.Tensor, last_pos: torch.Tensor | None = None):
         n, S = ids.shape

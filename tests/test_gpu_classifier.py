@@ -118,5 +118,13 @@ def test_train_classifier_learns():
     assert isinstance(res.scorer, OptClassifierScorer) and res.scorer.length_calibrated
     s = res.scorer.score_batch(t[:5], seed=0)
     assert all(v % res.scorer.bucket_size == res.scorer.bucket_size / 2.0 for v in s)
+    # save / load round trip (the scorer registry, predictors.py:486-527)
+    import tempfile, os
+    from paper_2408_15792_b200.predictors import load_scorer, save_scorer
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "cls.json")
+        save_scorer(res.scorer, path)
+        back = load_scorer(path)
+        assert isinstance(back, OptClassifierScorer) and back.score_batch(t[:50], 0) == res.scorer.score_batch(t[:50], 0)
     with pytest.raises(ValueError):
         train_classifier(t, _cfg(), n_buckets=1)
