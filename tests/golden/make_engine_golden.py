@@ -85,5 +85,33 @@ def main():
               c["metrics"]["n_dropped"], "dropped", c["metrics"]["n_preemptions"], "preemptions")
 
 
+def main_large():
+    """The cfg5 shape at 20k requests (BASELINE configs[4] runs 100k: the reference loop
+    takes ~6 min per 20k here): generate_poisson(40/s, sharegpt, seed 7, prompt_noise
+    0.25), max_batch 256, starvation 100 / 50, the default cost preset. Stored compactly:
+    the trace, the score table, the step count, sha256 of the canonical step records
+    and of the per-request rows, and the metrics."""
+    import time
+    t0 = time.perf_counter()
+    n, seed = 20000, 7
+    trace = generate_poisson(40.0, n, LengthDist.parse("sharegpt"), seed, prompt_noise=0.25)
+    rng = np.random.default_rng(seed + 100)
+    sc = rng.normal(size=n).astype(np.float32)
+    table = {r.id: float(sc[k]) for k, r in enumerate(trace.requests)}
+    sched = SchedulerConfig(max_batch=256, starvation_threshold=100, priority_quantum=50)
+    res = engine.run(trace, "ranking", TableScorer(table), sched, engine.COST_PRESETS["default"])
+    recs = res.records
+    out = {"generator": "make_engine_golden.py --large", "tag": "cfg5_poisson20k",
+           "sched": {"max_batch": 256, "starvation_threshold": 100, "priority_quantum": 50, "preemption": True},
+           "cost": "default", "kv_budget": None,
+           "requests": [[r.id, r.arrival_time, r.prompt_tokens, r.true_output_tokens] for r in trace.requests],
+           "scores": [table[r.id] for r in trace.requests], "metrics": res.metrics, "n_steps": len(recs),
+           "records_sha256": hashlib.sha256(canonical(recs).encode()).hexdigest(),
+           "rows_sha256": hashlib.sha256(canonical(res.requests).encode()).hexdigest(),
+           "reference_seconds": time.perf_counter() - t0}
+    (OUT.parent / "engine_golden_20k.json").write_text(json.dumps(out) + "\n")
+    print(out["tag"], out["n_steps"], "steps", f"{out['reference_seconds']:.0f} s")
+
+
 if __name__ == "__main__":
-    main()
+    main_large() if "--large" in sys.argv else main()

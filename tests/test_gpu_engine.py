@@ -84,3 +84,25 @@ def test_engine_mass_preemption_keeps_alive_order():
                          in_place_compaction=in_place)
         pre = [r["preempted"] for r in res.records if r["preempted"]]
         assert pre and len(pre[0]) == n1 and pre[0] == sorted(pre[0]) == list(range(n1))
+
+
+def test_engine_matches_reference_at_cfg5_scale():
+    """20k Poisson(40/s) sharegpt requests with the cfg5 scheduler settings (BASELINE
+    configs[4] at a fifth of its size): every step record and request row bit-identical
+    to the reference engine's (fixture: make_engine_golden.py --large)."""
+    import pathlib
+    from paper_2408_15792_b200 import engine
+    from paper_2408_15792_b200.schedulers import SchedulerConfig
+    from paper_2408_15792_b200.workload import Request
+    p = pathlib.Path(__file__).resolve().parent / "golden" / "engine_golden_20k.json"
+    if not p.exists():
+        pytest.skip("large engine golden not generated")
+    c = json.loads(p.read_text())
+    reqs = [Request(id=i, arrival_time=a, prompt_tokens=pt, true_output_tokens=o) for i, a, pt, o in c["requests"]]
+    res = engine.run(reqs, scores=c["scores"], sched=SchedulerConfig(**c["sched"]),
+                     cost=engine.COST_PRESETS[c["cost"]], record=True)
+    assert len(res.records) == c["n_steps"]
+    assert hashlib.sha256(_canonical(res.records).encode()).hexdigest() == c["records_sha256"]
+    assert hashlib.sha256(_canonical(res.requests).encode()).hexdigest() == c["rows_sha256"]
+    for k, v in c["metrics"].items():
+        assert res.metrics[k] == v, (k, res.metrics[k], v)
