@@ -296,13 +296,20 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_sort_emit(const RankKey* __re
 }
 
 constexpr int UPD_THREADS = 1024;
+constexpr int UPD_ITEMS = 4;  // rows per thread: element k * UPD_THREADS + tid of the block's chunk
+constexpr int UPD_CHUNK = UPD_THREADS * UPD_ITEMS;
 
 // State update (schedulers.py:224-240) + per-block counts of promoted / demoted.
-__global__ void starvation_update(rs_queue_soa q, const uint8_t* __restrict__ sched, int32_t threshold,
-                                  int32_t pquantum, uint8_t* __restrict__ pd, uint32_t* __restrict__ bcnt) {
-    const uint32_t i = blockIdx.x * UPD_THREADS + threadIdx.x;
-    uint8_t code = 0;
-    if (i < (uint32_t)q.n) {
+__global__ void __launch_bounds__(UPD_THREADS) starvation_update(rs_queue_soa q, const uint8_t* __restrict__ sched,
+                                                                 int32_t threshold, int32_t pquantum,
+                                                                 uint8_t* __restrict__ pd, uint32_t* __restrict__ bcnt) {
+    __shared__ uint32_t wsum[2][UPD_THREADS / 32];
+    uint32_t np = 0, nd = 0;
+#pragma unroll
+    for (int k = 0; k < UPD_ITEMS; ++k) {
+        const uint32_t i = blockIdx.x * UPD_CHUNK + k * UPD_THREADS + threadIdx.x;
+        if (i >= (uint32_t)q.n) break;
+        uint8_t code = 0;
         uint8_t f = q.flags[i];
         int32_t st = q.starvation[i];
         int32_t qu = q.quantum[i];
@@ -326,12 +333,25 @@ __global__ void starvation_update(rs_queue_soa q, const uint8_t* __restrict__ sc
         q.starvation[i] = st;
         q.quantum[i] = qu;
         pd[i] = code;
+        np += code == 1;
+        nd += code == 2;
     }
-    const int np = __syncthreads_count(code == 1);
-    const int nd = __syncthreads_count(code == 2);
-    if (threadIdx.x == 0) {
-        bcnt[2 * blockIdx.x] = np;
-        bcnt[2 * blockIdx.x + 1] = nd;
+    np = warp_sum(np);
+    nd = warp_sum(nd);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) {
+        wsum[0][w] = np;
+        wsum[1][w] = nd;
+    }
+    __syncthreads();
+    if (w == 0) {
+        uint32_t a = wsum[0][lane], b = wsum[1][lane];
+        a = warp_sum(a);
+        b = warp_sum(b);
+        if (lane == 0) {
+            bcnt[2 * blockIdx.x] = a;
+            bcnt[2 * blockIdx.x + 1] = b;
+        }
     }
 }
 
@@ -390,38 +410,65 @@ __global__ void __launch_bounds__(1024) scan_pairs(uint32_t* __restrict__ bcnt, 
     }
 }
 
-__global__ void scatter_pd(const uint8_t* __restrict__ pd, const int64_t* __restrict__ id, uint32_t n,
-                           const uint32_t* __restrict__ boff, int64_t* __restrict__ prom, int64_t* __restrict__ dem) {
-    __shared__ uint32_t wp[UPD_THREADS / 32], wd[UPD_THREADS / 32];
-    const uint32_t i = blockIdx.x * UPD_THREADS + threadIdx.x;
-    const uint8_t c = i < n ? pd[i] : 0;
+// Order-preserving compaction of the promoted / demoted ids: within a block, rows in
+// (item k, warp, lane) order = index order; per-(k, warp) counts scanned by one warp.
+__global__ void __launch_bounds__(UPD_THREADS) scatter_pd(const uint8_t* __restrict__ pd,
+                                                          const int64_t* __restrict__ id, uint32_t n,
+                                                          const uint32_t* __restrict__ boff,
+                                                          int64_t* __restrict__ prom, int64_t* __restrict__ dem) {
+    constexpr int NW = UPD_THREADS / 32;
+    __shared__ uint32_t cp[UPD_ITEMS * NW], cd[UPD_ITEMS * NW];
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const unsigned bp = __ballot_sync(0xffffffffu, c == 1);
-    const unsigned bd = __ballot_sync(0xffffffffu, c == 2);
-    if (lane == 0) {
-        wp[w] = __popc(bp);
-        wd[w] = __popc(bd);
+    uint8_t c[UPD_ITEMS];
+    unsigned bp[UPD_ITEMS], bd[UPD_ITEMS];
+#pragma unroll
+    for (int k = 0; k < UPD_ITEMS; ++k) {
+        const uint32_t i = blockIdx.x * UPD_CHUNK + k * UPD_THREADS + threadIdx.x;
+        c[k] = i < n ? pd[i] : 0;
+        bp[k] = __ballot_sync(0xffffffffu, c[k] == 1);
+        bd[k] = __ballot_sync(0xffffffffu, c[k] == 2);
+        if (lane == 0) {
+            cp[k * NW + w] = __popc(bp[k]);
+            cd[k * NW + w] = __popc(bd[k]);
+        }
     }
     __syncthreads();
-    if (w == 0) {
-        uint32_t xp = wp[lane], xd = wd[lane];
-        uint32_t ip = xp, id2 = xd;
+    if (w == 0) {  // exclusive scan of UPD_ITEMS * NW = 128 counts, 4 per lane
+        uint32_t vp[UPD_ITEMS], vd[UPD_ITEMS], sp = 0, sd = 0;
+#pragma unroll
+        for (int j = 0; j < UPD_ITEMS; ++j) {
+            vp[j] = cp[lane * UPD_ITEMS + j];
+            vd[j] = cd[lane * UPD_ITEMS + j];
+            sp += vp[j];
+            sd += vd[j];
+        }
+        uint32_t ip = sp, id2 = sd;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            uint32_t yp = __shfl_up_sync(0xffffffffu, ip, o);
-            uint32_t yd = __shfl_up_sync(0xffffffffu, id2, o);
+            const uint32_t yp = __shfl_up_sync(0xffffffffu, ip, o), yd = __shfl_up_sync(0xffffffffu, id2, o);
             if (lane >= (uint32_t)o) {
                 ip += yp;
                 id2 += yd;
             }
         }
-        wp[lane] = ip - xp;
-        wd[lane] = id2 - xd;
+        uint32_t ap = ip - sp, ad = id2 - sd;
+#pragma unroll
+        for (int j = 0; j < UPD_ITEMS; ++j) {
+            cp[lane * UPD_ITEMS + j] = ap;
+            cd[lane * UPD_ITEMS + j] = ad;
+            ap += vp[j];
+            ad += vd[j];
+        }
     }
     __syncthreads();
     const unsigned below = (1u << lane) - 1u;
-    if (c == 1) prom[boff[2 * blockIdx.x] + wp[w] + __popc(bp & below)] = id[i];
-    if (c == 2) dem[boff[2 * blockIdx.x + 1] + wd[w] + __popc(bd & below)] = id[i];
+    const uint32_t bp0 = boff[2 * blockIdx.x], bd0 = boff[2 * blockIdx.x + 1];
+#pragma unroll
+    for (int k = 0; k < UPD_ITEMS; ++k) {
+        const uint32_t i = blockIdx.x * UPD_CHUNK + k * UPD_THREADS + threadIdx.x;
+        if (c[k] == 1) prom[bp0 + cp[k * NW + w] + __popc(bp[k] & below)] = id[i];
+        if (c[k] == 2) dem[bd0 + cd[k * NW + w] + __popc(bd[k] & below)] = id[i];
+    }
 }
 
 __global__ void build_arrival_keys(const double* __restrict__ arr, const int64_t* __restrict__ id, uint32_t n,
@@ -586,7 +633,7 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         }
     }
     RS_LAUNCH_CHECK();
-    const uint32_t nblk = (n + UPD_THREADS - 1) / UPD_THREADS;
+    const uint32_t nblk = (n + UPD_CHUNK - 1) / UPD_CHUNK;
     starvation_update<<<nblk, UPD_THREADS, 0, st>>>(*q, w.sched, threshold, pquantum, w.pd, w.bcnt);
     RS_LAUNCH_CHECK();
     scan_pairs<<<1, 1024, 0, st>>>(w.bcnt, nblk, counts);

@@ -7,7 +7,7 @@ import torch  # noqa: E402
 from paper_2408_15792_b200 import _lib  # noqa: E402
 from paper_2408_15792_b200.schedulers import DeviceQueue, SchedulerConfig  # noqa: E402
 
-n = 1 << 20
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
 g = torch.Generator(device="cuda").manual_seed(4)
 dq = DeviceQueue(n, torch.device("cuda"), score_dtype=torch.float32)
 dq.score.copy_(torch.randn(n, device="cuda", generator=g))
