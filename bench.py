@@ -301,7 +301,7 @@ def size_sweep(pk, reps=3):
     from paper_2408_15792_b200.schedulers import DeviceQueue, SchedulerConfig
     out = {"tau": [], "rank_step": []}
     g = torch.Generator(device="cuda").manual_seed(11)
-    for n in (1 << 20, 1 << 24, 1 << 26):
+    for n in (1 << 20, 1 << 24, 1 << 26, 1 << 28):  # to 256M rows (2.15 GB of x, y), SURVEY 8d
         x = torch.randn(n, device="cuda", generator=g)
         y = torch.randint(1, 2049, (n,), device="cuda", generator=g, dtype=torch.int32)
         res = torch.empty(6, dtype=torch.int64, device="cuda")
@@ -311,7 +311,7 @@ def size_sweep(pk, reps=3):
                            "achieved_gbs": 8.0 * n / t / 1e6, "frac": 8.0 * n / t / 1e6 / pk["hbm_gbs"]})
         del x, y
     cfg = SchedulerConfig(max_batch=256, starvation_threshold=100, priority_quantum=50)
-    for n in (1 << 20, 1 << 24):
+    for n in (1 << 20, 1 << 24, 1 << 26):  # reorder to 64M rows
         dq = DeviceQueue(n, torch.device("cuda"), score_dtype=torch.float32)
         dq.score.copy_(torch.randn(n, device="cuda", generator=g))
         from paper_2408_15792_b200 import _lib
