@@ -412,156 +412,165 @@ __device__ __forceinline__ void listmle64_one(const float* __restrict__ gnet, co
     listmle64_scan(t0, t1, v0, v1, L, inv, s0, s1, loss_out + list, dg_out + (size_t)list * L);
 }
 
-// Two lists per warp (16 lanes x 4 items each) for the common case — labels < 1023 and
-// score ranges within the shifted-sum bound — so the shuffle stages of the sort and of
-// both scans serve two lists at once; any pair that falls outside it is redone one list
-// at a time by listmle64_one. Sorted element p of a list lives in lane 4p.. of its half:
-// lane p >> 2, packed register (p >> 1) & 1, 16-bit half p & 1.
-// W > 0: the bucket width as a compile-time constant (the training default, 10: the
-// floor division becomes a multiply-shift); W == 0: runtime `width`.
-template <int W>
-__global__ void __launch_bounds__(256) listmle_lengths64x2_kernel(const float* __restrict__ gnet,
+// LPW lists per warp (32 / LPW lanes x 64 * LPW / 32 items each) for the common case —
+// labels < 1023 and score ranges within the shifted-sum bound — so the shuffle stages of
+// the sort and of both scans serve LPW lists at once and the first log2(items) stages of
+// every bitonic merge stay inside a lane; any warp whose lists fall outside that case is
+// redone one list at a time by listmle64_one. Sorted element p of a list lives in lane
+// p / IPL of its group, packed register (p % IPL) / 2, 16-bit half p % 2.
+// W > 0: the bucket width as a compile-time constant (the training default, 10: the floor
+// division becomes a multiply-shift); W == 0: runtime `width`.
+template <int LPW, int W>
+__global__ void __launch_bounds__(256) listmle_lengths64xN_kernel(const float* __restrict__ gnet,
                                                                   const int32_t* __restrict__ lengths, int n_lists,
                                                                   int L, int width_rt, float* __restrict__ loss_out,
                                                                   float* __restrict__ dg_out) {
+    constexpr int LANES = 32 / LPW, IPL = 64 / LANES, NR = IPL / 2;
+    static_assert(IPL >= 2 && IPL % 2 == 0, "two 16-bit keys per register");
     const int width = W > 0 ? W : width_rt;
     constexpr float LOG2E = 1.4426950408889634f, LN2 = 0.6931471805599453f;
-    __shared__ float sg[8][2][64];  // per warp, per half: the list's scores (base-2 units)
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, half = lane >> 4, hl = lane & 15;
+    __shared__ float sg[8][LPW][64];  // per warp, per list: the scores (base-2 units)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane / LANES, hl = lane % LANES;
     const int warps_total = gridDim.x * (blockDim.x >> 5);
     const float inv = 1.0f / (float)L;
     const bool vec = (L & 3) == 0;
-    for (int pair = blockIdx.x * (blockDim.x >> 5) + wid; 2 * pair < n_lists; pair += warps_total) {
-        const int list = 2 * pair + half;
+    for (int grp = blockIdx.x * (blockDim.x >> 5) + wid; LPW * grp < n_lists; grp += warps_total) {
+        const int list = LPW * grp + sub;
         const bool live = list < n_lists;
-        // load 4 items per lane: item i = 4 hl + e
-        float gv[4];
-        int nv[4];
+        float gv[IPL];
+        int nv[IPL];
         const float* g = gnet + (size_t)list * L;
         const int32_t* len = lengths + (size_t)list * L;
-        if (live && vec && 4 * hl < L) {
-            const float4 g4 = __ldcs(reinterpret_cast<const float4*>(g) + hl);
-            const int4 n4 = __ldcs(reinterpret_cast<const int4*>(len) + hl);
-            gv[0] = g4.x; gv[1] = g4.y; gv[2] = g4.z; gv[3] = g4.w;
-            nv[0] = n4.x; nv[1] = n4.y; nv[2] = n4.z; nv[3] = n4.w;
+        if (live && vec && IPL * hl < L) {
+#pragma unroll
+            for (int q = 0; q < IPL / 4; ++q) {
+                const float4 g4 = __ldcs(reinterpret_cast<const float4*>(g + IPL * hl) + q);
+                const int4 n4 = __ldcs(reinterpret_cast<const int4*>(len + IPL * hl) + q);
+                gv[4 * q] = g4.x; gv[4 * q + 1] = g4.y; gv[4 * q + 2] = g4.z; gv[4 * q + 3] = g4.w;
+                nv[4 * q] = n4.x; nv[4 * q + 1] = n4.y; nv[4 * q + 2] = n4.z; nv[4 * q + 3] = n4.w;
+            }
         } else {
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int i = 4 * hl + e;
+            for (int e = 0; e < IPL; ++e) {
+                const int i = IPL * hl + e;
                 gv[e] = (live && i < L) ? __ldcs(g + i) : 0.f;
                 nv[e] = (live && i < L) ? __ldcs(len + i) : 0;
             }
         }
         bool ok = true;
-        uint32_t key[4];
+        uint32_t R[NR];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int i = 4 * hl + e;
+        for (int e = 0; e < IPL; ++e) {
+            const int i = IPL * hl + e;
             int lab = nv[e] / width;
             if (nv[e] < 0 && lab * width != nv[e]) --lab;  // floor division
             const bool valid = live && i < L;
             ok &= !valid || (lab >= 0 && lab < 1023);
-            key[e] = valid ? (((uint32_t)lab << 6) | (uint32_t)i) : 0xFFFFu;
-            sg[wid][half][i] = gv[e] * LOG2E;
+            const uint32_t key = valid ? (((uint32_t)lab << 6) | (uint32_t)i) : 0xFFFFu;
+            if (e & 1) R[e >> 1] |= key << 16; else R[e >> 1] = key;
+            sg[wid][sub][i] = gv[e] * LOG2E;
         }
-        // bitonic sort of 64 16-bit keys per half: R0 = (p1 | p0), R1 = (p3 | p2)
-        uint32_t R0 = key[0] | (key[1] << 16), R1 = key[2] | (key[3] << 16);
         if (__all_sync(0xffffffffu, ok)) {
 #pragma unroll
             for (int k = 2; k <= 64; k <<= 1) {
 #pragma unroll
                 for (int j = k >> 1; j > 0; j >>= 1) {
-                    if (j == 1) {
-                        // halves of a register: element p = 4 hl + 2 r + h, asc = (p & k) == 0
-                        const bool a0 = k == 2 ? true : ((4 * hl) & k) == 0;
-                        const bool a1 = k == 2 ? false : a0;
-                        uint32_t Q = __byte_perm(R0, 0, 0x1032);
-                        uint32_t mn = vmin16x2(R0, Q), mx = vmax16x2(R0, Q);
-                        R0 = __byte_perm(a0 ? mn : mx, a0 ? mx : mn, 0x7610);
-                        Q = __byte_perm(R1, 0, 0x1032);
-                        mn = vmin16x2(R1, Q);
-                        mx = vmax16x2(R1, Q);
-                        R1 = __byte_perm(a1 ? mn : mx, a1 ? mx : mn, 0x7610);
-                    } else if (j == 2) {
-                        // R0 vs R1 of the same lane (R0 holds the lower positions)
-                        const bool asc = ((4 * hl) & k) == 0;
-                        const uint32_t mn = vmin16x2(R0, R1), mx = vmax16x2(R0, R1);
-                        R0 = asc ? mn : mx;
-                        R1 = asc ? mx : mn;
-                    } else {
-                        const int lm = j >> 2;  // partner lane within the half
-                        const bool asc = ((4 * hl) & k) == 0;
+                    if (j == 1) {  // the two halves of each register
+#pragma unroll
+                        for (int ri = 0; ri < NR; ++ri) {
+                            const bool asc = ((IPL * hl + 2 * ri) & k) == 0;
+                            const uint32_t Q = __byte_perm(R[ri], 0, 0x1032);
+                            const uint32_t mn = vmin16x2(R[ri], Q), mx = vmax16x2(R[ri], Q);
+                            R[ri] = __byte_perm(asc ? mn : mx, asc ? mx : mn, 0x7610);
+                        }
+                    } else if (j < IPL) {  // two registers of the same lane
+#pragma unroll
+                        for (int ri = 0; ri < NR; ++ri) {
+                            const int rp = ri ^ (j >> 1);
+                            if (rp < ri) continue;
+                            const bool asc = ((IPL * hl + 2 * ri) & k) == 0;
+                            const uint32_t mn = vmin16x2(R[ri], R[rp]), mx = vmax16x2(R[ri], R[rp]);
+                            R[ri] = asc ? mn : mx;
+                            R[rp] = asc ? mx : mn;
+                        }
+                    } else {  // lanes hl and hl ^ (j / IPL) of the group
+                        const int lm = j / IPL;
+                        const bool asc = ((IPL * hl) & k) == 0;
                         const bool take_min = ((hl & lm) == 0) == asc;
-                        const uint32_t O0 = __shfl_xor_sync(0xffffffffu, R0, lm);
-                        const uint32_t O1 = __shfl_xor_sync(0xffffffffu, R1, lm);
-                        R0 = take_min ? vmin16x2(O0, R0) : vmax16x2(O0, R0);
-                        R1 = take_min ? vmin16x2(O1, R1) : vmax16x2(O1, R1);
+#pragma unroll
+                        for (int ri = 0; ri < NR; ++ri) {
+                            const uint32_t O = __shfl_xor_sync(0xffffffffu, R[ri], lm);
+                            R[ri] = take_min ? vmin16x2(O, R[ri]) : vmax16x2(O, R[ri]);
+                        }
                     }
                 }
             }
         }
         __syncwarp();
-        int s[4] = {(int)(R0 & 63), (int)((R0 >> 16) & 63), (int)(R1 & 63), (int)((R1 >> 16) & 63)};
-        float t[4];
-        bool v[4];
+        int sidx[IPL];
+        float t[IPL];
+        bool v[IPL];
         float M = LSE2_NONE, mneg = LSE2_NONE;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            v[e] = live && 4 * hl + e < L;
-            t[e] = v[e] ? sg[wid][half][s[e]] : LSE2_NONE;
+        for (int e = 0; e < IPL; ++e) {
+            sidx[e] = (int)((R[e >> 1] >> (16 * (e & 1))) & 63);
+            v[e] = live && IPL * hl + e < L;
+            t[e] = v[e] ? sg[wid][sub][sidx[e]] : LSE2_NONE;
             M = fmaxf(M, v[e] ? t[e] : LSE2_NONE);
             mneg = fmaxf(mneg, v[e] ? -t[e] : LSE2_NONE);
         }
 #pragma unroll
-        for (int o = 8; o; o >>= 1) {
+        for (int o = LANES / 2; o; o >>= 1) {
             M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
             mneg = fmaxf(mneg, __shfl_xor_sync(0xffffffffu, mneg, o));
         }
         const bool fast = !live || (M + mneg <= 100.f);
         if (!__all_sync(0xffffffffu, ok && fast)) {
             __syncwarp();
-            for (int h = 0; h < 2; ++h)
-                if (2 * pair + h < n_lists) listmle64_one(gnet, lengths, 2 * pair + h, L, width, loss_out, dg_out);
+            for (int h = 0; h < LPW; ++h)
+                if (LPW * grp + h < n_lists) listmle64_one(gnet, lengths, LPW * grp + h, L, width, loss_out, dg_out);
             continue;
         }
         // suffix sums of 2^(t - M): lse_p = M + log2(sum_{q >= p})
-        float w[4], sfx[4];
+        float w[IPL], sfx[IPL];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) w[e] = v[e] ? fast_ex2(t[e] - M) : 0.f;
-        sfx[3] = w[3];
-        sfx[2] = w[2] + sfx[3];
-        sfx[1] = w[1] + sfx[2];
-        sfx[0] = w[0] + sfx[1];
+        for (int e = 0; e < IPL; ++e) w[e] = v[e] ? fast_ex2(t[e] - M) : 0.f;
+        sfx[IPL - 1] = w[IPL - 1];
+#pragma unroll
+        for (int e = IPL - 2; e >= 0; --e) sfx[e] = w[e] + sfx[e + 1];
         float x = sfx[0];
 #pragma unroll
-        for (int o = 1; o < 16; o <<= 1) {
+        for (int o = 1; o < LANES; o <<= 1) {
             const float y = __shfl_down_sync(0xffffffffu, x, o);
-            if (hl + o < 16) x += y;
+            if (hl + o < LANES) x += y;
         }
         float tail = __shfl_down_sync(0xffffffffu, x, 1);
-        if (hl == 15) tail = 0.f;
-        float lse[4], part = 0.f;
+        if (hl == LANES - 1) tail = 0.f;
+        float lse[IPL], part = 0.f;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < IPL; ++e) {
             lse[e] = M + fast_lg2(sfx[e] + tail);
             part += v[e] ? lse[e] - t[e] : 0.f;
         }
 #pragma unroll
-        for (int o = 8; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        for (int o = LANES / 2; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
         // prefix sums of 2^(-lse - Mu), Mu = -lse of the last item (lse_{L-1} = t_{L-1})
-        const int lastl = (L - 1) >> 2, laste = (L - 1) & 3;
-        const float lastv = laste == 0 ? lse[0] : laste == 1 ? lse[1] : laste == 2 ? lse[2] : lse[3];
-        const float Mu = -__shfl_sync(0xffffffffu, lastv, half * 16 + lastl);
-        float c[4];
+        const int lastl = (L - 1) / IPL, laste = (L - 1) % IPL;
+        float lastv = lse[0];
+#pragma unroll
+        for (int e = 1; e < IPL; ++e)
+            if (e == laste) lastv = lse[e];
+        const float Mu = -__shfl_sync(0xffffffffu, lastv, sub * LANES + lastl);
+        float c[IPL];
         float acc = 0.f;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int e = 0; e < IPL; ++e) {
             acc += v[e] ? fast_ex2(-lse[e] - Mu) : 0.f;
             c[e] = acc;
         }
         x = acc;
 #pragma unroll
-        for (int o = 1; o < 16; o <<= 1) {
+        for (int o = 1; o < LANES; o <<= 1) {
             const float y = __shfl_up_sync(0xffffffffu, x, o);
             if (hl >= o) x += y;
         }
@@ -569,10 +578,10 @@ __global__ void __launch_bounds__(256) listmle_lengths64x2_kernel(const float* _
         if (hl == 0) head = 0.f;
         float* dg = dg_out + (size_t)list * L;
 #pragma unroll
-        for (int e = 0; e < 4; ++e)
-            if (v[e]) dg[s[e]] = (fast_ex2(t[e] + Mu + fast_lg2(head + c[e])) - 1.f) * inv;
+        for (int e = 0; e < IPL; ++e)
+            if (v[e]) dg[sidx[e]] = (fast_ex2(t[e] + Mu + fast_lg2(head + c[e])) - 1.f) * inv;
         if (live && hl == 0) loss_out[list] = part * LN2 * inv;
-        __syncwarp();  // sg is reused by the next pair
+        __syncwarp();  // sg is reused by the next group
     }
 }
 
@@ -623,12 +632,13 @@ extern "C" int rs_listmle_lengths(const float* g, const int32_t* lengths, int32_
             RS_CUDA(cudaGetDevice(&dev));
             RS_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
         }
-        const int pairs = (n_lists + 1) / 2;
-        const int blocks = (pairs + 7) / 8 < n_sm * 8 ? (pairs + 7) / 8 : n_sm * 8;
+        constexpr int LPW = 4;
+        const int groups = (n_lists + LPW - 1) / LPW;
+        const int blocks = (groups + 7) / 8 < n_sm * 8 ? (groups + 7) / 8 : n_sm * 8;
         if (width == 10)
-            listmle_lengths64x2_kernel<10><<<blocks, 256, 0, st>>>(g, lengths, n_lists, L, width, loss, dg);
+            listmle_lengths64xN_kernel<LPW, 10><<<blocks, 256, 0, st>>>(g, lengths, n_lists, L, width, loss, dg);
         else
-            listmle_lengths64x2_kernel<0><<<blocks, 256, 0, st>>>(g, lengths, n_lists, L, width, loss, dg);
+            listmle_lengths64xN_kernel<LPW, 0><<<blocks, 256, 0, st>>>(g, lengths, n_lists, L, width, loss, dg);
         RS_LAUNCH_CHECK();
         return RS_OK;
     }
