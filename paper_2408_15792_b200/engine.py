@@ -210,15 +210,23 @@ class DeviceEngine:
         ws = wn = None
         now, nxt, n_alive, step, n_finished = 0, 0, 0, 0, 0
         dev_now = None  # the device copy of the clock (out[0]) when known to equal `now`
+        # loop-invariant values and bound methods, hoisted (the loop runs ~10^5 times)
+        arr_list = self.arrival_ns.tolist()
+        pred_ns_per_req = self.cost.predictor_ns_per_request if self.charges_predictor else 0
+        max_batch, threshold, quantum = sched.max_batch, sched.starvation_threshold, sched.priority_quantum
+        calibrated, preemptive = int(self.length_calibrated), int(sched.preemption)
+        stat_host_copy, stat_dev, sync = self.stat_host.copy_, self.stat, stream.synchronize
         tot_prefill = tot_decode = tot_pred = 0
         dropped_all: list[int] = []
         records = []
         while True:
-            if n_alive == 0 and nxt < n and self.arrival_ns[nxt] > now:  # jump_if_idle
-                now = int(self.arrival_ns[nxt])
+            if n_alive == 0 and nxt < n and arr_list[nxt] > now:  # jump_if_idle
+                now = arr_list[nxt]
             # admit_due: the arrivals up to `now`; requests that could never hold their
             # full context in the KV budget are dropped (engine.py:224-243)
-            end = int(np.searchsorted(self.arrival_ns, now, side="right"))
+            end = nxt  # arrivals are sorted and few per step: walk instead of bisecting
+            while end < n and arr_list[end] <= now:
+                end += 1
             admitted = dropped = None
             k = 0
             if end > nxt:
@@ -239,14 +247,15 @@ class DeviceEngine:
                 break
             if limit_ns is not None and now >= limit_ns:
                 break
-            predictor_ns = k * self.cost.predictor_ns_per_request if self.charges_predictor else 0
+            predictor_ns = k * pred_ns_per_req
             if n_alive > ws_n:
                 ws_n = max(n_alive, 2 * ws_n)
                 ws, wn = _lib.workspace.get(lib.rs_rank_step_workspace_size(ws_n), self.dev)
             soas[cur].n = n_alive
-            check(rank_step(soa_refs[cur], sched.max_batch, budget, sched.starvation_threshold, sched.priority_quantum,
-                            int(self.length_calibrated), int(sched.preemption), run_p, prom_p, dem_p, cnt_p, ws, wn,
-                            st), "rs_rank_step")
+            rc = rank_step(soa_refs[cur], max_batch, budget, threshold, quantum, calibrated, preemptive, run_p, prom_p,
+                           dem_p, cnt_p, ws, wn, st)
+            if rc:
+                check(rc, "rs_rank_step")
             if now != dev_now:  # the clock moved on the host (idle jump / first step)
                 out_np[0] = now
                 self.out[:1].copy_(self.out_host[:1], non_blocking=True)
@@ -256,11 +265,13 @@ class DeviceEngine:
                 check(execute(q_refs[0], tr_ref, cost_ref, run_p, cnt_p, step, predictor_ns, out_p, pre_p, fin_p, st),
                       "rs_engine_execute")
             else:
-                check(execute_ex(q_refs[cur], q_refs[1 - cur], tr_ref, cost_ref, run_p, cnt_p, step, predictor_ns,
-                                 out_p, pre_p, fin_p, scratch_p, st), "rs_engine_execute_ex")
+                rc = execute_ex(q_refs[cur], q_refs[1 - cur], tr_ref, cost_ref, run_p, cnt_p, step, predictor_ns,
+                                out_p, pre_p, fin_p, scratch_p, st)
+                if rc:
+                    check(rc, "rs_engine_execute_ex")
                 cur = 1 - cur
-            self.stat_host.copy_(self.stat, non_blocking=True)
-            stream.synchronize()
+            stat_host_copy(stat_dev, non_blocking=True)
+            sync()
             if cnt_np[3]:
                 raise ValueError("ranking policy: NaN effective score")
             now, iter_ns, prefill_ns, n_alive = int(out_np[0]), int(out_np[1]), int(out_np[2]), int(out_np[3])
