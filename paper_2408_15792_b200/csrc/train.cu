@@ -136,13 +136,25 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ d
 // Column sums of a [rows, cols] matrix (float or bf16) into per-block partial rows.
 template <typename T>
 __global__ void colsum_partial_kernel(const T* __restrict__ x, int rows, int cols, float* __restrict__ part) {
-    const int c = blockIdx.y * blockDim.x + threadIdx.x;
+    // VEC adjacent columns per thread through one 16-byte load per row (cols % VEC == 0);
+    // rows summed in order, so the result is the same as one column per thread
+    constexpr int VEC = 16 / sizeof(T);
+    const int c = (blockIdx.y * blockDim.x + threadIdx.x) * VEC;
     if (c >= cols) return;
     const int r0 = blockIdx.x * TR_ROWS_PER_BLOCK;
     const int r1 = min(rows, r0 + TR_ROWS_PER_BLOCK);
-    float acc = 0.f;
-    for (int r = r0; r < r1; ++r) acc += (float)x[(size_t)r * cols + c];
-    part[(size_t)blockIdx.x * cols + c] = acc;
+    float acc[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) acc[k] = 0.f;
+#pragma unroll 4
+    for (int r = r0; r < r1; ++r) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(x + (size_t)r * cols + c));
+        const T* vals = reinterpret_cast<const T*>(&u);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) acc[k] += (float)vals[k];
+    }
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) part[(size_t)blockIdx.x * cols + c + k] = acc[k];
 }
 
 // out[c] += sum over n_part partial rows (fixed order).
@@ -330,7 +342,9 @@ int ln_backward(const float* dy, const float* x, const void* w, float* dh, void*
 
 int colsum_add(const void* x, bool is_bf16, int rows, int cols, float* part, float* out, cudaStream_t st) {
     const int nblk = (rows + TR_ROWS_PER_BLOCK - 1) / TR_ROWS_PER_BLOCK;
-    dim3 grid(nblk, (cols + 255) / 256);
+    RS_CHECK_ARG(cols % 8 == 0, "colsum_add: cols %% 8 != 0");
+    const int vec = is_bf16 ? 8 : 4;
+    dim3 grid(nblk, (cols / vec + 255) / 256);
     if (is_bf16)
         colsum_partial_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), rows, cols,
                                                                      part);
