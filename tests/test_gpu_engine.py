@@ -106,3 +106,38 @@ def test_engine_matches_reference_at_cfg5_scale():
     assert hashlib.sha256(_canonical(res.requests).encode()).hexdigest() == c["rows_sha256"]
     for k, v in c["metrics"].items():
         assert res.metrics[k] == v, (k, res.metrics[k], v)
+
+
+class _OracleScores:
+    """The reference's OracleScorer (predictors.py:53-60): score = true output length,
+    length calibrated, no predictor charge."""
+
+    kind = "oracle"
+    length_calibrated = True
+    charges_predictor = False
+
+    def score_batch(self, requests, seed):
+        return [float(r.true_output_tokens) for r in requests]
+
+
+def test_oracle_ranking_reproduces_reference_srtf():
+    """Acceptance criterion 5 (test_acceptance.py:173-197) across implementations: the
+    device engine's ranking policy with oracle scores reproduces the reference's own
+    SRTF decisions (now / iter / run / preempted / promoted / demoted / admitted /
+    dropped / finished, every step) and metrics on its 100 random traces."""
+    import pathlib
+    from paper_2408_15792_b200 import engine
+    from paper_2408_15792_b200.schedulers import SchedulerConfig
+    from paper_2408_15792_b200.workload import Request
+    g = json.loads((pathlib.Path(__file__).resolve().parent / "golden" / "srtf_golden.json").read_text())
+    fields = g["fields"]
+    for i, c in enumerate(g["cases"]):
+        reqs = [Request(id=r, arrival_time=a, prompt_tokens=p, true_output_tokens=o) for r, a, p, o in c["requests"]]
+        res = engine.run(reqs, scorer=_OracleScores(), sched=SchedulerConfig(max_batch=c["max_batch"],
+                                                                            starvation_threshold=0),
+                         kv_budget=c["kv_budget"], cost=engine.COST_PRESETS["fast"], record=True)
+        dec = [{f: rec[f] for f in fields} for rec in res.records]
+        assert len(dec) == c["n_steps"], i
+        assert hashlib.sha256(_canonical(dec).encode()).hexdigest() == c["decisions_sha256"], i
+        for k, v in c["metrics"].items():
+            assert res.metrics[k] == v, (i, k, res.metrics[k], v)
