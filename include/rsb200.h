@@ -176,11 +176,53 @@ int rs_engine_execute(const rs_engine_queue* q, const rs_engine_trace* tr, const
 /* Same step with the surviving rows compacted out of place into q_out's columns (same
  * capacity and score dtype; q_out->n is ignored) by many CTAs instead of in place by one —
  * the caller swaps the two column sets every step. scratch_dev: int32[ceil(n / 1024)].
- * q_out == NULL is rs_engine_execute. */
+ * prev_run_dev (int64[>= max_batch]) / prev_n_dev (int32[1], 0 before the first step), both
+ * or neither: the previous step's batch, kept by the call, so preemption only looks at
+ * those rows instead of scanning the queue. q_out == NULL is in-place compaction. */
 int rs_engine_execute_ex(const rs_engine_queue* q, const rs_engine_queue* q_out, const rs_engine_trace* tr,
                          const rs_engine_cost* cost, const int64_t* run_dev, const int32_t* counts_dev, int32_t step,
                          int64_t predictor_ns, int64_t* out_dev, int64_t* preempted_dev, int64_t* finished_dev,
-                         int32_t* scratch_dev, void* stream);
+                         int32_t* scratch_dev, int64_t* prev_run_dev, int32_t* prev_n_dev, void* stream);
+/* The whole engine loop natively (engine.py:382-460; records are not produced — use the
+ * per-step calls for that): q2 / soa2 = the two column sets (views of the same columns),
+ * starting in set 0 with no alive rows. Host arrays: arrival_ns[n] (sorted), fits[n]
+ * (uint8: prompt + true output <= KV budget), adm_host int32[n] (pinned), dropped_host
+ * int64[n] (receives the dropped request indices). Device: adm_dev int32[n], stat_dev
+ * int64[8] (out[6] | counts int32[4]) with its pinned host mirror stat_host, the
+ * rank-step / execute outputs and workspace sized for n rows. limit_ns / stop_after <
+ * 0: none. Returns RS_ERR_NAN on a NaN effective score. */
+typedef struct rs_engine_loop {
+    int64_t n_requests;
+    const int64_t* arrival_ns;
+    const uint8_t* fits;
+    int32_t* adm_host;
+    int32_t* adm_dev;
+    int64_t* dropped_host;
+    int64_t* stat_dev;
+    int64_t* stat_host;
+    int64_t* run_dev;
+    int64_t* prom_dev;
+    int64_t* dem_dev;
+    int64_t* pre_dev;
+    int64_t* fin_dev;
+    int32_t* scratch_dev;
+    int64_t* prev_run_dev;  /* int64[max_batch], prev_n_dev int32[1] = 0: see rs_engine_execute_ex */
+    int32_t* prev_n_dev;
+    void* ws;
+    size_t ws_bytes;
+    int32_t max_batch, starvation_threshold, priority_quantum, length_calibrated, preemptive;
+    int64_t kv_budget;                 /* < 0: unlimited */
+    int64_t predictor_ns_per_request;  /* 0 when the scorer is not charged */
+    int64_t limit_ns;
+    int64_t stop_after_finished;
+} rs_engine_loop;
+typedef struct rs_engine_loop_out {
+    int64_t now_ns, steps, n_finished, next_arrival, n_dropped;
+    int64_t total_prefill_ns, total_decode_ns, total_predictor_ns;
+    int32_t final_set;
+} rs_engine_loop_out;
+int rs_engine_run(const rs_engine_queue* q2, const rs_queue_soa* soa2, const rs_engine_trace* tr,
+                  const rs_engine_cost* cost, const rs_engine_loop* loop, rs_engine_loop_out* out, void* stream);
 
 /* ---- §8f #2: prompt strings -> token ids on the device ---------------------------
  * The scorer's id map (workload.prompt_token_ids; the reference's salted crc32 token

@@ -60,6 +60,22 @@ class EngineCost(ctypes.Structure):
                 ("decode_table_len", c_i32)]
 
 
+class EngineLoop(ctypes.Structure):
+    _fields_ = [("n_requests", c_i64), ("arrival_ns", c_vp), ("fits", c_vp), ("adm_host", c_vp), ("adm_dev", c_vp),
+                ("dropped_host", c_vp), ("stat_dev", c_vp), ("stat_host", c_vp), ("run_dev", c_vp),
+                ("prom_dev", c_vp), ("dem_dev", c_vp), ("pre_dev", c_vp), ("fin_dev", c_vp), ("scratch_dev", c_vp),
+                ("prev_run_dev", c_vp), ("prev_n_dev", c_vp), ("ws", c_vp), ("ws_bytes", c_sz), ("max_batch", c_i32), ("starvation_threshold", c_i32),
+                ("priority_quantum", c_i32), ("length_calibrated", c_i32), ("preemptive", c_i32),
+                ("kv_budget", c_i64), ("predictor_ns_per_request", c_i64), ("limit_ns", c_i64),
+                ("stop_after_finished", c_i64)]
+
+
+class EngineLoopOut(ctypes.Structure):
+    _fields_ = [("now_ns", c_i64), ("steps", c_i64), ("n_finished", c_i64), ("next_arrival", c_i64),
+                ("n_dropped", c_i64), ("total_prefill_ns", c_i64), ("total_decode_ns", c_i64),
+                ("total_predictor_ns", c_i64), ("final_set", c_i32)]
+
+
 # name -> (restype, argtypes); the list mirrors include/rsb200.h exactly and
 # tests/test_lib_exports.py checks every declared symbol is exported.
 SIGNATURES = {
@@ -79,8 +95,11 @@ SIGNATURES = {
                                          c_vp]),
     "rs_engine_execute_ex": (ctypes.c_int, [ctypes.POINTER(EngineQueue), ctypes.POINTER(EngineQueue),
                                             ctypes.POINTER(EngineTrace), ctypes.POINTER(EngineCost), c_vp, c_vp, c_i32,
-                                            c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
+                                            c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rs_tokenize": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, ctypes.c_uint32, c_vp, c_vp, c_vp, c_vp]),
+    "rs_engine_run": (ctypes.c_int, [ctypes.POINTER(EngineQueue), ctypes.POINTER(QueueSoA), ctypes.POINTER(EngineTrace),
+                                     ctypes.POINTER(EngineCost), ctypes.POINTER(EngineLoop),
+                                     ctypes.POINTER(EngineLoopOut), c_vp]),
     "rs_rank_step_workspace_size": (c_sz, [c_i64]),
     "rs_rank_step": (ctypes.c_int, [ctypes.POINTER(QueueSoA), c_i32, c_i64, c_i32, c_i32, c_i32, c_i32,
                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),

@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(EX_THREADS) engine_execute_kernel(rs_engine_qu
                                                                     const int32_t* __restrict__ counts, int32_t step,
                                                                     int64_t predictor_ns, int64_t* __restrict__ out,
                                                                     int64_t* __restrict__ preempted,
-                                                                    int64_t* __restrict__ finished) {
+                                                                    int64_t* __restrict__ finished,
+                                                                    int64_t* __restrict__ prev_run,
+                                                                    int32_t* __restrict__ prev_n) {
     __shared__ int warp_tot[32];
     __shared__ unsigned long long prefill_tokens;
     __shared__ int n_pre;
@@ -91,18 +93,28 @@ __global__ void __launch_bounds__(EX_THREADS) engine_execute_kernel(rs_engine_qu
     }
     for (int k = tid; k < n_run; k += EX_THREADS) tr.run_stamp[run[k]] = step;
     __syncthreads();
-    // 1a. preemption (engine.py:248-256): RUNNING rows left out of the batch
-    for (int64_t row = tid; row < n; row += EX_THREADS) {
+    // 1a. preemption (engine.py:248-256): RUNNING rows left out of the batch. RUNNING is
+    // set only on the rows of a step's batch and cleared when they are left out, so with
+    // the previous batch at hand (prev_run) only those rows need looking at; else scan.
+    auto preempt_row = [&](int64_t row, int64_t id) {
         const uint8_t fl = q.flags[row];
-        if (fl & RS_FLAG_RUNNING) {
-            const int64_t id = q.id[row];
-            if (tr.run_stamp[id] != step) {
-                q.flags[row] = (uint8_t)((fl & ~RS_FLAG_RUNNING) | EX_PRE);
-                tr.n_preempted[id] += 1;
-                const int slot = atomicAdd(&n_pre, 1);
-                if (slot < EX_PRE_CAP) pre_rows[slot] = (int)row;
-            }
+        if ((fl & RS_FLAG_RUNNING) && tr.run_stamp[id] != step) {
+            q.flags[row] = (uint8_t)((fl & ~RS_FLAG_RUNNING) | EX_PRE);
+            tr.n_preempted[id] += 1;
+            const int slot = atomicAdd(&n_pre, 1);
+            if (slot < EX_PRE_CAP) pre_rows[slot] = (int)row;
         }
+    };
+    if (prev_run) {
+        const int pn = *prev_n;
+        for (int i = tid; i < pn; i += EX_THREADS) {
+            const int64_t id = prev_run[i];
+            if (tr.finish_ns[id] >= 0) continue;  // finished last step: already retired
+            preempt_row(tr.row_of[id], id);
+        }
+    } else {
+        for (int64_t row = tid; row < n; row += EX_THREADS)
+            if (q.flags[row] & RS_FLAG_RUNNING) preempt_row(row, q.id[row]);
     }
     __syncthreads();
     const int total_pre = n_pre;
@@ -205,6 +217,10 @@ __global__ void __launch_bounds__(EX_THREADS) engine_execute_kernel(rs_engine_qu
     }
     __syncthreads();
     if (tid == 0) out[5] = done_before;
+    if (prev_run) {  // this batch is the next step's RUNNING set
+        for (int k = tid; k < n_run; k += EX_THREADS) prev_run[k] = run[k];
+        if (tid == 0) *prev_n = n_run;
+    }
     if (!InPlace) return;
     // 4. stable in-place compaction of the rows still alive
     int64_t kept = 0;
@@ -320,21 +336,24 @@ extern "C" int rs_engine_execute_ex(const rs_engine_queue* q, const rs_engine_qu
                                     const rs_engine_trace* tr, const rs_engine_cost* cost, const int64_t* run_dev,
                                     const int32_t* counts_dev, int32_t step, int64_t predictor_ns, int64_t* out_dev,
                                     int64_t* preempted_dev, int64_t* finished_dev, int32_t* scratch_dev,
-                                    void* stream) {
+                                    int64_t* prev_run_dev, int32_t* prev_n_dev, void* stream) {
     RS_CHECK_ARG(q && tr && cost && run_dev && counts_dev && out_dev && preempted_dev && finished_dev,
                  "rs_engine_execute: NULL argument");
     RS_CHECK_ARG(cost->decode_table_len == 0 || cost->decode_table != nullptr, "rs_engine_execute: decode table");
     RS_CHECK_ARG(q_out == nullptr || (scratch_dev != nullptr && q_out->score_dtype == q->score_dtype),
                  "rs_engine_execute_ex: out-of-place compaction needs scratch and a matching q_out");
+    RS_CHECK_ARG((prev_run_dev == nullptr) == (prev_n_dev == nullptr), "rs_engine_execute_ex: prev_run / prev_n");
     cudaStream_t st = as_stream(stream);
     if (q_out == nullptr) {
         engine_execute_kernel<true><<<1, EX_THREADS, 0, st>>>(*q, *tr, *cost, run_dev, counts_dev, step, predictor_ns,
-                                                               out_dev, preempted_dev, finished_dev);
+                                                               out_dev, preempted_dev, finished_dev, prev_run_dev,
+                                                               prev_n_dev);
         RS_LAUNCH_CHECK();
         return RS_OK;
     }
     engine_execute_kernel<false><<<1, EX_THREADS, 0, st>>>(*q, *tr, *cost, run_dev, counts_dev, step, predictor_ns,
-                                                            out_dev, preempted_dev, finished_dev);
+                                                            out_dev, preempted_dev, finished_dev, prev_run_dev,
+                                                            prev_n_dev);
     RS_LAUNCH_CHECK();
     const int64_t nb64 = (q->n + EX_THREADS - 1) / EX_THREADS;
     const unsigned nb = nb64 > 0 ? (unsigned)nb64 : 1u;
@@ -350,5 +369,98 @@ extern "C" int rs_engine_execute(const rs_engine_queue* q, const rs_engine_trace
                                  int64_t predictor_ns, int64_t* out_dev, int64_t* preempted_dev,
                                  int64_t* finished_dev, void* stream) {
     return rs_engine_execute_ex(q, nullptr, tr, cost, run_dev, counts_dev, step, predictor_ns, out_dev, preempted_dev,
-                                finished_dev, nullptr, stream);
+                                finished_dev, nullptr, nullptr, nullptr, stream);
+}
+
+// ---- the engine loop itself, natively (record-free runs) ------------------------------
+// engine.py:382-460 as DeviceEngine.run drives it from Python, step for step: idle jump,
+// admission of the arrivals up to `now` (dropping requests whose full context can never
+// fit the KV budget), rank step, execute with out-of-place compaction into the other
+// column set, one 64-byte status read-back per step. The C++ loop saves the Python
+// interpreter's share of every step; the decisions are identical by construction (same
+// kernels, same order), which tests/test_gpu_engine.py checks against the reference.
+extern "C" int rs_engine_run(const rs_engine_queue* q2, const rs_queue_soa* soa2, const rs_engine_trace* tr,
+                             const rs_engine_cost* cost, const rs_engine_loop* lp, rs_engine_loop_out* res,
+                             void* stream) {
+    RS_CHECK_ARG(q2 && soa2 && tr && cost && lp && res, "rs_engine_run: NULL argument");
+    RS_CHECK_ARG(lp->arrival_ns && lp->fits && lp->adm_host && lp->adm_dev && lp->stat_dev && lp->stat_host &&
+                     lp->run_dev && lp->prom_dev && lp->dem_dev && lp->pre_dev && lp->fin_dev && lp->scratch_dev &&
+                     lp->dropped_host,
+                 "rs_engine_run: NULL buffer");
+    cudaStream_t st = as_stream(stream);
+    rs_engine_queue q[2] = {q2[0], q2[1]};
+    rs_queue_soa soa[2] = {soa2[0], soa2[1]};
+    int64_t* out = lp->stat_dev;                                    // int64[6]
+    int32_t* counts = reinterpret_cast<int32_t*>(lp->stat_dev + 6);  // int32[4]
+    const int64_t* hout = lp->stat_host;
+    const int32_t* hcnt = reinterpret_cast<const int32_t*>(lp->stat_host + 6);
+    const int64_t n = lp->n_requests;
+    int64_t now = 0, nxt = 0, n_alive = 0, step = 0, n_fin = 0, n_drop = 0, dev_now = -1;
+    int64_t tot_prefill = 0, tot_decode = 0, tot_pred = 0;
+    bool have_dev_now = false;
+    int cur = 0;
+    int status = RS_OK;
+    while (true) {
+        if (n_alive == 0 && nxt < n && lp->arrival_ns[nxt] > now) now = lp->arrival_ns[nxt];  // jump_if_idle
+        int64_t end = nxt;
+        while (end < n && lp->arrival_ns[end] <= now) ++end;
+        int32_t k = 0;
+        for (int64_t i = nxt; i < end; ++i) {
+            if (lp->fits[i])
+                lp->adm_host[k++] = (int32_t)i;
+            else
+                lp->dropped_host[n_drop++] = i;
+        }
+        nxt = end;
+        if (k) {
+            RS_CUDA(cudaMemcpyAsync(lp->adm_dev, lp->adm_host, (size_t)k * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+            q[cur].n = n_alive;
+            RS_TRY(rs_engine_admit(&q[cur], tr, lp->adm_dev, k, n_alive, st));
+            n_alive += k;
+        }
+        if (n_alive == 0) break;
+        if (lp->limit_ns >= 0 && now >= lp->limit_ns) break;
+        const int64_t pred = (int64_t)k * lp->predictor_ns_per_request;
+        soa[cur].n = n_alive;
+        RS_TRY(rs_rank_step(&soa[cur], lp->max_batch, lp->kv_budget, lp->starvation_threshold, lp->priority_quantum,
+                            lp->length_calibrated, lp->preemptive, lp->run_dev, lp->prom_dev, lp->dem_dev, counts,
+                            lp->ws, lp->ws_bytes, st));
+        if (!have_dev_now || now != dev_now) {  // the clock moved on the host (idle jump / first step)
+            lp->stat_host[0] = now;
+            RS_CUDA(cudaMemcpyAsync(out, lp->stat_host, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        }
+        q[cur].n = n_alive;
+        RS_TRY(rs_engine_execute_ex(&q[cur], &q[1 - cur], tr, cost, lp->run_dev, counts, (int32_t)step, pred, out,
+                                    lp->pre_dev, lp->fin_dev, lp->scratch_dev, lp->prev_run_dev, lp->prev_n_dev, st));
+        cur = 1 - cur;
+        RS_CUDA(cudaMemcpyAsync(lp->stat_host, lp->stat_dev, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaStreamSynchronize(st));
+        if (hcnt[3]) {
+            set_error("ranking policy: NaN effective score");
+            status = RS_ERR_NAN;
+            break;
+        }
+        const int64_t iter = hout[1], prefill = hout[2];
+        now = hout[0];
+        n_alive = hout[3];
+        dev_now = now;
+        have_dev_now = true;
+        n_fin += hout[5];
+        tot_prefill += prefill;
+        tot_pred += pred;
+        tot_decode += iter - prefill - pred;
+        ++step;
+        if (lp->stop_after_finished >= 0 && n_fin >= lp->stop_after_finished) break;
+        if (lp->limit_ns >= 0 && now >= lp->limit_ns) break;
+    }
+    res->now_ns = now;
+    res->steps = step;
+    res->n_finished = n_fin;
+    res->next_arrival = nxt;
+    res->n_dropped = n_drop;
+    res->total_prefill_ns = tot_prefill;
+    res->total_decode_ns = tot_decode;
+    res->total_predictor_ns = tot_pred;
+    res->final_set = cur;
+    return status;
 }

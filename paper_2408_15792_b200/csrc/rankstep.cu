@@ -136,6 +136,10 @@ __global__ void fill_budget(const uint32_t* __restrict__ order, const int32_t* _
 constexpr int SEL_BITS = 11, SEL_BINS = 1 << SEL_BITS, SEL_LEVELS = 9;  // 99 >= 96 bits
 constexpr int SEL_CAP = 2048;
 constexpr int SEL_SORT = 4096;  // >= max_batch + SEL_CAP, power of two
+// Below this many rows the full merge sort (a block-sort launch + log2(n / 2048) pass
+// launches) beats the select's SEL_LEVELS histogram launches + gather + final sort: the
+// engine loop's queues (10^3-10^5 rows) are all below it, cfg4's 1M queue is above.
+constexpr uint32_t SEL_MIN_N = 1u << 18;
 constexpr int SEL_THREADS = 1024;
 
 struct SelState {
@@ -600,9 +604,8 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
     build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
     RS_LAUNCH_CHECK();
     const uint32_t k = min(n, (uint32_t)max_batch);
-    if (kv_budget < 0 && n > (uint32_t)MS_SMALL_MAX && k + SEL_CAP <= (uint32_t)SEL_SORT) {
-        // top-k select (see sel_hist): <= SEL_LEVELS histogram passes, most no-ops. Queues
-        // of <= MS_SMALL_MAX rows take the one-kernel full sort below instead.
+    if (kv_budget < 0 && n > SEL_MIN_N && k + SEL_CAP <= (uint32_t)SEL_SORT) {
+        // top-k select (see sel_hist): <= SEL_LEVELS histogram passes, most no-ops
         static bool attr = false;
         const size_t smem = SEL_SORT * (sizeof(RankKey) + sizeof(uint32_t));
         if (!attr) {

@@ -144,6 +144,9 @@ class DeviceEngine:
                 "rank": torch.zeros(cap, dtype=i32, device=d), "id": torch.zeros(cap, dtype=i64, device=d),
                 "starv": torch.zeros(cap, dtype=i32, device=d), "quant": torch.zeros(cap, dtype=i32, device=d)})
         self.compact_scratch = torch.zeros((cap + 1023) // 1024 + 1, dtype=i32, device=d)
+        # the previous step's batch (rs_engine_execute_ex's prev_run / prev_n)
+        self.prev_run = torch.zeros(max(sched.max_batch, 1), dtype=i64, device=d)
+        self.prev_n = torch.zeros(1, dtype=i32, device=d)
         self.run_out = torch.empty(max(sched.max_batch, 1), dtype=i64, device=d)
         self.prom_out = torch.empty(cap, dtype=i64, device=d)
         self.dem_out = torch.empty(cap, dtype=i64, device=d)
@@ -181,7 +184,11 @@ class DeviceEngine:
         return _lib.QueueSoA(n_alive, _lib.RS_F64, *self._cols(self._sets[which]))
 
     def run(self, record: bool = False, stop_after_finished: int | None = None,
-            time_limit_s: float | None = None) -> EngineResult:
+            time_limit_s: float | None = None, native: bool = True) -> EngineResult:
+        """record=False (and native) runs the whole loop in C++ (rs_engine_run); record=True
+        steps from Python so every step's decision can be read back."""
+        if native and not record and not self.in_place:
+            return self._run_native(stop_after_finished, time_limit_s)
         lib = _lib.load()
         rank_step, execute, admit, check = lib.rs_rank_step, lib.rs_engine_execute, lib.rs_engine_admit, _lib.check
         st = _lib.stream_handle(self.dev)
@@ -199,6 +206,8 @@ class DeviceEngine:
         tr_ref, cost_ref = ctypes.byref(self._trace), ctypes.byref(self._cost)
         execute_ex = lib.rs_engine_execute_ex
         scratch_p = self.compact_scratch.data_ptr()
+        self.prev_n.zero_()
+        prev_run_p, prev_n_p = self.prev_run.data_ptr(), self.prev_n.data_ptr()
         cur = 0
         run_p, prom_p, dem_p, cnt_p = (self.run_out.data_ptr(), self.prom_out.data_ptr(), self.dem_out.data_ptr(),
                                        self.counts.data_ptr())
@@ -266,7 +275,7 @@ class DeviceEngine:
                       "rs_engine_execute")
             else:
                 rc = execute_ex(q_refs[cur], q_refs[1 - cur], tr_ref, cost_ref, run_p, cnt_p, step, predictor_ns,
-                                out_p, pre_p, fin_p, scratch_p, st)
+                                out_p, pre_p, fin_p, scratch_p, prev_run_p, prev_n_p, st)
                 if rc:
                     check(rc, "rs_engine_execute_ex")
                 cur = 1 - cur
@@ -302,6 +311,40 @@ class DeviceEngine:
         metrics = self._metrics(rows, now, step)
         metrics.update(total_prefill_ns=tot_prefill, total_decode_ns=tot_decode, total_predictor_ns=tot_pred)
         return EngineResult(metrics, rows, records, step)
+
+    def _run_native(self, stop_after_finished, time_limit_s) -> EngineResult:
+        lib = _lib.load()
+        n = len(self.reqs)
+        q2 = (_lib.EngineQueue * 2)(self._queue(0, 0), self._queue(0, 1))
+        soa2 = (_lib.QueueSoA * 2)(self._soa(0, 0), self._soa(0, 1))
+        fits = np.ascontiguousarray(((self.prompt.astype(np.int64) + self.true_out) <= self.kv_budget).astype(np.uint8))
+        arr = np.ascontiguousarray(self.arrival_ns, dtype=np.int64)
+        dropped = np.empty(max(n, 1), dtype=np.int64)
+        ws, wn = _lib.workspace.get(lib.rs_rank_step_workspace_size(max(n, 1)), self.dev)
+        sched = self.sched
+        self.prev_n.zero_()
+        lp = _lib.EngineLoop(
+            n, arr.ctypes.data, fits.ctypes.data, self.adm_host.data_ptr(), self.adm_dev.data_ptr(),
+            dropped.ctypes.data, self.stat.data_ptr(), self.stat_host.data_ptr(), self.run_out.data_ptr(),
+            self.prom_out.data_ptr(), self.dem_out.data_ptr(), self.pre_out.data_ptr(), self.fin_out.data_ptr(),
+            self.compact_scratch.data_ptr(), self.prev_run.data_ptr(), self.prev_n.data_ptr(), ws, wn,
+            sched.max_batch, sched.starvation_threshold,
+            sched.priority_quantum, int(self.length_calibrated), int(sched.preemption),
+            -1 if self.kv_budget >= UNLIMITED_KV else self.kv_budget,
+            self.cost.predictor_ns_per_request if self.charges_predictor else 0,
+            -1 if time_limit_s is None else int(round(time_limit_s * NS_PER_S)),
+            -1 if stop_after_finished is None else int(stop_after_finished))
+        out = _lib.EngineLoopOut()
+        rc = lib.rs_engine_run(q2, soa2, ctypes.byref(self._trace), ctypes.byref(self._cost), ctypes.byref(lp),
+                               ctypes.byref(out), _lib.stream_handle(self.dev))
+        if rc == _lib.RS_ERR_NAN:
+            raise ValueError("ranking policy: NaN effective score")
+        _lib.check(rc, "rs_engine_run")
+        rows = self._rows(set(dropped[:out.n_dropped].tolist()), out.next_arrival)
+        metrics = self._metrics(rows, out.now_ns, out.steps)
+        metrics.update(total_prefill_ns=out.total_prefill_ns, total_decode_ns=out.total_decode_ns,
+                       total_predictor_ns=out.total_predictor_ns)
+        return EngineResult(metrics, rows, [], out.steps)
 
     def _rows(self, dropped: set[int], n_arrived: int) -> list[dict]:
         first = self.first_tok.cpu().numpy()

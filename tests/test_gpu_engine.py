@@ -141,3 +141,36 @@ def test_oracle_ranking_reproduces_reference_srtf():
         assert hashlib.sha256(_canonical(dec).encode()).hexdigest() == c["decisions_sha256"], i
         for k, v in c["metrics"].items():
             assert res.metrics[k] == v, (i, k, res.metrics[k], v)
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2, 3])
+def test_engine_native_loop_matches_reference(golden, idx):
+    """record=False runs the loop natively (rs_engine_run): same rows and metrics as the
+    reference's engine.run on the recorded traces."""
+    from paper_2408_15792_b200 import engine
+    from paper_2408_15792_b200.schedulers import SchedulerConfig
+    from paper_2408_15792_b200.workload import Request
+    c = golden["engine_golden"]["cases"][idx]
+    reqs = [Request(id=i, arrival_time=a, prompt_tokens=p, true_output_tokens=o) for i, a, p, o in c["requests"]]
+    res = engine.run(reqs, scores=c["scores"], sched=SchedulerConfig(**c["sched"]),
+                     cost=engine.COST_PRESETS[c["cost"]], kv_budget=c["kv_budget"])
+    assert res.records == [] and res.steps == c["n_steps"]
+    assert res.requests == c["rows"]
+    for k, v in c["metrics"].items():
+        assert res.metrics[k] == v, (k, res.metrics[k], v)
+
+
+def test_engine_native_loop_at_cfg5_scale():
+    import pathlib
+    from paper_2408_15792_b200 import engine
+    from paper_2408_15792_b200.schedulers import SchedulerConfig
+    from paper_2408_15792_b200.workload import Request
+    p = pathlib.Path(__file__).resolve().parent / "golden" / "engine_golden_20k.json"
+    c = json.loads(p.read_text())
+    reqs = [Request(id=i, arrival_time=a, prompt_tokens=pt, true_output_tokens=o) for i, a, pt, o in c["requests"]]
+    res = engine.run(reqs, scores=c["scores"], sched=SchedulerConfig(**c["sched"]),
+                     cost=engine.COST_PRESETS[c["cost"]])
+    assert res.steps == c["n_steps"]
+    assert hashlib.sha256(_canonical(res.requests).encode()).hexdigest() == c["rows_sha256"]
+    for k, v in c["metrics"].items():
+        assert res.metrics[k] == v, (k, res.metrics[k], v)

@@ -121,7 +121,7 @@ def test_schedule_random_vs_oracle_large():
 
 
 @pytest.mark.parametrize("n,max_batch,dist", [(3000, 256, "normal"), (5000, 256, "normal"), (100_000, 256, "ties"),
-                                              (1 << 20, 1024, "normal"),
+                                              (300_000, 256, "ties"), (1 << 20, 1024, "normal"),
                                               (50_000, 2048, "bf16"), (10_000, 1, "ties")])
 def test_topk_select_matches_full_sort(n, max_batch, dist):
     """Unlimited KV uses the radix top-k select; a budget that never binds takes the
