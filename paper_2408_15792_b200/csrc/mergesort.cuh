@@ -323,12 +323,15 @@ __global__ void __launch_bounds__(MS_THREADS) ms_merge_pass(const K* __restrict_
     if (Count) block_add_count(inv, inv_out);
 }
 
-// Small inputs (one CTA's worth): a bitonic network over (key, index) pairs in shared
-// memory, 1024 threads. Ties are broken by the original index, so the result equals the
-// stable sort's; the merge sort's single-tile path is one 256-thread CTA walking eight
-// dependent merge levels, which leaves a lone SM latency-bound (~30 us for 2048
-// 16-byte keys against ~3 us here) — that is the per-step rank sort of the engine loop.
-constexpr int MS_SMALL_MAX = 4096;
+// Small inputs: a bitonic network over (key, index) pairs in shared memory, 1024 threads,
+// in one launch. Ties are broken by the original index, so the result equals the stable
+// sort's. Measured on the rank step (16-byte keys): faster than the block-sort path up to
+// ~1K keys (42 vs 52 us per step at 300), even at 1K, slower beyond (157 vs 71 us at 4K:
+// 78 barrier-separated stages of 16-byte shared-memory exchanges).
+#ifndef RS_MS_SMALL_MAX
+#define RS_MS_SMALL_MAX 1024
+#endif
+constexpr int MS_SMALL_MAX = RS_MS_SMALL_MAX;
 constexpr int MS_SMALL_THREADS = 1024;
 
 template <typename K>
