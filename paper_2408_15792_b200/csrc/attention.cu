@@ -41,7 +41,10 @@ constexpr int AT_W_KV = 8, AT_W_MMA = 9, AT_W_Q0 = 10;  // + AT_W_Q0 + 1; softma
 constexpr int AT_KVB = 4;  // K/V ring depth (one group of <= 4 blocks)
 // Q [2 slots][2] + K, V [AT_KVB] + the fp16 "ones" tile (F16V) + barriers
 constexpr int AT_SMEM = (4 + 2 * AT_KVB + 1) * AT_BUF + 1024 + 1024;
-constexpr float AT_RESCALE = 8.0f;  // lazy-rescale threshold (log2 units)
+constexpr float AT_RESCALE = 8.0f;
+#ifndef AT_POLL_NS
+#define AT_POLL_NS 32
+#endif  // lazy-rescale threshold (log2 units)
 // which of every 8 exponential pairs go to MUFU (bit set) vs the FMA-pipe polynomial
 #ifndef AT_MUFU_MASK
 #define AT_MUFU_MASK 0x57u  // 5 of 8 on MUFU (measured best of 0x11, 0x15, 0x55, 0x57, 0x77)
@@ -325,6 +328,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                         issue_pv(s0, 0);
                     else if (s1.live && mbar_test_wait(&bar->p_full[1], s1.bseq & 1))
                         issue_pv(s1, 1);
+                    else
+                        __nanosleep(AT_POLL_NS);  // back off: this warp shares its SM sub-partition
+                                                  // with two softmax warps and would steal their issue slots
                 }
             }
         }
