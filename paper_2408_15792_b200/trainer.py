@@ -13,6 +13,7 @@ per step and one rank this is the reference's update sequence.
 from __future__ import annotations
 
 import ctypes
+import dataclasses
 
 import torch
 from . import _lib, dp
@@ -72,6 +73,37 @@ class RankerTrainer:
                                             self.lr, self.betas[0], self.betas[1], self.eps, self.t,
                                             1.0 / float(total_lists), _lib.stream_handle(self.model.dev)),
                    "rs_adam_step")
+
+    # ---- checkpoint / resume ------------------------------------------------------------
+    def state_dict(self) -> dict:
+        """Everything the next step depends on: the fp32 master weights, both Adam moments,
+        the step count and hyper-parameters (the bf16 working copy is re-derived)."""
+        return {"format": "rsb200-ranker-trainer", "version": 1, "t": self.t, "lr": self.lr,
+                "betas": list(self.betas), "eps": self.eps, "bucket_width": self.bucket_width,
+                "config": dataclasses.asdict(self.model.cfg),
+                "master": self.master.cpu(), "m": self.m.cpu(), "v": self.v.cpu(),
+                "params_bf16": self.model.flat.cpu()}
+
+    def load_state_dict(self, sd: dict) -> None:
+        if sd.get("format") != "rsb200-ranker-trainer" or sd.get("version") != 1:
+            raise ValueError("not a ranker-trainer checkpoint")
+        if sd["config"] != dataclasses.asdict(self.model.cfg):
+            raise ValueError("checkpoint was written for a different ranker config")
+        if sd["master"].numel() != self.master.numel():
+            raise ValueError("checkpoint parameter count mismatch")
+        self.t, self.lr, self.eps = int(sd["t"]), float(sd["lr"]), float(sd["eps"])
+        self.betas, self.bucket_width = (float(sd["betas"][0]), float(sd["betas"][1])), int(sd["bucket_width"])
+        self.master.copy_(sd["master"])
+        self.m.copy_(sd["m"])
+        self.v.copy_(sd["v"])
+        self.model.flat.copy_(sd["params_bf16"])
+        self.grad.zero_()
+
+    def save_checkpoint(self, path: str) -> None:
+        torch.save(self.state_dict(), path)
+
+    def load_checkpoint(self, path: str) -> None:
+        self.load_state_dict(torch.load(path, map_location="cpu", weights_only=True))
 
     def step(self, ids: torch.Tensor, lengths: torch.Tensor, list_len: int, total_lists: int | None = None,
              last_pos: torch.Tensor | None = None):

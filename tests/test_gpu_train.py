@@ -217,3 +217,33 @@ def test_training_reduces_loss_and_is_deterministic():
     assert runs[0][0][-1] < 0.8 * runs[0][0][0], runs[0][0]
     assert runs[0][0] == runs[1][0]
     assert torch.equal(runs[0][1], runs[1][1])
+
+
+def test_trainer_checkpoint_resume_is_bitwise(tmp_path):
+    """Two optimizer steps, checkpoint, a fresh trainer resumes: the weights after two more
+    steps equal the uninterrupted run's bit for bit (the pass is deterministic)."""
+    from paper_2408_15792_b200.ranker import OptRanker, init_params
+    from paper_2408_15792_b200.trainer import RankerTrainer
+    cfg = _small_cfg()
+    g = torch.Generator().manual_seed(3)
+    batches = [(torch.randint(4, cfg.vocab, (32, 32), generator=g, dtype=torch.int32).cuda(),
+                torch.randint(1, 2049, (32,), generator=g, dtype=torch.int32).cuda()) for _ in range(4)]
+
+    def fresh():
+        return RankerTrainer(OptRanker(cfg, params=init_params(cfg, seed=2)), lr=1e-3, lists_per_micro=2)
+
+    a = fresh()
+    for ids, ln in batches:
+        a.step(ids, ln, 16)
+    b = fresh()
+    for ids, ln in batches[:2]:
+        b.step(ids, ln, 16)
+    path = str(tmp_path / "ckpt.pt")
+    b.save_checkpoint(path)
+    c = fresh()
+    c.load_checkpoint(path)
+    for ids, ln in batches[2:]:
+        c.step(ids, ln, 16)
+    assert c.t == a.t == 4
+    assert torch.equal(c.model.flat, a.model.flat) and torch.equal(c.master, a.master)
+    assert torch.equal(c.m, a.m) and torch.equal(c.v, a.v)
