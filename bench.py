@@ -385,6 +385,31 @@ def engine_metric(args, world, rank, pk):
         t2 = time.perf_counter()
         res = eng.run()
         t3 = time.perf_counter()
+    rescore = None
+    if rank == 0 and args.rescore_steps > 0:
+        # a capped "true re-score" variant — every step re-scores every
+        # alive request with the ranker (S = 128) instead of reading the score cache; the
+        # ranker is a pure function of the prompt, so the decisions must equal the cached
+        # run's over the same steps
+        K = args.rescore_steps
+        scored = [0]
+
+        def rescore_fn(alive_ids):
+            scored[0] += alive_ids.numel()
+            return (-model.forward(ids_d[alive_ids], last_d[alive_ids])).double()
+
+        eng_c = engine.DeviceEngine(reqs, scores, sched, engine.COST_PRESETS["default"])
+        ref = eng_c.run(max_steps=K, native=False)
+        eng_r = engine.DeviceEngine(reqs, scores, sched, engine.COST_PRESETS["default"])
+        torch.cuda.synchronize()
+        t4 = time.perf_counter()
+        res_r = eng_r.run(max_steps=K, rescore=rescore_fn)
+        t5 = time.perf_counter()
+        same = res_r.steps == ref.steps and res_r.requests == ref.requests
+        rescore = {"steps": res_r.steps, "prompts_rescored": scored[0], "seconds": t5 - t4,
+                   "steps_per_s": res_r.steps / (t5 - t4), "prompts_rescored_per_s": scored[0] / (t5 - t4),
+                   "decisions_equal_cached": bool(same),
+                   "note": f"first {K} steps, every alive request re-scored each step (OPT-125M shape, S = 128)"}
     if world > 1:
         torch.distributed.barrier()
     del model, ids_d
@@ -400,7 +425,7 @@ def engine_metric(args, world, rank, pk):
                                                                           "mean_latency_s", "p90_max_waiting_s",
                                                                           "execution_order_tau")},
             "workload": f"{n} Poisson(40/s) requests, sharegpt lengths, prompts 8-128 tokens, max_batch 256, "
-                        "starvation 100/50, default cost preset"}
+                        "starvation 100/50, default cost preset", "true_rescore": rescore}
 
 
 def train_step_metric(args, world, rank, pk):
@@ -609,6 +634,8 @@ def main():
     ap.add_argument("--train-steps", type=int, default=1)
     ap.add_argument("--e2e-requests", type=int, default=100000,
                     help="cfg5 loop size (BASELINE configs[4]: 100000; 0 disables)")
+    ap.add_argument("--rescore-steps", type=int, default=400,
+                    help="cfg5 capped true re-score variant: steps that re-score every alive request (0 disables)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -184,10 +184,14 @@ class DeviceEngine:
         return _lib.QueueSoA(n_alive, _lib.RS_F64, *self._cols(self._sets[which]))
 
     def run(self, record: bool = False, stop_after_finished: int | None = None,
-            time_limit_s: float | None = None, native: bool = True) -> EngineResult:
+            time_limit_s: float | None = None, native: bool = True, rescore=None,
+            max_steps: int | None = None) -> EngineResult:
         """record=False (and native) runs the whole loop in C++ (rs_engine_run); record=True
-        steps from Python so every step's decision can be read back."""
-        if native and not record and not self.in_place:
+        steps from Python so every step's decision can be read back. rescore (optional):
+        called every step with the alive requests' trace indices (int64 device tensor, queue
+        order) and returning their scores (float64 device tensor): the reference's
+        re-score-every-step mode (engine.py:414-428 with rescore=True) instead of the cache."""
+        if native and not record and not self.in_place and rescore is None and max_steps is None:
             return self._run_native(stop_after_finished, time_limit_s)
         lib = _lib.load()
         rank_step, execute, admit, check = lib.rs_rank_step, lib.rs_engine_execute, lib.rs_engine_admit, _lib.check
@@ -260,6 +264,9 @@ class DeviceEngine:
             if n_alive > ws_n:
                 ws_n = max(n_alive, 2 * ws_n)
                 ws, wn = _lib.workspace.get(lib.rs_rank_step_workspace_size(ws_n), self.dev)
+            if rescore is not None:
+                cols = self._sets[cur]
+                cols["score"][:n_alive].copy_(rescore(cols["id"][:n_alive]))
             soas[cur].n = n_alive
             rc = rank_step(soa_refs[cur], max_batch, budget, threshold, quantum, calibrated, preemptive, run_p, prom_p,
                            dem_p, cnt_p, ws, wn, st)
@@ -304,6 +311,8 @@ class DeviceEngine:
                 })
             step += 1
             if stop_after_finished is not None and n_finished >= stop_after_finished:
+                break
+            if max_steps is not None and step >= max_steps:
                 break
             if limit_ns is not None and now >= limit_ns:
                 break
