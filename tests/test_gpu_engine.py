@@ -174,3 +174,26 @@ def test_engine_native_loop_at_cfg5_scale():
     assert hashlib.sha256(_canonical(res.requests).encode()).hexdigest() == c["rows_sha256"]
     for k, v in c["metrics"].items():
         assert res.metrics[k] == v, (k, res.metrics[k], v)
+
+
+def test_engine_rescore_hook_matches_cache(golden):
+    """The per-step re-score hook (re-scoring every alive request, reference rescore=True
+    mode) gives the cached run's decisions when the scorer is a pure function."""
+    import torch
+    from paper_2408_15792_b200 import engine
+    from paper_2408_15792_b200.schedulers import SchedulerConfig
+    from paper_2408_15792_b200.workload import Request
+    c = golden["engine_golden"]["cases"][1]
+    reqs = [Request(id=i, arrival_time=a, prompt_tokens=p, true_output_tokens=o) for i, a, p, o in c["requests"]]
+    table = torch.tensor(c["scores"], dtype=torch.float64, device="cuda")
+    calls = []
+
+    def rescore(alive):
+        calls.append(alive.numel())
+        return table[alive]
+
+    kw = dict(sched=SchedulerConfig(**c["sched"]), cost=engine.COST_PRESETS[c["cost"]])
+    a = engine.DeviceEngine(reqs, c["scores"], **kw).run(max_steps=60, record=True)
+    b = engine.DeviceEngine(reqs, c["scores"], **kw).run(max_steps=60, record=True, rescore=rescore)
+    assert len(calls) == a.steps == b.steps == 60 and sum(calls) > 0
+    assert a.records == b.records and a.requests == b.requests
