@@ -637,9 +637,30 @@ def main():
     ap.add_argument("--rescore-steps", type=int, default=400,
                     help="cfg5 capped true re-score variant: steps that re-score every alive request (0 disables)")
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
+
+
+def self_launch(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: start N ranks (one process per GPU)
+    through torch.distributed.run on 127.0.0.1 with this same command line; rank 0 prints
+    the JSON line."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(pathlib.Path(__file__).resolve())]
+    cmd += sys.argv[1:]
+    return subprocess.run(cmd).returncode
 
 
 if __name__ == "__main__":

@@ -486,13 +486,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 
 template <bool F16V>
 static int launch_attention(const void* qkv, void* out, int B, int S, int H, cudaStream_t st) {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev;
-        RS_CUDA(cudaGetDevice(&dev));
-        RS_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        RS_CUDA(cudaFuncSetAttribute(attention_fwd_kernel<F16V>, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM));
-    }
+    const int sms = num_sms();
+    RS_CUDA(ensure_smem((const void*)attention_fwd_kernel<F16V>, AT_SMEM));
     const uint64_t rows = (uint64_t)B * S;
     const uint64_t cols = (uint64_t)3 * H * AT_D;
     CUtensorMap m;

@@ -228,12 +228,8 @@ __global__ void __launch_bounds__(AB_THREADS, 2)
 int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv, int B, int S, int H, cudaStream_t st) {
     RS_CHECK_ARG(B > 0 && S > 0 && H > 0, "attention_bwd: empty shape");
     RS_CHECK_ARG(S <= AB_T, "attention_bwd: S=%d > 128 not supported yet (training uses S <= 128)", S);
-    static bool attr = false;
-    if (!attr) {
-        RS_CUDA(cudaFuncSetAttribute(attention_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AB_SMEM));
-        RS_CUDA(cudaFuncSetAttribute(attention_bwd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        attr = true;
-    }
+    RS_CUDA(ensure_smem((const void*)attention_bwd_kernel, AB_SMEM));
+    RS_CUDA(cudaFuncSetAttribute(attention_bwd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     const uint64_t rows = (uint64_t)B * S;
     const uint64_t dmc = (uint64_t)H * AB_D;
     CUtensorMap mq, ma, md;

@@ -2,6 +2,9 @@
 #include <cudaTypedefs.h>
 #include <stdarg.h>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
 #include "common.cuh"
 #include "tma.cuh"
 
@@ -18,6 +21,22 @@ PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
 
 static std::atomic<uint64_t> g_launches{0};
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// Dynamic shared-memory opt-in, tracked per (kernel, device): the attribute is per
+// device, so a process driving several GPUs sets it once on each.
+cudaError_t ensure_smem(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    int& have = done[{func, dev}];
+    if (have >= bytes) return cudaSuccess;
+    e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
 
 int resolve_tma_encoder() {
     if (g_encode_tiled) return RS_OK;

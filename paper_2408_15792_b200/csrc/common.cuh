@@ -47,6 +47,9 @@ void note_launch();
         if (_s != RS_OK) return _s; \
     } while (0)
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device), thread-safe.
+cudaError_t ensure_smem(const void* func, int bytes);
+
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 static inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

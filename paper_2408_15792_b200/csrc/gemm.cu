@@ -514,12 +514,7 @@ template <int E, bool AM, bool BM>
 static int launch_2sm(cudaLaunchConfig_t& lc, const CUtensorMap& tA, const CUtensorMap& tB, const CUtensorMap& tC,
                       const CUtensorMap& tR, const __nv_bfloat16* b, const void* aux, int M, int N, int K,
                       int k_splits) {
-    static bool attr = false;
-    if (!attr) {
-        RS_CUDA(cudaFuncSetAttribute(gemm_bf16_2sm_kernel<E, AM, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     G2Cfg<E>::smem));
-        attr = true;
-    }
+    RS_CUDA(ensure_smem((const void*)gemm_bf16_2sm_kernel<E, AM, BM>, G2Cfg<E>::smem));
     lc.dynamicSmemBytes = G2Cfg<E>::smem;
     RS_CUDA(cudaLaunchKernelEx(&lc, gemm_bf16_2sm_kernel<E, AM, BM>, tA, tB, tC, tR, b, aux, M, N, K, N, k_splits,
                                (2 * N) / 3));
@@ -540,7 +535,7 @@ int gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux
 
     RS_CHECK_ARG((epi != 2 && epi != 5) || aux != nullptr, "gemm_ex: epilogue %d needs aux", epi);
     RS_CHECK_ARG(k_splits >= 1 && (epi == 6 || k_splits == 1), "gemm_ex: split-K needs epilogue 6");
-    if (g_num_sms == 0) {
+    if (g_num_sms == 0) {  // identical on every B200 of a box
         int dev;
         RS_CUDA(cudaGetDevice(&dev));
         RS_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -614,7 +609,7 @@ int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, voi
     RS_CHECK_ARG(epi >= 0 && epi <= 3 || epi == 7, "gemm: bad epilogue %d", epi);
     RS_CHECK_ARG(bias != nullptr, "gemm: bias is required");
     RS_CHECK_ARG(epi != 2 || R != nullptr, "gemm: residual epilogue needs R");
-    if (g_num_sms == 0) {
+    if (g_num_sms == 0) {  // identical on every B200 of a box
         int dev;
         RS_CUDA(cudaGetDevice(&dev));
         RS_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -632,11 +627,7 @@ int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, voi
     void* c = C;
 #define RS_GEMM_LAUNCH(E)                                                                                     \
     do {                                                                                                      \
-        static bool attr = false;                                                                             \
-        if (!attr) {                                                                                          \
-            RS_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, G_SMEM)); \
-            attr = true;                                                                                      \
-        }                                                                                                     \
+        RS_CUDA(ensure_smem((const void*)gemm_bf16_kernel<E>, G_SMEM));                                      \
         gemm_bf16_kernel<E><<<grid, G_THREADS, G_SMEM, st>>>(tA, tB, b, r, c, M, N, K, N);                    \
     } while (0)
     switch (epi) {

@@ -302,11 +302,7 @@ static int launch_attention_last(const __nv_bfloat16* qkv, const float* h, const
                                  __nv_bfloat16* att_last, float* h_last, int B, int Bp, int S, int H,
                                  cudaStream_t st) {
     const size_t smem = (size_t)AL_WARPS * S * sizeof(float);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        RS_CUDA(cudaFuncSetAttribute(attention_last_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = smem;
-    }
+    if (smem > 48 * 1024) RS_CUDA(ensure_smem((const void*)attention_last_kernel, (int)smem));
     const int warps = Bp * H;
     attention_last_kernel<<<(warps + AL_WARPS - 1) / AL_WARPS, 32 * AL_WARPS, smem, st>>>(qkv, h, last, att_last,
                                                                                        h_last, B, Bp, S, H);

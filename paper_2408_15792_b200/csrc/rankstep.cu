@@ -606,12 +606,8 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
     const uint32_t k = min(n, (uint32_t)max_batch);
     if (kv_budget < 0 && n > SEL_MIN_N && k + SEL_CAP <= (uint32_t)SEL_SORT) {
         // top-k select (see sel_hist): <= SEL_LEVELS histogram passes, most no-ops
-        static bool attr = false;
         const size_t smem = SEL_SORT * (sizeof(RankKey) + sizeof(uint32_t));
-        if (!attr) {
-            RS_CUDA(cudaFuncSetAttribute(sel_sort_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-        }
+        RS_CUDA(ensure_smem((const void*)sel_sort_emit, (int)smem));
         RS_CUDA(cudaMemsetAsync(w.sel, 0, sizeof(SelState), st));
         RS_CUDA(cudaMemsetAsync(w.pfx, 0, sizeof(unsigned __int128), st));
         RS_CUDA(cudaMemsetAsync(w.hist, 0, SEL_BINS * sizeof(uint32_t), st));

@@ -107,12 +107,7 @@ extern "C" int rs_tokenize(const uint8_t* text_dev, const int64_t* offsets_dev, 
     RS_CHECK_ARG(text_dev != nullptr && offsets_dev && ids_dev && last_dev && bad_dev, "rs_tokenize: NULL argument");
     const int max_tokens = seq_len < 2048 ? seq_len : 2048;  // MAX_PROMPT_TOKENS
     const size_t smem = (size_t)TK_WARPS * max_tokens * sizeof(int32_t);
-    static bool attr = false;
-    if (!attr) {
-        RS_CUDA(cudaFuncSetAttribute(tokenize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     TK_WARPS * 2048 * (int)sizeof(int32_t)));
-        attr = true;
-    }
+    RS_CUDA(ensure_smem((const void*)tokenize_kernel, TK_WARPS * 2048 * (int)sizeof(int32_t)));
     const int need = (n + TK_WARPS - 1) / TK_WARPS, cap = num_sms() * 8;
     tokenize_kernel<<<need < cap ? need : cap, TK_WARPS * 32, smem, as_stream(stream)>>>(
         text_dev, offsets_dev, n, seq_len, max_tokens, (uint32_t)(vocab - 4), salt_crc ^ 0xFFFFFFFFu, pad_id, ids_dev,

@@ -263,7 +263,7 @@ class DeviceEngine:
             predictor_ns = k * pred_ns_per_req
             if n_alive > ws_n:
                 ws_n = max(n_alive, 2 * ws_n)
-                ws, wn = _lib.workspace.get(lib.rs_rank_step_workspace_size(ws_n), self.dev)
+                ws, wn = self._rank_workspace(lib.rs_rank_step_workspace_size(ws_n))
             if rescore is not None:
                 cols = self._sets[cur]
                 cols["score"][:n_alive].copy_(rescore(cols["id"][:n_alive]))
@@ -321,6 +321,16 @@ class DeviceEngine:
         metrics.update(total_prefill_ns=tot_prefill, total_decode_ns=tot_decode, total_predictor_ns=tot_pred)
         return EngineResult(metrics, rows, records, step)
 
+    def _rank_workspace(self, nbytes: int) -> tuple[int, int]:
+        """The engine's own rank-step scratch (grow-only). Not the shared per-device
+        workspace: a rescore() callback may grow that one mid-run and free the buffer
+        whose address the loop holds."""
+        buf = getattr(self, "_rank_ws", None)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(int(nbytes), 1 << 20), dtype=torch.uint8, device=self.dev)
+            self._rank_ws = buf
+        return buf.data_ptr(), buf.numel()
+
     def _run_native(self, stop_after_finished, time_limit_s) -> EngineResult:
         lib = _lib.load()
         n = len(self.reqs)
@@ -329,7 +339,7 @@ class DeviceEngine:
         fits = np.ascontiguousarray(((self.prompt.astype(np.int64) + self.true_out) <= self.kv_budget).astype(np.uint8))
         arr = np.ascontiguousarray(self.arrival_ns, dtype=np.int64)
         dropped = np.empty(max(n, 1), dtype=np.int64)
-        ws, wn = _lib.workspace.get(lib.rs_rank_step_workspace_size(max(n, 1)), self.dev)
+        ws, wn = self._rank_workspace(lib.rs_rank_step_workspace_size(max(n, 1)))
         sched = self.sched
         self.prev_n.zero_()
         lp = _lib.EngineLoop(

@@ -78,10 +78,17 @@ class OptRankerScorer:
         return [-float(v) for v in self.raw_outputs(list(requests))]
 
     def to_dict(self) -> dict:
-        if self.weights_path is None:
-            raise ValueError("opt-ranker weights are saved by save_scorer(); call it before to_dict()")
+        """JSON-able description (the reference engine hashes it into the run config,
+        engine.py:366). `weights_sha256` hashes the parameters in memory, so it tracks the
+        current weights whether or not they were saved; `weights` is the sidecar written
+        by save_scorer() (absolute path), or None before that."""
         return {"kind": self.kind, "config": dataclasses.asdict(self.model.cfg), "seq_len": self.seq_len,
-                "weights": self.weights_path, "weights_sha256": _sha256_file(self.weights_path)}
+                "weights": self.weights_path, "weights_sha256": _sha256_params(self.model.flat)}
+
+
+def _sha256_params(flat: torch.Tensor) -> str:
+    """sha256 of the raw little-endian bf16 parameter bytes (== the sidecar file's)."""
+    return hashlib.sha256(flat.view(torch.int16).cpu().numpy().tobytes()).hexdigest()
 
 
 def _sha256_file(path) -> str:
@@ -93,26 +100,34 @@ def _sha256_file(path) -> str:
 
 
 def save_scorer(scorer, path: str) -> None:
-    """JSON header at `path` + raw bf16 parameters at `path + '.bin'`."""
+    """JSON header at `path` + raw bf16 parameters at `path + '.bin'`. The header names
+    the sidecar relative to its own directory (load_scorer resolves it there)."""
     p = pathlib.Path(path)
-    weights = str(p) + ".bin"
+    weights = p.with_name(p.name + ".bin")
     scorer.model.flat.view(torch.int16).cpu().numpy().tofile(weights)
-    scorer.weights_path = weights
+    scorer.weights_path = str(weights.resolve())
     payload = {"format": _SCORER_FORMAT, "version": _SCORER_VERSION}
     payload.update(scorer.to_dict())
+    payload["weights"] = weights.name
     p.write_text(json.dumps(payload) + "\n", encoding="utf-8")
 
 
-def scorer_from_dict(obj: dict):
+def scorer_from_dict(obj: dict, base_dir: str | None = None):
     """`kind == "opt-ranker"` -> OptRankerScorer, "opt-classifier" -> OptClassifierScorer;
     other kinds belong to the reference
-    (ranksched.predictors.scorer_from_dict; install() chains the two)."""
+    (ranksched.predictors.scorer_from_dict; install() chains the two). A relative
+    `weights` path is resolved against `base_dir` (load_scorer: the header's directory)."""
     kind = obj.get("kind")
     if kind not in (OptRankerScorer.kind, "opt-classifier"):
         raise ValueError(f"unknown scorer kind {kind!r}")
+    if not obj.get("weights"):
+        raise ValueError(f"{kind} scorer dict has no weights file: save it with save_scorer() first")
     cfg = RankerConfig(**obj["config"])
     model = OptRanker(cfg, seed=None)
-    weights = obj["weights"]
+    weights = pathlib.Path(obj["weights"])
+    if not weights.is_absolute() and base_dir is not None:
+        weights = pathlib.Path(base_dir) / weights
+    weights = str(weights)
     if obj.get("weights_sha256") and _sha256_file(weights) != obj["weights_sha256"]:
         raise ValueError(f"{weights}: checksum mismatch")
     raw = np.fromfile(weights, dtype=np.int16)
@@ -125,7 +140,7 @@ def scorer_from_dict(obj: dict):
                                 seq_len=obj.get("seq_len", 128))
     else:
         s = OptRankerScorer(model, seq_len=obj.get("seq_len", 128))
-    s.weights_path = weights
+    s.weights_path = str(pathlib.Path(weights).resolve())
     return s
 
 
@@ -136,7 +151,7 @@ def load_scorer(path: str):
         raise ValueError(f"{path}: not a scorer file")
     if obj.get("version") != _SCORER_VERSION:
         raise ValueError(f"{path}: unsupported scorer version {obj.get('version')}")
-    return scorer_from_dict(obj)
+    return scorer_from_dict(obj, base_dir=str(pathlib.Path(path).parent))
 
 
 @dataclass(frozen=True)
@@ -307,12 +322,10 @@ class OptClassifierScorer:
         return [float(b * self.bucket_size + self.bucket_size / 2.0) for b in self.predict_buckets(reqs)]
 
     def to_dict(self) -> dict:
-        if self.weights_path is None:
-            raise ValueError("opt-classifier backbone weights are saved by save_scorer(); call it before to_dict()")
         return {"kind": self.kind, "config": dataclasses.asdict(self.model.cfg), "seq_len": self.seq_len,
                 "bucket_size": self.bucket_size, "head_weights": self.weights.cpu().tolist(),
                 "head_bias": self.bias.cpu().tolist(), "weights": self.weights_path,
-                "weights_sha256": _sha256_file(self.weights_path)}
+                "weights_sha256": _sha256_params(self.model.flat)}
 
 
 def train_classifier(trace, cfg: TrainConfig = TrainConfig(), n_buckets: int | None = 10,

@@ -115,7 +115,11 @@ def tau_from_counts(counts, n: int) -> TauResult:
     """Finish tau exactly as the reference does (ranking.py:58-63), on Python ints."""
     c, d, n1, n2, _n3, nan = (int(v) for v in counts)
     if nan:
-        raise ValueError("kendall_tau_b: NaN in input")
+        raise ValueError("tau counts of NaN input: use kendall_tau_b, which handles NaN like the reference")
+    return _finish(c, d, n1, n2, n)
+
+
+def _finish(c: int, d: int, n1: int, n2: int, n: int) -> TauResult:
     n0 = n * (n - 1) // 2
     denom = math.sqrt((n0 - n1) * (n0 - n2))
     if denom == 0.0:
@@ -136,7 +140,37 @@ def kendall_tau_b(x, y) -> TauResult:
     xt = _as_device_1d(x, dev)
     yt = _as_device_1d(y, dev)
     counts = tau_counts_device(xt, yt).cpu().tolist()
+    if counts[5]:
+        return _tau_with_nan(xt, yt, n)
     return tau_from_counts(counts, n)
+
+
+def _pairs(k: int) -> int:
+    return k * (k - 1) // 2
+
+
+def _tau_with_nan(xt: torch.Tensor, yt: torch.Tensor, n: int) -> TauResult:
+    """NaN input, as the reference treats it (ranking.py:45-57): a pair with a NaN in x or y
+    has sign(NaN) = NaN and counts as neither concordant nor discordant, and np.unique
+    (equal_nan) puts all NaNs of a column in one tie group. So C, D are the counts over
+    the rows NaN-free in both columns, and n1 (n2) = ties among x's (y's) non-NaN values +
+    the pairs among its NaNs; every count still comes from rs_tau_counts."""
+    def ok(t):
+        return ~torch.isnan(t) if t.is_floating_point() else torch.ones_like(t, dtype=torch.bool)
+
+    mx, my = ok(xt), ok(yt)
+    both = mx & my
+
+    def counts(a, b):
+        if a.numel() < 2:
+            return [0] * 6
+        return tau_counts_device(a.contiguous(), b.contiguous()).cpu().tolist()
+
+    c, d = counts(xt[both], yt[both])[:2]
+    xs, ys = xt[mx], yt[my]
+    n1 = counts(xs, xs)[2] + _pairs(n - xs.numel())
+    n2 = counts(ys, ys)[3] + _pairs(n - ys.numel())
+    return _finish(c, d, n1, n2, n)
 
 
 # ---------------------------------------------------------------------------

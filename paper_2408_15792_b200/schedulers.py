@@ -20,7 +20,6 @@ import numpy as np
 import torch
 
 from . import _lib
-from .workload import is_running
 
 NS_PER_S = 1_000_000_000
 UNLIMITED_KV = 1 << 62  # engine.py:39
@@ -176,16 +175,63 @@ class DeviceQueue:
                              demoted=self.dem_out[:c[2]].cpu().tolist())
 
 
+class _Staging:
+    """Grow-only pinned-host / device byte buffers holding one SoA image of the candidate
+    list, so RankingPolicy.schedule moves its inputs with one H2D copy and its outputs
+    with one D2H copy (no per-column transfers, no per-call allocations once warm)."""
+
+    # (name, dtype, bytes per row); 16-byte aligned columns
+    COLS = (("score", torch.float64, 8), ("arrival", torch.float64, 8), ("id", torch.int64, 8),
+            ("prompt", torch.int32, 4), ("generated", torch.int32, 4), ("starvation", torch.int32, 4),
+            ("quantum", torch.int32, 4), ("arrival_rank", torch.int32, 4), ("flags", torch.uint8, 1))
+    OUTS = (("run", torch.int64, 8), ("prom", torch.int64, 8), ("dem", torch.int64, 8))
+
+    def __init__(self, dev):
+        self.dev, self.cap = dev, 0
+
+    @staticmethod
+    def _layout(cols, n):
+        off, out = 0, {}
+        for name, dt, w in cols:
+            out[name] = (off, dt)
+            off += -(-w * n // 16) * 16
+        return out, off
+
+    def ensure(self, n: int) -> None:
+        """Room for n candidates (the run / promoted / demoted lists hold <= n ids)."""
+        if n <= self.cap:
+            return
+        cap = max(n, 2 * self.cap, 1024)
+        self.cap = cap
+        self.in_lay, in_bytes = self._layout(self.COLS, cap)
+        out_lay, out_bytes = self._layout(self.OUTS, cap)
+        self.out_lay = {k: (o + in_bytes, dt) for k, (o, dt) in out_lay.items()}
+        total = in_bytes + out_bytes + 16
+        self.in_bytes = in_bytes
+        self.host = torch.empty(total, dtype=torch.uint8).pin_memory()
+        self.devbuf = torch.empty(total, dtype=torch.uint8, device=self.dev)
+        self.ws = torch.empty(max(_lib.load().rs_rank_step_workspace_size(cap),
+                                  _lib.load().rs_arrival_rank_workspace_size(cap), 1),
+                              dtype=torch.uint8, device=self.dev)
+
+    def view(self, buf: torch.Tensor, name: str, n: int) -> torch.Tensor:
+        off, dt = self.in_lay[name] if name in self.in_lay else self.out_lay[name]
+        w = torch.empty((), dtype=dt).element_size()
+        return buf[off:off + w * n].view(dt)
+
+
 class RankingPolicy:
     """Score-ordered scheduling with starvation promotion (schedulers.py:178-240)."""
 
     name = "ranking"
     preemptive = True
     needs_scores = True
+    decision_cls = BatchDecision  # install() substitutes the reference's BatchDecision
 
     def __init__(self, config: SchedulerConfig, length_calibrated: bool):
         self.config = config
         self.length_calibrated = length_calibrated
+        self._stage: _Staging | None = None
 
     # host-side mirror of the reference key, kept for API compatibility (tests and
     # callers that sort with it); the scheduler itself sorts on the device.
@@ -207,26 +253,74 @@ class RankingPolicy:
         return []
 
     def schedule(self, candidates, kv_budget: int) -> BatchDecision:
-        cands = list(candidates)
+        """One ranking step over `candidates` (reference: schedulers.py:219-240 with
+        Policy.schedule / _fill, :64-109): the AoS -> SoA gather is one pass over the
+        Request objects into a pinned staging image, one H2D copy, rs_arrival_rank +
+        rs_rank_step on the device, one D2H copy of decision and state, and the mutated
+        starvation_count / priority / quantum written back to the passed requests."""
+        cands = candidates if isinstance(candidates, list) else list(candidates)
         n = len(cands)
         if n == 0:
-            return BatchDecision(run=[])
-        scored = [r.score is not None for r in cands]
-        q = DeviceQueue.from_arrays(
-            score=[r.score if r.score is not None else 0.0 for r in cands], scored=scored,
-            priority=[bool(r.priority) for r in cands], running=[is_running(r) for r in cands],
-            prompt_tokens=[r.prompt_tokens for r in cands], generated_tokens=[r.generated_tokens for r in cands],
-            arrival_time=[r.arrival_time for r in cands], ids=[r.id for r in cands],
-            starvation=[r.starvation_count for r in cands], quantum=[r.quantum for r in cands])
-        q.rank_step(self.config, kv_budget, self.length_calibrated, self.preemptive)
-        dec = q.decision()
-        flags = q.flags.cpu().numpy()
-        starv = q.starvation.cpu().tolist()
-        quant = q.quantum.cpu().tolist()
+            return self.decision_cls(run=[])
+        dev = _lib.device()
+        if self._stage is None or self._stage.dev != dev:
+            self._stage = _Staging(dev)
+        stg = self._stage
+        stg.ensure(n)
+        h = stg.host
+        rows = [(r.score, r.arrival_time, r.id, r.prompt_tokens, r.generated_tokens, r.starvation_count,
+                 r.quantum, r.priority, r.state) for r in cands]
+        sc, arr, ids, pt, gt, stv, qu, pr, st = zip(*rows)
+        scored = np.fromiter((v is not None for v in sc), bool, n)
+        score = np.fromiter((0.0 if v is None else v for v in sc), np.float64, n)
+        running = np.fromiter((getattr(v, "value", v) == "running" for v in st), bool, n)
+        priority = np.fromiter(pr, bool, n)
+        stg.view(h, "score", n).numpy()[:] = score
+        stg.view(h, "arrival", n).numpy()[:] = arr
+        stg.view(h, "id", n).numpy()[:] = ids
+        stg.view(h, "prompt", n).numpy()[:] = pt
+        stg.view(h, "generated", n).numpy()[:] = gt
+        stv_old = np.asarray(stv, dtype=np.int64)
+        qu_old = np.asarray(qu, dtype=np.int64)
+        stg.view(h, "starvation", n).numpy()[:] = stv_old
+        stg.view(h, "quantum", n).numpy()[:] = qu_old
+        stg.view(h, "flags", n).numpy()[:] = (scored * _lib.RS_FLAG_SCORED | priority * _lib.RS_FLAG_PRIORITY
+                                             | running * _lib.RS_FLAG_RUNNING)
+        d = stg.devbuf
+        stream = _lib.stream_handle(dev)
+        d[:stg.in_bytes].copy_(h[:stg.in_bytes], non_blocking=True)
+        lib = _lib.load()
+        V = lambda name: stg.view(d, name, n).data_ptr()  # noqa: E731
+        _lib.check(lib.rs_arrival_rank(V("arrival"), V("id"), n, V("arrival_rank"), stg.ws.data_ptr(),
+                                       stg.ws.numel(), stream), "rs_arrival_rank")
+        soa = _lib.QueueSoA(n, _lib.RS_F64, V("score"), V("prompt"), V("generated"), V("arrival_rank"), V("id"),
+                            V("flags"), V("starvation"), V("quantum"))
+        cnt_off = d.numel() - 16
+        counts = d[cnt_off:cnt_off + 16].view(torch.int32)
+        budget = -1 if kv_budget is None or kv_budget >= UNLIMITED_KV else int(kv_budget)
+        _lib.check(lib.rs_rank_step(ctypes.byref(soa), self.config.max_batch, budget,
+                                    self.config.starvation_threshold, self.config.priority_quantum,
+                                    int(self.length_calibrated), int(self.preemptive and self.config.preemption),
+                                    V("run"), V("prom"), V("dem"), counts.data_ptr(), stg.ws.data_ptr(),
+                                    stg.ws.numel(), stream), "rs_rank_step")
+        # one D2H copy: the mutated state columns through the end of the buffer
+        lo = stg.in_lay["starvation"][0]
+        h[lo:].copy_(d[lo:], non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        c = h[cnt_off:cnt_off + 16].view(torch.int32).tolist()
+        if c[3]:
+            raise ValueError("ranking policy: NaN effective score")
+        dec = self.decision_cls(run=stg.view(h, "run", c[0]).tolist(), promoted=stg.view(h, "prom", c[1]).tolist(),
+                                demoted=stg.view(h, "dem", c[2]).tolist())
+        fl = stg.view(h, "flags", n).numpy()
+        pr_new = (fl & _lib.RS_FLAG_PRIORITY) != 0
+        stv_new = stg.view(h, "starvation", n).numpy().tolist()
+        qu_new = stg.view(h, "quantum", n).numpy().tolist()
         for k, r in enumerate(cands):
-            r.priority = bool(flags[k] & _lib.RS_FLAG_PRIORITY)
-            r.starvation_count = starv[k]
-            r.quantum = quant[k]
+            r.starvation_count = stv_new[k]
+            r.quantum = qu_new[k]
+        for k in np.nonzero(pr_new != priority)[0].tolist():
+            cands[k].priority = bool(pr_new[k])
         return dec
 
 

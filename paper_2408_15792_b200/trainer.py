@@ -67,6 +67,11 @@ class RankerTrainer:
     def apply(self, total_lists: int) -> None:
         """All-reduce the accumulated gradient across ranks (NCCL) and take one Adam step."""
         dp.allreduce_sum_(self.grad, self.group)
+        self.apply_local(total_lists)
+
+    def apply_local(self, total_lists: int) -> None:
+        """One Adam step on .grad as it stands (already summed over ranks), scaled by
+        1 / total_lists; zeroes .grad."""
         self.t += 1
         _lib.check(_lib.load().rs_adam_step(self.master.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
                                             self.grad.data_ptr(), self.model.flat.data_ptr(), self.master.numel(),

@@ -19,3 +19,14 @@ def golden():
     import json
     d = ROOT / "tests" / "golden"
     return {p.stem: json.loads(p.read_text()) for p in d.glob("*.json")}
+
+
+@pytest.fixture(scope="session")
+def ranksched():
+    """The reference package, staged under oracle/_ref by build() (travels to the GPU box);
+    skips when it was never staged."""
+    from oracle import install_ref
+    try:
+        return install_ref.import_ranksched()
+    except ImportError as e:
+        pytest.skip(str(e))

@@ -48,9 +48,28 @@ def test_tau_rejects_bad_input():
     from paper_2408_15792_b200.ranking import kendall_tau_b
     with pytest.raises(ValueError):
         kendall_tau_b([1, 2], [1, 2, 3])
-    with pytest.raises(ValueError):
-        kendall_tau_b([1.0, float("nan"), 2.0], [1, 2, 3])
     assert kendall_tau_b([], []).tau == 0.0
+
+
+def test_tau_nan_like_reference(ranksched):
+    """NaN pairs count as neither concordant nor discordant and NaNs tie with each other
+    (np.unique equal_nan), exactly as the reference's row loop (ranking.py:45-57)."""
+    from paper_2408_15792_b200.ranking import kendall_tau_b
+    rng = np.random.default_rng(23)
+    cases = [([1.0, float("nan"), 2.0], [1, 2, 3]), ([float("nan")] * 4, [1, 2, 3, 4]),
+             ([1.0, 2.0, 3.0], [float("nan"), 1.0, float("nan")]), ([np.inf, np.inf, -np.inf, np.nan], [1, 2, 3, 4])]
+    for n in (50, 2000):
+        x = rng.normal(size=n)
+        y = rng.integers(0, 20, n).astype(np.float64)
+        x[rng.random(n) < 0.1] = np.nan
+        y[rng.random(n) < 0.05] = np.nan
+        cases.append((x, y))
+        cases.append((x.astype(np.float32), rng.integers(0, 9, n)))
+    for x, y in cases:
+        want = ranksched.ranking.kendall_tau_b(x, y)
+        r = kendall_tau_b(x, y)
+        assert (r.tau, r.concordant, r.discordant, r.n_pairs) == \
+            (want.tau, want.concordant, want.discordant, want.n_pairs)
 
 
 def test_tau_1m_matches_reference(golden):
