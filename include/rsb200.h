@@ -25,6 +25,9 @@
  *                             (the OPT-125M-shape backbone of PAPER.md:195-201 that
  *                              replaces _Net.forward predictors.py:190-196)
  *   rs_ranker_* (training) <- _Net.backward / _Adam.step     predictors.py:198-225
+ *   rs_linear_* / rs_standard* <- the reference's own linear / MLP ranker
+ *                             (_Standardizer, _Net, train_ranking step, _Adam)
+ *                             predictors.py:159-225, 374-386 (cfg1 parity bridge)
  */
 #ifndef RSB200_H
 #define RSB200_H
@@ -344,6 +347,29 @@ int rs_attention_bwd(const void* qkv_dev, const void* att_dev, const void* dout_
                      int32_t S, int32_t H, void* stream);
 /* Number of kernels this library has launched in the process (all entry points). */
 uint64_t rs_launch_count(void);
+
+/* ---- linear / MLP ranker over the 24 prompt features (the cfg1 parity bridge) ------
+ * Replaces _Standardizer.fit / __call__ (predictors.py:159-172), _Net.forward / backward
+ * (predictors.py:175-206), one train_ranking minibatch step (predictors.py:374-386) and
+ * _Adam.step (predictors.py:209-225). float64 throughout. params = the reference's
+ * params list flattened: hidden == 0 -> [w (D), b]; hidden > 0 -> [W1 (D x H row-major),
+ * b1 (H), w2 (H), b2]. */
+int64_t rs_linear_n_params(int32_t n_features, int32_t hidden);
+int rs_standardizer_fit(const double* X_dev, int64_t n_rows, int32_t n_features, double* mean_dev,
+                        double* std_dev, void* stream);
+int rs_standardize(const double* X_dev, int64_t n_rows, int32_t n_features, const double* mean_dev,
+                   const double* std_dev, double* out_dev, void* stream);
+/* out[r] = net((X[r] - mean) / std) */
+int rs_linear_forward(const double* X_dev, int64_t n_rows, int32_t n_features, const double* mean_dev,
+                      const double* std_dev, int32_t hidden, const double* params_dev, double* out_dev,
+                      void* stream);
+/* One list: Xb = Xs[batch] (Xs already standardised), order = stable argsort(lengths[batch]
+ * // width), loss = ListMLE / n -> loss_dev[0], grads of (ListMLE / n) -> grad_dev
+ * (optional), Adam step t on params / m / v in place. n >= 2. */
+int rs_linear_train_step(const double* Xs_dev, const int64_t* batch_dev, const int64_t* lengths_dev, int32_t n,
+                         int32_t n_features, int32_t hidden, int32_t bucket_width, double* params_dev,
+                         double* adam_m_dev, double* adam_v_dev, double lr, double beta1, double beta2, double eps,
+                         int64_t t, double* loss_dev, double* grad_dev, void* stream);
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop
