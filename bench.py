@@ -102,61 +102,32 @@ def cpu_cores():
 
 
 # ---------------------------------------------------------------------------
-# CPU oracle-port measurements (cpu_baseline and the --impl reference arm)
+# CPU baselines (bench_cpu.py) and the --impl reference arm
 # ---------------------------------------------------------------------------
 
 
-def cpu_port_step(cfg, params, ids_np):
-    """Oracle port of the path on the host: fp32 OPT-shape forward (torch CPU, all
-    threads) + the reference ranking step restated in Python."""
-    from oracle import opt_ranker, schedule_oracle
-
-    g = opt_ranker.forward(params, cfg, ids_np).numpy()
-
-    class R:
-        __slots__ = ("id", "arrival_time", "prompt_tokens", "generated_tokens", "score", "state", "priority",
-                     "starvation_count", "quantum")
-
-    reqs = []
-    for k, gv in enumerate(g):
-        r = R()
-        r.id, r.arrival_time, r.prompt_tokens, r.generated_tokens = k, float(k), ids_np.shape[1], 0
-        r.score, r.state, r.priority, r.starvation_count, r.quantum = -float(gv), "waiting", False, 0, 0
-        reqs.append(r)
-    schedule_oracle.schedule(reqs, 1 << 62, max_batch=256, threshold=100, quantum=50, calibrated=False)
-    return g
-
-
-def cpu_baseline(cfg, S, n_prompts=16, reps=1):
-    from paper_2408_15792_b200.ranker import init_params
-    torch.set_num_threads(cpu_cores())
-    params = {k: v.to(torch.bfloat16).float() for k, v in init_params(cfg, 0).items()}
-    ids = np.random.default_rng(1).integers(4, cfg.vocab, (n_prompts, S)).astype(np.int32)
-    cpu_port_step(cfg, params, ids[:2])  # warm-up
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        cpu_port_step(cfg, params, ids)
-    dt = (time.perf_counter() - t0) / reps
-    return {"value": n_prompts / dt, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "port",
-            "sample": f"{n_prompts} prompts x {S} tokens per step: oracle fp32 OPT-125M-shape forward "
-                      f"(torch CPU) + oracle ranking step; {dt:.2f} s"}
+def cpu_baseline(cfg, S, n_prompts=16):
+    import bench_cpu
+    return bench_cpu.headline(cfg, S, n_prompts)
 
 
 def run_reference(args):
+    """The reference arm: the CPU path timed on the host cores, each step a bounded sample
+    of the headline workload (bench_cpu.HeadlineCPU: fp32 OPT forward port on all threads —
+    the reference has no OPT model — + the reference's own RankingPolicy.schedule)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_2408_15792_b200.ranker import RankerConfig, init_params
+    import bench_cpu
+    from paper_2408_15792_b200.ranker import RankerConfig
     cfg = RankerConfig.opt_125m()
-    torch.set_num_threads(cpu_cores())
-    params = {k: v.to(torch.bfloat16).float() for k, v in init_params(cfg, 0).items()}
     P = args.ref_prompts
-    ids = np.random.default_rng(1).integers(4, cfg.vocab, (P, args.seq)).astype(np.int32)
+    h = bench_cpu.HeadlineCPU(cfg, args.seq, P)
     for _ in range(args.warmup):
-        cpu_port_step(cfg, params, ids)
+        h.step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        cpu_port_step(cfg, params, ids)
+        h.step()
     dt = (time.perf_counter() - t0) / args.steps
     v = P / dt
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world, "steps": args.steps,
@@ -165,9 +136,8 @@ def run_reference(args):
             "config": {"workload": f"OPT-125M-shape ranker scoring {args.batch} prompts x {args.seq} tokens + score "
                                    f"sort; each CPU step is a bounded sample of {P} prompts",
                        "global_batch": args.batch, "seq_len": args.seq, "parallelism": "cpu"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": torch.get_num_threads(), "kind": "port",
-                             "sample": f"{P} prompts x {args.seq} tokens per step (oracle port: fp32 OPT forward + "
-                                       "ranking step)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": h.torch.get_num_threads(), "kind": h.kind,
+                             "sample": h.describe(dt)},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -278,18 +248,21 @@ def tau_and_rankstep(pk, reps=5):
     for dst, src in zip((dq.flags, dq.starvation, dq.quantum), snap):
         dst.copy_(src)
     rs_bytes = 34.0 * n
+    import bench_cpu
     return {
         "tau": {"metric": "Kendall tau-b pairs/sec (exact counts)", "value": pairs / (t / 1e3), "unit": "pairs/s",
                 "n": n, "ms": t, "ms_eager": t_eager, "note": "ms: the kernels replayed as one CUDA graph",
                 "roofline": {"bound": "hbm", "achieved": tau_bytes / t / 1e6, "peak": pk["hbm_gbs"],
                                               "unit": "GB/s", "frac": tau_bytes / t / 1e6 / pk["hbm_gbs"],
-                                              "traffic": sort_traffic("tau_1m"), "algorithmic_bytes": tau_bytes}},
+                                              "traffic": sort_traffic("tau_1m"), "algorithmic_bytes": tau_bytes},
+                "cpu_baseline": bench_cpu.tau()},
         "rank_step": {"metric": "requests ranked/sec (sort + fill + starvation bump)", "value": n / (tr / 1e3),
                       "unit": "requests/s", "n": n, "ms": tr, "ms_eager": tr_eager,
                       "roofline": {"bound": "hbm", "achieved": rs_bytes / tr / 1e6, "peak": pk["hbm_gbs"],
                                    "unit": "GB/s", "frac": rs_bytes / tr / 1e6 / pk["hbm_gbs"],
                                    "traffic": sort_traffic("rank_step_1m"),
-                                   "algorithmic_bytes": rs_bytes}},
+                                   "algorithmic_bytes": rs_bytes},
+                      "cpu_baseline": bench_cpu.rank_step()},
     }
 
 
@@ -332,50 +305,42 @@ def size_sweep(pk, reps=3):
         ranking.listmle_from_lengths(gl, ln)
         t = timed(lambda: ranking.listmle_from_lengths(gl, ln), reps)
         nbytes = 12.0 * n_lists * L + 4.0 * n_lists
+        import bench_cpu
         out["listmle"].append({"lists": n_lists, "list_len": L, "ms": t, "items_per_s": n_lists * L / (t / 1e3),
-                               "achieved_gbs": nbytes / t / 1e6, "frac": nbytes / t / 1e6 / pk["hbm_gbs"]})
+                               "achieved_gbs": nbytes / t / 1e6, "frac": nbytes / t / 1e6 / pk["hbm_gbs"],
+                               "cpu_baseline": bench_cpu.listmle()})
         del gl, ln
     torch.cuda.empty_cache()
     return out
 
 
-def synthetic_poisson(n, rate=40.0, seed=7, mu=5.3, sigma=0.9, max_len=2048):
-    """generate_poisson(rate, n, sharegpt, seed) in shape (workload.py:288-313, DIST_PRESETS
-    'sharegpt' = lognormal(5.3, 0.9) clipped to [1, 2048]); prompts become synthetic token
-    ids of length U[8, 128] (the A1 map's role)."""
-    from paper_2408_15792_b200.workload import Request
-    rng = np.random.default_rng(seed)
-    lengths = np.clip(np.rint(rng.lognormal(mu, sigma, n)), 1, max_len).astype(np.int64)
-    arrivals = np.cumsum(rng.exponential(1.0 / rate, n))
-    plen = rng.integers(8, 129, n)
-    reqs = [Request(id=i, arrival_time=float(arrivals[i]), prompt_tokens=int(plen[i]),
-                    true_output_tokens=int(lengths[i])) for i in range(n)]
-    return reqs, plen
-
-
 def engine_metric(args, world, rank, pk):
-    """cfg5 (BASELINE.json configs[4]): end-to-end scheduler loop. Every request's prompt
-    is scored once by the OPT-125M-shape ranker (S = 128, prompts sharded across ranks,
-    scores all-gathered: the score cache), then rank 0 runs the reference engine loop
-    (admission, ranking-policy step with starvation bump, execute, retirement) on the
-    device (paper_2408_15792_b200.engine) with max_batch 256, threshold 100, quantum 50,
-    the default cost preset. Wall clock of scoring + loop (the loop syncs once per step)."""
-    from paper_2408_15792_b200 import engine
+    """cfg5 (BASELINE.json configs[4]): end-to-end scheduler loop on the reference's own
+    trace generator, generate_poisson(40, n, sharegpt, seed 7, prompt_noise 0.25)
+    (workload.py:288-313; workload.generate_poisson draws the identical trace). Every
+    request's prompt is tokenized on the device and scored once by the OPT-125M-shape ranker
+    (S = 128, prompts sharded across ranks, scores all-gathered: the score cache — the
+    ranker is a pure function of the prompt), then rank 0 runs the engine loop
+    (admission, ranking-policy step with starvation bump, execute, retirement) on the device
+    (paper_2408_15792_b200.engine) with max_batch 256, threshold 100, quantum 50, the
+    default cost preset. Wall clock of scoring + loop (the loop syncs once per step)."""
+    from paper_2408_15792_b200 import dp, engine
     from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
     from paper_2408_15792_b200.schedulers import SchedulerConfig
+    from paper_2408_15792_b200.workload import LengthDist, generate_poisson, prompt_token_ids_device
     n = args.e2e_requests
-    reqs, plen = synthetic_poisson(n)
+    trace = generate_poisson(40.0, n, LengthDist.parse("sharegpt"), seed=7, prompt_noise=0.25)
+    reqs = trace.requests
+    prompts = [r.prompt for r in reqs]
     cfg = RankerConfig.opt_125m()
     model = OptRanker(cfg, seed=0)
-    gen = torch.Generator().manual_seed(3)
-    ids = torch.randint(4, cfg.vocab, (n, 128), generator=gen, dtype=torch.int32)
-    last = torch.from_numpy((plen - 1).astype(np.int32))
-    ids_d, last_d = ids.cuda(), last.cuda()
+    lo, hi = dp.shard_range(n, world, rank)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     t0 = time.perf_counter()
-    g = model.forward_sharded(ids_d, last_d)
+    ids_d, last_d = prompt_token_ids_device(prompts[lo:hi], 128, cfg.vocab, host_fallback=True)
+    g = dp.gather_scores(model.forward(ids_d, last_d), n)
     scores = (-g).double().cpu().numpy()
     t1 = time.perf_counter()
     res = None
@@ -393,10 +358,11 @@ def engine_metric(args, world, rank, pk):
         # run's over the same steps
         K = args.rescore_steps
         scored = [0]
+        all_ids, all_last = prompt_token_ids_device(prompts, 128, cfg.vocab, host_fallback=True)
 
         def rescore_fn(alive_ids):
             scored[0] += alive_ids.numel()
-            return (-model.forward(ids_d[alive_ids], last_d[alive_ids])).double()
+            return (-model.forward(all_ids[alive_ids], all_last[alive_ids])).double()
 
         eng_c = engine.DeviceEngine(reqs, scores, sched, engine.COST_PRESETS["default"])
         ref = eng_c.run(max_steps=K, native=False)
@@ -410,6 +376,7 @@ def engine_metric(args, world, rank, pk):
                    "steps_per_s": res_r.steps / (t5 - t4), "prompts_rescored_per_s": scored[0] / (t5 - t4),
                    "decisions_equal_cached": bool(same),
                    "note": f"first {K} steps, every alive request re-scored each step (OPT-125M shape, S = 128)"}
+        del all_ids, all_last
     if world > 1:
         torch.distributed.barrier()
     del model, ids_d
@@ -418,14 +385,19 @@ def engine_metric(args, world, rank, pk):
         return None
     score_s, loop_s = t1 - t0, t3 - t2
     m = res.metrics
-    return {"metric": "end-to-end scheduler loop requests/sec (score cache + device engine)",
+    line = {"metric": "end-to-end scheduler loop requests/sec (score cache + device engine)",
             "value": n / (score_s + loop_s), "unit": "requests/s", "requests": n, "steps": res.steps,
             "score_s": score_s, "loop_s": loop_s, "steps_per_s": res.steps / loop_s,
             "prompts_scored_per_s": n / score_s, "sim": {k: m[k] for k in ("n_finished", "makespan_s",
                                                                           "mean_latency_s", "p90_max_waiting_s",
                                                                           "execution_order_tau")},
-            "workload": f"{n} Poisson(40/s) requests, sharegpt lengths, prompts 8-128 tokens, max_batch 256, "
-                        "starvation 100/50, default cost preset", "true_rescore": rescore}
+            "workload": f"generate_poisson(40, {n}, sharegpt, seed=7, prompt_noise=0.25) (the reference's generator; "
+                        "identical trace), prompts tokenized on the device to 128 ids, max_batch 256, starvation "
+                        "100/50, default cost preset", "true_rescore": rescore}
+    if world == 1:
+        import bench_cpu
+        line["cpu_baseline"] = bench_cpu.engine_loop(trace, args.cpu_engine_prefix)
+    return line
 
 
 def train_step_metric(args, world, rank, pk):
@@ -467,10 +439,92 @@ def train_step_metric(args, world, rank, pk):
     tflops = flops / (ms / 1e3) / 1e12 / world
     del tr, model, ids, lengths
     torch.cuda.empty_cache()
-    return {"metric": "ListMLE training prompts/sec (1024 lists x 64 prompts x 128 tokens per step, DP)",
+    line = {"metric": "ListMLE training prompts/sec (1024 lists x 64 prompts x 128 tokens per step, DP)",
             "value": prompts / (ms / 1e3), "unit": "prompts/s", "ms_per_step": ms, "steps": args.train_steps,
             "global_lists": n_lists, "list_len": list_len, "seq_len": S, "flops_per_step": flops,
             "tflops_per_gpu": tflops, "frac_of_sustained": tflops / pk["bf16_tflops_sustained"]}
+    if rank == 0 and world == 1:
+        import bench_cpu
+        line["cpu_baseline"] = bench_cpu.train_step(cfg, S)
+        line["cpu_baseline_listmle"] = bench_cpu.listmle(n_lists, list_len)
+    return line
+
+
+def plugin_e2e(args, model, sched, world, rank, dev, barrier, max_over_ranks):
+    """End to end through the drop-in plugin API, exactly the calls the reference's
+    engine.run makes each step (engine.py:414-430): OptRankerScorer.score_batch(requests)
+    on this rank's B Request objects with S-token prompt strings (prompts -> ids on the
+    device, forward, scores back as Python floats), the scores written to the requests,
+    then on rank 0 RankingPolicy.schedule(candidates, kv_budget) over all B x world
+    requests (SoA gather, H2D, rs_arrival_rank + rs_rank_step, D2H, state written back).
+    With N > 1 the score lists are all-gathered (NCCL) before the schedule call."""
+    import torch.distributed as dist
+    from paper_2408_15792_b200.predictors import OptRankerScorer
+    from paper_2408_15792_b200.schedulers import UNLIMITED_KV, RankingPolicy
+    from paper_2408_15792_b200.workload import _VOCAB, Request, prompt_token_ids_device
+    B, S = args.batch, args.seq
+    words = np.array(_VOCAB, dtype=object)
+    rng = np.random.default_rng(1000 + rank)
+    prompts = [" ".join(words[rng.integers(0, len(words), S)]) for _ in range(B)]
+    mine = [Request(id=rank * B + k, arrival_time=float(rank * B + k), prompt_tokens=S, true_output_tokens=1,
+                    prompt=p) for k, p in enumerate(prompts)]
+    allreq = mine
+    if rank == 0 and world > 1:
+        allreq = mine + [Request(id=k, arrival_time=float(k), prompt_tokens=S, true_output_tokens=1)
+                         for k in range(B, B * world)]
+    scorer = OptRankerScorer(model, seq_len=S)
+    pol = RankingPolicy(sched, scorer.length_calibrated)
+    gbuf = torch.empty(B * world, dtype=torch.float64, device=dev)
+    parts = {"score_batch": 0.0, "gather": 0.0, "schedule": 0.0}
+
+    def step():
+        t0 = time.perf_counter()
+        sc = scorer.score_batch(mine, 0)
+        t1 = time.perf_counter()
+        if world > 1:
+            dist.all_gather_into_tensor(gbuf, torch.tensor(sc, dtype=torch.float64, device=dev))
+            sc = gbuf.cpu().tolist() if rank == 0 else sc
+        t2 = time.perf_counter()
+        dec = None
+        if rank == 0:
+            for r, v in zip(allreq, sc):
+                r.score = v
+            dec = pol.schedule(allreq, UNLIMITED_KV)
+        t3 = time.perf_counter()
+        parts["score_batch"] += t1 - t0
+        parts["gather"] += t2 - t1
+        parts["schedule"] += t3 - t2
+        return dec
+
+    step()
+    for k in parts:
+        parts[k] = 0.0
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    barrier()
+    ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / args.steps)
+    # breakdown of score_batch: the device tokenizer alone, and the host-map tokenizer
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    prompt_token_ids_device(prompts, S, model.cfg.vocab, host_fallback=True)
+    torch.cuda.synchronize()
+    tok_dev = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    OptRankerScorer(model, seq_len=S, device_tokenizer=False).encode(mine)
+    tok_host = time.perf_counter() - t0
+    text_bytes = sum(len(p) for p in prompts)
+    n_all = B * world
+    return {"value": n_all / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": text_bytes + 8 * (B + 1) + (45 * n_all if rank == 0 else 0),
+            "d2h_bytes_per_step": 4 * B + (37 * n_all if rank == 0 else 0),
+            "path": "OptRankerScorer.score_batch(requests) [prompt bytes H2D, rs_tokenize, rs_ranker_forward, scores "
+                    "D2H] -> request.score = s -> RankingPolicy.schedule(requests, kv) [SoA staging H2D, "
+                    "rs_arrival_rank + rs_rank_step, decision + state D2H, write-back]",
+            "breakdown_ms": {k: v * 1e3 / args.steps for k, v in parts.items()},
+            "tokenize_ms": {"device": tok_dev * 1e3, "host_map": tok_host * 1e3},
+            "requests": f"{B} Request objects per rank with {S}-token prompts drawn from the reference vocabulary"}
 
 
 def run_ours(args):
@@ -557,7 +611,7 @@ def run_ours(args):
     launches = int(lib.rs_launch_count() - l0)
     value = B * world / (ms / 1e3)
 
-    # end to end through the public API with host buffers (H2D ids, D2H run ids)
+    # C-ABI level with host buffers (H2D token ids, D2H run ids): e2e_ids
     step_e2e()
     barrier()
     t0 = time.perf_counter()
@@ -565,6 +619,8 @@ def run_ours(args):
         step_e2e()
     barrier()
     e2e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / args.steps)
+    # the headline e2e: the plugin calls the reference's engine makes (engine.py:414-430)
+    plugin = plugin_e2e(args, model, sched, world, rank, dev, barrier, max_over_ranks)
 
     extras = {}
     if rank == 0 and not args.no_extras:
@@ -595,8 +651,10 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (activations ~10 GB per 1M-token chunk)"},
         "roofline": extras.get("roofline"),
         "cpu_baseline": extras.get("cpu_baseline"),
-        "e2e": {"value": B * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * S * 4,
-                "d2h_bytes_per_step": sched.max_batch * 8 + 16, "ms_per_step": e2e_ms},
+        "e2e": plugin,
+        "e2e_ids": {"value": B * world / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": B * S * 4,
+                    "d2h_bytes_per_step": sched.max_batch * 8 + 16, "ms_per_step": e2e_ms,
+                    "path": "pinned token ids H2D -> rs_ranker_forward -> (all-gather) -> rs_rank_step -> run ids D2H"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "model_flops": {"per_prompt": flops, "per_prompt_unpruned": cfg.flops_per_prompt(S),
@@ -625,7 +683,7 @@ def main():
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--seq", type=int, default=512)
     ap.add_argument("--cpu-prompts", type=int, default=16)
-    ap.add_argument("--ref-prompts", type=int, default=4)
+    ap.add_argument("--ref-prompts", type=int, default=16)
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--train-lists", type=int, default=1024)
@@ -634,6 +692,8 @@ def main():
     ap.add_argument("--train-steps", type=int, default=1)
     ap.add_argument("--e2e-requests", type=int, default=100000,
                     help="cfg5 loop size (BASELINE configs[4]: 100000; 0 disables)")
+    ap.add_argument("--cpu-engine-prefix", type=int, default=5000,
+                    help="cfg5 CPU baseline: reference engine.run over this many leading requests")
     ap.add_argument("--rescore-steps", type=int, default=400,
                     help="cfg5 capped true re-score variant: steps that re-score every alive request (0 disables)")
     args = ap.parse_args()

@@ -21,14 +21,15 @@ def _ln(x, w, b):
     return F.layer_norm(x, (x.shape[-1],), w, b, eps=1e-5)
 
 
-@torch.no_grad()
-def hidden_states(params, cfg, ids) -> torch.Tensor:
-    ids = torch.as_tensor(np.asarray(ids), dtype=torch.long)
+def hidden_states_grad(params, cfg, ids) -> torch.Tensor:
+    """hidden_states with autograd (the fp32 training reference / the CPU train baseline)."""
+    ids = torch.as_tensor(np.asarray(ids), dtype=torch.long, device=params["tok_emb"].device)
     B, S = ids.shape
     d, H = cfg.d_model, cfg.n_heads
     hd = d // H
-    h = params["tok_emb"][ids] + params["pos_emb"][torch.arange(S) + 2][None]
-    mask = torch.full((S, S), float("-inf")).triu(1)
+    dev = params["tok_emb"].device
+    h = params["tok_emb"][ids] + params["pos_emb"][torch.arange(S, device=dev) + 2][None]
+    mask = torch.full((S, S), float("-inf"), device=dev).triu(1)
     for layer in range(cfg.n_layers):
         p = {k.split(".")[-1]: v for k, v in params.items() if k.startswith(f"layers.{layer}.")}
         x = _ln(h, p["ln1_w"], p["ln1_b"])
@@ -47,12 +48,29 @@ def hidden_states(params, cfg, ids) -> torch.Tensor:
     return h
 
 
-@torch.no_grad()
-def forward(params, cfg, ids, last_pos=None) -> torch.Tensor:
-    """g [B] fp32 = head_w . LN_f(h[b, last_pos[b]]) + head_b (higher = shorter)."""
-    h = hidden_states(params, cfg, ids)
+hidden_states = torch.no_grad()(hidden_states_grad)
+
+
+def forward_grad(params, cfg, ids, last_pos=None) -> torch.Tensor:
+    """g [B] fp32 = head_w . LN_f(h[b, last_pos[b]]) + head_b (higher = shorter), with autograd."""
+    h = hidden_states_grad(params, cfg, ids)
     B, S = h.shape[:2]
     lp = torch.full((B,), S - 1, dtype=torch.long) if last_pos is None else torch.as_tensor(last_pos).long()
-    last = h[torch.arange(B), lp]
+    last = h[torch.arange(B), lp.to(h.device)]
     x = _ln(last, params["lnf_w"], params["lnf_b"])
     return x @ params["head_w"] + params["head_b"][0]
+
+
+forward = torch.no_grad()(forward_grad)
+
+
+def listmle_torch(g, lengths, width=10):
+    """sum over lists of list_mle_loss(g_list, stable argsort(len // width)) / n
+    (ranking.py:86-99, predictors.py:380-383) in torch (autograd-able)."""
+    total = 0.0
+    for gl, ll in zip(g, lengths):
+        order = torch.from_numpy(np.argsort(np.asarray(ll) // width, kind="stable")).to(gl.device)
+        t = gl[order]
+        lse = torch.logcumsumexp(t.flip(0), 0).flip(0)
+        total = total + (lse - t).sum() / len(gl)
+    return total

@@ -42,13 +42,16 @@ class OptRankerScorer:
     charges_predictor = True
 
     def __init__(self, model: OptRanker | None = None, seq_len: int = 128, cfg: RankerConfig | None = None,
-                 seed: int = 0, device_tokenizer: bool = False):
+                 seed: int = 0, device_tokenizer: bool | str = "auto"):
         self.model = model if model is not None else OptRanker(cfg or RankerConfig(), seed=seed)
         self.seq_len = int(seq_len)
         self.weights_path: str | None = None
-        # True: prompts -> ids on the device (rs_tokenize, identical ids; ASCII prompts
-        # only — others raise); False: the host map, any Unicode prompt
-        self.device_tokenizer = bool(device_tokenizer)
+        # prompts -> ids (identical either way): True = on the device (rs_tokenize; ASCII
+        # prompts only, others raise); False = the host map; "auto" = the device, with
+        # the host map patching in the rows of prompts that need Unicode-aware splitting
+        if device_tokenizer not in (True, False, "auto"):
+            raise ValueError("device_tokenizer must be True, False or 'auto'")
+        self.device_tokenizer = device_tokenizer
 
     def encode(self, requests) -> tuple[torch.Tensor, torch.Tensor]:
         """Prompts -> (ids int32 [n, S], last_pos int32 [n]) in pinned host memory."""
@@ -67,7 +70,8 @@ class OptRankerScorer:
         dev = self.model.dev
         if self.device_tokenizer:
             ids, last = prompt_token_ids_device([getattr(r, "prompt", "") or "" for r in requests], self.seq_len,
-                                                self.model.cfg.vocab, device=dev)
+                                                self.model.cfg.vocab, device=dev,
+                                                host_fallback=self.device_tokenizer == "auto")
             g = self.model.forward(ids, last)
         else:
             ids, last = self.encode(requests)

@@ -61,6 +61,25 @@ def test_scorer_device_tokenizer_same_scores():
     cfg = RankerConfig(n_layers=1)
     reqs = [Request(id=i, arrival_time=float(i), prompt_tokens=5, true_output_tokens=5, prompt=p)
             for i, p in enumerate(_random_prompts(rng, 64, 30))]
-    a = OptRankerScorer(cfg=cfg, seq_len=32, seed=0)
+    a = OptRankerScorer(cfg=cfg, seq_len=32, seed=0, device_tokenizer=False)
     b = OptRankerScorer(model=a.model, seq_len=32, device_tokenizer=True)
     assert a.score_batch(reqs, 0) == b.score_batch(reqs, 0)
+
+
+def test_scorer_auto_tokenizer_patches_unicode_rows():
+    """device_tokenizer='auto' (the default): ASCII prompts on the device, prompts needing
+    Unicode-aware splitting through the host map, same ids / scores as the host map."""
+    from paper_2408_15792_b200.predictors import OptRankerScorer
+    from paper_2408_15792_b200.ranker import RankerConfig
+    from paper_2408_15792_b200.workload import Request, prompt_token_ids, prompt_token_ids_device
+    prompts = ["plain words here", "cafÉ au lait", "no\u00a0break space", "", "  x  ", "ÅNGSTRÖM units"]
+    ids, last = prompt_token_ids_device(prompts, 8, host_fallback=True)
+    for k, p in enumerate(prompts):
+        want_ids, want_last = prompt_token_ids(p, 8)
+        np.testing.assert_array_equal(ids[k].cpu().numpy(), want_ids)
+        assert int(last[k]) == want_last
+    reqs = [Request(id=i, arrival_time=0.0, prompt_tokens=3, true_output_tokens=3, prompt=p)
+            for i, p in enumerate(prompts)]
+    a = OptRankerScorer(cfg=RankerConfig(n_layers=1), seq_len=8, seed=0, device_tokenizer=False)
+    b = OptRankerScorer(model=a.model, seq_len=8)
+    assert b.device_tokenizer == "auto" and a.score_batch(reqs, 0) == b.score_batch(reqs, 0)
