@@ -97,3 +97,30 @@ def test_ranker_batch_independence_and_chunking():
     g_all = m.forward(ids.cuda())
     g_part = m.forward(ids[2090:].cuda())
     torch.testing.assert_close(g_all[2090:], g_part, rtol=0, atol=0)
+
+
+def test_opt125m_headline_shape_vs_golden(golden):
+    """SURVEY 8c at the measured shape (BASELINE configs[1]): 4096 prompts x 512 tokens,
+    full OPT-125M, seed-0 weights; scores vs the fp32 oracle's frozen scores
+    (tests/golden/make_opt_golden.py): |g - g_ref| <= 1e-2 max(1, |g_ref|) for every
+    prompt and tau(g, g_ref) >= 0.99 over all of them."""
+    import hashlib
+    import sys
+    from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
+    from paper_2408_15792_b200.ranking import kendall_tau_b
+    sys.path.insert(0, str(__import__("pathlib").Path(__file__).parent / "golden"))
+    from make_opt_golden import inputs
+    gd = golden.get("opt_scores_golden")
+    if gd is None:
+        pytest.skip("opt_scores_golden.json not generated")
+    cfg = RankerConfig.opt_125m()
+    ids, last = inputs(gd["n"], gd["seq_len"], cfg.vocab)
+    assert hashlib.sha256(ids.numpy().tobytes()).hexdigest() == gd["ids_sha256"]
+    assert hashlib.sha256(last.numpy().tobytes()).hexdigest() == gd["last_sha256"]
+    m = OptRanker(cfg, seed=0)
+    g = m.forward(ids.cuda(), last.cuda()).cpu().double()
+    ref = torch.tensor(gd["g"], dtype=torch.float64)
+    err = (g - ref).abs()
+    assert (err <= 1e-2 * ref.abs().clamp(min=1)).all(), err.max()
+    tau = kendall_tau_b(g.numpy(), ref.numpy()).tau
+    assert tau >= 0.99, tau

@@ -163,6 +163,70 @@ def test_gradient_matches_autograd(S, list_len, n_lists, mb):
     assert len(report) > 20
 
 
+_MATRICES = ("qkv_w", "out_w", "fc1_w", "fc2_w", "tok_emb", "head_w")
+
+
+def test_gradient_full_opt125m_shape():
+    """The same comparison at the full OPT-125M dimensions cfg3 is measured on (d = 768,
+    12 layers, 12 heads, FFN 3072, vocab 50272), 2 lists x 16 prompts x 128 tokens.
+
+    Bar, per tensor: every weight matrix (QKV, out-proj, FC1, FC2 of all 12 layers, the
+    used token-embedding rows, the head) meets the plain 2e-2 relative-Frobenius bar
+    against fp32 autograd. Vectors whose ListMLE gradient nearly cancels across a list
+    (biases, LayerNorm weights / biases, position embeddings: shared by every prompt of
+    the list, so only the small prompt-to-prompt differences survive the sum) are held to
+    the storage-precision floor instead — the deviation of the fp32 graph with bf16
+    rounding exactly where the CUDA pass stores bf16 — as 1.5 x floor + 2e-3; the test
+    prints each tensor's error and floor."""
+    from paper_2408_15792_b200.ranker import OptRanker, RankerConfig, init_params
+    from paper_2408_15792_b200.trainer import RankerTrainer
+    cfg = RankerConfig.opt_125m()
+    params = init_params(cfg, seed=5)
+    g = torch.Generator().manual_seed(6)
+    for k in params:
+        if k.endswith("_b") or "ln" in k:
+            params[k] = params[k] + 0.05 * torch.randn(params[k].shape, generator=g)
+    model = OptRanker(cfg, params=params)
+    n_lists, list_len, S = 2, 16, 128
+    n = n_lists * list_len
+    ids = torch.randint(4, cfg.vocab, (n, S), generator=g, dtype=torch.int32)
+    lengths = torch.randint(1, 2049, (n,), generator=g, dtype=torch.int32)
+    tr = RankerTrainer(model, lists_per_micro=2)
+    loss = tr.accumulate(ids.cuda(), lengths.cuda(), list_len).cpu()
+    ref32, ref_loss = _ref_grads(model, cfg, ids, lengths, n_lists, list_len, emulate=False)
+    emu, _ = _ref_grads(model, cfg, ids, lengths, n_lists, list_len, emulate=True)
+    np.testing.assert_allclose(loss.numpy(), ref_loss, rtol=2e-2, atol=2e-3)
+    hw_scale = ref32["head_w"].norm().item()
+    rows, bad = [], []
+    for name, ref in ref32.items():
+        got = tr.grad[model.offsets[name]:model.offsets[name] + ref.numel()].view(ref.shape)
+        e = emu[name]
+        if name in _SHIFT_INVARIANT:
+            err = (got - ref).abs().max().item() / hw_scale
+            rows.append((name, "abs/|d head_w|", err, None))
+            if err > 1e-2:
+                bad.append(rows[-1])
+            continue
+        if name in ("tok_emb", "pos_emb"):
+            used = ref.abs().sum(1) > 0
+            got, ref, e = got[used], ref[used], e[used]
+        r_32 = ((got - ref).norm() / ref.norm()).item()
+        floor = ((e - ref).norm() / ref.norm()).item()
+        leaf = name.split(".")[-1]
+        if leaf in _MATRICES:
+            rows.append((name, "plain 2e-2", r_32, floor))
+            if r_32 > 2e-2:
+                bad.append(rows[-1])
+        else:
+            rows.append((name, "1.5 floor + 2e-3", r_32, floor))
+            if r_32 > max(2e-2, 1.5 * floor + 2e-3):
+                bad.append(rows[-1])
+    print("\n".join(f"{n:24s} {bar:18s} err {e:.4f} floor {'-' if f is None else f'{f:.4f}'}"
+                    for n, bar, e, f in rows))
+    assert sum(r[1] == "plain 2e-2" for r in rows) == 4 * cfg.n_layers + 2
+    assert not bad, bad
+
+
 def test_adam_first_step_is_minus_lr_sign():
     """test_predictors.py:116-132: Adam's first step moves every parameter by -lr*sign(g)."""
     from paper_2408_15792_b200 import _lib
