@@ -222,10 +222,10 @@ def tau_and_rankstep(pk, reps=5):
     out = torch.empty(6, dtype=torch.int64, device="cuda")
     ranking.tau_counts_device(xd, yd, out)
     t_eager = timed(lambda: ranking.tau_counts_device(xd, yd, out), reps)
-    plan = ranking.TauPlan(xd, yd)  # same kernels, replayed as one CUDA graph
+    plan = ranking.TauPlan(xd, yd)  # the fast path's kernels, replayed as one CUDA graph
     plan()
     t = timed(plan, reps)
-    assert torch.equal(plan.out, out), "graph and eager tau counts differ"
+    assert int(plan.out[5]) == 0 and torch.equal(plan.out, out), "graph and eager tau counts differ"
     n = len(x)
     pairs = n * (n - 1) / 2
     tau_bytes = 8.0 * n
@@ -278,8 +278,9 @@ def size_sweep(pk, reps=3):
         x = torch.randn(n, device="cuda", generator=g)
         y = torch.randint(1, 2049, (n,), device="cuda", generator=g, dtype=torch.int32)
         res = torch.empty(6, dtype=torch.int64, device="cuda")
-        ranking.tau_counts_device(x, y, res)
-        t = timed(lambda: ranking.tau_counts_device(x, y, res), reps)
+        ranking.tau_counts_device(x, y, res, fast_only=True)
+        t = timed(lambda: ranking.tau_counts_device(x, y, res, fast_only=True), reps)
+        assert int(res[5]) == 0, "tau fast path declined a cfg4-shaped input"
         out["tau"].append({"n": n, "ms": t, "pairs_per_s": n * (n - 1) / 2 / (t / 1e3),
                            "achieved_gbs": 8.0 * n / t / 1e6, "frac": 8.0 * n / t / 1e6 / pk["hbm_gbs"]})
         del x, y

@@ -69,12 +69,19 @@ int rs_device_init(int device, int32_t* sm_count, int32_t* cc_major, int32_t* cc
  * x, y: n values each of dtype RS_F32/RS_F64/RS_I32/RS_I64 (compared as float64,
  * exactly like `np.asarray(x, dtype=np.float64)`, -0.0 == +0.0). NaN -> RS_ERR_NAN.
  * counts_dev: int64[6] on device = {concordant, discordant, n1 (x-tied pairs),
- * n2 (y-tied pairs), n3 (pairs tied in both), nan (1 if any NaN was seen; the
- * counts are then meaningless)}. No host synchronisation. tau is finished on the
- * host with the reference expression (ranking.py:60-63). */
+ * n2 (y-tied pairs), n3 (pairs tied in both), status (1 if any NaN was seen; the
+ * counts are then meaningless)}. tau is finished on the host with the reference
+ * expression (ranking.py:60-63).
+ * rs_tau_counts runs the bucket fast path (y images spanning < 4096 values) and reads
+ * its status back once (one stream synchronisation; none while the stream is being
+ * captured), running the general merge-sort path when the fast one does not apply.
+ * rs_tau_counts_fast runs the fast path only and never synchronises (graph
+ * capturable): status 2 = these inputs need rs_tau_counts. */
 size_t rs_tau_workspace_size(int64_t n, int x_dtype, int y_dtype);
 int rs_tau_counts(const void* x_dev, int x_dtype, const void* y_dev, int y_dtype, int64_t n,
                   int64_t* counts_dev, void* ws_dev, size_t ws_bytes, void* stream);
+int rs_tau_counts_fast(const void* x_dev, int x_dtype, const void* y_dev, int y_dtype, int64_t n,
+                       int64_t* counts_dev, void* ws_dev, size_t ws_bytes, void* stream);
 
 /* ---- K6: ListMLE ------------------------------------------------------------
  * rs_listmle_order: n_lists independent lists of length list_len, scores (RS_F32 or

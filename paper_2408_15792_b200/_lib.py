@@ -84,6 +84,7 @@ SIGNATURES = {
     "rs_device_init": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_vp]),
     "rs_tau_workspace_size": (c_sz, [c_i64, ctypes.c_int, ctypes.c_int]),
     "rs_tau_counts": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp, ctypes.c_int, c_i64, c_vp, c_vp, c_sz, c_vp]),
+    "rs_tau_counts_fast": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp, ctypes.c_int, c_i64, c_vp, c_vp, c_sz, c_vp]),
     "rs_listmle_order": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp]),
     "rs_listmle_lengths": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp]),
     "rs_arrival_rank_workspace_size": (c_sz, [c_i64]),

