@@ -401,17 +401,20 @@ def engine_metric(args, world, rank, pk):
     return line
 
 
-def train_step_metric(args, world, rank, pk):
+def train_step_metric(args, world, rank, pk, n_lists=None, S=None, micro=None, baselines=True):
     """cfg3 (BASELINE.json configs[2]): one ListMLE optimizer step over a global batch of
     1024 lists x 64 prompts x 128 tokens, lists sharded across ranks, gradient all-reduce
-    (NCCL) + fused Adam. Device time by CUDA events, max over ranks."""
+    (NCCL) + fused Adam. Device time by CUDA events, max over ranks. Also run at S = 512
+    (SURVEY 8d's secondary cfg3 run; the blocked attention backward) on fewer lists."""
     from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
     from paper_2408_15792_b200.trainer import RankerTrainer
     cfg = RankerConfig.opt_125m()
-    n_lists, list_len, S = args.train_lists, 64, args.train_seq
+    n_lists = n_lists or args.train_lists
+    S = S or args.train_seq
+    list_len = 64
     mine = len(range(rank, n_lists, world))
     model = OptRanker(cfg, seed=0)
-    tr = RankerTrainer(model, lr=2e-5, lists_per_micro=args.train_micro)
+    tr = RankerTrainer(model, lr=2e-5, lists_per_micro=micro or args.train_micro)
     gen = torch.Generator().manual_seed(2000 + rank)
     ids = torch.randint(4, cfg.vocab, (mine * list_len, S), generator=gen, dtype=torch.int32).cuda()
     lengths = torch.randint(1, 2049, (mine * list_len,), generator=gen, dtype=torch.int32).cuda()
@@ -440,11 +443,11 @@ def train_step_metric(args, world, rank, pk):
     tflops = flops / (ms / 1e3) / 1e12 / world
     del tr, model, ids, lengths
     torch.cuda.empty_cache()
-    line = {"metric": "ListMLE training prompts/sec (1024 lists x 64 prompts x 128 tokens per step, DP)",
+    line = {"metric": f"ListMLE training prompts/sec ({n_lists} lists x 64 prompts x {S} tokens per step, DP)",
             "value": prompts / (ms / 1e3), "unit": "prompts/s", "ms_per_step": ms, "steps": args.train_steps,
             "global_lists": n_lists, "list_len": list_len, "seq_len": S, "flops_per_step": flops,
             "tflops_per_gpu": tflops, "frac_of_sustained": tflops / pk["bf16_tflops_sustained"]}
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and baselines:
         import bench_cpu
         line["cpu_baseline"] = bench_cpu.train_step(cfg, S)
         line["cpu_baseline_listmle"] = bench_cpu.listmle(n_lists, list_len)
@@ -630,6 +633,9 @@ def run_ours(args):
         extras["size_sweep"] = size_sweep(pk)
     if not args.no_extras and not args.no_train:
         extras["train_step"] = train_step_metric(args, world, rank, pk)
+        if args.train512_lists > 0:
+            extras["train_step_s512"] = train_step_metric(args, world, rank, pk, n_lists=args.train512_lists, S=512,
+                                                          micro=4, baselines=False)
     if not args.no_extras and args.e2e_requests > 0:
         extras["e2e_loop"] = engine_metric(args, world, rank, pk)
     if rank == 0 and not args.no_extras:
@@ -666,6 +672,7 @@ def run_ours(args):
         "tau": extras.get("tau"),
         "rank_step": extras.get("rank_step"),
         "train_step": extras.get("train_step"),
+        "train_step_s512": extras.get("train_step_s512"),
         "size_sweep": extras.get("size_sweep"),
         "e2e_loop": extras.get("e2e_loop"),
     }
@@ -691,6 +698,8 @@ def main():
     ap.add_argument("--train-seq", type=int, default=128)
     ap.add_argument("--train-micro", type=int, default=16)
     ap.add_argument("--train-steps", type=int, default=1)
+    ap.add_argument("--train512-lists", type=int, default=64,
+                    help="cfg3 secondary run at S = 512 over this many lists of 64 (0 disables)")
     ap.add_argument("--e2e-requests", type=int, default=100000,
                     help="cfg5 loop size (BASELINE configs[4]: 100000; 0 disables)")
     ap.add_argument("--cpu-engine-prefix", type=int, default=5000,

@@ -352,6 +352,12 @@ int rs_gemm_bf16_ex(const void* A_dev, const void* W_dev, const void* bias_dev, 
  * qkv, its output att [B*S, H*64] and dout = d loss / d att. */
 int rs_attention_bwd(const void* qkv_dev, const void* att_dev, const void* dout_dev, void* dqkv_dev, int32_t B,
                      int32_t S, int32_t H, void* stream);
+/* Causal attention backward for 128 < S <= 512 (128-token blocks: a dQ kernel that also
+ * writes each row's log-sum-exp and rowsum(dO * O) into the workspace, then a dK / dV
+ * kernel); same layouts as rs_attention_bwd. */
+size_t rs_attention_bwd_long_workspace_size(int32_t B, int32_t S, int32_t H);
+int rs_attention_bwd_long(const void* qkv_dev, const void* att_dev, const void* dout_dev, void* dqkv_dev,
+                          int32_t B, int32_t S, int32_t H, void* ws_dev, size_t ws_bytes, void* stream);
 /* Number of kernels this library has launched in the process (all entry points). */
 uint64_t rs_launch_count(void);
 

@@ -25,6 +25,9 @@
 
 namespace rs {
 int attention_fwd(const void* qkv, void* out, int B, int S, int H, cudaStream_t st);
+size_t attention_bwd_long_ws(int B, int S, int H);
+int attention_bwd_long(const void* qkv, const void* att, const void* dout, void* dqkv, int B, int S, int H, void* ws,
+                       size_t ws_bytes, cudaStream_t st);
 int ranker_embed(const int32_t* ids, const void* P, int64_t off_tok, int64_t off_pos, float* h, int n_tok, int S,
                  int d, int vocab, int mp, cudaStream_t st);
 int ranker_ln(const float* x, const void* w, const void* b, void* y, int rows, int d, cudaStream_t st);
@@ -53,6 +56,8 @@ struct TrainWs {
     __nv_bfloat16 *dh16, *da, *dqkv, *df;
     void* ews;
     size_t ews_bytes;
+    void* abw;  // attention backward scratch for S > 128 (row LSE and D)
+    size_t abw_bytes;
 };
 
 static int wgrad_splits(int M, int N, int K) {
@@ -65,7 +70,7 @@ static int wgrad_splits(int M, int N, int K) {
 }
 
 template <typename A>
-static void train_layout(A& a, const rs_ranker_config& c, int64_t Tp, int P, TrainWs* w, int n_classes = 0) {
+static void train_layout(A& a, const rs_ranker_config& c, int64_t Tp, int P, int S, TrainWs* w, int n_classes = 0) {
     const int L = c.n_layers;
     const int64_t d = c.d_model, F = c.d_ffn;
     TrainWs t{};
@@ -99,6 +104,8 @@ static void train_layout(A& a, const rs_ranker_config& c, int64_t Tp, int P, Tra
     t.df = a.template take<__nv_bfloat16>(Tp * F);
     t.ews_bytes = embed_backward_ws((int)Tp);
     t.ews = a.template take<uint8_t>(t.ews_bytes);
+    t.abw_bytes = S > 128 ? attention_bwd_long_ws(P, S, c.n_heads) : 0;
+    t.abw = a.template take<uint8_t>(t.abw_bytes);
     if (w) *w = t;
 }
 struct TrSizer {
@@ -176,7 +183,10 @@ static int train_backward(const rs_ranker_config* cfg, const __nv_bfloat16* P16,
         RS_TRY(slices_add(w.wpart, sp, (int64_t)d * d, grad + off(OFF_OUT_W, l), st));
         RS_TRY(colsum_add(w.dh, false, n_tok, d, w.rpart, grad + off(OFF_OUT_B, l), st));
         RS_TRY(gemm_bf16_ex(w.dh16, P16 + off(OFF_OUT_W, l), nullptr, nullptr, w.da, T, d, d, 0, 0, 1, 1, st));
-        RS_TRY(attention_bwd(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, st));
+        if (S <= 128)
+            RS_TRY(attention_bwd(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, st));
+        else
+            RS_TRY(attention_bwd_long(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, w.abw, w.abw_bytes, st));
         // QKV: qkv = x1 Wqkv^T + b
         sp = wgrad_splits(3 * d, d, T);
         RS_TRY(gemm_bf16_ex(w.dqkv, w.x1[l], nullptr, nullptr, w.wpart, 3 * d, d, T, 6, 1, 1, sp, st));
@@ -201,7 +211,7 @@ extern "C" size_t rs_ranker_grad_workspace_size(const rs_ranker_config* cfg, int
     const int P = lists_per_micro * list_len;
     const int64_t Tp = ((int64_t)P * S + 255) / 256 * 256;
     TrSizer s;
-    train_layout(s, *cfg, Tp, P, nullptr);
+    train_layout(s, *cfg, Tp, P, S, nullptr);
     return s.s.used + 4096;
 }
 
@@ -211,7 +221,7 @@ extern "C" int rs_ranker_grad(const rs_ranker_config* cfg, const void* params, f
                               size_t ws_bytes, void* stream) {
     cudaStream_t st = as_stream(stream);
     RS_CHECK_ARG(cfg && params && grad && ids && lengths && loss_out, "rs_ranker_grad: NULL argument");
-    RS_CHECK_ARG(n_lists > 0 && list_len >= 1 && S >= 1 && S <= 128, "rs_ranker_grad: need S <= 128 (got %d)", S);
+    RS_CHECK_ARG(n_lists > 0 && list_len >= 1 && S >= 1 && S <= 512, "rs_ranker_grad: need S <= 512 (got %d)", S);
     RS_CHECK_ARG(bucket_width >= 1, "bucket_width must be >= 1");
     RS_CHECK_ARG(lists_per_micro >= 1, "lists_per_micro must be >= 1");
     RS_CHECK_ARG(cfg->n_layers <= 63 && cfg->d_model == cfg->n_heads * 64, "rs_ranker_grad: bad config");
@@ -232,7 +242,7 @@ extern "C" int rs_ranker_grad(const rs_ranker_config* cfg, const void* params, f
         {
             const int Pm = lists_per_micro * list_len;
             const int64_t Tm = ((int64_t)Pm * S + 255) / 256 * 256;
-            train_layout(ar, *cfg, Tm, Pm, &w);
+            train_layout(ar, *cfg, Tm, Pm, S, &w);
         }
         const int32_t* mids = ids + (int64_t)l0 * list_len * S;
         const int32_t* mlen = lengths + (int64_t)l0 * list_len;
@@ -264,7 +274,7 @@ extern "C" size_t rs_ranker_grad_cls_workspace_size(const rs_ranker_config* cfg,
     const int P = prompts_per_micro;
     const int64_t Tp = ((int64_t)P * S + 255) / 256 * 256;
     TrSizer s;
-    train_layout(s, *cfg, Tp, P, nullptr, n_classes);
+    train_layout(s, *cfg, Tp, P, S, nullptr, n_classes);
     return s.s.used + 4096;
 }
 
@@ -276,7 +286,7 @@ extern "C" int rs_ranker_grad_cls(const rs_ranker_config* cfg, const void* param
     cudaStream_t st = as_stream(stream);
     RS_CHECK_ARG(cfg && params && grad && ids && labels && cls_w && cls_b && cls_grad && loss_out,
                  "rs_ranker_grad_cls: NULL argument");
-    RS_CHECK_ARG(n_prompts > 0 && S >= 1 && S <= 128, "rs_ranker_grad_cls: need S <= 128 (got %d)", S);
+    RS_CHECK_ARG(n_prompts > 0 && S >= 1 && S <= 512, "rs_ranker_grad_cls: need S <= 512 (got %d)", S);
     RS_CHECK_ARG(n_classes >= 2 && prompts_per_micro >= 1, "rs_ranker_grad_cls: need >= 2 classes");
     RS_CHECK_ARG(cfg->n_layers <= 63 && cfg->d_model == cfg->n_heads * 64, "rs_ranker_grad_cls: bad config");
     if (ws_bytes < rs_ranker_grad_cls_workspace_size(cfg, prompts_per_micro, S, n_classes)) {
@@ -294,7 +304,7 @@ extern "C" int rs_ranker_grad_cls(const rs_ranker_config* cfg, const void* param
         TrainWs w;
         {
             const int64_t Tm = ((int64_t)prompts_per_micro * S + 255) / 256 * 256;
-            train_layout(ar, *cfg, Tm, prompts_per_micro, &w, C);
+            train_layout(ar, *cfg, Tm, prompts_per_micro, S, &w, C);
         }
         const int32_t* mids = ids + (int64_t)p0 * S;
         const int32_t* mlast = last_pos ? last_pos + p0 : nullptr;

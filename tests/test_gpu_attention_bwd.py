@@ -1,4 +1,5 @@
-"""Attention backward (S <= 128) vs torch autograd in fp32."""
+"""Attention backward vs torch autograd in fp32: S <= 128 (rs_attention_bwd) and the
+blocked 128 < S <= 512 kernels (rs_attention_bwd_long)."""
 
 import pytest
 import torch
@@ -27,3 +28,38 @@ def test_attention_bwd_matches_autograd(B, S, H):
     err = (dqkv.float() - ref).abs().max().item()
     scale = ref.abs().max().item()
     assert err <= 3e-2 * max(1.0, scale), (err, scale)
+
+
+@pytest.mark.parametrize("B,S,H", [(2, 512, 4), (1, 300, 12), (3, 200, 2), (1, 129, 1), (4, 256, 12)])
+def test_attention_bwd_long_matches_autograd(B, S, H):
+    from paper_2408_15792_b200 import _lib
+    _lib.device()
+    g = torch.Generator(device="cuda").manual_seed(B * S + H + 7)
+    qkv = (torch.randn(B * S, 3 * H * 64, device="cuda", generator=g)).bfloat16()
+    dout = torch.randn(B * S, H * 64, device="cuda", generator=g).bfloat16()
+    att = torch.empty(B * S, H * 64, dtype=torch.bfloat16, device="cuda")
+    lib = _lib.load()
+    _lib.check(lib.rs_attention_fwd(qkv.data_ptr(), att.data_ptr(), B, S, H, _lib.stream_handle()))
+    dqkv = torch.full((B * S, 3 * H * 64), float("nan"), dtype=torch.bfloat16, device="cuda")
+    n_ws = lib.rs_attention_bwd_long_workspace_size(B, S, H)
+    ws = torch.empty(n_ws, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.rs_attention_bwd_long(qkv.data_ptr(), att.data_ptr(), dout.data_ptr(), dqkv.data_ptr(), B, S, H,
+                                         ws.data_ptr(), n_ws, _lib.stream_handle()), "rs_attention_bwd_long")
+    x = qkv.float().requires_grad_(True)
+    q, k, v = x.view(B, S, 3, H, 64).permute(2, 0, 3, 1, 4)
+    o = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
+    o.permute(0, 2, 1, 3).reshape(B * S, H * 64).backward(dout.float())
+    ref = x.grad
+    assert torch.isfinite(dqkv.float()).all()
+    err = (dqkv.float() - ref).abs().max().item()
+    scale = ref.abs().max().item()
+    assert err <= 3e-2 * max(1.0, scale), (err, scale)
+    rel = ((dqkv.float() - ref).norm() / ref.norm()).item()
+    assert rel <= 1e-2, rel
+
+
+def test_attention_bwd_long_rejects_out_of_range():
+    from paper_2408_15792_b200 import _lib
+    _lib.device()
+    lib = _lib.load()
+    assert lib.rs_attention_bwd_long(None, None, None, None, 1, 513, 1, None, 0, None) == _lib.RS_ERR_INVALID

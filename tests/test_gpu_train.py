@@ -106,7 +106,8 @@ def _ref_grads(model, cfg, ids, lengths, n_lists, list_len, emulate):
 _SHIFT_INVARIANT = ("head_b", "lnf_b")
 
 
-@pytest.mark.parametrize("S,list_len,n_lists,mb", [(64, 16, 4, 2), (128, 8, 3, 3), (100, 16, 2, 1)])
+@pytest.mark.parametrize("S,list_len,n_lists,mb", [(64, 16, 4, 2), (128, 8, 3, 3), (100, 16, 2, 1),
+                                                  (512, 4, 2, 1), (300, 8, 2, 2)])
 def test_gradient_matches_autograd(S, list_len, n_lists, mb):
     """rs_ranker_grad vs torch fp32 autograd on the same bf16-rounded parameters.
 
@@ -122,7 +123,7 @@ def test_gradient_matches_autograd(S, list_len, n_lists, mb):
     emulation itself (two independent bf16 noises: <= 2 x floor + 2e-3)."""
     from paper_2408_15792_b200.ranker import OptRanker, init_params
     from paper_2408_15792_b200.trainer import RankerTrainer
-    cfg = _small_cfg()
+    cfg = _small_cfg(max_pos=max(128, S))  # S > 128: the blocked attention backward
     params = init_params(cfg, seed=5)
     g = torch.Generator().manual_seed(6)
     for k in params:  # non-trivial LN / bias values
