@@ -16,6 +16,8 @@
 #include "common.cuh"
 #include "mergesort.cuh"
 #include "tau_fast.cuh"
+#include <cstdlib>
+#include <cstring>
 
 namespace rs {
 
@@ -378,6 +380,16 @@ extern "C" size_t rs_tau_workspace_size(int64_t n, int x_dtype, int y_dtype) {
 }
 
 namespace rs {
+// Below this many rows the general path's fixed launch chain beats the bucket path's
+// (measured on B200, tools/gpu_tau_cross.sh); RS_TAU_PATH=fast|general forces one.
+constexpr int64_t TAU_FAST_MIN_N = 1 << 18;
+static int tau_path_choice(int64_t n) {  // 1 = fast, 0 = general
+    if (const char* e = getenv("RS_TAU_PATH")) {
+        if (!strcmp(e, "fast")) return 1;
+        if (!strcmp(e, "general")) return 0;
+    }
+    return n >= TAU_FAST_MIN_N ? 1 : 0;
+}
 // Fast path (tau_fast.cu) on the raw 32-bit inputs, or on 32-bit dense-rank images of
 // 64-bit inputs. counts[5] = 2 afterwards when the general path is needed.
 static int tau_fast_path(const void* x, int xd, const void* y, int yd, uint32_t n, int64_t* counts, TauWs& w,
@@ -416,6 +428,7 @@ extern "C" int rs_tau_counts_fast(const void* x, int xd, const void* y, int yd, 
     Arena ar(ws, ws_bytes);
     TauWs w;
     tau_layout(ar, (uint64_t)n, is64(xd) || is64(yd), &w);
+    if (!tau_path_choice(n)) return tau_general(x, xd, y, yd, n, counts, w, st);  // sync-free as well
     const size_t used = align_up(ar.used, 256);
     return tau_fast_path(x, xd, y, yd, (uint32_t)n, counts, w, static_cast<char*>(ws) + used, ws_bytes - used, st);
 }
@@ -438,6 +451,7 @@ extern "C" int rs_tau_counts(const void* x, int xd, const void* y, int yd, int64
     Arena ar(ws, ws_bytes);
     TauWs w;
     tau_layout(ar, (uint64_t)n, is64(xd) || is64(yd), &w);
+    if (!tau_path_choice(n)) return tau_general(x, xd, y, yd, n, counts, w, st);
     const size_t used = align_up(ar.used, 256);
     RS_TRY(tau_fast_path(x, xd, y, yd, (uint32_t)n, counts, w, static_cast<char*>(ws) + used, ws_bytes - used, st));
     // Inside a stream capture the fast path is all that is recorded (counts[5] == 2 then

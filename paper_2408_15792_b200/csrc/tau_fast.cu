@@ -172,15 +172,29 @@ __global__ void __launch_bounds__(TF_T) tf_minmax(const void* __restrict__ x, in
         ymax = max(ymax, __shfl_xor_sync(0xffffffffu, ymax, o));
     }
     nan = __any_sync(0xffffffffu, nan);
-    if ((threadIdx.x & 31) == 0) {
-        atomicMax(&p->nxmin, nxmin);
-        atomicMax(&p->xmax, xmax);
-        atomicMax(&p->nymin, nymin);
-        atomicMax(&p->ymax, ymax);
-        if (nan) atomicOr(&p->nan, 1);
+    // block reduce, then one atomic per value per block (per-warp atomics on the same four
+    // words serialise at L2)
+    __shared__ uint32_t red[4][TF_T / 32];
+    __shared__ int rnan;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) rnan = 0;
+    __syncthreads();
+    if (lane == 0) {
+        red[0][wid] = nxmin;
+        red[1][wid] = xmax;
+        red[2][wid] = nymin;
+        red[3][wid] = ymax;
+        if (nan) rnan = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        uint32_t v = 0;
+        for (int k = 0; k < TF_T / 32; ++k) v = max(v, red[threadIdx.x][k]);
+        uint32_t* dst = threadIdx.x == 0 ? &p->nxmin : threadIdx.x == 1 ? &p->xmax : threadIdx.x == 2 ? &p->nymin : &p->ymax;
+        atomicMax(dst, v);
+        if (threadIdx.x == 0 && rnan) atomicOr(&p->nan, 1);
     }
 }
-
 
 // ---- tile-sorted scatter ---------------------------------------------------------------
 // One tile of up to TF_ST_TILE keys is counting-sorted by its 12-bit bin in shared memory
@@ -1048,7 +1062,7 @@ int tau_fast_counts(const void* x, int xd, const void* y, int yd, uint32_t n, in
     RS_CUDA(cudaMemsetAsync(w.p, 0, sizeof(TfParams), st));
     RS_CUDA(cudaMemsetAsync(w.acc, 0, 8 * sizeof(unsigned long long), st));
     {
-        const uint32_t g = std::min<uint32_t>((n / 4 + TF_T) / TF_T, (uint32_t)sms * 8);
+        const uint32_t g = std::min<uint32_t>((n / 4 + TF_T) / TF_T, (uint32_t)sms * 2);
         tf_minmax<<<g, TF_T, 0, st>>>(x, xd, y, yd, n, w.p);
         RS_LAUNCH_CHECK();
     }

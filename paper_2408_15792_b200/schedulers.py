@@ -209,7 +209,9 @@ class _Staging:
         total = in_bytes + out_bytes + 16
         self.in_bytes = in_bytes
         self.host = torch.empty(total, dtype=torch.uint8).pin_memory()
-        self.devbuf = torch.empty(total, dtype=torch.uint8, device=self.dev)
+        # zeroed once: the single D2H copy after a step also reads the unwritten tail of
+        # the run / promoted / demoted slots (never consumed, but defined for initcheck)
+        self.devbuf = torch.zeros(total, dtype=torch.uint8, device=self.dev)
         self.ws = torch.empty(max(_lib.load().rs_rank_step_workspace_size(cap),
                                   _lib.load().rs_arrival_rank_workspace_size(cap), 1),
                               dtype=torch.uint8, device=self.dev)

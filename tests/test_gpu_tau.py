@@ -185,9 +185,11 @@ def _fast_cases(rng):
 @pytest.mark.parametrize("case", ["normal", "bf16_ties", "near_one_split", "small_int_x", "all_x_equal",
                                   "all_y_equal", "huge_single", "crowded_two_values", "crowded_child_fallback", "f64_x_i64_y",
                                   "neg_zero", "tiny"])
-def test_tau_fast_path_vs_oracle(case):
+def test_tau_fast_path_vs_oracle(case, monkeypatch):
     """The bucket fast path (and its fallback) against the exhaustive pair oracle:
-    C, D, n1, n2, n3 bit-exact."""
+    C, D, n1, n2, n3 bit-exact (RS_TAU_PATH=fast: these sizes are below the crossover
+    where rs_tau_counts picks the fast path by itself)."""
+    monkeypatch.setenv("RS_TAU_PATH", "fast")
     from oracle import tau_c
     from paper_2408_15792_b200.ranking import tau_counts_device
     x, y = _fast_cases(np.random.default_rng(41))[case]
@@ -203,8 +205,9 @@ def test_tau_fast_path_vs_oracle(case):
         assert fast == got
 
 
-def test_tau_plan_counts_falls_back():
+def test_tau_plan_counts_falls_back(monkeypatch):
     """TauPlan replays the fast path only; counts() runs the general path when y is wide."""
+    monkeypatch.setenv("RS_TAU_PATH", "fast")
     from paper_2408_15792_b200 import ranking
     g = torch.Generator(device="cuda").manual_seed(6)
     x = torch.randn(200_000, device="cuda", generator=g)
@@ -215,13 +218,18 @@ def test_tau_plan_counts_falls_back():
 
 
 @pytest.mark.parametrize("n", [1 << 20, 1 << 26])
-def test_tau_fast_equals_general_large(n):
+def test_tau_fast_equals_general_large(n, monkeypatch):
     """At sizes with level-2 splits over many chunks, the fast path equals the general
-    path on the same ranks (y small vs y scaled past the 4096-value window)."""
+    path on the same inputs (forced by RS_TAU_PATH) and on the same ranks with y scaled past
+    the 4096-value window."""
     from paper_2408_15792_b200.ranking import tau_counts_device
     g = torch.Generator(device="cuda").manual_seed(n & 0xffff)
     x = torch.randn(n, device="cuda", generator=g)
     y = torch.randint(1, 2049, (n,), device="cuda", generator=g, dtype=torch.int32)
+    monkeypatch.setenv("RS_TAU_PATH", "fast")
     a = tau_counts_device(x, y, fast_only=True).cpu().tolist()
-    b = tau_counts_device(x, y * 100_000).cpu().tolist()
-    assert a[5] == 0 and a == b
+    monkeypatch.setenv("RS_TAU_PATH", "general")
+    b = tau_counts_device(x, y).cpu().tolist()
+    monkeypatch.delenv("RS_TAU_PATH")
+    c = tau_counts_device(x, y * 100_000).cpu().tolist()
+    assert a[5] == 0 and a == b and a[:2] == c[:2] and a[4] == c[4]

@@ -49,6 +49,12 @@ def main(which: str = "all"):
             ranking.kendall_tau_b(x, rng.integers(0, 50, n))                       # bucket fast path
             ranking.kendall_tau_b(x, rng.normal(size=n))                           # general y, f64
             ranking.kendall_tau_b(rng.integers(0, 9, n).astype(np.int64), x)       # 64-bit x
+        import os
+        os.environ["RS_TAU_PATH"] = "fast"  # the bucket path at sanitizer sizes (below its crossover)
+        for n in (5, 3000, 40_000):
+            x = rng.normal(size=n).astype(np.float32)
+            ranking.kendall_tau_b(x, rng.integers(0, 50, n))
+            ranking.kendall_tau_b(rng.integers(0, 9, n).astype(np.int64), rng.integers(0, 9, n))
         n = 40_000
         near1 = (1.0 + 1e-4 * rng.normal(size=n)).astype(np.float32)              # level-2 splits
         ranking.kendall_tau_b(near1, rng.integers(1, 2049, n))
@@ -57,6 +63,7 @@ def main(which: str = "all"):
             c = (one + rng.integers(0, width, n).astype(np.int32)).view(np.float32)
             c[:2] = (-1e30, 1e30)
             ranking.kendall_tau_b(c, rng.integers(1, 2049, n))
+        del os.environ["RS_TAU_PATH"]
         s = torch.randn(300, 64, dtype=torch.float64, device="cuda")
         o = torch.argsort(torch.rand(300, 64, device="cuda"), dim=1)
         ranking.list_mle_batched(s, o)
