@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "mergesort.cuh"
 #include <type_traits>
+#include <algorithm>
 
 namespace rs {
 
@@ -144,6 +145,9 @@ constexpr uint32_t SEL_MIN_N = 1u << 18;
 constexpr int SEL_THREADS = 1024;
 
 struct SelState {
+    uint32_t dom_ok;       // level 0 left <= dom_cap rows at or below its bucket: compact them
+    uint32_t compacted;    // the passes after level 1 read the compacted rows
+    uint32_t dom_overflow; // a CTA's slice of the compacted buffer overflowed: keep reading columns
     uint32_t level;        // next level to histogram
     uint32_t less;         // keys strictly below the current prefix bucket
     uint32_t done;         // 1: final level reached (prefix covers the k-th key)
@@ -221,26 +225,99 @@ __device__ __forceinline__ void soa64_value4(const SrcSoa64& s, uint32_t i, unsi
     }
 }
 // Row loop of the select kernels: 4-row vector steps for SrcSoa64 on aligned columns,
-// scalar rows otherwise (and for the tail).
+// scalar rows otherwise (and for the tail). Trip counts are warp-uniform (f gets a valid
+// flag) so f may use full-warp ballots.
 template <typename Src, typename F>
 __device__ __forceinline__ void sel_rows(const Src& src, uint32_t n, F&& f) {
     const uint32_t stride = gridDim.x * SEL_THREADS;
+    const uint32_t wbase = blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u), lane = threadIdx.x & 31u;
     uint32_t done = 0;
     if constexpr (std::is_same<Src, SrcSoa64>::value) {
         const bool al = ((reinterpret_cast<uintptr_t>(src.score) | reinterpret_cast<uintptr_t>(src.arrival_rank)) & 15u) == 0 &&
                         (reinterpret_cast<uintptr_t>(src.flags) & 3u) == 0;
         if (al) {
             const uint32_t n4 = n & ~3u;
-            for (uint32_t i = (blockIdx.x * SEL_THREADS + threadIdx.x) * 4u; i < n4; i += stride * 4u) {
-                unsigned __int128 v[4];
-                soa64_value4(src, i, v);
+            for (uint32_t i0 = wbase * 4u; i0 < n4; i0 += stride * 4u) {
+                const uint32_t i = i0 + lane * 4u;
+                const bool ok = i < n4;
+                unsigned __int128 v[4] = {0, 0, 0, 0};
+                if (ok) soa64_value4(src, i, v);
 #pragma unroll
-                for (int k = 0; k < 4; ++k) f(i + k, v[k]);
+                for (int k = 0; k < 4; ++k) f(i + k, v[k], ok);
             }
             done = n4;
         }
     }
-    for (uint32_t i = done + blockIdx.x * SEL_THREADS + threadIdx.x; i < n; i += stride) f(i, src.value(i));
+    for (uint32_t i0 = done + wbase; i0 < n; i0 += stride) {
+        const uint32_t i = i0 + lane;
+        const bool ok = i < n;
+        f(i, ok ? src.value(i) : (unsigned __int128)0, ok);
+    }
+}
+// Like sel_rows, but hands f up to four consecutive rows per lane at once (i0, values,
+// count); warp-uniform trip counts.
+template <typename Src, typename F>
+__device__ __forceinline__ void sel_rows4(const Src& src, uint32_t n, F&& f) {
+    const uint32_t stride = gridDim.x * SEL_THREADS;
+    const uint32_t wbase = blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u), lane = threadIdx.x & 31u;
+    uint32_t done = 0;
+    if constexpr (std::is_same<Src, SrcSoa64>::value) {
+        const bool al = ((reinterpret_cast<uintptr_t>(src.score) | reinterpret_cast<uintptr_t>(src.arrival_rank)) & 15u) == 0 &&
+                        (reinterpret_cast<uintptr_t>(src.flags) & 3u) == 0;
+        if (al) {
+            const uint32_t n4 = n & ~3u;
+            for (uint32_t i0 = wbase * 4u; i0 < n4; i0 += stride * 4u) {
+                const uint32_t i = i0 + lane * 4u;
+                unsigned __int128 v[4] = {0, 0, 0, 0};
+                const int nv = i < n4 ? 4 : 0;
+                if (nv) soa64_value4(src, i, v);
+                f(i, v, nv);
+            }
+            done = n4;
+        }
+    }
+    for (uint32_t i0 = done + wbase; i0 < n; i0 += stride) {
+        const uint32_t i = i0 + lane;
+        unsigned __int128 v[4] = {0, 0, 0, 0};
+        const int nv = i < n ? 1 : 0;
+        if (nv) v[0] = src.value(i);
+        f(i, v, nv);
+    }
+}
+// Rows already filtered by the level-1 pass: (value, row) pairs, one slice of `capc` per
+// CTA (the select kernels keep the same grid, so CTA c re-reads the rows it kept).
+struct SrcBuf {
+    const unsigned __int128* v;
+    const uint32_t* idx;
+    const uint32_t* cnt;
+    uint32_t capc;
+};
+template <typename F>
+__device__ __forceinline__ void buf_rows(const SrcBuf& b, F&& f) {
+    const uint32_t n = b.cnt[blockIdx.x];
+    const size_t off = (size_t)blockIdx.x * b.capc;
+    for (uint32_t i0 = threadIdx.x & ~31u; i0 < n; i0 += SEL_THREADS) {
+        const uint32_t i = i0 + (threadIdx.x & 31u);
+        const bool ok = i < n;
+        f(ok ? b.idx[off + i] : 0u, ok ? b.v[off + i] : (unsigned __int128)0, ok);
+    }
+}
+// warp-aggregated append of (v, row) for the lanes with p set
+__device__ __forceinline__ void sel_append(bool p, unsigned __int128 v, uint32_t row, uint32_t* counter,
+                                           unsigned __int128* ov, uint32_t* oi, uint32_t cap) {
+    const unsigned b = __ballot_sync(0xffffffffu, p);
+    if (!b) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(b) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(counter, (uint32_t)__popc(b));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (p) {
+        const uint32_t pos = base + (uint32_t)__popc(b & ((1u << lane) - 1u));
+        if (pos < cap) {
+            ov[pos] = v;
+            oi[pos] = row;
+        }
+    }
 }
 
 template <typename Src>
@@ -249,22 +326,78 @@ __device__ __forceinline__ uint32_t sel_digit(unsigned __int128 v, uint32_t leve
 }
 
 template <typename Src>
-__device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c);
+__device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c,
+                               uint32_t dom_cap);
 
 template <typename Src>
 __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, SelState* __restrict__ st,
                                                         unsigned __int128* __restrict__ pfx128,
-                                                        uint32_t* __restrict__ hist, uint32_t k) {
+                                                        uint32_t* __restrict__ hist, uint32_t k,
+                                                        unsigned __int128* __restrict__ dom_v,
+                                                        uint32_t* __restrict__ dom_i, uint32_t* __restrict__ dom_cnt,
+                                                        uint32_t dom_cap) {
     if (st->done) return;
     __shared__ uint32_t h[SEL_BINS];
+    __shared__ uint32_t scnt;
     for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) h[b] = 0;
+    if (threadIdx.x == 0) scnt = 0;
     __syncthreads();
+    const uint32_t capc = dom_cap / gridDim.x;
     const uint32_t level = st->level;
     const unsigned __int128 want = *pfx128;  // prefix digits in place (lower bits zero)
     const int shift = Src::BITS - SEL_BITS * (int)level;
-    sel_rows(src, n, [&](uint32_t, unsigned __int128 v) {
-        if (level == 0 || (v >> shift) == (want >> shift)) atomicAdd(&h[sel_digit<Src>(v, level)], 1u);
-    });
+    if (st->compacted) {
+        buf_rows(SrcBuf{dom_v, dom_i, dom_cnt, capc}, [&](uint32_t, unsigned __int128 v, bool ok) {
+            if (ok && (v >> shift) == (want >> shift)) atomicAdd(&h[sel_digit<Src>(v, level)], 1u);
+        });
+    } else if (level == 1 && st->dom_ok) {
+        // level 1 over all rows also keeps every row at or below the level-0 bucket (all
+        // candidates: the passes after this one read only them), in this CTA's slice
+        const size_t off = (size_t)blockIdx.x * capc;
+        const unsigned __int128 wsh = want >> shift;
+        sel_rows4(src, n, [&](uint32_t i0, const unsigned __int128 (&v)[4], int nv) {
+            // the lane's kept rows (<= 4), one warp scan + one shared atomic per warp
+            uint32_t keep = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const unsigned __int128 t = v[k] >> shift;
+                if (k < nv && t <= wsh) keep |= 1u << k;
+                if (k < nv && t == wsh) atomicAdd(&h[sel_digit<Src>(v[k], level)], 1u);
+            }
+            const uint32_t c = __popc(keep);
+            uint32_t x = c;
+            const uint32_t lane = threadIdx.x & 31u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+            if (!tot) return;
+            uint32_t base = 0;
+            if (lane == 31) base = atomicAdd(&scnt, tot);
+            base = __shfl_sync(0xffffffffu, base, 31) + x - c;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (keep >> k & 1u) {
+                    if (base < capc) {
+                        dom_v[off + base] = v[k];
+                        dom_i[off + base] = i0 + k;
+                    }
+                    ++base;
+                }
+            }
+        });
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            dom_cnt[blockIdx.x] = min(scnt, capc);
+            if (scnt > capc) atomicOr(&st->dom_overflow, 1u);
+        }
+    } else {
+        sel_rows(src, n, [&](uint32_t, unsigned __int128 v, bool ok) {
+            if (ok && (level == 0 || (v >> shift) == (want >> shift))) atomicAdd(&h[sel_digit<Src>(v, level)], 1u);
+        });
+    }
     __syncthreads();
     for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS)
         if (h[b]) atomicAdd(&hist[b], h[b]);
@@ -276,14 +409,16 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, Sel
     __syncthreads();
     if (last) {
         __threadfence();
-        sel_pick_block<Src>(st, pfx128, hist, k, h);
+        if (threadIdx.x == 0 && level == 1 && st->dom_ok && !st->dom_overflow) st->compacted = 1;
+        sel_pick_block<Src>(st, pfx128, hist, k, h, dom_cap);
     }
 }
 
 // One block: choose the bucket holding the k-th key from the level's global histogram
 // (c = shared scratch of SEL_BINS words), clear the histogram for the next level.
 template <typename Src>
-__device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c) {
+__device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c,
+                               uint32_t dom_cap) {
     __shared__ uint32_t pick, below;
     for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) c[b] = __ldcg(&hist[b]);
     __syncthreads();
@@ -320,6 +455,7 @@ __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t
         st->less += below;
         st->level = level + 1;
         st->arrived = 0;
+        if (level == 0) st->dom_ok = (st->less + c[pick] <= dom_cap) ? 1u : 0u;
         if (c[pick] <= SEL_CAP || level + 1 == Src::LEVELS) {
             st->done = 1;
             st->final_level = level + 1;
@@ -331,18 +467,19 @@ __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t
 template <typename Src>
 __global__ void __launch_bounds__(SEL_THREADS) sel_gather(Src src, uint32_t n, SelState* __restrict__ st,
                                                           const unsigned __int128* __restrict__ pfx128,
-                                                          unsigned __int128* __restrict__ ck, uint32_t* __restrict__ ci) {
+                                                          unsigned __int128* __restrict__ ck, uint32_t* __restrict__ ci,
+                                                          const unsigned __int128* __restrict__ dom_v,
+                                                          const uint32_t* __restrict__ dom_i,
+                                                          const uint32_t* __restrict__ dom_cnt, uint32_t dom_cap) {
     const int shift = Src::BITS - SEL_BITS * (int)st->final_level;
     const unsigned __int128 lim = *pfx128 >> shift;
-    sel_rows(src, n, [&](uint32_t i, unsigned __int128 v) {
-        if ((v >> shift) <= lim) {
-            const uint32_t slot = atomicAdd(&st->n_cand, 1u);
-            if (slot < SEL_SORT) {
-                ck[slot] = v;
-                ci[slot] = i;
-            }
-        }
-    });
+    auto take = [&](uint32_t i, unsigned __int128 v, bool ok) {
+        sel_append(ok && (v >> shift) <= lim, v, i, &st->n_cand, ck, ci, SEL_SORT);
+    };
+    if (st->compacted)
+        buf_rows(SrcBuf{dom_v, dom_i, dom_cnt, dom_cap / gridDim.x}, take);
+    else
+        sel_rows(src, n, take);
 }
 
 // one block: sort the <= SEL_SORT candidates (bitonic, smem), emit the first k in order
@@ -754,6 +891,10 @@ struct RankWs {
     uint32_t* hist;
     unsigned __int128* ck;
     uint32_t* ci;
+    unsigned __int128* dv;
+    uint32_t* di;
+    uint32_t* dcnt;
+    uint32_t dcap;
     int* splits;
 };
 template <typename A>
@@ -773,8 +914,13 @@ static void rank_layout(A& a, uint64_t n, RankWs* w) {
     auto hi = a.template take<uint32_t>(SEL_BINS);
     auto ck = a.template take<unsigned __int128>(SEL_SORT);
     auto ci = a.template take<uint32_t>(SEL_SORT);
+    // rows kept by the select's level-1 pass (at most 4M: beyond, the passes read the columns)
+    const uint32_t dcap = (uint32_t)std::min<uint64_t>(n, 1u << 22);
+    auto dv = a.template take<unsigned __int128>(n > SEL_MIN_N ? dcap : 1);
+    auto di = a.template take<uint32_t>(n > SEL_MIN_N ? dcap : 1);
+    auto dc = a.template take<uint32_t>(1024);  // per-CTA kept-row counts (grid <= 1024)
     auto sp = a.template take<int>(ms_splits(np));
-    if (w) *w = RankWs{ka, kb, va, vb, sc, pd, bc, er, sl, px, hi, ck, ci, sp};
+    if (w) *w = RankWs{ka, kb, va, vb, sc, pd, bc, er, sl, px, hi, ck, ci, dv, di, dc, n > SEL_MIN_N ? dcap : 0u, sp};
 }
 struct RankSizer {
     ArenaSizer s;
@@ -870,19 +1016,19 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
             // keys straight from the queue columns: no key pass, 9 B per row per level
             const SrcSoa64 src{static_cast<const float*>(q->score), q->flags, q->arrival_rank, preemptive, counts + 3};
             for (int level = 0; level < SrcSoa64::LEVELS; ++level) {
-                sel_hist<SrcSoa64><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.hist, k);
+                sel_hist<SrcSoa64><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.hist, k, w.dv, w.di, w.dcnt, w.dcap);
                 RS_LAUNCH_CHECK();
             }
-            sel_gather<SrcSoa64><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.ck, w.ci);
+            sel_gather<SrcSoa64><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.ck, w.ci, w.dv, w.di, w.dcnt, w.dcap);
         } else {
             build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
             RS_LAUNCH_CHECK();
             const SrcKeys src{w.kb};
             for (int level = 0; level < SrcKeys::LEVELS; ++level) {
-                sel_hist<SrcKeys><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.hist, k);
+                sel_hist<SrcKeys><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.hist, k, w.dv, w.di, w.dcnt, w.dcap);
                 RS_LAUNCH_CHECK();
             }
-            sel_gather<SrcKeys><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.ck, w.ci);
+            sel_gather<SrcKeys><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.ck, w.ci, w.dv, w.di, w.dcnt, w.dcap);
         }
         RS_LAUNCH_CHECK();
         sel_sort_emit<<<1, SEL_THREADS, smem, st>>>(w.ck, w.ci, w.sel, q->id, k, run, w.sched, counts);
