@@ -182,6 +182,11 @@ __device__ __forceinline__ float fast_ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float fast_lg2(float x) {
     float y;
     asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -412,6 +417,74 @@ __device__ __forceinline__ void listmle64_one(const float* __restrict__ gnet, co
     listmle64_scan(t0, t1, v0, v1, L, inv, s0, s1, loss_out + list, dg_out + (size_t)list * L);
 }
 
+// 64 16-bit keys over an 8-lane group (lanes hl = 0..7 of the group, partner lanes by
+// shfl_xor with masks < 8), 8 keys per lane in 4 registers: sorted position p = 8 hl + e
+// lives in register e & 3, half e >> 2. The network is the all-ascending form of bitonic
+// sort — each merge of width k starts with a "flip" stage (p against p ^ (k - 1)) followed
+// by half-cleaners (p against p ^ j), and every comparator puts the minimum at the lower
+// position — so the in-lane stages need no direction selects: j = 1 and j = 2 compare whole
+// registers (min/max of both halves at once), j = 4 the two halves of one register.
+__device__ __forceinline__ uint32_t hswap(uint32_t x) { return __byte_perm(x, 0, 0x1032); }
+__device__ __forceinline__ void cas16x2(uint32_t& a, uint32_t& b) {  // a <- min, b <- max (per half)
+    const uint32_t mn = vmin16x2(a, b), mx = vmax16x2(a, b);
+    a = mn;
+    b = mx;
+}
+__device__ __forceinline__ void sort64_flip8(uint32_t (&R)[4], int hl) {
+    // j = 4 half-cleaner: low half (e) gets the min, high half (e + 4) the max
+    auto j4 = [&]() {
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t S = hswap(R[r]);
+            R[r] = __byte_perm(vmin16x2(R[r], S), vmax16x2(R[r], S), 0x7610);
+        }
+    };
+    auto j2 = [&]() { cas16x2(R[0], R[2]); cas16x2(R[1], R[3]); };
+    auto j1 = [&]() { cas16x2(R[0], R[1]); cas16x2(R[2], R[3]); };
+    auto xlane = [&](int m, bool lower) {  // half-cleaner across lanes hl, hl ^ m
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t O = __shfl_xor_sync(0xffffffffu, R[r], m);
+            R[r] = lower ? vmin16x2(R[r], O) : vmax16x2(R[r], O);
+        }
+    };
+    auto xflip = [&](int m, bool lower) {  // e <-> 7 - e of lane hl ^ m: partner's R[3 - r], halves swapped
+        uint32_t O[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) O[r] = __shfl_xor_sync(0xffffffffu, R[3 - r], m);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uint32_t S = hswap(O[r]);
+            R[r] = lower ? vmin16x2(R[r], S) : vmax16x2(R[r], S);
+        }
+    };
+    // k = 2: flip = j1;  k = 4: flip e <-> 3 - e, then j1
+    j1();
+    cas16x2(R[0], R[3]);
+    cas16x2(R[1], R[2]);
+    j1();
+    // k = 8: flip e <-> 7 - e inside the lane: (R0, R3) and (R1, R2) with halves crossed
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const uint32_t S = hswap(R[3 - r]);
+        const uint32_t mn = vmin16x2(R[r], S), mx = vmax16x2(R[r], S);
+        R[r] = __byte_perm(mn, mx, 0x7610);      // {e_r, e_{r+4}}       = {mn.lo, mx.hi}
+        R[3 - r] = __byte_perm(mn, mx, 0x5432);  // {e_{3-r}, e_{7-r}} = {mn.hi, mx.lo}
+    }
+    j2();
+    j1();
+    // k = 16, 32, 64: flip across lanes, cross-lane half-cleaners, then the in-lane ones
+    xflip(1, (hl & 1) == 0);
+    j4(); j2(); j1();
+    xflip(3, (hl & 2) == 0);
+    xlane(1, (hl & 1) == 0);
+    j4(); j2(); j1();
+    xflip(7, (hl & 4) == 0);
+    xlane(2, (hl & 2) == 0);
+    xlane(1, (hl & 1) == 0);
+    j4(); j2(); j1();
+}
+
 // LPW lists per warp (32 / LPW lanes x 64 * LPW / 32 items each) for the common case —
 // labels < 1023 and score ranges within the shifted-sum bound — so the shuffle stages of
 // the sort and of both scans serve LPW lists at once and the first log2(items) stages of
@@ -420,16 +493,19 @@ __device__ __forceinline__ void listmle64_one(const float* __restrict__ gnet, co
 // p / IPL of its group, packed register (p % IPL) / 2, 16-bit half p % 2.
 // W > 0: the bucket width as a compile-time constant (the training default, 10: the floor
 // division becomes a multiply-shift); W == 0: runtime `width`.
-template <int LPW, int W>
+// LC > 0: the list length as a compile-time constant (the cfg3 shape, 64: every validity
+// test folds away); LC == 0: runtime `L_rt`.
+template <int LPW, int W, int LC>
 __global__ void __launch_bounds__(256) listmle_lengths64xN_kernel(const float* __restrict__ gnet,
                                                                   const int32_t* __restrict__ lengths, int n_lists,
-                                                                  int L, int width_rt, float* __restrict__ loss_out,
+                                                                  int L_rt, int width_rt, float* __restrict__ loss_out,
                                                                   float* __restrict__ dg_out) {
+    const int L = LC > 0 ? LC : L_rt;
     constexpr int LANES = 32 / LPW, IPL = 64 / LANES, NR = IPL / 2;
     static_assert(IPL >= 2 && IPL % 2 == 0, "two 16-bit keys per register");
     const int width = W > 0 ? W : width_rt;
     constexpr float LOG2E = 1.4426950408889634f, LN2 = 0.6931471805599453f;
-    __shared__ float sg[8][LPW][64];  // per warp, per list: the scores (base-2 units)
+    __shared__ __align__(16) float sg[8][LPW][64];  // per warp, per list: the scores (base-2 units)
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, sub = lane / LANES, hl = lane % LANES;
     const int warps_total = gridDim.x * (blockDim.x >> 5);
     const float inv = 1.0f / (float)L;
@@ -467,10 +543,16 @@ __global__ void __launch_bounds__(256) listmle_lengths64xN_kernel(const float* _
             const bool valid = live && i < L;
             ok &= !valid || (lab >= 0 && lab < 1023);
             const uint32_t key = valid ? (((uint32_t)lab << 6) | (uint32_t)i) : 0xFFFFu;
-            if (e & 1) R[e >> 1] |= key << 16; else R[e >> 1] = key;
+            if constexpr (IPL == 8) {  // sort64_flip8 layout: register e & 3, half e >> 2
+                if (e >> 2) R[e & 3] |= key << 16; else R[e & 3] = key;
+            } else {
+                if (e & 1) R[e >> 1] |= key << 16; else R[e >> 1] = key;
+            }
             sg[wid][sub][i] = gv[e] * LOG2E;
         }
-        if (__all_sync(0xffffffffu, ok)) {
+        if constexpr (IPL == 8) {
+            if (__all_sync(0xffffffffu, ok)) sort64_flip8(R, hl);
+        } else if (__all_sync(0xffffffffu, ok)) {
 #pragma unroll
             for (int k = 2; k <= 64; k <<= 1) {
 #pragma unroll
@@ -513,8 +595,10 @@ __global__ void __launch_bounds__(256) listmle_lengths64xN_kernel(const float* _
         float M = LSE2_NONE, mneg = LSE2_NONE;
 #pragma unroll
         for (int e = 0; e < IPL; ++e) {
-            sidx[e] = (int)((R[e >> 1] >> (16 * (e & 1))) & 63);
-            v[e] = live && IPL * hl + e < L;
+            sidx[e] = IPL == 8 ? (int)((R[e & 3] >> (16 * (e >> 2))) & 63) : (int)((R[e >> 1] >> (16 * (e & 1))) & 63);
+            // L == 64: a dead group (past n_lists) computes on zeros (its shuffles stay inside
+            // its own lanes) and stores nothing, so no per-item masks
+            v[e] = LC == 64 ? true : (live && IPL * hl + e < L);
             t[e] = v[e] ? sg[wid][sub][sidx[e]] : LSE2_NONE;
             M = fmaxf(M, v[e] ? t[e] : LSE2_NONE);
             mneg = fmaxf(mneg, v[e] ? -t[e] : LSE2_NONE);
@@ -546,26 +630,33 @@ __global__ void __launch_bounds__(256) listmle_lengths64xN_kernel(const float* _
         }
         float tail = __shfl_down_sync(0xffffffffu, x, 1);
         if (hl == LANES - 1) tail = 0.f;
-        float lse[IPL], part = 0.f;
+        // In units of the suffix sums s_e = sfx_e + tail (= 2^(lse_e - M)):
+        //   lse_e - t_e          = lg2(s_e) - (t_e - M)                         (the loss terms)
+        //   2^(-lse_e - Mu)      = s_last / s_e,  Mu = -lse_{L-1}, s_last = w_{L-1}
+        //   2^(t_e + L_e)        = w_e * (head + c_e) / s_last   (L_e = Mu + lg2(head + c_e))
+        // so the second scan and the gradient need one reciprocal per item and no ex2 / lg2
+        float sv[IPL], pl = 0.f, pt = 0.f;
 #pragma unroll
         for (int e = 0; e < IPL; ++e) {
-            lse[e] = M + fast_lg2(sfx[e] + tail);
-            part += v[e] ? lse[e] - t[e] : 0.f;
+            sv[e] = sfx[e] + tail;
+            pl += v[e] ? fast_lg2(sv[e]) : 0.f;
+            pt += v[e] ? t[e] - M : 0.f;
         }
+        float part = pl - pt;
 #pragma unroll
         for (int o = LANES / 2; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        // prefix sums of 2^(-lse - Mu), Mu = -lse of the last item (lse_{L-1} = t_{L-1})
         const int lastl = (L - 1) / IPL, laste = (L - 1) % IPL;
-        float lastv = lse[0];
+        float lastv = w[0];
 #pragma unroll
         for (int e = 1; e < IPL; ++e)
-            if (e == laste) lastv = lse[e];
-        const float Mu = -__shfl_sync(0xffffffffu, lastv, sub * LANES + lastl);
+            if (e == laste) lastv = w[e];
+        const float s_last = __shfl_sync(0xffffffffu, lastv, sub * LANES + lastl);
+        const float r_last = fast_rcp(s_last);
         float c[IPL];
         float acc = 0.f;
 #pragma unroll
         for (int e = 0; e < IPL; ++e) {
-            acc += v[e] ? fast_ex2(-lse[e] - Mu) : 0.f;
+            acc += v[e] ? s_last * fast_rcp(sv[e]) : 0.f;
             c[e] = acc;
         }
         x = acc;
@@ -576,10 +667,28 @@ __global__ void __launch_bounds__(256) listmle_lengths64xN_kernel(const float* _
         }
         float head = __shfl_up_sync(0xffffffffu, x, 1);
         if (hl == 0) head = 0.f;
-        float* dg = dg_out + (size_t)list * L;
+        float gr[IPL];
 #pragma unroll
-        for (int e = 0; e < IPL; ++e)
-            if (v[e]) dg[sidx[e]] = (fast_ex2(t[e] + Mu + fast_lg2(head + c[e])) - 1.f) * inv;
+        for (int e = 0; e < IPL; ++e) gr[e] = fmaf(w[e] * r_last, head + c[e], -1.f) * inv;
+        float* dg = dg_out + (size_t)list * L;
+        if constexpr (LC == 64 && IPL % 4 == 0) {
+            // scatter into the list's smem row (every score has been read: sg is free), then
+            // each lane stores its own IPL contiguous items as 16-B vectors
+            __syncwarp();
+#pragma unroll
+            for (int e = 0; e < IPL; ++e) sg[wid][sub][sidx[e]] = gr[e];
+            __syncwarp();
+            if (live) {
+#pragma unroll
+                for (int q = 0; q < IPL / 4; ++q)
+                    __stcs(reinterpret_cast<float4*>(dg + IPL * hl) + q,
+                           *reinterpret_cast<const float4*>(&sg[wid][sub][IPL * hl + 4 * q]));
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < IPL; ++e)
+                if (v[e]) dg[sidx[e]] = gr[e];
+        }
         if (live && hl == 0) loss_out[list] = part * LN2 * inv;
         __syncwarp();  // sg is reused by the next group
     }
@@ -635,10 +744,12 @@ extern "C" int rs_listmle_lengths(const float* g, const int32_t* lengths, int32_
         constexpr int LPW = 4;
         const int groups = (n_lists + LPW - 1) / LPW;
         const int blocks = (groups + 7) / 8 < n_sm * 8 ? (groups + 7) / 8 : n_sm * 8;
-        if (width == 10)
-            listmle_lengths64xN_kernel<LPW, 10><<<blocks, 256, 0, st>>>(g, lengths, n_lists, L, width, loss, dg);
+        if (width == 10 && L == 64)
+            listmle_lengths64xN_kernel<LPW, 10, 64><<<blocks, 256, 0, st>>>(g, lengths, n_lists, L, width, loss, dg);
+        else if (width == 10)
+            listmle_lengths64xN_kernel<LPW, 10, 0><<<blocks, 256, 0, st>>>(g, lengths, n_lists, L, width, loss, dg);
         else
-            listmle_lengths64xN_kernel<LPW, 0><<<blocks, 256, 0, st>>>(g, lengths, n_lists, L, width, loss, dg);
+            listmle_lengths64xN_kernel<LPW, 0, 0><<<blocks, 256, 0, st>>>(g, lengths, n_lists, L, width, loss, dg);
         RS_LAUNCH_CHECK();
         return RS_OK;
     }
