@@ -13,6 +13,7 @@
 // Device pipeline: key build -> stable merge sort of (RankKey, index) -> greedy fill
 // (one warp; prefix-sum resolution of each 32-wide chunk) -> elementwise state update
 // with order-preserving compaction of promoted / demoted ids.
+#include <utility>
 #include "common.cuh"
 #include "mergesort.cuh"
 #include <type_traits>
@@ -143,6 +144,10 @@ constexpr int SEL_SORT = 4096;  // >= max_batch + SEL_CAP, power of two
 // engine loop's queues (10^3-10^5 rows) are all below it, cfg4's 1M queue is above.
 constexpr uint32_t SEL_MIN_N = 1u << 18;
 constexpr int SEL_THREADS = 1024;
+constexpr int SEL_PHASE_A = 8;  // level-0 chunks per warp counted before the CTA's bin bound is fixed
+// level 0 keeps its candidates only for queues this large (smaller ones: the level-1 pass
+// over the columns is cheaper than level 0's second read of its phase-A rows)
+constexpr uint32_t SEL_L0_KEEP_N = 1u << 23;
 
 struct SelState {
     uint32_t dom_ok;       // level 0 left <= dom_cap rows at or below its bucket: compact them
@@ -160,8 +165,11 @@ struct SelState {
 // RankingPolicy sort order, left-aligned in BITS bits (digit L = bits
 // [BITS - 11 (L + 1), BITS - 11 L)).
 // SrcKeys: materialised 96-bit RankKeys [class:3 | eff(f64 image):64 | rank:29] << 3.
+// V: the value type the kernels compute in; the value's virtual BITS-bit image is
+// (V)value << PAD (SrcSoa64 works in 64-bit registers: no 128-bit shifts per row).
 struct SrcKeys {
-    static constexpr int BITS = 99, LEVELS = 9;
+    using V = unsigned __int128;
+    static constexpr int BITS = 99, LEVELS = 9, PAD = 0;
     const RankKey* keys;
     __device__ __forceinline__ unsigned __int128 value(uint32_t i) const {
         const RankKey k = keys[i];
@@ -175,13 +183,14 @@ struct SrcKeys {
 // length calibrated): [class:3 | f32 image:32 | rank:29] << 2. The f32 -> f64 cast is
 // monotone and injective, so this orders exactly like the 96-bit key.
 struct SrcSoa64 {
-    static constexpr int BITS = 66, LEVELS = 6;
+    using V = uint64_t;
+    static constexpr int BITS = 66, LEVELS = 6, PAD = 2;
     const float* score;
     const uint8_t* flags;
     const uint32_t* arrival_rank;
     int preemptive;
     int* err;
-    __device__ __forceinline__ unsigned __int128 value(uint32_t i) const {
+    __device__ __forceinline__ uint64_t value(uint32_t i) const {
         const uint8_t f = flags[i];
         const bool scored = f & RS_FLAG_SCORED;
         const bool prio = f & RS_FLAG_PRIORITY;
@@ -193,15 +202,23 @@ struct SrcSoa64 {
         }
         const uint32_t pin = preemptive ? 0u : (running ? 0u : 1u);
         const uint32_t cls = (pin << 2) | ((scored ? 1u : 0u) << 1) | (prio ? 0u : 1u);
-        const uint64_t v = ((uint64_t)cls << 61) | ((uint64_t)orderable_f32(s) << 29) |
-                           (uint64_t)(arrival_rank[i] & RANK_MASK);
-        return (unsigned __int128)v << 2;
+        return ((uint64_t)cls << 61) | ((uint64_t)orderable_f32(s) << 29) | (uint64_t)(arrival_rank[i] & RANK_MASK);
     }
 };
+// (virtual value) >> s, computed in V
+template <typename Src>
+__device__ __forceinline__ typename Src::V vshr(typename Src::V v, int s) {
+    if (s - Src::PAD >= (int)(8 * sizeof(v))) return 0;
+    return s >= Src::PAD ? (v >> (s - Src::PAD)) : (v << (Src::PAD - s));
+}
+template <typename Src>
+__device__ __forceinline__ unsigned __int128 to128(typename Src::V v) {
+    return (unsigned __int128)v << Src::PAD;
+}
 
 // Four consecutive rows i..i+3 (i % 4 == 0, all < n, 16-B aligned columns): one 16-B load
 // of scores and of arrival ranks, one 4-B load of flags.
-__device__ __forceinline__ void soa64_value4(const SrcSoa64& s, uint32_t i, unsigned __int128 (&v)[4]) {
+__device__ __forceinline__ void soa64_value4(const SrcSoa64& s, uint32_t i, uint64_t (&v)[4]) {
     const float4 sc = *reinterpret_cast<const float4*>(s.score + i);
     const uint4 ar = *reinterpret_cast<const uint4*>(s.arrival_rank + i);
     const uint32_t fl = *reinterpret_cast<const uint32_t*>(s.flags + i);
@@ -220,9 +237,50 @@ __device__ __forceinline__ void soa64_value4(const SrcSoa64& s, uint32_t i, unsi
         }
         const uint32_t pin = s.preemptive ? 0u : (running ? 0u : 1u);
         const uint32_t cls = (pin << 2) | ((scored ? 1u : 0u) << 1) | (prio ? 0u : 1u);
-        const uint64_t w = ((uint64_t)cls << 61) | ((uint64_t)orderable_f32(x) << 29) | (uint64_t)(arv[k] & RANK_MASK);
-        v[k] = (unsigned __int128)w << 2;
+        v[k] = ((uint64_t)cls << 61) | ((uint64_t)orderable_f32(x) << 29) | (uint64_t)(arv[k] & RANK_MASK);
     }
+}
+// Class bits of the four rows of a packed flag word, one per byte (bit 2: not pinned,
+// bit 1: scored, bit 0: not priority) — the RankingPolicy class order of SrcSoa64::value.
+__device__ __forceinline__ uint32_t soa64_classes(uint32_t fw, int preemptive) {
+    const uint32_t s1 = (fw & 0x01010101u) << 1;
+    const uint32_t s0 = (~fw >> 1) & 0x01010101u;
+    const uint32_t s2 = preemptive ? 0u : (~fw & 0x04040404u);
+    return s2 | s1 | s0;
+}
+// Order-preserving image of a row's effective score (0 for unscored rows; -0.0 -> +0.0);
+// NaN scores are OR-ed into nan.
+__device__ __forceinline__ uint32_t soa64_img(float sc, bool scored, bool& nan) {
+    const float x = scored ? sc + 0.0f : 0.0f;  // + 0.0f: -0.0 -> +0.0 (as orderable_f32)
+    nan |= x != x;
+    const uint32_t b = __float_as_uint(x);
+    return b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
+}
+// The top 32 bits of the SoA key, (class << 29) | (f32 image >> 3), of four consecutive
+// rows (aligned, all < n) from one 16-B score load and one 4-B flag load (no arrival
+// ranks); lo (optional) gets the key's low word without the rank, img << 29.
+__device__ __forceinline__ void soa64_hi4(const SrcSoa64& s, uint32_t i, uint32_t (&hi)[4], uint32_t* lo = nullptr) {
+    const float4 sc = *reinterpret_cast<const float4*>(s.score + i);
+    const uint32_t fl = *reinterpret_cast<const uint32_t*>(s.flags + i);
+    const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
+    const uint32_t C = soa64_classes(fl, s.preemptive);
+    bool nan = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const uint32_t img = soa64_img(scv[k], (fl >> (8 * k)) & RS_FLAG_SCORED, nan);
+        hi[k] = (((C >> (8 * k)) & 7u) << 29) | (img >> 3);
+        if (lo) lo[k] = img << 29;
+    }
+    if (nan) atomicOr(s.err, 1);
+}
+// Warp-aggregated add of 1 per lane into bin `digit` of a shared histogram at shared
+// address `hbase`, for all 32 lanes (warp-uniform, all lanes active): the lanes holding
+// the same digit add once, from the highest such lane, by a predicated red.shared.
+__device__ __forceinline__ void hist_add_all(uint32_t hbase, uint32_t digit) {
+    const unsigned peers = __match_any_sync(0xffffffffu, digit);
+    const uint32_t lead = (threadIdx.x & 31u) == (uint32_t)(31 - __clz(peers));
+    asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p red.shared.add.u32 [%0], %1; }"
+                 :: "r"(hbase + 4u * digit), "r"((uint32_t)__popc(peers)), "r"(lead) : "memory");
 }
 // Row loop of the select kernels: 4-row vector steps for SrcSoa64 on aligned columns,
 // scalar rows otherwise (and for the tail). Trip counts are warp-uniform (f gets a valid
@@ -240,7 +298,7 @@ __device__ __forceinline__ void sel_rows(const Src& src, uint32_t n, F&& f) {
             for (uint32_t i0 = wbase * 4u; i0 < n4; i0 += stride * 4u) {
                 const uint32_t i = i0 + lane * 4u;
                 const bool ok = i < n4;
-                unsigned __int128 v[4] = {0, 0, 0, 0};
+                uint64_t v[4] = {0, 0, 0, 0};
                 if (ok) soa64_value4(src, i, v);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) f(i + k, v[k], ok);
@@ -251,7 +309,7 @@ __device__ __forceinline__ void sel_rows(const Src& src, uint32_t n, F&& f) {
     for (uint32_t i0 = done + wbase; i0 < n; i0 += stride) {
         const uint32_t i = i0 + lane;
         const bool ok = i < n;
-        f(i, ok ? src.value(i) : (unsigned __int128)0, ok);
+        f(i, ok ? src.value(i) : (typename Src::V)0, ok);
     }
 }
 // Like sel_rows, but hands f up to four consecutive rows per lane at once (i0, values,
@@ -268,7 +326,7 @@ __device__ __forceinline__ void sel_rows4(const Src& src, uint32_t n, F&& f) {
             const uint32_t n4 = n & ~3u;
             for (uint32_t i0 = wbase * 4u; i0 < n4; i0 += stride * 4u) {
                 const uint32_t i = i0 + lane * 4u;
-                unsigned __int128 v[4] = {0, 0, 0, 0};
+                uint64_t v[4] = {0, 0, 0, 0};
                 const int nv = i < n4 ? 4 : 0;
                 if (nv) soa64_value4(src, i, v);
                 f(i, v, nv);
@@ -278,7 +336,7 @@ __device__ __forceinline__ void sel_rows4(const Src& src, uint32_t n, F&& f) {
     }
     for (uint32_t i0 = done + wbase; i0 < n; i0 += stride) {
         const uint32_t i = i0 + lane;
-        unsigned __int128 v[4] = {0, 0, 0, 0};
+        typename Src::V v[4] = {0, 0, 0, 0};
         const int nv = i < n ? 1 : 0;
         if (nv) v[0] = src.value(i);
         f(i, v, nv);
@@ -286,20 +344,21 @@ __device__ __forceinline__ void sel_rows4(const Src& src, uint32_t n, F&& f) {
 }
 // Rows already filtered by the level-1 pass: (value, row) pairs, one slice of `capc` per
 // CTA (the select kernels keep the same grid, so CTA c re-reads the rows it kept).
+template <typename V>
 struct SrcBuf {
-    const unsigned __int128* v;
+    const V* v;
     const uint32_t* idx;
     const uint32_t* cnt;
     uint32_t capc;
 };
-template <typename F>
-__device__ __forceinline__ void buf_rows(const SrcBuf& b, F&& f) {
+template <typename V, typename F>
+__device__ __forceinline__ void buf_rows(const SrcBuf<V>& b, F&& f) {
     const uint32_t n = b.cnt[blockIdx.x];
     const size_t off = (size_t)blockIdx.x * b.capc;
     for (uint32_t i0 = threadIdx.x & ~31u; i0 < n; i0 += SEL_THREADS) {
         const uint32_t i = i0 + (threadIdx.x & 31u);
         const bool ok = i < n;
-        f(ok ? b.idx[off + i] : 0u, ok ? b.v[off + i] : (unsigned __int128)0, ok);
+        f(ok ? b.idx[off + i] : 0u, ok ? b.v[off + i] : (V)0, ok);
     }
 }
 // warp-aggregated append of (v, row) for the lanes with p set
@@ -321,15 +380,40 @@ __device__ __forceinline__ void sel_append(bool p, unsigned __int128 v, uint32_t
 }
 
 template <typename Src>
-__device__ __forceinline__ uint32_t sel_digit(unsigned __int128 v, uint32_t level) {
-    return (uint32_t)(v >> (Src::BITS - SEL_BITS * (level + 1))) & (SEL_BINS - 1);
+__device__ __forceinline__ uint32_t sel_digit(typename Src::V v, uint32_t level) {
+    return (uint32_t)vshr<Src>(v, Src::BITS - SEL_BITS * (int)(level + 1)) & (SEL_BINS - 1);
 }
 
 template <typename Src>
 __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c,
                                uint32_t dom_cap);
 
+// Warp-aggregated shared-memory histogram increment: lanes holding the same digit add once
+// (the SoA keys concentrate on few level-0 / level-1 bins: one atomic per lane would
+// serialise on them). Warp-uniform call; lanes with !p take no part.
+__device__ __forceinline__ void hist_add_warp(uint32_t* h, uint32_t digit, bool p) {
+    if (!__any_sync(0xffffffffu, p)) return;
+    const uint32_t key = p ? digit : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, key);
+    if (p && (threadIdx.x & 31u) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&h[digit], (uint32_t)__popc(peers));
+}
+
 template <typename Src>
+__device__ __forceinline__ bool soa64_aligned(const Src& s) {
+    if constexpr (std::is_same<Src, SrcSoa64>::value)
+        return ((reinterpret_cast<uintptr_t>(s.score) | reinterpret_cast<uintptr_t>(s.arrival_rank)) & 15u) == 0 &&
+               (reinterpret_cast<uintptr_t>(s.flags) & 3u) == 0;
+    else
+        return false;
+}
+template <typename Src>
+__device__ __forceinline__ const SrcSoa64& soa64_of(const Src& s) {
+    if constexpr (std::is_same<Src, SrcSoa64>::value) return s;
+    else { __trap(); return *reinterpret_cast<const SrcSoa64*>(&s); }
+}
+// LEVEL: the level this launch histograms (the host launches LEVEL = 0, 1, ... in order;
+// st->level == LEVEL unless the select is already done), so every shift is a constant.
+template <typename Src, int LEVEL>
 __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, SelState* __restrict__ st,
                                                         unsigned __int128* __restrict__ pfx128,
                                                         uint32_t* __restrict__ hist, uint32_t k,
@@ -337,33 +421,105 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, Sel
                                                         uint32_t* __restrict__ dom_i, uint32_t* __restrict__ dom_cnt,
                                                         uint32_t dom_cap) {
     if (st->done) return;
-    __shared__ uint32_t h[SEL_BINS];
+    __shared__ uint32_t h[SEL_BINS + 1];  // [SEL_BINS]: scratch for masked-off lanes
     __shared__ uint32_t scnt;
     for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) h[b] = 0;
     if (threadIdx.x == 0) scnt = 0;
     __syncthreads();
     const uint32_t capc = dom_cap / gridDim.x;
-    const uint32_t level = st->level;
-    const unsigned __int128 want = *pfx128;  // prefix digits in place (lower bits zero)
-    const int shift = Src::BITS - SEL_BITS * (int)level;
+    using V = typename Src::V;
+    constexpr uint32_t level = LEVEL;
+    constexpr int shift = Src::BITS - SEL_BITS * LEVEL;
+    const V wsh = (V)(*pfx128 >> shift);  // the chosen prefix digits
+    V* dv = reinterpret_cast<V*>(dom_v);
     if (st->compacted) {
-        buf_rows(SrcBuf{dom_v, dom_i, dom_cnt, capc}, [&](uint32_t, unsigned __int128 v, bool ok) {
-            if (ok && (v >> shift) == (want >> shift)) atomicAdd(&h[sel_digit<Src>(v, level)], 1u);
+        buf_rows(SrcBuf<V>{dv, dom_i, dom_cnt, capc}, [&](uint32_t, V v, bool ok) {
+            if (ok && vshr<Src>(v, shift) == wsh) atomicAdd(&h[sel_digit<Src>(v, level)], 1u);
         });
-    } else if (level == 1 && st->dom_ok) {
+    } else if (LEVEL == 1 && st->dom_ok && soa64_aligned(src)) {
+        // as below, on the top 32 key bits (scores + flags, 5 B per row): the level-0 digit
+        // decides keep / count, the arrival rank is read only for the kept rows
+        const SrcSoa64& so = soa64_of(src);
+        const size_t off = (size_t)blockIdx.x * capc;
+        const uint32_t w0 = (uint32_t)wsh, lane = threadIdx.x & 31u;
+        auto rows = [&](uint32_t i0, const uint32_t (&hi)[4], const uint32_t (&lo)[4], int nv) {
+            uint32_t keep = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t d0 = hi[q] >> 21;
+                if (q < nv && d0 <= w0) keep |= 1u << q;
+                hist_add_warp(h, (hi[q] >> 10) & (SEL_BINS - 1), q < nv && d0 == w0);
+            }
+            if (!__any_sync(0xffffffffu, keep)) return;
+            const uint32_t c = __popc(keep);
+            uint32_t x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+            uint32_t base = 0;
+            if (lane == 31) base = atomicAdd(&scnt, tot);
+            base = __shfl_sync(0xffffffffu, base, 31) + x - c;
+            if (!keep) return;
+            uint32_t ar[4];
+            if (nv == 4) {  // the lane's four arrival ranks in one 16-B load
+                const uint4 a4 = *reinterpret_cast<const uint4*>(so.arrival_rank + i0);
+                ar[0] = a4.x; ar[1] = a4.y; ar[2] = a4.z; ar[3] = a4.w;
+            } else {
+                ar[0] = so.arrival_rank[i0];
+                ar[1] = ar[2] = ar[3] = 0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (keep >> q & 1u) {
+                    if (base < capc) {
+                        dv[off + base] = (V)(((uint64_t)hi[q] << 32) | lo[q] | (ar[q] & RANK_MASK));
+                        dom_i[off + base] = i0 + q;
+                    }
+                    ++base;
+                }
+            }
+        };
+        const uint32_t stride = gridDim.x * SEL_THREADS;
+        const uint32_t n4 = n & ~3u;
+        for (uint32_t j0 = (blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u)) * 4u; j0 < n4; j0 += stride * 4u) {
+            const uint32_t i = j0 + lane * 4u;
+            uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+            const int nv = i < n4 ? 4 : 0;
+            if (nv) soa64_hi4(so, i, hi, lo);
+            rows(i, hi, lo, nv);
+        }
+        for (uint32_t i = n4 + blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u) + lane; i - lane < n; i += stride) {
+            uint32_t hi[4] = {0, 0, 0, 0}, lo[4] = {0, 0, 0, 0};
+            const int nv = i < n ? 1 : 0;
+            if (nv) {
+                const uint64_t v = so.value(i);
+                hi[0] = (uint32_t)(v >> 32);
+                lo[0] = (uint32_t)v & ~RANK_MASK;
+            }
+            rows(i, hi, lo, nv);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            dom_cnt[blockIdx.x] = min(scnt, capc);
+            if (scnt > capc) atomicOr(&st->dom_overflow, 1u);
+        }
+    } else if (LEVEL == 1 && st->dom_ok) {
         // level 1 over all rows also keeps every row at or below the level-0 bucket (all
         // candidates: the passes after this one read only them), in this CTA's slice
         const size_t off = (size_t)blockIdx.x * capc;
-        const unsigned __int128 wsh = want >> shift;
-        sel_rows4(src, n, [&](uint32_t i0, const unsigned __int128 (&v)[4], int nv) {
+        sel_rows4(src, n, [&](uint32_t i0, const V (&v)[4], int nv) {
             // the lane's kept rows (<= 4), one warp scan + one shared atomic per warp
             uint32_t keep = 0;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                const unsigned __int128 t = v[k] >> shift;
+                const V t = vshr<Src>(v[k], shift);
                 if (k < nv && t <= wsh) keep |= 1u << k;
-                if (k < nv && t == wsh) atomicAdd(&h[sel_digit<Src>(v[k], level)], 1u);
+                hist_add_warp(h, sel_digit<Src>(v[k], level), k < nv && t == wsh);
             }
+            if (!__any_sync(0xffffffffu, keep)) return;  // most warps keep nothing
             const uint32_t c = __popc(keep);
             uint32_t x = c;
             const uint32_t lane = threadIdx.x & 31u;
@@ -381,7 +537,7 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, Sel
             for (int k = 0; k < 4; ++k) {
                 if (keep >> k & 1u) {
                     if (base < capc) {
-                        dom_v[off + base] = v[k];
+                        dv[off + base] = v[k];
                         dom_i[off + base] = i0 + k;
                     }
                     ++base;
@@ -393,9 +549,213 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, Sel
             dom_cnt[blockIdx.x] = min(scnt, capc);
             if (scnt > capc) atomicOr(&st->dom_overflow, 1u);
         }
+    } else if (LEVEL == 0 && soa64_aligned(src) && n >= SEL_L0_KEEP_N) {
+        // Level 0 on scores + flags only (5 B per row): the digit is (class << 8) | the top
+        // byte of the f32 image. Phase A counts every row of the warp's first SEL_PHASE_A
+        // chunks; the CTA then knows a bin U holding, with all bins below it, >= k of its
+        // own rows, so the k-th key's bin is <= U. Phase B counts only rows at or below U
+        // and keeps them (full key + row) in this CTA's slice of the candidate buffer; the
+        // phase-A rows at or below U are kept by a second (L2-resident) read at the end.
+        // With every slice in capacity the later levels read only the kept rows (no
+        // level-1 pass over the columns); otherwise level 1 runs its own keep pass.
+        const SrcSoa64& so = soa64_of(src);
+        const uint32_t stride = gridDim.x * SEL_THREADS * 4u, lane = threadIdx.x & 31u;
+        const uint32_t n4 = n & ~3u;
+        const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(h);
+        const size_t off = (size_t)blockIdx.x * capc;
+        const uint32_t i_first = (blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u)) * 4u + lane * 4u;
+        __shared__ uint32_t sU;
+        bool nan = false;
+        // keep (v, row) of the lane's rows in `keep` (bit q: row i + q), warp-aggregated
+        // mark (bit 31 of the stored row index): a phase-A row, already counted. Phase-B rows
+        // are counted from the slice at the end (or here, when the slice is full)
+        auto append = [&](uint32_t i, uint32_t keep, const uint32_t (&img)[4], uint32_t C, uint32_t mark) {
+            if (!__any_sync(0xffffffffu, keep)) return;
+            const uint32_t c = __popc(keep);
+            uint32_t x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= (uint32_t)o) x += y;
+            }
+            const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+            uint32_t base = 0;
+            if (lane == 31) base = atomicAdd(&scnt, tot);
+            base = __shfl_sync(0xffffffffu, base, 31) + x - c;
+            if (!keep) return;
+            const uint4 a4 = *reinterpret_cast<const uint4*>(so.arrival_rank + i);
+            const uint32_t ar[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (keep >> q & 1u) {
+                    const uint64_t v = (((uint64_t)((C >> (8 * q)) & 7u)) << 61) | ((uint64_t)img[q] << 29) |
+                                       (uint64_t)(ar[q] & RANK_MASK);
+                    if (base < capc) {
+                        dv[off + base] = (V)v;
+                        dom_i[off + base] = (i + q) | mark;
+                    } else if (!mark) {
+                        atomicAdd(&h[(uint32_t)(v >> 53)], 1u);  // dropped (slice full): count now
+                    }
+                    ++base;
+                }
+            }
+        };
+        // one chunk of four rows per lane: count (rows <= U), keep (rows <= U when `kp`)
+        auto chunk = [&](uint32_t i, float4 sc, uint32_t fw, uint32_t U, bool phase_a) {
+            const bool ok = i < n4;
+            const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
+            const uint32_t C = soa64_classes(fw, so.preemptive);
+            uint32_t img[4], keep = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                img[q] = soa64_img(scv[q], (fw >> (8 * q)) & RS_FLAG_SCORED, nan);
+                const uint32_t d = __byte_perm(img[q], C, 0x4443u + 0x0010u * q) & (SEL_BINS - 1);
+                const bool p = ok && d <= U;
+                keep |= (p ? 1u : 0u) << q;
+                if (phase_a) hist_add_all(hbase, p ? d : (uint32_t)SEL_BINS);  // every row counted
+            }
+            if (!phase_a) append(i, keep, img, C, 0u);
+        };
+        auto load = [&](uint32_t i, float4& sc, uint32_t& fl) {
+            sc = make_float4(0.f, 0.f, 0.f, 0.f);
+            fl = 0;
+            if (i < n4) {
+                sc = __ldcs(reinterpret_cast<const float4*>(so.score + i));
+                fl = __ldcs(reinterpret_cast<const uint32_t*>(so.flags + i));
+            }
+        };
+        // phase A (block-uniform: SEL_PHASE_A chunks per warp, masked past n4)
+        for (int it = 0; it < SEL_PHASE_A; ++it) {
+            float4 sc;
+            uint32_t fl;
+            const uint32_t i = i_first + it * stride;
+            load(i, sc, fl);
+            chunk(i, sc, fl, SEL_BINS - 1, true);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // U = first bin whose inclusive prefix count reaches k
+            uint32_t acc = 0, U = SEL_BINS - 1;
+            for (uint32_t b0 = 0; b0 < SEL_BINS; b0 += 32) {
+                uint32_t x = h[b0 + lane];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= (uint32_t)o) x += y;
+                }
+                const unsigned hit = __ballot_sync(0xffffffffu, acc + x >= k);
+                if (hit) {
+                    U = b0 + (uint32_t)(__ffs(hit) - 1);
+                    break;
+                }
+                acc += __shfl_sync(0xffffffffu, x, 31);
+            }
+            if (lane == 0) sU = U;
+        }
+        __syncthreads();
+        const uint32_t U = sU;
+        // phase B, the next chunk's loads issued before this one is processed
+        {
+            uint32_t i = i_first + SEL_PHASE_A * stride;
+            float4 sc;
+            uint32_t fl;
+            load(i, sc, fl);
+            for (; i - lane * 4u < n4; i += stride) {  // warp-uniform trip count
+                const float4 cs = sc;
+                const uint32_t cf = fl;
+                load(i + stride, sc, fl);
+                chunk(i, cs, cf, U, false);
+            }
+        }
+        // phase-A rows at or below U (no counting: they are in the histogram already)
+        for (int it = 0; it < SEL_PHASE_A; ++it) {
+            const uint32_t i = i_first + it * stride;
+            if (i - lane * 4u >= n4) break;  // warp-uniform
+            float4 sc;
+            uint32_t fl;
+            load(i, sc, fl);
+            const bool ok = i < n4;
+            const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
+            const uint32_t C = soa64_classes(fl, so.preemptive);
+            uint32_t img[4], keep = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                img[q] = soa64_img(scv[q], (fl >> (8 * q)) & RS_FLAG_SCORED, nan);
+                const uint32_t d = __byte_perm(img[q], C, 0x4443u + 0x0010u * q) & (SEL_BINS - 1);
+                keep |= ((ok && d <= U) ? 1u : 0u) << q;
+            }
+            append(i, keep, img, C, 0x80000000u);
+        }
+        if (nan) atomicOr(so.err, 1);
+        // tail rows (< 4): counted and kept one per lane, warp-uniform trip count
+        for (uint32_t t = n4 + blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u) + lane; t - lane < n;
+             t += gridDim.x * SEL_THREADS) {
+            const bool ok = t < n;
+            const uint64_t v = ok ? so.value(t) : 0ull;
+            const uint32_t d = (uint32_t)(v >> 53);
+            hist_add_warp(h, d, ok);
+            const bool kp = ok && d <= U;
+            const unsigned bb = __ballot_sync(0xffffffffu, kp);
+            if (bb) {
+                uint32_t base = 0;
+                if (lane == (uint32_t)(__ffs(bb) - 1)) base = atomicAdd(&scnt, (uint32_t)__popc(bb));
+                base = __shfl_sync(0xffffffffu, base, __ffs(bb) - 1) + (uint32_t)__popc(bb & ((1u << lane) - 1u));
+                if (kp && base < capc) {
+                    dv[off + base] = (V)v;
+                    dom_i[off + base] = t | 0x80000000u;  // counted above
+                }
+            }
+        }
+        __syncthreads();
+        // count the stored phase-B rows; clear the marks
+        const uint32_t ns = min(scnt, capc);
+        for (uint32_t e = threadIdx.x; e < ns; e += SEL_THREADS) {
+            const uint32_t r = dom_i[off + e];
+            if (r & 0x80000000u) dom_i[off + e] = r & 0x7fffffffu;
+            else atomicAdd(&h[(uint32_t)((uint64_t)dv[off + e] >> 53)], 1u);
+        }
+        if (threadIdx.x == 0) {
+            dom_cnt[blockIdx.x] = ns;
+            if (scnt > capc) atomicOr(&st->dom_overflow, 1u);
+        }
+    } else if (LEVEL == 0 && soa64_aligned(src)) {
+        // smaller queues: the same digit from scores + flags, every row counted, no keep
+        const SrcSoa64& so = soa64_of(src);
+        const uint32_t stride = gridDim.x * SEL_THREADS * 4u, lane = threadIdx.x & 31u;
+        const uint32_t n4 = n & ~3u;
+        const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(h);
+        uint32_t i = (blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u)) * 4u + lane * 4u;
+        float4 sc = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint32_t fl = 0;
+        if (i < n4) {
+            sc = __ldcs(reinterpret_cast<const float4*>(so.score + i));
+            fl = __ldcs(reinterpret_cast<const uint32_t*>(so.flags + i));
+        }
+        bool nan = false;
+        for (; i - lane * 4u < n4; i += stride) {  // warp-uniform trip count
+            const bool ok = i < n4;
+            const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
+            const uint32_t fw = fl;
+            if (i + stride < n4) {
+                sc = __ldcs(reinterpret_cast<const float4*>(so.score + i + stride));
+                fl = __ldcs(reinterpret_cast<const uint32_t*>(so.flags + i + stride));
+            }
+            const uint32_t C = soa64_classes(fw, so.preemptive);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t img = soa64_img(scv[q], (fw >> (8 * q)) & RS_FLAG_SCORED, nan);
+                const uint32_t d = __byte_perm(img, C, 0x4443u + 0x0010u * q) & (SEL_BINS - 1);
+                hist_add_all(hbase, ok ? d : (uint32_t)SEL_BINS);
+            }
+        }
+        if (nan) atomicOr(so.err, 1);
+        for (uint32_t t = n4 + blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u) + lane; t - lane < n;
+             t += gridDim.x * SEL_THREADS) {
+            const bool ok = t < n;  // tail rows (< 4), warp-uniform trip count
+            hist_add_warp(h, ok ? sel_digit<Src>(src.value(t), 0) : 0u, ok);
+        }
     } else {
-        sel_rows(src, n, [&](uint32_t, unsigned __int128 v, bool ok) {
-            if (ok && (level == 0 || (v >> shift) == (want >> shift))) atomicAdd(&h[sel_digit<Src>(v, level)], 1u);
+        sel_rows(src, n, [&](uint32_t, V v, bool ok) {
+            hist_add_warp(h, sel_digit<Src>(v, level), ok && (LEVEL == 0 || vshr<Src>(v, shift) == wsh));
         });
     }
     __syncthreads();
@@ -409,7 +769,11 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, Sel
     __syncthreads();
     if (last) {
         __threadfence();
-        if (threadIdx.x == 0 && level == 1 && st->dom_ok && !st->dom_overflow) st->compacted = 1;
+        if (threadIdx.x == 0) {
+            if (LEVEL == 0 && soa64_aligned(src) && n >= SEL_L0_KEEP_N && !st->dom_overflow) st->compacted = 1;  // kept by level 0
+            if (LEVEL == 0) st->dom_overflow = 0;  // level 1's own keep pass (if any) starts clean
+            if (LEVEL == 1 && st->dom_ok && !st->dom_overflow) st->compacted = 1;
+        }
         sel_pick_block<Src>(st, pfx128, hist, k, h, dom_cap);
     }
 }
@@ -471,13 +835,14 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_gather(Src src, uint32_t n, S
                                                           const unsigned __int128* __restrict__ dom_v,
                                                           const uint32_t* __restrict__ dom_i,
                                                           const uint32_t* __restrict__ dom_cnt, uint32_t dom_cap) {
+    using V = typename Src::V;
     const int shift = Src::BITS - SEL_BITS * (int)st->final_level;
-    const unsigned __int128 lim = *pfx128 >> shift;
-    auto take = [&](uint32_t i, unsigned __int128 v, bool ok) {
-        sel_append(ok && (v >> shift) <= lim, v, i, &st->n_cand, ck, ci, SEL_SORT);
+    const V lim = (V)(*pfx128 >> shift);
+    auto take = [&](uint32_t i, V v, bool ok) {
+        sel_append(ok && vshr<Src>(v, shift) <= lim, to128<Src>(v), i, &st->n_cand, ck, ci, SEL_SORT);
     };
     if (st->compacted)
-        buf_rows(SrcBuf{dom_v, dom_i, dom_cnt, dom_cap / gridDim.x}, take);
+        buf_rows(SrcBuf<V>{reinterpret_cast<const V*>(dom_v), dom_i, dom_cnt, dom_cap / gridDim.x}, take);
     else
         sel_rows(src, n, take);
 }
@@ -922,6 +1287,12 @@ static void rank_layout(A& a, uint64_t n, RankWs* w) {
     auto sp = a.template take<int>(ms_splits(np));
     if (w) *w = RankWs{ka, kb, va, vb, sc, pd, bc, er, sl, px, hi, ck, ci, dv, di, dc, n > SEL_MIN_N ? dcap : 0u, sp};
 }
+// the select's histogram launches, LEVEL = 0 .. Src::LEVELS - 1 in order
+template <typename Src, int... L>
+static void sel_levels(std::integer_sequence<int, L...>, uint32_t gb, cudaStream_t st, const Src& src, uint32_t n,
+                       const RankWs& w, uint32_t k) {
+    ((sel_hist<Src, L><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.hist, k, w.dv, w.di, w.dcnt, w.dcap)), ...);
+}
 struct RankSizer {
     ArenaSizer s;
     template <typename T>
@@ -1015,19 +1386,13 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         if (soa64) {
             // keys straight from the queue columns: no key pass, 9 B per row per level
             const SrcSoa64 src{static_cast<const float*>(q->score), q->flags, q->arrival_rank, preemptive, counts + 3};
-            for (int level = 0; level < SrcSoa64::LEVELS; ++level) {
-                sel_hist<SrcSoa64><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.hist, k, w.dv, w.di, w.dcnt, w.dcap);
-                RS_LAUNCH_CHECK();
-            }
+            sel_levels<SrcSoa64>(std::make_integer_sequence<int, SrcSoa64::LEVELS>{}, gb, st, src, n, w, k);
             sel_gather<SrcSoa64><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.ck, w.ci, w.dv, w.di, w.dcnt, w.dcap);
         } else {
             build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
             RS_LAUNCH_CHECK();
             const SrcKeys src{w.kb};
-            for (int level = 0; level < SrcKeys::LEVELS; ++level) {
-                sel_hist<SrcKeys><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.hist, k, w.dv, w.di, w.dcnt, w.dcap);
-                RS_LAUNCH_CHECK();
-            }
+            sel_levels<SrcKeys>(std::make_integer_sequence<int, SrcKeys::LEVELS>{}, gb, st, src, n, w, k);
             sel_gather<SrcKeys><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.ck, w.ci, w.dv, w.di, w.dcnt, w.dcap);
         }
         RS_LAUNCH_CHECK();

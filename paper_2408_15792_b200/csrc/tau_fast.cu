@@ -214,9 +214,13 @@ struct TfStSmem {
 };
 constexpr size_t TF_ST_SMEM = sizeof(TfStSmem);
 
-// key[k] / bin[k] valid for k with e = k * TF_ST_T + tid < m
+// key[k] / bin[k] valid for k with e = k * TF_ST_T + tid < m. `placed()` runs once the
+// tile sits in shared memory (key / bin dead): the caller issues the next tile's loads
+// there, so they overlap the write-out.
+template <typename F>
 __device__ __forceinline__ void tf_tile_scatter(TfStSmem& s, const uint32_t (&key)[TF_ST_PER],
-                                                const uint32_t (&bin)[TF_ST_PER], int m, uint32_t* __restrict__ out) {
+                                                const uint32_t (&bin)[TF_ST_PER], int m, uint32_t* __restrict__ out,
+                                                F&& placed) {
     constexpr int PER = TF_BINS / TF_ST_T;
     for (int v = threadIdx.x; v < TF_BINS; v += TF_ST_T) s.lcnt[v] = 0;
     __syncthreads();
@@ -248,6 +252,7 @@ __device__ __forceinline__ void tf_tile_scatter(TfStSmem& s, const uint32_t (&ke
             s.sbin[pos] = (uint16_t)bin[k];
         }
     }
+    placed();
     __syncthreads();
     for (int e = threadIdx.x; e < m; e += TF_ST_T) {
         const uint32_t b = s.sbin[e];
@@ -342,21 +347,36 @@ __global__ void __launch_bounds__(TF_ST_T, 1) tf_scatter1(const void* __restrict
     if (blockIdx.x == 0 && threadIdx.x == TF_ST_T - 1) off1[TF_BINS] = base + sum;
     __syncthreads();
     const uint32_t beg = blockIdx.x * ch, end = min(n, beg + ch);
+    // the next tile's raw words are loaded while this tile is written out, so the HBM
+    // reads overlap it (one CTA per SM: nothing else would)
+    const uint32_t* xw = static_cast<const uint32_t*>(x);
+    const uint32_t* yw = static_cast<const uint32_t*>(y);
+    uint32_t rx[TF_ST_PER], ry[TF_ST_PER / 2];  // raw x words; y offsets (< 4096) two per register
+    auto fetch = [&](uint32_t t0) {
+        const int m = (int)min((uint32_t)TF_ST_TILE, end - t0);
+#pragma unroll
+        for (int k = 0; k < TF_ST_PER; ++k) {
+            const int e = k * TF_ST_T + threadIdx.x;
+            rx[k] = e < m ? __ldcs(xw + t0 + e) : 0u;
+            const uint32_t yo = e < m ? (tf_conv(__ldcs(yw + t0 + e), yd) - d.ymin) & 0xFFFFu : 0u;
+            if (k & 1) ry[k >> 1] |= yo << 16; else ry[k >> 1] = yo;
+        }
+    };
+    if (beg < end) fetch(beg);
     for (uint32_t t0 = beg; t0 < end; t0 += TF_ST_TILE) {
         const int m = (int)min((uint32_t)TF_ST_TILE, end - t0);
         uint32_t key[TF_ST_PER], bin[TF_ST_PER];
 #pragma unroll
         for (int k = 0; k < TF_ST_PER; ++k) {
-            const int e = k * TF_ST_T + threadIdx.x;
-            key[k] = 0;
-            bin[k] = 0;
-            if (e < m) {
-                const uint32_t xi = tf_img(x, xd, t0 + e), yi = tf_img(y, yd, t0 + e);
-                key[k] = tf_key1(xi, yi, d);
-                bin[k] = tf_digit1(xi, d);
-            }
+            const uint32_t xi = tf_conv(rx[k], xd);
+            const uint32_t xr = xi - d.xmin;
+            const uint32_t rem = d.r1 ? (xr & ((1u << d.r1) - 1u)) : 0u;
+            key[k] = (rem << 12) | ((ry[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);  // == tf_key1(xi, yi, d)
+            bin[k] = tf_digit1(xi, d);
         }
-        tf_tile_scatter(s, key, bin, m, A);
+        tf_tile_scatter(s, key, bin, m, A, [&] {
+            if (t0 + TF_ST_TILE < end) fetch(t0 + TF_ST_TILE);
+        });
     }
 }
 
@@ -562,16 +582,27 @@ __global__ void __launch_bounds__(TF_ST_T, 1) tf_scatter2(const TfParams* __rest
         const uint32_t* pr = pre2 + (size_t)item * TF_BINS;
         for (int v = threadIdx.x; v < TF_BINS; v += TF_ST_T) s.cur[v] = pr[v];
         __syncthreads();
+        uint32_t raw[TF_ST_PER];
+        auto fetch = [&](uint32_t t0) {
+            const int m = (int)min((uint32_t)TF_ST_TILE, it.end - t0);
+#pragma unroll
+            for (int k = 0; k < TF_ST_PER; ++k) {
+                const int e = k * TF_ST_T + threadIdx.x;
+                raw[k] = e < m ? __ldcs(A + t0 + e) : 0u;
+            }
+        };
+        if (it.beg < it.end) fetch(it.beg);
         for (uint32_t t0 = it.beg; t0 < it.end; t0 += TF_ST_TILE) {
             const int m = (int)min((uint32_t)TF_ST_TILE, it.end - t0);
             uint32_t key[TF_ST_PER], bin[TF_ST_PER];
 #pragma unroll
             for (int k = 0; k < TF_ST_PER; ++k) {
-                const int e = k * TF_ST_T + threadIdx.x;
-                key[k] = e < m ? A[t0 + e] : 0u;
+                key[k] = raw[k];
                 bin[k] = key[k] >> sh;
             }
-            tf_tile_scatter(s, key, bin, m, B);
+            tf_tile_scatter(s, key, bin, m, B, [&] {
+                if (t0 + TF_ST_TILE < it.end) fetch(t0 + TF_ST_TILE);
+            });
         }
     }
 }
@@ -711,22 +742,22 @@ __device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint
                 const int mid = (lo + hi) >> 1;
                 if (!(sk[tf_pidx(b0 + diag - 1 - mid)] < sk[tf_pidx(a0 + mid)])) lo = mid + 1; else hi = mid;
             }
+            // branch-free serial merge of this thread's 16 outputs: the consumed side is
+            // reloaded from a clamped index (an exhausted run's head is never taken)
             int i = lo, j = diag - lo;
-            uint32_t ka = i < la ? sk[tf_pidx(a0 + i)] : 0xffffffffu;
-            uint32_t kb = j < lb ? sk[tf_pidx(b0 + j)] : 0xffffffffu;
+            uint32_t ka = sk[tf_pidx(a0 + min(i, la - 1))];  // la >= 16
+            uint32_t kb = sk[tf_pidx(lb > 0 ? b0 + min(j, lb - 1) : a0)];
 #pragma unroll
             for (int k = 0; k < TF_ITEMS; ++k) {
-                const bool take_a = i < la && (j >= lb || !(kb < ka));
-                if (take_a) {
-                    r[k] = ka;
-                    ++i;
-                    ka = i < la ? sk[tf_pidx(a0 + i)] : 0xffffffffu;
-                } else {
-                    r[k] = kb;
-                    ++j;
-                    if (Count) inv += (unsigned long long)(la - i);
-                    kb = j < lb ? sk[tf_pidx(b0 + j)] : 0xffffffffu;
-                }
+                const bool take_b = j < lb && (i >= la || kb < ka);
+                r[k] = take_b ? kb : ka;
+                if (Count) inv += take_b ? (unsigned long long)(la - i) : 0ull;
+                i += take_b ? 0 : 1;
+                j += take_b ? 1 : 0;
+                const int nx = take_b ? b0 + min(j, lb - 1) : a0 + min(i, la - 1);
+                const uint32_t v = sk[tf_pidx(nx)];
+                ka = take_b ? ka : v;
+                kb = take_b ? v : kb;
             }
         }
         __syncthreads();

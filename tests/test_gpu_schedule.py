@@ -122,7 +122,11 @@ def test_schedule_random_vs_oracle_large():
 
 @pytest.mark.parametrize("n,max_batch,dist", [(3000, 256, "normal"), (5000, 256, "normal"), (100_000, 256, "ties"),
                                               (300_000, 256, "ties"), (1 << 20, 1024, "normal"),
-                                              (50_000, 2048, "bf16"), (10_000, 1, "ties")])
+                                              (50_000, 2048, "bf16"), (10_000, 1, "ties"),
+                                              # >= 2^23 rows: level 0 keeps the candidates itself (one
+                                              # column pass); "const" overflows the kept slices (fallback)
+                                              ((1 << 23) + 5, 256, "normal"), (1 << 23, 1024, "ties"),
+                                              (1 << 23, 256, "const"), ((1 << 23) + 3, 512, "bf16")])
 def test_topk_select_matches_full_sort(n, max_batch, dist):
     """Unlimited KV uses the radix top-k select; a budget that never binds takes the
     full-sort path. Both must give the same batch, promotions and state."""
@@ -134,6 +138,8 @@ def test_topk_select_matches_full_sort(n, max_batch, dist):
         score = rng.normal(size=n).astype(np.float32).astype(np.float64)
     elif dist == "ties":
         score = rng.integers(0, 7, n).astype(np.float64)
+    elif dist == "const":
+        score = np.full(n, 0.5)
     else:
         score = rng.normal(size=n).astype(np.float32)
         score = (score.view(np.uint32) & 0xFFFF0000).view(np.float32).astype(np.float64)
