@@ -88,7 +88,8 @@ static void train_layout(A& a, const rs_ranker_config& c, int64_t Tp, int P, int
     t.dx = a.template take<float>(Tp * d);
     t.wpart = a.template take<float>((int64_t)64 * wmax);
     const int64_t nrb = (Tp + 63) / 64 + 1;
-    t.rpart = a.template take<float>(nrb * 2 * (F > 3 * d ? F : 3 * d) + (int64_t)(P + 1) * (3 * d + 1));
+    // column-reduction partials + their group scratch; the head's (P + 1) rows + scratch
+    t.rpart = a.template take<float>(nrb * 2 * (F > 3 * d ? F : 3 * d) + (int64_t)(P + 1 + P / 16 + 1) * (3 * d + 1));
     t.g = a.template take<float>(P);
     t.dg = a.template take<float>(P);
     if (n_classes > 0) {
@@ -167,7 +168,8 @@ static int train_backward(const rs_ranker_config* cfg, const __nv_bfloat16* P16,
         sp = wgrad_splits(d, F, T);
         RS_TRY(gemm_bf16_ex(w.dh16, w.f[l], nullptr, nullptr, w.wpart, d, F, T, 6, 1, 1, sp, st));
         RS_TRY(slices_add(w.wpart, sp, (int64_t)d * F, grad + off(OFF_FC2_W, l), st));
-        RS_TRY(colsum_add(w.dh, false, n_tok, d, w.rpart, grad + off(OFF_FC2_B, l), st));
+        // below the top layer the LN1 backward of layer l + 1 already summed dh's columns
+        if (l == L - 1) RS_TRY(colsum_add(w.dh, false, n_tok, d, w.rpart, grad + off(OFF_FC2_B, l), st));
         RS_TRY(gemm_bf16_ex(w.dh16, P16 + off(OFF_FC2_W, l), nullptr, w.f[l], w.df, T, F, d, 5, 0, 1, 1, st));
         // FC1: f = relu(x2 W1^T + b1)
         sp = wgrad_splits(F, d, T);
@@ -176,12 +178,11 @@ static int train_backward(const rs_ranker_config* cfg, const __nv_bfloat16* P16,
         RS_TRY(colsum_add(w.df, true, n_tok, F, w.rpart, grad + off(OFF_FC1_B, l), st));
         RS_TRY(gemm_bf16_ex(w.df, P16 + off(OFF_FC1_W, l), nullptr, nullptr, w.dx, T, d, F, 4, 0, 1, 1, st));
         RS_TRY(ln_backward(w.dx, w.h_mid[l], P16 + off(OFF_LN2_W, l), w.dh, w.dh16, w.rpart, n_tok, d,
-                           grad + off(OFF_LN2_W, l), nullptr, st));
+                           grad + off(OFF_LN2_W, l), nullptr, st, grad + off(OFF_OUT_B, l)));
         // out-proj: h_mid = h_in + a Wo^T + bo
         sp = wgrad_splits(d, d, T);
         RS_TRY(gemm_bf16_ex(w.dh16, w.att[l], nullptr, nullptr, w.wpart, d, d, T, 6, 1, 1, sp, st));
         RS_TRY(slices_add(w.wpart, sp, (int64_t)d * d, grad + off(OFF_OUT_W, l), st));
-        RS_TRY(colsum_add(w.dh, false, n_tok, d, w.rpart, grad + off(OFF_OUT_B, l), st));
         RS_TRY(gemm_bf16_ex(w.dh16, P16 + off(OFF_OUT_W, l), nullptr, nullptr, w.da, T, d, d, 0, 0, 1, 1, st));
         if (S <= 128)
             RS_TRY(attention_bwd(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, st));
@@ -194,7 +195,7 @@ static int train_backward(const rs_ranker_config* cfg, const __nv_bfloat16* P16,
         RS_TRY(colsum_add(w.dqkv, true, n_tok, 3 * d, w.rpart, grad + off(OFF_QKV_B, l), st));
         RS_TRY(gemm_bf16_ex(w.dqkv, P16 + off(OFF_QKV_W, l), nullptr, nullptr, w.dx, T, d, 3 * d, 4, 0, 1, 1, st));
         RS_TRY(ln_backward(w.dx, w.h_in[l], P16 + off(OFF_LN1_W, l), w.dh, w.dh16, w.rpart, n_tok, d,
-                           grad + off(OFF_LN1_W, l), nullptr, st));
+                           grad + off(OFF_LN1_W, l), nullptr, st, l > 0 ? grad + off(OFF_FC2_B, l - 1) : nullptr));
     }
     RS_TRY(embed_backward(mids, P, S, cfg->vocab, w.dh, d, grad + off(OFF_TOK, 0), grad + off(OFF_POS, 0), w.ews,
                           w.ews_bytes, st));

@@ -14,6 +14,7 @@ namespace rs {
 
 constexpr float TR_LN_EPS = 1e-5f;
 constexpr int TR_ROWS_PER_BLOCK = 64;  // rows folded into one partial row of a column sum
+constexpr int LNB_ROWS_PER_BLOCK = 256;  // LN backward: 32 rows per warp, 4x fewer partial rows to reduce
 
 template <int VPL>
 __device__ __forceinline__ void tr_load_f32(const float* __restrict__ x, int lane, float (&v)[VPL * 8]) {
@@ -65,8 +66,10 @@ __device__ __forceinline__ void tr_load_w(const __nv_bfloat16* __restrict__ w, i
 // LayerNorm backward, one warp per row (d = 256 * VPL). dy = gradient w.r.t. the LN output,
 // x = LN input (fp32 residual stream), w = LN weight. dh (fp32) += dx, and dh_bf16 gets a
 // bf16 copy of the updated dh (the next GEMM operand). Per-block partial rows of
-// dw = sum dy * xhat and db = sum dy go to part[blockIdx.x] ([2][d]).
-template <int VPL>
+// dw = sum dy * xhat and db = sum dy go to part[blockIdx.x] ([2][d]); with CS also the
+// column sums of the updated dh ([3][d] rows): the bias gradient of the projection whose
+// output dh is (no separate pass over dh).
+template <int VPL, bool CS>
 __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ dy, const float* __restrict__ x,
                                                      const __nv_bfloat16* __restrict__ w, float* __restrict__ dh,
                                                      __nv_bfloat16* __restrict__ dh_bf16, float* __restrict__ part,
@@ -76,11 +79,13 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ d
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float wv[VPL * 8];
     tr_load_w<VPL>(w, lane, wv);
-    float dwp[VPL * 8], dbp[VPL * 8];
+    float dwp[VPL * 8], dbp[VPL * 8], dhp[CS ? VPL * 8 : 1];
 #pragma unroll
     for (int e = 0; e < VPL * 8; ++e) dwp[e] = dbp[e] = 0.f;
-    const int r0 = blockIdx.x * TR_ROWS_PER_BLOCK;
-    for (int r = r0 + wid; r < min(rows, r0 + TR_ROWS_PER_BLOCK); r += 8) {
+#pragma unroll
+    for (int e = 0; e < (CS ? VPL * 8 : 1); ++e) dhp[e] = 0.f;
+    const int r0 = blockIdx.x * LNB_ROWS_PER_BLOCK;
+    for (int r = r0 + wid; r < min(rows, r0 + LNB_ROWS_PER_BLOCK); r += 8) {
         float xv[VPL * 8], g[VPL * 8];
         tr_load_f32<VPL>(x + (size_t)r * d, lane, xv);
         tr_load_f32<VPL>(dy + (size_t)r * d, lane, g);
@@ -112,7 +117,10 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ d
         float hv[VPL * 8];
         tr_load_f32<VPL>(dh + (size_t)r * d, lane, hv);
 #pragma unroll
-        for (int e = 0; e < VPL * 8; ++e) hv[e] += rstd * (g[e] - sg - xv[e] * sgx);
+        for (int e = 0; e < VPL * 8; ++e) {
+            hv[e] += rstd * (g[e] - sg - xv[e] * sgx);
+            if constexpr (CS) dhp[e] += hv[e];
+        }
         tr_store_f32<VPL>(dh + (size_t)r * d, lane, hv);
         tr_store_bf16<VPL>(dh_bf16 + (size_t)r * d, lane, hv);
     }
@@ -124,12 +132,27 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ d
             red[wid][1][(lane + 32 * k) * 8 + e] = dbp[k * 8 + e];
         }
     __syncthreads();
+    constexpr int ld = (CS ? 3 : 2) * d;
     for (int cidx = threadIdx.x; cidx < 2 * d; cidx += blockDim.x) {
         const int which = cidx / d, col = cidx % d;
         float acc = 0.f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) acc += red[k][which][col];
-        part[(size_t)blockIdx.x * 2 * d + cidx] = acc;
+        part[(size_t)blockIdx.x * ld + cidx] = acc;
+    }
+    if constexpr (CS) {
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) red[wid][0][(lane + 32 * k) * 8 + e] = dhp[k * 8 + e];
+        __syncthreads();
+        for (int col = threadIdx.x; col < d; col += blockDim.x) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) acc += red[k][0][col];
+            part[(size_t)blockIdx.x * ld + 2 * d + col] = acc;
+        }
     }
 }
 
@@ -158,38 +181,45 @@ __global__ void colsum_partial_kernel(const T* __restrict__ x, int rows, int col
 }
 
 // out[c] += sum over n_part partial rows (fixed order).
-__global__ void reduce_rows_add_kernel(const float* __restrict__ part, int n_part, int cols, float* __restrict__ out) {
+__global__ void reduce_rows_add_kernel(const float* __restrict__ part, int n_part, int cols, float* __restrict__ out,
+                                       int ld) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cols) return;
     float acc = 0.f;
-    for (int p = 0; p < n_part; ++p) acc += part[(size_t)p * cols + c];
+#pragma unroll 8
+    for (int p = 0; p < n_part; ++p) acc += part[(size_t)p * ld + c];
     out[c] += acc;
 }
 
 // First level of a two-level column reduction: scratch[g][c] = sum of partial rows
-// [64 g, 64 g + 64) (fixed order), so no thread walks thousands of dependent rows.
+// [RR_GROUP g, RR_GROUP (g + 1)) (fixed order), so no thread walks thousands of dependent
+// rows and even a few hundred partial rows spread over many blocks.
+constexpr int RR_GROUP = 16;
 __global__ void reduce_rows_group_kernel(const float* __restrict__ part, int n_part, int cols,
-                                         float* __restrict__ scratch) {
+                                         float* __restrict__ scratch, int ld) {
     const int c = blockIdx.y * blockDim.x + threadIdx.x;
     if (c >= cols) return;
-    const int p0 = blockIdx.x * 64, p1 = min(n_part, p0 + 64);
+    const int p0 = blockIdx.x * RR_GROUP, p1 = min(n_part, p0 + RR_GROUP);
     float acc = 0.f;
-    for (int p = p0; p < p1; ++p) acc += part[(size_t)p * cols + c];
+#pragma unroll 8
+    for (int p = p0; p < p1; ++p) acc += part[(size_t)p * ld + c];
     scratch[(size_t)blockIdx.x * cols + c] = acc;
 }
 
-// out[c] += sum of the n_part partial rows of `part` (deterministic; scratch holds
-// ceil(n_part / 64) rows and must not overlap part).
-static int reduce_rows_add(const float* part, int n_part, int cols, float* out, float* scratch, cudaStream_t st) {
-    if (n_part <= 64) {
-        reduce_rows_add_kernel<<<(cols + 255) / 256, 256, 0, st>>>(part, n_part, cols, out);
+// out[c] += sum of the n_part partial rows of `part` (row stride ld >= cols; deterministic;
+// scratch holds ceil(n_part / RR_GROUP) rows of cols and must not overlap part).
+static int reduce_rows_add(const float* part, int n_part, int cols, float* out, float* scratch, cudaStream_t st,
+                           int ld = 0) {
+    if (ld == 0) ld = cols;
+    if (n_part <= 2 * RR_GROUP) {
+        reduce_rows_add_kernel<<<(cols + 255) / 256, 256, 0, st>>>(part, n_part, cols, out, ld);
         RS_LAUNCH_CHECK();
         return RS_OK;
     }
-    const int g = (n_part + 63) / 64;
-    reduce_rows_group_kernel<<<dim3(g, (cols + 255) / 256), 256, 0, st>>>(part, n_part, cols, scratch);
+    const int g = (n_part + RR_GROUP - 1) / RR_GROUP;
+    reduce_rows_group_kernel<<<dim3(g, (cols + 255) / 256), 256, 0, st>>>(part, n_part, cols, scratch, ld);
     RS_LAUNCH_CHECK();
-    reduce_rows_add_kernel<<<(cols + 255) / 256, 256, 0, st>>>(scratch, g, cols, out);
+    reduce_rows_add_kernel<<<(cols + 255) / 256, 256, 0, st>>>(scratch, g, cols, out, cols);
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
@@ -323,21 +353,30 @@ __global__ void adam_kernel(float* __restrict__ master, float* __restrict__ m, f
 // ---- host launchers -------------------------------------------------------------------
 
 int ln_backward(const float* dy, const float* x, const void* w, float* dh, void* dh_bf16, float* part, int rows,
-                int d, float* dw_out, float* db_out, cudaStream_t st) {
-    const int nblk = (rows + TR_ROWS_PER_BLOCK - 1) / TR_ROWS_PER_BLOCK;
+                int d, float* dw_out, float* db_out, cudaStream_t st, float* dhsum_out) {
+    const int nblk = (rows + LNB_ROWS_PER_BLOCK - 1) / LNB_ROWS_PER_BLOCK;
     const __nv_bfloat16* wb = static_cast<const __nv_bfloat16*>(w);
     __nv_bfloat16* hb = static_cast<__nv_bfloat16*>(dh_bf16);
+    const bool cs = dhsum_out != nullptr;
+#define RS_LNB(V)                                                                          \
+    if (cs) ln_bwd_kernel<V, true><<<nblk, 256, 0, st>>>(dy, x, wb, dh, hb, part, rows); \
+    else ln_bwd_kernel<V, false><<<nblk, 256, 0, st>>>(dy, x, wb, dh, hb, part, rows);
     switch (d / 256) {
-        case 1: ln_bwd_kernel<1><<<nblk, 256, 0, st>>>(dy, x, wb, dh, hb, part, rows); break;
-        case 2: ln_bwd_kernel<2><<<nblk, 256, 0, st>>>(dy, x, wb, dh, hb, part, rows); break;
-        case 3: ln_bwd_kernel<3><<<nblk, 256, 0, st>>>(dy, x, wb, dh, hb, part, rows); break;
+        case 1: RS_LNB(1) break;
+        case 2: RS_LNB(2) break;
+        case 3: RS_LNB(3) break;
         default: set_error("ln_backward: unsupported d=%d", d); return RS_ERR_INVALID;
     }
+#undef RS_LNB
     RS_LAUNCH_CHECK();
-    // part rows are [dw | db] of 2d columns: reduce both halves in one pass into
-    // a contiguous [dw_out, db_out] pair (the callers' LN weight and bias are adjacent).
+    // part rows are [dw | db (| dh column sums)]: dw and db reduce in one pass into a
+    // contiguous [dw_out, db_out] pair (the callers' LN weight and bias are adjacent)
     (void)db_out;
-    return reduce_rows_add(part, nblk, 2 * d, dw_out, part + (size_t)nblk * 2 * d, st);
+    const int ld = (cs ? 3 : 2) * d;
+    float* scratch = part + (size_t)nblk * ld;
+    RS_TRY(reduce_rows_add(part, nblk, 2 * d, dw_out, scratch, st, ld));
+    if (cs) RS_TRY(reduce_rows_add(part + 2 * d, nblk, d, dhsum_out, scratch, st, ld));
+    return RS_OK;
 }
 
 int colsum_add(const void* x, bool is_bf16, int rows, int cols, float* part, float* out, cudaStream_t st) {
@@ -419,13 +458,13 @@ int head_backward(const float* h, const int32_t* last, int B, int S, const void*
     RS_TRY(reduce_rows_add(part, B, cols, tot, tot + cols, st));
     // scatter: d hw -> g_hw, (d lnf_w, d lnf_b) -> g_lnf (adjacent), d hb -> g_hb
     if (g_hw) {
-        reduce_rows_add_kernel<<<(d + 255) / 256, 256, 0, st>>>(tot, 1, d, g_hw);
+        reduce_rows_add_kernel<<<(d + 255) / 256, 256, 0, st>>>(tot, 1, d, g_hw, d);
         RS_LAUNCH_CHECK();
     }
-    reduce_rows_add_kernel<<<(2 * d + 255) / 256, 256, 0, st>>>(tot + d, 1, 2 * d, g_lnf);
+    reduce_rows_add_kernel<<<(2 * d + 255) / 256, 256, 0, st>>>(tot + d, 1, 2 * d, g_lnf, 2 * d);
     RS_LAUNCH_CHECK();
     if (g_hb) {
-        reduce_rows_add_kernel<<<1, 32, 0, st>>>(tot + 3 * d, 1, 1, g_hb);
+        reduce_rows_add_kernel<<<1, 32, 0, st>>>(tot + 3 * d, 1, 1, g_hb, 1);
         RS_LAUNCH_CHECK();
     }
     return RS_OK;

@@ -6,9 +6,10 @@
 namespace rs {
 // LayerNorm backward over rows x d: dh += LN_bwd(dy; x, w), dh_bf16 = bf16(dh); adds the
 // LN weight / bias gradients into dw_out[0..d) and dw_out[d..2d) (weight and bias are
-// adjacent in the gradient layout; db_out is unused). part: ceil(rows/64) x 2d floats.
+// adjacent in the gradient layout; db_out is unused). dhsum_out (optional) += the column
+// sums of the updated dh. part: ceil(rows/64) x 3d floats + ceil(rows/4096) x 2d scratch.
 int ln_backward(const float* dy, const float* x, const void* w, float* dh, void* dh_bf16, float* part, int rows,
-                int d, float* dw_out, float* db_out, cudaStream_t st);
+                int d, float* dw_out, float* db_out, cudaStream_t st, float* dhsum_out = nullptr);
 // out[c] += sum over rows of x[:, c] (x float or bf16); part: ceil(rows/64) x cols floats.
 int colsum_add(const void* x, bool is_bf16, int rows, int cols, float* part, float* out, cudaStream_t st);
 // out[i] += sum over k slices of part[s * n + i]
