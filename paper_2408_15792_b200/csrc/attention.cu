@@ -517,9 +517,11 @@ int attention_fwd_f16v(const void* qkv, void* out, int B, int S, int H, cudaStre
 }  // namespace rs
 
 extern "C" int rs_attention_fwd(const void* qkv, void* out, int32_t B, int32_t S, int32_t H, void* stream) {
+    RS_NVTX();
     return rs::attention_fwd(qkv, out, B, S, H, rs::as_stream(stream));
 }
 
 extern "C" int rs_attention_fwd_f16v(const void* qkv, void* out, int32_t B, int32_t S, int32_t H, void* stream) {
+    RS_NVTX();
     return rs::attention_fwd_f16v(qkv, out, B, S, H, rs::as_stream(stream));
 }

@@ -245,5 +245,6 @@ int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv
 
 extern "C" int rs_attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv, int32_t B, int32_t S,
                                 int32_t H, void* stream) {
+    RS_NVTX();
     return rs::attention_bwd(qkv, att, dout, dqkv, B, S, H, rs::as_stream(stream));
 }

@@ -419,5 +419,6 @@ extern "C" size_t rs_attention_bwd_long_workspace_size(int32_t B, int32_t S, int
 
 extern "C" int rs_attention_bwd_long(const void* qkv, const void* att, const void* dout, void* dqkv, int32_t B,
                                      int32_t S, int32_t H, void* ws, size_t ws_bytes, void* stream) {
+    RS_NVTX();
     return rs::attention_bwd_long(qkv, att, dout, dqkv, B, S, H, ws, ws_bytes, rs::as_stream(stream));
 }

@@ -58,6 +58,7 @@ extern "C" int rs_version(void) { return 1; }
 extern "C" uint64_t rs_launch_count(void) { return rs::g_launches.load(); }
 
 extern "C" int rs_device_init(int device, int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
+    RS_NVTX();
     RS_CUDA(cudaSetDevice(device));
     cudaDeviceProp p;
     RS_CUDA(cudaGetDeviceProperties(&p, device));

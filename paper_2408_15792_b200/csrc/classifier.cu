@@ -105,6 +105,7 @@ using namespace rs;
 
 extern "C" int rs_cls_logits(const float* feat, const float* W, const float* b, int32_t B, int32_t d, int32_t C,
                              float* logits, void* stream) {
+    RS_NVTX();
     RS_CHECK_ARG(B >= 0 && d > 0 && C > 0, "rs_cls_logits: bad shape");
     if (B == 0) return RS_OK;
     RS_CHECK_ARG(feat && W && b && logits, "rs_cls_logits: NULL argument");
@@ -113,6 +114,7 @@ extern "C" int rs_cls_logits(const float* feat, const float* W, const float* b, 
 
 extern "C" int rs_cls_ce(const float* logits, const int32_t* labels, int32_t B, int32_t C, float* loss, float* dlogits,
                          int32_t* bad, void* stream) {
+    RS_NVTX();
     RS_CHECK_ARG(B >= 0 && C > 0, "rs_cls_ce: bad shape");
     if (B == 0) return RS_OK;
     RS_CHECK_ARG(logits && labels && loss && dlogits && bad, "rs_cls_ce: NULL argument");

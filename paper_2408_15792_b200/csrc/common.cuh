@@ -5,12 +5,24 @@
 #include <stdint.h>
 #include <stdio.h>
 #include "../../include/rsb200.h"
+#include <nvtx3/nvToolsExt.h>
 
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
 #error "rsb200 targets sm_100a only"
 #endif
 
 namespace rs {
+
+// NVTX range over a C-ABI entry point (nvtx3 is header-only: a no-op unless a profiler
+// injects itself), so nsys / ncu --nvtx timelines show the reference-facing calls.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define RS_NVTX() ::rs::NvtxRange rs_nvtx_range_(__func__)
+
 
 // Thread-local last-error message (set by every failing entry point).
 void set_error(const char* fmt, ...);

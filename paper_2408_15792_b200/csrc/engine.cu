@@ -323,6 +323,7 @@ using namespace rs;
 
 extern "C" int rs_engine_admit(const rs_engine_queue* q, const rs_engine_trace* tr, const int32_t* req_dev,
                                int32_t k, int64_t n_alive, void* stream) {
+    RS_NVTX();
     RS_CHECK_ARG(q && tr && (k == 0 || req_dev), "rs_engine_admit: NULL argument");
     RS_CHECK_ARG(k >= 0 && n_alive >= 0, "rs_engine_admit: negative count");
     if (k == 0) return RS_OK;
@@ -337,6 +338,7 @@ extern "C" int rs_engine_execute_ex(const rs_engine_queue* q, const rs_engine_qu
                                     const int32_t* counts_dev, int32_t step, int64_t predictor_ns, int64_t* out_dev,
                                     int64_t* preempted_dev, int64_t* finished_dev, int32_t* scratch_dev,
                                     int64_t* prev_run_dev, int32_t* prev_n_dev, void* stream) {
+    RS_NVTX();
     RS_CHECK_ARG(q && tr && cost && run_dev && counts_dev && out_dev && preempted_dev && finished_dev,
                  "rs_engine_execute: NULL argument");
     RS_CHECK_ARG(cost->decode_table_len == 0 || cost->decode_table != nullptr, "rs_engine_execute: decode table");
@@ -368,6 +370,7 @@ extern "C" int rs_engine_execute(const rs_engine_queue* q, const rs_engine_trace
                                  const int64_t* run_dev, const int32_t* counts_dev, int32_t step,
                                  int64_t predictor_ns, int64_t* out_dev, int64_t* preempted_dev,
                                  int64_t* finished_dev, void* stream) {
+    RS_NVTX();
     return rs_engine_execute_ex(q, nullptr, tr, cost, run_dev, counts_dev, step, predictor_ns, out_dev, preempted_dev,
                                 finished_dev, nullptr, nullptr, nullptr, stream);
 }
@@ -382,6 +385,7 @@ extern "C" int rs_engine_execute(const rs_engine_queue* q, const rs_engine_trace
 extern "C" int rs_engine_run(const rs_engine_queue* q2, const rs_queue_soa* soa2, const rs_engine_trace* tr,
                              const rs_engine_cost* cost, const rs_engine_loop* lp, rs_engine_loop_out* res,
                              void* stream) {
+    RS_NVTX();
     RS_CHECK_ARG(q2 && soa2 && tr && cost && lp && res, "rs_engine_run: NULL argument");
     RS_CHECK_ARG(lp->arrival_ns && lp->fits && lp->adm_host && lp->adm_dev && lp->stat_dev && lp->stat_host &&
                      lp->run_dev && lp->prom_dev && lp->dem_dev && lp->pre_dev && lp->fin_dev && lp->scratch_dev &&

@@ -646,10 +646,12 @@ int gemm_bf16(const void* A, const void* W, const void* bias, const void* R, voi
 extern "C" int rs_gemm_bf16_ex(const void* A, const void* W, const void* bias, const void* aux, void* C, int32_t M,
                                int32_t N, int32_t K, int32_t epi, int32_t a_mn, int32_t b_mn, int32_t k_splits,
                                void* stream) {
+    RS_NVTX();
     return rs::gemm_bf16_ex(A, W, bias, aux, C, M, N, K, epi, a_mn, b_mn, k_splits, rs::as_stream(stream));
 }
 
 extern "C" int rs_gemm_bf16(const void* A, const void* W, const void* bias, const void* R, void* C, int32_t M,
                             int32_t N, int32_t K, int32_t epi, void* stream) {
+    RS_NVTX();
     return rs::gemm_bf16(A, W, bias, R, C, M, N, K, epi, rs::as_stream(stream));
 }

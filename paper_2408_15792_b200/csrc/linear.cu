@@ -242,6 +242,7 @@ extern "C" int64_t rs_linear_n_params(int32_t n_features, int32_t hidden) {
 
 extern "C" int rs_standardizer_fit(const double* X, int64_t n_rows, int32_t n_features, double* mean, double* stdv,
                                    void* stream) {
+    RS_NVTX();
     RS_CHECK_ARG(n_rows >= 1 && n_features >= 1, "rs_standardizer_fit: need at least one row and one feature");
     standardizer_fit_kernel<<<n_features, 256, 0, as_stream(stream)>>>(X, n_rows, n_features, mean, stdv);
     RS_LAUNCH_CHECK();
@@ -250,6 +251,7 @@ extern "C" int rs_standardizer_fit(const double* X, int64_t n_rows, int32_t n_fe
 
 extern "C" int rs_standardize(const double* X, int64_t n_rows, int32_t n_features, const double* mean,
                               const double* stdv, double* out, void* stream) {
+    RS_NVTX();
     RS_CHECK_ARG(n_rows >= 0 && n_features >= 1, "rs_standardize: bad shape");
     if (n_rows == 0) return RS_OK;
     const int64_t total = n_rows * n_features;
@@ -261,6 +263,7 @@ extern "C" int rs_standardize(const double* X, int64_t n_rows, int32_t n_feature
 
 extern "C" int rs_linear_forward(const double* X, int64_t n_rows, int32_t n_features, const double* mean,
                                  const double* stdv, int32_t hidden, const double* params, double* out, void* stream) {
+    RS_NVTX();
     RS_CHECK_ARG(n_rows >= 0 && n_features >= 1 && hidden >= 0, "rs_linear_forward: bad shape");
     if (n_rows == 0) return RS_OK;
     const int blocks = (int)((n_rows + 127) / 128 < 148 * 8 ? (n_rows + 127) / 128 : 148 * 8);
@@ -278,6 +281,7 @@ extern "C" int rs_linear_train_step(const double* Xs, const int64_t* batch, cons
                                     int32_t n_features, int32_t hidden, int32_t bucket_width, double* params,
                                     double* adam_m, double* adam_v, double lr, double beta1, double beta2, double eps,
                                     int64_t t, double* loss_out, double* grad_out, void* stream) {
+    RS_NVTX();
     RS_CHECK_ARG(n >= 2 && n_features >= 1 && hidden >= 0, "rs_linear_train_step: need a list of >= 2 items");
     RS_CHECK_ARG(bucket_width >= 1, "bucket_width must be >= 1");
     RS_CHECK_ARG(t >= 1, "rs_linear_train_step: Adam step t must be >= 1");

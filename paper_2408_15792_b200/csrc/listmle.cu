@@ -702,6 +702,7 @@ static int listmle_warps(int L) { return L <= 1024 ? 4 : 1; }
 
 extern "C" int rs_listmle_order(const void* scores, int dtype, const int64_t* order, int32_t n_lists,
                                 int32_t L, void* loss, void* grad, int32_t* bad, void* stream) {
+    RS_NVTX();
     cudaStream_t st = as_stream(stream);
     RS_CHECK_ARG(dtype == RS_F32 || dtype == RS_F64, "rs_listmle_order: dtype must be f32/f64");
     RS_CHECK_ARG(n_lists >= 0 && L >= 0 && L <= 8192, "rs_listmle_order: need 0 <= list_len <= 8192");
@@ -729,6 +730,7 @@ extern "C" int rs_listmle_order(const void* scores, int dtype, const int64_t* or
 
 extern "C" int rs_listmle_lengths(const float* g, const int32_t* lengths, int32_t n_lists, int32_t L,
                                   int32_t width, float* loss, float* dg, void* stream) {
+    RS_NVTX();
     cudaStream_t st = as_stream(stream);
     RS_CHECK_ARG(width >= 1, "bucket_width must be >= 1");
     RS_CHECK_ARG(n_lists >= 0 && L >= 1 && L <= 4096, "rs_listmle_lengths: need 1 <= list_len <= 4096");

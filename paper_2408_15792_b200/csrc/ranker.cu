@@ -479,12 +479,14 @@ extern "C" size_t rs_ranker_workspace_size(const rs_ranker_config* cfg, int32_t 
 extern "C" int rs_ranker_forward(const rs_ranker_config* cfg, const void* params, const int32_t* ids,
                                  const int32_t* last_pos, int32_t B, int32_t S, float* g, float* score,
                                  void* ws, size_t ws_bytes, void* stream) {
+    RS_NVTX();
     return rs_ranker_forward_ex(cfg, params, ids, last_pos, B, S, g, score, nullptr, ws, ws_bytes, stream);
 }
 
 extern "C" int rs_ranker_forward_ex(const rs_ranker_config* cfg, const void* params, const int32_t* ids,
                                     const int32_t* last_pos, int32_t B, int32_t S, float* g, float* score,
                                     float* feat, void* ws, size_t ws_bytes, void* stream) {
+    RS_NVTX();
     cudaStream_t st = as_stream(stream);
     RS_TRY(check_cfg(cfg));
     RS_CHECK_ARG(B > 0 && S > 0 && S <= cfg->max_pos, "ranker: need B > 0 and 0 < S <= max_pos");

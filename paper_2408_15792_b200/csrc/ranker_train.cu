@@ -220,6 +220,7 @@ extern "C" int rs_ranker_grad(const rs_ranker_config* cfg, const void* params, f
                               const int32_t* last_pos, const int32_t* lengths, int32_t n_lists, int32_t list_len, int32_t S,
                               int32_t bucket_width, int32_t lists_per_micro, float* loss_out, void* ws,
                               size_t ws_bytes, void* stream) {
+    RS_NVTX();
     cudaStream_t st = as_stream(stream);
     RS_CHECK_ARG(cfg && params && grad && ids && lengths && loss_out, "rs_ranker_grad: NULL argument");
     RS_CHECK_ARG(n_lists > 0 && list_len >= 1 && S >= 1 && S <= 512, "rs_ranker_grad: need S <= 512 (got %d)", S);
@@ -284,6 +285,7 @@ extern "C" int rs_ranker_grad_cls(const rs_ranker_config* cfg, const void* param
                                   int32_t n_classes, const float* cls_w, const float* cls_b, float* cls_grad,
                                   int32_t prompts_per_micro, float* loss_out, void* ws, size_t ws_bytes,
                                   void* stream) {
+    RS_NVTX();
     cudaStream_t st = as_stream(stream);
     RS_CHECK_ARG(cfg && params && grad && ids && labels && cls_w && cls_b && cls_grad && loss_out,
                  "rs_ranker_grad_cls: NULL argument");

@@ -1316,6 +1316,7 @@ extern "C" size_t rs_arrival_rank_workspace_size(int64_t n) {
 
 extern "C" int rs_arrival_rank(const double* arr, const int64_t* id, int64_t n, uint32_t* rank, void* ws,
                                size_t ws_bytes, void* stream) {
+    RS_NVTX();
     cudaStream_t st = as_stream(stream);
     RS_CHECK_ARG(n >= 0 && n <= (int64_t)RANK_MASK, "rs_arrival_rank: n out of range");
     if (n == 0) return RS_OK;
@@ -1351,6 +1352,7 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
                             int32_t pquantum, int32_t calibrated, int32_t preemptive, int64_t* run,
                             int64_t* prom, int64_t* dem, int32_t* counts, void* ws, size_t ws_bytes,
                             void* stream) {
+    RS_NVTX();
     cudaStream_t st = as_stream(stream);
     RS_CHECK_ARG(q != nullptr, "rs_rank_step: queue is NULL");
     RS_CHECK_ARG(q->n >= 0 && q->n <= (int64_t)RANK_MASK, "rs_rank_step: n out of range");

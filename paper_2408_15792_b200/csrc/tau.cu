@@ -412,6 +412,7 @@ static int tau_general(const void* x, int xd, const void* y, int yd, int64_t n, 
 // to run rs_tau_counts (general path) instead.
 extern "C" int rs_tau_counts_fast(const void* x, int xd, const void* y, int yd, int64_t n, int64_t* counts,
                                   void* ws, size_t ws_bytes, void* stream) {
+    RS_NVTX();
     cudaStream_t st = as_stream(stream);
     RS_CHECK_ARG(n >= 0 && n < (int64_t)0xF0000000ll, "rs_tau_counts_fast: n=%lld out of range", (long long)n);
     RS_CHECK_ARG(xd >= RS_F32 && xd <= RS_I64 && yd >= RS_F32 && yd <= RS_I64, "rs_tau_counts_fast: bad dtype");
@@ -435,6 +436,7 @@ extern "C" int rs_tau_counts_fast(const void* x, int xd, const void* y, int yd, 
 
 extern "C" int rs_tau_counts(const void* x, int xd, const void* y, int yd, int64_t n, int64_t* counts,
                              void* ws, size_t ws_bytes, void* stream) {
+    RS_NVTX();
     cudaStream_t st = as_stream(stream);
     RS_CHECK_ARG(n >= 0 && n < (int64_t)0xF0000000ll, "rs_tau_counts: n=%lld out of range", (long long)n);
     RS_CHECK_ARG(xd >= RS_F32 && xd <= RS_I64 && yd >= RS_F32 && yd <= RS_I64, "rs_tau_counts: bad dtype");

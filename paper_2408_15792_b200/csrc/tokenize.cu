@@ -102,6 +102,7 @@ using namespace rs;
 extern "C" int rs_tokenize(const uint8_t* text_dev, const int64_t* offsets_dev, int32_t n, int32_t seq_len,
                            int32_t vocab, int32_t pad_id, uint32_t salt_crc, int32_t* ids_dev, int32_t* last_dev,
                            int32_t* bad_dev, void* stream) {
+    RS_NVTX();
     RS_CHECK_ARG(n >= 0 && seq_len >= 1 && vocab > 4, "rs_tokenize: need n >= 0, seq_len >= 1, vocab > 4");
     if (n == 0) return RS_OK;
     RS_CHECK_ARG(text_dev != nullptr && offsets_dev && ids_dev && last_dev && bad_dev, "rs_tokenize: NULL argument");

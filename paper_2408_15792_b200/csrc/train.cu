@@ -474,6 +474,7 @@ int head_backward(const float* h, const int32_t* last, int B, int S, const void*
 
 extern "C" int rs_adam_step(float* master, float* m, float* v, float* grad, void* params_bf16, int64_t n, float lr,
                             float beta1, float beta2, float eps, int64_t t, float grad_scale, void* stream) {
+    RS_NVTX();
     RS_CHECK_ARG(n >= 0 && t >= 1, "rs_adam_step: need n >= 0 and t >= 1");
     if (n == 0) return RS_OK;
     const float bc1 = 1.f - powf(beta1, (float)t), bc2 = 1.f - powf(beta2, (float)t);
