@@ -282,9 +282,12 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     const int kblocks_all = K / G2_BK;
     const int kb_per = (kblocks_all + k_splits - 1) / k_splits;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-    // work item w -> output tile (w / k_splits) and K split (w % k_splits)
+    // work item w -> output tile (w % n_tiles) and K split (w / n_tiles): split-major, so
+    // the clusters running at the same time share one K range (the wgrad token slab) and
+    // its A / B k-blocks are read from DRAM about once, then served from L2
+    const int n_tiles = (M / G2_BM) * tiles_n;
     auto kb_range = [&](int w, int& kb0, int& kb1) {
-        const int sp = w % k_splits;
+        const int sp = w / n_tiles;
         kb0 = sp * kb_per;
         kb1 = min(kblocks_all, kb0 + kb_per);
     };
@@ -295,7 +298,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int w = cid; w < n_work; w += ncl) {
-                const int tile = w / k_splits;
+                const int tile = w % n_tiles;
                 int kb0, kb1;
                 kb_range(w, kb0, kb1);
                 const int m0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
@@ -380,7 +383,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         auto prefetch_r = [&](int n) {
             const int w = cid + (n >> 3) * ncl;
             if (w >= n_work) return;
-            const int tile = w / k_splits;
+            const int tile = w % n_tiles;
             const int rm0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
             const int rn0 = (tile % tiles_n) * G2_BN;
             const int b = n % NBUF;
@@ -390,11 +393,11 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         if (G2Cfg<EPI>::streams && lane == 0)
             for (int n = 0; n < PD; ++n) prefetch_r(n);
         for (int w = cid; w < n_work; w += ncl) {
-            const int tile = w / k_splits;
+            const int tile = w % n_tiles;
             const int m0 = (tile / tiles_n) * G2_BM + rank * G2_HALF;
             const int n0 = (tile % tiles_n) * G2_BN;
-            // split-K partials land in slice (w % k_splits) of a [k_splits * M, N] buffer
-            const int mo = (EPI == 6) ? m0 + (w % k_splits) * M : m0;
+            // split-K partials land in slice (w / n_tiles) of a [k_splits * M, N] buffer
+            const int mo = (EPI == 6) ? m0 + (w / n_tiles) * M : m0;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
 #pragma unroll 1
