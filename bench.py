@@ -187,7 +187,9 @@ def gemm_roofline(pk, M=1 << 20, reps=5):
     achieved = tot_f / tot_t / 1e9
     # DRAM bytes of the same four launches from the committed ncu --set full capture
     traffic = None
-    tp = ROOT / "profiles" / "r01_gemm_traffic.json"
+    tp = ROOT / "profiles" / "r02_gemm_traffic.json"
+    if not tp.exists():
+        tp = ROOT / "profiles" / "r01_gemm_traffic.json"
     if tp.exists():
         tr = json.loads(tp.read_text())["per_shape"]
         keys = [f"{N}x{K}" for N, K, _ in shapes]
@@ -202,7 +204,9 @@ def gemm_roofline(pk, M=1 << 20, reps=5):
 
 def sort_traffic(key):
     """DRAM bytes (read + write) of one call from the committed ncu capture, or None."""
-    p = ROOT / "profiles" / "r01_sort_traffic.json"
+    p = ROOT / "profiles" / "r02_sort_traffic.json"
+    if not p.exists():
+        p = ROOT / "profiles" / "r01_sort_traffic.json"
     try:
         d = json.loads(p.read_text())[key]
         return d["dram_read_bytes"] + d["dram_write_bytes"]
