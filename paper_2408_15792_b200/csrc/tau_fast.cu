@@ -723,12 +723,15 @@ __device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint
             }
         }
     }
-    __syncthreads();
+    // A warp's threads own 32 * TF_ITEMS consecutive positions, so while both runs of a
+    // merge lie inside one warp's range (2w <= 32 * TF_ITEMS) a warp barrier suffices.
+    constexpr int WSPAN = 32 * TF_ITEMS;
+    if (2 * TF_ITEMS <= WSPAN) __syncwarp(); else __syncthreads();
     if (act) {
 #pragma unroll
         for (int k = 0; k < TF_ITEMS; ++k) sk[tf_pidx(t * TF_ITEMS + k)] = r[k];
     }
-    __syncthreads();
+    if (2 * TF_ITEMS <= WSPAN) __syncwarp(); else __syncthreads();
     for (int w = TF_ITEMS; w < mp; w <<= 1) {
         if (act) {
             // runs [pb, pb + la) and [pb + w, pb + w + lb), clipped at mp (any multiple of 16)
@@ -760,13 +763,15 @@ __device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint
                 kb = take_b ? v : kb;
             }
         }
-        __syncthreads();
+        // the next level (width 2w) reads runs of this one: warp-local while 4w <= WSPAN
+        if (2 * w <= WSPAN) __syncwarp(); else __syncthreads();
         if (act) {
 #pragma unroll
             for (int k = 0; k < TF_ITEMS; ++k) sk[tf_pidx(t * TF_ITEMS + k)] = r[k];
         }
-        __syncthreads();
+        if (4 * w <= WSPAN) __syncwarp(); else __syncthreads();
     }
+    __syncthreads();  // the callers read the sorted keys across warps
     return inv;
 }
 
