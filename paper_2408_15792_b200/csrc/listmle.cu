@@ -676,7 +676,8 @@ __global__ void __launch_bounds__(256) listmle_lengths64xN_kernel(const float* _
             // each lane stores its own IPL contiguous items as 16-B vectors
             __syncwarp();
 #pragma unroll
-            for (int e = 0; e < IPL; ++e) sg[wid][sub][sidx[e]] = gr[e];
+            for (int e = 0; e < IPL; ++e)
+                if (live) sg[wid][sub][sidx[e]] = gr[e];  // a dead group's keys all map to slot 63
             __syncwarp();
             if (live) {
 #pragma unroll

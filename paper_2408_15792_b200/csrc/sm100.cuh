@@ -53,14 +53,31 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// try_wait with a suspend-time hint: the thread sleeps in the barrier unit until the phase
+// completes (or the hint, in ns, runs out) instead of spinning on the issue port it
+// shares with the compute warps of its SM sub-partition.
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(100000u)
+        : "memory");
+    return ok != 0;
+}
 // Watchdog: a pipeline that deadlocks (a protocol bug) traps after ~10 s instead of
-// hanging the GPU; the host then sees cudaErrorLaunchFailure. The timer is read only
-// every 4096 failed polls, so the steady-state cost is one counter increment.
+// hanging the GPU; the host then sees cudaErrorLaunchFailure. The timer is read once per
+// 64 suspending polls (an inner loop of its own: a predicated timer read on every poll
+// would cost a dozen issue slots each).
 static __device__ __noinline__ void mbar_wait_slow(uint64_t* bar, uint32_t parity) {
     const uint64_t t0 = globaltimer_ns();
-    for (uint32_t k = 1;; ++k) {
-        if (mbar_try_wait(bar, parity)) return;
-        if ((k & 4095u) == 0 && globaltimer_ns() - t0 > 10000000000ull) __trap();
+    while (true) {
+#pragma unroll 1
+        for (int k = 0; k < 64; ++k)
+            if (mbar_try_wait_sleep(bar, parity)) return;
+        if (globaltimer_ns() - t0 > 10000000000ull) __trap();
     }
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
