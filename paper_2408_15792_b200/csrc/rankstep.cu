@@ -13,6 +13,7 @@
 // Device pipeline: key build -> stable merge sort of (RankKey, index) -> greedy fill
 // (one warp; prefix-sum resolution of each 32-wide chunk) -> elementwise state update
 // with order-preserving compaction of promoted / demoted ids.
+#include <cstdlib>
 #include <utility>
 #include "common.cuh"
 #include "mergesort.cuh"
@@ -138,11 +139,23 @@ __global__ void fill_budget(const uint32_t* __restrict__ order, const int32_t* _
 // decision are no-ops (the level count is data-dependent and decided on the device).
 constexpr int SEL_BITS = 11, SEL_BINS = 1 << SEL_BITS, SEL_LEVELS = 9;  // 99 >= 96 bits
 constexpr int SEL_CAP = 2048;
+// smaller queues stop at a smaller final bucket: the one-block sort of the candidates
+// (<= k + cap keys) is then a 1024-key network instead of a 4096-key one
+constexpr int SEL_CAP_SMALL = 512;
+constexpr uint32_t SEL_SMALL_N = 1u << 20;
 constexpr int SEL_SORT = 4096;  // >= max_batch + SEL_CAP, power of two
 // Below this many rows the full merge sort (a block-sort launch + log2(n / 2048) pass
 // launches) beats the select's SEL_LEVELS histogram launches + gather + final sort: the
 // engine loop's queues (10^3-10^5 rows) are all below it, cfg4's 1M queue is above.
-constexpr uint32_t SEL_MIN_N = 1u << 18;
+constexpr uint32_t SEL_MIN_N_DEFAULT = 1u << 14;
+// RS_SEL_MIN_N overrides the crossover (measurement experiments)
+static uint32_t sel_min_n() {
+    static const uint32_t v = [] {
+        const char* e = getenv("RS_SEL_MIN_N");
+        return e ? (uint32_t)strtoul(e, nullptr, 10) : SEL_MIN_N_DEFAULT;
+    }();
+    return v;
+}
 constexpr int SEL_THREADS = 1024;
 constexpr int SEL_PHASE_A = 8;  // level-0 chunks per warp counted before the CTA's bin bound is fixed
 // level 0 keeps its candidates only for queues this large (smaller ones: the level-1 pass
@@ -386,7 +399,7 @@ __device__ __forceinline__ uint32_t sel_digit(typename Src::V v, uint32_t level)
 
 template <typename Src>
 __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c,
-                               uint32_t dom_cap);
+                               uint32_t dom_cap, uint32_t cap);
 
 // Warp-aggregated shared-memory histogram increment: lanes holding the same digit add once
 // (the SoA keys concentrate on few level-0 / level-1 bins: one atomic per lane would
@@ -419,7 +432,7 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, Sel
                                                         uint32_t* __restrict__ hist, uint32_t k,
                                                         unsigned __int128* __restrict__ dom_v,
                                                         uint32_t* __restrict__ dom_i, uint32_t* __restrict__ dom_cnt,
-                                                        uint32_t dom_cap) {
+                                                        uint32_t dom_cap, uint32_t cap) {
     if (st->done) return;
     __shared__ uint32_t h[SEL_BINS + 1];  // [SEL_BINS]: scratch for masked-off lanes
     __shared__ uint32_t scnt;
@@ -774,7 +787,7 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, Sel
             if (LEVEL == 0) st->dom_overflow = 0;  // level 1's own keep pass (if any) starts clean
             if (LEVEL == 1 && st->dom_ok && !st->dom_overflow) st->compacted = 1;
         }
-        sel_pick_block<Src>(st, pfx128, hist, k, h, dom_cap);
+        sel_pick_block<Src>(st, pfx128, hist, k, h, dom_cap, cap);
     }
 }
 
@@ -782,7 +795,7 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, Sel
 // (c = shared scratch of SEL_BINS words), clear the histogram for the next level.
 template <typename Src>
 __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c,
-                               uint32_t dom_cap) {
+                               uint32_t dom_cap, uint32_t cap) {
     __shared__ uint32_t pick, below;
     for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) c[b] = __ldcg(&hist[b]);
     __syncthreads();
@@ -820,7 +833,7 @@ __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t
         st->level = level + 1;
         st->arrived = 0;
         if (level == 0) st->dom_ok = (st->less + c[pick] <= dom_cap) ? 1u : 0u;
-        if (c[pick] <= SEL_CAP || level + 1 == Src::LEVELS) {
+        if (c[pick] <= cap || level + 1 == Src::LEVELS) {
             st->done = 1;
             st->final_level = level + 1;
         }
@@ -895,6 +908,73 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_sort_emit(const unsigned __in
         sched[idx] = 1;
     }
     if (threadIdx.x == 0) counts[0] = (int32_t)k;
+}
+
+// The same for <= 1024 candidates: one element per thread, the bitonic stages of stride
+// < 32 over warp shuffles (no barriers), the wider ones through shared memory. Keys are
+// distinct (the arrival rank is in them), so the network's order is the sort order.
+__device__ __forceinline__ bool u128_less(const uint4& a, const uint4& b) {  // .w most significant
+    if (a.w != b.w) return a.w < b.w;
+    if (a.z != b.z) return a.z < b.z;
+    if (a.y != b.y) return a.y < b.y;
+    return a.x < b.x;
+}
+__global__ void __launch_bounds__(1024) sel_sort_emit_small(const unsigned __int128* __restrict__ ck,
+                                                            const uint32_t* __restrict__ ci,
+                                                            const SelState* __restrict__ st,
+                                                            const int64_t* __restrict__ id, uint32_t k,
+                                                            int64_t* __restrict__ run, uint8_t* __restrict__ sched,
+                                                            int32_t* __restrict__ counts) {
+    __shared__ uint4 sk[1024];
+    __shared__ uint32_t sv[1024];
+    const uint32_t m = min(st->n_cand, 1024u);
+    uint32_t P = 32;
+    while (P < m) P <<= 1;
+    const uint32_t t = threadIdx.x;
+    uint4 v = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    uint32_t ix = 0xffffffffu;
+    if (t < m) {
+        v = *reinterpret_cast<const uint4*>(ck + t);
+        ix = ci[t];
+    }
+    for (uint32_t kk = 2; kk <= P; kk <<= 1) {
+        const bool up = (t & kk) == 0;
+        for (uint32_t j = kk >> 1; j > 0; j >>= 1) {
+            uint4 o;
+            uint32_t oi;
+            if (j >= 32) {  // block-uniform branch
+                __syncthreads();
+                if (t < P) {
+                    sk[t] = v;
+                    sv[t] = ix;
+                }
+                __syncthreads();
+                if (t < P) {
+                    o = sk[t ^ j];
+                    oi = sv[t ^ j];
+                }
+            } else {
+                o.x = __shfl_xor_sync(0xffffffffu, v.x, j);
+                o.y = __shfl_xor_sync(0xffffffffu, v.y, j);
+                o.z = __shfl_xor_sync(0xffffffffu, v.z, j);
+                o.w = __shfl_xor_sync(0xffffffffu, v.w, j);
+                oi = __shfl_xor_sync(0xffffffffu, ix, j);
+            }
+            if (t < P) {
+                const bool lower = (t & j) == 0;
+                const bool take_o = (lower == up) ? u128_less(o, v) : u128_less(v, o);
+                if (take_o) {
+                    v = o;
+                    ix = oi;
+                }
+            }
+        }
+    }
+    if (t < k && t < P) {
+        run[t] = id[ix];
+        sched[ix] = 1;
+    }
+    if (t == 0) counts[0] = (int32_t)k;
 }
 
 constexpr int UPD_THREADS = 1024;
@@ -1281,17 +1361,19 @@ static void rank_layout(A& a, uint64_t n, RankWs* w) {
     auto ci = a.template take<uint32_t>(SEL_SORT);
     // rows kept by the select's level-1 pass (at most 4M: beyond, the passes read the columns)
     const uint32_t dcap = (uint32_t)std::min<uint64_t>(n, 1u << 22);
-    auto dv = a.template take<unsigned __int128>(n > SEL_MIN_N ? dcap : 1);
-    auto di = a.template take<uint32_t>(n > SEL_MIN_N ? dcap : 1);
+    auto dv = a.template take<unsigned __int128>(n > sel_min_n() ? dcap : 1);
+    auto di = a.template take<uint32_t>(n > sel_min_n() ? dcap : 1);
     auto dc = a.template take<uint32_t>(1024);  // per-CTA kept-row counts (grid <= 1024)
     auto sp = a.template take<int>(ms_splits(np));
-    if (w) *w = RankWs{ka, kb, va, vb, sc, pd, bc, er, sl, px, hi, ck, ci, dv, di, dc, n > SEL_MIN_N ? dcap : 0u, sp};
+    if (w) *w = RankWs{ka, kb, va, vb, sc, pd, bc, er, sl, px, hi, ck, ci, dv, di, dc, n > sel_min_n() ? dcap : 0u, sp};
 }
 // the select's histogram launches, LEVEL = 0 .. Src::LEVELS - 1 in order
 template <typename Src, int... L>
 static void sel_levels(std::integer_sequence<int, L...>, uint32_t gb, cudaStream_t st, const Src& src, uint32_t n,
                        const RankWs& w, uint32_t k) {
-    ((sel_hist<Src, L><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.hist, k, w.dv, w.di, w.dcnt, w.dcap)), ...);
+    const uint32_t cap = n <= SEL_SMALL_N ? SEL_CAP_SMALL : SEL_CAP;
+    ((sel_hist<Src, L><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.hist, k, w.dv, w.di, w.dcnt, w.dcap, cap)),
+     ...);
 }
 struct RankSizer {
     ArenaSizer s;
@@ -1377,7 +1459,7 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
     const int T = 256;
     const uint32_t k = min(n, (uint32_t)max_batch);
     const bool soa64 = q->score_dtype == RS_F32 && !calibrated;
-    if (kv_budget < 0 && n > SEL_MIN_N && k + SEL_CAP <= (uint32_t)SEL_SORT) {
+    if (kv_budget < 0 && n > sel_min_n() && k + SEL_CAP <= (uint32_t)SEL_SORT) {
         // top-k select (see sel_hist): <= LEVELS histogram passes, most no-ops
         const size_t smem = SEL_SORT * (sizeof(unsigned __int128) + sizeof(uint32_t));
         RS_CUDA(ensure_smem((const void*)sel_sort_emit, (int)smem));
@@ -1398,7 +1480,10 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
             sel_gather<SrcKeys><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.ck, w.ci, w.dv, w.di, w.dcnt, w.dcap);
         }
         RS_LAUNCH_CHECK();
-        sel_sort_emit<<<1, SEL_THREADS, smem, st>>>(w.ck, w.ci, w.sel, q->id, k, run, w.sched, counts);
+        if (n <= SEL_SMALL_N && k + SEL_CAP_SMALL <= 1024)  // candidates <= k + SEL_CAP_SMALL
+            sel_sort_emit_small<<<1, 1024, 0, st>>>(w.ck, w.ci, w.sel, q->id, k, run, w.sched, counts);
+        else
+            sel_sort_emit<<<1, SEL_THREADS, smem, st>>>(w.ck, w.ci, w.sel, q->id, k, run, w.sched, counts);
     } else {
         build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
         RS_LAUNCH_CHECK();
