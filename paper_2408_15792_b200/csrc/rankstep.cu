@@ -143,6 +143,7 @@ constexpr int SEL_CAP = 2048;
 // (<= k + cap keys) is then a 1024-key network instead of a 4096-key one
 constexpr int SEL_CAP_SMALL = 512;
 constexpr uint32_t SEL_SMALL_N = 1u << 20;
+constexpr uint32_t SEL_FUSED_N = 1u << 18;  // up to here the select is one cooperative launch (<= 64 CTAs)
 constexpr int SEL_SORT = 4096;  // >= max_batch + SEL_CAP, power of two
 // Below this many rows the full merge sort (a block-sort launch + log2(n / 2048) pass
 // launches) beats the select's SEL_LEVELS histogram launches + gather + final sort: the
@@ -172,6 +173,7 @@ struct SelState {
     uint32_t final_level;
     uint32_t n_cand;
     uint32_t arrived;  // blocks done with the current level's histogram
+    uint32_t bar_count, bar_gen;  // sel_fused's grid barrier
 };
 
 // Key sources for the select. Both give each row a distinct integer whose order is the
@@ -919,15 +921,13 @@ __device__ __forceinline__ bool u128_less(const uint4& a, const uint4& b) {  // 
     if (a.y != b.y) return a.y < b.y;
     return a.x < b.x;
 }
-__global__ void __launch_bounds__(1024) sel_sort_emit_small(const unsigned __int128* __restrict__ ck,
-                                                            const uint32_t* __restrict__ ci,
-                                                            const SelState* __restrict__ st,
-                                                            const int64_t* __restrict__ id, uint32_t k,
-                                                            int64_t* __restrict__ run, uint8_t* __restrict__ sched,
-                                                            int32_t* __restrict__ counts) {
-    __shared__ uint4 sk[1024];
-    __shared__ uint32_t sv[1024];
-    const uint32_t m = min(st->n_cand, 1024u);
+// one 1024-thread block; sk / sv: shared scratch of 1024 entries
+__device__ __forceinline__ void sel_emit_small_block(const unsigned __int128* __restrict__ ck,
+                                                     const uint32_t* __restrict__ ci, uint32_t n_cand,
+                                                     const int64_t* __restrict__ id, uint32_t k,
+                                                     int64_t* __restrict__ run, uint8_t* __restrict__ sched,
+                                                     int32_t* __restrict__ counts, uint4* sk, uint32_t* sv) {
+    const uint32_t m = min(n_cand, 1024u);
     uint32_t P = 32;
     while (P < m) P <<= 1;
     const uint32_t t = threadIdx.x;
@@ -975,6 +975,77 @@ __global__ void __launch_bounds__(1024) sel_sort_emit_small(const unsigned __int
         sched[ix] = 1;
     }
     if (t == 0) counts[0] = (int32_t)k;
+}
+__global__ void __launch_bounds__(1024) sel_sort_emit_small(const unsigned __int128* __restrict__ ck,
+                                                            const uint32_t* __restrict__ ci,
+                                                            const SelState* __restrict__ st,
+                                                            const int64_t* __restrict__ id, uint32_t k,
+                                                            int64_t* __restrict__ run, uint8_t* __restrict__ sched,
+                                                            int32_t* __restrict__ counts) {
+    __shared__ uint4 sk[1024];
+    __shared__ uint32_t sv[1024];
+    sel_emit_small_block(ck, ci, st->n_cand, id, k, run, sched, counts, sk, sv);
+}
+
+// ---- queues of 2^14 .. 2^18 rows: the whole select in one cooperative launch ----------
+// The levels' histogram passes, the bucket picks, the gather and the one-block sort of the
+// candidates, separated by grid barriers (all CTAs co-resident: cooperative launch), so a
+// step costs one launch instead of LEVELS + 2 (most of them no-ops past the decision).
+__device__ __forceinline__ void grid_barrier(uint32_t* count, volatile uint32_t* gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t g = *gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            *count = 0;
+            __threadfence();
+            atomicAdd(const_cast<uint32_t*>(gen), 1u);
+        } else {
+            while (*gen == g) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <typename Src>
+__global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, SelState* __restrict__ st,
+                                                         unsigned __int128* __restrict__ pfx128,
+                                                         uint32_t* __restrict__ hist, uint32_t k, uint32_t cap,
+                                                         unsigned __int128* __restrict__ ck, uint32_t* __restrict__ ci,
+                                                         uint32_t* __restrict__ bar, const int64_t* __restrict__ id,
+                                                         int64_t* __restrict__ run, uint8_t* __restrict__ sched,
+                                                         int32_t* __restrict__ counts) {
+    using V = typename Src::V;
+    __shared__ uint32_t h[SEL_BINS + 1];
+    __shared__ uint4 sk[1024];
+    __shared__ uint32_t sv[1024];
+    for (uint32_t level = 0; level < (uint32_t)Src::LEVELS; ++level) {
+        if (*(volatile uint32_t*)&st->done) break;  // written before the last barrier
+        for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) h[b] = 0;
+        __syncthreads();
+        const int shift = Src::BITS - SEL_BITS * (int)level;
+        const V wsh = level ? (V)(*(volatile unsigned __int128*)pfx128 >> shift) : (V)0;
+        sel_rows(src, n, [&](uint32_t, V v, bool ok) {
+            hist_add_warp(h, sel_digit<Src>(v, level), ok && (level == 0 || vshr<Src>(v, shift) == wsh));
+        });
+        __syncthreads();
+        for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS)
+            if (h[b]) atomicAdd(&hist[b], h[b]);
+        grid_barrier(bar, bar + 1);
+        if (blockIdx.x == 0) sel_pick_block<Src>(st, pfx128, hist, k, h, 0u, cap);
+        grid_barrier(bar, bar + 1);
+    }
+    {  // gather every key at or below the chosen bucket
+        const int shift = Src::BITS - SEL_BITS * (int)*(volatile uint32_t*)&st->final_level;
+        const V lim = (V)(*(volatile unsigned __int128*)pfx128 >> shift);
+        sel_rows(src, n, [&](uint32_t i, V v, bool ok) {
+            sel_append(ok && vshr<Src>(v, shift) <= lim, to128<Src>(v), i, &st->n_cand, ck, ci, SEL_SORT);
+        });
+    }
+    grid_barrier(bar, bar + 1);
+    if (blockIdx.x == 0)
+        sel_emit_small_block(ck, ci, *(volatile uint32_t*)&st->n_cand, id, k, run, sched, counts, sk, sv);
 }
 
 constexpr int UPD_THREADS = 1024;
@@ -1467,7 +1538,32 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         RS_CUDA(cudaMemsetAsync(w.pfx, 0, sizeof(unsigned __int128), st));
         RS_CUDA(cudaMemsetAsync(w.hist, 0, SEL_BINS * sizeof(uint32_t), st));
         const uint32_t gb = min((n / 4 + SEL_THREADS) / SEL_THREADS, (uint32_t)num_sms() * 2);
-        if (soa64) {
+        const bool fused = n <= SEL_FUSED_N && k + SEL_CAP_SMALL <= 1024;
+        if (fused) {
+            // one cooperative launch: levels, picks, gather and the candidates' sort
+            cudaLaunchConfig_t lc{};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeCooperative;
+            at[0].val.cooperative = 1;
+            lc.gridDim = dim3(gb);
+            lc.blockDim = dim3(SEL_THREADS);
+            lc.dynamicSmemBytes = 0;
+            lc.stream = st;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            uint32_t* bar = &w.sel->bar_count;
+            if (soa64) {
+                const SrcSoa64 src{static_cast<const float*>(q->score), q->flags, q->arrival_rank, preemptive, counts + 3};
+                RS_CUDA(cudaLaunchKernelEx(&lc, sel_fused<SrcSoa64>, src, n, w.sel, w.pfx, w.hist, k,
+                                           (uint32_t)SEL_CAP_SMALL, w.ck, w.ci, bar, q->id, run, w.sched, counts));
+            } else {
+                build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
+                RS_LAUNCH_CHECK();
+                const SrcKeys src{w.kb};
+                RS_CUDA(cudaLaunchKernelEx(&lc, sel_fused<SrcKeys>, src, n, w.sel, w.pfx, w.hist, k,
+                                           (uint32_t)SEL_CAP_SMALL, w.ck, w.ci, bar, q->id, run, w.sched, counts));
+            }
+        } else if (soa64) {
             // keys straight from the queue columns: no key pass, 9 B per row per level
             const SrcSoa64 src{static_cast<const float*>(q->score), q->flags, q->arrival_rank, preemptive, counts + 3};
             sel_levels<SrcSoa64>(std::make_integer_sequence<int, SrcSoa64::LEVELS>{}, gb, st, src, n, w, k);
@@ -1480,7 +1576,9 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
             sel_gather<SrcKeys><<<gb, SEL_THREADS, 0, st>>>(src, n, w.sel, w.pfx, w.ck, w.ci, w.dv, w.di, w.dcnt, w.dcap);
         }
         RS_LAUNCH_CHECK();
-        if (n <= SEL_SMALL_N && k + SEL_CAP_SMALL <= 1024)  // candidates <= k + SEL_CAP_SMALL
+        if (fused) {
+            // sorted and emitted inside sel_fused
+        } else if (n <= SEL_SMALL_N && k + SEL_CAP_SMALL <= 1024)  // candidates <= k + SEL_CAP_SMALL
             sel_sort_emit_small<<<1, 1024, 0, st>>>(w.ck, w.ci, w.sel, q->id, k, run, w.sched, counts);
         else
             sel_sort_emit<<<1, SEL_THREADS, smem, st>>>(w.ck, w.ci, w.sel, q->id, k, run, w.sched, counts);

@@ -159,3 +159,30 @@ def test_topk_select_matches_full_sort(n, max_batch, dist):
     assert d0.run == d1.run and len(d0.run) == min(n, max_batch)
     assert d0.promoted == d1.promoted and d0.demoted == d1.demoted
     assert (f0 == f1).all() and (s0 == s1).all() and (q0 == q1).all()
+
+
+@pytest.mark.parametrize("n", [40_000, 200_000, 1 << 20])
+def test_rank_step_graph_replay_equals_eager(n):
+    """The CUDA-graph replay of a rank step (40k / 200k rows: the cooperative fused select;
+    1M: the multi-launch select) equals two eager steps: batch, promotions and state."""
+    import torch
+    from paper_2408_15792_b200.schedulers import DeviceQueue, SchedulerConfig
+    rng = np.random.default_rng(n)
+    kw = dict(score=rng.normal(size=n), scored=rng.random(n) > 0.01, priority=rng.random(n) < 0.02,
+              running=rng.random(n) < 0.3, prompt_tokens=rng.integers(1, 100, n).astype(np.int32),
+              generated_tokens=rng.integers(0, 100, n).astype(np.int32), arrival_time=rng.random(n) * 100,
+              ids=rng.permutation(n).astype(np.int64), starvation=rng.integers(0, 100, n).astype(np.int32),
+              quantum=rng.integers(0, 3, n).astype(np.int32))
+    cfg = SchedulerConfig(max_batch=256, starvation_threshold=50, priority_quantum=5)
+    for calib in (False, True):
+        a = DeviceQueue.from_arrays(**kw, score_dtype=torch.float32)
+        b = DeviceQueue.from_arrays(**kw, score_dtype=torch.float32)
+        a.rank_step(cfg, None, length_calibrated=calib)
+        a.rank_step(cfg, None, length_calibrated=calib)
+        replay = b.rank_step_graph(cfg, None, length_calibrated=calib)  # one eager step + capture
+        replay()
+        torch.cuda.synchronize()
+        da, db = a.decision(), b.decision()
+        assert da.run == db.run and da.promoted == db.promoted and da.demoted == db.demoted
+        for x, y in ((a.flags, b.flags), (a.starvation, b.starvation), (a.quantum, b.quantum)):
+            assert torch.equal(x, y)
