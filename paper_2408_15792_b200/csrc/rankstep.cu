@@ -1001,7 +1001,7 @@ __device__ __forceinline__ void grid_barrier(uint32_t* count, volatile uint32_t*
             __threadfence();
             atomicAdd(const_cast<uint32_t*>(gen), 1u);
         } else {
-            while (*gen == g) __nanosleep(64);
+            while (*gen == g) {}
         }
         __threadfence();
     }
