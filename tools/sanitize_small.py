@@ -83,8 +83,11 @@ def main(which: str = "all"):
             pol = schedulers.RankingPolicy(schedulers.SchedulerConfig(max_batch=64), False)
             pol.schedule(reqs, 1 << 62)
             pol.schedule(reqs, 3000)
-        n = 300_000  # > 2^18: the top-k select path (f32 keys from the columns; f64 / calibrated keys)
-        for sdt, calib in ((torch.float32, False), (torch.float64, False), (torch.float32, True)):
+        # 40k rows: the one-launch cooperative select (sel_fused); 300k (> 2^18): the
+        # multi-launch select (f32 keys from the columns; f64 / calibrated keys)
+        for n, sdt, calib in ((40_000, torch.float32, False), (40_000, torch.float32, True),
+                              (300_000, torch.float32, False), (300_000, torch.float64, False),
+                              (300_000, torch.float32, True)):
             dq = schedulers.DeviceQueue.from_arrays(
                 score=rng.normal(size=n), scored=rng.random(n) < 0.95, priority=rng.random(n) < 0.01,
                 running=np.zeros(n, bool), prompt_tokens=rng.integers(1, 100, n),
