@@ -698,23 +698,25 @@ __global__ void __launch_bounds__(TF_SCAN_T) tf_groups(const TfParams* __restric
 }
 
 // ---- K9: the leaf walk -------------------------------------------------------------
-__device__ __forceinline__ int tf_pidx(int e) { return e + (e >> 4); }
+// one pad word per IT keys (the per-thread runs of IT consecutive keys start in different banks)
+template <int IT>
+__device__ __forceinline__ int tf_pidx(int e) { return e + (e >> (IT == 16 ? 4 : 3)); }
 
 // CTA merge sort of mp (a multiple of 16, <= TF_CAP) u32 keys in padded smem; threads
 // t < mp/16 own 16 consecutive outputs. Stable; with Count, returns the number of
 // strict inversions (pairs i < j with key_i > key_j) seen by this thread.
-template <bool Count>
-__device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint32_t (&r)[TF_ITEMS]) {
+template <bool Count, int IT>
+__device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint32_t (&r)[IT]) {
     const int t = threadIdx.x;
-    const bool act = t < (mp >> 4);
+    const bool act = t < mp / IT;
     unsigned long long inv = 0;
     if (act) {
 #pragma unroll
-        for (int k = 0; k < TF_ITEMS; ++k) r[k] = sk[tf_pidx(t * TF_ITEMS + k)];
+        for (int k = 0; k < IT; ++k) r[k] = sk[tf_pidx<IT>(t * IT + k)];
 #pragma unroll
-        for (int rd = 0; rd < TF_ITEMS; ++rd) {
+        for (int rd = 0; rd < IT; ++rd) {
 #pragma unroll
-            for (int k = (rd & 1); k + 1 < TF_ITEMS; k += 2) {
+            for (int k = (rd & 1); k + 1 < IT; k += 2) {
                 const uint32_t a = r[k], b = r[k + 1];
                 const bool sw = b < a;
                 r[k] = sw ? b : a;
@@ -723,19 +725,19 @@ __device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint
             }
         }
     }
-    // A warp's threads own 32 * TF_ITEMS consecutive positions, so while both runs of a
-    // merge lie inside one warp's range (2w <= 32 * TF_ITEMS) a warp barrier suffices.
-    constexpr int WSPAN = 32 * TF_ITEMS;
-    if (2 * TF_ITEMS <= WSPAN) __syncwarp(); else __syncthreads();
+    // A warp's threads own 32 * IT consecutive positions, so while both runs of a
+    // merge lie inside one warp's range (2w <= 32 * IT) a warp barrier suffices.
+    constexpr int WSPAN = 32 * IT;
+    if (2 * IT <= WSPAN) __syncwarp(); else __syncthreads();
     if (act) {
 #pragma unroll
-        for (int k = 0; k < TF_ITEMS; ++k) sk[tf_pidx(t * TF_ITEMS + k)] = r[k];
+        for (int k = 0; k < IT; ++k) sk[tf_pidx<IT>(t * IT + k)] = r[k];
     }
-    if (2 * TF_ITEMS <= WSPAN) __syncwarp(); else __syncthreads();
-    for (int w = TF_ITEMS; w < mp; w <<= 1) {
+    if (2 * IT <= WSPAN) __syncwarp(); else __syncthreads();
+    for (int w = IT; w < mp; w <<= 1) {
         if (act) {
             // runs [pb, pb + la) and [pb + w, pb + w + lb), clipped at mp (any multiple of 16)
-            const int pos = t * TF_ITEMS;
+            const int pos = t * IT;
             const int pb = pos & ~(2 * w - 1);
             const int diag = pos - pb;
             const int a0 = pb, b0 = pb + w;
@@ -743,22 +745,22 @@ __device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint
             int lo = max(0, diag - lb), hi = min(diag, la);
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
-                if (!(sk[tf_pidx(b0 + diag - 1 - mid)] < sk[tf_pidx(a0 + mid)])) lo = mid + 1; else hi = mid;
+                if (!(sk[tf_pidx<IT>(b0 + diag - 1 - mid)] < sk[tf_pidx<IT>(a0 + mid)])) lo = mid + 1; else hi = mid;
             }
             // branch-free serial merge of this thread's 16 outputs: the consumed side is
             // reloaded from a clamped index (an exhausted run's head is never taken)
             int i = lo, j = diag - lo;
-            uint32_t ka = sk[tf_pidx(a0 + min(i, la - 1))];  // la >= 16
-            uint32_t kb = sk[tf_pidx(lb > 0 ? b0 + min(j, lb - 1) : a0)];
+            uint32_t ka = sk[tf_pidx<IT>(a0 + min(i, la - 1))];  // la >= IT
+            uint32_t kb = sk[tf_pidx<IT>(lb > 0 ? b0 + min(j, lb - 1) : a0)];
 #pragma unroll
-            for (int k = 0; k < TF_ITEMS; ++k) {
+            for (int k = 0; k < IT; ++k) {
                 const bool take_b = j < lb && (i >= la || kb < ka);
                 r[k] = take_b ? kb : ka;
                 if (Count) inv += take_b ? (unsigned long long)(la - i) : 0ull;
                 i += take_b ? 0 : 1;
                 j += take_b ? 1 : 0;
                 const int nx = take_b ? b0 + min(j, lb - 1) : a0 + min(i, la - 1);
-                const uint32_t v = sk[tf_pidx(nx)];
+                const uint32_t v = sk[tf_pidx<IT>(nx)];
                 ka = take_b ? ka : v;
                 kb = take_b ? v : kb;
             }
@@ -767,7 +769,7 @@ __device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint
         if (2 * w <= WSPAN) __syncwarp(); else __syncthreads();
         if (act) {
 #pragma unroll
-            for (int k = 0; k < TF_ITEMS; ++k) sk[tf_pidx(t * TF_ITEMS + k)] = r[k];
+            for (int k = 0; k < IT; ++k) sk[tf_pidx<IT>(t * IT + k)] = r[k];
         }
         if (4 * w <= WSPAN) __syncwarp(); else __syncthreads();
     }
@@ -820,6 +822,7 @@ __device__ __forceinline__ int tf_excl_max(int v, int* sw) {
 
 constexpr size_t TF_LEAF_SMEM = (size_t)(TF_CAP + TF_CAP / 16) * 4 + 2 * TF_BINS * 4;
 
+template <int IT>
 __global__ void __launch_bounds__(TF_LEAF_T, 2) tf_leaf(const TfParams* __restrict__ p, uint32_t n,
                                                         const TfGroup* __restrict__ groups,
                                                         const uint32_t* __restrict__ gstart,
@@ -922,20 +925,20 @@ __global__ void __launch_bounds__(TF_LEAF_T, 2) tf_leaf(const TfParams* __restri
             }
             continue;
         }
-        const int mp = ((int)m + TF_ITEMS - 1) / TF_ITEMS * TF_ITEMS;
-        for (int e = threadIdx.x; e < mp; e += TF_LEAF_T) sk[tf_pidx(e)] = e < (int)m ? src[e] : 0xffffffffu;
+        const int mp = ((int)m + IT - 1) / IT * IT;
+        for (int e = threadIdx.x; e < mp; e += TF_LEAF_T) sk[tf_pidx<IT>(e)] = e < (int)m ? src[e] : 0xffffffffu;
         __syncthreads();
-        uint32_t r[TF_ITEMS];
-        tf_sort<false>(sk, mp, r);  // by (x_rem, y)
+        uint32_t r[IT];
+        tf_sort<false, IT>(sk, mp, r);  // by (x_rem, y)
         // tied runs in x (key >> 12) and in (x, y) (key); cross term; histogram update
         const int t = threadIdx.x;
-        const bool act = t < (mp >> 4);
+        const bool act = t < mp / IT;
         int hx = -1, hk = -1;  // last run head (position) inside this thread
         uint32_t prevk = 0;
-        if (act && t > 0) prevk = sk[tf_pidx(t * TF_ITEMS - 1)];
+        if (act && t > 0) prevk = sk[tf_pidx<IT>(t * IT - 1)];
 #pragma unroll
-        for (int k = 0; k < TF_ITEMS; ++k) {
-            const int pos = t * TF_ITEMS + k;
+        for (int k = 0; k < IT; ++k) {
+            const int pos = t * IT + k;
             const uint32_t key = r[k];
             const uint32_t pk = k ? r[k - 1] : prevk;
             if (act && (pos == 0 || (key >> 12) != (pk >> 12))) hx = pos;
@@ -945,8 +948,8 @@ __global__ void __launch_bounds__(TF_LEAF_T, 2) tf_leaf(const TfParams* __restri
         hk = tf_excl_max(act ? hk : -1, swi);
         if (act) {
 #pragma unroll
-            for (int k = 0; k < TF_ITEMS; ++k) {
-                const int pos = t * TF_ITEMS + k;
+            for (int k = 0; k < IT; ++k) {
+                const int pos = t * IT + k;
                 const uint32_t key = r[k];
                 const uint32_t pk = k ? r[k - 1] : prevk;
                 if (pos == 0 || (key >> 12) != (pk >> 12)) hx = pos;
@@ -964,13 +967,13 @@ __global__ void __launch_bounds__(TF_LEAF_T, 2) tf_leaf(const TfParams* __restri
         // in-group D = strict inversions of the y sequence in (x, y) order
         if (act) {
 #pragma unroll
-            for (int k = 0; k < TF_ITEMS; ++k) {
-                const int pos = t * TF_ITEMS + k;
-                sk[tf_pidx(pos)] = pos < (int)m ? (r[k] & 4095u) : 0xffffffffu;
+            for (int k = 0; k < IT; ++k) {
+                const int pos = t * IT + k;
+                sk[tf_pidx<IT>(pos)] = pos < (int)m ? (r[k] & 4095u) : 0xffffffffu;
             }
         }
         __syncthreads();
-        D += tf_sort<true>(sk, mp, r);
+        D += tf_sort<true, IT>(sk, mp, r);
     }
     acc_add(D, acc + 0);
     acc_add(n1, acc + 1);
@@ -1127,8 +1130,14 @@ int tau_fast_counts(const void* x, int xd, const void* y, int yd, uint32_t n, in
     tf_groups<<<z.max_split, TF_SCAN_T, TF_CHILD_SMEM, st>>>(w.p, w.off1, w.srank, z.cap, w.ctot, w.ng, w.gbase,
                                                              w.groups, w.gstart);
     RS_LAUNCH_CHECK();
-    RS_CUDA(ensure_smem((const void*)tf_leaf, (int)TF_LEAF_SMEM));
-    tf_leaf<<<z.leaf_ctas, TF_LEAF_T, TF_LEAF_SMEM, st>>>(w.p, n, w.groups, w.gstart, A, B, w.hc, w.acc);
+    RS_CUDA(ensure_smem((const void*)tf_leaf<8>, (int)TF_LEAF_SMEM));
+    RS_CUDA(ensure_smem((const void*)tf_leaf<16>, (int)TF_LEAF_SMEM));
+    // groups of <= 4096 keys (the smaller queues): 8 keys per thread, so twice the threads
+    // share each merge (half the serial merge steps per level, one level more)
+    if (z.cap <= TF_CAP / 2)
+        tf_leaf<8><<<z.leaf_ctas, TF_LEAF_T, TF_LEAF_SMEM, st>>>(w.p, n, w.groups, w.gstart, A, B, w.hc, w.acc);
+    else
+        tf_leaf<16><<<z.leaf_ctas, TF_LEAF_T, TF_LEAF_SMEM, st>>>(w.p, n, w.groups, w.gstart, A, B, w.hc, w.acc);
     RS_LAUNCH_CHECK();
     tf_colscan<<<TF_BINS / 32, 256, 0, st>>>(w.hc, z.leaf_ctas, w.p, w.prec, nullptr, w.acc + 2);
     RS_LAUNCH_CHECK();
