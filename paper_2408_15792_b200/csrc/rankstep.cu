@@ -987,67 +987,6 @@ __global__ void __launch_bounds__(1024) sel_sort_emit_small(const unsigned __int
     sel_emit_small_block(ck, ci, st->n_cand, id, k, run, sched, counts, sk, sv);
 }
 
-// ---- queues of 2^14 .. 2^18 rows: the whole select in one cooperative launch ----------
-// The levels' histogram passes, the bucket picks, the gather and the one-block sort of the
-// candidates, separated by grid barriers (all CTAs co-resident: cooperative launch), so a
-// step costs one launch instead of LEVELS + 2 (most of them no-ops past the decision).
-__device__ __forceinline__ void grid_barrier(uint32_t* count, volatile uint32_t* gen) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const uint32_t g = *gen;
-        __threadfence();
-        if (atomicAdd(count, 1u) == gridDim.x - 1) {
-            *count = 0;
-            __threadfence();
-            atomicAdd(const_cast<uint32_t*>(gen), 1u);
-        } else {
-            while (*gen == g) {}
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
-
-template <typename Src>
-__global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, SelState* __restrict__ st,
-                                                         unsigned __int128* __restrict__ pfx128,
-                                                         uint32_t* __restrict__ hist, uint32_t k, uint32_t cap,
-                                                         unsigned __int128* __restrict__ ck, uint32_t* __restrict__ ci,
-                                                         uint32_t* __restrict__ bar, const int64_t* __restrict__ id,
-                                                         int64_t* __restrict__ run, uint8_t* __restrict__ sched,
-                                                         int32_t* __restrict__ counts) {
-    using V = typename Src::V;
-    __shared__ uint32_t h[SEL_BINS + 1];
-    __shared__ uint4 sk[1024];
-    __shared__ uint32_t sv[1024];
-    for (uint32_t level = 0; level < (uint32_t)Src::LEVELS; ++level) {
-        if (*(volatile uint32_t*)&st->done) break;  // written before the last barrier
-        for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) h[b] = 0;
-        __syncthreads();
-        const int shift = Src::BITS - SEL_BITS * (int)level;
-        const V wsh = level ? (V)(*(volatile unsigned __int128*)pfx128 >> shift) : (V)0;
-        sel_rows(src, n, [&](uint32_t, V v, bool ok) {
-            hist_add_warp(h, sel_digit<Src>(v, level), ok && (level == 0 || vshr<Src>(v, shift) == wsh));
-        });
-        __syncthreads();
-        for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS)
-            if (h[b]) atomicAdd(&hist[b], h[b]);
-        grid_barrier(bar, bar + 1);
-        if (blockIdx.x == 0) sel_pick_block<Src>(st, pfx128, hist, k, h, 0u, cap);
-        grid_barrier(bar, bar + 1);
-    }
-    {  // gather every key at or below the chosen bucket
-        const int shift = Src::BITS - SEL_BITS * (int)*(volatile uint32_t*)&st->final_level;
-        const V lim = (V)(*(volatile unsigned __int128*)pfx128 >> shift);
-        sel_rows(src, n, [&](uint32_t i, V v, bool ok) {
-            sel_append(ok && vshr<Src>(v, shift) <= lim, to128<Src>(v), i, &st->n_cand, ck, ci, SEL_SORT);
-        });
-    }
-    grid_barrier(bar, bar + 1);
-    if (blockIdx.x == 0)
-        sel_emit_small_block(ck, ci, *(volatile uint32_t*)&st->n_cand, id, k, run, sched, counts, sk, sv);
-}
-
 constexpr int UPD_THREADS = 1024;
 constexpr int UPD_ITEMS = 4;  // rows per thread: element k * UPD_THREADS + tid of the block's chunk
 constexpr int UPD_CHUNK = UPD_THREADS * UPD_ITEMS;
@@ -1110,15 +1049,16 @@ __global__ void __launch_bounds__(UPD_THREADS) starvation_update(rs_queue_soa q,
 
 // Exclusive scan of the interleaved (promoted, demoted) block counts by one block
 // (per-thread chunk sums, then warp-shuffle scans); writes the totals to counts[1, 2].
-__global__ void __launch_bounds__(1024) scan_pairs(uint32_t* __restrict__ bcnt, uint32_t nblk,
-                                                   int32_t* __restrict__ counts) {
+// (one 1024-thread block; src == dst allowed: each thread reads its entries before writing them)
+__device__ __forceinline__ void scan_pairs_block(const uint32_t* src, uint32_t* dst, uint32_t nblk,
+                                                 int32_t* __restrict__ counts) {
     __shared__ uint32_t wp[32], wd[32];
     const uint32_t per = (nblk + 1023) / 1024;
     const uint32_t b0 = threadIdx.x * per, b1 = min(nblk, b0 + per);
     uint32_t sp = 0, sd = 0;
     for (uint32_t b = b0; b < b1; ++b) {
-        sp += bcnt[2 * b];
-        sd += bcnt[2 * b + 1];
+        sp += src[2 * b];
+        sd += src[2 * b + 1];
     }
     const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t ip = sp, id2 = sd;
@@ -1155,12 +1095,16 @@ __global__ void __launch_bounds__(1024) scan_pairs(uint32_t* __restrict__ bcnt, 
     __syncthreads();
     uint32_t ap = (w ? wp[w - 1] : 0u) + ip - sp, ad = (w ? wd[w - 1] : 0u) + id2 - sd;
     for (uint32_t b = b0; b < b1; ++b) {
-        const uint32_t vp = bcnt[2 * b], vd = bcnt[2 * b + 1];
-        bcnt[2 * b] = ap;
-        bcnt[2 * b + 1] = ad;
+        const uint32_t vp = src[2 * b], vd = src[2 * b + 1];
+        dst[2 * b] = ap;
+        dst[2 * b + 1] = ad;
         ap += vp;
         ad += vd;
     }
+}
+__global__ void __launch_bounds__(1024) scan_pairs(uint32_t* __restrict__ bcnt, uint32_t nblk,
+                                                   int32_t* __restrict__ counts) {
+    scan_pairs_block(bcnt, bcnt, nblk, counts);
 }
 
 // Order-preserving compaction of the promoted / demoted ids: within a block, rows in
@@ -1257,10 +1201,11 @@ __device__ __forceinline__ uint8_t upd_row(uint8_t& f, int32_t& st, int32_t& qu,
 // Also compacts, order-preserving within the block, the promoted / demoted row indices
 // into plist / dlist at the block's slice (the rows are few: the copy kernel then reads
 // only them instead of a per-row code array).
-__global__ void __launch_bounds__(UPV_T) starvation_update_v(rs_queue_soa q, const uint8_t* __restrict__ sched,
-                                                             int32_t threshold, int32_t pquantum,
-                                                             uint32_t* __restrict__ plist, uint32_t* __restrict__ dlist,
-                                                             uint32_t* __restrict__ bcnt) {
+// (one 1024-thread block per 16K-row chunk; also run inside sel_fused)
+__device__ __forceinline__ void upd_chunk_v(const rs_queue_soa& q, const uint8_t* __restrict__ sched,
+                                            int32_t threshold, int32_t pquantum, uint32_t* __restrict__ plist,
+                                            uint32_t* __restrict__ dlist, uint32_t* __restrict__ bcnt,
+                                            const uint32_t chunk) {
     constexpr int NW = UPV_T / 32;
     __shared__ uint32_t cp[UPV_IT * NW], cd[UPV_IT * NW];
     const uint32_t n = (uint32_t)q.n;
@@ -1268,7 +1213,7 @@ __global__ void __launch_bounds__(UPV_T) starvation_update_v(rs_queue_soa q, con
     uint32_t codes[UPV_IT], ep[UPV_IT], ed[UPV_IT];
 #pragma unroll
     for (int it = 0; it < UPV_IT; ++it) {
-        const uint32_t i = blockIdx.x * UPV_CHUNK + it * (UPV_T * 4) + threadIdx.x * 4;
+        const uint32_t i = chunk * UPV_CHUNK + it * (UPV_T * 4) + threadIdx.x * 4;
         if (i + 3 < n) {
             uint32_t fw = *reinterpret_cast<const uint32_t*>(q.flags + i);
             const uint32_t sw = *reinterpret_cast<const uint32_t*>(sched + i);
@@ -1351,12 +1296,12 @@ __global__ void __launch_bounds__(UPV_T) starvation_update_v(rs_queue_soa q, con
             ad += vd[j];
         }
         if (lane == 31) {
-            bcnt[2 * blockIdx.x] = ip;
-            bcnt[2 * blockIdx.x + 1] = id2;
+            bcnt[2 * chunk] = ip;
+            bcnt[2 * chunk + 1] = id2;
         }
     }
     __syncthreads();
-    const uint32_t base = blockIdx.x * UPV_CHUNK;
+    const uint32_t base = chunk * UPV_CHUNK;
 #pragma unroll
     for (int it = 0; it < UPV_IT; ++it) {
         if (!codes[it]) continue;
@@ -1370,17 +1315,105 @@ __global__ void __launch_bounds__(UPV_T) starvation_update_v(rs_queue_soa q, con
         }
     }
 }
+__global__ void __launch_bounds__(UPV_T) starvation_update_v(rs_queue_soa q, const uint8_t* __restrict__ sched,
+                                                             int32_t threshold, int32_t pquantum,
+                                                             uint32_t* __restrict__ plist, uint32_t* __restrict__ dlist,
+                                                             uint32_t* __restrict__ bcnt) {
+    upd_chunk_v(q, sched, threshold, pquantum, plist, dlist, bcnt, blockIdx.x);
+}
 
 // promoted / demoted ids from the per-block lists, at the scanned block offsets
+__device__ __forceinline__ void copy_pd_chunk(const uint32_t* __restrict__ plist, const uint32_t* __restrict__ dlist,
+                                              const uint32_t* __restrict__ bcnt_raw, const uint32_t* __restrict__ boff,
+                                              const int64_t* __restrict__ id, int64_t* __restrict__ prom,
+                                              int64_t* __restrict__ dem, const uint32_t b) {
+    const uint32_t base = b * UPV_CHUNK;
+    const uint32_t np = bcnt_raw[2 * b], nd = bcnt_raw[2 * b + 1];
+    for (uint32_t k = threadIdx.x; k < np; k += blockDim.x) prom[boff[2 * b] + k] = id[plist[base + k]];
+    for (uint32_t k = threadIdx.x; k < nd; k += blockDim.x) dem[boff[2 * b + 1] + k] = id[dlist[base + k]];
+}
 __global__ void __launch_bounds__(256) copy_pd_lists(const uint32_t* __restrict__ plist,
                                                      const uint32_t* __restrict__ dlist,
                                                      const uint32_t* __restrict__ bcnt_raw,
                                                      const uint32_t* __restrict__ boff, const int64_t* __restrict__ id,
                                                      int64_t* __restrict__ prom, int64_t* __restrict__ dem) {
-    const uint32_t b = blockIdx.x, base = b * UPV_CHUNK;
-    const uint32_t np = bcnt_raw[2 * b], nd = bcnt_raw[2 * b + 1];
-    for (uint32_t k = threadIdx.x; k < np; k += 256) prom[boff[2 * b] + k] = id[plist[base + k]];
-    for (uint32_t k = threadIdx.x; k < nd; k += 256) dem[boff[2 * b + 1] + k] = id[dlist[base + k]];
+    copy_pd_chunk(plist, dlist, bcnt_raw, boff, id, prom, dem, blockIdx.x);
+}
+
+// ---- queues of 2^14 .. 2^18 rows: the whole select in one cooperative launch ----------
+// The levels' histogram passes, the bucket picks, the gather and the one-block sort of the
+// candidates, separated by grid barriers (all CTAs co-resident: cooperative launch), so a
+// step costs one launch instead of LEVELS + 2 (most of them no-ops past the decision).
+__device__ __forceinline__ void grid_barrier(uint32_t* count, volatile uint32_t* gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t g = *gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == gridDim.x - 1) {
+            *count = 0;
+            __threadfence();
+            atomicAdd(const_cast<uint32_t*>(gen), 1u);
+        } else {
+            while (*gen == g) {}
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <typename Src>
+__global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, SelState* __restrict__ st,
+                                                         unsigned __int128* __restrict__ pfx128,
+                                                         uint32_t* __restrict__ hist, uint32_t k, uint32_t cap,
+                                                         unsigned __int128* __restrict__ ck, uint32_t* __restrict__ ci,
+                                                         uint32_t* __restrict__ bar, const int64_t* __restrict__ id,
+                                                         int64_t* __restrict__ run, uint8_t* __restrict__ sched,
+                                                         int32_t* __restrict__ counts, rs_queue_soa q, int32_t threshold,
+                                                         int32_t pquantum, uint32_t* __restrict__ plist,
+                                                         uint32_t* __restrict__ dlist, uint32_t* __restrict__ raw,
+                                                         uint32_t* __restrict__ boff, int64_t* __restrict__ prom,
+                                                         int64_t* __restrict__ dem) {
+    using V = typename Src::V;
+    __shared__ uint32_t h[SEL_BINS + 1];
+    __shared__ uint4 sk[1024];
+    __shared__ uint32_t sv[1024];
+    for (uint32_t level = 0; level < (uint32_t)Src::LEVELS; ++level) {
+        if (*(volatile uint32_t*)&st->done) break;  // written before the last barrier
+        for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) h[b] = 0;
+        __syncthreads();
+        const int shift = Src::BITS - SEL_BITS * (int)level;
+        const V wsh = level ? (V)(*(volatile unsigned __int128*)pfx128 >> shift) : (V)0;
+        sel_rows(src, n, [&](uint32_t, V v, bool ok) {
+            hist_add_warp(h, sel_digit<Src>(v, level), ok && (level == 0 || vshr<Src>(v, shift) == wsh));
+        });
+        __syncthreads();
+        for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS)
+            if (h[b]) atomicAdd(&hist[b], h[b]);
+        grid_barrier(bar, bar + 1);
+        if (blockIdx.x == 0) sel_pick_block<Src>(st, pfx128, hist, k, h, 0u, cap);
+        grid_barrier(bar, bar + 1);
+    }
+    {  // gather every key at or below the chosen bucket
+        const int shift = Src::BITS - SEL_BITS * (int)*(volatile uint32_t*)&st->final_level;
+        const V lim = (V)(*(volatile unsigned __int128*)pfx128 >> shift);
+        sel_rows(src, n, [&](uint32_t i, V v, bool ok) {
+            sel_append(ok && vshr<Src>(v, shift) <= lim, to128<Src>(v), i, &st->n_cand, ck, ci, SEL_SORT);
+        });
+    }
+    grid_barrier(bar, bar + 1);
+    if (blockIdx.x == 0)
+        sel_emit_small_block(ck, ci, *(volatile uint32_t*)&st->n_cand, id, k, run, sched, counts, sk, sv);
+    if (plist == nullptr) return;  // the state update runs as separate kernels (unaligned columns)
+    // the state update (schedulers.py:224-240) and the ordered promoted / demoted lists:
+    // starvation_update_v's chunks, scan_pairs and copy_pd_lists, between grid barriers
+    grid_barrier(bar, bar + 1);  // the batch's sched flags are set
+    const uint32_t nblk = (n + UPV_CHUNK - 1) / UPV_CHUNK;
+    for (uint32_t c = blockIdx.x; c < nblk; c += gridDim.x)
+        upd_chunk_v(q, sched, threshold, pquantum, plist, dlist, raw, c);
+    grid_barrier(bar, bar + 1);
+    if (blockIdx.x == 0) scan_pairs_block(raw, boff, nblk, counts);
+    grid_barrier(bar, bar + 1);
+    for (uint32_t c = blockIdx.x; c < nblk; c += gridDim.x) copy_pd_chunk(plist, dlist, raw, boff, id, prom, dem, c);
 }
 
 __global__ void build_arrival_keys(const double* __restrict__ arr, const int64_t* __restrict__ id, uint32_t n,
@@ -1530,6 +1563,9 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
     const int T = 256;
     const uint32_t k = min(n, (uint32_t)max_batch);
     const bool soa64 = q->score_dtype == RS_F32 && !calibrated;
+    const bool vec = (reinterpret_cast<uintptr_t>(q->flags) & 3u) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(q->starvation) | reinterpret_cast<uintptr_t>(q->quantum)) & 15u) == 0;
+    bool fused_update = false;
     if (kv_budget < 0 && n > sel_min_n() && k + SEL_CAP <= (uint32_t)SEL_SORT) {
         // top-k select (see sel_hist): <= LEVELS histogram passes, most no-ops
         const size_t smem = SEL_SORT * (sizeof(unsigned __int128) + sizeof(uint32_t));
@@ -1539,6 +1575,11 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         RS_CUDA(cudaMemsetAsync(w.hist, 0, SEL_BINS * sizeof(uint32_t), st));
         const uint32_t gb = min((n / 4 + SEL_THREADS) / SEL_THREADS, (uint32_t)num_sms() * 2);
         const bool fused = n <= SEL_FUSED_N && k + SEL_CAP_SMALL <= 1024;
+        fused_update = fused && vec;
+        const uint32_t unblk = (n + UPV_CHUNK - 1) / UPV_CHUNK;
+        uint32_t* f_plist = fused_update ? reinterpret_cast<uint32_t*>(w.va) : nullptr;
+        uint32_t* f_dlist = reinterpret_cast<uint32_t*>(w.vb);
+        uint32_t* f_raw = w.bcnt + 2 * unblk;
         if (fused) {
             // one cooperative launch: levels, picks, gather and the candidates' sort
             cudaLaunchConfig_t lc{};
@@ -1555,13 +1596,15 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
             if (soa64) {
                 const SrcSoa64 src{static_cast<const float*>(q->score), q->flags, q->arrival_rank, preemptive, counts + 3};
                 RS_CUDA(cudaLaunchKernelEx(&lc, sel_fused<SrcSoa64>, src, n, w.sel, w.pfx, w.hist, k,
-                                           (uint32_t)SEL_CAP_SMALL, w.ck, w.ci, bar, q->id, run, w.sched, counts));
+                                           (uint32_t)SEL_CAP_SMALL, w.ck, w.ci, bar, q->id, run, w.sched, counts, *q,
+                                           threshold, pquantum, f_plist, f_dlist, f_raw, w.bcnt, prom, dem));
             } else {
                 build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
                 RS_LAUNCH_CHECK();
                 const SrcKeys src{w.kb};
                 RS_CUDA(cudaLaunchKernelEx(&lc, sel_fused<SrcKeys>, src, n, w.sel, w.pfx, w.hist, k,
-                                           (uint32_t)SEL_CAP_SMALL, w.ck, w.ci, bar, q->id, run, w.sched, counts));
+                                           (uint32_t)SEL_CAP_SMALL, w.ck, w.ci, bar, q->id, run, w.sched, counts, *q,
+                                           threshold, pquantum, f_plist, f_dlist, f_raw, w.bcnt, prom, dem));
             }
         } else if (soa64) {
             // keys straight from the queue columns: no key pass, 9 B per row per level
@@ -1597,8 +1640,7 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         }
     }
     RS_LAUNCH_CHECK();
-    const bool vec = (reinterpret_cast<uintptr_t>(q->flags) & 3u) == 0 &&
-                     ((reinterpret_cast<uintptr_t>(q->starvation) | reinterpret_cast<uintptr_t>(q->quantum)) & 15u) == 0;
+    if (fused_update) return RS_OK;  // done inside sel_fused
     if (vec) {
         const uint32_t nblk = (n + UPV_CHUNK - 1) / UPV_CHUNK;
         uint32_t* plist = reinterpret_cast<uint32_t*>(w.va);  // the sort buffers are idle here
