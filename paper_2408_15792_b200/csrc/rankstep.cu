@@ -148,7 +148,7 @@ constexpr int SEL_SORT = 4096;  // >= max_batch + SEL_CAP, power of two
 // Below this many rows the full merge sort (a block-sort launch + log2(n / 2048) pass
 // launches) beats the select's SEL_LEVELS histogram launches + gather + final sort: the
 // engine loop's queues (10^3-10^5 rows) are all below it, cfg4's 1M queue is above.
-constexpr uint32_t SEL_MIN_N_DEFAULT = 1u << 14;
+constexpr uint32_t SEL_MIN_N_DEFAULT = 1u << 11;
 // RS_SEL_MIN_N overrides the crossover (measurement experiments)
 static uint32_t sel_min_n() {
     static const uint32_t v = [] {
@@ -1340,7 +1340,7 @@ __global__ void __launch_bounds__(256) copy_pd_lists(const uint32_t* __restrict_
     copy_pd_chunk(plist, dlist, bcnt_raw, boff, id, prom, dem, blockIdx.x);
 }
 
-// ---- queues of 2^14 .. 2^18 rows: the whole select in one cooperative launch ----------
+// ---- queues of 2^11 .. 2^18 rows: the whole select in one cooperative launch ----------
 // The levels' histogram passes, the bucket picks, the gather and the one-block sort of the
 // candidates, separated by grid barriers (all CTAs co-resident: cooperative launch), so a
 // step costs one launch instead of LEVELS + 2 (most of them no-ops past the decision).
