@@ -19,6 +19,7 @@
 // dgrad GEMMs read the weights MN-major, wgrad GEMMs read both activations MN-major
 // (split-K partial slices reduced in a fixed order), so the pass is deterministic.
 #include <cuda_bf16.h>
+#include <algorithm>
 #include "common.cuh"
 #include "gemm.cuh"
 #include "train.cuh"
@@ -60,13 +61,29 @@ struct TrainWs {
     size_t abw_bytes;
 };
 
+// K splits of a wgrad GEMM: work items (tile, split) run one per CTA pair, so pick the
+// split count whose items fill whole waves of CTA pairs best (at least ~one wave; ties to
+// fewer splits: fewer fp32 partial slices to write and reduce). The earlier rule (items ~
+// SMs) left 2.07-2.4 waves, i.e. a 30% idle tail, on every shape here.
 static int wgrad_splits(int M, int N, int K) {
     const int tiles = (M / 256) * (N / 256);
-    int s = (148 + tiles - 1) / tiles;
+    const int ncl = num_sms() / 2;
     const int kb = K / 64;
-    if (s > kb / 8) s = kb / 8;
-    if (s > 64) s = 64;
-    return s < 1 ? 1 : s;
+    const int smax = std::max(1, std::min(64, kb / 8));
+    int best = 1;
+    double best_eff = -1.0;
+    for (int s = 1; s <= smax; ++s) {
+        const int items = tiles * s;
+        if (items * 10 < ncl * 9 && s < smax) continue;  // less than ~one wave: too few items
+        const int waves = (items + ncl - 1) / ncl;
+        const double eff = (double)items / (double)(waves * ncl);
+        if (eff >= 0.95) return s;  // the fewest splits that keep >= 95% of the pairs busy
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = s;
+        }
+    }
+    return best;
 }
 
 template <typename A>
