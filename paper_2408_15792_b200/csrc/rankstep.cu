@@ -144,6 +144,7 @@ constexpr int SEL_CAP = 2048;
 constexpr int SEL_CAP_SMALL = 512;
 constexpr uint32_t SEL_SMALL_N = 1u << 20;
 constexpr uint32_t SEL_FUSED_N = 1u << 18;  // up to here the select is one cooperative launch (<= 64 CTAs)
+constexpr uint32_t SEL_CLUSTER_N = 1u << 16;  // up to here that launch is one <= 8-CTA cluster
 constexpr int SEL_SORT = 4096;  // >= max_batch + SEL_CAP, power of two
 // Below this many rows the full merge sort (a block-sort launch + log2(n / 2048) pass
 // launches) beats the select's SEL_LEVELS histogram launches + gather + final sort: the
@@ -1361,7 +1362,9 @@ __device__ __forceinline__ void grid_barrier(uint32_t* count, volatile uint32_t*
     __syncthreads();
 }
 
-template <typename Src>
+// CL: the grid is one thread-block cluster (<= 8 CTAs), so the barriers are the hardware
+// cluster barrier (release / acquire at cluster scope) instead of the global-memory one.
+template <typename Src, bool CL>
 __global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, SelState* __restrict__ st,
                                                          unsigned __int128* __restrict__ pfx128,
                                                          uint32_t* __restrict__ hist, uint32_t k, uint32_t cap,
@@ -1377,6 +1380,14 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, Se
     __shared__ uint32_t h[SEL_BINS + 1];
     __shared__ uint4 sk[1024];
     __shared__ uint32_t sv[1024];
+    auto gsync = [&]() {
+        if constexpr (CL) {
+            __syncthreads();
+            asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        } else {
+            grid_barrier(bar, bar + 1);
+        }
+    };
     for (uint32_t level = 0; level < (uint32_t)Src::LEVELS; ++level) {
         if (*(volatile uint32_t*)&st->done) break;  // written before the last barrier
         for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) h[b] = 0;
@@ -1389,9 +1400,9 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, Se
         __syncthreads();
         for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS)
             if (h[b]) atomicAdd(&hist[b], h[b]);
-        grid_barrier(bar, bar + 1);
+        gsync();
         if (blockIdx.x == 0) sel_pick_block<Src>(st, pfx128, hist, k, h, 0u, cap);
-        grid_barrier(bar, bar + 1);
+        gsync();
     }
     {  // gather every key at or below the chosen bucket
         const int shift = Src::BITS - SEL_BITS * (int)*(volatile uint32_t*)&st->final_level;
@@ -1400,19 +1411,19 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, Se
             sel_append(ok && vshr<Src>(v, shift) <= lim, to128<Src>(v), i, &st->n_cand, ck, ci, SEL_SORT);
         });
     }
-    grid_barrier(bar, bar + 1);
+    gsync();
     if (blockIdx.x == 0)
         sel_emit_small_block(ck, ci, *(volatile uint32_t*)&st->n_cand, id, k, run, sched, counts, sk, sv);
     if (plist == nullptr) return;  // the state update runs as separate kernels (unaligned columns)
     // the state update (schedulers.py:224-240) and the ordered promoted / demoted lists:
     // starvation_update_v's chunks, scan_pairs and copy_pd_lists, between grid barriers
-    grid_barrier(bar, bar + 1);  // the batch's sched flags are set
+    gsync();  // the batch's sched flags are set
     const uint32_t nblk = (n + UPV_CHUNK - 1) / UPV_CHUNK;
     for (uint32_t c = blockIdx.x; c < nblk; c += gridDim.x)
         upd_chunk_v(q, sched, threshold, pquantum, plist, dlist, raw, c);
-    grid_barrier(bar, bar + 1);
+    gsync();
     if (blockIdx.x == 0) scan_pairs_block(raw, boff, nblk, counts);
-    grid_barrier(bar, bar + 1);
+    gsync();
     for (uint32_t c = blockIdx.x; c < nblk; c += gridDim.x) copy_pd_chunk(plist, dlist, raw, boff, id, prom, dem, c);
 }
 
@@ -1581,31 +1592,43 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         uint32_t* f_dlist = reinterpret_cast<uint32_t*>(w.vb);
         uint32_t* f_raw = w.bcnt + 2 * unblk;
         if (fused) {
-            // one cooperative launch: levels, picks, gather and the candidates' sort
+            // one launch: levels, picks, gather, the candidates' sort and the state update;
+            // up to SEL_CLUSTER_N rows the grid is one cluster of <= 8 CTAs (hardware
+            // barriers), above it a cooperative grid with global-memory barriers
+            const bool cl = n <= SEL_CLUSTER_N;
+            const uint32_t grid = cl ? min(gb, 8u) : gb;
             cudaLaunchConfig_t lc{};
             cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeCooperative;
-            at[0].val.cooperative = 1;
-            lc.gridDim = dim3(gb);
+            if (cl) {
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = grid;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+            } else {
+                at[0].id = cudaLaunchAttributeCooperative;
+                at[0].val.cooperative = 1;
+            }
+            lc.gridDim = dim3(grid);
             lc.blockDim = dim3(SEL_THREADS);
             lc.dynamicSmemBytes = 0;
             lc.stream = st;
             lc.attrs = at;
             lc.numAttrs = 1;
             uint32_t* bar = &w.sel->bar_count;
+#define RS_SEL_FUSED(SRC, CL)                                                                                   \
+    RS_CUDA(cudaLaunchKernelEx(&lc, sel_fused<SRC, CL>, src, n, w.sel, w.pfx, w.hist, k, (uint32_t)SEL_CAP_SMALL, \
+                               w.ck, w.ci, bar, q->id, run, w.sched, counts, *q, threshold, pquantum, f_plist,  \
+                               f_dlist, f_raw, w.bcnt, prom, dem))
             if (soa64) {
                 const SrcSoa64 src{static_cast<const float*>(q->score), q->flags, q->arrival_rank, preemptive, counts + 3};
-                RS_CUDA(cudaLaunchKernelEx(&lc, sel_fused<SrcSoa64>, src, n, w.sel, w.pfx, w.hist, k,
-                                           (uint32_t)SEL_CAP_SMALL, w.ck, w.ci, bar, q->id, run, w.sched, counts, *q,
-                                           threshold, pquantum, f_plist, f_dlist, f_raw, w.bcnt, prom, dem));
+                if (cl) RS_SEL_FUSED(SrcSoa64, true); else RS_SEL_FUSED(SrcSoa64, false);
             } else {
                 build_rank_keys<<<(n + T - 1) / T, T, 0, st>>>(*q, calibrated, preemptive, w.kb, counts + 3);
                 RS_LAUNCH_CHECK();
                 const SrcKeys src{w.kb};
-                RS_CUDA(cudaLaunchKernelEx(&lc, sel_fused<SrcKeys>, src, n, w.sel, w.pfx, w.hist, k,
-                                           (uint32_t)SEL_CAP_SMALL, w.ck, w.ci, bar, q->id, run, w.sched, counts, *q,
-                                           threshold, pquantum, f_plist, f_dlist, f_raw, w.bcnt, prom, dem));
+                if (cl) RS_SEL_FUSED(SrcKeys, true); else RS_SEL_FUSED(SrcKeys, false);
             }
+#undef RS_SEL_FUSED
         } else if (soa64) {
             // keys straight from the queue columns: no key pass, 9 B per row per level
             const SrcSoa64 src{static_cast<const float*>(q->score), q->flags, q->arrival_rank, preemptive, counts + 3};
