@@ -297,8 +297,19 @@ __global__ void __launch_bounds__(256) tf_colscan(const uint32_t* __restrict__ h
     const uint32_t bin = blockIdx.x * 32 + lane;
     const uint32_t rpw = (rows + 7) / 8;
     const uint32_t r0 = min(rows, wid * rpw), r1 = min(rows, r0 + rpw);
+    // the warp's rows (<= RMAX at every n: rows ~ one per SM) are loaded once, all at once
+    constexpr int RMAX = 24;
+    const bool inreg = r1 - r0 <= (uint32_t)RMAX;
+    uint32_t vals[RMAX];
     uint32_t s = 0;
-    for (uint32_t r = r0; r < r1; ++r) s += hist[(size_t)r * TF_BINS + bin];
+    if (inreg) {
+#pragma unroll
+        for (int k = 0; k < RMAX; ++k) vals[k] = r0 + k < r1 ? hist[(size_t)(r0 + k) * TF_BINS + bin] : 0u;
+#pragma unroll
+        for (int k = 0; k < RMAX; ++k) s += vals[k];
+    } else {
+        for (uint32_t r = r0; r < r1; ++r) s += hist[(size_t)r * TF_BINS + bin];
+    }
     wt[wid][lane] = s;
     __syncthreads();
     uint32_t run = 0, all = 0;
@@ -306,10 +317,19 @@ __global__ void __launch_bounds__(256) tf_colscan(const uint32_t* __restrict__ h
         if (k < wid) run += wt[k][lane];
         all += wt[k][lane];
     }
-    for (uint32_t r = r0; r < r1; ++r) {
-        const uint32_t v = hist[(size_t)r * TF_BINS + bin];
-        pre[(size_t)r * TF_BINS + bin] = run;
-        run += v;
+    if (inreg) {
+#pragma unroll
+        for (int k = 0; k < RMAX; ++k)
+            if (r0 + k < r1) {
+                pre[(size_t)(r0 + k) * TF_BINS + bin] = run;
+                run += vals[k];
+            }
+    } else {
+        for (uint32_t r = r0; r < r1; ++r) {
+            const uint32_t v = hist[(size_t)r * TF_BINS + bin];
+            pre[(size_t)r * TF_BINS + bin] = run;
+            run += v;
+        }
     }
     if (tot && wid == 0) tot[bin] = all;
     if (n2) {
