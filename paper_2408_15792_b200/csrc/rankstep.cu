@@ -427,6 +427,44 @@ __device__ __forceinline__ const SrcSoa64& soa64_of(const Src& s) {
     if constexpr (std::is_same<Src, SrcSoa64>::value) return s;
     else { __trap(); return *reinterpret_cast<const SrcSoa64*>(&s); }
 }
+// Level 0 of the select on the score and flag columns only (aligned SrcSoa64): every row
+// counted into the shared histogram h (+ a scratch bin at SEL_BINS), next chunk prefetched.
+__device__ __forceinline__ void sel_l0_soa(const SrcSoa64& so, uint32_t n, uint32_t* h) {
+    const uint32_t stride = gridDim.x * SEL_THREADS * 4u, lane = threadIdx.x & 31u;
+    const uint32_t n4 = n & ~3u;
+    const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(h);
+    uint32_t i = (blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u)) * 4u + lane * 4u;
+    float4 sc = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t fl = 0;
+    if (i < n4) {
+        sc = __ldcs(reinterpret_cast<const float4*>(so.score + i));
+        fl = __ldcs(reinterpret_cast<const uint32_t*>(so.flags + i));
+    }
+    bool nan = false;
+    for (; i - lane * 4u < n4; i += stride) {  // warp-uniform trip count
+        const bool ok = i < n4;
+        const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
+        const uint32_t fw = fl;
+        if (i + stride < n4) {
+            sc = __ldcs(reinterpret_cast<const float4*>(so.score + i + stride));
+            fl = __ldcs(reinterpret_cast<const uint32_t*>(so.flags + i + stride));
+        }
+        const uint32_t C = soa64_classes(fw, so.preemptive);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t img = soa64_img(scv[q], (fw >> (8 * q)) & RS_FLAG_SCORED, nan);
+            const uint32_t d = __byte_perm(img, C, 0x4443u + 0x0010u * q) & (SEL_BINS - 1);
+            hist_add_all(hbase, ok ? d : (uint32_t)SEL_BINS);
+        }
+    }
+    if (nan) atomicOr(so.err, 1);
+    for (uint32_t t = n4 + blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u) + lane; t - lane < n;
+         t += gridDim.x * SEL_THREADS) {
+        const bool ok = t < n;  // tail rows (< 4), warp-uniform trip count
+        hist_add_warp(h, ok ? sel_digit<SrcSoa64>(so.value(t), 0) : 0u, ok);
+    }
+}
+
 // LEVEL: the level this launch histograms (the host launches LEVEL = 0, 1, ... in order;
 // st->level == LEVEL unless the select is already done), so every shift is a constant.
 template <typename Src, int LEVEL>
@@ -735,40 +773,7 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, Sel
         }
     } else if (LEVEL == 0 && soa64_aligned(src)) {
         // smaller queues: the same digit from scores + flags, every row counted, no keep
-        const SrcSoa64& so = soa64_of(src);
-        const uint32_t stride = gridDim.x * SEL_THREADS * 4u, lane = threadIdx.x & 31u;
-        const uint32_t n4 = n & ~3u;
-        const uint32_t hbase = (uint32_t)__cvta_generic_to_shared(h);
-        uint32_t i = (blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u)) * 4u + lane * 4u;
-        float4 sc = make_float4(0.f, 0.f, 0.f, 0.f);
-        uint32_t fl = 0;
-        if (i < n4) {
-            sc = __ldcs(reinterpret_cast<const float4*>(so.score + i));
-            fl = __ldcs(reinterpret_cast<const uint32_t*>(so.flags + i));
-        }
-        bool nan = false;
-        for (; i - lane * 4u < n4; i += stride) {  // warp-uniform trip count
-            const bool ok = i < n4;
-            const float scv[4] = {sc.x, sc.y, sc.z, sc.w};
-            const uint32_t fw = fl;
-            if (i + stride < n4) {
-                sc = __ldcs(reinterpret_cast<const float4*>(so.score + i + stride));
-                fl = __ldcs(reinterpret_cast<const uint32_t*>(so.flags + i + stride));
-            }
-            const uint32_t C = soa64_classes(fw, so.preemptive);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t img = soa64_img(scv[q], (fw >> (8 * q)) & RS_FLAG_SCORED, nan);
-                const uint32_t d = __byte_perm(img, C, 0x4443u + 0x0010u * q) & (SEL_BINS - 1);
-                hist_add_all(hbase, ok ? d : (uint32_t)SEL_BINS);
-            }
-        }
-        if (nan) atomicOr(so.err, 1);
-        for (uint32_t t = n4 + blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u) + lane; t - lane < n;
-             t += gridDim.x * SEL_THREADS) {
-            const bool ok = t < n;  // tail rows (< 4), warp-uniform trip count
-            hist_add_warp(h, ok ? sel_digit<Src>(src.value(t), 0) : 0u, ok);
-        }
+        sel_l0_soa(soa64_of(src), n, h);
     } else {
         sel_rows(src, n, [&](uint32_t, V v, bool ok) {
             hist_add_warp(h, sel_digit<Src>(v, level), ok && (LEVEL == 0 || vshr<Src>(v, shift) == wsh));
@@ -1394,9 +1399,13 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, Se
         __syncthreads();
         const int shift = Src::BITS - SEL_BITS * (int)level;
         const V wsh = level ? (V)(*(volatile unsigned __int128*)pfx128 >> shift) : (V)0;
-        sel_rows(src, n, [&](uint32_t, V v, bool ok) {
-            hist_add_warp(h, sel_digit<Src>(v, level), ok && (level == 0 || vshr<Src>(v, shift) == wsh));
-        });
+        if (level == 0 && soa64_aligned(src)) {
+            sel_l0_soa(soa64_of(src), n, h);
+        } else {
+            sel_rows(src, n, [&](uint32_t, V v, bool ok) {
+                hist_add_warp(h, sel_digit<Src>(v, level), ok && (level == 0 || vshr<Src>(v, shift) == wsh));
+            });
+        }
         __syncthreads();
         for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS)
             if (h[b]) atomicAdd(&hist[b], h[b]);
@@ -1585,6 +1594,8 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         RS_CUDA(cudaMemsetAsync(w.pfx, 0, sizeof(unsigned __int128), st));
         RS_CUDA(cudaMemsetAsync(w.hist, 0, SEL_BINS * sizeof(uint32_t), st));
         const uint32_t gb = min((n / 4 + SEL_THREADS) / SEL_THREADS, (uint32_t)num_sms() * 2);
+        // (measured: at 2^20 rows the multi-launch select below is faster, 68 vs 82 us as a
+        // CUDA graph — the grid barriers over 148 CTAs cost more than the launches they save)
         const bool fused = n <= SEL_FUSED_N && k + SEL_CAP_SMALL <= 1024;
         fused_update = fused && vec;
         const uint32_t unblk = (n + UPV_CHUNK - 1) / UPV_CHUNK;
@@ -1596,7 +1607,8 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
             // up to SEL_CLUSTER_N rows the grid is one cluster of <= 8 CTAs (hardware
             // barriers), above it a cooperative grid with global-memory barriers
             const bool cl = n <= SEL_CLUSTER_N;
-            const uint32_t grid = cl ? min(gb, 8u) : gb;
+            // cooperative: one 1024-thread CTA per SM at most (register file)
+            const uint32_t grid = cl ? min(gb, 8u) : min(gb, (uint32_t)num_sms());
             cudaLaunchConfig_t lc{};
             cudaLaunchAttribute at[1];
             if (cl) {
