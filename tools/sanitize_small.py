@@ -83,9 +83,11 @@ def main(which: str = "all"):
             pol = schedulers.RankingPolicy(schedulers.SchedulerConfig(max_batch=64), False)
             pol.schedule(reqs, 1 << 62)
             pol.schedule(reqs, 3000)
-        # 40k rows: the one-launch cooperative select (sel_fused); 300k (> 2^18): the
-        # multi-launch select (f32 keys from the columns; f64 / calibrated keys)
+        # 40k rows: the one-launch select as one CTA cluster (sel_fused<.., true>); 100k: as
+        # a cooperative grid; 300k (> 2^18): the multi-launch select (f32 keys from the
+        # columns; f64 / calibrated keys)
         for n, sdt, calib in ((40_000, torch.float32, False), (40_000, torch.float32, True),
+                              (100_000, torch.float32, False), (100_000, torch.float64, True),
                               (300_000, torch.float32, False), (300_000, torch.float64, False),
                               (300_000, torch.float32, True)):
             dq = schedulers.DeviceQueue.from_arrays(
