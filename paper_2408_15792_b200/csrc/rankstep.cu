@@ -14,9 +14,11 @@
 // (one warp; prefix-sum resolution of each 32-wide chunk) -> elementwise state update
 // with order-preserving compaction of promoted / demoted ids.
 #include <cstdlib>
+#include <cstring>
 #include <utility>
 #include "common.cuh"
 #include "mergesort.cuh"
+#include "engine_exec.cuh"
 #include <type_traits>
 #include <algorithm>
 
@@ -25,10 +27,8 @@ namespace rs {
 constexpr uint32_t RANK_BITS = 29;
 constexpr uint32_t RANK_MASK = (1u << RANK_BITS) - 1u;
 
-__global__ void build_rank_keys(rs_queue_soa q, int calibrated, int preemptive, RankKey* __restrict__ keys,
-                                int* __restrict__ err) {
-    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= (uint32_t)q.n) return;
+__device__ __forceinline__ RankKey rank_key_of(const rs_queue_soa& q, uint32_t i, int calibrated, int preemptive,
+                                               int* __restrict__ err) {
     const uint8_t f = q.flags[i];
     const bool scored = f & RS_FLAG_SCORED;
     const bool prio = f & RS_FLAG_PRIORITY;
@@ -46,7 +46,13 @@ __global__ void build_rank_keys(rs_queue_soa q, int calibrated, int preemptive, 
     k.eff = orderable_f64(eff);
     k.cr = (cls << RANK_BITS) | (q.arrival_rank[i] & RANK_MASK);
     k.pad = 0;
-    keys[i] = k;
+    return k;
+}
+__global__ void build_rank_keys(rs_queue_soa q, int calibrated, int preemptive, RankKey* __restrict__ keys,
+                                int* __restrict__ err) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (uint32_t)q.n) return;
+    keys[i] = rank_key_of(q, i, calibrated, preemptive, err);
 }
 
 // Unlimited KV budget: run = first min(max_batch, n) of the sorted order.
@@ -804,15 +810,39 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, Sel
 template <typename Src>
 __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c,
                                uint32_t dom_cap, uint32_t cap) {
-    __shared__ uint32_t pick, below;
-    for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) c[b] = __ldcg(&hist[b]);
+    // two-level search for the bin holding the need-th key: each of the 32 warps sums its
+    // 64 bins, warp 0 scans the 32 sums, the warp owning the bin scans its own 64
+    static_assert(SEL_BINS == 64 * (SEL_THREADS / 32), "64 bins per warp");
+    __shared__ uint32_t pick, below, wsum[32], wsel, wbefore;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t c0 = __ldcg(&hist[wid * 64 + lane]), c1 = __ldcg(&hist[wid * 64 + 32 + lane]);
+    c[wid * 64 + lane] = c0;
+    c[wid * 64 + 32 + lane] = c1;
+    const uint32_t ws = warp_sum(c0 + c1);
+    if (lane == 0) wsum[wid] = ws;
     __syncthreads();
-    if (threadIdx.x < 32) {  // one warp: chunked prefix sums over the bins
-        const uint32_t need = k - st->less;  // >= 1
-        uint32_t acc = 0, b0 = 0;
-        const int lane = threadIdx.x;
-        for (; b0 < SEL_BINS; b0 += 32) {
-            const uint32_t v = c[b0 + lane];
+    const uint32_t need = k - st->less;  // >= 1
+    if (wid == 0) {
+        const uint32_t v = wsum[lane];
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const unsigned hit = __ballot_sync(0xffffffffu, x >= need);  // the total is >= need
+        const int f = __ffs(hit) - 1;
+        if (lane == f) {
+            wsel = (uint32_t)f;
+            wbefore = x - v;
+        }
+    }
+    __syncthreads();
+    if (wid == (int)wsel) {
+        uint32_t acc = wbefore;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            const uint32_t v = half ? c1 : c0;
             uint32_t x = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -822,10 +852,9 @@ __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t
             const unsigned hit = __ballot_sync(0xffffffffu, acc + x >= need);
             if (hit) {
                 const int f = __ffs(hit) - 1;
-                const uint32_t xf = __shfl_sync(0xffffffffu, x, f), vf = __shfl_sync(0xffffffffu, v, f);
-                if (lane == 0) {
-                    pick = b0 + f;
-                    below = acc + xf - vf;
+                if (lane == f) {
+                    pick = (uint32_t)(wid * 64 + half * 32 + f);
+                    below = acc + x - v;
                 }
                 break;
             }
@@ -981,6 +1010,42 @@ __device__ __forceinline__ void sel_emit_small_block(const unsigned __int128* __
         sched[ix] = 1;
     }
     if (t == 0) counts[0] = (int32_t)k;
+}
+// The same emit spread over every CTA of a fused select: each candidate's place in the
+// order is the number of candidates with a smaller key (the <= 1024 keys staged in each
+// CTA's shared memory; a CTA ranks every gridDim.x-th candidate, S threads per candidate
+// over strided slices of the keys). Live keys are distinct; the finished rows the engine
+// loop leaves in place share the all-ones key, above every live one, so they never place
+// below k. counts[0] = k.
+__device__ __forceinline__ void sel_emit_rank(const unsigned __int128* __restrict__ ck,
+                                              const uint32_t* __restrict__ ci, uint32_t n_cand,
+                                              const int64_t* __restrict__ id, uint32_t k, int64_t* __restrict__ run,
+                                              uint8_t* __restrict__ sched, int32_t* __restrict__ counts, uint4* sk) {
+    const uint32_t m = min(n_cand, 1024u), t = threadIdx.x;
+    for (uint32_t i = t; i < m; i += blockDim.x) sk[i] = __ldcg(reinterpret_cast<const uint4*>(ck + i));
+    if (blockIdx.x == 0 && t == 0) counts[0] = (int32_t)k;
+    __syncthreads();
+    const uint32_t G = gridDim.x;
+    const uint32_t nl = m > blockIdx.x ? (m - blockIdx.x + G - 1) / G : 0u;  // this CTA's candidates
+    if (nl == 0) return;
+    uint32_t S = 32;
+    while (S > 1 && S * nl > blockDim.x) S >>= 1;
+    for (uint32_t base = 0; base < nl * S; base += blockDim.x) {  // (one pass unless nl > blockDim.x)
+        const uint32_t w = base + t, j = w / S, seg = w % S;
+        const bool act = j < nl;
+        const uint32_t c = blockIdx.x + j * G;
+        uint32_t cnt = 0;
+        if (act) {
+            const uint4 key = sk[c];
+            for (uint32_t x = seg; x < m; x += S) cnt += u128_less(sk[x], key) ? 1u : 0u;
+        }
+        for (uint32_t o = S >> 1; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (act && seg == 0 && cnt < k) {
+            const uint32_t row = __ldcg(ci + c);
+            run[cnt] = id[row];
+            sched[row] = 1;
+        }
+    }
 }
 __global__ void __launch_bounds__(1024) sel_sort_emit_small(const unsigned __int128* __restrict__ ck,
                                                             const uint32_t* __restrict__ ci,
@@ -1369,32 +1434,39 @@ __device__ __forceinline__ void grid_barrier(uint32_t* count, volatile uint32_t*
 
 // CL: the grid is one thread-block cluster (<= 8 CTAs), so the barriers are the hardware
 // cluster barrier (release / acquire at cluster scope) instead of the global-memory one.
-template <typename Src, bool CL>
-__global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, SelState* __restrict__ st,
-                                                         unsigned __int128* __restrict__ pfx128,
-                                                         uint32_t* __restrict__ hist, uint32_t k, uint32_t cap,
-                                                         unsigned __int128* __restrict__ ck, uint32_t* __restrict__ ci,
-                                                         uint32_t* __restrict__ bar, const int64_t* __restrict__ id,
-                                                         int64_t* __restrict__ run, uint8_t* __restrict__ sched,
-                                                         int32_t* __restrict__ counts, rs_queue_soa q, int32_t threshold,
-                                                         int32_t pquantum, uint32_t* __restrict__ plist,
-                                                         uint32_t* __restrict__ dlist, uint32_t* __restrict__ raw,
-                                                         uint32_t* __restrict__ boff, int64_t* __restrict__ prom,
-                                                         int64_t* __restrict__ dem) {
+template <bool CL>
+__device__ __forceinline__ void sel_gsync(uint32_t* bar) {
+    if constexpr (CL) {
+        __syncthreads();
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    } else {
+        grid_barrier(bar, bar + 1);
+    }
+}
+
+// The select body (run by every CTA of the grid; h / sk / sv: the CTA's shared scratch).
+// plist == nullptr: no state update; prom == nullptr: the update without the ordered
+// promoted / demoted id lists (the engine loop does not read them).
+struct NoMark {
+    __device__ __forceinline__ void operator()(int) const {}
+};
+template <typename Src, bool CL, typename Mark = NoMark>
+__device__ __forceinline__ void sel_fused_body(const Src& src, uint32_t n, SelState* __restrict__ st,
+                                               unsigned __int128* __restrict__ pfx128, uint32_t* __restrict__ hist,
+                                               uint32_t k, uint32_t cap, unsigned __int128* __restrict__ ck,
+                                               uint32_t* __restrict__ ci, uint32_t* __restrict__ bar,
+                                               const int64_t* __restrict__ id, int64_t* __restrict__ run,
+                                               uint8_t* __restrict__ sched, int32_t* __restrict__ counts,
+                                               const rs_queue_soa& q, int32_t threshold, int32_t pquantum,
+                                               uint32_t* __restrict__ plist, uint32_t* __restrict__ dlist,
+                                               uint32_t* __restrict__ raw, uint32_t* __restrict__ boff,
+                                               int64_t* __restrict__ prom, int64_t* __restrict__ dem, uint32_t* h,
+                                               uint4* sk, uint32_t* sv, const Mark& mark = Mark{}) {
     using V = typename Src::V;
-    __shared__ uint32_t h[SEL_BINS + 1];
-    __shared__ uint4 sk[1024];
-    __shared__ uint32_t sv[1024];
-    auto gsync = [&]() {
-        if constexpr (CL) {
-            __syncthreads();
-            asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-        } else {
-            grid_barrier(bar, bar + 1);
-        }
-    };
+    auto gsync = [&]() { sel_gsync<CL>(bar); };
     for (uint32_t level = 0; level < (uint32_t)Src::LEVELS; ++level) {
         if (*(volatile uint32_t*)&st->done) break;  // written before the last barrier
+        mark(20);
         for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) h[b] = 0;
         __syncthreads();
         const int shift = Src::BITS - SEL_BITS * (int)level;
@@ -1409,9 +1481,13 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, Se
         __syncthreads();
         for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS)
             if (h[b]) atomicAdd(&hist[b], h[b]);
+        mark(12);
         gsync();
+        mark(13);
         if (blockIdx.x == 0) sel_pick_block<Src>(st, pfx128, hist, k, h, 0u, cap);
+        mark(14);
         gsync();
+        mark(15);
     }
     {  // gather every key at or below the chosen bucket
         const int shift = Src::BITS - SEL_BITS * (int)*(volatile uint32_t*)&st->final_level;
@@ -1420,20 +1496,44 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, Se
             sel_append(ok && vshr<Src>(v, shift) <= lim, to128<Src>(v), i, &st->n_cand, ck, ci, SEL_SORT);
         });
     }
+    mark(8);
     gsync();
-    if (blockIdx.x == 0)
-        sel_emit_small_block(ck, ci, *(volatile uint32_t*)&st->n_cand, id, k, run, sched, counts, sk, sv);
+    mark(9);
+    sel_emit_rank(ck, ci, *(volatile uint32_t*)&st->n_cand, id, k, run, sched, counts, sk);
+    mark(16);
     if (plist == nullptr) return;  // the state update runs as separate kernels (unaligned columns)
     // the state update (schedulers.py:224-240) and the ordered promoted / demoted lists:
     // starvation_update_v's chunks, scan_pairs and copy_pd_lists, between grid barriers
     gsync();  // the batch's sched flags are set
+    mark(10);
     const uint32_t nblk = (n + UPV_CHUNK - 1) / UPV_CHUNK;
     for (uint32_t c = blockIdx.x; c < nblk; c += gridDim.x)
         upd_chunk_v(q, sched, threshold, pquantum, plist, dlist, raw, c);
     gsync();
+    mark(11);
+    if (prom == nullptr) return;
     if (blockIdx.x == 0) scan_pairs_block(raw, boff, nblk, counts);
     gsync();
     for (uint32_t c = blockIdx.x; c < nblk; c += gridDim.x) copy_pd_chunk(plist, dlist, raw, boff, id, prom, dem, c);
+}
+
+template <typename Src, bool CL>
+__global__ void __launch_bounds__(SEL_THREADS) sel_fused(Src src, uint32_t n, SelState* __restrict__ st,
+                                                         unsigned __int128* __restrict__ pfx128,
+                                                         uint32_t* __restrict__ hist, uint32_t k, uint32_t cap,
+                                                         unsigned __int128* __restrict__ ck, uint32_t* __restrict__ ci,
+                                                         uint32_t* __restrict__ bar, const int64_t* __restrict__ id,
+                                                         int64_t* __restrict__ run, uint8_t* __restrict__ sched,
+                                                         int32_t* __restrict__ counts, rs_queue_soa q, int32_t threshold,
+                                                         int32_t pquantum, uint32_t* __restrict__ plist,
+                                                         uint32_t* __restrict__ dlist, uint32_t* __restrict__ raw,
+                                                         uint32_t* __restrict__ boff, int64_t* __restrict__ prom,
+                                                         int64_t* __restrict__ dem) {
+    __shared__ uint32_t h[SEL_BINS + 1];
+    __shared__ uint4 sk[1024];
+    __shared__ uint32_t sv[1024];
+    sel_fused_body<Src, CL>(src, n, st, pfx128, hist, k, cap, ck, ci, bar, id, run, sched, counts, q, threshold,
+                            pquantum, plist, dlist, raw, boff, prom, dem, h, sk, sv);
 }
 
 __global__ void build_arrival_keys(const double* __restrict__ arr, const int64_t* __restrict__ id, uint32_t n,
@@ -1504,6 +1604,303 @@ struct RankSizer {
     template <typename T>
     T* take(size_t c) { s.take<T>(c); return nullptr; }
 };
+
+// The state update alone (no promoted / demoted lists), grid-stride over 4-row groups
+// (flags 4-B, starvation / quantum 16-B aligned: the engine's columns).
+__device__ __forceinline__ void upd_rows_plain(const rs_queue_soa& q, const uint8_t* __restrict__ sched, uint32_t n,
+                                               int32_t threshold, int32_t pquantum) {
+    const uint32_t n4 = n & ~3u, G = gridDim.x * blockDim.x;
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) * 4u; i < n4; i += 4u * G) {
+        const uint32_t fw = *reinterpret_cast<const uint32_t*>(q.flags + i);
+        const uint32_t sw = *reinterpret_cast<const uint32_t*>(sched + i);
+        const int4 st = *reinterpret_cast<const int4*>(q.starvation + i);
+        const int4 qu = *reinterpret_cast<const int4*>(q.quantum + i);
+        int32_t sa[4] = {st.x, st.y, st.z, st.w}, qa[4] = {qu.x, qu.y, qu.z, qu.w};
+        uint32_t nf = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint8_t f = (uint8_t)(fw >> (8 * k));
+            upd_row(f, sa[k], qa[k], (sw >> (8 * k)) & 0xffu, threshold, pquantum);
+            nf |= (uint32_t)f << (8 * k);
+        }
+        *reinterpret_cast<uint32_t*>(q.flags + i) = nf;
+        *reinterpret_cast<int4*>(q.starvation + i) = make_int4(sa[0], sa[1], sa[2], sa[3]);
+        *reinterpret_cast<int4*>(q.quantum + i) = make_int4(qa[0], qa[1], qa[2], qa[3]);
+    }
+    const uint32_t r = n4 + blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) {
+        uint8_t f = q.flags[r];
+        int32_t st = q.starvation[r], qu = q.quantum[r];
+        upd_row(f, st, qu, sched[r], threshold, pquantum);
+        q.flags[r] = f;
+        q.starvation[r] = st;
+        q.quantum[r] = qu;
+    }
+}
+
+// ---- the whole engine loop as one launch (record-free runs, unlimited KV budget) -------
+// engine.py:382-460 step for step, on one thread-block cluster: CTA 0 does the bookkeeping
+// the host loop did (idle jump, admission of the arrivals up to `now` in arrival order,
+// dropping requests whose full context never fits, the stop tests, the step's clock and
+// totals), then every CTA runs the rank step (keys, the fused select, the state update),
+// CTA 0 the execute phases — separated by cluster barriers. No launch or host round trip
+// per step remains. Finished rows are not compacted out every step (a step retires about
+// one row of tens of thousands): they stay in place flagged EX_DONE, rank after every live
+// row (all-ones key) and are compacted out, into the other column set, once they are an
+// eighth of the rows. Nothing the record-free run reports depends on row positions (the
+// sort key carries the arrival rank; only the per-step id lists, not written here, follow
+// row order), so the decisions are the per-kernel host loop's — tests/test_gpu_engine.py
+// checks both against the reference.
+constexpr int ENGINE_LOOP_CTAS = 8;  // one portable cluster
+// CTA 0's loop state (shared memory; copied to global memory for the host at the end)
+struct EngineLoopState {
+    int64_t now, nxt, n_rows, n_alive, step, n_fin, n_drop, tot_prefill, tot_decode, tot_pred, pred;
+    int32_t cur, stop, status, acct;
+};
+// what the other CTAs need of it, published by CTA 0 before a barrier
+struct EngineLoopPub {
+    int64_t n_rows, n_alive, step, live;
+    int32_t stop, compact;
+};
+struct EngineLoopArgs {
+    rs_engine_queue q[2];
+    rs_queue_soa soa[2];
+    rs_engine_trace tr;
+    rs_engine_cost cost;
+    const uint8_t* fits;
+    int64_t* dropped;
+    int64_t n_req;
+    int32_t* counts;   // int32[4]
+    int64_t *run, *pre, *fin, *prev_run;
+    int32_t *prev_n, *block_keep;
+    SelState* sel;
+    unsigned __int128* pfx;
+    uint32_t* hist;
+    unsigned __int128* ck;
+    uint32_t* ci;
+    RankKey* keys;
+    uint8_t* sched;
+    int32_t max_batch, threshold, pquantum, calibrated, preemptive;
+    int64_t pred_per_req, limit_ns, stop_after;
+    EngineLoopState* ls;
+    EngineLoopPub* pub;
+    unsigned long long* prof;  // RS_ENGINE_PROF: per-phase ns totals (CTA 0's view), else null
+};
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// CTA 0, between the previous step's last barrier and this step's first: account the
+// previous step, stop tests, reset the select state, idle jump + admission (engine.py:
+// 404-413: the arrivals up to `now`, in trace order, the ones that can never fit dropped)
+__device__ void engine_loop_head(const EngineLoopArgs& a, EngineLoopState& S, int64_t* out, int cur,
+                                 int* warp_tot, int* s_first) {
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        if (S.acct) {
+            const int64_t iter = out[1], prefill = out[2];
+            S.now = out[0];
+            S.n_alive -= out[5];
+            S.n_fin += out[5];
+            S.tot_prefill += prefill;
+            S.tot_pred += S.pred;
+            S.tot_decode += iter - prefill - S.pred;
+            S.step += 1;
+            if ((a.stop_after >= 0 && S.n_fin >= a.stop_after) || (a.limit_ns >= 0 && S.now >= a.limit_ns))
+                S.stop = 1;
+        }
+        if (!S.stop && S.n_alive == 0 && S.nxt < a.n_req) {
+            const int64_t t = a.tr.arrival_ns[S.nxt];
+            if (t > S.now) S.now = t;  // jump_if_idle
+        }
+    }
+    if (tid < 4) a.counts[tid] = 0;
+    if (tid == 32) {
+        SelState* st = a.sel;
+        st->dom_ok = st->compacted = st->dom_overflow = 0;
+        st->level = st->less = st->done = st->final_level = st->n_cand = st->arrived = 0;
+        *a.pfx = 0;
+    }
+    __syncthreads();
+    if (S.stop) {
+        if (tid == 0) {
+            S.cur = cur;
+            a.pub->stop = 1;
+        }
+        return;
+    }
+    const int64_t now = S.now, n_rows = S.n_rows;
+    int64_t nxt = S.nxt, n_drop = S.n_drop;
+    int64_t kadm = 0;
+    const rs_engine_queue& q = a.q[cur];
+    for (;;) {
+        if (tid == 0) *s_first = EX_THREADS;
+        __syncthreads();
+        const int64_t i = nxt + tid;
+        if (!(i < a.n_req && a.tr.arrival_ns[i] <= now)) atomicMin(s_first, tid);
+        __syncthreads();
+        const int first = *(volatile int*)s_first;
+        const bool valid = tid < first;  // the arrivals are the prefix up to the first later one
+        if (first == 0) break;           // (no scans needed: the common case of no arrival)
+        const bool fit = valid && a.fits[i];
+        int tf, td;
+        const int pf = block_excl_scan(fit ? 1 : 0, warp_tot, tf);
+        if (fit) engine_admit_row(q, a.tr, (int)i, n_rows + kadm + pf);
+        const int pd = block_excl_scan(valid && !fit ? 1 : 0, warp_tot, td);
+        if (valid && !fit) a.dropped[n_drop + pd] = i;
+        kadm += tf;
+        n_drop += td;
+        nxt += first;
+        if (first < EX_THREADS) break;
+    }
+    if (tid == 0) {
+        S.nxt = nxt;
+        S.n_drop = n_drop;
+        S.n_rows = n_rows + kadm;
+        S.n_alive += kadm;
+        S.pred = kadm * a.pred_per_req;
+        EngineLoopPub* pub = a.pub;
+        if (S.n_alive == 0 || (a.limit_ns >= 0 && now >= a.limit_ns)) {
+            S.stop = 1;
+            S.cur = cur;
+            pub->stop = 1;
+        } else {
+            S.acct = 1;
+            out[0] = now;  // the execute phase advances the clock from here
+            pub->n_rows = S.n_rows;
+            pub->n_alive = S.n_alive;
+            pub->step = S.step;
+        }
+    }
+    __syncthreads();  // (s_first / warp_tot reuse)
+}
+
+struct LoopMark {
+    unsigned long long* prof;
+    unsigned long long* t0;
+    __device__ __forceinline__ void operator()(int ph) const {
+        if (prof != nullptr && ph >= 20) {
+            prof[ph] += 1;  // a count, not a time
+        } else if (prof != nullptr) {
+            const unsigned long long t = gtimer();
+            prof[ph] += t - *t0;
+            *t0 = t;
+        }
+    }
+};
+
+template <bool CL>
+__global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_constant__ EngineLoopArgs a) {
+    __shared__ uint32_t h[SEL_BINS + 1];
+    __shared__ uint4 sk[1024];  // also the execute phase's preempted-row scratch (EX_PRE_CAP ints)
+    __shared__ uint32_t sv[1024];
+    __shared__ int warp_tot[32];
+    __shared__ int s_int;
+    __shared__ long long s_base;
+    __shared__ EngineLoopState S;  // CTA 0's
+    __shared__ int64_t s_out[6];  // CTA 0's execute results (rs_engine_execute's out_dev)
+    static_assert(sizeof(sk) >= EX_PRE_CAP * sizeof(int), "pre_rows scratch");
+    uint32_t* bar = &a.sel->bar_count;
+    volatile EngineLoopPub* pub = a.pub;
+    const uint32_t G = gridDim.x * SEL_THREADS;
+    unsigned long long t0 = 0;
+    const LoopMark mark{a.prof != nullptr && blockIdx.x == 0 && threadIdx.x == 0 ? a.prof : nullptr, &t0};
+    if (a.prof) t0 = gtimer();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        S = EngineLoopState{};
+        s_out[0] = 0;
+    }
+    __syncthreads();
+    for (int cur = 0;;) {
+        if (blockIdx.x == 0) engine_loop_head(a, S, s_out, cur, warp_tot, &s_int);
+        sel_gsync<CL>(bar);
+        mark(0);
+        if (pub->stop) break;
+        const uint32_t n = (uint32_t)pub->n_rows;
+        const uint32_t n_alive = (uint32_t)pub->n_alive;
+        const int32_t step = (int32_t)pub->step;
+        rs_queue_soa soa = a.soa[cur];
+        soa.n = n;
+        rs_engine_queue q = a.q[cur];
+        q.n = n;
+        // the rank step's keys (build_rank_keys; finished rows rank last) and cleared batch flags
+        for (uint32_t i = blockIdx.x * SEL_THREADS + threadIdx.x; i < n; i += G) {
+            a.sched[i] = 0;
+            RankKey key;
+            if (soa.flags[i] & EX_DONE) {
+                key.eff = ~0ull;
+                key.cr = ~0u;
+                key.pad = 0;
+            } else {
+                key = rank_key_of(soa, i, a.calibrated, a.preemptive, a.counts + 3);
+            }
+            a.keys[i] = key;
+        }
+        sel_gsync<CL>(bar);
+        mark(1);
+        if (*(volatile int32_t*)(a.counts + 3)) {  // NaN effective score: every CTA sees it
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                S.status = RS_ERR_NAN;
+                S.cur = cur;
+            }
+            break;
+        }
+        const uint32_t k = min(n_alive, (uint32_t)a.max_batch);
+        sel_fused_body<SrcKeys, CL>(SrcKeys{a.keys}, n, a.sel, a.pfx, a.hist, k, (uint32_t)SEL_CAP_SMALL, a.ck, a.ci,
+                                    bar, soa.id, a.run, a.sched, a.counts, soa, a.threshold, a.pquantum, nullptr,
+                                    nullptr, nullptr, nullptr, nullptr, nullptr, h, sk, sv, mark);
+        sel_gsync<CL>(bar);  // the batch's sched flags are set
+        mark(10);
+        upd_rows_plain(soa, a.sched, n, a.threshold, a.pquantum);  // schedulers.py:224-240
+        sel_gsync<CL>(bar);
+        mark(11);
+        if (blockIdx.x == 0) {
+            engine_execute_block<false, false>(q, a.tr, a.cost, a.run, a.counts, step, S.pred, s_out, a.pre, a.fin,
+                                               a.prev_run, a.prev_n, reinterpret_cast<int*>(sk), warp_tot);
+            if (threadIdx.x == 0) {  // compaction once the finished rows are an eighth of the rows
+                const int64_t live = S.n_alive - s_out[5];
+                pub->live = live;
+                pub->compact = (int64_t)(n - live) * 8 >= (int64_t)n ? 1 : 0;
+            }
+        }
+        sel_gsync<CL>(bar);
+        mark(6);
+        if (!pub->compact) continue;
+        const uint32_t live = (uint32_t)pub->live;
+        const uint32_t nb = (n + EX_THREADS - 1) / EX_THREADS;
+        for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
+            const int t = compact_count_chunk(q.flags, n, c, warp_tot);
+            if (threadIdx.x == 0) a.block_keep[c] = t;
+        }
+        sel_gsync<CL>(bar);
+        for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
+            if (threadIdx.x < 32) {
+                long long b = 0;
+                for (uint32_t j = threadIdx.x; j < c; j += 32) b += __ldcg(a.block_keep + j);
+                b = warp_sum(b);
+                if (threadIdx.x == 0) s_base = b;
+            }
+            __syncthreads();
+            compact_scatter_chunk(q, a.q[cur ^ 1], a.tr, c, s_base, warp_tot);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) S.n_rows = live;
+        cur ^= 1;
+        sel_gsync<CL>(bar);
+        mark(7);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.ls = S;
+}
+
+// RS_ENGINE_LOOP=host keeps the per-kernel host loop (measurement experiments)
+static bool engine_loop_device_enabled() {
+    static const bool v = [] {
+        const char* e = getenv("RS_ENGINE_LOOP");
+        return !(e && strcmp(e, "host") == 0);
+    }();
+    return v;
+}
 
 }  // namespace rs
 
@@ -1699,3 +2096,127 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
+
+namespace rs {
+// rs_engine_run's one-launch path (engine.cu): taken when the rank step is the fused
+// select (unlimited KV budget, max_batch + SEL_CAP_SMALL <= 1024) and the state columns
+// are aligned for its vector update; *handled = false leaves the run to the host loop.
+int rs_engine_run_device(const rs_engine_queue* q2, const rs_queue_soa* soa2, const rs_engine_trace* tr,
+                         const rs_engine_cost* cost, const rs_engine_loop* lp, rs_engine_loop_out* res,
+                         cudaStream_t st, bool* handled) {
+    *handled = false;
+    const int64_t n = lp->n_requests;
+    if (!engine_loop_device_enabled() || lp->kv_budget >= 0 || n <= 0 || n > (int64_t)RANK_MASK ||
+        lp->max_batch + SEL_CAP_SMALL > 1024 || lp->ws_bytes < rs_rank_step_workspace_size(n))
+        return RS_OK;
+    for (int c = 0; c < 2; ++c) {
+        const rs_queue_soa& s = soa2[c];
+        if ((reinterpret_cast<uintptr_t>(s.flags) & 3u) ||
+            ((reinterpret_cast<uintptr_t>(s.starvation) | reinterpret_cast<uintptr_t>(s.quantum)) & 15u))
+            return RS_OK;
+    }
+    *handled = true;
+    Arena ar(lp->ws, lp->ws_bytes);
+    RankWs w;
+    rank_layout(ar, (uint64_t)n, &w);
+    EngineLoopArgs a{};
+    for (int c = 0; c < 2; ++c) {
+        a.q[c] = q2[c];
+        a.soa[c] = soa2[c];
+    }
+    a.tr = *tr;
+    a.cost = *cost;
+    a.n_req = n;
+    a.counts = reinterpret_cast<int32_t*>(lp->stat_dev + 6);
+    a.run = lp->run_dev;
+    a.pre = lp->pre_dev;
+    a.fin = lp->fin_dev;
+    a.prev_run = lp->prev_run_dev;
+    a.prev_n = lp->prev_n_dev;
+    a.block_keep = lp->scratch_dev;
+    a.sel = w.sel;
+    a.pfx = w.pfx;
+    a.hist = w.hist;
+    a.ck = w.ck;
+    a.ci = w.ci;
+    a.keys = w.kb;
+    a.sched = w.sched;
+    a.max_batch = lp->max_batch;
+    a.threshold = lp->starvation_threshold;
+    a.pquantum = lp->priority_quantum;
+    a.calibrated = lp->length_calibrated;
+    a.preemptive = lp->preemptive;
+    a.pred_per_req = lp->predictor_ns_per_request;
+    a.limit_ns = lp->limit_ns;
+    a.stop_after = lp->stop_after_finished;
+    uint8_t* fits = nullptr;
+    int64_t* dropped = nullptr;
+    EngineLoopState* ls = nullptr;
+    RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&fits), (size_t)n, st));
+    RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dropped), (size_t)n * sizeof(int64_t), st));
+    RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ls), sizeof(EngineLoopState) + sizeof(EngineLoopPub), st));
+    a.fits = fits;
+    a.dropped = dropped;
+    a.ls = ls;
+    a.pub = reinterpret_cast<EngineLoopPub*>(ls + 1);
+    RS_CUDA(cudaMemcpyAsync(fits, lp->fits, (size_t)n, cudaMemcpyHostToDevice, st));
+    RS_CUDA(cudaMemsetAsync(ls, 0, sizeof(EngineLoopState) + sizeof(EngineLoopPub), st));
+    RS_CUDA(cudaMemsetAsync(w.sel, 0, sizeof(SelState), st));
+    RS_CUDA(cudaMemsetAsync(w.hist, 0, SEL_BINS * sizeof(uint32_t), st));
+    cudaLaunchConfig_t lc{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    int ctas = ENGINE_LOOP_CTAS;
+    if (const char* e = getenv("RS_ENGINE_CTAS")) ctas = atoi(e);  // measurement experiments (<= 16)
+    if (ctas > 8) RS_CUDA(cudaFuncSetAttribute(engine_loop_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    at[0].val.clusterDim.x = ctas;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.gridDim = dim3(ctas);
+    lc.blockDim = dim3(SEL_THREADS);
+    lc.stream = st;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    const bool prof = getenv("RS_ENGINE_PROF") != nullptr;
+    if (prof) {
+        RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.prof), 32 * sizeof(unsigned long long), st));
+        RS_CUDA(cudaMemsetAsync(a.prof, 0, 32 * sizeof(unsigned long long), st));
+    }
+    RS_CUDA(cudaLaunchKernelEx(&lc, engine_loop_kernel<true>, a));
+    if (prof) {
+        unsigned long long p[32];
+        RS_CUDA(cudaMemcpyAsync(p, a.prof, sizeof(p), cudaMemcpyDeviceToHost, st));
+        RS_CUDA(cudaStreamSynchronize(st));
+        RS_CUDA(cudaFreeAsync(a.prof, st));
+        static const char* names[] = {"head", "keys", "", "", "", "", "execute", "compact", "gather",
+                                      "gather_barrier", "emit_barrier", "update+bar", "level_pass", "level_bar1",
+                                      "level_pick", "level_bar2", "emit"};
+        for (int i = 0; i < 17; ++i)
+            if (names[i][0]) fprintf(stderr, "engine_loop %-16s %10.3f ms\n", names[i], p[i] * 1e-6);
+        fprintf(stderr, "engine_loop levels %llu\n", p[20]);
+    }
+    EngineLoopState h{};
+    RS_CUDA(cudaMemcpyAsync(&h, ls, sizeof(h), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    if (h.n_drop > 0)
+        RS_CUDA(cudaMemcpyAsync(lp->dropped_host, dropped, (size_t)h.n_drop * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaFreeAsync(fits, st));
+    RS_CUDA(cudaFreeAsync(dropped, st));
+    RS_CUDA(cudaFreeAsync(ls, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    res->now_ns = h.now;
+    res->steps = h.step;
+    res->n_finished = h.n_fin;
+    res->next_arrival = h.nxt;
+    res->n_dropped = h.n_drop;
+    res->total_prefill_ns = h.tot_prefill;
+    res->total_decode_ns = h.tot_decode;
+    res->total_predictor_ns = h.tot_pred;
+    res->final_set = h.cur;
+    if (h.status == RS_ERR_NAN) {
+        set_error("ranking policy: NaN effective score");
+        return RS_ERR_NAN;
+    }
+    return RS_OK;
+}
+}  // namespace rs
