@@ -189,16 +189,21 @@ struct SelState {
 // SrcKeys: materialised 96-bit RankKeys [class:3 | eff(f64 image):64 | rank:29] << 3.
 // V: the value type the kernels compute in; the value's virtual BITS-bit image is
 // (V)value << PAD (SrcSoa64 works in 64-bit registers: no 128-bit shifts per row).
+__device__ __forceinline__ unsigned __int128 rank_key_value(const RankKey& k) {
+    const unsigned __int128 v = ((unsigned __int128)(k.cr >> 29) << 93) | ((unsigned __int128)k.eff << 29) |
+                                (unsigned __int128)(k.cr & RANK_MASK);
+    return v << 3;
+}
 struct SrcKeys {
     using V = unsigned __int128;
     static constexpr int BITS = 99, LEVELS = 9, PAD = 0;
     const RankKey* keys;
-    __device__ __forceinline__ unsigned __int128 value(uint32_t i) const {
-        const RankKey k = keys[i];
-        const unsigned __int128 v = ((unsigned __int128)(k.cr >> 29) << 93) |
-                                    ((unsigned __int128)k.eff << 29) | (unsigned __int128)(k.cr & RANK_MASK);
-        return v << 3;
-    }
+    __device__ __forceinline__ unsigned __int128 value(uint32_t i) const { return rank_key_value(keys[i]); }
+    // split access for batched passes (sel_rows_batch): every load first, then the values
+    using Raw = RankKey;
+    static constexpr int BATCH = 4;
+    __device__ __forceinline__ Raw load(uint32_t i) const { return keys[i]; }
+    __device__ __forceinline__ unsigned __int128 finish(const Raw& r, uint32_t) const { return rank_key_value(r); }
 };
 // SrcSoa64: built on the fly from the queue columns (score f32, flags, arrival rank; 9 B
 // per row, nothing materialised) when the effective score is the raw f32 score (not
@@ -334,6 +339,42 @@ __device__ __forceinline__ void sel_rows(const Src& src, uint32_t n, F&& f) {
         f(i, ok ? src.value(i) : (typename Src::V)0, ok);
     }
 }
+// sel_rows for sources with a split load / finish (Src::Raw): each warp takes R x 32
+// consecutive rows per step and issues all R loads before any value is handed to f, so
+// a thread has R rows in flight (the small-grid passes of the fused select are bound by
+// load latency, not bandwidth). Warp-uniform trip count.
+template <int R, typename Src, typename F>
+__device__ __forceinline__ void sel_rows_batch(const Src& src, uint32_t n, F&& f) {
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t stride = gridDim.x * SEL_THREADS * R;
+    for (uint32_t i0 = (blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u)) * R; i0 < n; i0 += stride) {
+        typename Src::Raw raw[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const uint32_t i = i0 + 32u * j + lane;
+            if (i < n) raw[j] = src.load(i);
+        }
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const uint32_t i = i0 + 32u * j + lane;
+            const bool ok = i < n;
+            f(i, ok ? src.finish(raw[j], i) : (typename Src::V)0, ok);
+        }
+    }
+}
+template <typename T, typename = void>
+struct has_raw : std::false_type {};
+template <typename T>
+struct has_raw<T, std::void_t<typename T::Raw>> : std::true_type {};
+// the fused select's passes: batched where the source splits its loads
+template <typename Src, typename F>
+__device__ __forceinline__ void sel_rows_fused(const Src& src, uint32_t n, F&& f) {
+    if constexpr (has_raw<Src>::value)
+        sel_rows_batch<Src::BATCH>(src, n, f);
+    else
+        sel_rows(src, n, f);
+}
+
 // Like sel_rows, but hands f up to four consecutive rows per lane at once (i0, values,
 // count); warp-uniform trip counts.
 template <typename Src, typename F>
@@ -805,23 +846,18 @@ __global__ void __launch_bounds__(SEL_THREADS) sel_hist(Src src, uint32_t n, Sel
     }
 }
 
-// One block: choose the bucket holding the k-th key from the level's global histogram
-// (c = shared scratch of SEL_BINS words), clear the histogram for the next level.
-template <typename Src>
-__device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c,
-                               uint32_t dom_cap, uint32_t cap) {
-    // two-level search for the bin holding the need-th key: each of the 32 warps sums its
-    // 64 bins, warp 0 scans the 32 sums, the warp owning the bin scans its own 64
+// The bin holding the need-th key (need >= 1 <= the bins' total), 1024-thread block, thread
+// t holding bins (t / 32) * 64 + t % 32 and + 32: each warp sums its 64 bins, warp 0 scans
+// the 32 sums, the warp owning the bin scans its own 64. pick / below (the keys in the
+// bins before it) returned to every thread.
+__device__ __forceinline__ void sel_bin_search(uint32_t c0, uint32_t c1, uint32_t need, uint32_t& pick_out,
+                                               uint32_t& below_out) {
     static_assert(SEL_BINS == 64 * (SEL_THREADS / 32), "64 bins per warp");
     __shared__ uint32_t pick, below, wsum[32], wsel, wbefore;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const uint32_t c0 = __ldcg(&hist[wid * 64 + lane]), c1 = __ldcg(&hist[wid * 64 + 32 + lane]);
-    c[wid * 64 + lane] = c0;
-    c[wid * 64 + 32 + lane] = c1;
     const uint32_t ws = warp_sum(c0 + c1);
     if (lane == 0) wsum[wid] = ws;
     __syncthreads();
-    const uint32_t need = k - st->less;  // >= 1
     if (wid == 0) {
         const uint32_t v = wsum[lane];
         uint32_t x = v;
@@ -830,7 +866,7 @@ __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t
             const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
-        const unsigned hit = __ballot_sync(0xffffffffu, x >= need);  // the total is >= need
+        const unsigned hit = __ballot_sync(0xffffffffu, x >= need);
         const int f = __ffs(hit) - 1;
         if (lane == f) {
             wsel = (uint32_t)f;
@@ -862,6 +898,53 @@ __device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t
         }
     }
     __syncthreads();
+    pick_out = pick;
+    below_out = below;
+}
+
+// The fused select's per-CTA copy of the pick state (the engine loop: every CTA picks from
+// the per-CTA histogram slices itself, no second barrier per level).
+struct SelLocal {
+    unsigned __int128 pfx;
+    uint32_t less, level, done, final_level;
+};
+template <typename Src>
+__device__ __forceinline__ void sel_pick_local(SelLocal& L, const uint32_t* __restrict__ slices, uint32_t nsl,
+                                               uint32_t k, uint32_t cap) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t c0 = 0, c1 = 0;
+    for (uint32_t s = 0; s < nsl; ++s) {
+        c0 += __ldcg(&slices[s * SEL_BINS + wid * 64 + lane]);
+        c1 += __ldcg(&slices[s * SEL_BINS + wid * 64 + 32 + lane]);
+    }
+    uint32_t pick, below;
+    sel_bin_search(c0, c1, k - L.less, pick, below);
+    const int pl = (int)(pick & 63u);
+    if (wid == (int)(pick >> 6) && lane == (pl & 31)) {  // the thread holding the bin
+        const uint32_t cnt = pl < 32 ? c0 : c1;
+        const uint32_t level = L.level;
+        L.pfx |= (unsigned __int128)pick << (Src::BITS - SEL_BITS * (level + 1));
+        L.less += below;
+        L.level = level + 1;
+        if (cnt <= cap || level + 1 == Src::LEVELS) {
+            L.done = 1;
+            L.final_level = level + 1;
+        }
+    }
+    __syncthreads();
+}
+
+// One block: choose the bucket holding the k-th key from the level's global histogram
+// (c = shared scratch of SEL_BINS words), clear the histogram for the next level.
+template <typename Src>
+__device__ void sel_pick_block(SelState* st, unsigned __int128* pfx128, uint32_t* hist, uint32_t k, uint32_t* c,
+                               uint32_t dom_cap, uint32_t cap) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t c0 = __ldcg(&hist[wid * 64 + lane]), c1 = __ldcg(&hist[wid * 64 + 32 + lane]);
+    c[wid * 64 + lane] = c0;
+    c[wid * 64 + 32 + lane] = c1;
+    uint32_t pick, below;
+    sel_bin_search(c0, c1, k - st->less, pick, below);
     for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) hist[b] = 0;
     if (threadIdx.x == 0) {
         const uint32_t level = st->level;
@@ -1017,13 +1100,19 @@ __device__ __forceinline__ void sel_emit_small_block(const unsigned __int128* __
 // over strided slices of the keys). Live keys are distinct; the finished rows the engine
 // loop leaves in place share the all-ones key, above every live one, so they never place
 // below k. counts[0] = k.
+// thr (optional): the key placed at rank `target` is stored there (all ones if there are
+// <= target candidates) — the engine loop's next speculative threshold.
 __device__ __forceinline__ void sel_emit_rank(const unsigned __int128* __restrict__ ck,
                                               const uint32_t* __restrict__ ci, uint32_t n_cand,
                                               const int64_t* __restrict__ id, uint32_t k, int64_t* __restrict__ run,
-                                              uint8_t* __restrict__ sched, int32_t* __restrict__ counts, uint4* sk) {
+                                              uint8_t* __restrict__ sched, int32_t* __restrict__ counts, uint4* sk,
+                                              unsigned __int128* thr = nullptr, uint32_t target = 0) {
     const uint32_t m = min(n_cand, 1024u), t = threadIdx.x;
     for (uint32_t i = t; i < m; i += blockDim.x) sk[i] = __ldcg(reinterpret_cast<const uint4*>(ck + i));
-    if (blockIdx.x == 0 && t == 0) counts[0] = (int32_t)k;
+    if (blockIdx.x == 0 && t == 0) {
+        counts[0] = (int32_t)k;
+        if (thr != nullptr && m <= target) *thr = ~(unsigned __int128)0;
+    }
     __syncthreads();
     const uint32_t G = gridDim.x;
     const uint32_t nl = m > blockIdx.x ? (m - blockIdx.x + G - 1) / G : 0u;  // this CTA's candidates
@@ -1044,6 +1133,10 @@ __device__ __forceinline__ void sel_emit_rank(const unsigned __int128* __restric
             const uint32_t row = __ldcg(ci + c);
             run[cnt] = id[row];
             sched[row] = 1;
+        }
+        if (thr != nullptr && act && seg == 0 && cnt == target) {
+            const uint4 kv = sk[c];
+            *reinterpret_cast<uint4*>(thr) = kv;
         }
     }
 }
@@ -1450,7 +1543,7 @@ __device__ __forceinline__ void sel_gsync(uint32_t* bar) {
 struct NoMark {
     __device__ __forceinline__ void operator()(int) const {}
 };
-template <typename Src, bool CL, typename Mark = NoMark>
+template <typename Src, bool CL, typename Mark = NoMark, typename Src0 = Src>
 __device__ __forceinline__ void sel_fused_body(const Src& src, uint32_t n, SelState* __restrict__ st,
                                                unsigned __int128* __restrict__ pfx128, uint32_t* __restrict__ hist,
                                                uint32_t k, uint32_t cap, unsigned __int128* __restrict__ ck,
@@ -1461,45 +1554,73 @@ __device__ __forceinline__ void sel_fused_body(const Src& src, uint32_t n, SelSt
                                                uint32_t* __restrict__ plist, uint32_t* __restrict__ dlist,
                                                uint32_t* __restrict__ raw, uint32_t* __restrict__ boff,
                                                int64_t* __restrict__ prom, int64_t* __restrict__ dem, uint32_t* h,
-                                               uint4* sk, uint32_t* sv, const Mark& mark = Mark{}) {
+                                               uint4* sk, uint32_t* sv, const Mark& mark = Mark{},
+                                               const Src0* src0 = nullptr, uint32_t* slices = nullptr,
+                                               uint32_t k_sel = 0, unsigned __int128* thr = nullptr) {
+    // k_sel (>= k, optional): the select keeps every key up to the k_sel-th (the emit still
+    // places k); thr: see sel_emit_rank (target k_sel)
+    if (k_sel < k) k_sel = k;
+    // src0 (optional): level 0's row values, e.g. keys built (and stored for src) on the way.
+    // slices (optional, 2 x gridDim.x x SEL_BINS words): each CTA stores its level histogram
+    // in its own slice (level parity double-buffered) and every CTA picks the bucket itself
+    // from their sum — no global atomics, one barrier per level instead of two (small grids).
     using V = typename Src::V;
+    static_assert(std::is_same<typename Src0::V, V>::value && Src0::BITS == Src::BITS, "level-0 source");
     auto gsync = [&]() { sel_gsync<CL>(bar); };
+    __shared__ SelLocal L;
+    if (slices != nullptr) {
+        if (threadIdx.x == 0) L = SelLocal{0, 0u, 0u, 0u, 0u};
+        __syncthreads();
+    }
     for (uint32_t level = 0; level < (uint32_t)Src::LEVELS; ++level) {
-        if (*(volatile uint32_t*)&st->done) break;  // written before the last barrier
+        if (slices != nullptr ? L.done != 0 : *(volatile uint32_t*)&st->done != 0) break;
         mark(20);
         for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) h[b] = 0;
         __syncthreads();
         const int shift = Src::BITS - SEL_BITS * (int)level;
-        const V wsh = level ? (V)(*(volatile unsigned __int128*)pfx128 >> shift) : (V)0;
+        const V wsh = level ? (V)((slices != nullptr ? L.pfx : *(volatile unsigned __int128*)pfx128) >> shift) : (V)0;
         if (level == 0 && soa64_aligned(src)) {
             sel_l0_soa(soa64_of(src), n, h);
+        } else if (level == 0 && src0 != nullptr) {
+            sel_rows_fused(*src0, n, [&](uint32_t, V v, bool ok) { hist_add_warp(h, sel_digit<Src>(v, 0), ok); });
         } else {
-            sel_rows(src, n, [&](uint32_t, V v, bool ok) {
+            sel_rows_fused(src, n, [&](uint32_t, V v, bool ok) {
                 hist_add_warp(h, sel_digit<Src>(v, level), ok && (level == 0 || vshr<Src>(v, shift) == wsh));
             });
         }
         __syncthreads();
+        if (slices != nullptr) {
+            uint32_t* buf = slices + (size_t)(level & 1u) * gridDim.x * SEL_BINS;
+            for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS) buf[blockIdx.x * SEL_BINS + b] = h[b];
+            mark(12);
+            gsync();
+            mark(13);
+            sel_pick_local<Src>(L, buf, gridDim.x, k_sel, cap);
+            mark(14);
+            continue;
+        }
         for (int b = threadIdx.x; b < SEL_BINS; b += SEL_THREADS)
             if (h[b]) atomicAdd(&hist[b], h[b]);
         mark(12);
         gsync();
         mark(13);
-        if (blockIdx.x == 0) sel_pick_block<Src>(st, pfx128, hist, k, h, 0u, cap);
+        if (blockIdx.x == 0) sel_pick_block<Src>(st, pfx128, hist, k_sel, h, 0u, cap);
         mark(14);
         gsync();
         mark(15);
     }
     {  // gather every key at or below the chosen bucket
-        const int shift = Src::BITS - SEL_BITS * (int)*(volatile uint32_t*)&st->final_level;
-        const V lim = (V)(*(volatile unsigned __int128*)pfx128 >> shift);
-        sel_rows(src, n, [&](uint32_t i, V v, bool ok) {
+        const uint32_t fl = slices != nullptr ? L.final_level : *(volatile uint32_t*)&st->final_level;
+        const int shift = Src::BITS - SEL_BITS * (int)fl;
+        const V lim = (V)((slices != nullptr ? L.pfx : *(volatile unsigned __int128*)pfx128) >> shift);
+        sel_rows_fused(src, n, [&](uint32_t i, V v, bool ok) {
             sel_append(ok && vshr<Src>(v, shift) <= lim, to128<Src>(v), i, &st->n_cand, ck, ci, SEL_SORT);
         });
     }
     mark(8);
     gsync();
     mark(9);
-    sel_emit_rank(ck, ci, *(volatile uint32_t*)&st->n_cand, id, k, run, sched, counts, sk);
+    sel_emit_rank(ck, ci, *(volatile uint32_t*)&st->n_cand, id, k, run, sched, counts, sk, thr, k_sel);
     mark(16);
     if (plist == nullptr) return;  // the state update runs as separate kernels (unaligned columns)
     // the state update (schedulers.py:224-240) and the ordered promoted / demoted lists:
@@ -1652,6 +1773,7 @@ __device__ __forceinline__ void upd_rows_plain(const rs_queue_soa& q, const uint
 // row order), so the decisions are the per-kernel host loop's — tests/test_gpu_engine.py
 // checks both against the reference.
 constexpr int ENGINE_LOOP_CTAS = 8;  // one portable cluster
+constexpr uint32_t ENGINE_SPEC_MARGIN = 256;  // speculative threshold: rank k + this
 // CTA 0's loop state (shared memory; copied to global memory for the host at the end)
 struct EngineLoopState {
     int64_t now, nxt, n_rows, n_alive, step, n_fin, n_drop, tot_prefill, tot_decode, tot_pred, pred;
@@ -1676,6 +1798,8 @@ struct EngineLoopArgs {
     SelState* sel;
     unsigned __int128* pfx;
     uint32_t* hist;
+    uint32_t* slices;  // 2 x grid x SEL_BINS words
+    unsigned __int128* thr;  // speculative select threshold (all ones at the start)
     unsigned __int128* ck;
     uint32_t* ci;
     RankKey* keys;
@@ -1777,6 +1901,61 @@ __device__ void engine_loop_head(const EngineLoopArgs& a, EngineLoopState& S, in
     __syncthreads();  // (s_first / warp_tot reuse)
 }
 
+// The engine loop's level-0 source: builds each row's 96-bit key from the queue columns
+// (build_rank_keys; finished rows get the all-ones key, after every live row), stores it
+// for the later levels (SrcKeys) and clears the row's batch flag.
+struct SrcEngBuild {
+    using V = unsigned __int128;
+    static constexpr int BITS = SrcKeys::BITS, LEVELS = SrcKeys::LEVELS, PAD = 0;
+    rs_queue_soa q;
+    RankKey* keys;
+    uint8_t* sched;
+    int calibrated, preemptive;
+    int* err;
+    __device__ __forceinline__ unsigned __int128 value(uint32_t i) const { return finish(load(i), i); }
+    // every column read unconditionally (no flags -> score dependency)
+    static constexpr int BATCH = 2;
+    struct Raw {
+        double score;
+        int32_t gen;
+        uint32_t rank;
+        uint8_t flags;
+    };
+    __device__ __forceinline__ Raw load(uint32_t i) const {
+        Raw r;
+        r.flags = q.flags[i];
+        r.score = q.score_dtype == RS_F32 ? (double)static_cast<const float*>(q.score)[i]
+                                          : static_cast<const double*>(q.score)[i];
+        r.gen = calibrated ? q.generated_tokens[i] : 0;
+        r.rank = q.arrival_rank[i];
+        return r;
+    }
+    __device__ __forceinline__ unsigned __int128 finish(const Raw& r, uint32_t i) const {
+        RankKey key;
+        if (r.flags & EX_DONE) {
+            key.eff = ~0ull;
+            key.cr = ~0u;
+        } else {
+            const bool scored = r.flags & RS_FLAG_SCORED;
+            const bool prio = r.flags & RS_FLAG_PRIORITY;
+            const bool running = r.flags & RS_FLAG_RUNNING;
+            double eff = 0.0;
+            if (scored) {
+                eff = calibrated ? r.score - (double)r.gen : r.score;
+                if (eff != eff) atomicOr(err, 1);
+            }
+            const uint32_t pin = preemptive ? 0u : (running ? 0u : 1u);
+            const uint32_t cls = (pin << 2) | ((scored ? 1u : 0u) << 1) | (prio ? 0u : 1u);
+            key.eff = orderable_f64(eff);
+            key.cr = (cls << RANK_BITS) | (r.rank & RANK_MASK);
+        }
+        key.pad = 0;
+        keys[i] = key;
+        sched[i] = 0;
+        return rank_key_value(key);
+    }
+};
+
 struct LoopMark {
     unsigned long long* prof;
     unsigned long long* t0;
@@ -1825,18 +2004,18 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
         soa.n = n;
         rs_engine_queue q = a.q[cur];
         q.n = n;
-        // the rank step's keys (build_rank_keys; finished rows rank last) and cleared batch flags
-        for (uint32_t i = blockIdx.x * SEL_THREADS + threadIdx.x; i < n; i += G) {
-            a.sched[i] = 0;
-            RankKey key;
-            if (soa.flags[i] & EX_DONE) {
-                key.eff = ~0ull;
-                key.cr = ~0u;
-                key.pad = 0;
-            } else {
-                key = rank_key_of(soa, i, a.calibrated, a.preemptive, a.counts + 3);
-            }
-            a.keys[i] = key;
+        // the rank step. One pass builds the keys and keeps every key below the threshold
+        // a previous step left (thr: the key then placed at rank k + ENGINE_SPEC_MARGIN).
+        // When that kept between k and 1024 keys they hold the k smallest (>= k keys lie
+        // below thr), so they are placed directly; otherwise the full select runs over the
+        // built keys, keeping k + ENGINE_SPEC_MARGIN keys, and resets thr. Exact either way.
+        const uint32_t k = min(n_alive, (uint32_t)a.max_batch);
+        {
+            const unsigned __int128 T = *(volatile unsigned __int128*)a.thr;
+            const SrcEngBuild src0{soa, a.keys, a.sched, a.calibrated, a.preemptive, a.counts + 3};
+            sel_rows_batch<SrcEngBuild::BATCH>(src0, n, [&](uint32_t i, unsigned __int128 v, bool ok) {
+                sel_append(ok && v < T, v, i, &a.sel->arrived, a.ck, a.ci, SEL_SORT);
+            });
         }
         sel_gsync<CL>(bar);
         mark(1);
@@ -1847,10 +2026,21 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
             }
             break;
         }
-        const uint32_t k = min(n_alive, (uint32_t)a.max_batch);
-        sel_fused_body<SrcKeys, CL>(SrcKeys{a.keys}, n, a.sel, a.pfx, a.hist, k, (uint32_t)SEL_CAP_SMALL, a.ck, a.ci,
-                                    bar, soa.id, a.run, a.sched, a.counts, soa, a.threshold, a.pquantum, nullptr,
-                                    nullptr, nullptr, nullptr, nullptr, nullptr, h, sk, sv, mark);
+        const uint32_t m = *(volatile uint32_t*)&a.sel->arrived;
+        if (m >= k && m <= 1024u) {
+            mark(21);
+            const bool reset = m > k + 2 * ENGINE_SPEC_MARGIN;  // too many below thr: lower it
+            sel_emit_rank(a.ck, a.ci, m, soa.id, k, a.run, a.sched, a.counts, sk, reset ? a.thr : nullptr,
+                          k + ENGINE_SPEC_MARGIN);
+            mark(16);
+        } else {
+            // (candidates <= ks + SEL_CAP_SMALL must fit the 1024-key emit)
+            const uint32_t ks = min(n_alive, max(k, min(k + ENGINE_SPEC_MARGIN, 1024u - SEL_CAP_SMALL)));
+            sel_fused_body<SrcKeys, CL, LoopMark>(SrcKeys{a.keys}, n, a.sel, a.pfx, a.hist, k, (uint32_t)SEL_CAP_SMALL,
+                                                  a.ck, a.ci, bar, soa.id, a.run, a.sched, a.counts, soa, a.threshold,
+                                                  a.pquantum, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, h,
+                                                  sk, sv, mark, (const SrcKeys*)nullptr, a.slices, ks, a.thr);
+        }
         sel_gsync<CL>(bar);  // the batch's sched flags are set
         mark(10);
         upd_rows_plain(soa, a.sched, n, a.threshold, a.pquantum);  // schedulers.py:224-240
@@ -2155,10 +2345,13 @@ int rs_engine_run_device(const rs_engine_queue* q2, const rs_queue_soa* soa2, co
     RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&fits), (size_t)n, st));
     RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dropped), (size_t)n * sizeof(int64_t), st));
     RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ls), sizeof(EngineLoopState) + sizeof(EngineLoopPub), st));
+    RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.slices), 2 * 16 * SEL_BINS * sizeof(uint32_t), st));
     a.fits = fits;
     a.dropped = dropped;
     a.ls = ls;
     a.pub = reinterpret_cast<EngineLoopPub*>(ls + 1);
+    RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.thr), sizeof(unsigned __int128), st));
+    RS_CUDA(cudaMemsetAsync(a.thr, 0xff, sizeof(unsigned __int128), st));
     RS_CUDA(cudaMemcpyAsync(fits, lp->fits, (size_t)n, cudaMemcpyHostToDevice, st));
     RS_CUDA(cudaMemsetAsync(ls, 0, sizeof(EngineLoopState) + sizeof(EngineLoopPub), st));
     RS_CUDA(cudaMemsetAsync(w.sel, 0, sizeof(SelState), st));
@@ -2167,7 +2360,7 @@ int rs_engine_run_device(const rs_engine_queue* q2, const rs_queue_soa* soa2, co
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     int ctas = ENGINE_LOOP_CTAS;
-    if (const char* e = getenv("RS_ENGINE_CTAS")) ctas = atoi(e);  // measurement experiments (<= 16)
+    if (const char* e = getenv("RS_ENGINE_CTAS")) ctas = std::min(16, std::max(1, atoi(e)));  // experiments
     if (ctas > 8) RS_CUDA(cudaFuncSetAttribute(engine_loop_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     at[0].val.clusterDim.x = ctas;
     at[0].val.clusterDim.y = 1;
@@ -2188,12 +2381,12 @@ int rs_engine_run_device(const rs_engine_queue* q2, const rs_queue_soa* soa2, co
         RS_CUDA(cudaMemcpyAsync(p, a.prof, sizeof(p), cudaMemcpyDeviceToHost, st));
         RS_CUDA(cudaStreamSynchronize(st));
         RS_CUDA(cudaFreeAsync(a.prof, st));
-        static const char* names[] = {"head", "keys", "", "", "", "", "execute", "compact", "gather",
+        static const char* names[] = {"head", "spec_pass", "", "", "", "", "execute", "compact", "gather",
                                       "gather_barrier", "emit_barrier", "update+bar", "level_pass", "level_bar1",
                                       "level_pick", "level_bar2", "emit"};
         for (int i = 0; i < 17; ++i)
             if (names[i][0]) fprintf(stderr, "engine_loop %-16s %10.3f ms\n", names[i], p[i] * 1e-6);
-        fprintf(stderr, "engine_loop levels %llu\n", p[20]);
+        fprintf(stderr, "engine_loop levels %llu fast steps %llu\n", p[20], p[21]);
     }
     EngineLoopState h{};
     RS_CUDA(cudaMemcpyAsync(&h, ls, sizeof(h), cudaMemcpyDeviceToHost, st));
@@ -2203,6 +2396,8 @@ int rs_engine_run_device(const rs_engine_queue* q2, const rs_queue_soa* soa2, co
     RS_CUDA(cudaFreeAsync(fits, st));
     RS_CUDA(cudaFreeAsync(dropped, st));
     RS_CUDA(cudaFreeAsync(ls, st));
+    RS_CUDA(cudaFreeAsync(a.slices, st));
+    RS_CUDA(cudaFreeAsync(a.thr, st));
     RS_CUDA(cudaStreamSynchronize(st));
     res->now_ns = h.now;
     res->steps = h.step;
