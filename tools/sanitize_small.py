@@ -6,7 +6,7 @@ attention forward (f16 V and bf16 V) and backward, LayerNorm / embedding / head,
 forward and rs_ranker_grad + Adam, classifier head + CE, ListMLE (order / lengths forms),
 tau counts (small-range y histogram path and the general merge path, 32- and 64-bit
 inputs), arrival rank + rank step (select and sort paths, KV budget), the device engine
-loop, the tokenizer and the linear bridge."""
+loop (the one-launch loop and the per-kernel steps), the tokenizer and the linear bridge."""
 
 from __future__ import annotations
 
@@ -102,6 +102,10 @@ def main(which: str = "all"):
         res = engine.run(list(trace), scores=list(np.random.default_rng(1).normal(size=len(trace))),
                          sched=schedulers.SchedulerConfig(max_batch=4), cost=engine.COST_PRESETS["unit"])
         assert res.metrics["n_finished"] == len(trace)
+        # the per-kernel step path too (record=True: admit / execute / compaction kernels)
+        rec = engine.DeviceEngine(list(trace), list(np.random.default_rng(1).normal(size=len(trace))),
+                                  schedulers.SchedulerConfig(max_batch=4), engine.COST_PRESETS["unit"]).run(record=True)
+        assert rec.metrics["n_finished"] == len(trace)
         prompt_token_ids_device(["a b c", "", "  hello   World ", "x " * 300], 16)
         wl = __import__("paper_2408_15792_b200.workload", fromlist=["x"])
         t = wl.generate_burst(120, wl.LengthDist.parse("sharegpt"), seed=1)
