@@ -1106,7 +1106,8 @@ __device__ __forceinline__ void sel_emit_rank(const unsigned __int128* __restric
                                               const uint32_t* __restrict__ ci, uint32_t n_cand,
                                               const int64_t* __restrict__ id, uint32_t k, int64_t* __restrict__ run,
                                               uint8_t* __restrict__ sched, int32_t* __restrict__ counts, uint4* sk,
-                                              unsigned __int128* thr = nullptr, uint32_t target = 0) {
+                                              unsigned __int128* thr = nullptr, uint32_t target = 0,
+                                              uint32_t* __restrict__ run_row = nullptr) {
     const uint32_t m = min(n_cand, 1024u), t = threadIdx.x;
     for (uint32_t i = t; i < m; i += blockDim.x) sk[i] = __ldcg(reinterpret_cast<const uint4*>(ck + i));
     if (blockIdx.x == 0 && t == 0) {
@@ -1133,6 +1134,7 @@ __device__ __forceinline__ void sel_emit_rank(const unsigned __int128* __restric
             const uint32_t row = __ldcg(ci + c);
             run[cnt] = id[row];
             sched[row] = 1;
+            if (run_row != nullptr) run_row[cnt] = row;
         }
         if (thr != nullptr && act && seg == 0 && cnt == target) {
             const uint4 kv = sk[c];
@@ -1556,7 +1558,8 @@ __device__ __forceinline__ void sel_fused_body(const Src& src, uint32_t n, SelSt
                                                int64_t* __restrict__ prom, int64_t* __restrict__ dem, uint32_t* h,
                                                uint4* sk, uint32_t* sv, const Mark& mark = Mark{},
                                                const Src0* src0 = nullptr, uint32_t* slices = nullptr,
-                                               uint32_t k_sel = 0, unsigned __int128* thr = nullptr) {
+                                               uint32_t k_sel = 0, unsigned __int128* thr = nullptr,
+                                               uint32_t* run_row = nullptr) {
     // k_sel (>= k, optional): the select keeps every key up to the k_sel-th (the emit still
     // places k); thr: see sel_emit_rank (target k_sel)
     if (k_sel < k) k_sel = k;
@@ -1620,7 +1623,7 @@ __device__ __forceinline__ void sel_fused_body(const Src& src, uint32_t n, SelSt
     mark(8);
     gsync();
     mark(9);
-    sel_emit_rank(ck, ci, *(volatile uint32_t*)&st->n_cand, id, k, run, sched, counts, sk, thr, k_sel);
+    sel_emit_rank(ck, ci, *(volatile uint32_t*)&st->n_cand, id, k, run, sched, counts, sk, thr, k_sel, run_row);
     mark(16);
     if (plist == nullptr) return;  // the state update runs as separate kernels (unaligned columns)
     // the state update (schedulers.py:224-240) and the ordered promoted / demoted lists:
@@ -1795,6 +1798,7 @@ struct EngineLoopArgs {
     int32_t* counts;   // int32[4]
     int64_t *run, *pre, *fin, *prev_run;
     int32_t *prev_n, *block_keep;
+    uint32_t* run_row;  // the batch's rows (int32[max_batch])
     SelState* sel;
     unsigned __int128* pfx;
     uint32_t* hist;
@@ -1956,6 +1960,106 @@ struct SrcEngBuild {
     }
 };
 
+// CTA 0 of the engine loop: _Sim.execute (engine.py:247-284) for the step's batch (run ids
+// and rows, n_run of them, sched[row] = 1 on them). Preemption (last step's batch rows
+// left out: prev_id / prev_row in shared memory, rows re-read through row_of after a
+// compaction) and the batch's prefill touch disjoint rows, so they run side by side
+// (threads 0..511 / 512..1023), every column the token phase needs loaded up front;
+// out: CTA 0's shared {now, iter, prefill, -, -, n_finished}.
+__device__ __forceinline__ void engine_execute_loop(const rs_engine_queue& q, const rs_engine_trace& tr,
+                                                    const rs_engine_cost& cost, const int64_t* __restrict__ run,
+                                                    const uint32_t* __restrict__ run_row, int n_run,
+                                                    const uint8_t* __restrict__ sched, int64_t predictor_ns,
+                                                    int64_t* out, int64_t* prev_id, uint32_t* prev_row, int& prev_n,
+                                                    bool prev_rows_ok, int* s_fin,
+                                                    unsigned long long* s_pf) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int pn = prev_n;
+    if (tid < pn) {
+        const int64_t id = prev_id[tid];
+        bool live = true;
+        uint32_t row;
+        if (prev_rows_ok) {
+            row = prev_row[tid];
+        } else {
+            live = tr.finish_ns[id] < 0;  // finished rows were compacted out
+            row = live ? (uint32_t)tr.row_of[id] : 0u;
+        }
+        if (live) {
+            const uint8_t fl = q.flags[row];
+            if (!(fl & EX_DONE) && (fl & RS_FLAG_RUNNING) && !sched[row]) {
+                q.flags[row] = (uint8_t)(fl & ~RS_FLAG_RUNNING);
+                tr.n_preempted[id] += 1;
+            }
+        }
+    }
+    const int kk = tid - EX_THREADS / 2;
+    const bool mine = kk >= 0 && kk < n_run;
+    int64_t id = 0, le = 0, mg = 0, ft = 0;
+    uint32_t row = 0;
+    uint8_t fl = 0;
+    int32_t gen = 0, to = 0;
+    unsigned long long pf = 0ull;
+    if (mine) {
+        id = run[kk];
+        row = run_row[kk];
+        fl = q.flags[row];
+        gen = q.generated_tokens[row];
+        const int32_t pr = q.prompt_tokens[row];
+        le = tr.last_event_ns[id];
+        mg = tr.max_gap_ns[id];
+        ft = tr.first_token_ns[id];
+        to = tr.true_output[id];
+        if (!(fl & RS_FLAG_RUNNING)) {  // prefill (engine.py:257-262)
+            pf = (unsigned long long)(pr + gen);
+            fl |= RS_FLAG_RUNNING;
+        }
+    }
+    pf = warp_sum(pf);
+    if (lane == 0 && pf) atomicAdd(s_pf, pf);
+    __syncthreads();
+    if (tid == 0) {  // the clock
+        long long dec;
+        if (cost.decode_table_len > 0) {
+            const int b = n_run < cost.decode_table_len ? n_run : cost.decode_table_len;
+            dec = cost.decode_table[b - 1];
+        } else {
+            dec = cost.decode_ns;
+        }
+        const long long pfn = (long long)*s_pf * cost.prefill_ns_per_token;
+        out[1] = pfn + dec + predictor_ns;
+        out[2] = pfn;
+        out[0] += out[1];
+    }
+    __syncthreads();
+    int fin = 0;
+    if (mine) {  // one token each (engine.py:270-280)
+        const long long now = out[0];
+        const int g = gen + 1;
+        q.generated_tokens[row] = g;
+        if (now - le > mg) tr.max_gap_ns[id] = now - le;
+        if (ft < 0) tr.first_token_ns[id] = now;
+        tr.last_event_ns[id] = now;
+        if (g >= to) {
+            tr.finish_ns[id] = now;
+            fl |= EX_DONE;
+            fin = 1;
+        }
+        q.flags[row] = fl;
+        prev_id[kk] = id;
+        prev_row[kk] = row;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, fin);
+    if (lane == 0 && b) atomicAdd(s_fin, __popc(b));
+    __syncthreads();
+    if (tid == 0) {
+        out[5] = *s_fin;
+        prev_n = n_run;
+        *s_fin = 0;
+        *s_pf = 0ull;
+    }
+}
+
 struct LoopMark {
     unsigned long long* prof;
     unsigned long long* t0;
@@ -1980,6 +2084,11 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
     __shared__ long long s_base;
     __shared__ EngineLoopState S;  // CTA 0's
     __shared__ int64_t s_out[6];  // CTA 0's execute results (rs_engine_execute's out_dev)
+    __shared__ int64_t s_prev_id[EX_THREADS / 2];  // CTA 0: last step's batch
+    __shared__ uint32_t s_prev_row[EX_THREADS / 2];
+    __shared__ int s_prev_n, s_fin;
+    __shared__ unsigned long long s_pf;
+    __shared__ bool s_prev_ok;
     static_assert(sizeof(sk) >= EX_PRE_CAP * sizeof(int), "pre_rows scratch");
     uint32_t* bar = &a.sel->bar_count;
     volatile EngineLoopPub* pub = a.pub;
@@ -1990,6 +2099,10 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         S = EngineLoopState{};
         s_out[0] = 0;
+        s_prev_n = 0;
+        s_fin = 0;
+        s_pf = 0ull;
+        s_prev_ok = true;
     }
     __syncthreads();
     for (int cur = 0;;) {
@@ -2031,7 +2144,7 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
             mark(21);
             const bool reset = m > k + 2 * ENGINE_SPEC_MARGIN;  // too many below thr: lower it
             sel_emit_rank(a.ck, a.ci, m, soa.id, k, a.run, a.sched, a.counts, sk, reset ? a.thr : nullptr,
-                          k + ENGINE_SPEC_MARGIN);
+                          k + ENGINE_SPEC_MARGIN, a.run_row);
             mark(16);
         } else {
             // (candidates <= ks + SEL_CAP_SMALL must fit the 1024-key emit)
@@ -2039,7 +2152,8 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
             sel_fused_body<SrcKeys, CL, LoopMark>(SrcKeys{a.keys}, n, a.sel, a.pfx, a.hist, k, (uint32_t)SEL_CAP_SMALL,
                                                   a.ck, a.ci, bar, soa.id, a.run, a.sched, a.counts, soa, a.threshold,
                                                   a.pquantum, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, h,
-                                                  sk, sv, mark, (const SrcKeys*)nullptr, a.slices, ks, a.thr);
+                                                  sk, sv, mark, (const SrcKeys*)nullptr, a.slices, ks, a.thr,
+                                                  a.run_row);
         }
         sel_gsync<CL>(bar);  // the batch's sched flags are set
         mark(10);
@@ -2047,9 +2161,10 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
         sel_gsync<CL>(bar);
         mark(11);
         if (blockIdx.x == 0) {
-            engine_execute_block<false, false>(q, a.tr, a.cost, a.run, a.counts, step, S.pred, s_out, a.pre, a.fin,
-                                               a.prev_run, a.prev_n, reinterpret_cast<int*>(sk), warp_tot);
-            if (threadIdx.x == 0) {  // compaction once the finished rows are an eighth of the rows
+            engine_execute_loop(q, a.tr, a.cost, a.run, a.run_row, (int)k, a.sched, S.pred, s_out, s_prev_id,
+                                s_prev_row, s_prev_n, s_prev_ok, &s_fin, &s_pf);
+            if (threadIdx.x == 0) {
+                s_prev_ok = true;  // compaction once the finished rows are an eighth of the rows
                 const int64_t live = S.n_alive - s_out[5];
                 pub->live = live;
                 pub->compact = (int64_t)(n - live) * 8 >= (int64_t)n ? 1 : 0;
@@ -2075,7 +2190,10 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
             __syncthreads();
             compact_scatter_chunk(q, a.q[cur ^ 1], a.tr, c, s_base, warp_tot);
         }
-        if (blockIdx.x == 0 && threadIdx.x == 0) S.n_rows = live;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            S.n_rows = live;
+            s_prev_ok = false;  // rows moved: the next preemption pass finds them through row_of
+        }
         cur ^= 1;
         sel_gsync<CL>(bar);
         mark(7);
@@ -2351,6 +2469,7 @@ int rs_engine_run_device(const rs_engine_queue* q2, const rs_queue_soa* soa2, co
     a.ls = ls;
     a.pub = reinterpret_cast<EngineLoopPub*>(ls + 1);
     RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.thr), sizeof(unsigned __int128), st));
+    RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.run_row), 1024 * sizeof(uint32_t), st));
     RS_CUDA(cudaMemsetAsync(a.thr, 0xff, sizeof(unsigned __int128), st));
     RS_CUDA(cudaMemcpyAsync(fits, lp->fits, (size_t)n, cudaMemcpyHostToDevice, st));
     RS_CUDA(cudaMemsetAsync(ls, 0, sizeof(EngineLoopState) + sizeof(EngineLoopPub), st));
@@ -2398,6 +2517,7 @@ int rs_engine_run_device(const rs_engine_queue* q2, const rs_queue_soa* soa2, co
     RS_CUDA(cudaFreeAsync(ls, st));
     RS_CUDA(cudaFreeAsync(a.slices, st));
     RS_CUDA(cudaFreeAsync(a.thr, st));
+    RS_CUDA(cudaFreeAsync(a.run_row, st));
     RS_CUDA(cudaStreamSynchronize(st));
     res->now_ns = h.now;
     res->steps = h.step;
