@@ -1731,7 +1731,8 @@ struct RankSizer {
 
 // The state update alone (no promoted / demoted lists), grid-stride over 4-row groups
 // (flags 4-B, starvation / quantum 16-B aligned: the engine's columns).
-__device__ __forceinline__ void upd_rows_plain(const rs_queue_soa& q, const uint8_t* __restrict__ sched, uint32_t n,
+// The batch flags are cleared on the way (the engine loop's next key pass needs them zero).
+__device__ __forceinline__ void upd_rows_plain(const rs_queue_soa& q, uint8_t* __restrict__ sched, uint32_t n,
                                                int32_t threshold, int32_t pquantum) {
     const uint32_t n4 = n & ~3u, G = gridDim.x * blockDim.x;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) * 4u; i < n4; i += 4u * G) {
@@ -1750,6 +1751,7 @@ __device__ __forceinline__ void upd_rows_plain(const rs_queue_soa& q, const uint
         *reinterpret_cast<uint32_t*>(q.flags + i) = nf;
         *reinterpret_cast<int4*>(q.starvation + i) = make_int4(sa[0], sa[1], sa[2], sa[3]);
         *reinterpret_cast<int4*>(q.quantum + i) = make_int4(qa[0], qa[1], qa[2], qa[3]);
+        if (sw) *reinterpret_cast<uint32_t*>(sched + i) = 0u;
     }
     const uint32_t r = n4 + blockIdx.x * blockDim.x + threadIdx.x;
     if (r < n) {
@@ -1759,6 +1761,7 @@ __device__ __forceinline__ void upd_rows_plain(const rs_queue_soa& q, const uint
         q.flags[r] = f;
         q.starvation[r] = st;
         q.quantum[r] = qu;
+        sched[r] = 0;
     }
 }
 
@@ -1905,60 +1908,103 @@ __device__ void engine_loop_head(const EngineLoopArgs& a, EngineLoopState& S, in
     __syncthreads();  // (s_first / warp_tot reuse)
 }
 
-// The engine loop's level-0 source: builds each row's 96-bit key from the queue columns
-// (build_rank_keys; finished rows get the all-ones key, after every live row), stores it
-// for the later levels (SrcKeys) and clears the row's batch flag.
+// One row's sort-key value (build_rank_keys, as SrcKeys reads it back) from its columns;
+// finished rows (EX_DONE, left in place by the engine loop) get all ones, after every live row.
+__device__ __forceinline__ RankKey eng_key(uint8_t f, double score, int32_t gen, uint32_t rank, int calibrated,
+                                           int preemptive, int* err) {
+    RankKey key;
+    key.pad = 0;
+    if (f & EX_DONE) {
+        key.eff = ~0ull;
+        key.cr = ~0u;
+        return key;
+    }
+    const bool scored = f & RS_FLAG_SCORED;
+    const bool prio = f & RS_FLAG_PRIORITY;
+    const bool running = f & RS_FLAG_RUNNING;
+    double eff = 0.0;
+    if (scored) {
+        eff = calibrated ? score - (double)gen : score;
+        if (eff != eff) atomicOr(err, 1);
+    }
+    const uint32_t pin = preemptive ? 0u : (running ? 0u : 1u);
+    const uint32_t cls = (pin << 2) | ((scored ? 1u : 0u) << 1) | (prio ? 0u : 1u);
+    key.eff = orderable_f64(eff);
+    key.cr = (cls << RANK_BITS) | (rank & RANK_MASK);
+    return key;
+}
+// The keys stored for SrcKeys (the engine loop's full-select fallback).
 struct SrcEngBuild {
     using V = unsigned __int128;
     static constexpr int BITS = SrcKeys::BITS, LEVELS = SrcKeys::LEVELS, PAD = 0;
     rs_queue_soa q;
     RankKey* keys;
-    uint8_t* sched;
     int calibrated, preemptive;
     int* err;
-    __device__ __forceinline__ unsigned __int128 value(uint32_t i) const { return finish(load(i), i); }
-    // every column read unconditionally (no flags -> score dependency)
-    static constexpr int BATCH = 2;
-    struct Raw {
-        double score;
-        int32_t gen;
-        uint32_t rank;
-        uint8_t flags;
-    };
-    __device__ __forceinline__ Raw load(uint32_t i) const {
-        Raw r;
-        r.flags = q.flags[i];
-        r.score = q.score_dtype == RS_F32 ? (double)static_cast<const float*>(q.score)[i]
-                                          : static_cast<const double*>(q.score)[i];
-        r.gen = calibrated ? q.generated_tokens[i] : 0;
-        r.rank = q.arrival_rank[i];
-        return r;
-    }
-    __device__ __forceinline__ unsigned __int128 finish(const Raw& r, uint32_t i) const {
-        RankKey key;
-        if (r.flags & EX_DONE) {
-            key.eff = ~0ull;
-            key.cr = ~0u;
-        } else {
-            const bool scored = r.flags & RS_FLAG_SCORED;
-            const bool prio = r.flags & RS_FLAG_PRIORITY;
-            const bool running = r.flags & RS_FLAG_RUNNING;
-            double eff = 0.0;
-            if (scored) {
-                eff = calibrated ? r.score - (double)r.gen : r.score;
-                if (eff != eff) atomicOr(err, 1);
-            }
-            const uint32_t pin = preemptive ? 0u : (running ? 0u : 1u);
-            const uint32_t cls = (pin << 2) | ((scored ? 1u : 0u) << 1) | (prio ? 0u : 1u);
-            key.eff = orderable_f64(eff);
-            key.cr = (cls << RANK_BITS) | (r.rank & RANK_MASK);
-        }
-        key.pad = 0;
+    __device__ __forceinline__ unsigned __int128 value(uint32_t i) const {
+        const double sc = q.score_dtype == RS_F32 ? (double)static_cast<const float*>(q.score)[i]
+                                                  : static_cast<const double*>(q.score)[i];
+        const RankKey key = eng_key(q.flags[i], sc, calibrated ? q.generated_tokens[i] : 0, q.arrival_rank[i],
+                                    calibrated, preemptive, err);
         keys[i] = key;
-        sched[i] = 0;
         return rank_key_value(key);
     }
 };
+// The engine loop's speculative pass: every row whose key lies below T appended to (ck, ci)
+// (count in *cnt). Four consecutive rows per lane, 16-B column loads (f64 scores, arrival
+// ranks, generated tokens) — the engine's columns are 16-B aligned.
+__device__ __forceinline__ void eng_spec_pass(const rs_queue_soa& q, uint32_t n, unsigned __int128 T, int calibrated,
+                                              int preemptive, int* err, uint32_t* cnt,
+                                              unsigned __int128* __restrict__ ck, uint32_t* __restrict__ ci) {
+    const uint32_t n4 = n & ~3u, lane = threadIdx.x & 31u, G4 = gridDim.x * SEL_THREADS * 4u;
+    const bool f64 = q.score_dtype == RS_F64;
+    for (uint32_t base = (blockIdx.x * SEL_THREADS + (threadIdx.x & ~31u)) * 4u; base < n4; base += G4) {
+        const uint32_t i = base + lane * 4u;
+        const bool ok = i < n4;
+        uint32_t fw = 0;
+        uint4 rk = make_uint4(0, 0, 0, 0);
+        int4 ge = make_int4(0, 0, 0, 0);
+        double sc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (ok) {
+            fw = *reinterpret_cast<const uint32_t*>(q.flags + i);
+            rk = *reinterpret_cast<const uint4*>(q.arrival_rank + i);
+            if (calibrated) ge = *reinterpret_cast<const int4*>(q.generated_tokens + i);
+            if (f64) {
+                const double2 a = *reinterpret_cast<const double2*>(static_cast<const double*>(q.score) + i);
+                const double2 b = *reinterpret_cast<const double2*>(static_cast<const double*>(q.score) + i + 2);
+                sc[0] = a.x;
+                sc[1] = a.y;
+                sc[2] = b.x;
+                sc[3] = b.y;
+            } else {
+                const float4 a = *reinterpret_cast<const float4*>(static_cast<const float*>(q.score) + i);
+                sc[0] = a.x;
+                sc[1] = a.y;
+                sc[2] = a.z;
+                sc[3] = a.w;
+            }
+        }
+        const uint32_t ra[4] = {rk.x, rk.y, rk.z, rk.w};
+        const int32_t ga[4] = {ge.x, ge.y, ge.z, ge.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const unsigned __int128 v =
+                rank_key_value(eng_key((uint8_t)(fw >> (8 * j)), sc[j], ga[j], ra[j], calibrated, preemptive, err));
+            sel_append(ok && v < T, v, i + j, cnt, ck, ci, SEL_SORT);
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 32) {  // the last n % 4 rows
+        const uint32_t i = n4 + lane;
+        const bool ok = i < n;
+        unsigned __int128 v = 0;
+        if (ok) {
+            const double s = f64 ? static_cast<const double*>(q.score)[i] : (double)static_cast<const float*>(q.score)[i];
+            v = rank_key_value(eng_key(q.flags[i], s, calibrated ? q.generated_tokens[i] : 0, q.arrival_rank[i],
+                                       calibrated, preemptive, err));
+        }
+        sel_append(ok && v < T, v, i, cnt, ck, ci, SEL_SORT);
+    }
+}
 
 // CTA 0 of the engine loop: _Sim.execute (engine.py:247-284) for the step's batch (run ids
 // and rows, n_run of them, sched[row] = 1 on them). Preemption (last step's batch rows
@@ -2123,13 +2169,8 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
         // below thr), so they are placed directly; otherwise the full select runs over the
         // built keys, keeping k + ENGINE_SPEC_MARGIN keys, and resets thr. Exact either way.
         const uint32_t k = min(n_alive, (uint32_t)a.max_batch);
-        {
-            const unsigned __int128 T = *(volatile unsigned __int128*)a.thr;
-            const SrcEngBuild src0{soa, a.keys, a.sched, a.calibrated, a.preemptive, a.counts + 3};
-            sel_rows_batch<SrcEngBuild::BATCH>(src0, n, [&](uint32_t i, unsigned __int128 v, bool ok) {
-                sel_append(ok && v < T, v, i, &a.sel->arrived, a.ck, a.ci, SEL_SORT);
-            });
-        }
+        eng_spec_pass(soa, n, *(volatile unsigned __int128*)a.thr, a.calibrated, a.preemptive, a.counts + 3,
+                      &a.sel->arrived, a.ck, a.ci);
         sel_gsync<CL>(bar);
         mark(1);
         if (*(volatile int32_t*)(a.counts + 3)) {  // NaN effective score: every CTA sees it
@@ -2147,6 +2188,9 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
                           k + ENGINE_SPEC_MARGIN, a.run_row);
             mark(16);
         } else {
+            const SrcEngBuild kb{soa, a.keys, a.calibrated, a.preemptive, a.counts + 3};
+            for (uint32_t i = blockIdx.x * SEL_THREADS + threadIdx.x; i < n; i += G) kb.value(i);
+            sel_gsync<CL>(bar);
             // (candidates <= ks + SEL_CAP_SMALL must fit the 1024-key emit)
             const uint32_t ks = min(n_alive, max(k, min(k + ENGINE_SPEC_MARGIN, 1024u - SEL_CAP_SMALL)));
             sel_fused_body<SrcKeys, CL, LoopMark>(SrcKeys{a.keys}, n, a.sel, a.pfx, a.hist, k, (uint32_t)SEL_CAP_SMALL,
@@ -2155,11 +2199,11 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
                                                   sk, sv, mark, (const SrcKeys*)nullptr, a.slices, ks, a.thr,
                                                   a.run_row);
         }
-        sel_gsync<CL>(bar);  // the batch's sched flags are set
+        sel_gsync<CL>(bar);  // the batch (run, run_row, sched) is set
         mark(10);
-        upd_rows_plain(soa, a.sched, n, a.threshold, a.pquantum);  // schedulers.py:224-240
-        sel_gsync<CL>(bar);
-        mark(11);
+        // execute, then the state update (schedulers.py:224-240): independent (the update
+        // touches the priority bit, starvation and quantum, execute the running / done bits
+        // and generated tokens), but both write flag bytes; the update clears sched
         if (blockIdx.x == 0) {
             engine_execute_loop(q, a.tr, a.cost, a.run, a.run_row, (int)k, a.sched, S.pred, s_out, s_prev_id,
                                 s_prev_row, s_prev_n, s_prev_ok, &s_fin, &s_pf);
@@ -2172,7 +2216,10 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
         }
         sel_gsync<CL>(bar);
         mark(6);
+        upd_rows_plain(soa, a.sched, n, a.threshold, a.pquantum);  // (admission, next, appends past n)
+        mark(11);
         if (!pub->compact) continue;
+        sel_gsync<CL>(bar);
         const uint32_t live = (uint32_t)pub->live;
         const uint32_t nb = (n + EX_THREADS - 1) / EX_THREADS;
         for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
@@ -2298,6 +2345,7 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         RS_CUDA(cudaMemsetAsync(w.sel, 0, sizeof(SelState), st));
         RS_CUDA(cudaMemsetAsync(w.pfx, 0, sizeof(unsigned __int128), st));
         RS_CUDA(cudaMemsetAsync(w.hist, 0, SEL_BINS * sizeof(uint32_t), st));
+    RS_CUDA(cudaMemsetAsync(w.sched, 0, (size_t)n, st));  // kept zero between steps by the update
         const uint32_t gb = min((n / 4 + SEL_THREADS) / SEL_THREADS, (uint32_t)num_sms() * 2);
         // (measured: at 2^20 rows the multi-launch select below is faster, 68 vs 82 us as a
         // CUDA graph — the grid barriers over 148 CTAs cost more than the launches they save)
@@ -2417,10 +2465,12 @@ int rs_engine_run_device(const rs_engine_queue* q2, const rs_queue_soa* soa2, co
     if (!engine_loop_device_enabled() || lp->kv_budget >= 0 || n <= 0 || n > (int64_t)RANK_MASK ||
         lp->max_batch + SEL_CAP_SMALL > 1024 || lp->ws_bytes < rs_rank_step_workspace_size(n))
         return RS_OK;
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < 2; ++c) {  // the vector column accesses (eng_spec_pass, upd_rows_plain)
         const rs_queue_soa& s = soa2[c];
         if ((reinterpret_cast<uintptr_t>(s.flags) & 3u) ||
-            ((reinterpret_cast<uintptr_t>(s.starvation) | reinterpret_cast<uintptr_t>(s.quantum)) & 15u))
+            ((reinterpret_cast<uintptr_t>(s.starvation) | reinterpret_cast<uintptr_t>(s.quantum) |
+              reinterpret_cast<uintptr_t>(s.score) | reinterpret_cast<uintptr_t>(s.arrival_rank) |
+              reinterpret_cast<uintptr_t>(s.generated_tokens)) & 15u))
             return RS_OK;
     }
     *handled = true;
@@ -2475,6 +2525,7 @@ int rs_engine_run_device(const rs_engine_queue* q2, const rs_queue_soa* soa2, co
     RS_CUDA(cudaMemsetAsync(ls, 0, sizeof(EngineLoopState) + sizeof(EngineLoopPub), st));
     RS_CUDA(cudaMemsetAsync(w.sel, 0, sizeof(SelState), st));
     RS_CUDA(cudaMemsetAsync(w.hist, 0, SEL_BINS * sizeof(uint32_t), st));
+    RS_CUDA(cudaMemsetAsync(w.sched, 0, (size_t)n, st));  // kept zero between steps by the update
     cudaLaunchConfig_t lc{};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
