@@ -1778,7 +1778,8 @@ __device__ __forceinline__ void upd_rows_plain(const rs_queue_soa& q, uint8_t* _
 // sort key carries the arrival rank; only the per-step id lists, not written here, follow
 // row order), so the decisions are the per-kernel host loop's — tests/test_gpu_engine.py
 // checks both against the reference.
-constexpr int ENGINE_LOOP_CTAS = 8;  // one portable cluster
+constexpr int ENGINE_LOOP_CTAS = 8;        // one portable cluster
+constexpr int ENGINE_LOOP_CTAS_WIDE = 16;  // non-portable, where the device can place it
 constexpr uint32_t ENGINE_SPEC_MARGIN = 256;  // speculative threshold: rank k + this
 // CTA 0's loop state (shared memory; copied to global memory for the host at the end)
 struct EngineLoopState {
@@ -1807,6 +1808,7 @@ struct EngineLoopArgs {
     uint32_t* hist;
     uint32_t* slices;  // 2 x grid x SEL_BINS words
     unsigned __int128* thr;  // speculative select threshold (all ones at the start)
+    uint32_t margin;         // ENGINE_SPEC_MARGIN (RS_ENGINE_MARGIN overrides: experiments)
     unsigned __int128* ck;
     uint32_t* ci;
     RankKey* keys;
@@ -2183,16 +2185,16 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
         const uint32_t m = *(volatile uint32_t*)&a.sel->arrived;
         if (m >= k && m <= 1024u) {
             mark(21);
-            const bool reset = m > k + 2 * ENGINE_SPEC_MARGIN;  // too many below thr: lower it
+            const bool reset = m > k + 2 * a.margin;  // too many below thr: lower it
             sel_emit_rank(a.ck, a.ci, m, soa.id, k, a.run, a.sched, a.counts, sk, reset ? a.thr : nullptr,
-                          k + ENGINE_SPEC_MARGIN, a.run_row);
+                          k + a.margin, a.run_row);
             mark(16);
         } else {
             const SrcEngBuild kb{soa, a.keys, a.calibrated, a.preemptive, a.counts + 3};
             for (uint32_t i = blockIdx.x * SEL_THREADS + threadIdx.x; i < n; i += G) kb.value(i);
             sel_gsync<CL>(bar);
             // (candidates <= ks + SEL_CAP_SMALL must fit the 1024-key emit)
-            const uint32_t ks = min(n_alive, max(k, min(k + ENGINE_SPEC_MARGIN, 1024u - SEL_CAP_SMALL)));
+            const uint32_t ks = min(n_alive, max(k, min(k + a.margin, 1024u - SEL_CAP_SMALL)));
             sel_fused_body<SrcKeys, CL, LoopMark>(SrcKeys{a.keys}, n, a.sel, a.pfx, a.hist, k, (uint32_t)SEL_CAP_SMALL,
                                                   a.ck, a.ci, bar, soa.id, a.run, a.sched, a.counts, soa, a.threshold,
                                                   a.pquantum, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, h,
@@ -2499,6 +2501,8 @@ int rs_engine_run_device(const rs_engine_queue* q2, const rs_queue_soa* soa2, co
     a.ci = w.ci;
     a.keys = w.kb;
     a.sched = w.sched;
+    a.margin = ENGINE_SPEC_MARGIN;
+    if (const char* e = getenv("RS_ENGINE_MARGIN")) a.margin = (uint32_t)std::min(512, std::max(1, atoi(e)));
     a.max_batch = lp->max_batch;
     a.threshold = lp->starvation_threshold;
     a.pquantum = lp->priority_quantum;
@@ -2529,17 +2533,27 @@ int rs_engine_run_device(const rs_engine_queue* q2, const rs_queue_soa* soa2, co
     cudaLaunchConfig_t lc{};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    int ctas = ENGINE_LOOP_CTAS;
-    if (const char* e = getenv("RS_ENGINE_CTAS")) ctas = std::min(16, std::max(1, atoi(e)));  // experiments
-    if (ctas > 8) RS_CUDA(cudaFuncSetAttribute(engine_loop_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    at[0].val.clusterDim.x = ctas;
+    // 16 CTAs (a non-portable cluster: measured 18.0 vs 20.6 us per cfg5 step with 8) when
+    // the device can place one, else the portable 8; RS_ENGINE_CTAS overrides (experiments)
+    int ctas = ENGINE_LOOP_CTAS_WIDE;
+    if (const char* e = getenv("RS_ENGINE_CTAS")) ctas = std::min(16, std::max(1, atoi(e)));
+    RS_CUDA(cudaFuncSetAttribute(engine_loop_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
-    lc.gridDim = dim3(ctas);
     lc.blockDim = dim3(SEL_THREADS);
     lc.stream = st;
     lc.attrs = at;
     lc.numAttrs = 1;
+    for (;;) {
+        at[0].val.clusterDim.x = ctas;
+        lc.gridDim = dim3(ctas);
+        int fit = 0;
+        if (ctas <= ENGINE_LOOP_CTAS ||
+            (cudaOccupancyMaxActiveClusters(&fit, engine_loop_kernel<true>, &lc) == cudaSuccess && fit >= 1))
+            break;
+        (void)cudaGetLastError();
+        ctas = ENGINE_LOOP_CTAS;
+    }
     const bool prof = getenv("RS_ENGINE_PROF") != nullptr;
     if (prof) {
         RS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&a.prof), 32 * sizeof(unsigned long long), st));
