@@ -328,7 +328,8 @@ def engine_metric(args, world, rank, pk):
     ranker is a pure function of the prompt), then rank 0 runs the engine loop
     (admission, ranking-policy step with starvation bump, execute, retirement) on the device
     (paper_2408_15792_b200.engine) with max_batch 256, threshold 100, quantum 50, the
-    default cost preset. Wall clock of scoring + loop (the loop syncs once per step)."""
+    default cost preset. Wall clock of scoring + loop (the whole loop is one cluster launch:
+    rs_engine_run's device path, csrc/rankstep.cu engine_loop_kernel)."""
     from paper_2408_15792_b200 import dp, engine
     from paper_2408_15792_b200.ranker import OptRanker, RankerConfig
     from paper_2408_15792_b200.schedulers import SchedulerConfig
