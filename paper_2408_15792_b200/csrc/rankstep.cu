@@ -156,6 +156,11 @@ constexpr int SEL_SORT = 4096;  // >= max_batch + SEL_CAP, power of two
 // launches) beats the select's SEL_LEVELS histogram launches + gather + final sort: the
 // engine loop's queues (10^3-10^5 rows) are all below it, cfg4's 1M queue is above.
 constexpr uint32_t SEL_MIN_N_DEFAULT = 1u << 11;
+// environment overrides of the select's crossovers (measurement experiments)
+static uint32_t env_u32(const char* name, uint32_t dflt) {
+    const char* e = getenv(name);
+    return e ? (uint32_t)strtoul(e, nullptr, 10) : dflt;
+}
 // RS_SEL_MIN_N overrides the crossover (measurement experiments)
 static uint32_t sel_min_n() {
     static const uint32_t v = [] {
@@ -2347,11 +2352,10 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
         RS_CUDA(cudaMemsetAsync(w.sel, 0, sizeof(SelState), st));
         RS_CUDA(cudaMemsetAsync(w.pfx, 0, sizeof(unsigned __int128), st));
         RS_CUDA(cudaMemsetAsync(w.hist, 0, SEL_BINS * sizeof(uint32_t), st));
-    RS_CUDA(cudaMemsetAsync(w.sched, 0, (size_t)n, st));  // kept zero between steps by the update
         const uint32_t gb = min((n / 4 + SEL_THREADS) / SEL_THREADS, (uint32_t)num_sms() * 2);
         // (measured: at 2^20 rows the multi-launch select below is faster, 68 vs 82 us as a
         // CUDA graph — the grid barriers over 148 CTAs cost more than the launches they save)
-        const bool fused = n <= SEL_FUSED_N && k + SEL_CAP_SMALL <= 1024;
+        const bool fused = n <= env_u32("RS_SEL_FUSED_N", SEL_FUSED_N) && k + SEL_CAP_SMALL <= 1024;
         fused_update = fused && vec;
         const uint32_t unblk = (n + UPV_CHUNK - 1) / UPV_CHUNK;
         uint32_t* f_plist = fused_update ? reinterpret_cast<uint32_t*>(w.va) : nullptr;
@@ -2361,9 +2365,16 @@ extern "C" int rs_rank_step(const rs_queue_soa* q, int32_t max_batch, int64_t kv
             // one launch: levels, picks, gather, the candidates' sort and the state update;
             // up to SEL_CLUSTER_N rows the grid is one cluster of <= 8 CTAs (hardware
             // barriers), above it a cooperative grid with global-memory barriers
-            const bool cl = n <= SEL_CLUSTER_N;
+            const bool cl = n <= env_u32("RS_SEL_CLUSTER_N", SEL_CLUSTER_N);
             // cooperative: one 1024-thread CTA per SM at most (register file)
-            const uint32_t grid = cl ? min(gb, 8u) : min(gb, (uint32_t)num_sms());
+            const uint32_t csz = min(env_u32("RS_SEL_CLUSTER", 8u), 16u);  // (experiments: 16 non-portable)
+            const uint32_t grid = cl ? min(gb, csz) : min(gb, (uint32_t)num_sms());
+            if (cl && grid > 8) {
+                if (soa64)
+                    RS_CUDA(cudaFuncSetAttribute(sel_fused<SrcSoa64, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                else
+                    RS_CUDA(cudaFuncSetAttribute(sel_fused<SrcKeys, true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            }
             cudaLaunchConfig_t lc{};
             cudaLaunchAttribute at[1];
             if (cl) {
