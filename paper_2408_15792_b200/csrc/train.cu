@@ -236,6 +236,38 @@ __global__ void reduce_slices_add_kernel(const float* __restrict__ part, int k, 
 // Embedding backward over tokens sorted by id (order[] = token index, keys[] = id):
 // the warp at the start of each run of equal ids sums the run's rows in order and adds
 // the total to dE[id] -- each dE row is written by exactly one warp.
+// DPL = d / 32 columns per lane, held in registers: the run's rows are walked once (each
+// row's DPL loads independent, the run's row indices fetched 32 at a time), same order of
+// additions per column as the generic kernel below.
+template <int DPL>
+__global__ void embed_bwd_tok_regs_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ order, int n,
+                                          const float* __restrict__ dh, float* __restrict__ dE) {
+    constexpr int d = DPL * 32;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const uint32_t id = keys[i];
+    if (i > 0 && keys[i - 1] == id) return;
+    float acc[DPL];
+#pragma unroll
+    for (int k = 0; k < DPL; ++k) acc[k] = 0.f;
+    for (int j0 = i; j0 < n; j0 += 32) {
+        const int j = j0 + lane;
+        const bool in = j < n && keys[j] == id;
+        const unsigned run = __ballot_sync(0xffffffffu, in);
+        const int len = __popc(run) == 32 ? 32 : __ffs(~run) - 1;  // the run continues only while contiguous
+        const uint32_t row = in ? order[j] : 0u;
+        for (int r = 0; r < len; ++r) {
+            const float* src = dh + (size_t)__shfl_sync(0xffffffffu, row, r) * d + lane;
+#pragma unroll
+            for (int k = 0; k < DPL; ++k) acc[k] += src[32 * k];
+        }
+        if (len < 32) break;
+    }
+    float* dst = dE + (size_t)id * d + lane;
+#pragma unroll
+    for (int k = 0; k < DPL; ++k) dst[32 * k] += acc[k];
+}
 __global__ void embed_bwd_tok_kernel(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ order, int n,
                                      const float* __restrict__ dh, int d, float* __restrict__ dE) {
     const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -249,13 +281,25 @@ __global__ void embed_bwd_tok_kernel(const uint32_t* __restrict__ keys, const ui
         dE[(size_t)id * d + c] += acc;
     }
 }
-// Position-embedding backward: dP[p + 2] += sum over prompts of dh[b * S + p] (fixed order).
-__global__ void embed_bwd_pos_kernel(const float* __restrict__ dh, int B, int S, int d, float* __restrict__ dP) {
-    const int p = blockIdx.x;
-    for (int c = threadIdx.x; c < d; c += blockDim.x) {
-        float acc = 0.f;
-        for (int b = 0; b < B; ++b) acc += dh[((size_t)b * S + p) * d + c];
-        dP[(size_t)(p + 2) * d + c] += acc;
+// Position-embedding backward: dP[p + 2] += sum over prompts of dh[b * S + p] (fixed order:
+// EBP_G interleaved partial sums per column, then added in group order). Block (32 columns,
+// EBP_G prompt groups) per (position, 32-column slice): S x d / 32 blocks instead of S, so
+// the pass streams dh at HBM speed (one block per position had left it latency-bound).
+constexpr int EBP_G = 8;
+__global__ void __launch_bounds__(32 * EBP_G) embed_bwd_pos_kernel(const float* __restrict__ dh, int B, int S, int d,
+                                                                   float* __restrict__ dP) {
+    __shared__ float part[EBP_G][33];
+    const int p = blockIdx.x, c = blockIdx.y * 32 + threadIdx.x, g = threadIdx.y;
+    float acc = 0.f;
+    if (c < d)
+        for (int b = g; b < B; b += EBP_G) acc += dh[((size_t)b * S + p) * d + c];
+    part[g][threadIdx.x] = acc;
+    __syncthreads();
+    if (g == 0 && c < d) {
+        float s = part[0][threadIdx.x];
+#pragma unroll
+        for (int k = 1; k < EBP_G; ++k) s += part[k][threadIdx.x];
+        dP[(size_t)(p + 2) * d + c] += s;
     }
 }
 __global__ void ids_to_keys_kernel(const int32_t* __restrict__ ids, int n, int vocab, uint32_t* __restrict__ keys) {
@@ -430,9 +474,14 @@ int embed_backward(const int32_t* ids, int B, int S, int vocab, const float* dh,
     RS_LAUNCH_CHECK();
     uint32_t *sk, *sv;
     RS_TRY((merge_sort<uint32_t, true, false>(keys, nullptr, n, k0, k1, v0, v1, nullptr, st, &sk, &sv, splits)));
-    embed_bwd_tok_kernel<<<(n + 7) / 8, 256, 0, st>>>(sk, sv, n, dh, d, dE);
+    switch (d) {
+        case 256: embed_bwd_tok_regs_kernel<8><<<(n + 7) / 8, 256, 0, st>>>(sk, sv, n, dh, dE); break;
+        case 512: embed_bwd_tok_regs_kernel<16><<<(n + 7) / 8, 256, 0, st>>>(sk, sv, n, dh, dE); break;
+        case 768: embed_bwd_tok_regs_kernel<24><<<(n + 7) / 8, 256, 0, st>>>(sk, sv, n, dh, dE); break;
+        default: embed_bwd_tok_kernel<<<(n + 7) / 8, 256, 0, st>>>(sk, sv, n, dh, d, dE); break;
+    }
     RS_LAUNCH_CHECK();
-    embed_bwd_pos_kernel<<<S, 256, 0, st>>>(dh, B, S, d, dP);
+    embed_bwd_pos_kernel<<<dim3(S, (d + 31) / 32), dim3(32, EBP_G), 0, st>>>(dh, B, S, d, dP);
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
