@@ -186,8 +186,8 @@ __global__ void reduce_rows_add_kernel(const float* __restrict__ part, int n_par
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= cols) return;
     float acc = 0.f;
-#pragma unroll 8
-    for (int p = 0; p < n_part; ++p) acc += part[(size_t)p * ld + c];
+#pragma unroll 32
+    for (int p = 0; p < n_part; ++p) acc += part[(size_t)p * ld + c];  // (32 loads in flight, same order)
     out[c] += acc;
 }
 
