@@ -341,6 +341,11 @@ int rs_attention_fwd(const void* qkv_dev, void* out_dev, int32_t B, int32_t S, i
                      void* stream);
 int rs_attention_fwd_f16v(const void* qkv_dev, void* out_dev, int32_t B, int32_t S, int32_t H,
                           void* stream);
+/* rs_attention_fwd that also writes each row's log2-sum-exp of the scaled scores,
+ * lse_dev[(b * H + h) * S + row] (fp32; P = 2^(s / 8 * log2 e - lse)) for
+ * rs_attention_bwd_lse (the ranker's training forward). */
+int rs_attention_fwd_lse(const void* qkv_dev, void* out_dev, float* lse_dev, int32_t B, int32_t S, int32_t H,
+                         void* stream);
 /* General CTA-pair GEMM used by the backward pass: a_mn / b_mn = operand stored
  * MN-contiguous ([K, M] / [K, N]); epi 4 = fp32 out, 5 = bf16 out * (aux > 0) (ReLU
  * backward, aux bf16 [M, N]), 6 = fp32 split-K partials (C holds k_splits x [M, N]).
@@ -352,6 +357,10 @@ int rs_gemm_bf16_ex(const void* A_dev, const void* W_dev, const void* bias_dev, 
  * qkv, its output att [B*S, H*64] and dout = d loss / d att. */
 int rs_attention_bwd(const void* qkv_dev, const void* att_dev, const void* dout_dev, void* dqkv_dev, int32_t B,
                      int32_t S, int32_t H, void* stream);
+/* The same given the forward's lse (rs_attention_fwd_lse): P in one pass, no row max /
+ * sum recompute (S <= 128). */
+int rs_attention_bwd_lse(const void* qkv_dev, const void* att_dev, const void* dout_dev, const float* lse_dev,
+                         void* dqkv_dev, int32_t B, int32_t S, int32_t H, void* stream);
 /* Causal attention backward for 128 < S <= 512 (128-token blocks: a dQ kernel that also
  * writes each row's log-sum-exp and rowsum(dO * O) into the workspace, then a dK / dV
  * kernel); same layouts as rs_attention_bwd. */

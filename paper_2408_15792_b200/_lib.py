@@ -125,6 +125,8 @@ SIGNATURES = {
     "rs_adam_step": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.c_float, ctypes.c_float,
                                     ctypes.c_float, ctypes.c_float, c_i64, ctypes.c_float, c_vp]),
     "rs_attention_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
+    "rs_attention_fwd_lse": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
+    "rs_attention_bwd_lse": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "rs_attention_bwd_long_workspace_size": (c_sz, [c_i32, c_i32, c_i32]),
     "rs_attention_bwd_long": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_sz, c_vp]),
     "rs_linear_n_params": (c_i64, [c_i32, c_i32]),

@@ -154,7 +154,7 @@ __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_
 template <bool F16V>
 __global__ void __launch_bounds__(AT_THREADS, 1)
     attention_fwd_kernel(const __grid_constant__ CUtensorMap tqkv, __nv_bfloat16* __restrict__ out, int B, int S,
-                         int H) {
+                         int H, float* __restrict__ lse) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;                  // [slot][2]
@@ -466,6 +466,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
                 tc_fence_before();
                 const float inv = 1.f / l;
                 const int qi = t * AT_TILE + r;
+                // the row's log2-sum-exp (scaled scores): P = 2^(s c - lse) for the backward
+                if (lse != nullptr && qi < S) lse[((size_t)b * H + h) * S + qi] = m_run + __log2f(l);
                 if (qi < S) {
                     uint4* o4 = reinterpret_cast<uint4*>(out + ((size_t)b * S + qi) * dm + h * AT_D);
 #pragma unroll
@@ -485,7 +487,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1)
 }
 
 template <bool F16V>
-static int launch_attention(const void* qkv, void* out, int B, int S, int H, cudaStream_t st) {
+static int launch_attention(const void* qkv, void* out, int B, int S, int H, cudaStream_t st, float* lse) {
     const int sms = num_sms();
     RS_CUDA(ensure_smem((const void*)attention_fwd_kernel<F16V>, AT_SMEM));
     const uint64_t rows = (uint64_t)B * S;
@@ -496,15 +498,21 @@ static int launch_attention(const void* qkv, void* out, int B, int S, int H, cud
     const int gU = AT_MAXKB / n_qt;
     const int n_groups = (B * H + gU - 1) / gU;
     const int grid = n_groups < sms ? n_groups : sms;
-    attention_fwd_kernel<F16V><<<grid, AT_THREADS, AT_SMEM, st>>>(m, static_cast<__nv_bfloat16*>(out), B, S, H);
+    attention_fwd_kernel<F16V><<<grid, AT_THREADS, AT_SMEM, st>>>(m, static_cast<__nv_bfloat16*>(out), B, S, H, lse);
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
 
-int attention_fwd_impl(const void* qkv, void* out, int B, int S, int H, int v_f16, cudaStream_t st) {
+int attention_fwd_impl(const void* qkv, void* out, int B, int S, int H, int v_f16, cudaStream_t st,
+                       float* lse = nullptr) {
     RS_CHECK_ARG(B > 0 && S > 0 && H > 0, "attention: empty shape");
     RS_CHECK_ARG(S <= AT_TILE * AT_MAXKB, "attention: S=%d > %d not supported", S, AT_TILE * AT_MAXKB);
-    return v_f16 ? launch_attention<true>(qkv, out, B, S, H, st) : launch_attention<false>(qkv, out, B, S, H, st);
+    return v_f16 ? launch_attention<true>(qkv, out, B, S, H, st, lse)
+                 : launch_attention<false>(qkv, out, B, S, H, st, lse);
+}
+// the training forward: also the rows' log2-sum-exp, lse[(b H + h) S + row] (fp32)
+int attention_fwd_lse(const void* qkv, void* out, float* lse, int B, int S, int H, cudaStream_t st) {
+    return attention_fwd_impl(qkv, out, B, S, H, 0, st, lse);
 }
 
 int attention_fwd(const void* qkv, void* out, int B, int S, int H, cudaStream_t st) {
@@ -524,4 +532,11 @@ extern "C" int rs_attention_fwd(const void* qkv, void* out, int32_t B, int32_t S
 extern "C" int rs_attention_fwd_f16v(const void* qkv, void* out, int32_t B, int32_t S, int32_t H, void* stream) {
     RS_NVTX();
     return rs::attention_fwd_f16v(qkv, out, B, S, H, rs::as_stream(stream));
+}
+
+extern "C" int rs_attention_fwd_lse(const void* qkv, void* out, float* lse, int32_t B, int32_t S, int32_t H,
+                                    void* stream) {
+    RS_NVTX();
+    RS_CHECK_ARG(lse != nullptr, "rs_attention_fwd_lse: lse is NULL");
+    return rs::attention_fwd_lse(qkv, out, lse, B, S, H, rs::as_stream(stream));
 }

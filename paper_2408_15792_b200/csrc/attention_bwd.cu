@@ -21,7 +21,8 @@ using namespace sm100;
 constexpr int AB_T = 128, AB_D = 64;
 constexpr int AB_TILE_BYTES = AB_T * AB_D * 2;  // 16 KB
 constexpr int AB_SQ_BYTES = AB_T * AB_T * 2;    // 32 KB (P or dS)
-constexpr int AB_THREADS = 192;
+constexpr int AB_THREADS = 192;       // TMA warp, MMA warp, 4 softmax warps (one query row each)
+constexpr int AB_THREADS_LSE = 320;   // with the forward's LSE: 8 softmax warps, two per row (64 keys each)
 // Two CTAs per SM (each CTA is a serial load -> MMA -> softmax -> MMA -> store chain, so a
 // second resident CTA overlaps one's phases with the other's): 112 KB of tiles and 256
 // TMEM columns each. V is dead once S / dP are computed and O once D is, so dS reuses V's
@@ -40,16 +41,14 @@ __device__ __forceinline__ float ab_exp2(float x) {
     return y;
 }
 
-// element (row, c) of a 128-row x 64-col bf16 tile stored K-major SW128 by TMA
-__device__ __forceinline__ float tile_elem(const uint8_t* tile, int row, int c) {
-    const int off = row * 128 + ((((c >> 3) ^ (row & 7)) << 4)) + (c & 7) * 2;
-    return __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(tile + off));
-}
-
-__global__ void __launch_bounds__(AB_THREADS, 2)
+// LSE: the forward's row log2-sum-exp is given (lse[(b H + h) S + row]), so P comes from S
+// in one pass with no row max / sum, and two warps share each row (key halves): half the
+// per-thread softmax work on the CTA's serial chain.
+template <bool LSE>
+__global__ void __launch_bounds__(LSE ? AB_THREADS_LSE : AB_THREADS, 2)
     attention_bwd_kernel(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tatt,
                          const __grid_constant__ CUtensorMap tdo, __nv_bfloat16* __restrict__ dqkv, int B, int S,
-                         int H) {
+                         int H, const float* __restrict__ lse) {
     // the SW128 tiles need 1024-B alignment; dynamic shared memory of a kernel without
     // static shared memory starts at the window base (checked, not padded: padding would
     // push two CTAs past the SM's 228 KB)
@@ -74,7 +73,7 @@ __global__ void __launch_bounds__(AB_THREADS, 2)
         tma_prefetch_desc(&tqkv);
         mbar_init(&bar->load_full, 1);
         mbar_init(&bar->s_full, 1);
-        mbar_init(&bar->p_full, 4);
+        mbar_init(&bar->p_full, LSE ? 8 : 4);
         mbar_init(&bar->g_full, 1);
         fence_barrier_init();
     }
@@ -125,6 +124,88 @@ __global__ void __launch_bounds__(AB_THREADS, 2)
             }
             mma_commit(&bar->g_full);
         }
+    } else if (LSE) {
+        const int q4 = warp & 3, half = (warp - 2) >> 2;  // TMEM lane quadrant; key half
+        const int r = q4 * 32 + lane;
+        const uint32_t la = (uint32_t)(q4 * 32) << 16;
+        const float c = 0.125f * 1.4426950408889634f;
+        const int nvalid = min(S, AB_T);
+        const bool row_ok = r < nvalid;
+        const int lim = row_ok ? r : -1;
+        const float ls = row_ok ? lse[((size_t)b * H + h) * S + r] : 0.f;
+        mbar_wait(&bar->load_full, 0);
+        float Dr = 0.f;  // D = rowsum(dO * O), both halves (16-B chunks of the SW128 tiles)
+#pragma unroll
+        for (int ch = 0; ch < AB_D / 8; ++ch) {
+            const int off = r * 128 + ((ch ^ (r & 7)) << 4);
+            const uint4 a = *reinterpret_cast<const uint4*>(sdO + off);
+            const uint4 o = *reinterpret_cast<const uint4*>(sO + off);
+            const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 af = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&aw[q]));
+                const float2 of = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[q]));
+                Dr += af.x * of.x;
+                Dr += af.y * of.y;
+            }
+        }
+        // P is written over O: both halves of every row have read O first (named barrier
+        // over the 8 softmax warps)
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        mbar_wait(&bar->s_full, 0);
+        tc_fence_after();
+        // keys [64 half, 64 half + 64) of the row; a key half entirely past the diagonal
+        // of this warp's rows is P = dS = 0 without reading S
+#pragma unroll 1
+        for (int cc = half * 64; cc < half * 64 + 64; cc += 32) {
+            uint32_t v[32], dp[32];
+            tmem_ld_32x32b_x32(tS + la + cc, v);
+            tmem_ld_32x32b_x32(tdP + la + cc, dp);
+            tmem_ld_wait();
+            uint32_t pk[16], dk[16];
+#pragma unroll
+            for (int e = 0; e < 32; e += 2) {
+                const float p0 = (cc + e <= lim) ? ab_exp2(__uint_as_float(v[e]) * c - ls) : 0.f;
+                const float p1 = (cc + e + 1 <= lim) ? ab_exp2(__uint_as_float(v[e + 1]) * c - ls) : 0.f;
+                const float s0 = p0 * (__uint_as_float(dp[e]) - Dr) * 0.125f;
+                const float s1 = p1 * (__uint_as_float(dp[e + 1]) - Dr) * 0.125f;
+                pk[e / 2] = pack_bf16(p0, p1);
+                dk[e / 2] = pack_bf16(s0, s1);
+            }
+            const int off = (cc >> 6) * (AB_T * 128) + r * 128;
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const int ch = ((cc & 63) >> 3) + qq;
+                *reinterpret_cast<uint4*>(sP + off + ((ch ^ (r & 7)) << 4)) =
+                    make_uint4(pk[4 * qq], pk[4 * qq + 1], pk[4 * qq + 2], pk[4 * qq + 3]);
+                *reinterpret_cast<uint4*>(sdS + off + ((ch ^ (r & 7)) << 4)) =
+                    make_uint4(dk[4 * qq], dk[4 * qq + 1], dk[4 * qq + 2], dk[4 * qq + 3]);
+            }
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar->p_full);
+        mbar_wait(&bar->g_full, 0);
+        tc_fence_after();
+        {  // this half's 32 of the 64 columns of dQ, dK, dV
+            __nv_bfloat16* base = dqkv + (size_t)(row0 + r) * 3 * dm + h * AB_D + half * 32;
+            const uint32_t src[3] = {tdQ, tdK, tdV};
+#pragma unroll
+            for (int which = 0; which < 3; ++which) {
+                uint32_t a0[32];
+                tmem_ld_32x32b_x32(src[which] + la + half * 32, a0);
+                tmem_ld_wait();
+                if (!row_ok) continue;
+                uint4* o4 = reinterpret_cast<uint4*>(base + which * dm);
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq)
+                    o4[qq] = make_uint4(pack_bf16(__uint_as_float(a0[8 * qq]), __uint_as_float(a0[8 * qq + 1])),
+                                        pack_bf16(__uint_as_float(a0[8 * qq + 2]), __uint_as_float(a0[8 * qq + 3])),
+                                        pack_bf16(__uint_as_float(a0[8 * qq + 4]), __uint_as_float(a0[8 * qq + 5])),
+                                        pack_bf16(__uint_as_float(a0[8 * qq + 6]), __uint_as_float(a0[8 * qq + 7])));
+            }
+        }
     } else {
         const int q4 = warp & 3;
         const int r = q4 * 32 + lane;  // query row (S, dP, dQ) / key row (dK, dV) == TMEM lane
@@ -134,10 +215,23 @@ __global__ void __launch_bounds__(AB_THREADS, 2)
         const bool row_ok = r < nvalid;
         const int lim = row_ok ? r : -1;  // causal: key kk valid iff kk <= lim
         mbar_wait(&bar->load_full, 0);
-        // D = rowsum(dO * O)
+        // D = rowsum(dO * O): the row's eight 16-B chunks of each tile (SW128: chunk ch of
+        // row r at (ch ^ (r & 7)) * 16), same order of products as element by element
         float Dr = 0.f;
-#pragma unroll 8
-        for (int cc = 0; cc < AB_D; ++cc) Dr += tile_elem(sdO, r, cc) * tile_elem(sO, r, cc);
+#pragma unroll
+        for (int ch = 0; ch < AB_D / 8; ++ch) {
+            const int off = r * 128 + ((ch ^ (r & 7)) << 4);
+            const uint4 a = *reinterpret_cast<const uint4*>(sdO + off);
+            const uint4 o = *reinterpret_cast<const uint4*>(sO + off);
+            const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 af = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&aw[q]));
+                const float2 of = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ow[q]));
+                Dr += af.x * of.x;
+                Dr += af.y * of.y;
+            }
+        }
         mbar_wait(&bar->s_full, 0);
         tc_fence_after();
         uint32_t v[32];
@@ -225,18 +319,25 @@ __global__ void __launch_bounds__(AB_THREADS, 2)
     if (warp == 1) tmem_dealloc<256>(tmem);
 }
 
-int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv, int B, int S, int H, cudaStream_t st) {
+int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv, int B, int S, int H, cudaStream_t st,
+                  const float* lse) {
     RS_CHECK_ARG(B > 0 && S > 0 && H > 0, "attention_bwd: empty shape");
     RS_CHECK_ARG(S <= AB_T, "attention_bwd: S=%d > 128 not supported yet (training uses S <= 128)", S);
-    RS_CUDA(ensure_smem((const void*)attention_bwd_kernel, AB_SMEM));
-    RS_CUDA(cudaFuncSetAttribute(attention_bwd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    const void* kfn = lse ? (const void*)attention_bwd_kernel<true> : (const void*)attention_bwd_kernel<false>;
+    RS_CUDA(ensure_smem(kfn, AB_SMEM));
+    RS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     const uint64_t rows = (uint64_t)B * S;
     const uint64_t dmc = (uint64_t)H * AB_D;
     CUtensorMap mq, ma, md;
     RS_TRY(make_tmap_bf16(&mq, qkv, rows, 3 * dmc, 3 * dmc * 2, AB_T, AB_D));
     RS_TRY(make_tmap_bf16(&ma, att, rows, dmc, dmc * 2, AB_T, AB_D));
     RS_TRY(make_tmap_bf16(&md, dout, rows, dmc, dmc * 2, AB_T, AB_D));
-    attention_bwd_kernel<<<B * H, AB_THREADS, AB_SMEM, st>>>(mq, ma, md, static_cast<__nv_bfloat16*>(dqkv), B, S, H);
+    if (lse)
+        attention_bwd_kernel<true><<<B * H, AB_THREADS_LSE, AB_SMEM, st>>>(mq, ma, md, static_cast<__nv_bfloat16*>(dqkv),
+                                                                           B, S, H, lse);
+    else
+        attention_bwd_kernel<false><<<B * H, AB_THREADS, AB_SMEM, st>>>(mq, ma, md, static_cast<__nv_bfloat16*>(dqkv),
+                                                                        B, S, H, nullptr);
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
@@ -246,5 +347,12 @@ int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv
 extern "C" int rs_attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv, int32_t B, int32_t S,
                                 int32_t H, void* stream) {
     RS_NVTX();
-    return rs::attention_bwd(qkv, att, dout, dqkv, B, S, H, rs::as_stream(stream));
+    return rs::attention_bwd(qkv, att, dout, dqkv, B, S, H, rs::as_stream(stream), nullptr);
+}
+
+extern "C" int rs_attention_bwd_lse(const void* qkv, const void* att, const void* dout, const float* lse, void* dqkv,
+                                    int32_t B, int32_t S, int32_t H, void* stream) {
+    RS_NVTX();
+    RS_CHECK_ARG(lse != nullptr, "rs_attention_bwd_lse: lse is NULL");
+    return rs::attention_bwd(qkv, att, dout, dqkv, B, S, H, rs::as_stream(stream), lse);
 }

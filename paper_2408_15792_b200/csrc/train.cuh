@@ -21,5 +21,6 @@ int embed_backward(const int32_t* ids, int B, int S, int vocab, const float* dh,
 int head_backward(const float* h, const int32_t* last, int B, int S, const void* lw, const void* lb, const void* hw,
                   const float* dg, float* dh, float* part, int d, float* g_hw, float* g_lnf, float* g_hb,
                   cudaStream_t st, const float* dfeat = nullptr);
-int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv, int B, int S, int H, cudaStream_t st);
+int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv, int B, int S, int H, cudaStream_t st,
+                  const float* lse = nullptr);
 }  // namespace rs
