@@ -48,7 +48,7 @@ template <bool LSE>
 __global__ void __launch_bounds__(LSE ? AB_THREADS_LSE : AB_THREADS, 2)
     attention_bwd_kernel(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tatt,
                          const __grid_constant__ CUtensorMap tdo, __nv_bfloat16* __restrict__ dqkv, int B, int S,
-                         int H, const float* __restrict__ lse) {
+                         int H, const float* __restrict__ lse, float* __restrict__ colsum) {
     // the SW128 tiles need 1024-B alignment; dynamic shared memory of a kernel without
     // static shared memory starts at the window base (checked, not padded: padding would
     // push two CTAs past the SM's 228 KB)
@@ -191,19 +191,56 @@ __global__ void __launch_bounds__(LSE ? AB_THREADS_LSE : AB_THREADS, 2)
         {  // this half's 32 of the 64 columns of dQ, dK, dV
             __nv_bfloat16* base = dqkv + (size_t)(row0 + r) * 3 * dm + h * AB_D + half * 32;
             const uint32_t src[3] = {tdQ, tdK, tdV};
+            // colsum (optional): the prompt's column sums of the bf16 dQ | dK | dV (the
+            // q / k / v bias gradients' share of this prompt): each warp's 32 rows summed
+            // by a register transpose-reduction, the four row quadrants in fixed order
+            // through shared memory (Q's tile: every MMA has completed)
+            float* red = reinterpret_cast<float*>(sQ);  // [3][4 quadrants][2 halves][32]
 #pragma unroll
             for (int which = 0; which < 3; ++which) {
                 uint32_t a0[32];
                 tmem_ld_32x32b_x32(src[which] + la + half * 32, a0);
                 tmem_ld_wait();
-                if (!row_ok) continue;
-                uint4* o4 = reinterpret_cast<uint4*>(base + which * dm);
+                uint32_t pk[16];
 #pragma unroll
-                for (int qq = 0; qq < 4; ++qq)
-                    o4[qq] = make_uint4(pack_bf16(__uint_as_float(a0[8 * qq]), __uint_as_float(a0[8 * qq + 1])),
-                                        pack_bf16(__uint_as_float(a0[8 * qq + 2]), __uint_as_float(a0[8 * qq + 3])),
-                                        pack_bf16(__uint_as_float(a0[8 * qq + 4]), __uint_as_float(a0[8 * qq + 5])),
-                                        pack_bf16(__uint_as_float(a0[8 * qq + 6]), __uint_as_float(a0[8 * qq + 7])));
+                for (int e = 0; e < 16; ++e) pk[e] = pack_bf16(__uint_as_float(a0[2 * e]), __uint_as_float(a0[2 * e + 1]));
+                if (row_ok) {
+                    uint4* o4 = reinterpret_cast<uint4*>(base + which * dm);
+#pragma unroll
+                    for (int qq = 0; qq < 4; ++qq) o4[qq] = make_uint4(pk[4 * qq], pk[4 * qq + 1], pk[4 * qq + 2], pk[4 * qq + 3]);
+                }
+                if (colsum != nullptr) {
+                    float v[32];
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pk[e]));
+                        v[2 * e] = row_ok ? f.x : 0.f;
+                        v[2 * e + 1] = row_ok ? f.y : 0.f;
+                    }
+                    // lane j ends with the sum over the warp's rows of column j
+#pragma unroll
+                    for (int o = 16; o >= 1; o >>= 1) {
+                        const bool up = (lane & o) != 0;
+#pragma unroll
+                        for (int i = 0; i < o; ++i) {
+                            const float send = up ? v[i] : v[i + o];
+                            const float keep = up ? v[i + o] : v[i];
+                            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                        }
+                    }
+                    red[((which * 4 + q4) * 2 + half) * 32 + lane] = v[0];
+                }
+            }
+            if (colsum != nullptr) {
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (q4 == 0) {
+#pragma unroll
+                    for (int which = 0; which < 3; ++which) {
+                        const float* rr = red + (which * 4 * 2 + half) * 32 + lane;
+                        colsum[(size_t)b * 3 * dm + which * dm + h * AB_D + half * 32 + lane] =
+                            ((rr[0] + rr[64]) + rr[128]) + rr[192];
+                    }
+                }
             }
         }
     } else {
@@ -320,7 +357,7 @@ __global__ void __launch_bounds__(LSE ? AB_THREADS_LSE : AB_THREADS, 2)
 }
 
 int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv, int B, int S, int H, cudaStream_t st,
-                  const float* lse) {
+                  const float* lse, float* colsum) {
     RS_CHECK_ARG(B > 0 && S > 0 && H > 0, "attention_bwd: empty shape");
     RS_CHECK_ARG(S <= AB_T, "attention_bwd: S=%d > 128 not supported yet (training uses S <= 128)", S);
     const void* kfn = lse ? (const void*)attention_bwd_kernel<true> : (const void*)attention_bwd_kernel<false>;
@@ -334,10 +371,10 @@ int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv
     RS_TRY(make_tmap_bf16(&md, dout, rows, dmc, dmc * 2, AB_T, AB_D));
     if (lse)
         attention_bwd_kernel<true><<<B * H, AB_THREADS_LSE, AB_SMEM, st>>>(mq, ma, md, static_cast<__nv_bfloat16*>(dqkv),
-                                                                           B, S, H, lse);
+                                                                           B, S, H, lse, colsum);
     else
         attention_bwd_kernel<false><<<B * H, AB_THREADS, AB_SMEM, st>>>(mq, ma, md, static_cast<__nv_bfloat16*>(dqkv),
-                                                                        B, S, H, nullptr);
+                                                                        B, S, H, nullptr, nullptr);
     RS_LAUNCH_CHECK();
     return RS_OK;
 }
@@ -347,12 +384,12 @@ int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv
 extern "C" int rs_attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv, int32_t B, int32_t S,
                                 int32_t H, void* stream) {
     RS_NVTX();
-    return rs::attention_bwd(qkv, att, dout, dqkv, B, S, H, rs::as_stream(stream), nullptr);
+    return rs::attention_bwd(qkv, att, dout, dqkv, B, S, H, rs::as_stream(stream), nullptr, nullptr);
 }
 
 extern "C" int rs_attention_bwd_lse(const void* qkv, const void* att, const void* dout, const float* lse, void* dqkv,
                                     int32_t B, int32_t S, int32_t H, void* stream) {
     RS_NVTX();
     RS_CHECK_ARG(lse != nullptr, "rs_attention_bwd_lse: lse is NULL");
-    return rs::attention_bwd(qkv, att, dout, dqkv, B, S, H, rs::as_stream(stream), lse);
+    return rs::attention_bwd(qkv, att, dout, dqkv, B, S, H, rs::as_stream(stream), lse, nullptr);
 }

@@ -207,15 +207,17 @@ static int train_backward(const rs_ranker_config* cfg, const __nv_bfloat16* P16,
         RS_TRY(gemm_bf16_ex(w.dh16, w.att[l], nullptr, nullptr, w.wpart, d, d, T, 6, 1, 1, sp, st));
         RS_TRY(slices_add(w.wpart, sp, (int64_t)d * d, grad + off(OFF_OUT_W, l), st));
         RS_TRY(gemm_bf16_ex(w.dh16, P16 + off(OFF_OUT_W, l), nullptr, nullptr, w.da, T, d, d, 0, 0, 1, 1, st));
-        if (S <= 128)
-            RS_TRY(attention_bwd(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, st, w.lse[l]));
-        else
+        if (S <= 128) {  // (+ the QKV bias gradient's per-prompt column sums, reduced here)
+            RS_TRY(attention_bwd(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, st, w.lse[l], w.rpart));
+            RS_TRY(rows_add(w.rpart, P, 3 * d, grad + off(OFF_QKV_B, l), w.rpart + (size_t)P * 3 * d, st));
+        } else {
             RS_TRY(attention_bwd_long(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, w.abw, w.abw_bytes, st));
+        }
         // QKV: qkv = x1 Wqkv^T + b
         sp = wgrad_splits(3 * d, d, T);
         RS_TRY(gemm_bf16_ex(w.dqkv, w.x1[l], nullptr, nullptr, w.wpart, 3 * d, d, T, 6, 1, 1, sp, st));
         RS_TRY(slices_add(w.wpart, sp, (int64_t)3 * d * d, grad + off(OFF_QKV_W, l), st));
-        RS_TRY(colsum_add(w.dqkv, true, n_tok, 3 * d, w.rpart, grad + off(OFF_QKV_B, l), st));
+        if (S > 128) RS_TRY(colsum_add(w.dqkv, true, n_tok, 3 * d, w.rpart, grad + off(OFF_QKV_B, l), st));
         RS_TRY(gemm_bf16_ex(w.dqkv, P16 + off(OFF_QKV_W, l), nullptr, nullptr, w.dx, T, d, 3 * d, 4, 0, 1, 1, st));
         RS_TRY(ln_backward(w.dx, w.h_in[l], P16 + off(OFF_LN1_W, l), w.dh, w.dh16, w.rpart, n_tok, d,
                            grad + off(OFF_LN1_W, l), nullptr, st, l > 0 ? grad + off(OFF_FC2_B, l - 1) : nullptr));

@@ -423,6 +423,10 @@ int ln_backward(const float* dy, const float* x, const void* w, float* dh, void*
     return RS_OK;
 }
 
+int rows_add(const float* part, int n_part, int cols, float* out, float* scratch, cudaStream_t st) {
+    return reduce_rows_add(part, n_part, cols, out, scratch, st);
+}
+
 int colsum_add(const void* x, bool is_bf16, int rows, int cols, float* part, float* out, cudaStream_t st) {
     const int nblk = (rows + TR_ROWS_PER_BLOCK - 1) / TR_ROWS_PER_BLOCK;
     RS_CHECK_ARG(cols % 8 == 0, "colsum_add: cols %% 8 != 0");

@@ -21,6 +21,10 @@ int embed_backward(const int32_t* ids, int B, int S, int vocab, const float* dh,
 int head_backward(const float* h, const int32_t* last, int B, int S, const void* lw, const void* lb, const void* hw,
                   const float* dg, float* dh, float* part, int d, float* g_hw, float* g_lnf, float* g_hb,
                   cudaStream_t st, const float* dfeat = nullptr);
+// lse: the forward's row log2-sum-exp (attention_fwd_lse); colsum (needs lse): B x 3 H 64
+// floats, row b = the column sums of prompt b's dQ | dK | dV rows (the bias gradients)
 int attention_bwd(const void* qkv, const void* att, const void* dout, void* dqkv, int B, int S, int H, cudaStream_t st,
-                  const float* lse = nullptr);
+                  const float* lse = nullptr, float* colsum = nullptr);
+// out[c] += sum of the n_part rows of part (fixed order); scratch: ceil(n_part / 16) x cols
+int rows_add(const float* part, int n_part, int cols, float* out, float* scratch, cudaStream_t st);
 }  // namespace rs
