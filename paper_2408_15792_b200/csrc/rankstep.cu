@@ -1770,6 +1770,45 @@ __device__ __forceinline__ void upd_rows_plain(const rs_queue_soa& q, uint8_t* _
     }
 }
 
+// The engine loop's state update on CTAs 1 .. gridDim.x - 1 while CTA 0 executes: the
+// priority bit flipped with word atomics (execute sets / clears other bits of the same
+// bytes), starvation / quantum stored as before; the batch flags stay (CTA 0 clears them
+// at the next step's start).
+__device__ __forceinline__ void upd_rows_loop(const rs_queue_soa& q, const uint8_t* __restrict__ sched, uint32_t n,
+                                              int32_t threshold, int32_t pquantum) {
+    const uint32_t n4 = n & ~3u, parts = gridDim.x - 1, part = blockIdx.x - 1;
+    const uint32_t G = parts * blockDim.x;
+    for (uint32_t i = (part * blockDim.x + threadIdx.x) * 4u; i < n4; i += 4u * G) {
+        const uint32_t fw = *reinterpret_cast<const volatile uint32_t*>(q.flags + i);
+        const uint32_t sw = *reinterpret_cast<const uint32_t*>(sched + i);
+        const int4 st = *reinterpret_cast<const int4*>(q.starvation + i);
+        const int4 qu = *reinterpret_cast<const int4*>(q.quantum + i);
+        int32_t sa[4] = {st.x, st.y, st.z, st.w}, qa[4] = {qu.x, qu.y, qu.z, qu.w};
+        uint32_t delta = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint8_t f = (uint8_t)(fw >> (8 * k));
+            const uint8_t f0 = f;
+            upd_row(f, sa[k], qa[k], (sw >> (8 * k)) & 0xffu, threshold, pquantum);
+            delta |= (uint32_t)((f ^ f0) & RS_FLAG_PRIORITY) << (8 * k);
+        }
+        if (delta) atomicXor(reinterpret_cast<unsigned int*>(q.flags + i), delta);
+        *reinterpret_cast<int4*>(q.starvation + i) = make_int4(sa[0], sa[1], sa[2], sa[3]);
+        *reinterpret_cast<int4*>(q.quantum + i) = make_int4(qa[0], qa[1], qa[2], qa[3]);
+    }
+    const uint32_t r = n4 + part * blockDim.x + threadIdx.x;
+    if (r < n) {
+        uint8_t f = *reinterpret_cast<const volatile uint8_t*>(q.flags + r);
+        const uint8_t f0 = f;
+        int32_t st = q.starvation[r], qu = q.quantum[r];
+        upd_row(f, st, qu, sched[r], threshold, pquantum);
+        if ((f ^ f0) & RS_FLAG_PRIORITY)
+            atomicXor(reinterpret_cast<unsigned int*>(q.flags + (r & ~3u)), (unsigned int)RS_FLAG_PRIORITY << (8 * (r & 3u)));
+        q.starvation[r] = st;
+        q.quantum[r] = qu;
+    }
+}
+
 // ---- the whole engine loop as one launch (record-free runs, unlimited KV budget) -------
 // engine.py:382-460 step for step, on one thread-block cluster: CTA 0 does the bookkeeping
 // the host loop did (idle jump, admission of the arrivals up to `now` in arrival order,
@@ -1910,6 +1949,9 @@ __device__ void engine_loop_head(const EngineLoopArgs& a, EngineLoopState& S, in
             pub->n_rows = S.n_rows;
             pub->n_alive = S.n_alive;
             pub->step = S.step;
+            // compaction (this step, before its key pass) once the finished rows are an eighth
+            pub->live = S.n_alive;
+            pub->compact = (S.n_rows - S.n_alive) * 8 >= S.n_rows ? 1 : 0;
         }
     }
     __syncthreads();  // (s_first / warp_tot reuse)
@@ -2013,6 +2055,15 @@ __device__ __forceinline__ void eng_spec_pass(const rs_queue_soa& q, uint32_t n,
     }
 }
 
+// Flag bits set / cleared with word atomics: in the engine loop the state update (priority
+// bit) runs on the other CTAs while CTA 0 executes (running / done bits), on the same bytes.
+__device__ __forceinline__ void flags_or(uint8_t* flags, uint32_t row, uint8_t bits) {
+    atomicOr(reinterpret_cast<unsigned int*>(flags + (row & ~3u)), (unsigned int)bits << (8 * (row & 3u)));
+}
+__device__ __forceinline__ void flags_and_not(uint8_t* flags, uint32_t row, uint8_t bits) {
+    atomicAnd(reinterpret_cast<unsigned int*>(flags + (row & ~3u)), ~((unsigned int)bits << (8 * (row & 3u))));
+}
+
 // CTA 0 of the engine loop: _Sim.execute (engine.py:247-284) for the step's batch (run ids
 // and rows, n_run of them, sched[row] = 1 on them). Preemption (last step's batch rows
 // left out: prev_id / prev_row in shared memory, rows re-read through row_of after a
@@ -2041,7 +2092,7 @@ __device__ __forceinline__ void engine_execute_loop(const rs_engine_queue& q, co
         if (live) {
             const uint8_t fl = q.flags[row];
             if (!(fl & EX_DONE) && (fl & RS_FLAG_RUNNING) && !sched[row]) {
-                q.flags[row] = (uint8_t)(fl & ~RS_FLAG_RUNNING);
+                flags_and_not(q.flags, row, RS_FLAG_RUNNING);
                 tr.n_preempted[id] += 1;
             }
         }
@@ -2098,7 +2149,8 @@ __device__ __forceinline__ void engine_execute_loop(const rs_engine_queue& q, co
             fl |= EX_DONE;
             fin = 1;
         }
-        q.flags[row] = fl;
+        const uint8_t set = fl & (uint8_t)(RS_FLAG_RUNNING | EX_DONE);  // (the priority bit is the update's)
+        if (set) flags_or(q.flags, row, set);
         prev_id[kk] = id;
         prev_row[kk] = row;
     }
@@ -2163,18 +2215,48 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
         sel_gsync<CL>(bar);
         mark(0);
         if (pub->stop) break;
-        const uint32_t n = (uint32_t)pub->n_rows;
+        uint32_t n = (uint32_t)pub->n_rows;
         const uint32_t n_alive = (uint32_t)pub->n_alive;
         const int32_t step = (int32_t)pub->step;
+        // last step's batch flags off (the update on the other CTAs has read them)
+        if (blockIdx.x == 0 && threadIdx.x < (uint32_t)s_prev_n) a.sched[s_prev_row[threadIdx.x]] = 0;
+        if (pub->compact) {  // finished rows out, into the other column set (stable)
+            const uint32_t live = (uint32_t)pub->live;
+            const rs_engine_queue qc = [&] { rs_engine_queue t = a.q[cur]; t.n = n; return t; }();
+            const uint32_t nb = (n + EX_THREADS - 1) / EX_THREADS;
+            for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
+                const int t = compact_count_chunk(qc.flags, n, c, warp_tot);
+                if (threadIdx.x == 0) a.block_keep[c] = t;
+            }
+            sel_gsync<CL>(bar);
+            for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
+                if (threadIdx.x < 32) {
+                    long long bsum = 0;
+                    for (uint32_t j = threadIdx.x; j < c; j += 32) bsum += __ldcg(a.block_keep + j);
+                    bsum = warp_sum(bsum);
+                    if (threadIdx.x == 0) s_base = bsum;
+                }
+                __syncthreads();
+                compact_scatter_chunk(qc, a.q[cur ^ 1], a.tr, c, s_base, warp_tot);
+            }
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                S.n_rows = live;
+                s_prev_ok = false;  // rows moved: the preemption pass finds them through row_of
+            }
+            cur ^= 1;
+            n = live;
+            sel_gsync<CL>(bar);
+            mark(7);
+        }
         rs_queue_soa soa = a.soa[cur];
         soa.n = n;
         rs_engine_queue q = a.q[cur];
         q.n = n;
         // the rank step. One pass builds the keys and keeps every key below the threshold
-        // a previous step left (thr: the key then placed at rank k + ENGINE_SPEC_MARGIN).
-        // When that kept between k and 1024 keys they hold the k smallest (>= k keys lie
-        // below thr), so they are placed directly; otherwise the full select runs over the
-        // built keys, keeping k + ENGINE_SPEC_MARGIN keys, and resets thr. Exact either way.
+        // a previous step left (thr: the key then placed at rank k + margin). When that
+        // kept between k and 1024 keys they hold the k smallest (>= k keys lie below thr),
+        // so they are placed directly; otherwise the full select runs over the built keys,
+        // keeping k + margin keys, and resets thr. Exact either way.
         const uint32_t k = min(n_alive, (uint32_t)a.max_batch);
         eng_spec_pass(soa, n, *(volatile unsigned __int128*)a.thr, a.calibrated, a.preemptive, a.counts + 3,
                       &a.sel->arrived, a.ck, a.ci);
@@ -2208,49 +2290,18 @@ __global__ void __launch_bounds__(SEL_THREADS) engine_loop_kernel(const __grid_c
         }
         sel_gsync<CL>(bar);  // the batch (run, run_row, sched) is set
         mark(10);
-        // execute, then the state update (schedulers.py:224-240): independent (the update
-        // touches the priority bit, starvation and quantum, execute the running / done bits
-        // and generated tokens), but both write flag bytes; the update clears sched
+        // CTA 0 executes while the other CTAs run the state update (schedulers.py:224-240):
+        // disjoint state (running / done bits, tokens vs priority bit, starvation, quantum),
+        // the shared flag bytes written with word atomics; the next step's first barrier
+        // joins them
         if (blockIdx.x == 0) {
             engine_execute_loop(q, a.tr, a.cost, a.run, a.run_row, (int)k, a.sched, S.pred, s_out, s_prev_id,
                                 s_prev_row, s_prev_n, s_prev_ok, &s_fin, &s_pf);
-            if (threadIdx.x == 0) {
-                s_prev_ok = true;  // compaction once the finished rows are an eighth of the rows
-                const int64_t live = S.n_alive - s_out[5];
-                pub->live = live;
-                pub->compact = (int64_t)(n - live) * 8 >= (int64_t)n ? 1 : 0;
-            }
+            if (threadIdx.x == 0) s_prev_ok = true;
+            mark(6);
+        } else {
+            upd_rows_loop(soa, a.sched, n, a.threshold, a.pquantum);
         }
-        sel_gsync<CL>(bar);
-        mark(6);
-        upd_rows_plain(soa, a.sched, n, a.threshold, a.pquantum);  // (admission, next, appends past n)
-        mark(11);
-        if (!pub->compact) continue;
-        sel_gsync<CL>(bar);
-        const uint32_t live = (uint32_t)pub->live;
-        const uint32_t nb = (n + EX_THREADS - 1) / EX_THREADS;
-        for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
-            const int t = compact_count_chunk(q.flags, n, c, warp_tot);
-            if (threadIdx.x == 0) a.block_keep[c] = t;
-        }
-        sel_gsync<CL>(bar);
-        for (uint32_t c = blockIdx.x; c < nb; c += gridDim.x) {
-            if (threadIdx.x < 32) {
-                long long b = 0;
-                for (uint32_t j = threadIdx.x; j < c; j += 32) b += __ldcg(a.block_keep + j);
-                b = warp_sum(b);
-                if (threadIdx.x == 0) s_base = b;
-            }
-            __syncthreads();
-            compact_scatter_chunk(q, a.q[cur ^ 1], a.tr, c, s_base, warp_tot);
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            S.n_rows = live;
-            s_prev_ok = false;  // rows moved: the next preemption pass finds them through row_of
-        }
-        cur ^= 1;
-        sel_gsync<CL>(bar);
-        mark(7);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.ls = S;
 }
