@@ -200,7 +200,13 @@ int rs_engine_execute_ex(const rs_engine_queue* q, const rs_engine_queue* q_out,
  * int64[n] (receives the dropped request indices). Device: adm_dev int32[n], stat_dev
  * int64[8] (out[6] | counts int32[4]) with its pinned host mirror stat_host, the
  * rank-step / execute outputs and workspace sized for n rows. limit_ns / stop_after <
- * 0: none. Returns RS_ERR_NAN on a NaN effective score. */
+ * 0: none. Returns RS_ERR_NAN on a NaN effective score.
+ * With an unlimited KV budget, max_batch <= 512 and 16-B aligned columns the whole loop
+ * is ONE launch (a thread-block cluster stepping the queue on the device; finished rows
+ * are compacted out lazily, so final_set / the queue columns at return hold the alive
+ * rows among finished ones, and the last step's state update is applied); otherwise the
+ * host steps the per-kernel calls. RS_ENGINE_LOOP=host forces the latter. Both give the
+ * same per-request results. */
 typedef struct rs_engine_loop {
     int64_t n_requests;
     const int64_t* arrival_ns;
