@@ -22,6 +22,9 @@ CASES = {
                       "default"),
     "no_predictor_charge": (4000, 80.0, dict(max_batch=256), dict(charges_predictor=False), {}, "unit"),
     "kv_budget": (3000, 40.0, dict(max_batch=64), dict(kv_budget=20000), {}, "default"),  # host loop either way
+    # every request at t = 0: the first step admits 6000 rows (admission in 1024-row chunks)
+    "burst": (6000, None, dict(max_batch=200, starvation_threshold=40, priority_quantum=6), {}, {}, "fast"),
+    "max_batch_1": (600, 40.0, dict(max_batch=1, starvation_threshold=5, priority_quantum=2), {}, {}, "fast"),
 }
 
 
@@ -29,9 +32,12 @@ def main(name):
     import numpy as np
     from paper_2408_15792_b200 import engine
     from paper_2408_15792_b200.schedulers import SchedulerConfig
-    from paper_2408_15792_b200.workload import LengthDist, generate_poisson
+    from paper_2408_15792_b200.workload import LengthDist, generate_burst, generate_poisson
     n, rate, sk, ek, rk, cost = CASES[name]
-    reqs = list(generate_poisson(rate, n, LengthDist.parse("sharegpt"), seed=11, prompt_noise=0.25))
+    if rate is None:
+        reqs = list(generate_burst(n, LengthDist.parse("sharegpt"), seed=11, prompt_noise=0.25))
+    else:
+        reqs = list(generate_poisson(rate, n, LengthDist.parse("sharegpt"), seed=11, prompt_noise=0.25))
     scores = np.random.default_rng(12).normal(size=n)
     eng = engine.DeviceEngine(reqs, scores, SchedulerConfig(**sk), engine.COST_PRESETS[cost], **ek)
     res = eng.run(**rk)

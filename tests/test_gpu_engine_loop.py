@@ -2,7 +2,8 @@
 engine_loop_kernel) against the per-kernel host loop (RS_ENGINE_LOOP=host) on the
 configurations the loop handles differently: length-calibrated keys, non-preemptive
 pinning, stop-after-finished and time-limit exits, the largest batch the fused select
-takes (512), no predictor charge, and a KV budget (which keeps the host loop). Same
+takes (512), no predictor charge, a KV budget (which keeps the host loop), a burst
+admitted in one step, and a batch of one. Same
 per-request rows, metrics and step counts. The host loop's decisions are checked step for
 step against the reference's engine.run in test_gpu_engine.py."""
 
@@ -18,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 HELPER = pathlib.Path(__file__).resolve().parent / "engine_loop_case.py"
 CASES = ["calibrated", "non_preemptive", "stop_after", "time_limit", "max_batch_512", "no_predictor_charge",
-         "kv_budget"]
+         "kv_budget", "burst", "max_batch_1"]
 
 
 def _run(name, host):
