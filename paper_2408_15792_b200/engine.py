@@ -14,7 +14,9 @@ the reference charges predictor time only at the first scoring either way.
 Records, per-request rows and metrics use the reference's keys and arithmetic (integer
 nanoseconds, math.fsum means, nearest-rank p90), so a run can be compared bit for bit
 with `ranksched.engine.run(trace, "ranking", scorer)` on the same scores
-(tests/test_gpu_engine.py, against fixtures recorded from the reference).
+(tests/test_gpu_engine.py, against fixtures recorded from the reference). Record-free
+runs execute the whole loop as one device launch (csrc/rankstep.cu engine_loop_kernel;
+tests/test_gpu_engine_loop.py checks it against the per-step path).
 """
 
 from __future__ import annotations
@@ -186,8 +188,10 @@ class DeviceEngine:
     def run(self, record: bool = False, stop_after_finished: int | None = None,
             time_limit_s: float | None = None, native: bool = True, rescore=None,
             max_steps: int | None = None) -> EngineResult:
-        """record=False (and native) runs the whole loop in C++ (rs_engine_run); record=True
-        steps from Python so every step's decision can be read back. rescore (optional):
+        """record=False (and native) runs the whole loop natively (rs_engine_run: with an
+        unlimited KV budget one cluster launch steps the queue on the device, else a C++
+        host loop over the per-step kernels); record=True steps from Python so every
+        step's decision can be read back. rescore (optional):
         called every step with the alive requests' trace indices (int64 device tensor, queue
         order) and returning their scores (float64 device tensor): the reference's
         re-score-every-step mode (engine.py:414-428 with rescore=True) instead of the cache."""
