@@ -285,8 +285,14 @@ def size_sweep(pk, reps=3):
         ranking.tau_counts_device(x, y, res, fast_only=True)
         t = timed(lambda: ranking.tau_counts_device(x, y, res, fast_only=True), reps)
         assert int(res[5]) == 0, "tau fast path declined a cfg4-shaped input"
+        # comparator, not a path: a library radix sort (torch.sort = CUB) of the (x, index)
+        # pairs alone. Every exact O(n log n) count orders x first, so this is the floor a
+        # sort-based tau sits above; vs_sort = sort_ms / ms
+        torch.sort(x)
+        ts = timed(lambda: torch.sort(x), reps)
         out["tau"].append({"n": n, "ms": t, "pairs_per_s": n * (n - 1) / 2 / (t / 1e3),
-                           "achieved_gbs": 8.0 * n / t / 1e6, "frac": 8.0 * n / t / 1e6 / pk["hbm_gbs"]})
+                           "achieved_gbs": 8.0 * n / t / 1e6, "frac": 8.0 * n / t / 1e6 / pk["hbm_gbs"],
+                           "sort_ms": ts, "vs_sort": ts / t})
         del x, y
     cfg = SchedulerConfig(max_batch=256, starvation_threshold=100, priority_quantum=50)
     for n in (1 << 20, 1 << 24, 1 << 26):  # reorder to 64M rows
