@@ -400,6 +400,46 @@ __global__ void __launch_bounds__(TF_ST_T, 1) tf_scatter1(const void* __restrict
     }
 }
 
+// ---- K4: level-2 plan (one CTA) ----------------------------------------------------
+// split[b] = bucket b holds > cap keys with different x; items = its CH2-chunks.
+__global__ void __launch_bounds__(TF_SCAN_T) tf_plan2(const TfParams* __restrict__ p,
+                                                      const uint32_t* __restrict__ off1, uint32_t cap, uint32_t ch2,
+                                                      uint32_t* __restrict__ srank, uint32_t* __restrict__ ibase,
+                                                      uint32_t* __restrict__ ng) {
+    const TfDerived d = tf_derive(p);
+    if (!d.ok) return;
+    __shared__ uint32_t sw[32];
+    constexpr int PER = TF_BINS / TF_SCAN_T;
+    uint32_t sp[PER], it[PER], ssum = 0, isum = 0;
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int b = threadIdx.x * PER + k;
+        const uint32_t m = off1[b + 1] - off1[b];
+        const bool split = m > cap && d.r1 > 0;
+        sp[k] = ssum;
+        it[k] = isum;
+        ssum += split;
+        isum += split ? (m + ch2 - 1) / ch2 : 0u;
+        ng[b] = (!split && m > 0) ? 1u : 0u;
+    }
+    uint32_t stot, itot;
+    __shared__ uint32_t tots[2];
+    const uint32_t sb = block_excl_scan<TF_SCAN_T>(ssum, sw, &tots[0]);
+    const uint32_t ib = block_excl_scan<TF_SCAN_T>(isum, sw, &tots[1]);
+    stot = tots[0];
+    itot = tots[1];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+        const int b = threadIdx.x * PER + k;
+        srank[b] = sb + sp[k];
+        ibase[b] = ib + it[k];
+    }
+    if (threadIdx.x == 0) {
+        srank[TF_BINS] = stot;
+        ibase[TF_BINS] = itot;
+    }
+}
+
 __device__ __forceinline__ uint32_t upper_bound_u32(const uint32_t* a, uint32_t n, uint32_t v) {
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
@@ -499,86 +539,6 @@ __device__ __forceinline__ uint32_t tf_child_heads(TfChildSmem& s, uint32_t T) {
     return heads;
 }
 
-// ---- K4: level-2 plan + level-1 groups (one CTA) -------------------------------------
-// split[b] = bucket b holds > cap keys with different x; items = its CH2-chunks. The
-// unsplit buckets form groups by the children's rule (tf_child_heads over the bucket
-// sizes): runs of small buckets share a group of < cap keys, so a small queue's leaf walk
-// is not one group per bucket. glen1[b] = the keys of the group headed by bucket b.
-__global__ void __launch_bounds__(TF_SCAN_T) tf_plan2(const TfParams* __restrict__ p,
-                                                      const uint32_t* __restrict__ off1, uint32_t cap, uint32_t ch2,
-                                                      uint32_t* __restrict__ srank, uint32_t* __restrict__ ibase,
-                                                      uint32_t* __restrict__ ng, uint32_t* __restrict__ glen1) {
-    const TfDerived d = tf_derive(p);
-    if (!d.ok) return;
-    extern __shared__ __align__(16) uint8_t tf_child_raw[];
-    TfChildSmem& s = *reinterpret_cast<TfChildSmem*>(tf_child_raw);
-    __shared__ uint32_t sw[32];
-    constexpr int PER = TF_BINS / TF_SCAN_T;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t sp[PER], it[PER], ssum = 0, isum = 0;
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-        const int b = threadIdx.x * PER + k;
-        const uint32_t m = off1[b + 1] - off1[b];
-        const bool split = m > cap && d.r1 > 0;
-        s.ct[b] = m;
-        sp[k] = ssum;
-        it[k] = isum;
-        ssum += split;
-        isum += split ? (m + ch2 - 1) / ch2 : 0u;
-    }
-    __syncthreads();
-    const uint32_t heads = tf_child_heads(s, cap / 2);  // a split bucket (> cap keys) is a head
-    // next head after each bucket: exclusive suffix min over threads of the first head
-    constexpr uint32_t NONE = 0xffffffffu;
-    uint32_t fb = NONE;
-#pragma unroll
-    for (int k = PER - 1; k >= 0; --k)
-        if (heads >> k & 1u) fb = (uint32_t)(threadIdx.x * PER + k);
-    uint32_t x = fb;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t yv = __shfl_down_sync(0xffffffffu, x, o);
-        if (lane + o < 32) x = min(x, yv);
-    }
-    if (lane == 0) s.sw[wid] = x;
-    __syncthreads();
-    uint32_t nb = __shfl_down_sync(0xffffffffu, x, 1);
-    if (lane == 31) nb = NONE;
-    for (int k = wid + 1; k < TF_SCAN_T / 32; ++k) nb = min(nb, s.sw[k]);
-#pragma unroll
-    for (int k = PER - 1; k >= 0; --k) {
-        const int b = threadIdx.x * PER + k;
-        const uint32_t m = s.ct[b];
-        const bool split = m > cap && d.r1 > 0;
-        const bool head = heads >> k & 1u;
-        if (d.r1 == 0) {  // one x value per bucket: each bucket a single-x group
-            ng[b] = m > 0 ? 1u : 0u;
-            glen1[b] = m;
-        } else {
-            ng[b] = (!split && head) ? 1u : 0u;
-            glen1[b] = (nb == NONE ? s.tot : s.cs[nb]) - s.cs[b];
-        }
-        if (head) nb = (uint32_t)b;
-    }
-    uint32_t stot, itot;
-    __shared__ uint32_t tots[2];
-    const uint32_t sb = block_excl_scan<TF_SCAN_T>(ssum, sw, &tots[0]);
-    const uint32_t ib = block_excl_scan<TF_SCAN_T>(isum, sw, &tots[1]);
-    stot = tots[0];
-    itot = tots[1];
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-        const int b = threadIdx.x * PER + k;
-        srank[b] = sb + sp[k];
-        ibase[b] = ib + it[k];
-    }
-    if (threadIdx.x == 0) {
-        srank[TF_BINS] = stot;
-        ibase[TF_BINS] = itot;
-    }
-}
-
 // ---- K6: level-2 column scan + child totals + group count, one CTA per bucket ----
 __global__ void __launch_bounds__(TF_SCAN_T) tf_scan2(const TfParams* __restrict__ p,
                                                       const uint32_t* __restrict__ off1,
@@ -668,8 +628,7 @@ __global__ void __launch_bounds__(TF_ST_T, 1) tf_scatter2(const TfParams* __rest
 }
 
 // Group record: start, len, flags (bit0: keys in B, bit1: single x, bit2: a crowded
-// level-2 child: > cap keys over at most 2^r2 distinct x, bit3: several level-1 buckets,
-// the first one in pad).
+// level-2 child: > cap keys over at most 2^r2 distinct x).
 struct TfGroup {
     uint32_t start, len, flags, pad;
 };
@@ -679,8 +638,7 @@ struct TfGroup {
 __global__ void __launch_bounds__(TF_SCAN_T) tf_gscan(const TfParams* __restrict__ p,
                                                       const uint32_t* __restrict__ off1,
                                                       const uint32_t* __restrict__ srank,
-                                                      const uint32_t* __restrict__ ng, const uint32_t* __restrict__ glen1,
-                                                      uint32_t* __restrict__ gbase,
+                                                      const uint32_t* __restrict__ ng, uint32_t* __restrict__ gbase,
                                                       TfGroup* __restrict__ groups, uint32_t* __restrict__ gstart,
                                                       TfParams* __restrict__ pw) {
     const TfDerived d = tf_derive(p);
@@ -700,9 +658,8 @@ __global__ void __launch_bounds__(TF_SCAN_T) tf_gscan(const TfParams* __restrict
         const uint32_t g = base + loc[k];
         gbase[b] = g;
         const uint32_t m = off1[b + 1] - off1[b];
-        if (m && srank[b + 1] == srank[b] && ng[b]) {  // unsplit group head: its keys are in A
-            const uint32_t len = glen1[b];
-            groups[g] = TfGroup{off1[b], len, (d.r1 == 0 ? 2u : 0u) | (len != m ? 8u : 0u), (uint32_t)b};
+        if (m && srank[b + 1] == srank[b]) {  // unsplit: one group in A
+            groups[g] = TfGroup{off1[b], m, d.r1 == 0 ? 2u : 0u, 0u};
             gstart[g] = off1[b];
         }
     }
@@ -768,25 +725,12 @@ __device__ __forceinline__ int tf_pidx(int e) { return e + (e >> (IT == 16 ? 4 :
 // CTA merge sort of mp (a multiple of 16, <= TF_CAP) u32 keys in padded smem; threads
 // t < mp/16 own 16 consecutive outputs. Stable; with Count, returns the number of
 // strict inversions (pairs i < j with key_i > key_j) seen by this thread.
-// Seg: the positions are cut into segments (ss[pos] = the first position of pos's
-// segment) and each segment is sorted on its own — the order is (segment, key). A merge
-// of two runs sorted that way leaves every segment's keys on that segment's positions
-// (the runs cover contiguous positions), so an element's segment is always the one of
-// the position it sits on, and ss never changes: B at position qb precedes A at pa < qb
-// iff ss[qb] <= pa (same segment) and its key is smaller.
-template <bool Count, int IT, bool Seg = false>
-__device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint32_t (&r)[IT],
-                                                      const uint16_t* ss = nullptr) {
+template <bool Count, int IT>
+__device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint32_t (&r)[IT]) {
     const int t = threadIdx.x;
     const bool act = t < mp / IT;
     unsigned long long inv = 0;
     if (act) {
-        uint32_t same = ~0u;  // bit k: positions t*IT + k and + k + 1 share a segment
-        if (Seg) {
-            same = 0;
-#pragma unroll
-            for (int k = 0; k + 1 < IT; ++k) same |= (uint32_t)((int)ss[t * IT + k + 1] <= t * IT + k) << k;
-        }
 #pragma unroll
         for (int k = 0; k < IT; ++k) r[k] = sk[tf_pidx<IT>(t * IT + k)];
 #pragma unroll
@@ -794,7 +738,7 @@ __device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint
 #pragma unroll
             for (int k = (rd & 1); k + 1 < IT; k += 2) {
                 const uint32_t a = r[k], b = r[k + 1];
-                const bool sw = b < a && (same >> k & 1u);
+                const bool sw = b < a;
                 r[k] = sw ? b : a;
                 r[k + 1] = sw ? a : b;
                 if (Count) inv += sw;
@@ -821,19 +765,16 @@ __device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint
             int lo = max(0, diag - lb), hi = min(diag, la);
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
-                const int qb = b0 + diag - 1 - mid, pa = a0 + mid;
-                const bool b_first = sk[tf_pidx<IT>(qb)] < sk[tf_pidx<IT>(pa)] && (!Seg || (int)ss[qb] <= pa);
-                if (!b_first) lo = mid + 1; else hi = mid;
+                if (!(sk[tf_pidx<IT>(b0 + diag - 1 - mid)] < sk[tf_pidx<IT>(a0 + mid)])) lo = mid + 1; else hi = mid;
             }
             // branch-free serial merge of this thread's 16 outputs: the consumed side is
             // reloaded from a clamped index (an exhausted run's head is never taken)
             int i = lo, j = diag - lo;
             uint32_t ka = sk[tf_pidx<IT>(a0 + min(i, la - 1))];  // la >= IT
             uint32_t kb = sk[tf_pidx<IT>(lb > 0 ? b0 + min(j, lb - 1) : a0)];
-            int sb = Seg ? (int)ss[lb > 0 ? b0 + min(j, lb - 1) : a0] : 0;
 #pragma unroll
             for (int k = 0; k < IT; ++k) {
-                const bool take_b = j < lb && (i >= la || (kb < ka && (!Seg || sb <= a0 + i)));
+                const bool take_b = j < lb && (i >= la || kb < ka);
                 r[k] = take_b ? kb : ka;
                 if (Count) inv += take_b ? (unsigned long long)(la - i) : 0ull;
                 i += take_b ? 0 : 1;
@@ -842,7 +783,6 @@ __device__ __forceinline__ unsigned long long tf_sort(uint32_t* sk, int mp, uint
                 const uint32_t v = sk[tf_pidx<IT>(nx)];
                 ka = take_b ? ka : v;
                 kb = take_b ? v : kb;
-                if (Seg) sb = (int)ss[lb > 0 ? b0 + min(j, lb - 1) : a0];
             }
         }
         // the next level (width 2w) reads runs of this one: warp-local while 4w <= WSPAN
@@ -900,14 +840,13 @@ __device__ __forceinline__ int tf_excl_max(int v, int* sw) {
     return carry;  // max over all earlier threads
 }
 
-constexpr size_t TF_LEAF_SMEM = (size_t)(TF_CAP + TF_CAP / 16) * 4 + 2 * TF_BINS * 4 + TF_CAP * 2;
+constexpr size_t TF_LEAF_SMEM = (size_t)(TF_CAP + TF_CAP / 16) * 4 + 2 * TF_BINS * 4;
 
 template <int IT>
 __global__ void __launch_bounds__(TF_LEAF_T, 2) tf_leaf(const TfParams* __restrict__ p, uint32_t n,
                                                         const TfGroup* __restrict__ groups,
                                                         const uint32_t* __restrict__ gstart,
                                                         const uint32_t* __restrict__ A, const uint32_t* __restrict__ B,
-                                                        const uint32_t* __restrict__ off1,
                                                         uint32_t* __restrict__ hc, unsigned long long* __restrict__ acc) {
     const TfDerived d = tf_derive(p);
     if (!d.ok || p->fail) return;
@@ -915,7 +854,6 @@ __global__ void __launch_bounds__(TF_LEAF_T, 2) tf_leaf(const TfParams* __restri
     uint32_t* sk = tf_sm;                                  // TF_CAP + pad
     uint32_t* hist = sk + TF_CAP + TF_CAP / 16;             // running y histogram of this CTA
     uint32_t* gt = hist + TF_BINS;                          // suffix sums
-    uint16_t* ss = reinterpret_cast<uint16_t*>(gt + TF_BINS);  // segment starts (multi-bucket groups)
     __shared__ uint32_t sw[32];
     __shared__ int swi[32];
     __shared__ uint32_t s_g[2];
@@ -1009,57 +947,22 @@ __global__ void __launch_bounds__(TF_LEAF_T, 2) tf_leaf(const TfParams* __restri
         }
         const int mp = ((int)m + IT - 1) / IT * IT;
         for (int e = threadIdx.x; e < mp; e += TF_LEAF_T) sk[tf_pidx<IT>(e)] = e < (int)m ? src[e] : 0xffffffffu;
-        const bool multi = gr.flags & 8u;  // several level-1 buckets: key1 omits their digits
-        const int t = threadIdx.x;
-        const bool act = t < mp / IT;
-        if (multi) {
-            // ss[pos] = start of pos's bucket (relative): mark the bucket starts, then an
-            // inclusive max-scan over positions (thread t owns positions t*IT .. + IT - 1)
-            for (int e = t; e < mp; e += TF_LEAF_T) ss[e] = 0;
-            __syncthreads();
-            for (uint32_t bb = gr.pad + t; bb < (uint32_t)TF_BINS; bb += TF_LEAF_T) {
-                const uint32_t s0 = off1[bb];
-                if (s0 >= gr.start + m) break;
-                ss[s0 - gr.start] = (uint16_t)(s0 - gr.start);
-            }
-            if (t == 0 && (int)m < mp) ss[m] = (uint16_t)m;  // the padding: a segment of its own
-            __syncthreads();
-            int run = -1;
-            if (act) {
-#pragma unroll
-                for (int k = 0; k < IT; ++k) run = max(run, (int)ss[t * IT + k]);
-            }
-            int carry = tf_excl_max(act ? run : -1, swi);
-            if (act) {
-#pragma unroll
-                for (int k = 0; k < IT; ++k) {
-                    carry = max(carry, (int)ss[t * IT + k]);
-                    ss[t * IT + k] = (uint16_t)carry;
-                }
-            }
-        }
         __syncthreads();
         uint32_t r[IT];
-        if (multi) tf_sort<false, IT, true>(sk, mp, r, ss);  // by (bucket, x_rem, y)
-        else tf_sort<false, IT>(sk, mp, r);                 // by (x_rem, y)
-        // tied runs in x (key >> 12) and in (x, y) (key) — a bucket start begins new runs;
-        // cross term; histogram update
+        tf_sort<false, IT>(sk, mp, r);  // by (x_rem, y)
+        // tied runs in x (key >> 12) and in (x, y) (key); cross term; histogram update
+        const int t = threadIdx.x;
+        const bool act = t < mp / IT;
         int hx = -1, hk = -1;  // last run head (position) inside this thread
         uint32_t prevk = 0;
         if (act && t > 0) prevk = sk[tf_pidx<IT>(t * IT - 1)];
-        uint32_t cut = 0;  // bit k: position t*IT + k starts a bucket
-        if (multi && act) {
-#pragma unroll
-            for (int k = 0; k < IT; ++k) cut |= (uint32_t)((int)ss[t * IT + k] == t * IT + k) << k;
-        }
 #pragma unroll
         for (int k = 0; k < IT; ++k) {
             const int pos = t * IT + k;
             const uint32_t key = r[k];
             const uint32_t pk = k ? r[k - 1] : prevk;
-            const bool c = cut >> k & 1u;
-            if (act && (pos == 0 || c || (key >> 12) != (pk >> 12))) hx = pos;
-            if (act && (pos == 0 || c || key != pk)) hk = pos;
+            if (act && (pos == 0 || (key >> 12) != (pk >> 12))) hx = pos;
+            if (act && (pos == 0 || key != pk)) hk = pos;
         }
         hx = tf_excl_max(act ? hx : -1, swi);
         hk = tf_excl_max(act ? hk : -1, swi);
@@ -1069,9 +972,8 @@ __global__ void __launch_bounds__(TF_LEAF_T, 2) tf_leaf(const TfParams* __restri
                 const int pos = t * IT + k;
                 const uint32_t key = r[k];
                 const uint32_t pk = k ? r[k - 1] : prevk;
-                const bool c = cut >> k & 1u;
-                if (pos == 0 || c || (key >> 12) != (pk >> 12)) hx = pos;
-                if (pos == 0 || c || key != pk) hk = pos;
+                if (pos == 0 || (key >> 12) != (pk >> 12)) hx = pos;
+                if (pos == 0 || key != pk) hk = pos;
                 if (pos < (int)m) {
                     n1 += (unsigned long long)(pos - hx);
                     n3 += (unsigned long long)(pos - hk);
@@ -1167,7 +1069,7 @@ static TfSizes tf_sizes(uint64_t n) {
 struct TfWs {
     TfParams* p;
     unsigned long long* acc;
-    uint32_t *hist1, *pre1, *tot1, *off1, *srank, *ibase, *ng, *glen1, *gbase, *hist2, *pre2, *ctot, *gstart, *hc, *prec;
+    uint32_t *hist1, *pre1, *tot1, *off1, *srank, *ibase, *ng, *gbase, *hist2, *pre2, *ctot, *gstart, *hc, *prec;
     TfGroup* groups;
 };
 template <typename Ar>
@@ -1183,7 +1085,6 @@ static void tf_layout(Ar& a, uint64_t n, TfWs* w) {
     t.srank = a.template take<uint32_t>(TF_BINS + 1);
     t.ibase = a.template take<uint32_t>(TF_BINS + 1);
     t.ng = a.template take<uint32_t>(TF_BINS);
-    t.glen1 = a.template take<uint32_t>(TF_BINS);
     t.gbase = a.template take<uint32_t>(TF_BINS);
     t.hist2 = a.template take<uint32_t>((size_t)z.max_items * TF_BINS);
     t.pre2 = a.template take<uint32_t>((size_t)z.max_items * TF_BINS);
@@ -1232,8 +1133,7 @@ int tau_fast_counts(const void* x, int xd, const void* y, int yd, uint32_t n, in
     RS_CUDA(ensure_smem((const void*)tf_scatter2, (int)TF_ST_SMEM));
     tf_scatter1<<<z.nch1, TF_ST_T, TF_ST_SMEM, st>>>(x, xd, y, yd, n, z.ch1, w.p, w.pre1, w.tot1, w.off1, A);
     RS_LAUNCH_CHECK();
-    RS_CUDA(ensure_smem((const void*)tf_plan2, (int)TF_CHILD_SMEM));
-    tf_plan2<<<1, TF_SCAN_T, TF_CHILD_SMEM, st>>>(w.p, w.off1, z.cap, z.ch2, w.srank, w.ibase, w.ng, w.glen1);
+    tf_plan2<<<1, TF_SCAN_T, 0, st>>>(w.p, w.off1, z.cap, z.ch2, w.srank, w.ibase, w.ng);
     RS_LAUNCH_CHECK();
     const uint32_t g2 = std::min<uint32_t>(z.max_items, (uint32_t)sms * 4);
     tf_count2<<<g2, TF_T, 0, st>>>(w.p, w.off1, w.ibase, z.ch2, A, w.hist2);
@@ -1245,7 +1145,7 @@ int tau_fast_counts(const void* x, int xd, const void* y, int yd, uint32_t n, in
     tf_scatter2<<<std::min<uint32_t>(z.max_items, (uint32_t)sms), TF_ST_T, TF_ST_SMEM, st>>>(w.p, w.off1, w.ibase, z.ch2,
                                                                                         w.pre2, A, B);
     RS_LAUNCH_CHECK();
-    tf_gscan<<<1, TF_SCAN_T, 0, st>>>(w.p, w.off1, w.srank, w.ng, w.glen1, w.gbase, w.groups, w.gstart, w.p);
+    tf_gscan<<<1, TF_SCAN_T, 0, st>>>(w.p, w.off1, w.srank, w.ng, w.gbase, w.groups, w.gstart, w.p);
     RS_LAUNCH_CHECK();
     tf_groups<<<z.max_split, TF_SCAN_T, TF_CHILD_SMEM, st>>>(w.p, w.off1, w.srank, z.cap, w.ctot, w.ng, w.gbase,
                                                              w.groups, w.gstart);
@@ -1255,9 +1155,9 @@ int tau_fast_counts(const void* x, int xd, const void* y, int yd, uint32_t n, in
     // groups of <= 4096 keys (the smaller queues): 8 keys per thread, so twice the threads
     // share each merge (half the serial merge steps per level, one level more)
     if (z.cap <= TF_CAP / 2)
-        tf_leaf<8><<<z.leaf_ctas, TF_LEAF_T, TF_LEAF_SMEM, st>>>(w.p, n, w.groups, w.gstart, A, B, w.off1, w.hc, w.acc);
+        tf_leaf<8><<<z.leaf_ctas, TF_LEAF_T, TF_LEAF_SMEM, st>>>(w.p, n, w.groups, w.gstart, A, B, w.hc, w.acc);
     else
-        tf_leaf<16><<<z.leaf_ctas, TF_LEAF_T, TF_LEAF_SMEM, st>>>(w.p, n, w.groups, w.gstart, A, B, w.off1, w.hc, w.acc);
+        tf_leaf<16><<<z.leaf_ctas, TF_LEAF_T, TF_LEAF_SMEM, st>>>(w.p, n, w.groups, w.gstart, A, B, w.hc, w.acc);
     RS_LAUNCH_CHECK();
     tf_colscan<<<TF_BINS / 32, 256, 0, st>>>(w.hc, z.leaf_ctas, w.p, w.prec, nullptr, w.acc + 2);
     RS_LAUNCH_CHECK();

@@ -42,6 +42,10 @@ if "--time-only" not in sys.argv:
     print("mismatches", bad)
 
 
+if "--check-only" in sys.argv:
+    sys.exit(1 if bad else 0)
+
+
 def timed(fn, reps=10):
     fn()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
