@@ -373,6 +373,11 @@ int rs_attention_bwd_lse(const void* qkv_dev, const void* att_dev, const void* d
 size_t rs_attention_bwd_long_workspace_size(int32_t B, int32_t S, int32_t H);
 int rs_attention_bwd_long(const void* qkv_dev, const void* att_dev, const void* dout_dev, void* dqkv_dev,
                           int32_t B, int32_t S, int32_t H, void* ws_dev, size_t ws_bytes, void* stream);
+/* The same given the forward's lse (rs_attention_fwd_lse, [b, h, row]): the dQ kernel
+ * skips its row-statistics pass (the ranker's training backward for S > 128). */
+int rs_attention_bwd_long_lse(const void* qkv_dev, const void* att_dev, const void* dout_dev, const float* lse_dev,
+                              void* dqkv_dev, int32_t B, int32_t S, int32_t H, void* ws_dev, size_t ws_bytes,
+                              void* stream);
 /* Number of kernels this library has launched in the process (all entry points). */
 uint64_t rs_launch_count(void);
 

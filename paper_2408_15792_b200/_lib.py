@@ -129,6 +129,8 @@ SIGNATURES = {
     "rs_attention_bwd_lse": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp]),
     "rs_attention_bwd_long_workspace_size": (c_sz, [c_i32, c_i32, c_i32]),
     "rs_attention_bwd_long": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_sz, c_vp]),
+    "rs_attention_bwd_long_lse": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_vp, c_sz,
+                                                 c_vp]),
     "rs_linear_n_params": (c_i64, [c_i32, c_i32]),
     "rs_standardizer_fit": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
     "rs_standardize": (ctypes.c_int, [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp]),

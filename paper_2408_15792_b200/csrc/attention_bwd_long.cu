@@ -7,7 +7,8 @@
 // query blocks i >= j. Two kernels, each owning one accumulator in TMEM, so nothing is
 // accumulated through global memory (no atomics, deterministic):
 //   dq kernel, CTA (b, h, i): pass 1 over j <= i: S_ij = Q_i K_j^T -> online row max / sum
-//             -> row LSE (base 2) and D_i = rowsum(dO_i * O_i), both written to scratch;
+//             -> row LSE (base 2) and D_i = rowsum(dO_i * O_i), both written to scratch
+//             (given the training forward's LSE, pass 1 is skipped: only D is computed);
 //             pass 2 over j <= i: S_ij, dP_ij = dO_i V_j^T -> dS = P (dP - D) / 8 ->
 //             dQ_i += dS K_j.
 //   dkv kernel, CTA (b, h, j): over i >= j: S_ij, dP_ij (P from the saved LSE) ->
@@ -93,7 +94,8 @@ constexpr int ALQ_SMEM = 5 * AL_TILE + AL_SQ + 128;  // Q dO O | K V | dS
 __global__ void __launch_bounds__(AL_THREADS, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tatt,
                        const __grid_constant__ CUtensorMap tdo, __nv_bfloat16* __restrict__ dqkv,
-                       float* __restrict__ lse_out, float* __restrict__ d_out, int B, int S, int H) {
+                       float* __restrict__ lse_out, float* __restrict__ d_out, const float* __restrict__ lse_in,
+                       int B, int S, int H) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw;
     if ((smem_u32(smem) & 1023u) != 0u) __trap();
@@ -133,8 +135,8 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
             tma_load_2d(sdO, &tdo, &bar->ld, h * AL_D, row0 + i * AL_T);
             tma_load_2d(sO, &tatt, &bar->ld, h * AL_D, row0 + i * AL_T);
             int it = 0;
-            // pass 1: S blocks for the row statistics
-            for (int j = 0; j <= i; ++j, ++it) {
+            // pass 1: S blocks for the row statistics (skipped given the forward's LSE)
+            for (int j = 0; lse_in == nullptr && j <= i; ++j, ++it) {
                 if (j > 0) mbar_wait(&bar->s_free, (j - 1) & 1);  // S read, K free
                 mbar_arrive_expect_tx(&bar->kv, AL_TILE);
                 tma_load_2d(sK, &tqkv, &bar->kv, dm + h * AL_D, row0 + j * AL_T);
@@ -146,7 +148,8 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
                     mma_bf16_ss(tS, desc_kmajor_sw128(q + s * 32), desc_kmajor_sw128(k + s * 32), id_ss, s != 0);
                 mma_commit(&bar->s_full);
             }
-            mbar_wait(&bar->s_free, i & 1);
+            if (lse_in == nullptr) mbar_wait(&bar->s_free, i & 1);
+            if (lse_in != nullptr) mbar_wait(&bar->ld, 0);
             // pass 2: dS blocks -> dQ
             for (int j = 0; j <= i; ++j, ++it) {
                 if (j > 0) mbar_wait(&bar->g_done, (j - 1) & 1);  // dQ MMA done: K, V, dS free
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
         int it = 0;
         float m = -INFINITY, l = 0.f;
         uint32_t v[32];
-        for (int j = 0; j <= i; ++j, ++it) {
+        for (int j = 0; lse_in == nullptr && j <= i; ++j, ++it) {
             mbar_wait(&bar->s_full, it & 1);
             tc_fence_after();
 #pragma unroll 1
@@ -208,10 +211,12 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar->s_free);
         }
-        const float lse2 = (row_ok && l > 0.f) ? m * AL_C + al_lg2(l) : 0.f;
+        // row statistics, [b, h, row] with row stride S (the forward's LSE layout)
+        const float lse2 = lse_in != nullptr ? (row_ok ? lse_in[(size_t)bh * S + qg] : 0.f)
+                                             : ((row_ok && l > 0.f) ? m * AL_C + al_lg2(l) : 0.f);
         if (row_ok) {
-            lse_out[(size_t)bh * nq * AL_T + qg] = lse2;
-            d_out[(size_t)bh * nq * AL_T + qg] = Dr;
+            if (lse_in == nullptr) lse_out[(size_t)bh * S + qg] = lse2;
+            d_out[(size_t)bh * S + qg] = Dr;
         }
         for (int j = 0; j <= i; ++j, ++it) {
             mbar_wait(&bar->s_full, it & 1);
@@ -333,8 +338,8 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
         for (int i = j; i < nq; ++i, ++t) {
             const int qg = i * AL_T + r;
             const bool row_ok = qg < S;
-            const float lse2 = row_ok ? lse_in[(size_t)bh * nq * AL_T + qg] : 0.f;
-            const float Dr = row_ok ? d_in[(size_t)bh * nq * AL_T + qg] : 0.f;
+            const float lse2 = row_ok ? lse_in[(size_t)bh * S + qg] : 0.f;
+            const float Dr = row_ok ? d_in[(size_t)bh * S + qg] : 0.f;
             mbar_wait(&bar->s_full, t & 1);
             tc_fence_after();
             if (t > 0) mbar_wait(&bar->g_done, (t - 1) & 1);  // previous dV / dK MMAs read sP, sdS
@@ -387,8 +392,10 @@ size_t attention_bwd_long_ws(int B, int S, int H) {
     return 2 * (size_t)B * H * nq * AL_T * sizeof(float) + 256;
 }
 
+// lse_fwd: the training forward's row LSE (attention_fwd_lse, [b, h, row]) — the dQ
+// kernel then skips its statistics pass; nullptr recomputes it into the workspace.
 int attention_bwd_long(const void* qkv, const void* att, const void* dout, void* dqkv, int B, int S, int H, void* ws,
-                       size_t ws_bytes, cudaStream_t st) {
+                       size_t ws_bytes, cudaStream_t st, const float* lse_fwd) {
     RS_CHECK_ARG(B > 0 && S > AL_T && S <= AL_T * AL_MAXB && H > 0, "attention_bwd_long: need 128 < S <= 512");
     RS_CHECK_ARG(ws_bytes >= attention_bwd_long_ws(B, S, H), "attention_bwd_long: workspace too small");
     RS_CUDA(ensure_smem((const void*)attn_bwd_dq_kernel, ALQ_SMEM));
@@ -403,9 +410,10 @@ int attention_bwd_long(const void* qkv, const void* att, const void* dout, void*
     RS_TRY(make_tmap_bf16(&ma, att, rows, dmc, dmc * 2, AL_T, AL_D));
     RS_TRY(make_tmap_bf16(&md, dout, rows, dmc, dmc * 2, AL_T, AL_D));
     attn_bwd_dq_kernel<<<B * H * nq, AL_THREADS, ALQ_SMEM, st>>>(mq, ma, md, static_cast<__nv_bfloat16*>(dqkv), lse,
-                                                                 dd, B, S, H);
+                                                                 dd, lse_fwd, B, S, H);
     RS_LAUNCH_CHECK();
-    attn_bwd_dkv_kernel<<<B * H * nq, AL_THREADS, ALK_SMEM, st>>>(mq, md, static_cast<__nv_bfloat16*>(dqkv), lse, dd,
+    attn_bwd_dkv_kernel<<<B * H * nq, AL_THREADS, ALK_SMEM, st>>>(mq, md, static_cast<__nv_bfloat16*>(dqkv),
+                                                                  lse_fwd != nullptr ? lse_fwd : lse, dd,
                                                                   B, S, H);
     RS_LAUNCH_CHECK();
     return RS_OK;
@@ -420,5 +428,16 @@ extern "C" size_t rs_attention_bwd_long_workspace_size(int32_t B, int32_t S, int
 extern "C" int rs_attention_bwd_long(const void* qkv, const void* att, const void* dout, void* dqkv, int32_t B,
                                      int32_t S, int32_t H, void* ws, size_t ws_bytes, void* stream) {
     RS_NVTX();
-    return rs::attention_bwd_long(qkv, att, dout, dqkv, B, S, H, ws, ws_bytes, rs::as_stream(stream));
+    return rs::attention_bwd_long(qkv, att, dout, dqkv, B, S, H, ws, ws_bytes, rs::as_stream(stream), nullptr);
+}
+
+extern "C" int rs_attention_bwd_long_lse(const void* qkv, const void* att, const void* dout, const float* lse,
+                                         void* dqkv, int32_t B, int32_t S, int32_t H, void* ws, size_t ws_bytes,
+                                         void* stream) {
+    RS_NVTX();
+    if (lse == nullptr) {
+        rs::set_error("rs_attention_bwd_long_lse: lse is NULL");
+        return RS_ERR_INVALID;
+    }
+    return rs::attention_bwd_long(qkv, att, dout, dqkv, B, S, H, ws, ws_bytes, rs::as_stream(stream), lse);
 }

@@ -29,7 +29,7 @@ int attention_fwd(const void* qkv, void* out, int B, int S, int H, cudaStream_t 
 int attention_fwd_lse(const void* qkv, void* out, float* lse, int B, int S, int H, cudaStream_t st);
 size_t attention_bwd_long_ws(int B, int S, int H);
 int attention_bwd_long(const void* qkv, const void* att, const void* dout, void* dqkv, int B, int S, int H, void* ws,
-                       size_t ws_bytes, cudaStream_t st);
+                       size_t ws_bytes, cudaStream_t st, const float* lse_fwd);
 int ranker_embed(const int32_t* ids, const void* P, int64_t off_tok, int64_t off_pos, float* h, int n_tok, int S,
                  int d, int vocab, int mp, cudaStream_t st);
 int ranker_ln(const float* x, const void* w, const void* b, void* y, int rows, int d, cudaStream_t st);
@@ -51,7 +51,7 @@ struct TrainWs {
     float* h_in[64];  // L + 1 entries (h_in[L] = final residual stream)
     float* h_mid[64];
     __nv_bfloat16 *x1[64], *qkv[64], *att[64], *x2[64], *f[64];
-    float* lse[64];  // attention rows' log2-sum-exp (S <= 128: the backward's P in one pass)
+    float* lse[64];  // attention rows' log2-sum-exp (the backward's P in one pass)
     // backward scratch
     float *dh, *dx, *wpart, *rpart, *g, *dg;
     float *feat, *logits, *dlogits, *dfeat;  // classification head (rs_ranker_grad_cls)
@@ -101,7 +101,7 @@ static void train_layout(A& a, const rs_ranker_config& c, int64_t Tp, int P, int
         t.att[l] = a.template take<__nv_bfloat16>(Tp * d);
         t.x2[l] = a.template take<__nv_bfloat16>(Tp * d);
         t.f[l] = a.template take<__nv_bfloat16>(Tp * F);
-        t.lse[l] = a.template take<float>(S <= 128 ? (int64_t)P * c.n_heads * S : 0);
+        t.lse[l] = a.template take<float>((int64_t)P * c.n_heads * S);
     }
     const int64_t wmax = (F * d > 3 * d * d ? F * d : 3 * d * d);
     t.dh = a.template take<float>(Tp * d);
@@ -161,10 +161,7 @@ static int train_forward(const rs_ranker_config* cfg, const __nv_bfloat16* P16, 
         RS_TRY(ranker_ln(w.h_in[l], P16 + off(OFF_LN1_W, l), P16 + off(OFF_LN1_B, l), w.x1[l], (int)Tp, d, st));
         RS_TRY(gemm_bf16(w.x1[l], P16 + off(OFF_QKV_W, l), P16 + off(OFF_QKV_B, l), nullptr, w.qkv[l], (int)Tp,
                          3 * d, d, 0, st));
-        if (S <= 128)
-            RS_TRY(attention_fwd_lse(w.qkv[l], w.att[l], w.lse[l], P, S, H, st));
-        else
-            RS_TRY(attention_fwd(w.qkv[l], w.att[l], P, S, H, st));
+        RS_TRY(attention_fwd_lse(w.qkv[l], w.att[l], w.lse[l], P, S, H, st));
         RS_TRY(gemm_bf16(w.att[l], P16 + off(OFF_OUT_W, l), P16 + off(OFF_OUT_B, l), w.h_in[l], w.h_mid[l],
                          (int)Tp, d, d, 2, st));
         RS_TRY(ranker_ln(w.h_mid[l], P16 + off(OFF_LN2_W, l), P16 + off(OFF_LN2_B, l), w.x2[l], (int)Tp, d, st));
@@ -211,7 +208,7 @@ static int train_backward(const rs_ranker_config* cfg, const __nv_bfloat16* P16,
             RS_TRY(attention_bwd(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, st, w.lse[l], w.rpart));
             RS_TRY(rows_add(w.rpart, P, 3 * d, grad + off(OFF_QKV_B, l), w.rpart + (size_t)P * 3 * d, st));
         } else {
-            RS_TRY(attention_bwd_long(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, w.abw, w.abw_bytes, st));
+            RS_TRY(attention_bwd_long(w.qkv[l], w.att[l], w.da, w.dqkv, P, S, H, w.abw, w.abw_bytes, st, w.lse[l]));
         }
         // QKV: qkv = x1 Wqkv^T + b
         sp = wgrad_splits(3 * d, d, T);

@@ -66,8 +66,11 @@ def test_attention_bwd_lse_matches_autograd(B, S, H):
     assert err <= 3e-2 * max(1.0, scale), (err, scale)
 
 
+@pytest.mark.parametrize("fwd_lse", [False, True])
 @pytest.mark.parametrize("B,S,H", [(2, 512, 4), (1, 300, 12), (3, 200, 2), (1, 129, 1), (4, 256, 12)])
-def test_attention_bwd_long_matches_autograd(B, S, H):
+def test_attention_bwd_long_matches_autograd(B, S, H, fwd_lse):
+    """fwd_lse: the training path — the forward writes each row's LSE and the dQ kernel
+    takes it instead of recomputing the row statistics (rs_attention_bwd_long_lse)."""
     from paper_2408_15792_b200 import _lib
     _lib.device()
     g = torch.Generator(device="cuda").manual_seed(B * S + H + 7)
@@ -75,12 +78,18 @@ def test_attention_bwd_long_matches_autograd(B, S, H):
     dout = torch.randn(B * S, H * 64, device="cuda", generator=g).bfloat16()
     att = torch.empty(B * S, H * 64, dtype=torch.bfloat16, device="cuda")
     lib = _lib.load()
-    _lib.check(lib.rs_attention_fwd(qkv.data_ptr(), att.data_ptr(), B, S, H, _lib.stream_handle()))
+    lse = torch.full((B * H * S,), float("nan"), dtype=torch.float32, device="cuda")
+    _lib.check(lib.rs_attention_fwd_lse(qkv.data_ptr(), att.data_ptr(), lse.data_ptr(), B, S, H, _lib.stream_handle()))
     dqkv = torch.full((B * S, 3 * H * 64), float("nan"), dtype=torch.bfloat16, device="cuda")
     n_ws = lib.rs_attention_bwd_long_workspace_size(B, S, H)
-    ws = torch.empty(n_ws, dtype=torch.uint8, device="cuda")
-    _lib.check(lib.rs_attention_bwd_long(qkv.data_ptr(), att.data_ptr(), dout.data_ptr(), dqkv.data_ptr(), B, S, H,
-                                         ws.data_ptr(), n_ws, _lib.stream_handle()), "rs_attention_bwd_long")
+    ws = torch.full((n_ws,), 0xFF, dtype=torch.uint8, device="cuda")  # NaN scratch: must be written before read
+    if fwd_lse:
+        _lib.check(lib.rs_attention_bwd_long_lse(qkv.data_ptr(), att.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                                                 dqkv.data_ptr(), B, S, H, ws.data_ptr(), n_ws, _lib.stream_handle()),
+                   "rs_attention_bwd_long_lse")
+    else:
+        _lib.check(lib.rs_attention_bwd_long(qkv.data_ptr(), att.data_ptr(), dout.data_ptr(), dqkv.data_ptr(), B, S,
+                                             H, ws.data_ptr(), n_ws, _lib.stream_handle()), "rs_attention_bwd_long")
     x = qkv.float().requires_grad_(True)
     q, k, v = x.view(B, S, 3, H, 64).permute(2, 0, 3, 1, 4)
     o = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=True)
