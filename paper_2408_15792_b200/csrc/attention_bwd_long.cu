@@ -34,6 +34,7 @@ constexpr float AL_C = 0.125f * 1.4426950408889634f;
 
 struct AlBars {
     uint64_t ld, kv, s_full, s_free, p_full, g_done;
+    uint64_t kvb[2];  // double-buffered operand loads of the main loop
     uint32_t tmem;
 };
 
@@ -85,11 +86,13 @@ __device__ __forceinline__ void al_init(AlBars* bar) {
     mbar_init(&bar->s_free, 4);
     mbar_init(&bar->p_full, 4);
     mbar_init(&bar->g_done, 1);
+    mbar_init(&bar->kvb[0], 1);
+    mbar_init(&bar->kvb[1], 1);
     fence_barrier_init();
 }
 
 // ---- dQ (+ LSE, D) ----------------------------------------------------------------------
-constexpr int ALQ_SMEM = 5 * AL_TILE + AL_SQ + 128;  // Q dO O | K V | dS
+constexpr int ALQ_SMEM = 7 * AL_TILE + AL_SQ + 128;  // Q dO O | K V | dS | K' V' (next block)
 
 __global__ void __launch_bounds__(AL_THREADS, 1)
     attn_bwd_dq_kernel(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tatt,
@@ -105,7 +108,9 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
     uint8_t* sK = sO + AL_TILE;
     uint8_t* sV = sK + AL_TILE;
     uint8_t* sdS = sV + AL_TILE;
-    AlBars* bar = reinterpret_cast<AlBars*>(sdS + AL_SQ);
+    uint8_t* sK1 = sdS + AL_SQ;
+    uint8_t* sV1 = sK1 + AL_TILE;
+    AlBars* bar = reinterpret_cast<AlBars*>(sV1 + AL_TILE);
     const int nq = (S + AL_T - 1) / AL_T;
     const int i = blockIdx.x % nq, bh = blockIdx.x / nq;
     const int b = bh / H, h = bh % H;
@@ -148,28 +153,38 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
                     mma_bf16_ss(tS, desc_kmajor_sw128(q + s * 32), desc_kmajor_sw128(k + s * 32), id_ss, s != 0);
                 mma_commit(&bar->s_full);
             }
-            if (lse_in == nullptr) mbar_wait(&bar->s_free, i & 1);
+            if (lse_in == nullptr) mbar_wait(&bar->s_free, i & 1);  // pass 1's last S read: K free
             if (lse_in != nullptr) mbar_wait(&bar->ld, 0);
-            // pass 2: dS blocks -> dQ
-            for (int j = 0; j <= i; ++j, ++it) {
-                if (j > 0) mbar_wait(&bar->g_done, (j - 1) & 1);  // dQ MMA done: K, V, dS free
-                mbar_arrive_expect_tx(&bar->kv, 2 * AL_TILE);
-                tma_load_2d(sK, &tqkv, &bar->kv, dm + h * AL_D, row0 + j * AL_T);
-                tma_load_2d(sV, &tqkv, &bar->kv, 2 * dm + h * AL_D, row0 + j * AL_T);
-                mbar_wait(&bar->kv, it & 1);
+            // pass 2: dS blocks -> dQ. K, V double-buffered: block j + 1's loads are in
+            // flight while block j's softmax and dQ MMA run
+            auto load_kv = [&](int jj) {
+                const int u = jj & 1;
+                mbar_arrive_expect_tx(&bar->kvb[u], 2 * AL_TILE);
+                tma_load_2d(u ? sK1 : sK, &tqkv, &bar->kvb[u], dm + h * AL_D, row0 + jj * AL_T);
+                tma_load_2d(u ? sV1 : sV, &tqkv, &bar->kvb[u], 2 * dm + h * AL_D, row0 + jj * AL_T);
+            };
+            load_kv(0);
+            for (int j = 0; j <= i; ++j) {
+                const int u = j & 1;
+                const uint32_t kj = smem_u32(u ? sK1 : sK), vj = smem_u32(u ? sV1 : sV);
+                mbar_wait(&bar->kvb[u], (j >> 1) & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int s = 0; s < AL_D / 16; ++s) {
-                    mma_bf16_ss(tS, desc_kmajor_sw128(q + s * 32), desc_kmajor_sw128(k + s * 32), id_ss, s != 0);
-                    mma_bf16_ss(tdP, desc_kmajor_sw128(dO + s * 32), desc_kmajor_sw128(v + s * 32), id_ss, s != 0);
+                    mma_bf16_ss(tS, desc_kmajor_sw128(q + s * 32), desc_kmajor_sw128(kj + s * 32), id_ss, s != 0);
+                    mma_bf16_ss(tdP, desc_kmajor_sw128(dO + s * 32), desc_kmajor_sw128(vj + s * 32), id_ss, s != 0);
                 }
                 mma_commit(&bar->s_full);
+                if (j < i) {
+                    if (j > 0) mbar_wait(&bar->g_done, (j - 1) & 1);  // dQ MMA j - 1 read the other K
+                    load_kv(j + 1);
+                }
                 mbar_wait(&bar->p_full, j & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int s = 0; s < AL_T / 16; ++s)
                     mma_bf16_ss(tdQ, desc_kmajor_sw128(ds + (s >> 2) * (AL_T * 128) + (s & 3) * 32),
-                                desc_mnmajor_sw128(k + s * 2048, 8192), id_nn, (j > 0 || s > 0) ? 1u : 0u);
+                                desc_mnmajor_sw128(kj + s * 2048, 8192), id_nn, (j > 0 || s > 0) ? 1u : 0u);
                 mma_commit(&bar->g_done);
             }
         }
@@ -259,7 +274,7 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
 }
 
 // ---- dK, dV --------------------------------------------------------------------------
-constexpr int ALK_SMEM = 4 * AL_TILE + 2 * AL_SQ + 128;  // K V | Q dO | P dS
+constexpr int ALK_SMEM = 6 * AL_TILE + 2 * AL_SQ + 128;  // K V | Q dO | P dS | Q' dO' (next block)
 
 __global__ void __launch_bounds__(AL_THREADS, 1)
     attn_bwd_dkv_kernel(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tdo,
@@ -274,7 +289,9 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
     uint8_t* sdO = sQ + AL_TILE;
     uint8_t* sP = sdO + AL_TILE;
     uint8_t* sdS = sP + AL_SQ;
-    AlBars* bar = reinterpret_cast<AlBars*>(sdS + AL_SQ);
+    uint8_t* sQ1 = sdS + AL_SQ;
+    uint8_t* sdO1 = sQ1 + AL_TILE;
+    AlBars* bar = reinterpret_cast<AlBars*>(sdO1 + AL_TILE);
     const int nq = (S + AL_T - 1) / AL_T;
     const int j = blockIdx.x % nq, bh = blockIdx.x / nq;
     const int b = bh / H, h = bh % H;
@@ -302,29 +319,40 @@ __global__ void __launch_bounds__(AL_THREADS, 1)
             mbar_arrive_expect_tx(&bar->ld, 2 * AL_TILE);
             tma_load_2d(sK, &tqkv, &bar->ld, dm + h * AL_D, row0 + j * AL_T);
             tma_load_2d(sV, &tqkv, &bar->ld, 2 * dm + h * AL_D, row0 + j * AL_T);
+            // Q, dO double-buffered: block i + 1's loads are in flight while block i's
+            // softmax and dV / dK MMAs run
+            auto load_qdo = [&](int tt, int ii) {
+                const int u = tt & 1;
+                mbar_arrive_expect_tx(&bar->kvb[u], 2 * AL_TILE);
+                tma_load_2d(u ? sQ1 : sQ, &tqkv, &bar->kvb[u], h * AL_D, row0 + ii * AL_T);
+                tma_load_2d(u ? sdO1 : sdO, &tdo, &bar->kvb[u], h * AL_D, row0 + ii * AL_T);
+            };
+            load_qdo(0, j);
             for (int i = j, t = 0; i < nq; ++i, ++t) {
-                if (t > 0) mbar_wait(&bar->g_done, (t - 1) & 1);  // Q, dO, P, dS free
-                mbar_arrive_expect_tx(&bar->kv, 2 * AL_TILE);
-                tma_load_2d(sQ, &tqkv, &bar->kv, h * AL_D, row0 + i * AL_T);
-                tma_load_2d(sdO, &tdo, &bar->kv, h * AL_D, row0 + i * AL_T);
-                mbar_wait(&bar->kv, t & 1);
+                const int u = t & 1;
+                const uint32_t qi = smem_u32(u ? sQ1 : sQ), oi = smem_u32(u ? sdO1 : sdO);
+                mbar_wait(&bar->kvb[u], (t >> 1) & 1);
                 if (t == 0) mbar_wait(&bar->ld, 0);
                 tc_fence_after();
 #pragma unroll
                 for (int s = 0; s < AL_D / 16; ++s) {
-                    mma_bf16_ss(tS, desc_kmajor_sw128(q + s * 32), desc_kmajor_sw128(k + s * 32), id_ss, s != 0);
-                    mma_bf16_ss(tdP, desc_kmajor_sw128(dO + s * 32), desc_kmajor_sw128(v + s * 32), id_ss, s != 0);
+                    mma_bf16_ss(tS, desc_kmajor_sw128(qi + s * 32), desc_kmajor_sw128(k + s * 32), id_ss, s != 0);
+                    mma_bf16_ss(tdP, desc_kmajor_sw128(oi + s * 32), desc_kmajor_sw128(v + s * 32), id_ss, s != 0);
                 }
                 mma_commit(&bar->s_full);
+                if (i + 1 < nq) {
+                    if (t > 0) mbar_wait(&bar->g_done, (t - 1) & 1);  // MMAs of t - 1 read the other Q, dO
+                    load_qdo(t + 1, i + 1);
+                }
                 mbar_wait(&bar->p_full, t & 1);
                 tc_fence_after();
 #pragma unroll
                 for (int s = 0; s < AL_T / 16; ++s) {
                     const uint32_t acc = (t > 0 || s > 0) ? 1u : 0u;
                     mma_bf16_ss(tdV, desc_mnmajor_sw128(p + s * 2048, AL_T * 128),
-                                desc_mnmajor_sw128(dO + s * 2048, 8192), id_tn, acc);
+                                desc_mnmajor_sw128(oi + s * 2048, 8192), id_tn, acc);
                     mma_bf16_ss(tdK, desc_mnmajor_sw128(ds + s * 2048, AL_T * 128),
-                                desc_mnmajor_sw128(q + s * 2048, 8192), id_tn, acc);
+                                desc_mnmajor_sw128(qi + s * 2048, 8192), id_tn, acc);
                 }
                 mma_commit(&bar->g_done);
             }

@@ -4,4 +4,3 @@ for k in 1 2; do
 echo "old S512"; RSB200_LIB=$PWD/tools/_ab/librsb200_old.so timeout 600 python tools/train_time.py 64 512 2>&1 | tail -1
 echo "new S512"; timeout 600 python tools/train_time.py 64 512 2>&1 | tail -1
 done
-echo "new S128"; timeout 600 python tools/train_time.py 1024 128 2>&1 | tail -1
