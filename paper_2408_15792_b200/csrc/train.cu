@@ -87,8 +87,10 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ d
     const int r0 = blockIdx.x * LNB_ROWS_PER_BLOCK;
     for (int r = r0 + wid; r < min(rows, r0 + LNB_ROWS_PER_BLOCK); r += 8) {
         float xv[VPL * 8], g[VPL * 8];
+        float hv[VPL * 8];
         tr_load_f32<VPL>(x + (size_t)r * d, lane, xv);
         tr_load_f32<VPL>(dy + (size_t)r * d, lane, g);
+        tr_load_f32<VPL>(dh + (size_t)r * d, lane, hv);  // all three rows in flight at once
         float s = 0.f;
 #pragma unroll
         for (int e = 0; e < VPL * 8; ++e) s += xv[e];
@@ -114,8 +116,6 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ d
         }
         sg = warp_sum(sg) * (1.0f / d);
         sgx = warp_sum(sgx) * (1.0f / d);
-        float hv[VPL * 8];
-        tr_load_f32<VPL>(dh + (size_t)r * d, lane, hv);
 #pragma unroll
         for (int e = 0; e < VPL * 8; ++e) {
             hv[e] += rstd * (g[e] - sg - xv[e] * sgx);
